@@ -1,0 +1,279 @@
+/*
+ * weft_gpu.h — the C-ABI drop-in boundary of the B200-native implicit-
+ * integration hot path of P-Cloth (arXiv 2008.00409).
+ *
+ * The reference engine ("weft", /root/reference/proj) is C++20; its hot path
+ * is called from exactly one place per step, Simulator::step_impl
+ * (proj/src/driver.cpp:136-161). This header exports plain-C entry points,
+ * plain pointers and sizes only, one per reference interface the GPU path
+ * replaces (each cited below as file:line of the reference). A C++ caller of
+ * the reference keeps its types and calls these through the thin wrapper in
+ * paper_2008_00409_b200/host/weft_dropin.hpp.
+ *
+ * Conventions
+ *  - Every entry point returns a weft_status; on failure the message of the
+ *    reference's exception (same wording) is available from
+ *    weft_gpu_last_error() (thread-local).
+ *  - Array arguments may be host or device pointers (cudaMemcpyDefault/UVA);
+ *    they are borrowed for the duration of the call. All device state is
+ *    owned by the context. Output buffers are caller-allocated; passing NULL
+ *    where a size query is documented returns only the size.
+ *  - Vectors of vertices are flat doubles, 3 per vertex (x0,y0,z0,x1,...),
+ *    the layout of std::vector<Vec3>/DistVector<double> gathered.
+ *  - Every call is synchronous on return (Engine::parallel fork-join
+ *    semantics, proj/include/weft/exec.hpp:99-101).
+ */
+#ifndef WEFT_GPU_H
+#define WEFT_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes mirror the reference's error hierarchy
+ * (proj/include/weft/common.hpp:16-47, proj/include/weft/solver.hpp:10-13). */
+typedef enum weft_status {
+  WEFT_OK = 0,
+  WEFT_ERR_DIMENSION = 1, /* weft::DimensionError */
+  WEFT_ERR_SOLVER = 2,    /* weft::SolverError    */
+  WEFT_ERR_EXEC = 3,      /* weft::ExecError: CUDA/NCCL failure, names the GPU */
+  WEFT_ERR_TOPOLOGY = 4,  /* weft::TopologyError  */
+  WEFT_ERR_SCHEDULE = 5,  /* weft::ScheduleError  */
+  WEFT_ERR_INVALID = 6    /* invalid argument or call order */
+} weft_status;
+
+/* Message of the last failed call on this thread ("" if none). */
+const char* weft_gpu_last_error(void);
+
+/* ---------------------------------------------------------------------- */
+/* Element records (proj/include/weft/elements.hpp:11-81)                  */
+/* ---------------------------------------------------------------------- */
+
+/* ElementKind, same order as the reference enum (elements.hpp:11). */
+enum { WEFT_STRETCH = 0, WEFT_BEND = 1, WEFT_SPRING = 2, WEFT_EXTERNAL = 3, WEFT_CONTACT = 4 };
+/* JacobianMode (elements.hpp:13-16). */
+enum { WEFT_JAC_EXACT = 0, WEFT_JAC_SPD_PROJECTED = 1 };
+
+/* Flat AssemblyElement (elements.hpp:71-77); `data` holds the variant
+ * payload of the element's kind:
+ *   STRETCH  (StretchData, :20-27): pwu[0..2] pwv[3..5] area[6] k_warp[7]
+ *                                   k_weft[8] k_shear[9]
+ *   BEND     (BendData, :30-33):    rest_angle[0] stiffness[1]
+ *   SPRING   (SpringData, :35-38):  rest_length[0] stiffness[1]
+ *   EXTERNAL (ExternalData, :40-43): force[0..2] drag[3]
+ *   CONTACT  (ContactData, :51-62): normal[0..2] w[3..6] bias[7]
+ *             activation[8] stiffness[9] friction[10] tangential_damping[11]
+ *             frozen_normal_force[12] rel_vel_bias[13..15]
+ */
+typedef struct weft_element {
+  int32_t kind;
+  int32_t stencil_size;
+  int32_t stencil[4];
+  double damping;
+  double data[18];
+} weft_element;
+
+/* ---------------------------------------------------------------------- */
+/* Context                                                                */
+/* ---------------------------------------------------------------------- */
+
+typedef struct weft_gpu_ctx weft_gpu_ctx;
+
+typedef struct weft_gpu_options {
+  int32_t cuda_device; /* CUDA ordinal this context runs on */
+  /* Logical row partitions n: the reference's Engine(n)/make_partitions
+   * (proj/src/exec.cpp:10-23). Fixes the SpMV accumulation order
+   * (proj/include/weft/sparse.hpp:72-101) and the dot-product reduction
+   * order (proj/src/exec.cpp:170-174). n must be a power of two when > 1
+   * (proj/src/topology.cpp:7-11). */
+  int32_t partitions;
+  /* Partitions [part_begin, part_end) are resident on this GPU; the rest
+   * live on peer ranks (multi-process). Single-process: 0 and partitions. */
+  int32_t part_begin;
+  int32_t part_end;
+} weft_gpu_options;
+
+/* Creates a context (replaces Engine construction, exec.cpp:145-148). */
+weft_status weft_gpu_create(const weft_gpu_options* opts, weft_gpu_ctx** out);
+weft_status weft_gpu_destroy(weft_gpu_ctx* ctx);
+
+/* ---------------------------------------------------------------------- */
+/* Partitions and schedule (proj/src/exec.cpp:10-27, proj/src/topology.cpp)*/
+/* ---------------------------------------------------------------------- */
+
+/* make_partitions (exec.cpp:10-23): begin/end arrays of length `devices`. */
+weft_status weft_make_partitions(int32_t vertex_count, int32_t devices, int32_t* begin, int32_t* end);
+/* generate_work_queues(FatTree::make(n)) (topology.cpp:79-89): for device
+ * d, node k: peer[d*(n-1)+k], vec[d*(n-1)+k]. */
+weft_status weft_work_queues(int32_t devices, int32_t* peer, int32_t* vec);
+
+/* ---------------------------------------------------------------------- */
+/* Sparse matrix + SpMV (proj/include/weft/bell.hpp, sparse.hpp)          */
+/* ---------------------------------------------------------------------- */
+
+/* Loads a global 3x3-block matrix given as block CSR with ascending columns
+ * per row, values row-major per block (9 doubles). Equivalent of
+ * partition_matrix(global, make_partitions(rows, n)) (sparse.hpp:103-147). */
+weft_status weft_gpu_set_matrix(weft_gpu_ctx* ctx, int32_t block_rows, const int64_t* row_ptr,
+                                const int32_t* cols, const double* vals);
+
+/* y = A x with the pipelined order of spmv_pipelined (sparse.hpp:72-101):
+ * per row the own-partition sub-block sum first, then the other sub-blocks
+ * in work-queue order. x, y: 3*block_rows doubles. Bitwise equal to
+ * oracle::spmv_partitioned_serial (src/oracle/sparse_oracle.hpp:12-42). */
+weft_status weft_gpu_spmv(weft_gpu_ctx* ctx, const double* x, double* y);
+
+/* Matrix shape of the context's current system (assembled or loaded). */
+typedef struct weft_matrix_info {
+  int32_t block_rows;
+  int32_t max_row_blocks; /* widest compacted row */
+  int64_t nnzb;           /* live blocks */
+  int64_t padded_slots;   /* device storage slots (sliced-ELL) */
+} weft_matrix_info;
+weft_status weft_gpu_matrix_info(weft_gpu_ctx* ctx, weft_matrix_info* info);
+
+/* Downloads the current system as global block CSR, ascending columns
+ * (gather_matrix, sparse.hpp:149-173). Any pointer may be NULL. */
+weft_status weft_gpu_download_matrix(weft_gpu_ctx* ctx, int64_t* row_ptr, int32_t* cols, double* vals);
+/* Downloads the assembled right-hand side (3*block_rows doubles). */
+weft_status weft_gpu_download_rhs(weft_gpu_ctx* ctx, double* rhs);
+
+/* ---------------------------------------------------------------------- */
+/* PCG (proj/include/weft/solver.hpp:15-178)                              */
+/* ---------------------------------------------------------------------- */
+
+enum { WEFT_PRECOND_NONE = 0, WEFT_PRECOND_BLOCK_JACOBI = 1 }; /* solver.hpp:15 */
+
+typedef struct weft_pcg_config { /* PcgConfig, solver.hpp:17-21 */
+  double rel_tolerance;          /* default 1e-4 */
+  int32_t max_iterations;        /* default 400 */
+  int32_t preconditioner;        /* default WEFT_PRECOND_BLOCK_JACOBI */
+} weft_pcg_config;
+
+typedef struct weft_pcg_report { /* PcgReport, solver.hpp:23-29 */
+  int32_t iterations;
+  int32_t converged;
+  double rel_residual;
+  /* Optional histories (length >= max_iterations, may be NULL): */
+  double* residual_history;
+  double* precond_norm_history;
+} weft_pcg_report;
+
+/* Solves A x = b for the context's current matrix (pcg_solve,
+ * solver.hpp:36-178). b may be NULL to use the assembled rhs. x receives the
+ * solution (3*block_rows doubles; NULL keeps it on the device). Returns
+ * WEFT_ERR_SOLVER with the reference's message on non-finite/non-positive
+ * curvature or divergence; non-convergence is only flagged. */
+weft_status weft_gpu_pcg(weft_gpu_ctx* ctx, const double* b, double* x, const weft_pcg_config* config,
+                         weft_pcg_report* report);
+
+/* ---------------------------------------------------------------------- */
+/* Assembly (proj/include/weft/assembly.hpp:48-220, physics.hpp:44-69)    */
+/* ---------------------------------------------------------------------- */
+
+/* Per-vertex data of SystemInputs (assembly.hpp:51-60): mass, pinned. */
+weft_status weft_gpu_set_vertices(weft_gpu_ctx* ctx, int32_t vertex_count, const double* mass,
+                                  const uint8_t* pinned);
+/* The static element list (build_elements order: triangles, hinges,
+ * vertices; physics.cpp:5-63). Precomputes its sparsity contribution. */
+weft_status weft_gpu_set_elements(weft_gpu_ctx* ctx, int64_t count, const weft_element* elements);
+/* Per-step elements appended after the static list (contacts,
+ * physics.hpp:50-52). count may be 0. */
+weft_status weft_gpu_set_contacts(weft_gpu_ctx* ctx, int64_t count, const weft_element* contacts);
+
+/* fill_matrix<double> (assembly.hpp:74-220) over static + contact
+ * elements: rebuilds the sparsity pattern and values of
+ * A = M - (dt^2 + c dt) J (+ dt D) and rhs = dt f(x_adv) on the device.
+ * x_cur, x_adv, velocity: 3*p doubles. jac_mode: WEFT_JAC_*. */
+weft_status weft_gpu_fill_matrix(weft_gpu_ctx* ctx, const double* x_cur, const double* x_adv,
+                                 const double* velocity, double dt, int32_t jac_mode);
+
+/* step_system<double> (physics.hpp:44-69): x_adv = x + dt v computed on
+ * the device, then fill_matrix. */
+weft_status weft_gpu_step_system(weft_gpu_ctx* ctx, const double* x, const double* v, double dt,
+                                 int32_t jac_mode);
+
+/* ---------------------------------------------------------------------- */
+/* Spatial-hash broad phase (proj/src/collision.cpp:77-192,205-210,329-378)*/
+/* ---------------------------------------------------------------------- */
+
+enum { WEFT_DISCRETE = 0, WEFT_CONTINUOUS = 1 }; /* CollisionMode, collision.hpp:18 */
+
+/* Static soup topology (CollisionSoup::build, collision.cpp:95-116). */
+weft_status weft_gpu_set_soup(weft_gpu_ctx* ctx, int32_t vertex_count, int32_t tri_count,
+                              const int32_t* tris);
+
+/* build_grid (collision.cpp:118-179) on the device. x_end is ignored in
+ * Discrete mode. Bit-exact with the reference: cell size from the serial
+ * diagonal sum, lattice boxes, cell keys, per-cell triangle lists and
+ * workload prefix. */
+weft_status weft_gpu_build_grid(weft_gpu_ctx* ctx, const double* x_begin, const double* x_end,
+                                int32_t mode, double thickness, double cell_scale);
+
+typedef struct weft_grid_info {
+  double cell_size;
+  int64_t cells;   /* occupied cells */
+  int64_t entries; /* (cell, triangle) memberships */
+  int64_t total;   /* WorkloadTable::total, sum of c(c-1)/2 */
+} weft_grid_info;
+weft_status weft_gpu_grid_info(weft_gpu_ctx* ctx, weft_grid_info* info);
+
+/* HashGrid + WorkloadTable (collision.hpp:59-70) as flat arrays; any may be
+ * NULL. cell_offsets/prefix have cells+1 entries; tri_boxes 6 per triangle
+ * (lo xyz, hi xyz inclusive). */
+weft_status weft_gpu_download_grid(weft_gpu_ctx* ctx, uint64_t* cell_keys, int64_t* cell_offsets,
+                                   int32_t* cell_tris, int64_t* prefix, int64_t* tri_boxes);
+
+/* Candidate triangle pairs of the flattened pair range [begin, end)
+ * (narrow_phase_range's walk + min-common-cell rule, collision.cpp:
+ * 329-378): each lattice-overlapping pair t1 < t2 exactly once across all
+ * ranges. pairs: 2 int32 per candidate, in walk order. pairs == NULL ->
+ * count only. */
+weft_status weft_gpu_candidates(weft_gpu_ctx* ctx, int64_t begin, int64_t end, int64_t* count,
+                                int32_t* pairs);
+
+/* split_workload (collision.cpp:181-192). */
+weft_status weft_split_workload(int64_t total, int32_t devices, int64_t* begin, int64_t* end);
+
+/* ---------------------------------------------------------------------- */
+/* Device-resident hot-path step (Simulator::step_impl stages 1-4 + CCD   */
+/* broad phase, proj/src/driver.cpp:96-215, without narrow phase/zones)   */
+/* ---------------------------------------------------------------------- */
+
+typedef struct weft_sim_params {
+  double dt;
+  double thickness;  /* CollisionParams::thickness */
+  double cell_scale; /* CollisionParams::cell_scale */
+  weft_pcg_config pcg;
+  int32_t jac_mode;
+} weft_sim_params;
+
+typedef struct weft_step_report {
+  int32_t pcg_iterations;
+  int32_t pcg_converged;
+  double pcg_residual;
+  int64_t dcd_candidates;
+  int64_t ccd_candidates;
+  double ms_broad;    /* device time of both broad phases */
+  double ms_assemble; /* device time of fill_matrix */
+  double ms_solve;    /* device time of the PCG */
+} weft_step_report;
+
+/* Uploads the state (x, v: 3*p doubles each; the soup positions of the
+ * cloth are x). Requires vertices, elements and soup to be set. */
+weft_status weft_gpu_sim_set_state(weft_gpu_ctx* ctx, const double* x, const double* v);
+/* One step on device-resident state: DCD grid + candidates on x, assembly
+ * of step_system at x, PCG, v += dv, x_cand = x + dt v, CCD grid +
+ * candidates on (x, x_cand), commit x = x_cand. */
+weft_status weft_gpu_sim_step(weft_gpu_ctx* ctx, const weft_sim_params* params, weft_step_report* report);
+/* Reads the state back (either pointer may be NULL). */
+weft_status weft_gpu_sim_get_state(weft_gpu_ctx* ctx, double* x, double* v);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* WEFT_GPU_H */

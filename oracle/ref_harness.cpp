@@ -1,0 +1,563 @@
+// ref_harness.cpp — C-ABI over the UNMODIFIED reference engine (TEST
+// INFRASTRUCTURE). Compiled with the reference sources into
+// oracle/_ref/libweft_ref.so by `make -C oracle ref`; loaded via ctypes by
+// tests/ (parity checks and golden-fixture generation) and by bench.py's
+// reference arm. It only marshals flat arrays into the reference's own types
+// and calls the reference's public functions; no algorithm lives here except
+// the candidate-pair walk, which replays narrow_phase_range's loop
+// (proj/src/collision.cpp:329-378) over the reference's own HashGrid because
+// the reference does not expose candidates separately.
+#include <chrono>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "oracle/physics_oracle.hpp"
+#include "oracle/sparse_oracle.hpp"
+#include "oracle/collision_oracle.hpp"
+#include "weft/assembly.hpp"
+#include "weft/collision.hpp"
+#include "weft/mesh.hpp"
+#include "weft/physics.hpp"
+#include "weft/solver.hpp"
+
+#include "../include/weft_gpu.h"
+
+using namespace weft;
+
+namespace {
+
+thread_local std::string g_err;
+
+AssemblyElement to_element(const weft_element& f) {
+  AssemblyElement e;
+  e.kind = static_cast<ElementKind>(f.kind);
+  e.stencil_size = f.stencil_size;
+  for (int i = 0; i < 4; ++i) e.stencil[static_cast<std::size_t>(i)] = f.stencil[i];
+  e.damping = f.damping;
+  const double* d = f.data;
+  switch (e.kind) {
+    case ElementKind::Stretch: {
+      StretchData s;
+      s.pwu = {d[0], d[1], d[2]};
+      s.pwv = {d[3], d[4], d[5]};
+      s.area = d[6];
+      s.k_warp = d[7];
+      s.k_weft = d[8];
+      s.k_shear = d[9];
+      e.data = s;
+      break;
+    }
+    case ElementKind::Bend:
+      e.data = BendData{d[0], d[1]};
+      break;
+    case ElementKind::Spring:
+      e.data = SpringData{d[0], d[1]};
+      break;
+    case ElementKind::External:
+      e.data = ExternalData{Vec3(d[0], d[1], d[2]), d[3]};
+      break;
+    case ElementKind::Contact: {
+      ContactData c;
+      c.normal = Vec3(d[0], d[1], d[2]);
+      c.w = {d[3], d[4], d[5], d[6]};
+      c.bias = d[7];
+      c.activation = d[8];
+      c.stiffness = d[9];
+      c.friction = d[10];
+      c.tangential_damping = d[11];
+      c.frozen_normal_force = d[12];
+      c.rel_vel_bias = Vec3(d[13], d[14], d[15]);
+      e.data = c;
+      break;
+    }
+  }
+  return e;
+}
+
+weft_element from_element(const AssemblyElement& e) {
+  weft_element f{};
+  f.kind = static_cast<int32_t>(e.kind);
+  f.stencil_size = e.stencil_size;
+  for (int i = 0; i < 4; ++i) f.stencil[i] = e.stencil[static_cast<std::size_t>(i)];
+  f.damping = e.damping;
+  double* d = f.data;
+  switch (e.kind) {
+    case ElementKind::Stretch: {
+      const auto& s = std::get<StretchData>(e.data);
+      for (int i = 0; i < 3; ++i) {
+        d[i] = s.pwu[static_cast<std::size_t>(i)];
+        d[3 + i] = s.pwv[static_cast<std::size_t>(i)];
+      }
+      d[6] = s.area;
+      d[7] = s.k_warp;
+      d[8] = s.k_weft;
+      d[9] = s.k_shear;
+      break;
+    }
+    case ElementKind::Bend: {
+      const auto& b = std::get<BendData>(e.data);
+      d[0] = b.rest_angle;
+      d[1] = b.stiffness;
+      break;
+    }
+    case ElementKind::Spring: {
+      const auto& s = std::get<SpringData>(e.data);
+      d[0] = s.rest_length;
+      d[1] = s.stiffness;
+      break;
+    }
+    case ElementKind::External: {
+      const auto& x = std::get<ExternalData>(e.data);
+      for (int i = 0; i < 3; ++i) d[i] = x.force[i];
+      d[3] = x.drag;
+      break;
+    }
+    case ElementKind::Contact: {
+      const auto& c = std::get<ContactData>(e.data);
+      for (int i = 0; i < 3; ++i) d[i] = c.normal[i];
+      for (int i = 0; i < 4; ++i) d[3 + i] = c.w[static_cast<std::size_t>(i)];
+      d[7] = c.bias;
+      d[8] = c.activation;
+      d[9] = c.stiffness;
+      d[10] = c.friction;
+      d[11] = c.tangential_damping;
+      d[12] = c.frozen_normal_force;
+      for (int i = 0; i < 3; ++i) d[13 + i] = c.rel_vel_bias[i];
+      break;
+    }
+  }
+  return f;
+}
+
+std::vector<Vec3> to_vec3(const double* x, int count) {
+  std::vector<Vec3> out(static_cast<std::size_t>(count));
+  for (int i = 0; i < count; ++i) out[static_cast<std::size_t>(i)] = Vec3(x[3 * i], x[3 * i + 1], x[3 * i + 2]);
+  return out;
+}
+
+struct Csr {
+  int rows = 0;
+  std::vector<int64_t> row_ptr;
+  std::vector<int32_t> cols;
+  std::vector<double> vals;
+  std::vector<double> rhs;
+};
+
+Csr from_bell(const BellMatrix<double>& a) {
+  Csr c;
+  c.rows = a.block_rows();
+  c.row_ptr.assign(static_cast<std::size_t>(c.rows) + 1, 0);
+  for (int r = 0; r < c.rows; ++r) {
+    for (int s = 0; s < a.ell_width(); ++s) {
+      const int32_t col = a.col_at(r, s);
+      if (col == BellMatrix<double>::kNoBlock) break;
+      c.cols.push_back(col);
+      for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) c.vals.push_back(a.value_at(r, s, i, j));
+    }
+    c.row_ptr[static_cast<std::size_t>(r) + 1] = static_cast<int64_t>(c.cols.size());
+  }
+  return c;
+}
+
+BellMatrix<double> to_bell(int rows, const int64_t* row_ptr, const int32_t* cols, const double* vals) {
+  std::vector<BlockEntry<double>> entries;
+  for (int r = 0; r < rows; ++r) {
+    for (int64_t k = row_ptr[r]; k < row_ptr[r + 1]; ++k) {
+      BlockEntry<double> e;
+      e.row = r;
+      e.col = cols[k];
+      for (int i = 0; i < 9; ++i) e.m[static_cast<std::size_t>(i)] = vals[9 * k + i];
+      entries.push_back(e);
+    }
+  }
+  return BellMatrix<double>::from_entries(rows, entries);
+}
+
+ValidatedSchedule schedule_for(int n) {
+  return n == 1 ? ValidatedSchedule() : ValidatedSchedule(generate_work_queues(FatTree::make(n)), n);
+}
+
+int set_error(const std::exception& e) {
+  g_err = e.what();
+  if (dynamic_cast<const SolverError*>(&e)) return WEFT_ERR_SOLVER;
+  if (dynamic_cast<const DimensionError*>(&e)) return WEFT_ERR_DIMENSION;
+  if (dynamic_cast<const ExecError*>(&e)) return WEFT_ERR_EXEC;
+  if (dynamic_cast<const TopologyError*>(&e)) return WEFT_ERR_TOPOLOGY;
+  if (dynamic_cast<const ScheduleError*>(&e)) return WEFT_ERR_SCHEDULE;
+  return WEFT_ERR_INVALID;
+}
+
+struct MeshHandle {
+  ClothMesh mesh;
+};
+
+struct GridHandle {
+  GridBuildResult built;
+  std::vector<int64_t> offsets;
+  std::vector<int32_t> flat;
+};
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_err.c_str(); }
+
+// ---------------------------------------------------------------- systems
+void* ref_fill_matrix(int32_t p, int32_t n, int64_t n_elem, const weft_element* elems, const double* x_cur,
+                      const double* x_adv, const double* vel, const double* mass, const uint8_t* pinned,
+                      double dt, int32_t mode, int32_t* status) {
+  try {
+    std::vector<AssemblyElement> elements;
+    elements.reserve(static_cast<std::size_t>(n_elem));
+    for (int64_t i = 0; i < n_elem; ++i) elements.push_back(to_element(elems[i]));
+    const auto xc = to_vec3(x_cur, p), xa = to_vec3(x_adv, p), v = to_vec3(vel, p);
+    std::vector<double> m(mass, mass + p);
+    std::vector<uint8_t> pin(pinned, pinned + p);
+    SystemInputs in;
+    in.elements = elements;
+    in.x_current = xc;
+    in.x_advanced = xa;
+    in.velocity = v;
+    in.mass = m;
+    in.pinned = pin;
+    in.dt = dt;
+    in.mode = mode == WEFT_JAC_EXACT ? JacobianMode::Exact : JacobianMode::SpdProjected;
+    Engine engine(n);
+    const auto parts = make_partitions(p, n);
+    const auto dist = distribute_elements(elements, parts);
+    const auto sys = fill_matrix<double>(engine, dist, in, parts);
+    auto* out = new Csr(from_bell(gather_matrix(sys.matrix)));
+    out->rhs = sys.rhs.gather();
+    *status = 0;
+    return out;
+  } catch (const std::exception& e) {
+    *status = set_error(e);
+    return nullptr;
+  }
+}
+
+void ref_system_info(void* h, int32_t* rows, int64_t* nnzb) {
+  auto* c = static_cast<Csr*>(h);
+  *rows = c->rows;
+  *nnzb = static_cast<int64_t>(c->cols.size());
+}
+
+void ref_system_copy(void* h, int64_t* row_ptr, int32_t* cols, double* vals, double* rhs) {
+  auto* c = static_cast<Csr*>(h);
+  if (row_ptr) std::memcpy(row_ptr, c->row_ptr.data(), c->row_ptr.size() * sizeof(int64_t));
+  if (cols) std::memcpy(cols, c->cols.data(), c->cols.size() * sizeof(int32_t));
+  if (vals) std::memcpy(vals, c->vals.data(), c->vals.size() * sizeof(double));
+  if (rhs && !c->rhs.empty()) std::memcpy(rhs, c->rhs.data(), c->rhs.size() * sizeof(double));
+}
+
+void ref_system_free(void* h) { delete static_cast<Csr*>(h); }
+
+// oracle::random_bell (src/oracle/sparse_oracle.cpp:7-23) as CSR.
+void* ref_random_bell(uint64_t seed, int32_t rows, int32_t extra) {
+  oracle::Rng rng(seed);
+  return new Csr(from_bell(oracle::random_bell(rng, rows, extra)));
+}
+
+// ---------------------------------------------------------------- SpMV/PCG
+int32_t ref_spmv(int32_t rows, const int64_t* row_ptr, const int32_t* cols, const double* vals, int32_t n,
+                 const double* x, double* y) {
+  try {
+    const auto global = to_bell(rows, row_ptr, cols, vals);
+    const auto parts = make_partitions(rows, n);
+    const auto split = partition_matrix(global, parts);
+    Engine engine(n);
+    const auto sched = schedule_for(n);
+    DistVector<double> xv(&engine, parts), yv(&engine, parts);
+    for (int d = 0; d < n; ++d) {
+      const auto& part = parts[static_cast<std::size_t>(d)];
+      std::copy(x + 3 * part.begin, x + 3 * part.end, xv.local(d).begin());
+    }
+    SpmvWorkspace<double> ws(n, split.padded_len);
+    spmv_pipelined(engine, split, sched, xv, yv, ws);
+    const auto yg = yv.gather();
+    std::copy(yg.begin(), yg.end(), y);
+    return 0;
+  } catch (const std::exception& e) {
+    return set_error(e);
+  }
+}
+
+int32_t ref_pcg(int32_t rows, const int64_t* row_ptr, const int32_t* cols, const double* vals, int32_t n,
+                const double* b, double* x, const weft_pcg_config* cfg, weft_pcg_report* rep) {
+  try {
+    const auto global = to_bell(rows, row_ptr, cols, vals);
+    const auto parts = make_partitions(rows, n);
+    const auto split = partition_matrix(global, parts);
+    Engine engine(n);
+    const auto sched = schedule_for(n);
+    DistVector<double> bv(&engine, parts), xv(&engine, parts);
+    for (int d = 0; d < n; ++d) {
+      const auto& part = parts[static_cast<std::size_t>(d)];
+      std::copy(b + 3 * part.begin, b + 3 * part.end, bv.local(d).begin());
+    }
+    PcgConfig config;
+    config.rel_tolerance = cfg->rel_tolerance;
+    config.max_iterations = cfg->max_iterations;
+    config.preconditioner =
+        cfg->preconditioner == WEFT_PRECOND_NONE ? Preconditioner::None : Preconditioner::BlockJacobi;
+    const auto r = pcg_solve(engine, split, sched, bv, xv, config);
+    const auto xg = xv.gather();
+    std::copy(xg.begin(), xg.end(), x);
+    rep->iterations = r.iterations;
+    rep->converged = r.converged ? 1 : 0;
+    rep->rel_residual = r.rel_residual;
+    if (rep->residual_history)
+      std::copy(r.residual_history.begin(), r.residual_history.end(), rep->residual_history);
+    if (rep->precond_norm_history)
+      std::copy(r.precond_norm_history.begin(), r.precond_norm_history.end(), rep->precond_norm_history);
+    return 0;
+  } catch (const std::exception& e) {
+    return set_error(e);
+  }
+}
+
+// ---------------------------------------------------------------- meshes
+void* ref_grid_mesh(int32_t nx, int32_t ny, double w, double h, double ox, double oy, double oz, double density) {
+  try {
+    return new MeshHandle{make_grid_mesh(nx, ny, w, h, Vec3(ox, oy, oz), density)};
+  } catch (const std::exception& e) {
+    set_error(e);
+    return nullptr;
+  }
+}
+
+void* ref_build_mesh(int32_t nverts, const double* verts, int32_t ntris, const int32_t* tris, double density) {
+  try {
+    std::vector<std::array<int, 3>> t(static_cast<std::size_t>(ntris));
+    for (int i = 0; i < ntris; ++i) t[static_cast<std::size_t>(i)] = {tris[3 * i], tris[3 * i + 1], tris[3 * i + 2]};
+    return new MeshHandle{ClothMesh::build(to_vec3(verts, nverts), std::move(t), density)};
+  } catch (const std::exception& e) {
+    set_error(e);
+    return nullptr;
+  }
+}
+
+// oracle::random_cloth (src/oracle/physics_oracle.cpp:90-101).
+void* ref_random_cloth(uint64_t seed, int32_t max_side) {
+  oracle::Rng rng(seed);
+  return new MeshHandle{oracle::random_cloth(rng, max_side)};
+}
+
+void ref_mesh_info(void* h, int32_t* verts, int32_t* tris, int32_t* hinges, int32_t* edges) {
+  const auto& m = static_cast<MeshHandle*>(h)->mesh;
+  *verts = m.vertex_count();
+  *tris = m.triangle_count();
+  *hinges = static_cast<int32_t>(m.hinges.size());
+  *edges = static_cast<int32_t>(m.edges.size());
+}
+
+// rest (3/v), tris (3/t), tri_rest (7/t: pwu, pwv, area; degenerate flag
+// in tri_degenerate), hinges (4 ints + rest_angle + stiffness_scale),
+// vertex_area, vertex_mass. Any pointer may be NULL.
+void ref_mesh_copy(void* h, double* rest, int32_t* tris, double* tri_rest, uint8_t* tri_degenerate,
+                   int32_t* hinge_verts, double* hinge_data, double* vertex_area, double* vertex_mass) {
+  const auto& m = static_cast<MeshHandle*>(h)->mesh;
+  for (int v = 0; v < m.vertex_count() && rest; ++v)
+    for (int c = 0; c < 3; ++c) rest[3 * v + c] = m.rest_positions[static_cast<std::size_t>(v)][c];
+  for (int t = 0; t < m.triangle_count(); ++t) {
+    const auto& tr = m.triangles[static_cast<std::size_t>(t)];
+    const auto& r = m.tri_rest[static_cast<std::size_t>(t)];
+    for (int c = 0; c < 3; ++c) {
+      if (tris) tris[3 * t + c] = tr[static_cast<std::size_t>(c)];
+      if (tri_rest) {
+        tri_rest[7 * t + c] = r.pwu[static_cast<std::size_t>(c)];
+        tri_rest[7 * t + 3 + c] = r.pwv[static_cast<std::size_t>(c)];
+      }
+    }
+    if (tri_rest) tri_rest[7 * t + 6] = r.area;
+    if (tri_degenerate) tri_degenerate[t] = r.degenerate ? 1 : 0;
+  }
+  for (std::size_t k = 0; k < m.hinges.size(); ++k) {
+    for (int c = 0; c < 4; ++c)
+      if (hinge_verts) hinge_verts[4 * k + static_cast<std::size_t>(c)] = m.hinges[k].verts[static_cast<std::size_t>(c)];
+    if (hinge_data) {
+      hinge_data[2 * k] = m.hinges[k].rest_angle;
+      hinge_data[2 * k + 1] = m.hinges[k].stiffness_scale;
+    }
+  }
+  for (int v = 0; v < m.vertex_count(); ++v) {
+    if (vertex_area) vertex_area[v] = m.vertex_area[static_cast<std::size_t>(v)];
+    if (vertex_mass) vertex_mass[v] = m.vertex_mass[static_cast<std::size_t>(v)];
+  }
+}
+
+// build_elements (src/physics.cpp:5-63): writes up to `cap` records,
+// returns the element count. material: stretch_warp, stretch_weft, shear,
+// bend, density, damping, air_drag (physics.hpp:8-16).
+int64_t ref_build_elements(void* h, const double* material, const double* gravity, const double* wind,
+                           weft_element* out, int64_t cap) {
+  const auto& m = static_cast<MeshHandle*>(h)->mesh;
+  MaterialParams params;
+  params.stretch_warp = material[0];
+  params.stretch_weft = material[1];
+  params.shear = material[2];
+  params.bend = material[3];
+  params.density = material[4];
+  params.damping = material[5];
+  params.air_drag = material[6];
+  const auto elements = build_elements(m, params, Vec3(gravity[0], gravity[1], gravity[2]),
+                                       Vec3(wind[0], wind[1], wind[2]));
+  for (std::size_t i = 0; i < elements.size() && static_cast<int64_t>(i) < cap; ++i) out[i] = from_element(elements[i]);
+  return static_cast<int64_t>(elements.size());
+}
+
+void ref_mesh_free(void* h) { delete static_cast<MeshHandle*>(h); }
+
+// ---------------------------------------------------------------- elements
+void ref_element_eval(const weft_element* fe, int32_t count_x, const double* x, const double* v, int32_t mode,
+                      double* force, double* jac, double* fric, double* vdamp) {
+  const auto e = to_element(*fe);
+  const auto xs = to_vec3(x, count_x), vs = to_vec3(v, count_x);
+  const auto f = element_force(e, xs);
+  const auto j = element_jacobian(e, xs, mode == WEFT_JAC_EXACT ? JacobianMode::Exact : JacobianMode::SpdProjected);
+  const auto fr = element_friction_force(e, vs);
+  ElementJacobian vd;
+  element_velocity_damping(e, vd);
+  for (int a = 0; a < 4; ++a) {
+    for (int c = 0; c < 3; ++c) {
+      force[3 * a + c] = f.f[static_cast<std::size_t>(a)][c];
+      fric[3 * a + c] = fr.f[static_cast<std::size_t>(a)][c];
+    }
+    for (int b = 0; b < 4; ++b)
+      for (int r = 0; r < 3; ++r)
+        for (int c = 0; c < 3; ++c) {
+          jac[(a * 4 + b) * 9 + r * 3 + c] = j.block[static_cast<std::size_t>(a)][static_cast<std::size_t>(b)](r, c);
+          vdamp[(a * 4 + b) * 9 + r * 3 + c] = vd.block[static_cast<std::size_t>(a)][static_cast<std::size_t>(b)](r, c);
+        }
+  }
+}
+
+// ---------------------------------------------------------------- broad phase
+void* ref_build_grid(int32_t vertex_count, int32_t tri_count, const int32_t* tris, const double* x0,
+                     const double* x1, int32_t mode, double thickness, double cell_scale) {
+  std::vector<std::array<int, 3>> t(static_cast<std::size_t>(tri_count));
+  for (int i = 0; i < tri_count; ++i) t[static_cast<std::size_t>(i)] = {tris[3 * i], tris[3 * i + 1], tris[3 * i + 2]};
+  const auto soup = CollisionSoup::build(std::move(t), vertex_count,
+                                         std::vector<std::uint8_t>(static_cast<std::size_t>(vertex_count), 1));
+  const auto xb = to_vec3(x0, vertex_count);
+  const auto xe = to_vec3(x1 ? x1 : x0, vertex_count);
+  CollisionParams params;
+  params.thickness = thickness;
+  params.cell_scale = cell_scale;
+  auto* g = new GridHandle{build_grid(soup, xb, xe, mode == WEFT_CONTINUOUS ? CollisionMode::Continuous
+                                                                           : CollisionMode::Discrete,
+                                      params), {}, {}};
+  g->offsets.push_back(0);
+  for (const auto& tl : g->built.grid.cell_tris) {
+    g->flat.insert(g->flat.end(), tl.begin(), tl.end());
+    g->offsets.push_back(static_cast<int64_t>(g->flat.size()));
+  }
+  return g;
+}
+
+void ref_grid_info(void* h, double* cell_size, int64_t* cells, int64_t* entries, int64_t* total) {
+  const auto* g = static_cast<GridHandle*>(h);
+  *cell_size = g->built.grid.cell_size;
+  *cells = static_cast<int64_t>(g->built.grid.cell_keys.size());
+  *entries = static_cast<int64_t>(g->flat.size());
+  *total = g->built.table.total;
+}
+
+void ref_grid_copy(void* h, uint64_t* keys, int64_t* offsets, int32_t* cell_tris, int64_t* prefix, int64_t* boxes) {
+  const auto* g = static_cast<GridHandle*>(h);
+  const auto& gr = g->built.grid;
+  if (keys) std::copy(gr.cell_keys.begin(), gr.cell_keys.end(), keys);
+  if (offsets) std::copy(g->offsets.begin(), g->offsets.end(), offsets);
+  if (cell_tris) std::copy(g->flat.begin(), g->flat.end(), cell_tris);
+  if (prefix) std::copy(g->built.table.prefix.begin(), g->built.table.prefix.end(), prefix);
+  if (boxes)
+    for (std::size_t t = 0; t < gr.tri_boxes.size(); ++t)
+      for (int c = 0; c < 6; ++c) boxes[6 * t + static_cast<std::size_t>(c)] = gr.tri_boxes[t][static_cast<std::size_t>(c)];
+}
+
+// split_workload (collision.cpp:181-192) over the reference grid's table.
+void ref_grid_split(void* h, int32_t devices, int64_t* begin, int64_t* end) {
+  const auto ranges = split_workload(static_cast<GridHandle*>(h)->built.table, devices);
+  for (int d = 0; d < devices; ++d) {
+    begin[d] = ranges[static_cast<std::size_t>(d)].begin;
+    end[d] = ranges[static_cast<std::size_t>(d)].end;
+  }
+}
+
+// Candidate pairs of [begin, end): the loop of narrow_phase_range
+// (collision.cpp:340-376) with narrow_phase_pair replaced by emission.
+int64_t ref_grid_candidates(void* h, int64_t begin, int64_t end, int32_t* pairs) {
+  const auto* g = static_cast<GridHandle*>(h);
+  const auto& grid = g->built.grid;
+  const auto& table = g->built.table;
+  if (begin >= end) return 0;
+  std::size_t cell = static_cast<std::size_t>(
+      std::upper_bound(table.prefix.begin(), table.prefix.end(), begin) - table.prefix.begin() - 1);
+  const std::int64_t local = begin - table.prefix[cell];
+  int i = 0, j = 0;
+  {
+    const int s = static_cast<int>(grid.cell_tris[cell].size());
+    std::int64_t remaining = local;
+    while (remaining >= s - 1 - i) {
+      remaining -= s - 1 - i;
+      ++i;
+    }
+    j = i + 1 + static_cast<int>(remaining);
+  }
+  int64_t count = 0;
+  for (std::int64_t gi = begin; gi < end; ++gi) {
+    while (gi >= table.prefix[cell + 1]) {
+      ++cell;
+      i = 0;
+      j = 1;
+    }
+    const auto& tl = grid.cell_tris[cell];
+    const int t1 = tl[static_cast<std::size_t>(i)];
+    const int t2 = tl[static_cast<std::size_t>(j)];
+    const auto& a = grid.tri_boxes[static_cast<std::size_t>(t1)];
+    const auto& b = grid.tri_boxes[static_cast<std::size_t>(t2)];
+    constexpr std::int64_t bias = 1 << 20;
+    const std::uint64_t key = (static_cast<std::uint64_t>(std::max(a[0], b[0]) + bias) << 42) |
+                              (static_cast<std::uint64_t>(std::max(a[1], b[1]) + bias) << 21) |
+                              static_cast<std::uint64_t>(std::max(a[2], b[2]) + bias);
+    if (key == grid.cell_keys[cell]) {
+      if (pairs) {
+        pairs[2 * count] = t1;
+        pairs[2 * count + 1] = t2;
+      }
+      ++count;
+    }
+    if (++j >= static_cast<int>(tl.size())) {
+      ++i;
+      j = i + 1;
+    }
+  }
+  return count;
+}
+
+void ref_grid_free(void* h) { delete static_cast<GridHandle*>(h); }
+
+// oracle::random_two_cloth_scene (src/oracle/collision_oracle.cpp:110-138).
+// Returns vertex count; fills tris (cap) / x_begin / x_end when non-NULL.
+int32_t ref_two_cloth_scene(uint64_t seed, int32_t max_side, int32_t* tri_count, int32_t* tris, double* x0,
+                            double* x1) {
+  oracle::Rng rng(seed);
+  const auto s = oracle::random_two_cloth_scene(rng, max_side);
+  *tri_count = static_cast<int32_t>(s.soup.triangles.size());
+  if (tris)
+    for (std::size_t t = 0; t < s.soup.triangles.size(); ++t)
+      for (int c = 0; c < 3; ++c) tris[3 * t + static_cast<std::size_t>(c)] = s.soup.triangles[t][static_cast<std::size_t>(c)];
+  for (std::size_t v = 0; v < s.x_begin.size(); ++v)
+    for (int c = 0; c < 3; ++c) {
+      if (x0) x0[3 * v + static_cast<std::size_t>(c)] = s.x_begin[v][c];
+      if (x1) x1[3 * v + static_cast<std::size_t>(c)] = s.x_end[v][c];
+    }
+  return s.soup.vertex_count;
+}
+
+}  // extern "C"
