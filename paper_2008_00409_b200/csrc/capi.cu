@@ -1,0 +1,266 @@
+// capi.cu — the extern "C" boundary (include/weft_gpu.h). Every entry
+// point converts exceptions into a weft_status plus a thread-local message
+// worded like the reference's exception.
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "ctx.cuh"
+
+struct weft_gpu_ctx {
+  weft_gpu::Ctx c;
+};
+
+namespace {
+thread_local std::string g_last_error;
+
+template <class F>
+weft_status guard(weft_gpu_ctx* ctx, F&& f) {
+  try {
+    if (ctx) WG_CUDA(cudaSetDevice(ctx->c.device));
+    f();
+    return WEFT_OK;
+  } catch (const weft_gpu::Error& e) {
+    g_last_error = e.what();
+    return e.status;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return WEFT_ERR_INVALID;
+  }
+}
+
+void need(bool ok, weft_status s, const char* msg) {
+  if (!ok) throw weft_gpu::Error(s, msg);
+}
+
+bool is_pow2(int n) { return n > 0 && (n & (n - 1)) == 0; }
+
+// generate_work_queues (proj/src/topology.cpp:34-89).
+void gen_range(int lo, int hi, std::vector<std::vector<int>>& peer, std::vector<std::vector<int>>& vec) {
+  const int size = hi - lo;
+  if (size == 1) return;
+  const int half = size / 2, mid = lo + half;
+  gen_range(lo, mid, peer, vec);
+  gen_range(mid, hi, peer, vec);
+  const size_t child = peer[static_cast<size_t>(lo)].size();
+  for (int i = lo; i < mid; ++i) {
+    peer[i].push_back(i + half);
+    vec[i].push_back(i + half);
+  }
+  for (int j = mid; j < hi; ++j) {
+    peer[j].push_back(j - half);
+    vec[j].push_back(j - half);
+  }
+  for (int i = lo; i < hi; ++i) {
+    const int off = i < mid ? half : -half;
+    for (size_t k = 0; k < child; ++k) {
+      peer[i].push_back(peer[i][k]);
+      vec[i].push_back(vec[i][k] + off);
+    }
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* weft_gpu_last_error(void) { return g_last_error.c_str(); }
+
+weft_status weft_make_partitions(int32_t p, int32_t n, int32_t* begin, int32_t* end) {
+  return guard(nullptr, [&] {
+    if (n < 1) throw weft_gpu::Error(WEFT_ERR_TOPOLOGY, "device count must be >= 1");
+    if (p < 0) throw weft_gpu::Error(WEFT_ERR_DIMENSION, "negative vertex count");
+    const auto pm = weft_gpu::PartMap::make(p, n);
+    for (int d = 0; d < n; ++d) {
+      begin[d] = pm.begin(d);
+      end[d] = pm.end(d);
+    }
+  });
+}
+
+weft_status weft_work_queues(int32_t n, int32_t* peer, int32_t* vec) {
+  return guard(nullptr, [&] {
+    if (!is_pow2(n))
+      throw weft_gpu::Error(WEFT_ERR_TOPOLOGY,
+                            "work queue generation requires power-of-two devices, got " + std::to_string(n));
+    std::vector<std::vector<int>> pr(static_cast<size_t>(n)), vc(static_cast<size_t>(n));
+    gen_range(0, n, pr, vc);
+    for (int d = 0; d < n; ++d)
+      for (int k = 0; k < n - 1; ++k) {
+        peer[d * (n - 1) + k] = pr[d][k];
+        vec[d * (n - 1) + k] = vc[d][k];
+      }
+  });
+}
+
+weft_status weft_split_workload(int64_t total, int32_t devices, int64_t* begin, int64_t* end) {
+  return guard(nullptr, [&] {
+    need(devices >= 1, WEFT_ERR_TOPOLOGY, "device count must be >= 1");
+    const int64_t base = total / devices, extra = total % devices;
+    int64_t cursor = 0;
+    for (int d = 0; d < devices; ++d) {
+      const int64_t size = base + (d < extra ? 1 : 0);
+      begin[d] = cursor;
+      end[d] = cursor + size;
+      cursor += size;
+    }
+  });
+}
+
+weft_status weft_gpu_create(const weft_gpu_options* opts, weft_gpu_ctx** out) {
+  *out = nullptr;
+  auto* ctx = new weft_gpu_ctx();
+  const weft_status st = guard(nullptr, [&] {
+    auto& c = ctx->c;
+    c.device = opts ? opts->cuda_device : 0;
+    c.nparts = opts ? opts->partitions : 1;
+    c.part_begin = opts ? opts->part_begin : 0;
+    c.part_end = opts ? opts->part_end : c.nparts;
+    if (c.nparts < 1 || c.nparts > weft_gpu::kMaxParts)
+      throw weft_gpu::Error(WEFT_ERR_TOPOLOGY, "partition count must be in [1, 8]");
+    if (!is_pow2(c.nparts))
+      throw weft_gpu::Error(WEFT_ERR_TOPOLOGY,
+                            "fat-tree requires a power-of-two device count, got " + std::to_string(c.nparts));
+    if (c.part_begin != 0 || c.part_end != c.nparts)
+      throw weft_gpu::Error(WEFT_ERR_INVALID, "multi-process partition ranges are created through weft_gpu_create_dist");
+    int count = 0;
+    WG_CUDA(cudaGetDeviceCount(&count));
+    if (c.device < 0 || c.device >= count)
+      throw weft_gpu::Error(WEFT_ERR_EXEC, "device " + std::to_string(c.device) + " failed: no such CUDA device");
+    WG_CUDA(cudaSetDevice(c.device));
+    WG_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+    for (auto& e : c.ev) WG_CUDA(cudaEventCreate(&e));
+    c.scalars.resize(64);
+    // accumulation group order from the work queues
+    const int n = c.nparts;
+    c.go.n = n;
+    std::memset(c.go.qpos, 0, sizeof(c.go.qpos));
+    c.queue_vec.assign(static_cast<size_t>(n * (n > 1 ? n - 1 : 0)), 0);
+    if (n > 1) {
+      std::vector<std::vector<int>> pr(static_cast<size_t>(n)), vc(static_cast<size_t>(n));
+      gen_range(0, n, pr, vc);
+      for (int d = 0; d < n; ++d)
+        for (int k = 0; k < n - 1; ++k) {
+          c.queue_vec[static_cast<size_t>(d * (n - 1) + k)] = vc[d][k];
+          c.go.qpos[d][vc[d][k]] = static_cast<int8_t>(k + 1);
+        }
+    }
+  });
+  if (st != WEFT_OK) {
+    delete ctx;
+    return st;
+  }
+  *out = ctx;
+  return WEFT_OK;
+}
+
+weft_status weft_gpu_destroy(weft_gpu_ctx* ctx) {
+  if (!ctx) return WEFT_OK;
+  const weft_status st = guard(ctx, [&] {
+    auto& c = ctx->c;
+    weft_gpu::pcg_free(c);
+    WG_CUDA(cudaStreamSynchronize(c.stream));
+    for (auto& e : c.ev) cudaEventDestroy(e);
+    cudaStreamDestroy(c.stream);
+  });
+  delete ctx;
+  return st;
+}
+
+weft_status weft_gpu_set_matrix(weft_gpu_ctx* ctx, int32_t rows, const int64_t* row_ptr, const int32_t* cols,
+                                const double* vals) {
+  return guard(ctx, [&] {
+    need(row_ptr != nullptr, WEFT_ERR_INVALID, "set_matrix: row_ptr is NULL");
+    // The CSR is read on the host; copy device inputs first.
+    std::vector<int64_t> rp(static_cast<size_t>(rows) + 1);
+    WG_CUDA(cudaMemcpy(rp.data(), row_ptr, rp.size() * sizeof(int64_t), cudaMemcpyDefault));
+    const int64_t nnzb = rp.back();
+    std::vector<int32_t> cl(static_cast<size_t>(nnzb));
+    std::vector<double> vl(9 * static_cast<size_t>(nnzb));
+    if (nnzb) {
+      WG_CUDA(cudaMemcpy(cl.data(), cols, cl.size() * sizeof(int32_t), cudaMemcpyDefault));
+      WG_CUDA(cudaMemcpy(vl.data(), vals, vl.size() * sizeof(double), cudaMemcpyDefault));
+    }
+    weft_gpu::set_matrix_csr(ctx->c, rows, rp.data(), cl.data(), vl.data());
+  });
+}
+
+weft_status weft_gpu_spmv(weft_gpu_ctx* ctx, const double* x, double* y) {
+  return guard(ctx, [&] {
+    auto& c = ctx->c;
+    need(c.has_matrix, WEFT_ERR_INVALID, "spmv: no matrix");
+    const size_t len = 3 * static_cast<size_t>(c.A.rows);
+    c.r.resize(len);
+    c.q.resize(len);
+    WG_CUDA(cudaMemcpyAsync(c.r.data(), x, len * sizeof(double), cudaMemcpyDefault, c.stream));
+    weft_gpu::spmv(c, c.r.data(), c.q.data());
+    WG_CUDA(cudaMemcpyAsync(y, c.q.data(), len * sizeof(double), cudaMemcpyDefault, c.stream));
+    WG_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+
+weft_status weft_gpu_matrix_info(weft_gpu_ctx* ctx, weft_matrix_info* info) {
+  return guard(ctx, [&] {
+    auto& c = ctx->c;
+    need(c.has_matrix, WEFT_ERR_INVALID, "matrix_info: no matrix");
+    info->block_rows = c.A.rows;
+    info->max_row_blocks = c.A.max_len;
+    info->nnzb = c.A.nnzb;
+    info->padded_slots = c.A.total;
+  });
+}
+
+weft_status weft_gpu_download_matrix(weft_gpu_ctx* ctx, int64_t* row_ptr, int32_t* cols, double* vals) {
+  return guard(ctx, [&] {
+    need(ctx->c.has_matrix, WEFT_ERR_INVALID, "download_matrix: no matrix");
+    weft_gpu::download_csr(ctx->c, row_ptr, cols, vals);
+  });
+}
+
+weft_status weft_gpu_download_rhs(weft_gpu_ctx* ctx, double* rhs) {
+  return guard(ctx, [&] {
+    auto& c = ctx->c;
+    need(c.has_rhs, WEFT_ERR_INVALID, "download_rhs: no assembled system");
+    WG_CUDA(cudaMemcpyAsync(rhs, c.rhs.data(), 3 * sizeof(double) * c.A.rows, cudaMemcpyDefault, c.stream));
+    WG_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+
+weft_status weft_gpu_pcg(weft_gpu_ctx* ctx, const double* b, double* x, const weft_pcg_config* config,
+                         weft_pcg_report* report) {
+  return guard(ctx, [&] {
+    auto& c = ctx->c;
+    need(c.has_matrix, WEFT_ERR_INVALID, "pcg: no matrix");
+    need(config != nullptr, WEFT_ERR_INVALID, "pcg: config is NULL");
+    const size_t len = 3 * static_cast<size_t>(c.A.rows);
+    const double* bdev = nullptr;
+    if (b) {
+      c.bvec.resize(len);
+      WG_CUDA(cudaMemcpyAsync(c.bvec.data(), b, len * sizeof(double), cudaMemcpyDefault, c.stream));
+      bdev = c.bvec.data();
+    } else {
+      need(c.has_rhs, WEFT_ERR_INVALID, "pcg: b is NULL and no assembled rhs");
+      bdev = c.rhs.data();
+    }
+    weft_gpu::PcgResult r;
+    try {
+      r = weft_gpu::pcg_solve(c, bdev, *config, report ? report->residual_history : nullptr,
+                              report ? report->precond_norm_history : nullptr);
+    } catch (...) {
+      if (report) report->iterations = 0;
+      throw;
+    }
+    if (report) {
+      report->iterations = r.iterations;
+      report->converged = r.converged;
+      report->rel_residual = r.rel_residual;
+    }
+    if (x) {
+      if (r.iterations == 0) WG_CUDA(cudaMemsetAsync(c.xs.data(), 0, len * sizeof(double), c.stream));
+      WG_CUDA(cudaMemcpyAsync(x, c.xs.data(), len * sizeof(double), cudaMemcpyDefault, c.stream));
+      WG_CUDA(cudaStreamSynchronize(c.stream));
+    }
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,114 @@
+// common.cuh — shared device/host infrastructure for libweft_gpu.so.
+//
+// The whole library is compiled with -fmad=false: every FP64 expression is
+// evaluated as separately rounded multiplies and adds in the association the
+// reference uses (see oracle/shim/Eigen/Dense), which is what makes the
+// assembled matrix and the SpMV bitwise equal to the CPU reference.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/weft_gpu.h"
+
+namespace weft_gpu {
+
+// Error carrying a weft_status; converted at the C-ABI boundary.
+struct Error : std::runtime_error {
+  weft_status status;
+  Error(weft_status s, const std::string& m) : std::runtime_error(m), status(s) {}
+};
+
+inline void cuda_check(cudaError_t e, const char* what, int device) {
+  if (e != cudaSuccess) {
+    // ExecError wording of the reference (proj/src/exec.cpp:164).
+    throw Error(WEFT_ERR_EXEC, "device " + std::to_string(device) + " failed: " + what + ": " +
+                                   cudaGetErrorString(e));
+  }
+}
+
+#define WG_CUDA(call) ::weft_gpu::cuda_check((call), #call, ::weft_gpu::current_device())
+
+inline int current_device() {
+  int d = -1;
+  cudaGetDevice(&d);
+  return d;
+}
+
+// Growable device buffer (capacity never shrinks; memory is plentiful on a
+// 180 GB part, re-allocation per step is not).
+template <class T>
+struct DBuf {
+  T* ptr = nullptr;
+  size_t cap = 0;
+  size_t n = 0;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  ~DBuf() {
+    if (ptr) cudaFree(ptr);
+  }
+  void resize(size_t count) {
+    if (count > cap) {
+      if (ptr) WG_CUDA(cudaFree(ptr));
+      ptr = nullptr;
+      size_t c = count + count / 8 + 16;
+      WG_CUDA(cudaMalloc(&ptr, c * sizeof(T)));
+      cap = c;
+    }
+    n = count;
+  }
+  T* data() const { return ptr; }
+  size_t size() const { return n; }
+  size_t bytes() const { return n * sizeof(T); }
+  void upload(const T* src, size_t count, cudaStream_t s) {
+    resize(count);
+    if (count) WG_CUDA(cudaMemcpyAsync(ptr, src, count * sizeof(T), cudaMemcpyDefault, s));
+  }
+  void download(T* dst, size_t count, cudaStream_t s) const {
+    if (count) WG_CUDA(cudaMemcpyAsync(dst, ptr, count * sizeof(T), cudaMemcpyDefault, s));
+  }
+  void zero(cudaStream_t s) {
+    if (n) WG_CUDA(cudaMemsetAsync(ptr, 0, n * sizeof(T), s));
+  }
+};
+
+constexpr int kSlice = 32;  // sliced-ELL slice height (one warp of rows)
+constexpr int kMaxParts = 8;
+
+// PartitionMap::owner (proj/include/weft/assembly.hpp:27-31).
+struct PartMap {
+  int p = 0, n = 1, base = 0, extra = 0;
+  __host__ __device__ int owner(int v) const {
+    const int split = extra * (base + 1);
+    if (v < split) return v / (base + 1);
+    return extra + (v - split) / (base > 1 ? base : 1);
+  }
+  __host__ __device__ int begin(int d) const { return d * base + (d < extra ? d : extra); }
+  __host__ __device__ int end(int d) const { return begin(d) + base + (d < extra ? 1 : 0); }
+  static PartMap make(int p, int n) {
+    PartMap m;
+    m.p = p;
+    m.n = n;
+    m.base = p / n;
+    m.extra = p % n;
+    return m;
+  }
+};
+
+// Per-partition processing order of column owners: qpos[d][o] = position of
+// owner o in device d's accumulation order (0 = own sub-block, k = k-th
+// work-queue node; proj/include/weft/sparse.hpp:89-95).
+struct GroupOrder {
+  int n = 1;
+  int8_t qpos[kMaxParts][kMaxParts];
+};
+
+inline int div_up(long long a, long long b) { return static_cast<int>((a + b - 1) / b); }
+
+}  // namespace weft_gpu

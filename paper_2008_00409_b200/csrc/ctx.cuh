@@ -1,0 +1,137 @@
+// ctx.cuh — the device-resident session behind weft_gpu_ctx.
+#pragma once
+
+#include "common.cuh"
+
+namespace weft_gpu {
+
+// Sliced-ELL (SELL-32) 3x3-block matrix. Slot k of row r lives at
+// slice_off[r/32] + 32*k + r%32; the nine block components are nine planes
+// of `total` doubles each (the reference's nine SoA value planes,
+// proj/include/weft/bell.hpp:61-79, re-laid slot-major per warp of rows so
+// one load instruction moves 256 contiguous bytes). Per row, slots are
+// ordered by accumulation group (own partition first, then the work-queue
+// order) and by ascending column within a group; the group position is
+// packed in bits 28..30 of the column word.
+struct SellMatrix {
+  int rows = 0;
+  int nslices = 0;
+  int64_t total = 0;  // slots incl. padding
+  int64_t nnzb = 0;
+  int max_len = 0;
+  DBuf<int64_t> slice_off;  // nslices + 1
+  DBuf<int32_t> rowlen;     // rows
+  DBuf<int32_t> cols;       // total (packed col | group << 28; -1 padding)
+  DBuf<double> vals;        // 9 * total
+};
+
+constexpr int kColMask = 0x0FFFFFFF;
+constexpr int kGroupShift = 28;
+
+struct PcgState;  // device scalars, see pcg.cu
+
+struct Ctx {
+  int device = 0;
+  int nparts = 1;
+  int part_begin = 0, part_end = 1;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev[8] = {};
+
+  // ---- vertices / partitions
+  int p = 0;
+  PartMap pm;
+  GroupOrder go;
+  std::vector<int> queue_vec;  // n*(n-1)
+  DBuf<double> mass;
+  DBuf<uint8_t> pinned;
+
+  // ---- elements (static list followed by per-step contacts)
+  int64_t n_static = 0, n_contacts = 0;
+  DBuf<int4> est;         // stencil per element (-1 padded)
+  DBuf<int2> einfo;       // (kind | stencil_size << 8, payload offset)
+  DBuf<double> edamp;     // element damping
+  DBuf<double> epay;      // payload pool
+  int64_t static_pay = 0;  // payload doubles used by static elements
+  // static row incidences: per row, (element*4 + a) ascending element
+  DBuf<int64_t> inc_ptr;  // p + 1
+  DBuf<int32_t> inc;
+  // static pattern: per row ascending columns (CSR)
+  DBuf<int64_t> spat_ptr;  // p + 1
+  DBuf<int32_t> spat;
+  int static_max_len = 0;
+  // contact incidences (rebuilt per step)
+  DBuf<int64_t> cinc_ptr;  // p + 1
+  DBuf<int32_t> cinc;      // (contact index * 4 + a), ascending contact
+  bool have_pattern_for_contacts = false;
+
+  // ---- assembled / loaded system
+  SellMatrix A;
+  DBuf<double> rhs;
+  bool has_matrix = false;
+  bool has_rhs = false;
+
+  // ---- vectors of the current step (3p doubles)
+  DBuf<double> x_cur, x_adv, vel;
+
+  // ---- PCG work
+  DBuf<double> r, z, pv, q, xs, dinv, bvec;
+  DBuf<double> partials;
+  DBuf<double> hist, phist;
+  PcgState* pcg = nullptr;       // device
+  void* pcg_host = nullptr;      // pinned mirror
+
+  // ---- broad phase
+  int soup_verts = 0, soup_tris = 0;
+  DBuf<int32_t> tris;          // 3 per triangle
+  DBuf<double> box_lo, box_hi; // 3 per triangle
+  DBuf<double> diag;           // per triangle
+  DBuf<double> cell_size;      // 1
+  DBuf<int32_t> lat;           // 6 per triangle
+  DBuf<int64_t> ecount;        // per triangle entries (+1 for scan)
+  DBuf<uint64_t> keys_a, keys_b;
+  DBuf<int32_t> vals_a, vals_b;
+  DBuf<uint64_t> cell_keys;
+  DBuf<int64_t> cell_off;      // cells + 1
+  DBuf<int64_t> wprefix;       // cells + 1
+  DBuf<int32_t> cell_flag;
+  int64_t grid_entries = 0, grid_cells = 0, grid_total = 0;
+  double grid_cell_size = 0.0;
+  DBuf<int64_t> cand_count;
+  DBuf<int32_t> cand_pairs;
+  bool has_grid = false;
+
+  // ---- CUB scratch
+  DBuf<unsigned char> scratch;
+  DBuf<int64_t> scalars;  // small device scratch
+
+  // ---- resident simulation state
+  DBuf<double> sim_x, sim_v, sim_xc;
+  bool has_state = false;
+};
+
+// ---- entry points implemented across the .cu files
+void set_matrix_csr(Ctx& c, int rows, const int64_t* row_ptr, const int32_t* cols, const double* vals);
+void spmv(Ctx& c, const double* x_dev, double* y_dev);
+void download_csr(Ctx& c, int64_t* row_ptr, int32_t* cols, double* vals);
+struct PcgResult {
+  int iterations = 0;
+  int converged = 0;
+  double rel_residual = 0.0;
+};
+PcgResult pcg_solve(Ctx& c, const double* b_dev, const weft_pcg_config& cfg, double* hist_host,
+                    double* phist_host);
+void pcg_free(Ctx& c);
+
+void set_vertices(Ctx& c, int p, const double* mass, const uint8_t* pinned);
+void set_elements(Ctx& c, int64_t count, const weft_element* elems);
+void set_contacts(Ctx& c, int64_t count, const weft_element* elems);
+void fill_matrix(Ctx& c, double dt, int mode);  // uses c.x_cur, c.x_adv, c.vel
+
+void set_soup(Ctx& c, int verts, int ntris, const int32_t* tris);
+void build_grid(Ctx& c, const double* x0_dev, const double* x1_dev, int mode, double thickness, double cell_scale);
+int64_t candidates(Ctx& c, int64_t begin, int64_t end, int32_t* pairs_dev_or_null);
+
+// CUB scratch helper
+void* scratch(Ctx& c, size_t bytes);
+
+}  // namespace weft_gpu

@@ -1,0 +1,643 @@
+// sparse.cu — sliced-ELL 3x3-block matrix, SpMV and block-Jacobi PCG.
+//
+// Reference: BellMatrix::multiply_into/accumulate (proj/src/bell.cpp:87-129),
+// spmv_pipelined (proj/include/weft/sparse.hpp:72-101) and pcg_solve
+// (proj/include/weft/solver.hpp:36-178).
+//
+// SpMV is HBM-bound (~0.2 FLOP/B): one thread per block row walks its slots
+// (coalesced 256-byte plane loads per warp per component), gathers x from
+// L2, and keeps the reference's per-row order exactly: a fresh partial sum
+// per partition group, the own group assigned first, the others added in
+// work-queue order. The PCG is device-driven: two kernels per iteration,
+// (1) SpMV with the search direction p = z + beta p formed on the fly and
+// the p.q partial fused into the epilogue, the last block finalising alpha;
+// (2) the x/r update, block-Jacobi z = D^-1 r and the r.r / r.z partials,
+// the last block finalising the residual test and beta. Dot products are
+// reduced per partition in a fixed tree and then summed in ascending
+// partition order (Engine::all_reduce_sum, proj/src/exec.cpp:170-174).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+
+#include "ctx.cuh"
+
+namespace weft_gpu {
+
+// ---------------------------------------------------------------------------
+// Matrix view passed to kernels
+// ---------------------------------------------------------------------------
+struct SellView {
+  int rows;
+  int64_t total;
+  const int64_t* __restrict__ slice_off;
+  const int32_t* __restrict__ rowlen;
+  const int32_t* __restrict__ cols;
+  const double* __restrict__ vals;
+};
+
+static SellView view(const SellMatrix& A) {
+  return SellView{A.rows, A.total, A.slice_off.data(), A.rowlen.data(), A.cols.data(), A.vals.data()};
+}
+
+// Blocks are aligned to partitions so that every block's dot partial
+// belongs to exactly one partition.
+struct PartBlocks {
+  int n;
+  int bstart[kMaxParts + 1];
+  int rbegin[kMaxParts];
+  int rend[kMaxParts];
+};
+
+static PartBlocks part_blocks(const PartMap& pm, int threads) {
+  PartBlocks pb{};
+  pb.n = pm.n;
+  pb.bstart[0] = 0;
+  for (int d = 0; d < pm.n; ++d) {
+    pb.rbegin[d] = pm.begin(d);
+    pb.rend[d] = pm.end(d);
+    pb.bstart[d + 1] = pb.bstart[d] + div_up(pb.rend[d] - pb.rbegin[d], threads);
+  }
+  return pb;
+}
+
+__device__ __forceinline__ int block_part(const PartBlocks& pb, int b) {
+  int d = 0;
+  while (d + 1 < pb.n && b >= pb.bstart[d + 1]) ++d;
+  return d;
+}
+
+// ---------------------------------------------------------------------------
+// Row product in the reference order
+// ---------------------------------------------------------------------------
+// PMode 0: x given. PMode 1: x = z (first PCG iteration, p = z).
+// PMode 2: x = z + beta * p_old on the fly (PCG p update).
+template <int PMode>
+__device__ __forceinline__ void row_product(const SellView& A, int r, int ngroups, const double* __restrict__ x,
+                                            const double* __restrict__ pold, double beta, double& y0, double& y1,
+                                            double& y2) {
+  const int len = A.rowlen[r];
+  const int64_t base = A.slice_off[r >> 5] + (r & 31);
+  const int64_t T = A.total;
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+  int cg = 0;
+  y0 = y1 = y2 = 0.0;
+#pragma unroll 2
+  for (int k = 0; k < len; ++k) {
+    const int64_t at = base + (int64_t)k * kSlice;
+    const int packed = __ldg(A.cols + at);
+    const int c = packed & kColMask;
+    const int g = (int)((unsigned)packed >> kGroupShift);
+    while (cg < g) {
+      if (cg == 0) {
+        y0 = a0;
+        y1 = a1;
+        y2 = a2;
+      } else {
+        y0 = y0 + a0;
+        y1 = y1 + a1;
+        y2 = y2 + a2;
+      }
+      a0 = a1 = a2 = 0.0;
+      ++cg;
+    }
+    const double* v = A.vals + at;
+    const double v0 = __ldg(v), v1 = __ldg(v + T), v2 = __ldg(v + 2 * T);
+    const double v3 = __ldg(v + 3 * T), v4 = __ldg(v + 4 * T), v5 = __ldg(v + 5 * T);
+    const double v6 = __ldg(v + 6 * T), v7 = __ldg(v + 7 * T), v8 = __ldg(v + 8 * T);
+    double x0 = x[3 * c], x1 = x[3 * c + 1], x2 = x[3 * c + 2];
+    if (PMode == 2) {
+      x0 = x0 + beta * pold[3 * c];
+      x1 = x1 + beta * pold[3 * c + 1];
+      x2 = x2 + beta * pold[3 * c + 2];
+    }
+    a0 = a0 + ((v0 * x0 + v1 * x1) + v2 * x2);
+    a1 = a1 + ((v3 * x0 + v4 * x1) + v5 * x2);
+    a2 = a2 + ((v6 * x0 + v7 * x1) + v8 * x2);
+  }
+  while (cg < ngroups) {
+    if (cg == 0) {
+      y0 = a0;
+      y1 = a1;
+      y2 = a2;
+    } else {
+      y0 = y0 + a0;
+      y1 = y1 + a1;
+      y2 = y2 + a2;
+    }
+    a0 = a1 = a2 = 0.0;
+    ++cg;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_spmv(SellView A, int ngroups, const double* __restrict__ x,
+                                              double* __restrict__ y) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= A.rows) return;
+  double y0, y1, y2;
+  row_product<0>(A, r, ngroups, x, nullptr, 0.0, y0, y1, y2);
+  y[3 * r] = y0;
+  y[3 * r + 1] = y1;
+  y[3 * r + 2] = y2;
+}
+
+void spmv(Ctx& c, const double* x_dev, double* y_dev) {
+  if (!c.has_matrix) throw Error(WEFT_ERR_INVALID, "spmv: no matrix loaded");
+  const int threads = 256;
+  if (c.A.rows == 0) return;
+  k_spmv<<<div_up(c.A.rows, threads), threads, 0, c.stream>>>(view(c.A), c.go.n, x_dev, y_dev);
+  WG_CUDA(cudaGetLastError());
+}
+
+// ---------------------------------------------------------------------------
+// Host construction of the SELL layout from a global CSR (set_matrix path)
+// ---------------------------------------------------------------------------
+void set_matrix_csr(Ctx& c, int rows, const int64_t* row_ptr, const int32_t* cols, const double* vals) {
+  if (rows < 0) throw Error(WEFT_ERR_DIMENSION, "set_matrix: negative row count");
+  if (rows >= (1 << 28)) throw Error(WEFT_ERR_DIMENSION, "set_matrix: more than 2^28 block rows");
+  c.pm = PartMap::make(rows, c.nparts);
+  if (rows < c.nparts) throw Error(WEFT_ERR_DIMENSION, "set_matrix: fewer rows than partitions");
+  SellMatrix& A = c.A;
+  A.rows = rows;
+  A.nslices = div_up(rows, kSlice);
+  std::vector<int32_t> len(static_cast<size_t>(rows));
+  std::vector<int64_t> soff(static_cast<size_t>(A.nslices) + 1, 0);
+  int64_t nnzb = 0;
+  int maxlen = 0;
+  for (int r = 0; r < rows; ++r) {
+    const int64_t l = row_ptr[r + 1] - row_ptr[r];
+    if (l < 0) throw Error(WEFT_ERR_DIMENSION, "set_matrix: row_ptr not monotone");
+    len[static_cast<size_t>(r)] = static_cast<int32_t>(l);
+    nnzb += l;
+    maxlen = std::max<int>(maxlen, static_cast<int>(l));
+  }
+  for (int s = 0; s < A.nslices; ++s) {
+    int w = 0;
+    for (int r = s * kSlice; r < std::min(rows, (s + 1) * kSlice); ++r) w = std::max(w, len[static_cast<size_t>(r)]);
+    soff[static_cast<size_t>(s) + 1] = soff[static_cast<size_t>(s)] + static_cast<int64_t>(w) * kSlice;
+  }
+  const int64_t total = soff.back();
+  std::vector<int32_t> hc(static_cast<size_t>(total), -1);
+  std::vector<double> hv(9 * static_cast<size_t>(total), 0.0);
+  std::vector<std::pair<int, int64_t>> order;  // (group, csr index)
+  for (int r = 0; r < rows; ++r) {
+    const int d = c.pm.owner(r);
+    order.clear();
+    for (int64_t k = row_ptr[r]; k < row_ptr[r + 1]; ++k) {
+      const int col = cols[k];
+      if (col < 0 || col >= rows) throw Error(WEFT_ERR_DIMENSION, "input vector too short for column index");
+      order.push_back({c.go.qpos[d][c.pm.owner(col)], k});
+    }
+    std::stable_sort(order.begin(), order.end(),
+                     [](const auto& a, const auto& b) { return a.first < b.first; });
+    const int64_t base = soff[static_cast<size_t>(r / kSlice)] + r % kSlice;
+    for (size_t s = 0; s < order.size(); ++s) {
+      const int64_t at = base + static_cast<int64_t>(s) * kSlice;
+      const int64_t k = order[s].second;
+      hc[static_cast<size_t>(at)] = cols[k] | (order[s].first << kGroupShift);
+      for (int q = 0; q < 9; ++q) hv[static_cast<size_t>(q * total + at)] = vals[9 * k + q];
+    }
+  }
+  A.total = total;
+  A.nnzb = nnzb;
+  A.max_len = maxlen;
+  A.slice_off.upload(soff.data(), soff.size(), c.stream);
+  A.rowlen.upload(len.data(), len.size(), c.stream);
+  A.cols.upload(hc.data(), hc.size(), c.stream);
+  A.vals.upload(hv.data(), hv.size(), c.stream);
+  WG_CUDA(cudaStreamSynchronize(c.stream));
+  c.has_matrix = true;
+  c.has_rhs = false;
+}
+
+// Global CSR with ascending columns (gather_matrix, sparse.hpp:149-173).
+void download_csr(Ctx& c, int64_t* row_ptr, int32_t* cols, double* vals) {
+  SellMatrix& A = c.A;
+  std::vector<int64_t> soff(A.slice_off.size());
+  std::vector<int32_t> len(static_cast<size_t>(A.rows));
+  std::vector<int32_t> hc(static_cast<size_t>(A.total));
+  A.slice_off.download(soff.data(), soff.size(), c.stream);
+  A.rowlen.download(len.data(), len.size(), c.stream);
+  A.cols.download(hc.data(), hc.size(), c.stream);
+  std::vector<double> hv;
+  if (vals) {
+    hv.resize(9 * static_cast<size_t>(A.total));
+    A.vals.download(hv.data(), hv.size(), c.stream);
+  }
+  WG_CUDA(cudaStreamSynchronize(c.stream));
+  int64_t cursor = 0;
+  std::vector<std::pair<int, int64_t>> order;
+  if (row_ptr) row_ptr[0] = 0;
+  for (int r = 0; r < A.rows; ++r) {
+    const int64_t base = soff[static_cast<size_t>(r / kSlice)] + r % kSlice;
+    order.clear();
+    for (int k = 0; k < len[static_cast<size_t>(r)]; ++k) {
+      const int64_t at = base + static_cast<int64_t>(k) * kSlice;
+      order.push_back({hc[static_cast<size_t>(at)] & kColMask, at});
+    }
+    std::sort(order.begin(), order.end());
+    for (const auto& [col, at] : order) {
+      if (cols) cols[cursor] = col;
+      if (vals)
+        for (int q = 0; q < 9; ++q) vals[9 * cursor + q] = hv[static_cast<size_t>(q * A.total + at)];
+      ++cursor;
+    }
+    if (row_ptr) row_ptr[r + 1] = cursor;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Deterministic block reduction helpers
+// ---------------------------------------------------------------------------
+template <int NV>
+__device__ __forceinline__ void block_sum(double (&v)[NV], double* smem /* NV * 32 */) {
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v[i] = v[i] + __shfl_xor_sync(0xffffffffu, v[i], o);
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nw = blockDim.x >> 5;
+  if (lane == 0)
+#pragma unroll
+    for (int i = 0; i < NV; ++i) smem[i * 32 + warp] = v[i];
+  __syncthreads();
+  if (warp == 0) {
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      double t = lane < nw ? smem[i * 32 + lane] : 0.0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) t = t + __shfl_xor_sync(0xffffffffu, t, o);
+      v[i] = t;
+    }
+  }
+  __syncthreads();
+}
+
+// Sums partials[b*NV + i] over blocks of each partition (fixed strided
+// order + fixed tree), then over partitions in ascending order. Called by
+// all threads of the last block; result valid in thread 0.
+template <int NV>
+__device__ void finalize_sums(const PartBlocks& pb, const double* partials, double (&out)[NV], double* smem) {
+  double total[NV];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) total[i] = 0.0;
+  for (int d = 0; d < pb.n; ++d) {
+    double v[NV];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) v[i] = 0.0;
+    for (int b = pb.bstart[d] + threadIdx.x; b < pb.bstart[d + 1]; b += blockDim.x)
+#pragma unroll
+      for (int i = 0; i < NV; ++i) v[i] = v[i] + __ldcg(partials + (size_t)b * NV + i);
+    block_sum<NV>(v, smem);
+#pragma unroll
+    for (int i = 0; i < NV; ++i) total[i] = total[i] + v[i];  // only thread 0's value is used
+  }
+#pragma unroll
+  for (int i = 0; i < NV; ++i) out[i] = total[i];
+}
+
+// ---------------------------------------------------------------------------
+// PCG
+// ---------------------------------------------------------------------------
+struct PcgState {
+  double rho, alpha, beta, b_norm, tol, r_norm;
+  int iter;       // completed iterations
+  int done;       // 1 = stop (converged, error, or max iterations)
+  int status;     // 0 ok, 1 non-finite curvature, 2 non-positive, 3 divergence
+  int converged;
+  int max_iter;
+  int first;      // next SpMV uses p = z
+  unsigned counter;
+};
+
+__device__ __forceinline__ bool last_block(unsigned* counter) {
+  __shared__ bool s_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned t = atomicAdd(counter, 1u);
+    s_last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (s_last) __threadfence();
+  return s_last;
+}
+
+// Row range of block b under partition-aligned blocking.
+__device__ __forceinline__ int block_row(const PartBlocks& pb, int b, int& rend) {
+  const int d = block_part(pb, b);
+  rend = pb.rend[d];
+  return pb.rbegin[d] + (b - pb.bstart[d]) * blockDim.x + threadIdx.x;
+}
+
+// dot(u, v) per partition + ascending sum into *out (used for ||b||, rho0).
+__global__ void __launch_bounds__(256) k_dot2(PartBlocks pb, const double* __restrict__ u, const double* __restrict__ v,
+                                              const double* __restrict__ u2, const double* __restrict__ v2,
+                                              double* partials, unsigned* counter, double* out) {
+  __shared__ double smem[2 * 32];
+  int rend;
+  const int r = block_row(pb, blockIdx.x, rend);
+  double s[2] = {0.0, 0.0};
+  if (r < rend) {
+    s[0] = (u[3 * r] * v[3 * r] + u[3 * r + 1] * v[3 * r + 1]) + u[3 * r + 2] * v[3 * r + 2];
+    if (u2) s[1] = (u2[3 * r] * v2[3 * r] + u2[3 * r + 1] * v2[3 * r + 1]) + u2[3 * r + 2] * v2[3 * r + 2];
+  }
+  block_sum<2>(s, smem);
+  if (threadIdx.x == 0) {
+    partials[2 * blockIdx.x] = s[0];
+    partials[2 * blockIdx.x + 1] = s[1];
+  }
+  if (!last_block(counter)) return;
+  double t[2];
+  finalize_sums<2>(pb, partials, t, smem);
+  if (threadIdx.x == 0) {
+    out[0] = t[0];
+    out[1] = t[1];
+    *counter = 0;
+  }
+}
+
+// Block-Jacobi inverse of the diagonal blocks (solver.hpp:49-65) with the
+// cofactor inverse of oracle/shim/Eigen/Dense; identity when absent.
+__global__ void k_dinv(SellView A, double* __restrict__ dinv) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= A.rows) return;
+  const int len = A.rowlen[r];
+  const int64_t base = A.slice_off[r >> 5] + (r & 31);
+  double m[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
+  for (int k = 0; k < len; ++k) {
+    const int64_t at = base + (int64_t)k * kSlice;
+    if ((A.cols[at] & kColMask) == r) {
+      for (int q = 0; q < 9; ++q) m[q] = A.vals[at + q * A.total];
+      break;
+    }
+  }
+#define M(i, j) m[(i) * 3 + (j)]
+#define COF(i, j)                                                                                   \
+  (M(((i) + 1) % 3, ((j) + 1) % 3) * M(((i) + 2) % 3, ((j) + 2) % 3) -                              \
+   M(((i) + 1) % 3, ((j) + 2) % 3) * M(((i) + 2) % 3, ((j) + 1) % 3))
+  const double c00 = COF(0, 0), c10 = COF(1, 0), c20 = COF(2, 0);
+  const double det = (c00 * M(0, 0) + c10 * M(1, 0)) + c20 * M(2, 0);
+  const double invdet = 1.0 / det;
+  double* o = dinv + 9 * (size_t)r;
+  o[0] = c00 * invdet;
+  o[1] = c10 * invdet;
+  o[2] = c20 * invdet;
+  o[3] = COF(0, 1) * invdet;
+  o[4] = COF(1, 1) * invdet;
+  o[5] = COF(2, 1) * invdet;
+  o[6] = COF(0, 2) * invdet;
+  o[7] = COF(1, 2) * invdet;
+  o[8] = COF(2, 2) * invdet;
+#undef COF
+#undef M
+}
+
+// apply_precond (solver.hpp:67-89): acc = 0; acc += m(i,j) * src[j].
+__device__ __forceinline__ void precond_row(const double* __restrict__ dinv, bool bj, int r, double r0, double r1,
+                                            double r2, double& z0, double& z1, double& z2) {
+  if (!bj) {
+    z0 = r0;
+    z1 = r1;
+    z2 = r2;
+    return;
+  }
+  const double* m = dinv + 9 * (size_t)r;
+  z0 = ((0.0 + m[0] * r0) + m[1] * r1) + m[2] * r2;
+  z1 = ((0.0 + m[3] * r0) + m[4] * r1) + m[5] * r2;
+  z2 = ((0.0 + m[6] * r0) + m[7] * r1) + m[8] * r2;
+}
+
+// PCG init: x = 0, r = b, z = M^-1 r (p = z is formed by the first SpMV).
+__global__ void k_pcg_init(int rows, const double* __restrict__ b, const double* __restrict__ dinv, bool bj,
+                           double* __restrict__ x, double* __restrict__ r, double* __restrict__ z,
+                           double* __restrict__ p) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= rows) return;
+  const double b0 = b[3 * i], b1 = b[3 * i + 1], b2 = b[3 * i + 2];
+  double z0, z1, z2;
+  precond_row(dinv, bj, i, b0, b1, b2, z0, z1, z2);
+  x[3 * i] = x[3 * i + 1] = x[3 * i + 2] = 0.0;
+  r[3 * i] = b0;
+  r[3 * i + 1] = b1;
+  r[3 * i + 2] = b2;
+  z[3 * i] = z0;
+  z[3 * i + 1] = z1;
+  z[3 * i + 2] = z2;
+  p[3 * i] = p[3 * i + 1] = p[3 * i + 2] = 0.0;
+}
+
+// Iteration kernel 1: q = A p with p = z (+ beta p) formed on the fly;
+// p.q partials; last block: curvature checks and alpha = rho / pq.
+__global__ void __launch_bounds__(256) k_pcg_spmv(SellView A, PartBlocks pb, int ngroups, const double* __restrict__ z,
+                                                  const double* __restrict__ p, double* __restrict__ q,
+                                                  double* partials, PcgState* st) {
+  __shared__ double smem[32];
+  if (st->done) return;
+  const bool first = st->first != 0;
+  const double beta = st->beta;
+  int rend;
+  const int r = block_row(pb, blockIdx.x, rend);
+  double s[1] = {0.0};
+  if (r < rend) {
+    double y0, y1, y2;
+    if (first) row_product<1>(A, r, ngroups, z, p, beta, y0, y1, y2);
+    else row_product<2>(A, r, ngroups, z, p, beta, y0, y1, y2);
+    q[3 * r] = y0;
+    q[3 * r + 1] = y1;
+    q[3 * r + 2] = y2;
+    double p0 = z[3 * r], p1 = z[3 * r + 1], p2 = z[3 * r + 2];
+    if (!first) {
+      p0 = p0 + beta * p[3 * r];
+      p1 = p1 + beta * p[3 * r + 1];
+      p2 = p2 + beta * p[3 * r + 2];
+    }
+    s[0] = (p0 * y0 + p1 * y1) + p2 * y2;
+  }
+  block_sum<1>(s, smem);
+  if (threadIdx.x == 0) partials[blockIdx.x] = s[0];
+  if (!last_block(&st->counter)) return;
+  double t[1];
+  finalize_sums<1>(pb, partials, t, smem);
+  if (threadIdx.x == 0) {
+    st->counter = 0;
+    const double pq = t[0];
+    const int it = st->iter + 1;
+    if (!isfinite(pq)) {
+      st->status = 1;
+      st->done = 1;
+      st->iter = it;
+    } else if (pq <= 0.0) {
+      st->status = 2;
+      st->done = 1;
+      st->iter = it;
+    } else {
+      st->alpha = st->rho / pq;
+    }
+  }
+}
+
+// Iteration kernel 2: p = z + beta p (own rows), x += alpha p,
+// r -= alpha q, z = M^-1 r; r.r and r.z partials; last block: residual
+// history, convergence test, beta.
+__global__ void __launch_bounds__(256) k_pcg_update(PartBlocks pb, const double* __restrict__ dinv, bool bj,
+                                                    double* __restrict__ x, double* __restrict__ r,
+                                                    double* __restrict__ z, double* __restrict__ p,
+                                                    const double* __restrict__ q, double* partials, PcgState* st,
+                                                    double* hist, double* phist) {
+  __shared__ double smem[2 * 32];
+  if (st->done) return;
+  const bool first = st->first != 0;
+  const double beta = st->beta, alpha = st->alpha;
+  int rend;
+  const int i = block_row(pb, blockIdx.x, rend);
+  double s[2] = {0.0, 0.0};
+  if (i < rend) {
+    double pr[3], rr[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const double zc = z[3 * i + c];
+      pr[c] = first ? zc : zc + beta * p[3 * i + c];
+      p[3 * i + c] = pr[c];
+      x[3 * i + c] = x[3 * i + c] + alpha * pr[c];
+      rr[c] = r[3 * i + c] - alpha * q[3 * i + c];
+      r[3 * i + c] = rr[c];
+    }
+    double z0, z1, z2;
+    precond_row(dinv, bj, i, rr[0], rr[1], rr[2], z0, z1, z2);
+    z[3 * i] = z0;
+    z[3 * i + 1] = z1;
+    z[3 * i + 2] = z2;
+    s[0] = (rr[0] * rr[0] + rr[1] * rr[1]) + rr[2] * rr[2];
+    s[1] = (rr[0] * z0 + rr[1] * z1) + rr[2] * z2;
+  }
+  block_sum<2>(s, smem);
+  if (threadIdx.x == 0) {
+    partials[2 * blockIdx.x] = s[0];
+    partials[2 * blockIdx.x + 1] = s[1];
+  }
+  if (!last_block(&st->counter)) return;
+  double t[2];
+  finalize_sums<2>(pb, partials, t, smem);
+  if (threadIdx.x == 0) {
+    st->counter = 0;
+    const int it = st->iter + 1;
+    st->iter = it;
+    st->first = 0;
+    const double r_norm = sqrt(t[0]);
+    st->r_norm = r_norm;
+    if (!isfinite(r_norm)) {
+      st->status = 3;
+      st->done = 1;
+      return;
+    }
+    hist[it - 1] = r_norm / st->b_norm;
+    const double rho_next = t[1];
+    phist[it - 1] = sqrt(rho_next > 0.0 ? rho_next : 0.0);
+    if (r_norm <= st->tol) {
+      st->converged = 1;
+      st->done = 1;
+      return;
+    }
+    st->beta = rho_next / st->rho;
+    st->rho = rho_next;
+    if (it >= st->max_iter) st->done = 1;
+  }
+}
+
+void pcg_free(Ctx& c) {
+  if (c.pcg) cudaFree(c.pcg);
+  if (c.pcg_host) cudaFreeHost(c.pcg_host);
+  c.pcg = nullptr;
+  c.pcg_host = nullptr;
+}
+
+PcgResult pcg_solve(Ctx& c, const double* b_dev, const weft_pcg_config& cfg, double* hist_host,
+                    double* phist_host) {
+  if (!c.has_matrix) throw Error(WEFT_ERR_INVALID, "pcg: no matrix");
+  const int rows = c.A.rows;
+  const size_t len = 3 * static_cast<size_t>(rows);
+  const int threads = 256;
+  if (!c.pcg) {
+    WG_CUDA(cudaMalloc(&c.pcg, sizeof(PcgState)));
+    WG_CUDA(cudaHostAlloc(&c.pcg_host, sizeof(PcgState), cudaHostAllocDefault));
+  }
+  for (auto* v : {&c.r, &c.z, &c.pv, &c.q, &c.xs}) v->resize(len);
+  const bool bj = cfg.preconditioner == WEFT_PRECOND_BLOCK_JACOBI;
+  c.dinv.resize(9 * static_cast<size_t>(rows) + 9);
+  const int max_it = std::max(cfg.max_iterations, 0);
+  c.hist.resize(static_cast<size_t>(max_it) + 1);
+  c.phist.resize(static_cast<size_t>(max_it) + 1);
+  const PartBlocks pb = part_blocks(c.pm, threads);
+  const int nblocks = pb.bstart[pb.n];
+  c.partials.resize(2 * static_cast<size_t>(nblocks) + 2);
+  const SellView A = view(c.A);
+  cudaStream_t s = c.stream;
+
+  PcgState init{};
+  init.max_iter = max_it;
+  init.first = 1;
+  WG_CUDA(cudaMemcpyAsync(c.pcg, &init, sizeof(init), cudaMemcpyHostToDevice, s));
+  double* dots = reinterpret_cast<double*>(c.scalars.data());
+  if (rows > 0) {
+    if (bj) k_dinv<<<div_up(rows, threads), threads, 0, s>>>(A, c.dinv.data());
+    k_pcg_init<<<div_up(rows, threads), threads, 0, s>>>(rows, b_dev, c.dinv.data(), bj, c.xs.data(), c.r.data(),
+                                                         c.z.data(), c.pv.data());
+    // ||b|| and rho = r.z (r = b)
+    k_dot2<<<nblocks, threads, 0, s>>>(pb, b_dev, b_dev, c.r.data(), c.z.data(), c.partials.data(),
+                                       &c.pcg->counter, dots);
+    WG_CUDA(cudaGetLastError());
+  }
+  double hd[2] = {0.0, 0.0};
+  if (rows > 0) WG_CUDA(cudaMemcpyAsync(hd, dots, sizeof(hd), cudaMemcpyDeviceToHost, s));
+  WG_CUDA(cudaStreamSynchronize(s));
+  PcgResult res;
+  const double b_norm = std::sqrt(hd[0]);
+  if (b_norm == 0.0) {
+    res.converged = 1;
+    return res;
+  }
+  init.b_norm = b_norm;
+  init.tol = cfg.rel_tolerance * b_norm;
+  init.rho = hd[1];
+  init.r_norm = b_norm;
+  init.done = max_it == 0 ? 1 : 0;
+  WG_CUDA(cudaMemcpyAsync(c.pcg, &init, sizeof(init), cudaMemcpyHostToDevice, s));
+
+  auto* hs = static_cast<PcgState*>(c.pcg_host);
+  int chunk = 4;
+  for (;;) {
+    for (int k = 0; k < chunk; ++k) {
+      k_pcg_spmv<<<nblocks, threads, 0, s>>>(A, pb, c.go.n, c.z.data(), c.pv.data(), c.q.data(), c.partials.data(),
+                                             c.pcg);
+      k_pcg_update<<<nblocks, threads, 0, s>>>(pb, c.dinv.data(), bj, c.xs.data(), c.r.data(), c.z.data(),
+                                               c.pv.data(), c.q.data(), c.partials.data(), c.pcg, c.hist.data(),
+                                               c.phist.data());
+    }
+    WG_CUDA(cudaGetLastError());
+    WG_CUDA(cudaMemcpyAsync(hs, c.pcg, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
+    WG_CUDA(cudaStreamSynchronize(s));
+    if (hs->done) break;
+    chunk = std::min(chunk * 2, 32);
+  }
+  res.iterations = hs->iter;
+  res.converged = hs->converged;
+  res.rel_residual = hs->r_norm / b_norm;
+  if (hs->status == 1)
+    throw Error(WEFT_ERR_SOLVER, "pcg: non-finite curvature at iteration " + std::to_string(hs->iter));
+  if (hs->status == 2)
+    throw Error(WEFT_ERR_SOLVER,
+                "pcg: non-positive curvature at iteration " + std::to_string(hs->iter) + " (matrix not SPD)");
+  if (hs->status == 3)
+    throw Error(WEFT_ERR_SOLVER,
+                "pcg: divergence (non-finite residual) at iteration " + std::to_string(hs->iter));
+  if (hist_host && res.iterations)
+    WG_CUDA(cudaMemcpyAsync(hist_host, c.hist.data(), sizeof(double) * res.iterations, cudaMemcpyDeviceToHost, s));
+  if (phist_host && res.iterations)
+    WG_CUDA(cudaMemcpyAsync(phist_host, c.phist.data(), sizeof(double) * res.iterations, cudaMemcpyDeviceToHost, s));
+  WG_CUDA(cudaStreamSynchronize(s));
+  return res;
+}
+
+}  // namespace weft_gpu

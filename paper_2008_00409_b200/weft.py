@@ -1,0 +1,359 @@
+"""Python host mirror of the reference hot-path interface over the C-ABI
+(include/weft_gpu.h). Names, argument meaning and error behaviour follow the
+reference C++ (proj/include/weft/*.hpp):
+
+* ``Engine(devices)``                 — weft::Engine(n) (exec.hpp:83-128): a GPU
+                                         context with n logical row partitions.
+* ``Engine.spmv_pipelined(A, x)``     — spmv_pipelined (sparse.hpp:72-101)
+* ``Engine.pcg_solve(A, b, cfg)``     — pcg_solve (solver.hpp:36-178)
+* ``Engine.fill_matrix(...)``         — fill_matrix (assembly.hpp:74-220)
+* ``Engine.step_system(...)``         — step_system (physics.hpp:44-69)
+* ``Engine.build_grid(...)``          — build_grid (collision.cpp:118-179)
+* ``Engine.candidates(...)``          — narrow_phase_range's candidate walk
+                                         (collision.cpp:329-378)
+* ``split_workload``, ``make_partitions``, ``generate_work_queues``.
+
+Errors raise the Python counterparts of the reference's exception classes
+(``DimensionError``, ``SolverError``, ``ExecError``, ...) with the reference's
+message text. The CUDA library is mandatory: importing this module on a box
+without ``libweft_gpu.so`` raises, there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libweft_gpu.so")
+
+STRETCH, BEND, SPRING, EXTERNAL, CONTACT = range(5)
+JAC_EXACT, JAC_SPD = 0, 1
+DISCRETE, CONTINUOUS = 0, 1
+PRECOND_NONE, PRECOND_BLOCK_JACOBI = 0, 1
+
+ELEMENT_DTYPE = np.dtype(
+    [("kind", "<i4"), ("stencil_size", "<i4"), ("stencil", "<i4", (4,)), ("damping", "<f8"), ("data", "<f8", (18,))],
+    align=True,
+)
+
+
+class Error(RuntimeError):
+    """weft::Error (common.hpp:16-20)."""
+
+
+class DimensionError(Error):
+    pass
+
+
+class SolverError(Error):
+    pass
+
+
+class ExecError(Error):
+    pass
+
+
+class TopologyError(Error):
+    pass
+
+
+class ScheduleError(Error):
+    pass
+
+
+_ERRORS = {1: DimensionError, 2: SolverError, 3: ExecError, 4: TopologyError, 5: ScheduleError, 6: Error}
+
+
+class Options(C.Structure):
+    _fields_ = [("cuda_device", C.c_int32), ("partitions", C.c_int32), ("part_begin", C.c_int32),
+                ("part_end", C.c_int32)]
+
+
+class PcgConfig(C.Structure):
+    """PcgConfig (solver.hpp:17-21)."""
+
+    _fields_ = [("rel_tolerance", C.c_double), ("max_iterations", C.c_int32), ("preconditioner", C.c_int32)]
+
+    def __init__(self, rel_tolerance=1e-4, max_iterations=400, preconditioner=PRECOND_BLOCK_JACOBI):
+        super().__init__(rel_tolerance, max_iterations, preconditioner)
+
+
+class _PcgReport(C.Structure):
+    _fields_ = [("iterations", C.c_int32), ("converged", C.c_int32), ("rel_residual", C.c_double),
+                ("residual_history", C.POINTER(C.c_double)), ("precond_norm_history", C.POINTER(C.c_double))]
+
+
+class MatrixInfo(C.Structure):
+    _fields_ = [("block_rows", C.c_int32), ("max_row_blocks", C.c_int32), ("nnzb", C.c_int64),
+                ("padded_slots", C.c_int64)]
+
+
+class GridInfo(C.Structure):
+    _fields_ = [("cell_size", C.c_double), ("cells", C.c_int64), ("entries", C.c_int64), ("total", C.c_int64)]
+
+
+class SimParams(C.Structure):
+    _fields_ = [("dt", C.c_double), ("thickness", C.c_double), ("cell_scale", C.c_double), ("pcg", PcgConfig),
+                ("jac_mode", C.c_int32)]
+
+
+class StepReport(C.Structure):
+    _fields_ = [("pcg_iterations", C.c_int32), ("pcg_converged", C.c_int32), ("pcg_residual", C.c_double),
+                ("dcd_candidates", C.c_int64), ("ccd_candidates", C.c_int64), ("ms_broad", C.c_double),
+                ("ms_assemble", C.c_double), ("ms_solve", C.c_double)]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2008_00409_b200.build` "
+                          "(no CPU fallback exists)")
+    lib = C.CDLL(LIB_PATH)
+    lib.weft_gpu_last_error.restype = C.c_char_p
+    return lib
+
+
+LIB = _load()
+
+
+def _ptr(a):
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        return a.ctypes.data_as(C.c_void_p)
+    if hasattr(a, "data_ptr"):  # torch tensor (device or host)
+        return C.c_void_p(a.data_ptr())
+    raise TypeError(type(a))
+
+
+def _check(status: int):
+    if status != 0:
+        msg = LIB.weft_gpu_last_error().decode()
+        raise _ERRORS.get(status, Error)(msg)
+
+
+def _f64(a):
+    return np.ascontiguousarray(a, np.float64).reshape(-1)
+
+
+# ---------------------------------------------------------------------------
+# free functions
+# ---------------------------------------------------------------------------
+def make_partitions(vertex_count: int, devices: int):
+    """make_partitions (exec.cpp:10-23) -> list of (begin, end)."""
+    b = np.zeros(devices, np.int32)
+    e = np.zeros(devices, np.int32)
+    _check(LIB.weft_make_partitions(C.c_int32(vertex_count), C.c_int32(devices), _ptr(b), _ptr(e)))
+    return list(zip(b.tolist(), e.tolist()))
+
+
+def generate_work_queues(devices: int):
+    """generate_work_queues(FatTree::make(n)) (topology.cpp:79-89) -> per
+    device list of (peer, vec)."""
+    m = max(devices - 1, 1)
+    peer = np.zeros(devices * m, np.int32)
+    vec = np.zeros(devices * m, np.int32)
+    _check(LIB.weft_work_queues(C.c_int32(devices), _ptr(peer), _ptr(vec)))
+    return [list(zip(peer[d * (devices - 1):(d + 1) * (devices - 1)].tolist(),
+                     vec[d * (devices - 1):(d + 1) * (devices - 1)].tolist())) for d in range(devices)]
+
+
+def split_workload(total: int, devices: int):
+    """split_workload (collision.cpp:181-192) -> list of (begin, end)."""
+    b = np.zeros(devices, np.int64)
+    e = np.zeros(devices, np.int64)
+    _check(LIB.weft_split_workload(C.c_int64(total), C.c_int32(devices), _ptr(b), _ptr(e)))
+    return list(zip(b.tolist(), e.tolist()))
+
+
+@dataclass
+class BlockCsr:
+    """Global 3x3-block matrix, ascending columns; values (nnzb, 9) row-major."""
+
+    rows: int
+    row_ptr: np.ndarray
+    cols: np.ndarray
+    vals: np.ndarray
+    rhs: np.ndarray | None = None
+
+
+@dataclass
+class PcgReport:
+    """PcgReport (solver.hpp:23-29)."""
+
+    iterations: int = 0
+    rel_residual: float = 0.0
+    converged: bool = False
+    residual_history: np.ndarray = field(default_factory=lambda: np.zeros(0))
+    precond_norm_history: np.ndarray = field(default_factory=lambda: np.zeros(0))
+
+
+@dataclass
+class HashGrid:
+    """HashGrid + WorkloadTable (collision.hpp:59-70) as flat arrays."""
+
+    cell_size: float
+    cell_keys: np.ndarray
+    cell_offsets: np.ndarray
+    cell_tris: np.ndarray
+    prefix: np.ndarray
+    tri_boxes: np.ndarray
+
+    @property
+    def total(self) -> int:
+        return int(self.prefix[-1]) if len(self.prefix) else 0
+
+
+class Engine:
+    """A GPU context with ``devices`` logical row partitions (weft::Engine)."""
+
+    def __init__(self, devices: int = 1, cuda_device: int = 0):
+        self._ctx = C.c_void_p()
+        opts = Options(cuda_device, devices, 0, devices)
+        _check(LIB.weft_gpu_create(C.byref(opts), C.byref(self._ctx)))
+        self.devices = devices
+
+    def close(self):
+        if self._ctx:
+            _check(LIB.weft_gpu_destroy(self._ctx))
+            self._ctx = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    # -- sparse -------------------------------------------------------------
+    def set_matrix(self, m: BlockCsr):
+        _check(LIB.weft_gpu_set_matrix(self._ctx, C.c_int32(m.rows), _ptr(np.ascontiguousarray(m.row_ptr, np.int64)),
+                                       _ptr(np.ascontiguousarray(m.cols, np.int32)), _ptr(_f64(m.vals))))
+
+    def spmv_pipelined(self, m: BlockCsr | None, x) -> np.ndarray:
+        if m is not None:
+            self.set_matrix(m)
+        info = self.matrix_info()
+        x = _f64(x)
+        if len(x) != 3 * info.block_rows:
+            raise DimensionError("spmv_pipelined: dim(x) != rows")
+        y = np.zeros(3 * info.block_rows)
+        _check(LIB.weft_gpu_spmv(self._ctx, _ptr(x), _ptr(y)))
+        return y
+
+    def matrix_info(self) -> MatrixInfo:
+        info = MatrixInfo()
+        _check(LIB.weft_gpu_matrix_info(self._ctx, C.byref(info)))
+        return info
+
+    def download_matrix(self) -> BlockCsr:
+        info = self.matrix_info()
+        rp = np.zeros(info.block_rows + 1, np.int64)
+        cols = np.zeros(max(info.nnzb, 1), np.int32)
+        vals = np.zeros(max(info.nnzb, 1) * 9)
+        _check(LIB.weft_gpu_download_matrix(self._ctx, _ptr(rp), _ptr(cols), _ptr(vals)))
+        return BlockCsr(info.block_rows, rp, cols[: info.nnzb], vals[: 9 * info.nnzb].reshape(-1, 9))
+
+    def download_rhs(self) -> np.ndarray:
+        info = self.matrix_info()
+        rhs = np.zeros(3 * info.block_rows)
+        _check(LIB.weft_gpu_download_rhs(self._ctx, _ptr(rhs)))
+        return rhs
+
+    def pcg_solve(self, m: BlockCsr | None, b, config: PcgConfig | None = None):
+        """pcg_solve; ``m=None`` uses the context's current (assembled)
+        matrix, ``b=None`` its assembled rhs. Returns (x, PcgReport)."""
+        if m is not None:
+            self.set_matrix(m)
+        config = config or PcgConfig()
+        info = self.matrix_info()
+        n = 3 * info.block_rows
+        x = np.zeros(n)
+        hist = np.zeros(max(config.max_iterations, 1))
+        phist = np.zeros(max(config.max_iterations, 1))
+        rep = _PcgReport(0, 0, 0.0, hist.ctypes.data_as(C.POINTER(C.c_double)),
+                         phist.ctypes.data_as(C.POINTER(C.c_double)))
+        bb = None if b is None else _f64(b)
+        _check(LIB.weft_gpu_pcg(self._ctx, _ptr(bb), _ptr(x), C.byref(config), C.byref(rep)))
+        return x, PcgReport(rep.iterations, rep.rel_residual, bool(rep.converged), hist[: rep.iterations].copy(),
+                            phist[: rep.iterations].copy())
+
+    # -- assembly -----------------------------------------------------------
+    def set_vertices(self, mass, pinned):
+        mass = _f64(mass)
+        pinned = np.ascontiguousarray(pinned, np.uint8)
+        _check(LIB.weft_gpu_set_vertices(self._ctx, C.c_int32(len(mass)), _ptr(mass), _ptr(pinned)))
+
+    def set_elements(self, elements):
+        e = np.ascontiguousarray(elements, ELEMENT_DTYPE)
+        _check(LIB.weft_gpu_set_elements(self._ctx, C.c_int64(len(e)), _ptr(e)))
+
+    def set_contacts(self, contacts):
+        e = np.ascontiguousarray(contacts if contacts is not None else np.zeros(0, ELEMENT_DTYPE), ELEMENT_DTYPE)
+        _check(LIB.weft_gpu_set_contacts(self._ctx, C.c_int64(len(e)), _ptr(e)))
+
+    def fill_matrix(self, x_current, x_advanced, velocity, dt: float, mode: int = JAC_SPD):
+        """fill_matrix over the context's static + contact elements; the
+        system stays resident (download_matrix / download_rhs to read)."""
+        _check(LIB.weft_gpu_fill_matrix(self._ctx, _ptr(_f64(x_current)), _ptr(_f64(x_advanced)),
+                                        _ptr(_f64(velocity)), C.c_double(dt), C.c_int32(mode)))
+
+    def step_system(self, x, v, dt: float, mode: int = JAC_SPD):
+        _check(LIB.weft_gpu_step_system(self._ctx, _ptr(_f64(x)), _ptr(_f64(v)), C.c_double(dt), C.c_int32(mode)))
+
+    # -- broad phase --------------------------------------------------------
+    def set_soup(self, vertex_count: int, tris):
+        t = np.ascontiguousarray(tris, np.int32).reshape(-1)
+        _check(LIB.weft_gpu_set_soup(self._ctx, C.c_int32(vertex_count), C.c_int32(len(t) // 3), _ptr(t)))
+
+    def build_grid(self, x_begin, x_end=None, mode: int = DISCRETE, thickness: float = 0.005,
+                   cell_scale: float = 1.5):
+        xb = _f64(x_begin)
+        xe = None if x_end is None else _f64(x_end)
+        _check(LIB.weft_gpu_build_grid(self._ctx, _ptr(xb), _ptr(xe), C.c_int32(mode), C.c_double(thickness),
+                                       C.c_double(cell_scale)))
+
+    def grid_info(self) -> GridInfo:
+        info = GridInfo()
+        _check(LIB.weft_gpu_grid_info(self._ctx, C.byref(info)))
+        return info
+
+    def download_grid(self, tri_count: int) -> HashGrid:
+        info = self.grid_info()
+        keys = np.zeros(info.cells, np.uint64)
+        off = np.zeros(info.cells + 1, np.int64)
+        tris = np.zeros(max(info.entries, 1), np.int32)
+        prefix = np.zeros(info.cells + 1, np.int64)
+        boxes = np.zeros(6 * max(tri_count, 1), np.int64)
+        _check(LIB.weft_gpu_download_grid(self._ctx, _ptr(keys), _ptr(off), _ptr(tris), _ptr(prefix), _ptr(boxes)))
+        return HashGrid(info.cell_size, keys, off, tris[: info.entries], prefix, boxes[: 6 * tri_count].reshape(-1, 6))
+
+    def candidates(self, begin: int | None = None, end: int | None = None) -> np.ndarray:
+        info = self.grid_info()
+        begin = 0 if begin is None else begin
+        end = info.total if end is None else end
+        n = C.c_int64()
+        _check(LIB.weft_gpu_candidates(self._ctx, C.c_int64(begin), C.c_int64(end), C.byref(n), None))
+        pairs = np.zeros(2 * max(n.value, 1), np.int32)
+        _check(LIB.weft_gpu_candidates(self._ctx, C.c_int64(begin), C.c_int64(end), C.byref(n), _ptr(pairs)))
+        return pairs[: 2 * n.value].reshape(-1, 2)
+
+    # -- device-resident step -----------------------------------------------
+    def sim_set_state(self, x, v):
+        _check(LIB.weft_gpu_sim_set_state(self._ctx, _ptr(_f64(x) if isinstance(x, np.ndarray) else x),
+                                          _ptr(_f64(v) if isinstance(v, np.ndarray) else v)))
+
+    def sim_step(self, params: SimParams) -> StepReport:
+        rep = StepReport()
+        _check(LIB.weft_gpu_sim_step(self._ctx, C.byref(params), C.byref(rep)))
+        return rep
+
+    def sim_get_state(self, x=None, v=None):
+        _check(LIB.weft_gpu_sim_get_state(self._ctx, _ptr(x), _ptr(v)))
