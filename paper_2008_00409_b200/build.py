@@ -18,17 +18,17 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-fmad=false", "-std=c++17",
-    "-Xcompiler", "-fPIC,-O2", "--expt-relaxed-constexpr",
+    "-Xcompiler", "-fPIC,-O2,-ffp-contract=off", "--expt-relaxed-constexpr",
 ]
 
-SOURCES = ["capi.cu", "sparse.cu", "assembly.cu", "broadphase.cu", "sim.cu"]
+SOURCES = ["capi.cu", "sparse.cu", "assembly.cu", "broadphase.cu", "sim.cu", "mesh.cpp"]
 
 
 def _compile(src: str, verbose: bool) -> str:
-    obj = os.path.join(OBJ, src.replace(".cu", ".o"))
+    obj = os.path.join(OBJ, os.path.splitext(src)[0] + ".o")
     path = os.path.join(CSRC, src)
     deps = [path] + [os.path.join(CSRC, h) for h in os.listdir(CSRC) if h.endswith(".cuh")]
-    deps.append(os.path.join(os.path.dirname(PKG), "include", "weft_gpu.h"))
+    deps += [os.path.join(os.path.dirname(PKG), "include", h) for h in ("weft_gpu.h", "weft_mesh.h")]
     if os.path.exists(obj) and all(os.path.getmtime(obj) >= os.path.getmtime(d) for d in deps):
         return obj
     cmd = [NVCC, *NVCC_FLAGS, "-c", path, "-o", obj]

@@ -1,0 +1,693 @@
+// assembly.cu — per-step dynamic assembly of A = M - (dt^2 + c dt) J (+ dt D)
+// and rhs = dt f(x + dt v) into the sliced-ELL matrix.
+//
+// Reference: distribute_elements (proj/src/assembly.cpp:5-54) and the
+// five-step fill_matrix (proj/include/weft/assembly.hpp:74-220).
+//
+// Design (B200):
+//  * The static element list (triangles, hinges, vertices; physics.cpp:5-63)
+//    fixes a static row incidence table (row -> (element, stencil slot) in
+//    ascending element order) and a static sparsity pattern; both are built
+//    once on the device by radix sort (CUB) when the elements are set.
+//  * Every step, contact elements (appended after the static list, as in
+//    step_system, physics.hpp:50-52) get their own incidence table and
+//    (row, col) pattern, merged row by row with the static pattern into a
+//    fresh sliced-ELL layout whose slots follow the SpMV accumulation order.
+//  * Values: one thread per block row walks its incidences in ascending
+//    element order, evaluates the element's row-a force and Jacobian blocks
+//    (elements.cuh) and accumulates into per-thread shared-memory slot
+//    accumulators — no atomics, the reference's per-slot summation order
+//    (mass first, then ascending element instances) is kept exactly, so the
+//    matrix is bitwise equal to the CPU reference and independent of the
+//    partition count (test_assembly.cpp:263-280).
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "ctx.cuh"
+#include "elements.cuh"
+
+namespace weft_gpu {
+
+void* scratch(Ctx& c, size_t bytes) {
+  c.scratch.resize(bytes + 256);
+  return c.scratch.data();
+}
+
+// ---------------------------------------------------------------------------
+// vertices / elements upload
+// ---------------------------------------------------------------------------
+void set_vertices(Ctx& c, int p, const double* mass, const uint8_t* pinned) {
+  if (p < 0) throw Error(WEFT_ERR_DIMENSION, "negative vertex count");
+  if (p >= (1 << 28)) throw Error(WEFT_ERR_DIMENSION, "more than 2^28 vertices");
+  if (p < c.nparts) throw Error(WEFT_ERR_DIMENSION, "fewer vertices than partitions");
+  c.p = p;
+  c.pm = PartMap::make(p, c.nparts);
+  c.mass.upload(mass, static_cast<size_t>(p), c.stream);
+  c.pinned.upload(pinned, static_cast<size_t>(p), c.stream);
+  c.n_static = c.n_contacts = 0;
+  c.static_pay = 0;
+  c.inc_ptr.resize(0);
+  c.spat_ptr.resize(0);
+  c.has_matrix = false;
+  c.has_rhs = false;
+  WG_CUDA(cudaStreamSynchronize(c.stream));
+}
+
+static int payload_size(int kind) {
+  switch (kind) {
+    case WEFT_STRETCH:
+      return 10;
+    case WEFT_BEND:
+    case WEFT_SPRING:
+      return 2;
+    case WEFT_EXTERNAL:
+      return 4;
+    case WEFT_CONTACT:
+      return 16;
+    default:
+      return -1;
+  }
+}
+
+// Converts flat records into the device SoA (stencil, info, damping,
+// payload pool) starting at element index `first` / payload offset `pay0`.
+static void upload_elements(Ctx& c, int64_t count, const weft_element* elems, int64_t first, int64_t pay0,
+                            int64_t* pay_used) {
+  std::vector<weft_element> host;
+  const weft_element* h = elems;
+  cudaPointerAttributes attr{};
+  if (cudaPointerGetAttributes(&attr, elems) == cudaSuccess && attr.type == cudaMemoryTypeDevice) {
+    host.resize(static_cast<size_t>(count));
+    WG_CUDA(cudaMemcpy(host.data(), elems, sizeof(weft_element) * count, cudaMemcpyDeviceToHost));
+    h = host.data();
+  }
+  cudaGetLastError();
+  std::vector<int4> st(static_cast<size_t>(count));
+  std::vector<int2> info(static_cast<size_t>(count));
+  std::vector<double> damp(static_cast<size_t>(count));
+  std::vector<double> pay;
+  pay.reserve(static_cast<size_t>(count) * 4);
+  for (int64_t i = 0; i < count; ++i) {
+    const weft_element& e = h[i];
+    const int ps = payload_size(e.kind);
+    if (ps < 0) throw Error(WEFT_ERR_INVALID, "element " + std::to_string(first + i) + ": unknown kind");
+    if (e.stencil_size < 1 || e.stencil_size > 4)
+      throw Error(WEFT_ERR_INVALID, "element " + std::to_string(first + i) + ": bad stencil size");
+    int s[4] = {-1, -1, -1, -1};
+    for (int a = 0; a < e.stencil_size; ++a) {
+      const int v = e.stencil[a];
+      if (v < 0 || v >= c.p)  // distribute_elements (assembly.cpp:18-22)
+        throw Error(WEFT_ERR_DIMENSION, "element " + std::to_string(first + i) + ": stencil vertex " +
+                                            std::to_string(v) + " outside all partitions");
+      s[a] = v;
+    }
+    st[static_cast<size_t>(i)] = make_int4(s[0], s[1], s[2], s[3]);
+    const int64_t off = pay0 + static_cast<int64_t>(pay.size());
+    if (off > INT32_MAX) throw Error(WEFT_ERR_DIMENSION, "element payload exceeds 2^31 doubles");
+    info[static_cast<size_t>(i)] = make_int2(e.kind | (e.stencil_size << 8), static_cast<int>(off));
+    damp[static_cast<size_t>(i)] = e.damping;
+    pay.insert(pay.end(), e.data, e.data + ps);
+  }
+  const size_t n_total = static_cast<size_t>(first + count);
+  const size_t pay_total = static_cast<size_t>(pay0) + pay.size();
+  // grow while preserving the static prefix
+  auto grow = [&](auto& buf, size_t need, size_t keep) {
+    using T = std::remove_reference_t<decltype(*buf.data())>;
+    if (need > buf.cap) {
+      DBuf<T> tmp;
+      tmp.resize(need);
+      if (keep) WG_CUDA(cudaMemcpyAsync(tmp.data(), buf.data(), keep * sizeof(T), cudaMemcpyDeviceToDevice, c.stream));
+      std::swap(tmp.ptr, buf.ptr);
+      std::swap(tmp.cap, buf.cap);
+    }
+    buf.n = need;
+  };
+  grow(c.est, n_total, static_cast<size_t>(first));
+  grow(c.einfo, n_total, static_cast<size_t>(first));
+  grow(c.edamp, n_total, static_cast<size_t>(first));
+  grow(c.epay, pay_total, static_cast<size_t>(pay0));
+  if (count) {
+    WG_CUDA(cudaMemcpyAsync(c.est.data() + first, st.data(), sizeof(int4) * count, cudaMemcpyHostToDevice, c.stream));
+    WG_CUDA(cudaMemcpyAsync(c.einfo.data() + first, info.data(), sizeof(int2) * count, cudaMemcpyHostToDevice, c.stream));
+    WG_CUDA(cudaMemcpyAsync(c.edamp.data() + first, damp.data(), sizeof(double) * count, cudaMemcpyHostToDevice, c.stream));
+  }
+  if (!pay.empty())
+    WG_CUDA(cudaMemcpyAsync(c.epay.data() + pay0, pay.data(), sizeof(double) * pay.size(), cudaMemcpyHostToDevice,
+                            c.stream));
+  WG_CUDA(cudaStreamSynchronize(c.stream));  // host staging vectors die here
+  *pay_used = static_cast<int64_t>(pay.size());
+}
+
+// ---------------------------------------------------------------------------
+// incidence tables: rows -> (element*4 + a), ascending element
+// ---------------------------------------------------------------------------
+__global__ void k_inc_emit(int64_t first, int64_t count, const int4* __restrict__ est, const int2* __restrict__ einfo,
+                           const uint8_t* __restrict__ pinned, uint32_t* __restrict__ keys, int32_t* __restrict__ vals,
+                           int* __restrict__ cnt, int64_t code_base) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  const int4 s = est[first + i];
+  const int ss = (einfo[first + i].x >> 8) & 0xff;
+  const int sv[4] = {s.x, s.y, s.z, s.w};
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    uint32_t key = 0xffffffffu;
+    if (a < ss && !pinned[sv[a]]) {
+      key = static_cast<uint32_t>(sv[a]);
+      atomicAdd(cnt + sv[a], 1);
+    }
+    keys[4 * i + a] = key;
+    vals[4 * i + a] = static_cast<int32_t>((code_base + i) * 4 + a);
+  }
+}
+
+static int bits_for(int64_t v) {
+  int b = 1;
+  while ((int64_t(1) << b) <= v) ++b;
+  return b;
+}
+
+// Builds (ptr, list) for elements [first, first+count); codes are
+// (code_base + i) * 4 + a.
+static void build_incidence(Ctx& c, int64_t first, int64_t count, int64_t code_base, DBuf<int64_t>& ptr,
+                            DBuf<int32_t>& list) {
+  const int p = c.p;
+  cudaStream_t s = c.stream;
+  DBuf<int> cnt;
+  cnt.resize(static_cast<size_t>(p) + 1);
+  cnt.zero(s);
+  ptr.resize(static_cast<size_t>(p) + 1);
+  const int64_t m = 4 * count;
+  DBuf<uint32_t> k1, k2;
+  DBuf<int32_t> v1;
+  k1.resize(static_cast<size_t>(m) + 1);
+  k2.resize(static_cast<size_t>(m) + 1);
+  v1.resize(static_cast<size_t>(m) + 1);
+  list.resize(static_cast<size_t>(m) + 1);
+  if (count) {
+    if ((code_base + count) * 4 > INT32_MAX) throw Error(WEFT_ERR_DIMENSION, "too many elements (> 2^29)");
+    k_inc_emit<<<div_up(count, 256), 256, 0, s>>>(first, count, c.est.data(), c.einfo.data(), c.pinned.data(),
+                                                  k1.data(), v1.data(), cnt.data(), code_base);
+    WG_CUDA(cudaGetLastError());
+    size_t tmp = 0;
+    const int end_bit = 32;
+    cub::DeviceRadixSort::SortPairs(nullptr, tmp, k1.data(), k2.data(), v1.data(), list.data(), (int)m, 0, end_bit, s);
+    void* t = scratch(c, tmp);
+    WG_CUDA(cub::DeviceRadixSort::SortPairs(t, tmp, k1.data(), k2.data(), v1.data(), list.data(), (int)m, 0,
+                                            end_bit, s));
+  }
+  // exclusive scan of counts -> ptr (int64)
+  size_t tmp = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt.data(), ptr.data(), p + 1, s);
+  void* t = scratch(c, tmp);
+  WG_CUDA(cub::DeviceScan::ExclusiveSum(t, tmp, cnt.data(), ptr.data(), p + 1, s));
+  WG_CUDA(cudaStreamSynchronize(s));
+}
+
+// ---------------------------------------------------------------------------
+// sparsity: sorted unique (row << 32 | col) keys -> CSR
+// ---------------------------------------------------------------------------
+__global__ void k_pair_count(int64_t first, int64_t count, const int4* __restrict__ est,
+                             const int2* __restrict__ einfo, const uint8_t* __restrict__ pinned,
+                             int64_t* __restrict__ out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  const int4 s = est[first + i];
+  const int ss = (einfo[first + i].x >> 8) & 0xff;
+  const int sv[4] = {s.x, s.y, s.z, s.w};
+  int live = 0;
+#pragma unroll
+  for (int a = 0; a < 4; ++a) live += (a < ss && !pinned[sv[a]]) ? 1 : 0;
+  out[i] = live * live;
+}
+
+__global__ void k_pair_emit(int64_t first, int64_t count, const int4* __restrict__ est,
+                            const int2* __restrict__ einfo, const uint8_t* __restrict__ pinned,
+                            const int64_t* __restrict__ off, uint64_t* __restrict__ keys) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  const int4 s = est[first + i];
+  const int ss = (einfo[first + i].x >> 8) & 0xff;
+  const int sv[4] = {s.x, s.y, s.z, s.w};
+  int64_t o = off[i];
+  for (int a = 0; a < ss; ++a) {
+    if (pinned[sv[a]]) continue;
+    for (int b = 0; b < ss; ++b) {
+      if (pinned[sv[b]]) continue;
+      keys[o++] = (static_cast<uint64_t>(sv[a]) << 32) | static_cast<uint32_t>(sv[b]);
+    }
+  }
+}
+
+__global__ void k_diag_keys(int p, uint64_t* __restrict__ keys) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < p) keys[r] = (static_cast<uint64_t>(r) << 32) | static_cast<uint32_t>(r);
+}
+
+__global__ void k_key_rows(int64_t n, const uint64_t* __restrict__ keys, int* __restrict__ cnt,
+                           int32_t* __restrict__ cols) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint64_t k = keys[i];
+  atomicAdd(cnt + (k >> 32), 1);
+  cols[i] = static_cast<int32_t>(k & 0xffffffffu);
+}
+
+// (row, col) pattern of elements [first, first+count) (+ the diagonal of
+// every row when with_diag), steps (1)-(3) of fill_matrix
+// (assembly.hpp:93-134), as CSR with ascending unique columns.
+static void build_pattern(Ctx& c, int64_t first, int64_t count, bool with_diag, DBuf<int64_t>& ptr,
+                          DBuf<int32_t>& cols) {
+  const int p = c.p;
+  cudaStream_t s = c.stream;
+  DBuf<int64_t> pc;
+  pc.resize(static_cast<size_t>(count) + 1);
+  int64_t npairs = 0;
+  if (count) {
+    k_pair_count<<<div_up(count, 256), 256, 0, s>>>(first, count, c.est.data(), c.einfo.data(), c.pinned.data(),
+                                                    pc.data());
+    size_t tmp = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tmp, pc.data(), pc.data(), count + 1, s);
+    void* t = scratch(c, tmp);
+    // last element of an exclusive scan over count+1 entries = total
+    WG_CUDA(cudaMemsetAsync(pc.data() + count, 0, sizeof(int64_t), s));
+    WG_CUDA(cub::DeviceScan::ExclusiveSum(t, tmp, pc.data(), pc.data(), count + 1, s));
+    WG_CUDA(cudaMemcpyAsync(&npairs, pc.data() + count, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    WG_CUDA(cudaStreamSynchronize(s));
+  }
+  const int64_t nk = npairs + (with_diag ? p : 0);
+  DBuf<uint64_t> k1, k2;
+  k1.resize(static_cast<size_t>(nk) + 1);
+  k2.resize(static_cast<size_t>(nk) + 1);
+  if (count)
+    k_pair_emit<<<div_up(count, 256), 256, 0, s>>>(first, count, c.est.data(), c.einfo.data(), c.pinned.data(),
+                                                   pc.data(), k1.data());
+  if (with_diag && p) k_diag_keys<<<div_up(p, 256), 256, 0, s>>>(p, k1.data() + npairs);
+  WG_CUDA(cudaGetLastError());
+  const int end_bit = 32 + bits_for(p);
+  DBuf<int64_t> nsel;
+  nsel.resize(1);
+  int64_t nu = 0;
+  if (nk) {
+    size_t tmp = 0;
+    cub::DeviceRadixSort::SortKeys(nullptr, tmp, k1.data(), k2.data(), nk, 0, end_bit, s);
+    size_t tmp2 = 0;
+    cub::DeviceSelect::Unique(nullptr, tmp2, k2.data(), k1.data(), nsel.data(), nk, s);
+    void* t = scratch(c, std::max(tmp, tmp2));
+    WG_CUDA(cub::DeviceRadixSort::SortKeys(t, tmp, k1.data(), k2.data(), nk, 0, end_bit, s));
+    WG_CUDA(cub::DeviceSelect::Unique(t, tmp2, k2.data(), k1.data(), nsel.data(), nk, s));
+    WG_CUDA(cudaMemcpyAsync(&nu, nsel.data(), sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    WG_CUDA(cudaStreamSynchronize(s));
+  }
+  DBuf<int> cnt;
+  cnt.resize(static_cast<size_t>(p) + 1);
+  cnt.zero(s);
+  cols.resize(static_cast<size_t>(nu) + 1);
+  ptr.resize(static_cast<size_t>(p) + 1);
+  if (nu) k_key_rows<<<div_up(nu, 256), 256, 0, s>>>(nu, k1.data(), cnt.data(), cols.data());
+  size_t tmp = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt.data(), ptr.data(), p + 1, s);
+  void* t = scratch(c, tmp);
+  WG_CUDA(cub::DeviceScan::ExclusiveSum(t, tmp, cnt.data(), ptr.data(), p + 1, s));
+  WG_CUDA(cudaStreamSynchronize(s));
+}
+
+void set_elements(Ctx& c, int64_t count, const weft_element* elems) {
+  if (c.p == 0 && count) throw Error(WEFT_ERR_INVALID, "set_elements: set_vertices first");
+  int64_t used = 0;
+  upload_elements(c, count, elems, 0, 0, &used);
+  c.n_static = count;
+  c.static_pay = used;
+  c.n_contacts = 0;
+  build_incidence(c, 0, count, 0, c.inc_ptr, c.inc);
+  build_pattern(c, 0, count, true, c.spat_ptr, c.spat);
+  c.cinc_ptr.resize(static_cast<size_t>(c.p) + 1);
+  c.cinc_ptr.zero(c.stream);
+  c.have_pattern_for_contacts = false;
+  c.has_matrix = false;
+  WG_CUDA(cudaStreamSynchronize(c.stream));
+}
+
+void set_contacts(Ctx& c, int64_t count, const weft_element* elems) {
+  if (c.p == 0) throw Error(WEFT_ERR_INVALID, "set_contacts: set_vertices first");
+  int64_t used = 0;
+  upload_elements(c, count, elems, c.n_static, c.static_pay, &used);
+  c.n_contacts = count;
+  // contact incidences: codes are the contact index (element n_static + i).
+  build_incidence(c, c.n_static, count, 0, c.cinc_ptr, c.cinc);
+  c.have_pattern_for_contacts = false;
+}
+
+// ---------------------------------------------------------------------------
+// merged pattern -> sliced-ELL layout in accumulation-group order
+// ---------------------------------------------------------------------------
+struct MergeIn {
+  const int64_t* sptr;
+  const int32_t* scol;
+  const int64_t* cptr;  // may be null (no contacts)
+  const int32_t* ccol;
+};
+
+// Walks the union of the static and contact columns of row r in ascending
+// order (both inputs sorted, each unique).
+template <class F>
+__device__ __forceinline__ void for_union(const MergeIn& m, int r, F&& f) {
+  int64_t i = m.sptr[r], ie = m.sptr[r + 1];
+  int64_t j = 0, je = 0;
+  if (m.cptr) {
+    j = m.cptr[r];
+    je = m.cptr[r + 1];
+  }
+  while (i < ie || j < je) {
+    int col;
+    if (j >= je || (i < ie && m.scol[i] <= m.ccol[j])) {
+      col = m.scol[i];
+      if (j < je && m.ccol[j] == col) ++j;
+      ++i;
+    } else {
+      col = m.ccol[j];
+      ++j;
+    }
+    f(col);
+  }
+}
+
+__global__ void k_merge_len(int p, MergeIn m, int32_t* __restrict__ len) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= p) return;
+  int n = 0;
+  for_union(m, r, [&](int) { ++n; });
+  len[r] = n;
+}
+
+__global__ void k_slice_width(int p, int nslices, const int32_t* __restrict__ len, int64_t* __restrict__ w) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= nslices) return;
+  int m = 0;
+  for (int r = s * kSlice; r < min(p, (s + 1) * kSlice); ++r) m = max(m, len[r]);
+  w[s] = static_cast<int64_t>(m) * kSlice;
+}
+
+// Writes the row's columns grouped by accumulation order: own partition
+// first, then the work-queue order (sparse.hpp:89-95); ascending inside a
+// group. Padding slots get -1.
+__global__ void k_merge_fill(int p, MergeIn m, PartMap pm, GroupOrder go, const int64_t* __restrict__ soff,
+                             const int32_t* __restrict__ len, int32_t* __restrict__ cols) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= p) return;
+  const int s = r >> 5;
+  const int64_t base = soff[s] + (r & 31);
+  const int width = static_cast<int>((soff[s + 1] - soff[s]) / kSlice);
+  const int d = pm.owner(r);
+  int k = 0;
+  for (int g = 0; g < go.n; ++g) {
+    for_union(m, r, [&](int col) {
+      const int o = pm.owner(col);
+      if (go.qpos[d][o] == g) {
+        cols[base + (int64_t)k * kSlice] = col | (g << kGroupShift);
+        ++k;
+      }
+    });
+  }
+  for (; k < width; ++k) cols[base + (int64_t)k * kSlice] = -1;
+}
+
+// Pattern of the contact elements (rows/cols among non-pinned vertices).
+static void build_layout(Ctx& c) {
+  cudaStream_t s = c.stream;
+  const int p = c.p;
+  DBuf<int64_t> cptr;
+  DBuf<int32_t> ccol;
+  MergeIn m{c.spat_ptr.data(), c.spat.data(), nullptr, nullptr};
+  if (c.n_contacts) {
+    build_pattern(c, c.n_static, c.n_contacts, false, cptr, ccol);
+    m.cptr = cptr.data();
+    m.ccol = ccol.data();
+  }
+  SellMatrix& A = c.A;
+  A.rows = p;
+  A.nslices = div_up(p, kSlice);
+  A.rowlen.resize(static_cast<size_t>(p) + 1);
+  A.slice_off.resize(static_cast<size_t>(A.nslices) + 1);
+  if (p) {
+    k_merge_len<<<div_up(p, 256), 256, 0, s>>>(p, m, A.rowlen.data());
+    k_slice_width<<<div_up(A.nslices, 256), 256, 0, s>>>(p, A.nslices, A.rowlen.data(), A.slice_off.data());
+  }
+  WG_CUDA(cudaMemsetAsync(A.slice_off.data() + A.nslices, 0, sizeof(int64_t), s));
+  size_t tmp = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tmp, A.slice_off.data(), A.slice_off.data(), A.nslices + 1, s);
+  void* t = scratch(c, tmp);
+  WG_CUDA(cub::DeviceScan::ExclusiveSum(t, tmp, A.slice_off.data(), A.slice_off.data(), A.nslices + 1, s));
+  // totals: slots, nnzb, max row length
+  int64_t total = 0;
+  WG_CUDA(cudaMemcpyAsync(&total, A.slice_off.data() + A.nslices, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  DBuf<int64_t> red;
+  red.resize(2);
+  int* lenp = A.rowlen.data();
+  size_t t1 = 0, t2 = 0;
+  cub::DeviceReduce::Sum(nullptr, t1, lenp, red.data(), p, s);
+  cub::DeviceReduce::Max(nullptr, t2, lenp, reinterpret_cast<int*>(red.data() + 1), p, s);
+  t = scratch(c, std::max(t1, t2));
+  int64_t hr[2] = {0, 0};
+  if (p) {
+    WG_CUDA(cub::DeviceReduce::Sum(t, t1, lenp, red.data(), p, s));
+    WG_CUDA(cudaMemsetAsync(red.data() + 1, 0, sizeof(int64_t), s));
+    WG_CUDA(cub::DeviceReduce::Max(t, t2, lenp, reinterpret_cast<int*>(red.data() + 1), p, s));
+    WG_CUDA(cudaMemcpyAsync(hr, red.data(), sizeof(hr), cudaMemcpyDeviceToHost, s));
+  }
+  WG_CUDA(cudaStreamSynchronize(s));
+  A.total = total;
+  A.nnzb = hr[0];
+  A.max_len = static_cast<int>(hr[1] & 0xffffffff);
+  A.cols.resize(static_cast<size_t>(total) + 1);
+  A.vals.resize(9 * static_cast<size_t>(total) + 9);
+  if (p)
+    k_merge_fill<<<div_up(p, 256), 256, 0, s>>>(p, m, c.pm, c.go, A.slice_off.data(), A.rowlen.data(), A.cols.data());
+  WG_CUDA(cudaGetLastError());
+  WG_CUDA(cudaStreamSynchronize(s));  // cptr/ccol die here
+}
+
+// ---------------------------------------------------------------------------
+// value fill
+// ---------------------------------------------------------------------------
+struct FillArgs {
+  int p;
+  int64_t n_static;
+  double dt;
+  bool exact;
+  int wcap;  // slots held in shared memory per thread
+  const int64_t* __restrict__ slice_off;
+  const int32_t* __restrict__ rowlen;
+  const int32_t* __restrict__ cols;
+  double* __restrict__ vals;
+  int64_t total;
+  double* __restrict__ rhs;
+  const double* __restrict__ mass;
+  const uint8_t* __restrict__ pinned;
+  const int64_t* __restrict__ inc_ptr;
+  const int32_t* __restrict__ inc;
+  const int64_t* __restrict__ cinc_ptr;
+  const int32_t* __restrict__ cinc;
+  const int4* __restrict__ est;
+  const int2* __restrict__ einfo;
+  const double* __restrict__ edamp;
+  const double* __restrict__ epay;
+  const double* __restrict__ xc;
+  const double* __restrict__ xa;
+  const double* __restrict__ vel;
+  int* __restrict__ bad_mass;  // min vertex id with non-positive mass
+};
+
+// Accumulator access: shared (Wide = false) or the output planes directly.
+template <bool Wide>
+struct Acc {
+  double* sm;   // [wcap][9][blockDim] for this block
+  int tid, bs;
+  double* gv;   // output planes (Wide)
+  int64_t total, base;
+  __device__ __forceinline__ double& at(int slot, int q) {
+    if (Wide) return gv[q * total + base + (int64_t)slot * kSlice];
+    return sm[(slot * 9 + q) * bs + tid];
+  }
+};
+
+template <bool Wide>
+__global__ void __launch_bounds__(64) k_fill(FillArgs f) {
+  extern __shared__ double smem[];
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  const int len = r < f.p ? f.rowlen[r] : 0;
+  const bool mine = r < f.p && (Wide ? len > f.wcap : len <= f.wcap);
+  if (!mine) return;
+  const int64_t base = f.slice_off[r >> 5] + (r & 31);
+  int32_t* colbuf = reinterpret_cast<int32_t*>(smem + (size_t)f.wcap * 9 * blockDim.x);
+  Acc<Wide> acc{smem, (int)threadIdx.x, (int)blockDim.x, f.vals, f.total, base};
+  auto col_of = [&](int k) -> int {
+    if (!Wide) return colbuf[k * blockDim.x + threadIdx.x];
+    return f.cols[base + (int64_t)k * kSlice] & kColMask;
+  };
+  for (int k = 0; k < len; ++k) {
+    if (!Wide) colbuf[k * blockDim.x + threadIdx.x] = f.cols[base + (int64_t)k * kSlice] & kColMask;
+#pragma unroll
+    for (int q = 0; q < 9; ++q) acc.at(k, q) = 0.0;
+  }
+  auto find = [&](int col) -> int {
+    for (int k = 0; k < len; ++k)
+      if (col_of(k) == col) return k;
+    return -1;
+  };
+  // (5) mass diagonal first (assembly.hpp:155-166)
+  const bool pin = f.pinned[r] != 0;
+  const double m = f.mass[r];
+  if (!pin && m <= 0.0) atomicMin(f.bad_mass, r);
+  {
+    const int ds = find(r);
+    const double mv = pin ? 1.0 : m;
+    acc.at(ds, 0) = acc.at(ds, 0) + mv;
+    acc.at(ds, 4) = acc.at(ds, 4) + mv;
+    acc.at(ds, 8) = acc.at(ds, 8) + mv;
+  }
+  double r0 = 0.0, r1 = 0.0, r2 = 0.0;
+  const double dt = f.dt;
+  // then every element instance of this row in ascending element order
+  for (int pass = 0; pass < 2; ++pass) {
+    const int64_t* ip = pass == 0 ? f.inc_ptr : f.cinc_ptr;
+    const int32_t* il = pass == 0 ? f.inc : f.cinc;
+    const int64_t i0 = ip[r], i1 = ip[r + 1];
+    for (int64_t ii = i0; ii < i1; ++ii) {
+      const int code = il[ii];
+      const int64_t e = (pass == 0 ? 0 : f.n_static) + (code >> 2);
+      const int a = code & 3;
+      const int4 s4 = f.est[e];
+      const int2 info = f.einfo[e];
+      const int kind = info.x & 0xff, ss = (info.x >> 8) & 0xff;
+      const double damping = f.edamp[e];
+      const int st[4] = {s4.x, s4.y, s4.z, s4.w};
+      RowEval ev;
+      eval_row(kind, ss, st, f.epay + info.y, a, f.xc, f.xa, f.vel, f.exact, ev);
+      // rhs (assembly.hpp:185-197)
+      double fx = ev.f[0], fy = ev.f[1], fz = ev.f[2];
+      if (damping > 0.0) {
+        for (int b = 0; b < ss; ++b) {
+          const V3 vb = ld3(f.vel, st[b]);
+          const double* M = ev.J[b];
+          const double m0 = (M[0] * vb.x + M[1] * vb.y) + M[2] * vb.z;
+          const double m1 = (M[3] * vb.x + M[4] * vb.y) + M[5] * vb.z;
+          const double m2 = (M[6] * vb.x + M[7] * vb.y) + M[8] * vb.z;
+          fx = fx + damping * m0;
+          fy = fy + damping * m1;
+          fz = fz + damping * m2;
+        }
+      }
+      r0 = r0 + dt * fx;
+      r1 = r1 + dt * fy;
+      r2 = r2 + dt * fz;
+      // matrix (assembly.hpp:199-215)
+      const double scale = dt * dt + damping * dt;
+      const double nscale = -scale;
+      for (int b = 0; b < ss; ++b) {
+        const int col = st[b];
+        if (f.pinned[col]) continue;
+        const int slot = find(col);
+#pragma unroll
+        for (int q = 0; q < 9; ++q) {
+          double cv = nscale * ev.J[b][q];
+          if (ev.damped) cv = cv + dt * ev.D[b][q];
+          acc.at(slot, q) = acc.at(slot, q) + cv;
+        }
+      }
+    }
+  }
+  f.rhs[3 * r] = r0;
+  f.rhs[3 * r + 1] = r1;
+  f.rhs[3 * r + 2] = r2;
+  if (!Wide) {
+    for (int k = 0; k < len; ++k)
+#pragma unroll
+      for (int q = 0; q < 9; ++q) f.vals[q * f.total + base + (int64_t)k * kSlice] = acc.at(k, q);
+  }
+}
+
+// Padding slots must hold zeros (they are never read by the SpMV, which
+// stops at rowlen, but downloads and ncu byte counts stay honest).
+__global__ void k_zero_padding(int p, const int64_t* __restrict__ soff, const int32_t* __restrict__ rowlen,
+                               double* __restrict__ vals, int64_t total) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= p) return;
+  const int s = r >> 5;
+  const int width = static_cast<int>((soff[s + 1] - soff[s]) / kSlice);
+  const int64_t base = soff[s] + (r & 31);
+  for (int k = rowlen[r]; k < width; ++k)
+#pragma unroll
+    for (int q = 0; q < 9; ++q) vals[q * total + base + (int64_t)k * kSlice] = 0.0;
+}
+
+constexpr int kFillThreads = 64;
+constexpr int kWideCap = 24;
+
+void fill_matrix(Ctx& c, const double* xc, const double* xa, const double* vel, double dt, int mode) {
+  if (!(dt > 0.0)) throw Error(WEFT_ERR_DIMENSION, "fill_matrix: dt must be positive");
+  if (c.p == 0 && c.n_static == 0) throw Error(WEFT_ERR_INVALID, "fill_matrix: set_vertices/set_elements first");
+  if (c.spat_ptr.size() != static_cast<size_t>(c.p) + 1) throw Error(WEFT_ERR_INVALID, "fill_matrix: set_elements first");
+  cudaStream_t s = c.stream;
+  const bool layout_cached = c.has_matrix && c.n_contacts == 0 && c.have_pattern_for_contacts;
+  if (!layout_cached) {
+    build_layout(c);
+    c.have_pattern_for_contacts = c.n_contacts == 0;
+  }
+  SellMatrix& A = c.A;
+  c.rhs.resize(3 * static_cast<size_t>(c.p) + 3);
+  c.scalars.resize(64);
+  int* bad = reinterpret_cast<int*>(c.scalars.data() + 8);
+  const int big = INT32_MAX;
+  WG_CUDA(cudaMemcpyAsync(bad, &big, sizeof(int), cudaMemcpyHostToDevice, s));
+  FillArgs f{};
+  f.p = c.p;
+  f.n_static = c.n_static;
+  f.dt = dt;
+  f.exact = mode == WEFT_JAC_EXACT;
+  f.wcap = std::min(A.max_len, kWideCap);
+  f.slice_off = A.slice_off.data();
+  f.rowlen = A.rowlen.data();
+  f.cols = A.cols.data();
+  f.vals = A.vals.data();
+  f.total = A.total;
+  f.rhs = c.rhs.data();
+  f.mass = c.mass.data();
+  f.pinned = c.pinned.data();
+  f.inc_ptr = c.inc_ptr.data();
+  f.inc = c.inc.data();
+  f.cinc_ptr = c.cinc_ptr.data();
+  f.cinc = c.cinc.data();
+  f.est = c.est.data();
+  f.einfo = c.einfo.data();
+  f.edamp = c.edamp.data();
+  f.epay = c.epay.data();
+  f.xc = xc;
+  f.xa = xa;
+  f.vel = vel;
+  f.bad_mass = bad;
+  if (c.p) {
+    if (!layout_cached)
+      k_zero_padding<<<div_up(c.p, 256), 256, 0, s>>>(c.p, A.slice_off.data(), A.rowlen.data(), A.vals.data(), A.total);
+    const size_t smem = static_cast<size_t>(f.wcap) * (9 * sizeof(double) + sizeof(int32_t)) * kFillThreads;
+    WG_CUDA(cudaFuncSetAttribute(k_fill<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    k_fill<false><<<div_up(c.p, kFillThreads), kFillThreads, smem, s>>>(f);
+    if (A.max_len > kWideCap) {
+      // rows wider than the shared-memory budget accumulate in place
+      k_fill<true><<<div_up(c.p, kFillThreads), kFillThreads, 0, s>>>(f);
+    }
+    WG_CUDA(cudaGetLastError());
+  }
+  int hbad = big;
+  WG_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s));
+  WG_CUDA(cudaStreamSynchronize(s));
+  if (hbad != big)
+    throw Error(WEFT_ERR_DIMENSION, "fill_matrix: vertex " + std::to_string(hbad) + " has non-positive mass");
+  c.has_matrix = true;
+  c.has_rhs = true;
+}
+
+}  // namespace weft_gpu

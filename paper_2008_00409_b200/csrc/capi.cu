@@ -7,10 +7,6 @@
 
 #include "ctx.cuh"
 
-struct weft_gpu_ctx {
-  weft_gpu::Ctx c;
-};
-
 namespace {
 thread_local std::string g_last_error;
 
@@ -65,6 +61,11 @@ void gen_range(int lo, int hi, std::vector<std::vector<int>>& peer, std::vector<
 extern "C" {
 
 const char* weft_gpu_last_error(void) { return g_last_error.c_str(); }
+
+weft_status weft_gpu_internal_set_error(const char* msg, weft_status s) {
+  g_last_error = msg;
+  return s;
+}
 
 weft_status weft_make_partitions(int32_t p, int32_t n, int32_t* begin, int32_t* end) {
   return guard(nullptr, [&] {

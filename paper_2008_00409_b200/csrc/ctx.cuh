@@ -125,7 +125,7 @@ void pcg_free(Ctx& c);
 void set_vertices(Ctx& c, int p, const double* mass, const uint8_t* pinned);
 void set_elements(Ctx& c, int64_t count, const weft_element* elems);
 void set_contacts(Ctx& c, int64_t count, const weft_element* elems);
-void fill_matrix(Ctx& c, double dt, int mode);  // uses c.x_cur, c.x_adv, c.vel
+void fill_matrix(Ctx& c, const double* xc, const double* xa, const double* vel, double dt, int mode);
 
 void set_soup(Ctx& c, int verts, int ntris, const int32_t* tris);
 void build_grid(Ctx& c, const double* x0_dev, const double* x1_dev, int mode, double thickness, double cell_scale);
@@ -135,3 +135,8 @@ int64_t candidates(Ctx& c, int64_t begin, int64_t end, int32_t* pairs_dev_or_nul
 void* scratch(Ctx& c, size_t bytes);
 
 }  // namespace weft_gpu
+
+// The opaque handle of the C-ABI.
+struct weft_gpu_ctx {
+  weft_gpu::Ctx c;
+};

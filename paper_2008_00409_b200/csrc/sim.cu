@@ -1,0 +1,231 @@
+// sim.cu — C-ABI for assembly and broad phase, and the device-resident
+// hot-path step (Simulator::step_impl stages 1-4 plus the CCD broad phase,
+// proj/src/driver.cpp:96-215; narrow phase and impact zones are out of
+// scope for this tier).
+#include <string>
+
+#include "ctx.cuh"
+
+namespace weft_gpu {
+namespace {
+
+// x_adv = x + dt v (physics.hpp:54-55)
+__global__ void k_advance(int64_t n, const double* __restrict__ x, const double* __restrict__ v, double dt,
+                          double* __restrict__ out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) out[i] = x[i] + dt * v[i];
+}
+
+// v += dv; x_cand = x + dt v (driver.cpp:165-176)
+__global__ void k_candidate(int64_t n, const double* __restrict__ x, double* __restrict__ v,
+                            const double* __restrict__ dv, double dt, double* __restrict__ xc) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double vi = v[i] + dv[i];
+  v[i] = vi;
+  xc[i] = x[i] + dt * vi;
+}
+
+void upload_vec(Ctx& c, DBuf<double>& dst, const double* src, size_t n) {
+  dst.resize(n);
+  if (n) WG_CUDA(cudaMemcpyAsync(dst.data(), src, n * sizeof(double), cudaMemcpyDefault, c.stream));
+}
+
+}  // namespace
+}  // namespace weft_gpu
+
+using weft_gpu::Ctx;
+using weft_gpu::Error;
+
+// Shares the boundary's error convention (capi.cu).
+extern "C" weft_status weft_gpu_internal_set_error(const char* msg, weft_status s);
+
+namespace {
+template <class F>
+weft_status guard2(weft_gpu_ctx* ctx, F&& f) {
+  try {
+    if (!ctx) throw Error(WEFT_ERR_INVALID, "null context");
+    WG_CUDA(cudaSetDevice(ctx->c.device));
+    f(ctx->c);
+    return WEFT_OK;
+  } catch (const Error& e) {
+    return weft_gpu_internal_set_error(e.what(), e.status);
+  } catch (const std::exception& e) {
+    return weft_gpu_internal_set_error(e.what(), WEFT_ERR_INVALID);
+  }
+}
+}  // namespace
+
+extern "C" {
+
+weft_status weft_gpu_set_vertices(weft_gpu_ctx* ctx, int32_t p, const double* mass, const uint8_t* pinned) {
+  return guard2(ctx, [&](Ctx& c) { weft_gpu::set_vertices(c, p, mass, pinned); });
+}
+
+weft_status weft_gpu_set_elements(weft_gpu_ctx* ctx, int64_t count, const weft_element* elements) {
+  return guard2(ctx, [&](Ctx& c) { weft_gpu::set_elements(c, count, elements); });
+}
+
+weft_status weft_gpu_set_contacts(weft_gpu_ctx* ctx, int64_t count, const weft_element* contacts) {
+  return guard2(ctx, [&](Ctx& c) { weft_gpu::set_contacts(c, count, contacts); });
+}
+
+weft_status weft_gpu_fill_matrix(weft_gpu_ctx* ctx, const double* x_cur, const double* x_adv, const double* velocity,
+                                 double dt, int32_t jac_mode) {
+  return guard2(ctx, [&](Ctx& c) {
+    const size_t n = 3 * static_cast<size_t>(c.p);
+    weft_gpu::upload_vec(c, c.x_cur, x_cur, n);
+    weft_gpu::upload_vec(c, c.x_adv, x_adv, n);
+    weft_gpu::upload_vec(c, c.vel, velocity, n);
+    weft_gpu::fill_matrix(c, c.x_cur.data(), c.x_adv.data(), c.vel.data(), dt, jac_mode);
+  });
+}
+
+weft_status weft_gpu_step_system(weft_gpu_ctx* ctx, const double* x, const double* v, double dt, int32_t jac_mode) {
+  return guard2(ctx, [&](Ctx& c) {
+    const size_t n = 3 * static_cast<size_t>(c.p);
+    weft_gpu::upload_vec(c, c.x_cur, x, n);
+    weft_gpu::upload_vec(c, c.vel, v, n);
+    c.x_adv.resize(n);
+    if (n)
+      weft_gpu::k_advance<<<weft_gpu::div_up(n, 256), 256, 0, c.stream>>>(n, c.x_cur.data(), c.vel.data(), dt,
+                                                                          c.x_adv.data());
+    WG_CUDA(cudaGetLastError());
+    weft_gpu::fill_matrix(c, c.x_cur.data(), c.x_adv.data(), c.vel.data(), dt, jac_mode);
+  });
+}
+
+weft_status weft_gpu_set_soup(weft_gpu_ctx* ctx, int32_t vertex_count, int32_t tri_count, const int32_t* tris) {
+  return guard2(ctx, [&](Ctx& c) { weft_gpu::set_soup(c, vertex_count, tri_count, tris); });
+}
+
+weft_status weft_gpu_build_grid(weft_gpu_ctx* ctx, const double* x_begin, const double* x_end, int32_t mode,
+                                double thickness, double cell_scale) {
+  return guard2(ctx, [&](Ctx& c) {
+    const size_t n = 3 * static_cast<size_t>(c.soup_verts);
+    if (!x_begin) throw Error(WEFT_ERR_INVALID, "build_grid: x_begin is NULL");
+    weft_gpu::upload_vec(c, c.x_cur, x_begin, n);
+    const bool ccd = mode == WEFT_CONTINUOUS;
+    if (ccd) {
+      if (!x_end) throw Error(WEFT_ERR_INVALID, "build_grid: continuous mode needs x_end");
+      weft_gpu::upload_vec(c, c.x_adv, x_end, n);
+    }
+    weft_gpu::build_grid(c, c.x_cur.data(), ccd ? c.x_adv.data() : c.x_cur.data(), mode, thickness, cell_scale);
+  });
+}
+
+weft_status weft_gpu_grid_info(weft_gpu_ctx* ctx, weft_grid_info* info) {
+  return guard2(ctx, [&](Ctx& c) {
+    if (!c.has_grid) throw Error(WEFT_ERR_INVALID, "grid_info: build_grid first");
+    info->cell_size = c.grid_cell_size;
+    info->cells = c.grid_cells;
+    info->entries = c.grid_entries;
+    info->total = c.grid_total;
+  });
+}
+
+weft_status weft_gpu_download_grid(weft_gpu_ctx* ctx, uint64_t* cell_keys, int64_t* cell_offsets, int32_t* cell_tris,
+                                   int64_t* prefix, int64_t* tri_boxes) {
+  return guard2(ctx, [&](Ctx& c) {
+    if (!c.has_grid) throw Error(WEFT_ERR_INVALID, "download_grid: build_grid first");
+    cudaStream_t s = c.stream;
+    if (cell_keys && c.grid_cells)
+      WG_CUDA(cudaMemcpyAsync(cell_keys, c.cell_keys.data(), 8 * c.grid_cells, cudaMemcpyDefault, s));
+    if (cell_offsets)
+      WG_CUDA(cudaMemcpyAsync(cell_offsets, c.cell_off.data(), 8 * (c.grid_cells + 1), cudaMemcpyDefault, s));
+    if (cell_tris && c.grid_entries)
+      WG_CUDA(cudaMemcpyAsync(cell_tris, c.vals_b.data(), 4 * c.grid_entries, cudaMemcpyDefault, s));
+    if (prefix) WG_CUDA(cudaMemcpyAsync(prefix, c.wprefix.data(), 8 * (c.grid_cells + 1), cudaMemcpyDefault, s));
+    std::vector<int32_t> lat;
+    if (tri_boxes && c.soup_tris) {
+      lat.resize(6 * static_cast<size_t>(c.soup_tris));
+      WG_CUDA(cudaMemcpyAsync(lat.data(), c.lat.data(), 4 * lat.size(), cudaMemcpyDeviceToHost, s));
+    }
+    WG_CUDA(cudaStreamSynchronize(s));
+    if (tri_boxes)
+      for (size_t i = 0; i < lat.size(); ++i) tri_boxes[i] = lat[i];
+  });
+}
+
+weft_status weft_gpu_candidates(weft_gpu_ctx* ctx, int64_t begin, int64_t end, int64_t* count, int32_t* pairs) {
+  return guard2(ctx, [&](Ctx& c) { *count = weft_gpu::candidates(c, begin, end, pairs); });
+}
+
+weft_status weft_gpu_sim_set_state(weft_gpu_ctx* ctx, const double* x, const double* v) {
+  return guard2(ctx, [&](Ctx& c) {
+    if (c.p == 0 || c.n_static == 0) throw Error(WEFT_ERR_INVALID, "sim_set_state: set vertices and elements first");
+    if (c.soup_verts != c.p) throw Error(WEFT_ERR_INVALID, "sim_set_state: soup must be the cloth (soup_verts == p)");
+    const size_t n = 3 * static_cast<size_t>(c.p);
+    weft_gpu::upload_vec(c, c.sim_x, x, n);
+    weft_gpu::upload_vec(c, c.sim_v, v, n);
+    c.sim_xc.resize(n);
+    WG_CUDA(cudaStreamSynchronize(c.stream));
+    c.has_state = true;
+  });
+}
+
+weft_status weft_gpu_sim_step(weft_gpu_ctx* ctx, const weft_sim_params* prm, weft_step_report* rep) {
+  return guard2(ctx, [&](Ctx& c) {
+    if (!c.has_state) throw Error(WEFT_ERR_INVALID, "sim_step: sim_set_state first");
+    cudaStream_t s = c.stream;
+    const int64_t n = 3 * static_cast<int64_t>(c.p);
+    const double dt = prm->dt;
+    cudaEvent_t* ev = c.ev;
+    // 1. proximity broad phase (DCD) on the current configuration
+    WG_CUDA(cudaEventRecord(ev[0], s));
+    weft_gpu::build_grid(c, c.sim_x.data(), c.sim_x.data(), WEFT_DISCRETE, prm->thickness, prm->cell_scale);
+    const int64_t dcd = weft_gpu::candidates(c, 0, c.grid_total, nullptr);
+    WG_CUDA(cudaEventRecord(ev[1], s));
+    // 2. assembly of step_system at (x, v)
+    c.x_adv.resize(static_cast<size_t>(n));
+    weft_gpu::k_advance<<<weft_gpu::div_up(n, 256), 256, 0, s>>>(n, c.sim_x.data(), c.sim_v.data(), dt,
+                                                                  c.x_adv.data());
+    weft_gpu::fill_matrix(c, c.sim_x.data(), c.x_adv.data(), c.sim_v.data(), dt, prm->jac_mode);
+    WG_CUDA(cudaEventRecord(ev[2], s));
+    // 3. PCG for dv
+    const weft_gpu::PcgResult pr = weft_gpu::pcg_solve(c, c.rhs.data(), prm->pcg, nullptr, nullptr);
+    WG_CUDA(cudaEventRecord(ev[3], s));
+    if (!pr.converged)  // driver.cpp:158-161
+      throw Error(WEFT_ERR_SOLVER, "PCG did not converge (residual " + std::to_string(pr.rel_residual) + ")");
+    // 4. candidate update
+    if (pr.iterations == 0) WG_CUDA(cudaMemsetAsync(c.xs.data(), 0, n * sizeof(double), s));
+    weft_gpu::k_candidate<<<weft_gpu::div_up(n, 256), 256, 0, s>>>(n, c.sim_x.data(), c.sim_v.data(), c.xs.data(),
+                                                                    dt, c.sim_xc.data());
+    WG_CUDA(cudaEventRecord(ev[4], s));
+    // 5. impact broad phase (CCD) over begin -> candidate
+    weft_gpu::build_grid(c, c.sim_x.data(), c.sim_xc.data(), WEFT_CONTINUOUS, prm->thickness, prm->cell_scale);
+    const int64_t ccd = weft_gpu::candidates(c, 0, c.grid_total, nullptr);
+    WG_CUDA(cudaEventRecord(ev[5], s));
+    // 7. commit (no zone correction in this tier)
+    std::swap(c.sim_x.ptr, c.sim_xc.ptr);
+    std::swap(c.sim_x.cap, c.sim_xc.cap);
+    WG_CUDA(cudaEventSynchronize(ev[5]));
+    float t01 = 0, t12 = 0, t23 = 0, t45 = 0;
+    cudaEventElapsedTime(&t01, ev[0], ev[1]);
+    cudaEventElapsedTime(&t12, ev[1], ev[2]);
+    cudaEventElapsedTime(&t23, ev[2], ev[3]);
+    cudaEventElapsedTime(&t45, ev[4], ev[5]);
+    if (rep) {
+      rep->pcg_iterations = pr.iterations;
+      rep->pcg_converged = pr.converged;
+      rep->pcg_residual = pr.rel_residual;
+      rep->dcd_candidates = dcd;
+      rep->ccd_candidates = ccd;
+      rep->ms_broad = t01 + t45;
+      rep->ms_assemble = t12;
+      rep->ms_solve = t23;
+    }
+  });
+}
+
+weft_status weft_gpu_sim_get_state(weft_gpu_ctx* ctx, double* x, double* v) {
+  return guard2(ctx, [&](Ctx& c) {
+    if (!c.has_state) throw Error(WEFT_ERR_INVALID, "sim_get_state: no state");
+    const size_t n = 3 * static_cast<size_t>(c.p);
+    if (x) WG_CUDA(cudaMemcpyAsync(x, c.sim_x.data(), n * sizeof(double), cudaMemcpyDefault, c.stream));
+    if (v) WG_CUDA(cudaMemcpyAsync(v, c.sim_v.data(), n * sizeof(double), cudaMemcpyDefault, c.stream));
+    WG_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+
+}  // extern "C"

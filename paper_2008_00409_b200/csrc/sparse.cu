@@ -208,6 +208,7 @@ void set_matrix_csr(Ctx& c, int rows, const int64_t* row_ptr, const int32_t* col
   WG_CUDA(cudaStreamSynchronize(c.stream));
   c.has_matrix = true;
   c.has_rhs = false;
+  c.have_pattern_for_contacts = false;
 }
 
 // Global CSR with ascending columns (gather_matrix, sparse.hpp:149-173).

@@ -357,3 +357,77 @@ class Engine:
 
     def sim_get_state(self, x=None, v=None):
         _check(LIB.weft_gpu_sim_get_state(self._ctx, _ptr(x), _ptr(v)))
+
+
+# ---------------------------------------------------------------------------
+# static mesh precompute (include/weft_mesh.h) — one-time host setup
+# ---------------------------------------------------------------------------
+LIB.weft_mesh_last_error.restype = C.c_char_p
+LIB.weft_mesh_destroy.argtypes = [C.c_void_p]
+
+DEFAULT_MATERIAL = (400.0, 400.0, 60.0, 2e-5, 0.15, 0.002, 0.0)  # MaterialParams (physics.hpp:8-16)
+
+
+def _mcheck(status: int):
+    if status != 0:
+        raise (DimensionError if status == 1 else Error)(LIB.weft_mesh_last_error().decode())
+
+
+class ClothMesh:
+    """ClothMesh (mesh.hpp:13-52): rest data, hinges, lumped masses."""
+
+    def __init__(self, handle: C.c_void_p):
+        self._h = handle
+        nv, nt, nh, ne = C.c_int32(), C.c_int32(), C.c_int32(), C.c_int32()
+        _mcheck(LIB.weft_mesh_info(self._h, C.byref(nv), C.byref(nt), C.byref(nh), C.byref(ne)))
+        nv, nt, nh = nv.value, nt.value, nh.value
+        self.rest = np.zeros(3 * nv)
+        self.triangles = np.zeros((nt, 3), np.int32)
+        self.tri_rest = np.zeros((nt, 7))
+        self.tri_degenerate = np.zeros(nt, np.uint8)
+        self.hinge_verts = np.zeros((nh, 4), np.int32)
+        self.hinge_data = np.zeros((nh, 2))
+        self.vertex_area = np.zeros(nv)
+        self.vertex_mass = np.zeros(nv)
+        _mcheck(LIB.weft_mesh_copy(self._h, _ptr(self.rest), _ptr(self.triangles), _ptr(self.tri_rest),
+                                   _ptr(self.tri_degenerate), _ptr(self.hinge_verts), _ptr(self.hinge_data),
+                                   _ptr(self.vertex_area), _ptr(self.vertex_mass)))
+
+    @property
+    def vertex_count(self) -> int:
+        return len(self.vertex_mass)
+
+    @classmethod
+    def build(cls, vertices, triangles, density: float) -> "ClothMesh":
+        v = _f64(vertices)
+        t = np.ascontiguousarray(triangles, np.int32).reshape(-1)
+        h = C.c_void_p()
+        _mcheck(LIB.weft_mesh_build(C.c_int32(len(v) // 3), _ptr(v), C.c_int32(len(t) // 3), _ptr(t),
+                                    C.c_double(density), C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def grid(cls, nx: int, ny: int, width: float, height: float, origin=(0.0, 0.0, 0.0), density: float = 0.15):
+        """make_grid_mesh (mesh.cpp:187-212)."""
+        h = C.c_void_p()
+        o = np.array(origin, np.float64)
+        _mcheck(LIB.weft_mesh_grid(C.c_int32(nx), C.c_int32(ny), C.c_double(width), C.c_double(height), _ptr(o),
+                                   C.c_double(density), C.byref(h)))
+        return cls(h)
+
+    def build_elements(self, material=DEFAULT_MATERIAL, gravity=(0.0, 0.0, -9.81), wind=(0.0, 0.0, 0.0)):
+        """build_elements (physics.cpp:5-63): triangles, hinges, vertices."""
+        mat = np.array(material, np.float64)
+        g = np.array(gravity, np.float64)
+        w = np.array(wind, np.float64)
+        n = C.c_int64()
+        _mcheck(LIB.weft_build_elements(self._h, _ptr(mat), _ptr(g), _ptr(w), None, C.c_int64(0), C.byref(n)))
+        out = np.zeros(n.value, ELEMENT_DTYPE)
+        _mcheck(LIB.weft_build_elements(self._h, _ptr(mat), _ptr(g), _ptr(w), _ptr(out), C.c_int64(n.value),
+                                        C.byref(n)))
+        return out
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            LIB.weft_mesh_destroy(self._h)
+            self._h = None

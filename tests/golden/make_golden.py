@@ -1,0 +1,59 @@
+"""Generates the golden fixtures under tests/golden/ from the COMPILED
+REFERENCE (oracle/_ref/libweft_ref.so, built from the unmodified sources in
+/root/reference by `make -C oracle ref`). Run here, where the reference
+exists; the .npz files are committed so GPU boxes (no /root/reference) can
+check against the reference's own outputs.
+
+    python tests/golden/make_golden.py
+"""
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.dirname(HERE))
+from oracle_bindings import CONTINUOUS, DISCRETE, JAC_EXACT, JAC_SPD, REF  # noqa: E402
+from problems import cloth_problem  # noqa: E402
+
+
+def main():
+    assert REF is not None, "oracle/_ref/libweft_ref.so missing: make -C oracle ref"
+    # assembly: random_cloth problems (test_assembly.cpp:55-71 recipe) with
+    # contacts / drag, both Jacobian modes, reference fill_matrix at n = 2.
+    for k, (seed, contacts, drag) in enumerate([(11, 0, False), (12, 5, True), (13, 9, False), (14, 3, True)]):
+        pr = cloth_problem(REF, seed, 7, contacts=contacts, drag=drag)
+        out = dict(elems=pr["elems"].view(np.uint8), x=pr["x"], x_adv=pr["x_adv"], v=pr["v"], mass=pr["mass"],
+                   pinned=pr["pinned"], dt=np.array(pr["dt"]))
+        for mode, tag in ((JAC_SPD, "spd"), (JAC_EXACT, "exact")):
+            s = REF.fill_matrix(pr["elems"], pr["x"], pr["x_adv"], pr["v"], pr["mass"], pr["pinned"], pr["dt"], mode, n=2)
+            out[f"{tag}_row_ptr"], out[f"{tag}_cols"], out[f"{tag}_vals"], out[f"{tag}_rhs"] = s.row_ptr, s.cols, s.vals, s.rhs
+        x, rep = REF.pcg(REF.fill_matrix(pr["elems"], pr["x"], pr["x_adv"], pr["v"], pr["mass"], pr["pinned"], pr["dt"]),
+                         out["spd_rhs"], 2, tol=1e-10)
+        out["pcg_x"], out["pcg_iterations"] = x, np.array(rep["iterations"])
+        np.savez_compressed(os.path.join(HERE, f"assembly_{k}.npz"), **out)
+    # broad phase: random_two_cloth_scene (collision_oracle.cpp:110-138).
+    for k, seed in enumerate([41, 42, 43]):
+        nv, tris, x0, x1 = REF.two_cloth_scene(seed, 8)
+        out = dict(nv=np.array(nv), tris=tris, x0=x0, x1=x1)
+        for mode, tag in ((DISCRETE, "dcd"), (CONTINUOUS, "ccd")):
+            g = REF.build_grid(nv, tris, x0, x1, mode=mode, thickness=0.01)
+            out[f"{tag}_cell_size"] = np.array(g.cell_size)
+            for f in ("tri_boxes", "cell_keys", "cell_offsets", "cell_tris", "prefix"):
+                out[f"{tag}_{f}"] = getattr(g, f)
+            out[f"{tag}_pairs"] = REF.candidates(g)
+            REF.free_grid(g)
+        np.savez_compressed(os.path.join(HERE, f"grid_{k}.npz"), **out)
+    # SpMV: oracle::random_bell (sparse_oracle.cpp:7-23), pipelined at n = 1, 2, 4.
+    for k, (seed, rows) in enumerate([(5, 7), (6, 40)]):
+        s = REF.random_bell(seed, rows, 3)
+        x = np.random.default_rng(seed).uniform(-2, 2, 3 * rows)
+        out = dict(rows=np.array(rows), row_ptr=s.row_ptr, cols=s.cols, vals=s.vals, x=x)
+        for n in (1, 2, 4):
+            out[f"y{n}"] = REF.spmv(s, x, n)
+        np.savez_compressed(os.path.join(HERE, f"spmv_{k}.npz"), **out)
+    print("golden fixtures written to", HERE)
+
+
+if __name__ == "__main__":
+    main()
