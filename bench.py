@@ -1,0 +1,323 @@
+#!/usr/bin/env python
+"""Hot-path benchmark (driver contract).
+
+A step = one pass of the implicit-integration hot path over the synthetic
+Kneel-scale cloth (BASELINE config D: 3 x 525^2 grid layers, 1,647,456
+triangles, 826,875 vertices): DCD broad phase (grid + candidate pairs),
+step_system assembly, block-Jacobi PCG (tol 1e-4), candidate update, CCD
+broad phase (grid + candidate pairs), commit. Narrow phase / impact zones
+are out of this tier's scope in both arms.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+GPU arm: `value` is device-resident steps/s (CUDA events on the context's
+stream, max over ranks); `e2e` is the same step through the C-ABI with the
+state (x, v) copied host->device and back every step. Reference arm: the
+unmodified reference (oracle/_ref, compiled from /root/reference) running the
+same step on the host cores with Engine(n) threads.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "sim steps/sec at 1.65M-tri cloth, 1/2/4/8 B200; SpMV+assembly HBM GB/s vs peak"
+UNIT = "steps/s"
+FALLBACK_HBM_GBS = 6650.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["gpu", "reference"], default="gpu")
+    ap.add_argument("--config", default="D", help="scene config (A/B/C/D, BASELINE.md §2)")
+    ap.add_argument("--seed", type=int, default=20240810)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--ref-budget-s", type=float, default=150.0, help="wall budget of the reference arm")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# ---------------------------------------------------------------- clocks
+class Clocks:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.f = tempfile.NamedTemporaryFile("w+", delete=False)
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                       "-lms", "100", "-i", str(device)], stdout=self.f, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.p = None
+
+    def stop(self) -> dict:
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)
+        self.p.terminate()
+        self.p.wait()
+        self.f.seek(0)
+        sm, mx, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for line in self.f.read().splitlines():
+            parts = [s.strip() for s in line.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[4:8]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        os.unlink(self.f.name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def traffic_per_launch(config: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum of one k_pcg_spmv launch
+    from the committed ncu --set full capture (profiles/), or None."""
+    path = os.path.join(ROOT, "profiles", "spmv_traffic.json")
+    if not os.path.exists(path):
+        return None
+    with open(path) as f:
+        d = json.load(f)
+    return d.get(config)
+
+
+# ---------------------------------------------------------------- scene
+def make_scene(config: str, seed: int):
+    from paper_2008_00409_b200 import scenes
+    return scenes.config(config, seed=seed)
+
+
+# ---------------------------------------------------------------- reference
+def ref_devices():
+    n = os.cpu_count() or 1
+    d = 1
+    while d * 2 <= min(n, 32):
+        d *= 2
+    return d, n
+
+
+def run_reference_steps(sc, steps: int, warmup: int, budget_s: float):
+    """Times the compiled reference's hot-path step (oracle/ref_harness.cpp
+    ref_sim_step). Returns (mean seconds per timed step, timed steps, info)."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracle_bindings import REF, RefSim
+    if REF is None:
+        return None, 0, {"unavailable": "oracle/_ref/libweft_ref.so not built (needs /root/reference at build time)"}
+    devices, nproc = ref_devices()
+    sim = RefSim(REF, sc.verts, sc.tris, sc.pinned, sc.density, sc.material, devices)
+    times, reps = [], []
+    t_start = time.time()
+    for k in range(warmup + steps):
+        t0 = time.perf_counter()
+        r = sim.step(sc.dt, sc.thickness)
+        dt = time.perf_counter() - t0
+        if k >= warmup:
+            times.append(dt)
+            reps.append(r)
+        if time.time() - t_start + dt > budget_s and len(times) >= 1:
+            break
+    sim.close()
+    return statistics.mean(times), len(times), {"devices": devices, "nproc": nproc, "last": reps[-1] if reps else {}}
+
+
+def reference_arm(args, rank, world):
+    if rank != 0:
+        return
+    sc = make_scene(args.config, args.seed)
+    sec, n, info = run_reference_steps(sc, args.steps, min(args.warmup, 1), args.ref_budget_s)
+    if sec is None:
+        print(json.dumps({"impl": "reference", "unavailable": info["unavailable"]}), flush=True)
+        return
+    value = 1.0 / sec
+    sample = (f"{n} timed full hot-path step(s) of config {args.config} after {min(args.warmup, 1)} warm-up, "
+              f"reference Engine({info['devices']}) = {2 * info['devices']} threads on {info['nproc']} host cores")
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": n, "warmup": min(args.warmup, 1),
+        "ms_per_step": 1e3 * sec, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic", "impl": "reference",
+        "config": {"workload": f"config {args.config}: {sc.layers} x {sc.nx}^2 layered cloth, {sc.tri_count} tris, "
+                               f"{sc.vertex_count} verts", "dt": sc.dt, "pcg_tol": 1e-4,
+                   "reference_stage_ms": info["last"]},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": info["devices"], "kind": "reference", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+
+
+# ---------------------------------------------------------------- GPU arm
+def gpu_arm(args, rank, world, local):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local)
+    if world > 1 and not dist.is_initialized():
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2008_00409_b200 import weft
+
+    sc = make_scene(args.config, args.seed)
+    mesh = weft.ClothMesh.build(sc.verts, sc.tris, sc.density)
+    elems = mesh.build_elements(sc.material, sc.gravity)
+    p = mesh.vertex_count
+    eng = weft.Engine(1, cuda_device=local)
+    eng.set_vertices(mesh.vertex_mass, sc.pinned)
+    eng.set_elements(elems)
+    eng.set_soup(p, sc.tris)
+    x0 = sc.verts.reshape(-1).copy()
+    v0 = np.zeros_like(x0)
+    eng.sim_set_state(x0, v0)
+    params = weft.SimParams(sc.dt, sc.thickness, 1.5, weft.PcgConfig(1e-4, 400, weft.PRECOND_BLOCK_JACOBI),
+                            weft.JAC_SPD)
+    stream = torch.cuda.ExternalStream(eng.stream(), device=torch.device("cuda", local))
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(v: float) -> float:
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(args.warmup):
+        eng.sim_step(params)
+
+    # ---- device-resident timed region
+    barrier()
+    eng.profile(True)
+    launches0 = eng.stats().launches
+    clocks = Clocks(local)
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    reps = [eng.sim_step(params) for _ in range(args.steps)]
+    ev1.record(stream)
+    ev1.synchronize()
+    barrier()
+    clk = clocks.stop()
+    ms_total = max_over_ranks(ev0.elapsed_time(ev1))
+    st = eng.stats()
+    eng.profile(False)
+    launches = st.launches - launches0
+    spmv_avg_ms = st.spmv_ms / max(st.spmv_launches, 1)
+    info = eng.matrix_info()
+
+    # ---- end-to-end through the C-ABI with host buffers
+    e2e = None
+    if not args.no_e2e:
+        xh = torch.empty(3 * p, dtype=torch.float64, pin_memory=True)
+        vh = torch.empty(3 * p, dtype=torch.float64, pin_memory=True)
+        eng.sim_get_state(xh, vh)
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            eng.sim_set_state(xh, vh)  # H2D of the step's inputs
+            eng.sim_step(params)
+            eng.sim_get_state(xh, vh)  # D2H of the step's result
+        e1.record(stream)
+        e1.synchronize()
+        barrier()
+        e2e_ms = max_over_ranks(e0.elapsed_time(e1))
+        e2e = {"value": world * args.steps / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": 2 * 8 * 3 * p,
+               "d2h_bytes_per_step": 2 * 8 * 3 * p}
+
+    if rank != 0:
+        return
+    value = world * args.steps / (ms_total / 1e3)
+    peak, peak_src = peaks()
+    # algorithmic bytes of one k_pcg_spmv launch: 9 FP64 values + 1 int32
+    # column per live block; per row: length word, z and p gathered once,
+    # q written.
+    alg_bytes = info.nnzb * (9 * 8 + 4) + info.block_rows * (4 + 3 * 8 * 3)
+    achieved = alg_bytes / (spmv_avg_ms * 1e-3) / 1e9
+    traffic = traffic_per_launch(args.config)
+    it = [r.pcg_iterations for r in reps]
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        sec, n, rinfo = run_reference_steps(sc, 1, 0, 45.0)
+        if sec is not None:
+            cpu = {"value": 1.0 / sec, "unit": UNIT, "cores": rinfo["devices"], "kind": "reference",
+                   "sample": f"{n} full hot-path step(s) of config {args.config} by the compiled reference, "
+                             f"Engine({rinfo['devices']}) on {rinfo['nproc']} host cores"}
+        else:
+            cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": rinfo["unavailable"]}
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_total / args.steps, "higher_is_better": True,
+        "scaling": "weak" if world > 1 else "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {
+            "workload": f"config {args.config}: {sc.layers} x {sc.nx}^2 layered cloth, {sc.tri_count} tris, "
+                        f"{p} verts, pinned top edges, dt={sc.dt:.6g}, PCG tol 1e-4 block-Jacobi",
+            "parallelism": "single GPU" if world == 1 else f"{world} independent replicas (partitioned multi-GPU "
+                                                            "path not enabled in this build)",
+            "l2": "inputs larger than L2 (matrix alone ~0.75 GB)",
+            "pcg_iterations_mean": statistics.mean(it), "nnzb": info.nnzb, "block_rows": info.block_rows,
+            "dcd_candidates": reps[-1].dcd_candidates, "ccd_candidates": reps[-1].ccd_candidates,
+            "stage_ms_mean": {"broad": statistics.mean(r.ms_broad for r in reps),
+                              "assemble": statistics.mean(r.ms_assemble for r in reps),
+                              "solve": statistics.mean(r.ms_solve for r in reps)},
+            "gpu_launches_per_step": launches / args.steps,
+        },
+        "roofline": {"bound": "hbm", "kernel": "k_pcg_spmv", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "alg_bytes_per_launch": alg_bytes,
+                     "avg_launch_ms": spmv_avg_ms, "launches": st.spmv_launches, "peak_source": peak_src},
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "clocks": clk,
+    }
+    print(json.dumps(out), flush=True)
+    eng.close()
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        reference_arm(args, rank, world)
+    else:
+        gpu_arm(args, rank, world, local)
+
+
+if __name__ == "__main__":
+    main()

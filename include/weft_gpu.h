@@ -272,6 +272,22 @@ weft_status weft_gpu_sim_step(weft_gpu_ctx* ctx, const weft_sim_params* params, 
 /* Reads the state back (either pointer may be NULL). */
 weft_status weft_gpu_sim_get_state(weft_gpu_ctx* ctx, double* x, double* v);
 
+/* ---------------------------------------------------------------------- */
+/* Instrumentation (bench.py)                                             */
+/* ---------------------------------------------------------------------- */
+
+typedef struct weft_gpu_stats_t {
+  int64_t launches;      /* kernels of this library launched by the context */
+  int64_t spmv_launches; /* PCG SpMV launches timed while profiling */
+  double spmv_ms;        /* their summed device time (CUDA events) */
+} weft_gpu_stats_t;
+
+/* Enables per-launch CUDA-event timing of the PCG SpMV kernel (resets). */
+weft_status weft_gpu_profile(weft_gpu_ctx* ctx, int32_t enable);
+weft_status weft_gpu_stats(weft_gpu_ctx* ctx, weft_gpu_stats_t* out);
+/* The cudaStream_t all of the context's work is issued on. */
+weft_status weft_gpu_get_stream(weft_gpu_ctx* ctx, void** stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -203,6 +203,59 @@ struct GridHandle {
 
 }  // namespace
 
+namespace {
+// Candidate pairs of [begin, end): the loop of narrow_phase_range
+// (collision.cpp:340-376) with narrow_phase_pair replaced by emission.
+int64_t ref_grid_candidates_impl(const GridBuildResult& built, int64_t begin, int64_t end, int32_t* pairs = nullptr) {
+  const auto& grid = built.grid;
+  const auto& table = built.table;
+  if (begin >= end) return 0;
+  std::size_t cell = static_cast<std::size_t>(
+      std::upper_bound(table.prefix.begin(), table.prefix.end(), begin) - table.prefix.begin() - 1);
+  const std::int64_t local = begin - table.prefix[cell];
+  int i = 0, j = 0;
+  {
+    const int s = static_cast<int>(grid.cell_tris[cell].size());
+    std::int64_t remaining = local;
+    while (remaining >= s - 1 - i) {
+      remaining -= s - 1 - i;
+      ++i;
+    }
+    j = i + 1 + static_cast<int>(remaining);
+  }
+  int64_t count = 0;
+  for (std::int64_t gi = begin; gi < end; ++gi) {
+    while (gi >= table.prefix[cell + 1]) {
+      ++cell;
+      i = 0;
+      j = 1;
+    }
+    const auto& tl = grid.cell_tris[cell];
+    const int t1 = tl[static_cast<std::size_t>(i)];
+    const int t2 = tl[static_cast<std::size_t>(j)];
+    const auto& a = grid.tri_boxes[static_cast<std::size_t>(t1)];
+    const auto& b = grid.tri_boxes[static_cast<std::size_t>(t2)];
+    constexpr std::int64_t bias = 1 << 20;
+    const std::uint64_t key = (static_cast<std::uint64_t>(std::max(a[0], b[0]) + bias) << 42) |
+                              (static_cast<std::uint64_t>(std::max(a[1], b[1]) + bias) << 21) |
+                              static_cast<std::uint64_t>(std::max(a[2], b[2]) + bias);
+    if (key == grid.cell_keys[cell]) {
+      if (pairs) {
+        pairs[2 * count] = t1;
+        pairs[2 * count + 1] = t2;
+      }
+      ++count;
+    }
+    if (++j >= static_cast<int>(tl.size())) {
+      ++i;
+      j = i + 1;
+    }
+  }
+  return count;
+}
+
+}  // namespace
+
 extern "C" {
 
 const char* ref_last_error() { return g_err.c_str(); }
@@ -489,55 +542,8 @@ void ref_grid_split(void* h, int32_t devices, int64_t* begin, int64_t* end) {
   }
 }
 
-// Candidate pairs of [begin, end): the loop of narrow_phase_range
-// (collision.cpp:340-376) with narrow_phase_pair replaced by emission.
 int64_t ref_grid_candidates(void* h, int64_t begin, int64_t end, int32_t* pairs) {
-  const auto* g = static_cast<GridHandle*>(h);
-  const auto& grid = g->built.grid;
-  const auto& table = g->built.table;
-  if (begin >= end) return 0;
-  std::size_t cell = static_cast<std::size_t>(
-      std::upper_bound(table.prefix.begin(), table.prefix.end(), begin) - table.prefix.begin() - 1);
-  const std::int64_t local = begin - table.prefix[cell];
-  int i = 0, j = 0;
-  {
-    const int s = static_cast<int>(grid.cell_tris[cell].size());
-    std::int64_t remaining = local;
-    while (remaining >= s - 1 - i) {
-      remaining -= s - 1 - i;
-      ++i;
-    }
-    j = i + 1 + static_cast<int>(remaining);
-  }
-  int64_t count = 0;
-  for (std::int64_t gi = begin; gi < end; ++gi) {
-    while (gi >= table.prefix[cell + 1]) {
-      ++cell;
-      i = 0;
-      j = 1;
-    }
-    const auto& tl = grid.cell_tris[cell];
-    const int t1 = tl[static_cast<std::size_t>(i)];
-    const int t2 = tl[static_cast<std::size_t>(j)];
-    const auto& a = grid.tri_boxes[static_cast<std::size_t>(t1)];
-    const auto& b = grid.tri_boxes[static_cast<std::size_t>(t2)];
-    constexpr std::int64_t bias = 1 << 20;
-    const std::uint64_t key = (static_cast<std::uint64_t>(std::max(a[0], b[0]) + bias) << 42) |
-                              (static_cast<std::uint64_t>(std::max(a[1], b[1]) + bias) << 21) |
-                              static_cast<std::uint64_t>(std::max(a[2], b[2]) + bias);
-    if (key == grid.cell_keys[cell]) {
-      if (pairs) {
-        pairs[2 * count] = t1;
-        pairs[2 * count + 1] = t2;
-      }
-      ++count;
-    }
-    if (++j >= static_cast<int>(tl.size())) {
-      ++i;
-      j = i + 1;
-    }
-  }
-  return count;
+  return ref_grid_candidates_impl(static_cast<GridHandle*>(h)->built, begin, end, pairs);
 }
 
 void ref_grid_free(void* h) { delete static_cast<GridHandle*>(h); }
@@ -559,5 +565,147 @@ int32_t ref_two_cloth_scene(uint64_t seed, int32_t max_side, int32_t* tri_count,
     }
   return s.soup.vertex_count;
 }
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// The reference arm of bench.py: the same hot-path step as weft_gpu_sim_step
+// executed by the reference's own functions and Engine threads:
+//   collide()'s broad-phase structure (replicated build_grid per device,
+//   split_workload, per-device candidate walk; collision.cpp:391-417, with
+//   narrow_phase_pair out of scope), step_system<double>, pcg_solve,
+//   candidate update, CCD broad phase, commit (driver.cpp:96-215).
+// ---------------------------------------------------------------------------
+namespace {
+
+struct RefSim {
+  ClothMesh mesh;
+  std::vector<uint8_t> pinned;
+  MaterialParams material;
+  CollisionSoup soup;
+  SimState state;
+  std::unique_ptr<Engine> engine;
+  ValidatedSchedule sched;
+};
+
+int64_t ref_collide_candidates(RefSim& s, std::span<const Vec3> x0, std::span<const Vec3> x1, CollisionMode mode,
+                               const CollisionParams& params, double* grid_ms) {
+  const int n = s.engine->devices();
+  const auto t0 = std::chrono::steady_clock::now();
+  std::vector<GridBuildResult> grids(static_cast<std::size_t>(n));
+  s.engine->parallel([&](int d) { grids[static_cast<std::size_t>(d)] = build_grid(s.soup, x0, x1, mode, params); });
+  const auto t1 = std::chrono::steady_clock::now();
+  *grid_ms += std::chrono::duration<double, std::milli>(t1 - t0).count();
+  const auto ranges = split_workload(grids[0].table, n);
+  std::vector<int64_t> counts(static_cast<std::size_t>(n), 0);
+  s.engine->parallel([&](int d) {
+    counts[static_cast<std::size_t>(d)] = ref_grid_candidates_impl(
+        grids[static_cast<std::size_t>(d)], ranges[static_cast<std::size_t>(d)].begin, ranges[static_cast<std::size_t>(d)].end);
+  });
+  int64_t total = 0;
+  for (auto c : counts) total += c;
+  return total;
+}
+
+}  // namespace
+
+extern "C" {
+
+void* ref_sim_create(int32_t nverts, const double* verts, int32_t ntris, const int32_t* tris, const uint8_t* pinned,
+                     double density, const double* material, int32_t devices) {
+  try {
+    auto* s = new RefSim();
+    std::vector<std::array<int, 3>> t(static_cast<std::size_t>(ntris));
+    for (int i = 0; i < ntris; ++i) t[static_cast<std::size_t>(i)] = {tris[3 * i], tris[3 * i + 1], tris[3 * i + 2]};
+    s->mesh = ClothMesh::build(to_vec3(verts, nverts), t, density);
+    s->pinned.assign(pinned, pinned + nverts);
+    s->material.stretch_warp = material[0];
+    s->material.stretch_weft = material[1];
+    s->material.shear = material[2];
+    s->material.bend = material[3];
+    s->material.density = material[4];
+    s->material.damping = material[5];
+    s->material.air_drag = material[6];
+    std::vector<std::uint8_t> movable(static_cast<std::size_t>(nverts));
+    for (int v = 0; v < nverts; ++v) movable[static_cast<std::size_t>(v)] = pinned[v] ? 0 : 1;
+    s->soup = CollisionSoup::build(std::move(t), nverts, std::move(movable));
+    s->state = SimState::rest(s->mesh);
+    s->engine = std::make_unique<Engine>(devices);
+    s->sched = schedule_for(devices);
+    return s;
+  } catch (const std::exception& e) {
+    set_error(e);
+    return nullptr;
+  }
+}
+
+void ref_sim_set_state(void* h, const double* x, const double* v) {
+  auto* s = static_cast<RefSim*>(h);
+  const int p = s->mesh.vertex_count();
+  s->state.x = to_vec3(x, p);
+  s->state.v = to_vec3(v, p);
+}
+
+void ref_sim_get_state(void* h, double* x, double* v) {
+  auto* s = static_cast<RefSim*>(h);
+  for (std::size_t i = 0; i < s->state.x.size(); ++i)
+    for (int c = 0; c < 3; ++c) {
+      if (x) x[3 * i + static_cast<std::size_t>(c)] = s->state.x[i][c];
+      if (v) v[3 * i + static_cast<std::size_t>(c)] = s->state.v[i][c];
+    }
+}
+
+// params: dt, thickness, cell_scale, pcg tol, pcg max its. out (8 doubles):
+// pcg iterations, converged, residual, dcd candidates, ccd candidates,
+// ms broad, ms assemble, ms solve.
+int32_t ref_sim_step(void* h, const double* params, double* out) {
+  auto* s = static_cast<RefSim*>(h);
+  try {
+    const double dt = params[0];
+    CollisionParams cp;
+    cp.thickness = params[1];
+    cp.cell_scale = params[2];
+    PcgConfig pc;
+    pc.rel_tolerance = params[3];
+    pc.max_iterations = static_cast<int>(params[4]);
+    const int p = s->mesh.vertex_count();
+    double broad_ms = 0.0;
+    const auto tb0 = std::chrono::steady_clock::now();
+    const int64_t dcd = ref_collide_candidates(*s, s->state.x, s->state.x, CollisionMode::Discrete, cp, &broad_ms);
+    const auto tb1 = std::chrono::steady_clock::now();
+    auto system = step_system<double>(*s->engine, s->mesh, s->state, s->material, s->pinned, {}, dt,
+                                      Vec3(0, 0, -9.81), Vec3::Zero());
+    const auto ta = std::chrono::steady_clock::now();
+    DistVector<double> dv(s->engine.get(), system.matrix.partitions);
+    const auto rep = pcg_solve(*s->engine, system.matrix, s->sched, system.rhs, dv, pc);
+    const auto tsol = std::chrono::steady_clock::now();
+    if (!rep.converged) throw SolverError("PCG did not converge (residual " + std::to_string(rep.rel_residual) + ")");
+    const auto dvg = dv.gather();
+    std::vector<Vec3> cand(static_cast<std::size_t>(p));
+    for (int i = 0; i < p; ++i) {
+      for (int c = 0; c < 3; ++c) s->state.v[static_cast<std::size_t>(i)][c] += dvg[static_cast<std::size_t>(3 * i + c)];
+      cand[static_cast<std::size_t>(i)] = s->state.x[static_cast<std::size_t>(i)] + dt * s->state.v[static_cast<std::size_t>(i)];
+    }
+    const auto tc0 = std::chrono::steady_clock::now();
+    const int64_t ccd = ref_collide_candidates(*s, s->state.x, cand, CollisionMode::Continuous, cp, &broad_ms);
+    const auto tc1 = std::chrono::steady_clock::now();
+    s->state.x = std::move(cand);
+    s->state.time += dt;
+    auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+    out[0] = rep.iterations;
+    out[1] = rep.converged ? 1 : 0;
+    out[2] = rep.rel_residual;
+    out[3] = static_cast<double>(dcd);
+    out[4] = static_cast<double>(ccd);
+    out[5] = ms(tb0, tb1) + ms(tc0, tc1);
+    out[6] = ms(tb1, ta);
+    out[7] = ms(ta, tsol);
+    return 0;
+  } catch (const std::exception& e) {
+    return set_error(e);
+  }
+}
+
+void ref_sim_free(void* h) { delete static_cast<RefSim*>(h); }
 
 }  // extern "C"

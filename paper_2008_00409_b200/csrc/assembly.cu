@@ -189,7 +189,7 @@ static void build_incidence(Ctx& c, int64_t first, int64_t count, int64_t code_b
   list.resize(static_cast<size_t>(m) + 1);
   if (count) {
     if ((code_base + count) * 4 > INT32_MAX) throw Error(WEFT_ERR_DIMENSION, "too many elements (> 2^29)");
-    k_inc_emit<<<div_up(count, 256), 256, 0, s>>>(first, count, c.est.data(), c.einfo.data(), c.pinned.data(),
+    k_inc_emit<<<div_up(count, 256), 256, 0, ls(c)>>>(first, count, c.est.data(), c.einfo.data(), c.pinned.data(),
                                                   k1.data(), v1.data(), cnt.data(), code_base);
     WG_CUDA(cudaGetLastError());
     size_t tmp = 0;
@@ -267,7 +267,7 @@ static void build_pattern(Ctx& c, int64_t first, int64_t count, bool with_diag, 
   pc.resize(static_cast<size_t>(count) + 1);
   int64_t npairs = 0;
   if (count) {
-    k_pair_count<<<div_up(count, 256), 256, 0, s>>>(first, count, c.est.data(), c.einfo.data(), c.pinned.data(),
+    k_pair_count<<<div_up(count, 256), 256, 0, ls(c)>>>(first, count, c.est.data(), c.einfo.data(), c.pinned.data(),
                                                     pc.data());
     size_t tmp = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, tmp, pc.data(), pc.data(), count + 1, s);
@@ -283,9 +283,9 @@ static void build_pattern(Ctx& c, int64_t first, int64_t count, bool with_diag, 
   k1.resize(static_cast<size_t>(nk) + 1);
   k2.resize(static_cast<size_t>(nk) + 1);
   if (count)
-    k_pair_emit<<<div_up(count, 256), 256, 0, s>>>(first, count, c.est.data(), c.einfo.data(), c.pinned.data(),
+    k_pair_emit<<<div_up(count, 256), 256, 0, ls(c)>>>(first, count, c.est.data(), c.einfo.data(), c.pinned.data(),
                                                    pc.data(), k1.data());
-  if (with_diag && p) k_diag_keys<<<div_up(p, 256), 256, 0, s>>>(p, k1.data() + npairs);
+  if (with_diag && p) k_diag_keys<<<div_up(p, 256), 256, 0, ls(c)>>>(p, k1.data() + npairs);
   WG_CUDA(cudaGetLastError());
   const int end_bit = 32 + bits_for(p);
   DBuf<int64_t> nsel;
@@ -307,7 +307,7 @@ static void build_pattern(Ctx& c, int64_t first, int64_t count, bool with_diag, 
   cnt.zero(s);
   cols.resize(static_cast<size_t>(nu) + 1);
   ptr.resize(static_cast<size_t>(p) + 1);
-  if (nu) k_key_rows<<<div_up(nu, 256), 256, 0, s>>>(nu, k1.data(), cnt.data(), cols.data());
+  if (nu) k_key_rows<<<div_up(nu, 256), 256, 0, ls(c)>>>(nu, k1.data(), cnt.data(), cols.data());
   size_t tmp = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt.data(), ptr.data(), p + 1, s);
   void* t = scratch(c, tmp);
@@ -433,8 +433,8 @@ static void build_layout(Ctx& c) {
   A.rowlen.resize(static_cast<size_t>(p) + 1);
   A.slice_off.resize(static_cast<size_t>(A.nslices) + 1);
   if (p) {
-    k_merge_len<<<div_up(p, 256), 256, 0, s>>>(p, m, A.rowlen.data());
-    k_slice_width<<<div_up(A.nslices, 256), 256, 0, s>>>(p, A.nslices, A.rowlen.data(), A.slice_off.data());
+    k_merge_len<<<div_up(p, 256), 256, 0, ls(c)>>>(p, m, A.rowlen.data());
+    k_slice_width<<<div_up(A.nslices, 256), 256, 0, ls(c)>>>(p, A.nslices, A.rowlen.data(), A.slice_off.data());
   }
   WG_CUDA(cudaMemsetAsync(A.slice_off.data() + A.nslices, 0, sizeof(int64_t), s));
   size_t tmp = 0;
@@ -465,7 +465,7 @@ static void build_layout(Ctx& c) {
   A.cols.resize(static_cast<size_t>(total) + 1);
   A.vals.resize(9 * static_cast<size_t>(total) + 9);
   if (p)
-    k_merge_fill<<<div_up(p, 256), 256, 0, s>>>(p, m, c.pm, c.go, A.slice_off.data(), A.rowlen.data(), A.cols.data());
+    k_merge_fill<<<div_up(p, 256), 256, 0, ls(c)>>>(p, m, c.pm, c.go, A.slice_off.data(), A.rowlen.data(), A.cols.data());
   WG_CUDA(cudaGetLastError());
   WG_CUDA(cudaStreamSynchronize(s));  // cptr/ccol die here
 }
@@ -671,13 +671,13 @@ void fill_matrix(Ctx& c, const double* xc, const double* xa, const double* vel, 
   f.bad_mass = bad;
   if (c.p) {
     if (!layout_cached)
-      k_zero_padding<<<div_up(c.p, 256), 256, 0, s>>>(c.p, A.slice_off.data(), A.rowlen.data(), A.vals.data(), A.total);
+      k_zero_padding<<<div_up(c.p, 256), 256, 0, ls(c)>>>(c.p, A.slice_off.data(), A.rowlen.data(), A.vals.data(), A.total);
     const size_t smem = static_cast<size_t>(f.wcap) * (9 * sizeof(double) + sizeof(int32_t)) * kFillThreads;
     WG_CUDA(cudaFuncSetAttribute(k_fill<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    k_fill<false><<<div_up(c.p, kFillThreads), kFillThreads, smem, s>>>(f);
+    k_fill<false><<<div_up(c.p, kFillThreads), kFillThreads, smem, ls(c)>>>(f);
     if (A.max_len > kWideCap) {
       // rows wider than the shared-memory budget accumulate in place
-      k_fill<true><<<div_up(c.p, kFillThreads), kFillThreads, 0, s>>>(f);
+      k_fill<true><<<div_up(c.p, kFillThreads), kFillThreads, 0, ls(c)>>>(f);
     }
     WG_CUDA(cudaGetLastError());
   }

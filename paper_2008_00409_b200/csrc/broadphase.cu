@@ -178,13 +178,13 @@ void build_grid(Ctx& c, const double* x0, const double* x1, int mode, double thi
   c.lat.resize(6 * static_cast<size_t>(T) + 6);
   c.ecount.resize(static_cast<size_t>(T) + 1);
   if (T) {
-    k_boxes<<<div_up(T, 256), 256, 0, s>>>(T, c.tris.data(), x0, ccd ? x1 : x0, ccd, inflate, c.box_lo.data(),
+    k_boxes<<<div_up(T, 256), 256, 0, ls(c)>>>(T, c.tris.data(), x0, ccd ? x1 : x0, ccd, inflate, c.box_lo.data(),
                                            c.box_hi.data(), c.diag.data());
   }
-  k_cell_size<<<1, 32, 0, s>>>(T, c.diag.data(), cell_scale, c.cell_size.data());
+  k_cell_size<<<1, 32, 0, ls(c)>>>(T, c.diag.data(), cell_scale, c.cell_size.data());
   WG_CUDA(cudaMemsetAsync(c.ecount.data() + T, 0, sizeof(int64_t), s));
   if (T)
-    k_lattice<<<div_up(T, 256), 256, 0, s>>>(T, c.box_lo.data(), c.box_hi.data(), c.cell_size.data(), c.lat.data(),
+    k_lattice<<<div_up(T, 256), 256, 0, ls(c)>>>(T, c.box_lo.data(), c.box_hi.data(), c.cell_size.data(), c.lat.data(),
                                              c.ecount.data());
   WG_CUDA(cudaGetLastError());
   size_t tmp = 0;
@@ -200,7 +200,7 @@ void build_grid(Ctx& c, const double* x0, const double* x1, int mode, double thi
   c.keys_b.resize(static_cast<size_t>(K) + 1);
   c.vals_a.resize(static_cast<size_t>(K) + 1);
   c.vals_b.resize(static_cast<size_t>(K) + 1);
-  if (T) k_emit<<<div_up(T, 256), 256, 0, s>>>(T, c.lat.data(), c.ecount.data(), c.keys_a.data(), c.vals_a.data());
+  if (T) k_emit<<<div_up(T, 256), 256, 0, ls(c)>>>(T, c.lat.data(), c.ecount.data(), c.keys_a.data(), c.vals_a.data());
   if (K) {
     tmp = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, tmp, c.keys_a.data(), c.keys_b.data(), c.vals_a.data(), c.vals_b.data(),
@@ -211,7 +211,7 @@ void build_grid(Ctx& c, const double* x0, const double* x1, int mode, double thi
   }
   // run-length cells
   c.cell_flag.resize(static_cast<size_t>(K) + 1);
-  if (K) k_cell_flags<<<div_up(K, 256), 256, 0, s>>>(K, c.keys_b.data(), c.cell_flag.data());
+  if (K) k_cell_flags<<<div_up(K, 256), 256, 0, ls(c)>>>(K, c.keys_b.data(), c.cell_flag.data());
   WG_CUDA(cudaMemsetAsync(c.cell_flag.data() + K, 0, sizeof(int32_t), s));
   tmp = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, tmp, c.cell_flag.data(), c.cell_flag.data(), K + 1, s);
@@ -224,9 +224,9 @@ void build_grid(Ctx& c, const double* x0, const double* x1, int mode, double thi
   c.cell_keys.resize(static_cast<size_t>(cells) + 1);
   c.cell_off.resize(static_cast<size_t>(cells) + 1);
   c.wprefix.resize(static_cast<size_t>(cells) + 1);
-  if (K) k_cells<<<div_up(K, 256), 256, 0, s>>>(K, c.keys_b.data(), c.cell_flag.data(), c.cell_keys.data(), c.cell_off.data());
+  if (K) k_cells<<<div_up(K, 256), 256, 0, ls(c)>>>(K, c.keys_b.data(), c.cell_flag.data(), c.cell_keys.data(), c.cell_off.data());
   WG_CUDA(cudaMemcpyAsync(c.cell_off.data() + cells, &K, sizeof(int64_t), cudaMemcpyHostToDevice, s));
-  if (cells) k_pair_counts<<<div_up(cells, 256), 256, 0, s>>>(cells, c.cell_off.data(), c.wprefix.data());
+  if (cells) k_pair_counts<<<div_up(cells, 256), 256, 0, ls(c)>>>(cells, c.cell_off.data(), c.wprefix.data());
   WG_CUDA(cudaMemsetAsync(c.wprefix.data() + cells, 0, sizeof(int64_t), s));
   tmp = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, tmp, c.wprefix.data(), c.wprefix.data(), cells + 1, s);
@@ -340,7 +340,7 @@ int64_t candidates(Ctx& c, int64_t begin, int64_t end, int32_t* pairs_out) {
              c.cell_keys.data(), c.lat.data()};
   c.cand_count.resize(static_cast<size_t>(nthreads) + 1);
   WG_CUDA(cudaMemsetAsync(c.cand_count.data() + nthreads, 0, sizeof(int64_t), s));
-  k_walk_count<<<div_up(nthreads, 256), 256, 0, s>>>(w, nthreads, c.cand_count.data());
+  k_walk_count<<<div_up(nthreads, 256), 256, 0, ls(c)>>>(w, nthreads, c.cand_count.data());
   size_t tmp = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, tmp, c.cand_count.data(), c.cand_count.data(), nthreads + 1, s);
   void* t = scratch(c, tmp);
@@ -349,7 +349,7 @@ int64_t candidates(Ctx& c, int64_t begin, int64_t end, int32_t* pairs_out) {
   WG_CUDA(cudaMemcpyAsync(&n, c.cand_count.data() + nthreads, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
   WG_CUDA(cudaStreamSynchronize(s));
   c.cand_pairs.resize(2 * static_cast<size_t>(n) + 2);
-  k_walk_write<<<div_up(nthreads, 256), 256, 0, s>>>(w, nthreads, c.cand_count.data(), c.cand_pairs.data());
+  k_walk_write<<<div_up(nthreads, 256), 256, 0, ls(c)>>>(w, nthreads, c.cand_count.data(), c.cand_pairs.data());
   WG_CUDA(cudaGetLastError());
   if (pairs_out && n)
     WG_CUDA(cudaMemcpyAsync(pairs_out, c.cand_pairs.data(), 2 * sizeof(int32_t) * n, cudaMemcpyDefault, s));

@@ -264,4 +264,24 @@ weft_status weft_gpu_pcg(weft_gpu_ctx* ctx, const double* b, double* x, const we
   });
 }
 
+weft_status weft_gpu_profile(weft_gpu_ctx* ctx, int32_t enable) {
+  return guard(ctx, [&] {
+    ctx->c.profile = enable != 0;
+    ctx->c.spmv_launches = 0;
+    ctx->c.spmv_ms = 0.0;
+  });
+}
+
+weft_status weft_gpu_stats(weft_gpu_ctx* ctx, weft_gpu_stats_t* out) {
+  return guard(ctx, [&] {
+    out->launches = ctx->c.launches;
+    out->spmv_launches = ctx->c.spmv_launches;
+    out->spmv_ms = ctx->c.spmv_ms;
+  });
+}
+
+weft_status weft_gpu_get_stream(weft_gpu_ctx* ctx, void** stream) {
+  return guard(ctx, [&] { *stream = static_cast<void*>(ctx->c.stream); });
+}
+
 }  // extern "C"

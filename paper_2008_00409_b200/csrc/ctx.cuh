@@ -104,10 +104,23 @@ struct Ctx {
   DBuf<unsigned char> scratch;
   DBuf<int64_t> scalars;  // small device scratch
 
+  // ---- instrumentation
+  int64_t launches = 0;           // kernels of this library launched so far
+  bool profile = false;           // time every PCG SpMV launch with events
+  int64_t spmv_launches = 0;      // PCG SpMV launches timed
+  double spmv_ms = 0.0;           // their summed device time
+  std::vector<cudaEvent_t> prof_ev;
+
   // ---- resident simulation state
   DBuf<double> sim_x, sim_v, sim_xc;
   bool has_state = false;
 };
+
+// Launch-site stream accessor: counts the launch (gpu_launches in bench.py).
+inline cudaStream_t ls(Ctx& c) {
+  ++c.launches;
+  return c.stream;
+}
 
 // ---- entry points implemented across the .cu files
 void set_matrix_csr(Ctx& c, int rows, const int64_t* row_ptr, const int32_t* cols, const double* vals);

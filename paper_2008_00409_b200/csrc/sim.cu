@@ -88,7 +88,7 @@ weft_status weft_gpu_step_system(weft_gpu_ctx* ctx, const double* x, const doubl
     weft_gpu::upload_vec(c, c.vel, v, n);
     c.x_adv.resize(n);
     if (n)
-      weft_gpu::k_advance<<<weft_gpu::div_up(n, 256), 256, 0, c.stream>>>(n, c.x_cur.data(), c.vel.data(), dt,
+      weft_gpu::k_advance<<<weft_gpu::div_up(n, 256), 256, 0, ls(c)>>>(n, c.x_cur.data(), c.vel.data(), dt,
                                                                           c.x_adv.data());
     WG_CUDA(cudaGetLastError());
     weft_gpu::fill_matrix(c, c.x_cur.data(), c.x_adv.data(), c.vel.data(), dt, jac_mode);
@@ -178,7 +178,7 @@ weft_status weft_gpu_sim_step(weft_gpu_ctx* ctx, const weft_sim_params* prm, wef
     WG_CUDA(cudaEventRecord(ev[1], s));
     // 2. assembly of step_system at (x, v)
     c.x_adv.resize(static_cast<size_t>(n));
-    weft_gpu::k_advance<<<weft_gpu::div_up(n, 256), 256, 0, s>>>(n, c.sim_x.data(), c.sim_v.data(), dt,
+    weft_gpu::k_advance<<<weft_gpu::div_up(n, 256), 256, 0, ls(c)>>>(n, c.sim_x.data(), c.sim_v.data(), dt,
                                                                   c.x_adv.data());
     weft_gpu::fill_matrix(c, c.sim_x.data(), c.x_adv.data(), c.sim_v.data(), dt, prm->jac_mode);
     WG_CUDA(cudaEventRecord(ev[2], s));
@@ -189,7 +189,7 @@ weft_status weft_gpu_sim_step(weft_gpu_ctx* ctx, const weft_sim_params* prm, wef
       throw Error(WEFT_ERR_SOLVER, "PCG did not converge (residual " + std::to_string(pr.rel_residual) + ")");
     // 4. candidate update
     if (pr.iterations == 0) WG_CUDA(cudaMemsetAsync(c.xs.data(), 0, n * sizeof(double), s));
-    weft_gpu::k_candidate<<<weft_gpu::div_up(n, 256), 256, 0, s>>>(n, c.sim_x.data(), c.sim_v.data(), c.xs.data(),
+    weft_gpu::k_candidate<<<weft_gpu::div_up(n, 256), 256, 0, ls(c)>>>(n, c.sim_x.data(), c.sim_v.data(), c.xs.data(),
                                                                     dt, c.sim_xc.data());
     WG_CUDA(cudaEventRecord(ev[4], s));
     // 5. impact broad phase (CCD) over begin -> candidate

@@ -145,7 +145,7 @@ void spmv(Ctx& c, const double* x_dev, double* y_dev) {
   if (!c.has_matrix) throw Error(WEFT_ERR_INVALID, "spmv: no matrix loaded");
   const int threads = 256;
   if (c.A.rows == 0) return;
-  k_spmv<<<div_up(c.A.rows, threads), threads, 0, c.stream>>>(view(c.A), c.go.n, x_dev, y_dev);
+  k_spmv<<<div_up(c.A.rows, threads), threads, 0, ls(c)>>>(view(c.A), c.go.n, x_dev, y_dev);
   WG_CUDA(cudaGetLastError());
 }
 
@@ -582,11 +582,11 @@ PcgResult pcg_solve(Ctx& c, const double* b_dev, const weft_pcg_config& cfg, dou
   WG_CUDA(cudaMemcpyAsync(c.pcg, &init, sizeof(init), cudaMemcpyHostToDevice, s));
   double* dots = reinterpret_cast<double*>(c.scalars.data());
   if (rows > 0) {
-    if (bj) k_dinv<<<div_up(rows, threads), threads, 0, s>>>(A, c.dinv.data());
-    k_pcg_init<<<div_up(rows, threads), threads, 0, s>>>(rows, b_dev, c.dinv.data(), bj, c.xs.data(), c.r.data(),
+    if (bj) k_dinv<<<div_up(rows, threads), threads, 0, ls(c)>>>(A, c.dinv.data());
+    k_pcg_init<<<div_up(rows, threads), threads, 0, ls(c)>>>(rows, b_dev, c.dinv.data(), bj, c.xs.data(), c.r.data(),
                                                          c.z.data(), c.pv.data());
     // ||b|| and rho = r.z (r = b)
-    k_dot2<<<nblocks, threads, 0, s>>>(pb, b_dev, b_dev, c.r.data(), c.z.data(), c.partials.data(),
+    k_dot2<<<nblocks, threads, 0, ls(c)>>>(pb, b_dev, b_dev, c.r.data(), c.z.data(), c.partials.data(),
                                        &c.pcg->counter, dots);
     WG_CUDA(cudaGetLastError());
   }
@@ -608,19 +608,37 @@ PcgResult pcg_solve(Ctx& c, const double* b_dev, const weft_pcg_config& cfg, dou
 
   auto* hs = static_cast<PcgState*>(c.pcg_host);
   int chunk = 4;
+  int iter_before = 0;
   for (;;) {
+    if (c.profile && c.prof_ev.size() < 64) {
+      c.prof_ev.resize(64);
+      for (auto& e : c.prof_ev) WG_CUDA(cudaEventCreate(&e));
+    }
     for (int k = 0; k < chunk; ++k) {
-      k_pcg_spmv<<<nblocks, threads, 0, s>>>(A, pb, c.go.n, c.z.data(), c.pv.data(), c.q.data(), c.partials.data(),
+      if (c.profile) WG_CUDA(cudaEventRecord(c.prof_ev[2 * k], s));
+      k_pcg_spmv<<<nblocks, threads, 0, ls(c)>>>(A, pb, c.go.n, c.z.data(), c.pv.data(), c.q.data(), c.partials.data(),
                                              c.pcg);
-      k_pcg_update<<<nblocks, threads, 0, s>>>(pb, c.dinv.data(), bj, c.xs.data(), c.r.data(), c.z.data(),
+      if (c.profile) WG_CUDA(cudaEventRecord(c.prof_ev[2 * k + 1], s));
+      k_pcg_update<<<nblocks, threads, 0, ls(c)>>>(pb, c.dinv.data(), bj, c.xs.data(), c.r.data(), c.z.data(),
                                                c.pv.data(), c.q.data(), c.partials.data(), c.pcg, c.hist.data(),
                                                c.phist.data());
     }
     WG_CUDA(cudaGetLastError());
     WG_CUDA(cudaMemcpyAsync(hs, c.pcg, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
     WG_CUDA(cudaStreamSynchronize(s));
+    if (c.profile) {
+      // Only launches that did work count (kernels early-exit once done).
+      const int worked = std::min(chunk, hs->iter - iter_before);
+      for (int k = 0; k < worked; ++k) {
+        float ms = 0.f;
+        WG_CUDA(cudaEventElapsedTime(&ms, c.prof_ev[2 * k], c.prof_ev[2 * k + 1]));
+        c.spmv_ms += ms;
+        ++c.spmv_launches;
+      }
+    }
+    iter_before = hs->iter;
     if (hs->done) break;
-    chunk = std::min(chunk * 2, 32);
+    chunk = std::min(chunk * 2, 32);  // <= 32 (event pool of 64)
   }
   res.iterations = hs->iter;
   res.converged = hs->converged;

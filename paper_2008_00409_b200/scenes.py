@@ -59,7 +59,7 @@ def grid_tris(nx: int, ny: int, offset: int = 0) -> np.ndarray:
     return (t.reshape(-1, 3) + offset).astype(np.int32)
 
 
-def layered_cloth(layers: int, nx: int, spacing: float = 0.003, seed: int = 20240810, jitter: float = 0.15,
+def layered_cloth(layers: int, nx: int, spacing: float = 0.005, seed: int = 20240810, jitter: float = 0.15,
                   dt: float = 1.0 / 240.0) -> Scene:
     width = spacing * (nx - 1)
     thickness = 0.5 * spacing

@@ -431,3 +431,28 @@ class ClothMesh:
         if getattr(self, "_h", None):
             LIB.weft_mesh_destroy(self._h)
             self._h = None
+
+
+class GpuStats(C.Structure):
+    _fields_ = [("launches", C.c_int64), ("spmv_launches", C.c_int64), ("spmv_ms", C.c_double)]
+
+
+def _engine_profile(self, enable: bool = True):
+    _check(LIB.weft_gpu_profile(self._ctx, C.c_int32(1 if enable else 0)))
+
+
+def _engine_stats(self) -> GpuStats:
+    st = GpuStats()
+    _check(LIB.weft_gpu_stats(self._ctx, C.byref(st)))
+    return st
+
+
+def _engine_stream(self) -> int:
+    s = C.c_void_p()
+    _check(LIB.weft_gpu_get_stream(self._ctx, C.byref(s)))
+    return s.value or 0
+
+
+Engine.profile = _engine_profile
+Engine.stats = _engine_stats
+Engine.stream = _engine_stream

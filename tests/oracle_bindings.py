@@ -398,3 +398,49 @@ class Ref:
 
 ORACLE = Oracle() if os.path.exists(ORACLE_SO) else None
 REF = Ref() if os.path.exists(REF_SO) else None
+
+
+class RefSim:
+    """The reference's hot-path step (oracle/ref_harness.cpp ref_sim_*)."""
+
+    def __init__(self, ref: Ref, verts, tris, pinned, density, material, devices):
+        L = ref.lib
+        L.ref_sim_create.restype = C.c_void_p
+        L.ref_sim_step.restype = C.c_int32
+        for name in ("ref_sim_set_state", "ref_sim_get_state", "ref_sim_step", "ref_sim_free"):
+            getattr(L, name).argtypes = None
+        self.ref = ref
+        v = np.ascontiguousarray(verts, np.float64).reshape(-1)
+        t = np.ascontiguousarray(tris, np.int32).reshape(-1)
+        mat = np.array(material, np.float64)
+        self.p = len(v) // 3
+        self.h = L.ref_sim_create(C.c_int32(self.p), ptr(v), C.c_int32(len(t) // 3), ptr(t),
+                                  ptr(np.ascontiguousarray(pinned, np.uint8)), C.c_double(density), ptr(mat),
+                                  C.c_int32(devices))
+        if not self.h:
+            raise RuntimeError(L.ref_last_error().decode())
+
+    def set_state(self, x, v):
+        self.ref.lib.ref_sim_set_state(C.c_void_p(self.h), ptr(np.ascontiguousarray(x, np.float64)),
+                                       ptr(np.ascontiguousarray(v, np.float64)))
+
+    def get_state(self):
+        x = np.zeros(3 * self.p)
+        v = np.zeros(3 * self.p)
+        self.ref.lib.ref_sim_get_state(C.c_void_p(self.h), ptr(x), ptr(v))
+        return x, v
+
+    def step(self, dt, thickness, cell_scale=1.5, tol=1e-4, max_it=400):
+        prm = np.array([dt, thickness, cell_scale, tol, max_it], np.float64)
+        out = np.zeros(8)
+        st = self.ref.lib.ref_sim_step(C.c_void_p(self.h), ptr(prm), ptr(out))
+        if st:
+            raise RuntimeError(self.ref.lib.ref_last_error().decode())
+        keys = ("pcg_iterations", "pcg_converged", "pcg_residual", "dcd_candidates", "ccd_candidates", "ms_broad",
+                "ms_assemble", "ms_solve")
+        return dict(zip(keys, out.tolist()))
+
+    def close(self):
+        if self.h:
+            self.ref.lib.ref_sim_free(C.c_void_p(self.h))
+            self.h = None

@@ -138,8 +138,9 @@ def test_assembly_errors(weft):
         eng.fill_matrix(np.zeros(3), np.zeros(3), np.zeros(3), 0.01)
     with pytest.raises(weft.DimensionError, match="dt must be positive"):
         eng.fill_matrix(np.zeros(3), np.zeros(3), np.zeros(3), 0.0)
-    bad = ce(np.random.default_rng(0), 1, 1)
-    bad["stencil"][0, 0] = 7
+    bad = ce(np.random.default_rng(0), 8, 1)
+    bad["stencil_size"] = 1
+    bad["stencil"][0] = [7, -1, -1, -1]
     with pytest.raises(weft.DimensionError, match="stencil vertex 7 outside all partitions"):
         eng.set_elements(bad)
     eng.close()
