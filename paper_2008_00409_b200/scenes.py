@@ -60,7 +60,7 @@ def grid_tris(nx: int, ny: int, offset: int = 0) -> np.ndarray:
 
 
 def layered_cloth(layers: int, nx: int, spacing: float = 0.005, seed: int = 20240810, jitter: float = 0.15,
-                  dt: float = 1.0 / 240.0) -> Scene:
+                  dt: float = 1.0 / 240.0, hanging: bool = True) -> Scene:
     width = spacing * (nx - 1)
     thickness = 0.5 * spacing
     dz = 1.5 * thickness
@@ -68,10 +68,12 @@ def layered_cloth(layers: int, nx: int, spacing: float = 0.005, seed: int = 2024
     gi, gj = np.meshgrid(np.arange(nx), np.arange(nx), indexing="xy")
     base = np.stack([width * gi.reshape(-1) / (nx - 1), width * gj.reshape(-1) / (nx - 1),
                      np.zeros(nx * nx)], 1)
+    if hanging:  # sheet in the x-z plane, grid row j = nx-1 on top (pinned), layers stacked along y
+        base = base[:, [0, 2, 1]]
     verts, tris, pinned = [], [], []
     for k in range(layers):
         v = base.copy()
-        v[:, 2] = k * dz
+        v[:, 1 if hanging else 2] = k * dz
         v += rng.uniform(-jitter * spacing, jitter * spacing, v.shape)
         verts.append(v)
         tris.append(grid_tris(nx, nx, k * nx * nx))

@@ -16,7 +16,7 @@ def weft():
     return w
 
 
-@pytest.mark.parametrize("layers,nx,steps,tol", [(1, 24, 6, 1e-10), (3, 16, 5, 1e-10), (2, 20, 4, 1e-4)])
+@pytest.mark.parametrize("layers,nx,steps,tol", [(1, 24, 6, 1e-9), (3, 16, 5, 1e-9), (2, 20, 4, 1e-4)])
 def test_sim_steps_match_reference(weft, layers, nx, steps, tol):
     from paper_2008_00409_b200 import scenes
     sc = scenes.layered_cloth(layers, nx, seed=3)
@@ -29,10 +29,10 @@ def test_sim_steps_match_reference(weft, layers, nx, steps, tol):
     x0 = sc.verts.reshape(-1).copy()
     eng.sim_set_state(x0, np.zeros_like(x0))
     ref = RefSim(REF, sc.verts, sc.tris, sc.pinned, sc.density, sc.material, 2)
-    params = weft.SimParams(sc.dt, sc.thickness, 1.5, weft.PcgConfig(tol, 400), weft.JAC_SPD)
+    params = weft.SimParams(sc.dt, sc.thickness, 1.5, weft.PcgConfig(tol, 3000), weft.JAC_SPD)
     for k in range(steps):
         rg = eng.sim_step(params)
-        rr = ref.step(sc.dt, sc.thickness, tol=tol)
+        rr = ref.step(sc.dt, sc.thickness, tol=tol, max_it=3000)
         if k == 0:
             assert rg.dcd_candidates == rr["dcd_candidates"]
         assert abs(rg.pcg_iterations - rr["pcg_iterations"]) <= 2
