@@ -91,23 +91,167 @@ __global__ void k_boxes(int ntris, const int32_t* __restrict__ tris, const doubl
 }
 
 // cell = max(cell_scale * (sum_t diag_t) / T, 1e-9) with the sum taken
-// strictly left to right (collision.cpp:124-133). One warp: coalesced
-// 32-wide loads, the dependent add chain evaluated uniformly on all lanes.
-__global__ void k_cell_size(int ntris, const double* __restrict__ diag, double cell_scale, double* __restrict__ out) {
-  const int lane = threadIdx.x;
-  double sum = 0.0;
-  double next = lane < ntris ? diag[lane] : 0.0;
-  for (int base = 0; base < ntris; base += 32) {
-    const double cur = next;
-    if (base + 32 + lane < ntris) next = __ldg(diag + base + 32 + lane);
-    const int cnt = min(32, ntris - base);
-    for (int j = 0; j < cnt; ++j) sum = sum + __shfl_sync(0xffffffffu, cur, j);
+// strictly left to right (collision.cpp:124-133), reproduced EXACTLY but
+// in parallel. While the running sum s stays inside one binade [2^e,
+// 2^(e+1)) every double is an integer multiple M of u = 2^(e-52), and
+// fl(s + d) = (M + round(d / u)) u: the rounding of each term is
+// independent of s except for exact ties, which round the result to an
+// even M. Each term is therefore a map M -> M + a[M mod 2] (a0 = a1 unless
+// d/u is a tie); such maps compose associatively, so one CTA scans a window
+// of 16K terms at a time, advances s by the exact composed offset up to the
+// first term whose partial sum would leave the binade, adds that term with a
+// plain IEEE add, and continues. Cost: (terms / 16K + binade crossings)
+// block scans instead of one dependent add per triangle.
+struct ParityMap {
+  long long a0, a1;  // offset applied when the running integer is even / odd
+};
+
+__device__ __forceinline__ ParityMap compose(ParityMap f, ParityMap g) {  // f, then g
+  ParityMap r;
+  r.a0 = f.a0 + ((f.a0 & 1) ? g.a1 : g.a0);
+  r.a1 = f.a1 + (((1 + f.a1) & 1) ? g.a1 : g.a0);
+  return r;
+}
+
+constexpr int kSumThreads = 1024;
+constexpr int kSumItems = 16;
+constexpr long long kTwo53 = 1LL << 53;
+
+__global__ void __launch_bounds__(kSumThreads) k_cell_size(int ntris, const double* __restrict__ diag,
+                                                           double cell_scale, double* __restrict__ out) {
+  extern __shared__ double sm_d[];  // kSumThreads * kSumItems terms
+  __shared__ ParityMap sm_warp[32];
+  __shared__ int sm_event;
+  __shared__ long long sm_M;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double s = 0.0;  // uniform across the block
+  int k = 0;
+  while (k < ntris) {
+    if (s == 0.0 || !(s >= 0x1p-1000) || !isfinite(s)) {
+      // start, tiny or non-finite running sums: plain serial adds
+      s = s + diag[k];
+      ++k;
+      if (!isfinite(s)) {
+        for (; k < ntris; ++k) s = s + diag[k];
+      }
+      continue;
+    }
+    const int e = ilogb(s);
+    const double inv_u = ldexp(1.0, 52 - e);
+    const long long ms = static_cast<long long>(s * inv_u);  // exact: s = ms * u
+    const int len = min(kSumThreads * kSumItems, ntris - k);
+    for (int i = tid; i < len; i += kSumThreads) sm_d[i] = diag[k + i];
+    if (tid == 0) sm_event = len;
+    __syncthreads();
+    // per-thread maps over its contiguous items
+    ParityMap loc[kSumItems];
+    ParityMap acc{0, 0};
+#pragma unroll
+    for (int i = 0; i < kSumItems; ++i) {
+      const int j = tid * kSumItems + i;
+      ParityMap m{0, 0};
+      if (j < len) {
+        const double x = sm_d[j] * inv_u;  // exact power-of-two scaling
+        if (!(x < 0x1p53)) {
+          m.a0 = m.a1 = kTwo53;  // certainly leaves the binade
+        } else {
+          const double fl = floor(x);
+          const double fr = x - fl;
+          const long long f = static_cast<long long>(fl);
+          if (fr < 0.5) m.a0 = m.a1 = f;
+          else if (fr > 0.5) m.a0 = m.a1 = f + 1;
+          else {  // tie: round the result to an even integer
+            m.a0 = f + (f & 1);
+            m.a1 = f + ((1 + f) & 1);
+          }
+        }
+      }
+      acc = compose(acc, m);
+      loc[i] = acc;  // thread-local inclusive prefix
+    }
+    // block exclusive scan of the per-thread maps (ordered composition)
+    ParityMap incl = acc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      ParityMap other;
+      other.a0 = __shfl_up_sync(0xffffffffu, incl.a0, o);
+      other.a1 = __shfl_up_sync(0xffffffffu, incl.a1, o);
+      if (lane >= o) incl = compose(other, incl);
+    }
+    if (lane == 31) sm_warp[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      ParityMap w = sm_warp[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        ParityMap other;
+        other.a0 = __shfl_up_sync(0xffffffffu, w.a0, o);
+        other.a1 = __shfl_up_sync(0xffffffffu, w.a1, o);
+        if (lane >= o) w = compose(other, w);
+      }
+      sm_warp[lane] = w;  // inclusive over warps
+    }
+    __syncthreads();
+    ParityMap excl{0, 0};
+    {
+      ParityMap lane_excl;
+      lane_excl.a0 = __shfl_up_sync(0xffffffffu, incl.a0, 1);
+      lane_excl.a1 = __shfl_up_sync(0xffffffffu, incl.a1, 1);
+      if (lane == 0) lane_excl = ParityMap{0, 0};
+      const ParityMap wp = warp > 0 ? sm_warp[warp - 1] : ParityMap{0, 0};
+      excl = compose(wp, lane_excl);
+    }
+    // first term whose running integer reaches 2^53 (binade exit)
+    const int p0 = static_cast<int>(ms & 1);
+    int first = len;
+#pragma unroll
+    for (int i = 0; i < kSumItems; ++i) {
+      const int j = tid * kSumItems + i;
+      if (j < len) {
+        const ParityMap t = compose(excl, loc[i]);
+        const long long M = ms + (p0 ? t.a1 : t.a0);
+        if (M >= kTwo53 && j < first) first = j;
+      }
+    }
+    if (first < len) atomicMin(&sm_event, first);
+    __syncthreads();
+    const int m = sm_event;
+    if (m > 0) {
+      // state after m terms: owned by the thread holding term m-1
+      const int owner = (m - 1) / kSumItems;
+      if (tid == owner) {
+        const ParityMap t = compose(excl, loc[(m - 1) % kSumItems]);
+        sm_M = ms + (p0 ? t.a1 : t.a0);
+      }
+      __syncthreads();
+      s = ldexp(static_cast<double>(sm_M), e - 52);
+    }
+    k += m;
+    if (m < len) {  // the binade-exit term: plain IEEE add
+      s = s + sm_d[m];
+      ++k;
+    }
+    __syncthreads();
   }
-  if (lane == 0) {
-    const double mean = ntris > 0 ? sum / ntris : 1.0;
+  if (tid == 0) {
+    const double mean = ntris > 0 ? s / ntris : 1.0;
     const double a = cell_scale * mean;
     out[0] = (a < 1e-9) ? 1e-9 : a;  // std::max(a, 1e-9)
   }
+}
+
+constexpr size_t kSumSmem = sizeof(double) * kSumThreads * kSumItems;
+
+static void launch_cell_size(Ctx& c, int n, const double* d, double scale, double* out) {
+  WG_CUDA(cudaFuncSetAttribute(k_cell_size, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSumSmem));
+  k_cell_size<<<1, kSumThreads, kSumSmem, ls(c)>>>(n, d, scale, out);
+}
+
+// Reference serial sum (validation only: weft_gpu_serial_sum).
+__global__ void k_serial_sum_naive(int n, const double* __restrict__ d, double* __restrict__ out) {
+  double s = 0.0;
+  for (int i = 0; i < n; ++i) s = s + d[i];
+  out[0] = s;
 }
 
 __global__ void k_lattice(int ntris, const double* __restrict__ lo, const double* __restrict__ hi,
@@ -181,7 +325,7 @@ void build_grid(Ctx& c, const double* x0, const double* x1, int mode, double thi
     k_boxes<<<div_up(T, 256), 256, 0, ls(c)>>>(T, c.tris.data(), x0, ccd ? x1 : x0, ccd, inflate, c.box_lo.data(),
                                            c.box_hi.data(), c.diag.data());
   }
-  k_cell_size<<<1, 32, 0, ls(c)>>>(T, c.diag.data(), cell_scale, c.cell_size.data());
+  launch_cell_size(c, T, c.diag.data(), cell_scale, c.cell_size.data());
   WG_CUDA(cudaMemsetAsync(c.ecount.data() + T, 0, sizeof(int64_t), s));
   if (T)
     k_lattice<<<div_up(T, 256), 256, 0, ls(c)>>>(T, c.box_lo.data(), c.box_hi.data(), c.cell_size.data(), c.lat.data(),
@@ -355,6 +499,21 @@ int64_t candidates(Ctx& c, int64_t begin, int64_t end, int32_t* pairs_out) {
     WG_CUDA(cudaMemcpyAsync(pairs_out, c.cand_pairs.data(), 2 * sizeof(int32_t) * n, cudaMemcpyDefault, s));
   WG_CUDA(cudaStreamSynchronize(s));
   return n;
+}
+
+// Test hook: exact parallel serial-order sum vs a one-thread serial loop.
+void serial_sum(Ctx& c, int n, const double* d_host, double* exact, double* naive) {
+  DBuf<double> d, o;
+  d.upload(d_host, static_cast<size_t>(n), c.stream);
+  o.resize(2);
+  launch_cell_size(c, n, d.data(), 1.0, o.data());  // cell = max(sum / n, 1e-9)
+  k_serial_sum_naive<<<1, 1, 0, ls(c)>>>(n, d.data(), o.data() + 1);
+  WG_CUDA(cudaGetLastError());
+  double h[2];
+  WG_CUDA(cudaMemcpyAsync(h, o.data(), sizeof(h), cudaMemcpyDeviceToHost, c.stream));
+  WG_CUDA(cudaStreamSynchronize(c.stream));
+  *exact = h[0];
+  *naive = h[1];
 }
 
 }  // namespace weft_gpu

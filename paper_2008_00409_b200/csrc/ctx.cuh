@@ -144,6 +144,8 @@ void set_soup(Ctx& c, int verts, int ntris, const int32_t* tris);
 void build_grid(Ctx& c, const double* x0_dev, const double* x1_dev, int mode, double thickness, double cell_scale);
 int64_t candidates(Ctx& c, int64_t begin, int64_t end, int32_t* pairs_dev_or_null);
 
+void serial_sum(Ctx& c, int n, const double* d_host, double* exact, double* naive);
+
 // CUB scratch helper
 void* scratch(Ctx& c, size_t bytes);
 

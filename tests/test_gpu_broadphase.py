@@ -81,3 +81,54 @@ def test_hot_cell_and_single_triangle(weft):
         eng.set_soup(3, np.array([[0, 1, 2]], np.int32))
         eng.build_grid(np.array([0, 0, 0, 0.1, 0, 0, 0, 0.1, 0.0]))
         assert eng.grid_info().total == 0 and len(eng.candidates()) == 0
+
+
+def _serial(d):
+    s = 0.0
+    for v in d.tolist():
+        s += v
+    return s
+
+
+@pytest.mark.parametrize("case", ["uniform", "equal_third", "equal_binary", "few_bits", "logwide", "zeros", "tiny",
+                                  "nan", "sizes"])
+def test_exact_serial_sum(weft, case):
+    import ctypes as C
+    rng = np.random.default_rng(7)
+    n = 1_650_000
+    if case == "uniform":
+        ds = [rng.uniform(0, 0.02, n)]
+    elif case == "equal_third":
+        ds = [np.full(n, 1.0 / 3.0)]
+    elif case == "equal_binary":
+        ds = [np.full(n, 0.0125), np.full(300_000, 0.5)]
+    elif case == "few_bits":
+        ds = [rng.integers(0, 64, n) * 2.0 ** -10, rng.integers(0, 3, 200_000) * 0.75]
+    elif case == "logwide":
+        ds = [10.0 ** rng.uniform(-10, 10, 200_000)]
+    elif case == "zeros":
+        d = rng.uniform(0, 1, 100_000)
+        d[:5000] = 0.0
+        d[50_000:60_000] = 0.0
+        ds = [d]
+    elif case == "tiny":
+        ds = [rng.uniform(0, 1e-305, 50_000), np.concatenate([np.full(100, 5e-324), rng.uniform(0, 1, 1000)])]
+    elif case == "nan":
+        d = rng.uniform(0, 1, 40_000)
+        d[20_000] = np.nan
+        e = rng.uniform(0, 1, 40_000)
+        e[30_000] = np.inf
+        ds = [d, e]
+    else:
+        ds = [rng.uniform(0, 1, m) for m in (0, 1, 2, 31, 33, 16383, 16384, 16385, 50_000)]
+    with weft.Engine(1) as eng:
+        for d in ds:
+            d = np.ascontiguousarray(d, np.float64)
+            me, sn = C.c_double(), C.c_double()
+            assert weft.LIB.weft_gpu_test_serial_sum(eng._ctx, C.c_int32(len(d)), d.ctypes.data_as(C.c_void_p),
+                                                      C.byref(me), C.byref(sn)) == 0
+            s = _serial(d)
+            assert (sn.value == s) or (np.isnan(sn.value) and np.isnan(s))
+            mean = s / len(d) if len(d) else 1.0
+            want = 1e-9 if mean < 1e-9 else mean
+            assert (me.value == want) or (np.isnan(me.value) and np.isnan(want)), (len(d), me.value, want)
