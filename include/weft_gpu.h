@@ -287,9 +287,10 @@ weft_status weft_gpu_profile(weft_gpu_ctx* ctx, int32_t enable);
 weft_status weft_gpu_stats(weft_gpu_ctx* ctx, weft_gpu_stats_t* out);
 /* Test hook for the exact serial-order sum behind build_grid's cell size
  * (collision.cpp:124-133): mean_exact = max(sum/n, 1e-9) from the parallel
- * exact kernel, sum_naive = the same sum by one GPU thread, left to right. */
-weft_status weft_gpu_test_serial_sum(weft_gpu_ctx* ctx, int32_t n, const double* d, double* mean_exact,
-                                     double* sum_naive);
+ * exact kernel (fast = 1: chunk-map fast path, 0: window scan only),
+ * sum_naive = the same sum by one GPU thread, left to right. */
+weft_status weft_gpu_test_serial_sum(weft_gpu_ctx* ctx, int32_t n, const double* d, int32_t fast,
+                                     double* mean_exact, double* sum_naive);
 /* The cudaStream_t all of the context's work is issued on. */
 weft_status weft_gpu_get_stream(weft_gpu_ctx* ctx, void** stream);
 

@@ -514,7 +514,7 @@ struct Acc {
   }
 };
 
-template <bool Wide>
+template <bool Wide, bool Exact>
 __global__ void __launch_bounds__(64) k_fill(FillArgs f) {
   extern __shared__ double smem[];
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
@@ -565,39 +565,41 @@ __global__ void __launch_bounds__(64) k_fill(FillArgs f) {
       const int kind = info.x & 0xff, ss = (info.x >> 8) & 0xff;
       const double damping = f.edamp[e];
       const int st[4] = {s4.x, s4.y, s4.z, s4.w};
-      RowEval ev;
-      eval_row(kind, ss, st, f.epay + info.y, a, f.xc, f.xa, f.vel, f.exact, ev);
-      // rhs (assembly.hpp:185-197)
-      double fx = ev.f[0], fy = ev.f[1], fz = ev.f[2];
+      const double scale = dt * dt + damping * dt;
+      const double nscale = -scale;
+      double fv[3];
+      double mv[4][3];  // J_ab v_b per stencil slot, for the damping term
+      eval_row<Exact>(kind, ss, st, f.epay + info.y, a, f.xc, f.xa, f.vel, fv,
+               [&](int b, const double* J, const double* D, bool add) {
+                 if (damping > 0.0) {
+                   const V3 vb = ld3(f.vel, st[b]);
+                   mv[b][0] = (J[0] * vb.x + J[1] * vb.y) + J[2] * vb.z;
+                   mv[b][1] = (J[3] * vb.x + J[4] * vb.y) + J[5] * vb.z;
+                   mv[b][2] = (J[6] * vb.x + J[7] * vb.y) + J[8] * vb.z;
+                 }
+                 const int col = st[b];
+                 if (!add || f.pinned[col]) return;
+                 const int slot = find(col);
+#pragma unroll
+                 for (int q = 0; q < 9; ++q) {
+                   double cv = nscale * J[q];
+                   if (D) cv = cv + dt * D[q];
+                   acc.at(slot, q) = acc.at(slot, q) + cv;
+                 }
+               });
+      // rhs (assembly.hpp:185-197): f = force + friction, then the damping
+      // products in ascending b, then rhs += dt f.
+      double fx = fv[0], fy = fv[1], fz = fv[2];
       if (damping > 0.0) {
         for (int b = 0; b < ss; ++b) {
-          const V3 vb = ld3(f.vel, st[b]);
-          const double* M = ev.J[b];
-          const double m0 = (M[0] * vb.x + M[1] * vb.y) + M[2] * vb.z;
-          const double m1 = (M[3] * vb.x + M[4] * vb.y) + M[5] * vb.z;
-          const double m2 = (M[6] * vb.x + M[7] * vb.y) + M[8] * vb.z;
-          fx = fx + damping * m0;
-          fy = fy + damping * m1;
-          fz = fz + damping * m2;
+          fx = fx + damping * mv[b][0];
+          fy = fy + damping * mv[b][1];
+          fz = fz + damping * mv[b][2];
         }
       }
       r0 = r0 + dt * fx;
       r1 = r1 + dt * fy;
       r2 = r2 + dt * fz;
-      // matrix (assembly.hpp:199-215)
-      const double scale = dt * dt + damping * dt;
-      const double nscale = -scale;
-      for (int b = 0; b < ss; ++b) {
-        const int col = st[b];
-        if (f.pinned[col]) continue;
-        const int slot = find(col);
-#pragma unroll
-        for (int q = 0; q < 9; ++q) {
-          double cv = nscale * ev.J[b][q];
-          if (ev.damped) cv = cv + dt * ev.D[b][q];
-          acc.at(slot, q) = acc.at(slot, q) + cv;
-        }
-      }
     }
   }
   f.rhs[3 * r] = r0;
@@ -673,11 +675,13 @@ void fill_matrix(Ctx& c, const double* xc, const double* xa, const double* vel, 
     if (!layout_cached)
       k_zero_padding<<<div_up(c.p, 256), 256, 0, ls(c)>>>(c.p, A.slice_off.data(), A.rowlen.data(), A.vals.data(), A.total);
     const size_t smem = static_cast<size_t>(f.wcap) * (9 * sizeof(double) + sizeof(int32_t)) * kFillThreads;
-    WG_CUDA(cudaFuncSetAttribute(k_fill<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    k_fill<false><<<div_up(c.p, kFillThreads), kFillThreads, smem, ls(c)>>>(f);
+    auto narrow = f.exact ? k_fill<false, true> : k_fill<false, false>;
+    auto wide = f.exact ? k_fill<true, true> : k_fill<true, false>;
+    WG_CUDA(cudaFuncSetAttribute(narrow, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    narrow<<<div_up(c.p, kFillThreads), kFillThreads, smem, ls(c)>>>(f);
     if (A.max_len > kWideCap) {
       // rows wider than the shared-memory budget accumulate in place
-      k_fill<true><<<div_up(c.p, kFillThreads), kFillThreads, 0, ls(c)>>>(f);
+      wide<<<div_up(c.p, kFillThreads), kFillThreads, 0, ls(c)>>>(f);
     }
     WG_CUDA(cudaGetLastError());
   }

@@ -21,6 +21,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <climits>
 #include <cmath>
 
 #include "ctx.cuh"
@@ -115,61 +116,72 @@ __device__ __forceinline__ ParityMap compose(ParityMap f, ParityMap g) {  // f, 
 
 constexpr int kSumThreads = 1024;
 constexpr int kSumItems = 16;
+constexpr int kSumChunk = kSumThreads * kSumItems;
 constexpr long long kTwo53 = 1LL << 53;
 
-__global__ void __launch_bounds__(kSumThreads) k_cell_size(int ntris, const double* __restrict__ diag,
-                                                           double cell_scale, double* __restrict__ out) {
-  extern __shared__ double sm_d[];  // kSumThreads * kSumItems terms
-  __shared__ ParityMap sm_warp[32];
-  __shared__ int sm_event;
-  __shared__ long long sm_M;
+// Parity map of one term d in the binade with 1/u = inv_u.
+__device__ __forceinline__ ParityMap term_map(double d, double inv_u, bool& huge) {
+  ParityMap m;
+  const double x = d * inv_u;  // exact power-of-two scaling
+  if (!(x < 0x1p53)) {
+    m.a0 = m.a1 = kTwo53;  // certainly leaves the binade
+    huge = true;
+  } else {
+    const double fl = floor(x);
+    const double fr = x - fl;
+    const long long f = static_cast<long long>(fl);
+    if (fr < 0.5) m.a0 = m.a1 = f;
+    else if (fr > 0.5) m.a0 = m.a1 = f + 1;
+    else {  // tie: round the result to an even integer
+      m.a0 = f + (f & 1);
+      m.a1 = f + ((1 + f) & 1);
+    }
+  }
+  return m;
+}
+
+// Processes terms [k, kend) into the uniform running sum s with the
+// window scan (exact). Must be called by all threads of the block.
+__device__ void sum_range(const double* __restrict__ diag, int k, const int kend, double& s, double* sm_d,
+                          ParityMap* sm_warp, int* sm_event, long long* sm_M) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  double s = 0.0;  // uniform across the block
-  int k = 0;
-  while (k < ntris) {
+  while (k < kend) {
     if (s == 0.0 || !(s >= 0x1p-1000) || !isfinite(s)) {
       // start, tiny or non-finite running sums: plain serial adds
       s = s + diag[k];
       ++k;
       if (!isfinite(s)) {
-        for (; k < ntris; ++k) s = s + diag[k];
+        for (; k < kend; ++k) s = s + diag[k];
       }
       continue;
     }
     const int e = ilogb(s);
     const double inv_u = ldexp(1.0, 52 - e);
     const long long ms = static_cast<long long>(s * inv_u);  // exact: s = ms * u
-    const int len = min(kSumThreads * kSumItems, ntris - k);
-    for (int i = tid; i < len; i += kSumThreads) sm_d[i] = diag[k + i];
-    if (tid == 0) sm_event = len;
+    const int len = min(kSumChunk, kend - k);
+    {
+      double r[kSumItems];
+#pragma unroll
+      for (int i = 0; i < kSumItems; ++i) {
+        const int j = tid + i * kSumThreads;
+        r[i] = j < len ? __ldcg(diag + k + j) : 0.0;
+      }
+#pragma unroll
+      for (int i = 0; i < kSumItems; ++i) sm_d[tid + i * kSumThreads] = r[i];
+    }
+    if (tid == 0) *sm_event = len;
     __syncthreads();
-    // per-thread maps over its contiguous items
     ParityMap loc[kSumItems];
     ParityMap acc{0, 0};
 #pragma unroll
     for (int i = 0; i < kSumItems; ++i) {
       const int j = tid * kSumItems + i;
       ParityMap m{0, 0};
-      if (j < len) {
-        const double x = sm_d[j] * inv_u;  // exact power-of-two scaling
-        if (!(x < 0x1p53)) {
-          m.a0 = m.a1 = kTwo53;  // certainly leaves the binade
-        } else {
-          const double fl = floor(x);
-          const double fr = x - fl;
-          const long long f = static_cast<long long>(fl);
-          if (fr < 0.5) m.a0 = m.a1 = f;
-          else if (fr > 0.5) m.a0 = m.a1 = f + 1;
-          else {  // tie: round the result to an even integer
-            m.a0 = f + (f & 1);
-            m.a1 = f + ((1 + f) & 1);
-          }
-        }
-      }
+      bool huge = false;
+      if (j < len) m = term_map(sm_d[j], inv_u, huge);
       acc = compose(acc, m);
-      loc[i] = acc;  // thread-local inclusive prefix
+      loc[i] = acc;
     }
-    // block exclusive scan of the per-thread maps (ordered composition)
     ParityMap incl = acc;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -189,19 +201,14 @@ __global__ void __launch_bounds__(kSumThreads) k_cell_size(int ntris, const doub
         other.a1 = __shfl_up_sync(0xffffffffu, w.a1, o);
         if (lane >= o) w = compose(other, w);
       }
-      sm_warp[lane] = w;  // inclusive over warps
+      sm_warp[lane] = w;
     }
     __syncthreads();
-    ParityMap excl{0, 0};
-    {
-      ParityMap lane_excl;
-      lane_excl.a0 = __shfl_up_sync(0xffffffffu, incl.a0, 1);
-      lane_excl.a1 = __shfl_up_sync(0xffffffffu, incl.a1, 1);
-      if (lane == 0) lane_excl = ParityMap{0, 0};
-      const ParityMap wp = warp > 0 ? sm_warp[warp - 1] : ParityMap{0, 0};
-      excl = compose(wp, lane_excl);
-    }
-    // first term whose running integer reaches 2^53 (binade exit)
+    ParityMap lane_excl;
+    lane_excl.a0 = __shfl_up_sync(0xffffffffu, incl.a0, 1);
+    lane_excl.a1 = __shfl_up_sync(0xffffffffu, incl.a1, 1);
+    if (lane == 0) lane_excl = ParityMap{0, 0};
+    const ParityMap excl = compose(warp > 0 ? sm_warp[warp - 1] : ParityMap{0, 0}, lane_excl);
     const int p0 = static_cast<int>(ms & 1);
     int first = len;
 #pragma unroll
@@ -213,18 +220,17 @@ __global__ void __launch_bounds__(kSumThreads) k_cell_size(int ntris, const doub
         if (M >= kTwo53 && j < first) first = j;
       }
     }
-    if (first < len) atomicMin(&sm_event, first);
+    if (first < len) atomicMin(sm_event, first);
     __syncthreads();
-    const int m = sm_event;
+    const int m = *sm_event;
     if (m > 0) {
-      // state after m terms: owned by the thread holding term m-1
       const int owner = (m - 1) / kSumItems;
       if (tid == owner) {
         const ParityMap t = compose(excl, loc[(m - 1) % kSumItems]);
-        sm_M = ms + (p0 ? t.a1 : t.a0);
+        *sm_M = ms + (p0 ? t.a1 : t.a0);
       }
       __syncthreads();
-      s = ldexp(static_cast<double>(sm_M), e - 52);
+      s = ldexp(static_cast<double>(*sm_M), e - 52);
     }
     k += m;
     if (m < len) {  // the binade-exit term: plain IEEE add
@@ -233,18 +239,112 @@ __global__ void __launch_bounds__(kSumThreads) k_cell_size(int ntris, const doub
     }
     __syncthreads();
   }
+}
+
+// Fast path, pass 1: approximate chunk sums (any order; only used to
+// predict the binade the exact running sum will be in at each chunk).
+__global__ void __launch_bounds__(256) k_chunk_approx(int n, const double* __restrict__ d, double* __restrict__ approx) {
+  __shared__ double sm[8];
+  const int c = blockIdx.x;
+  const int k0 = c * kSumChunk, k1 = min(n, k0 + kSumChunk);
+  double v = 0.0;
+  for (int i = k0 + threadIdx.x; i < k1; i += blockDim.x) v += d[i];
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < 8; ++w) t += sm[w];
+    approx[c] = t;
+  }
+}
+
+struct ChunkMap {
+  long long a0, a1;
+  int e;
+  int ok;
+};
+
+// Fast path, pass 2: each chunk's composed parity map in the binade
+// predicted from the approximate prefix.
+__global__ void __launch_bounds__(kSumThreads) k_chunk_maps(int n, const double* __restrict__ d,
+                                                            const double* __restrict__ approx,
+                                                            ChunkMap* __restrict__ maps) {
+  __shared__ double sm_r[32];
+  __shared__ ParityMap sm_w[32];
+  __shared__ int sm_huge;
+  const int c = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double pre = 0.0;
+  for (int i = tid; i < c; i += kSumThreads) pre += approx[i];
+  for (int o = 16; o > 0; o >>= 1) pre += __shfl_xor_sync(0xffffffffu, pre, o);
+  if (lane == 0) sm_r[warp] = pre;
+  if (tid == 0) sm_huge = 0;
+  __syncthreads();
+  double start = 0.0;
+  for (int w = 0; w < 32; ++w) start += sm_r[w];
+  const bool usable = start > 0x1p-1000 && isfinite(start);
+  const int e = usable ? ilogb(start) : 0;
+  const double inv_u = ldexp(1.0, 52 - e);
+  const int k0 = c * kSumChunk;
+  const int len = min(kSumChunk, n - k0);
+  ParityMap acc{0, 0};
+  bool huge = false;
+#pragma unroll
+  for (int i = 0; i < kSumItems; ++i) {
+    const int j = tid * kSumItems + i;
+    if (j < len && usable) acc = compose(acc, term_map(__ldg(d + k0 + j), inv_u, huge));
+  }
+  if (huge) sm_huge = 1;
+  // ordered reduction: lanes, then warps
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    ParityMap other;
+    other.a0 = __shfl_down_sync(0xffffffffu, acc.a0, o);
+    other.a1 = __shfl_down_sync(0xffffffffu, acc.a1, o);
+    if ((lane & (2 * o - 1)) == 0) acc = compose(acc, other);
+  }
+  if (lane == 0) sm_w[warp] = acc;
+  __syncthreads();
   if (tid == 0) {
+    ParityMap t{0, 0};
+    for (int w = 0; w < 32; ++w) t = compose(t, sm_w[w]);
+    maps[c] = ChunkMap{t.a0, t.a1, e, (usable && !sm_huge) ? 1 : 0};
+  }
+}
+
+// cell = max(cell_scale * mean, 1e-9): combine chunk maps in order with the
+// exact running sum; a chunk whose binade was mispredicted or that leaves
+// its binade is summed by the exact window scan instead.
+__global__ void __launch_bounds__(kSumThreads) k_cell_size(int ntris, const double* __restrict__ diag,
+                                                           const ChunkMap* __restrict__ maps, int nchunks,
+                                                           double cell_scale, double* __restrict__ out) {
+  extern __shared__ double sm_d[];
+  __shared__ ParityMap sm_warp[32];
+  __shared__ int sm_event;
+  __shared__ long long sm_M;
+  double s = 0.0;
+  for (int c = 0; c < nchunks; ++c) {
+    const int k0 = c * kSumChunk, k1 = min(ntris, k0 + kSumChunk);
+    bool fast = false;
+    if (maps) {
+      const ChunkMap cm = maps[c];
+      if (cm.ok && s >= 0x1p-1000 && isfinite(s) && ilogb(s) == cm.e) {
+        const double inv_u = ldexp(1.0, 52 - cm.e);
+        const long long ms = static_cast<long long>(s * inv_u);
+        const long long M = ms + ((ms & 1) ? cm.a1 : cm.a0);
+        if (M < kTwo53) {
+          s = ldexp(static_cast<double>(M), cm.e - 52);
+          fast = true;
+        }
+      }
+    }
+    if (!fast) sum_range(diag, k0, k1, s, sm_d, sm_warp, &sm_event, &sm_M);
+  }
+  if (threadIdx.x == 0) {
     const double mean = ntris > 0 ? s / ntris : 1.0;
     const double a = cell_scale * mean;
     out[0] = (a < 1e-9) ? 1e-9 : a;  // std::max(a, 1e-9)
   }
-}
-
-constexpr size_t kSumSmem = sizeof(double) * kSumThreads * kSumItems;
-
-static void launch_cell_size(Ctx& c, int n, const double* d, double scale, double* out) {
-  WG_CUDA(cudaFuncSetAttribute(k_cell_size, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSumSmem));
-  k_cell_size<<<1, kSumThreads, kSumSmem, ls(c)>>>(n, d, scale, out);
 }
 
 // Reference serial sum (validation only: weft_gpu_serial_sum).
@@ -253,6 +353,23 @@ __global__ void k_serial_sum_naive(int n, const double* __restrict__ d, double* 
   for (int i = 0; i < n; ++i) s = s + d[i];
   out[0] = s;
 }
+
+constexpr size_t kSumSmem = sizeof(double) * kSumThreads * kSumItems;
+
+static void launch_cell_size(Ctx& c, int n, const double* d, double scale, double* out, bool fast = true) {
+  const int nch = div_up(n, kSumChunk);
+  ChunkMap* maps = nullptr;
+  if (fast && nch > 0) {
+    c.sum_approx.resize(static_cast<size_t>(nch));
+    c.sum_maps.resize(static_cast<size_t>(nch) * sizeof(ChunkMap));
+    maps = reinterpret_cast<ChunkMap*>(c.sum_maps.data());
+    k_chunk_approx<<<nch, 256, 0, ls(c)>>>(n, d, c.sum_approx.data());
+    k_chunk_maps<<<nch, kSumThreads, 0, ls(c)>>>(n, d, c.sum_approx.data(), maps);
+  }
+  WG_CUDA(cudaFuncSetAttribute(k_cell_size, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSumSmem));
+  k_cell_size<<<1, kSumThreads, kSumSmem, ls(c)>>>(n, d, maps, nch, scale, out);
+}
+
 
 __global__ void k_lattice(int ntris, const double* __restrict__ lo, const double* __restrict__ hi,
                           const double* __restrict__ cellp, int* __restrict__ lat, int64_t* __restrict__ cnt) {
@@ -270,8 +387,51 @@ __global__ void k_lattice(int ntris, const double* __restrict__ lo, const double
   cnt[t] = static_cast<int64_t>(b[3] - b[0] + 1) * (b[4] - b[1] + 1) * (b[5] - b[2] + 1);
 }
 
-__global__ void k_emit(int ntris, const int* __restrict__ lat, const int64_t* __restrict__ off,
-                       uint64_t* __restrict__ keys, int32_t* __restrict__ vals) {
+// Lattice bounds (min lo, max hi per axis) so cell keys can be sorted in a
+// compact, order-isomorphic form: ((ix-x0)*ey + (iy-y0))*ez + (iz-z0)
+// orders cells exactly like the reference's packed 63-bit key.
+__global__ void k_lat_bounds(int ntris, const int* __restrict__ lat, int* __restrict__ bounds) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  int v[6] = {INT_MAX, INT_MAX, INT_MAX, INT_MIN, INT_MIN, INT_MIN};
+  if (t < ntris) {
+#pragma unroll
+    for (int c = 0; c < 6; ++c) v[c] = lat[6 * t + c];
+  }
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    for (int o = 16; o > 0; o >>= 1) {
+      v[c] = min(v[c], __shfl_xor_sync(0xffffffffu, v[c], o));
+      v[c + 3] = max(v[c + 3], __shfl_xor_sync(0xffffffffu, v[c + 3], o));
+    }
+  }
+  if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      atomicMin(bounds + c, v[c]);
+      atomicMax(bounds + 3 + c, v[c + 3]);
+    }
+  }
+}
+
+struct KeyFrame {
+  int x0, y0, z0;
+  long long ey, ez;
+  __device__ __forceinline__ unsigned long long compact(int ix, int iy, int iz) const {
+    return (static_cast<unsigned long long>(ix - x0) * ey + static_cast<unsigned long long>(iy - y0)) * ez +
+           static_cast<unsigned long long>(iz - z0);
+  }
+  __device__ __forceinline__ uint64_t packed(unsigned long long k) const {
+    const int iz = static_cast<int>(k % ez) + z0;
+    k /= ez;
+    const int iy = static_cast<int>(k % ey) + y0;
+    const int ix = static_cast<int>(k / ey) + x0;
+    return pack_cell(ix, iy, iz);
+  }
+};
+
+template <class K>
+__global__ void k_emit(int ntris, const int* __restrict__ lat, const int64_t* __restrict__ off, KeyFrame f,
+                       K* __restrict__ keys, int32_t* __restrict__ vals) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= ntris) return;
   const int* b = lat + 6 * t;
@@ -279,26 +439,28 @@ __global__ void k_emit(int ntris, const int* __restrict__ lat, const int64_t* __
   for (int ix = b[0]; ix <= b[3]; ++ix)
     for (int iy = b[1]; iy <= b[4]; ++iy)
       for (int iz = b[2]; iz <= b[5]; ++iz) {
-        keys[o] = pack_cell(ix, iy, iz);
+        keys[o] = static_cast<K>(f.compact(ix, iy, iz));
         vals[o] = t;
         ++o;
       }
 }
 
-__global__ void k_cell_flags(int64_t n, const uint64_t* __restrict__ keys, int32_t* __restrict__ flag) {
+template <class K>
+__global__ void k_cell_flags(int64_t n, const K* __restrict__ keys, int32_t* __restrict__ flag) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
   flag[i] = (i == 0 || keys[i] != keys[i - 1]) ? 1 : 0;
 }
 
 // flag has been exclusive-scanned into idx: cell index of each run start.
-__global__ void k_cells(int64_t n, const uint64_t* __restrict__ keys, const int32_t* __restrict__ flag_scan,
+template <class K>
+__global__ void k_cells(int64_t n, const K* __restrict__ keys, const int32_t* __restrict__ flag_scan, KeyFrame f,
                         uint64_t* __restrict__ cell_keys, int64_t* __restrict__ cell_off) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
   if (i == 0 || keys[i] != keys[i - 1]) {
     const int c = flag_scan[i];
-    cell_keys[c] = keys[i];
+    cell_keys[c] = f.packed(keys[i]);
     cell_off[c] = i;
   }
 }
@@ -335,27 +497,56 @@ void build_grid(Ctx& c, const double* x0, const double* x1, int mode, double thi
   cub::DeviceScan::ExclusiveSum(nullptr, tmp, c.ecount.data(), c.ecount.data(), T + 1, s);
   void* t = scratch(c, tmp);
   WG_CUDA(cub::DeviceScan::ExclusiveSum(t, tmp, c.ecount.data(), c.ecount.data(), T + 1, s));
+  int* bounds = reinterpret_cast<int*>(c.scalars.data() + 16);
+  const int init[6] = {INT_MAX, INT_MAX, INT_MAX, INT_MIN, INT_MIN, INT_MIN};
+  WG_CUDA(cudaMemcpyAsync(bounds, init, sizeof(init), cudaMemcpyHostToDevice, s));
+  if (T) k_lat_bounds<<<div_up(T, 256), 256, 0, ls(c)>>>(T, c.lat.data(), bounds);
   int64_t K = 0;
+  int hb[6];
   WG_CUDA(cudaMemcpyAsync(&K, c.ecount.data() + T, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  WG_CUDA(cudaMemcpyAsync(hb, bounds, sizeof(hb), cudaMemcpyDeviceToHost, s));
   WG_CUDA(cudaMemcpyAsync(&c.grid_cell_size, c.cell_size.data(), sizeof(double), cudaMemcpyDeviceToHost, s));
   WG_CUDA(cudaStreamSynchronize(s));
   if (K > (int64_t(1) << 31) - 1) throw Error(WEFT_ERR_DIMENSION, "build_grid: more than 2^31 cell entries");
+  KeyFrame f{0, 0, 0, 1, 1};
+  int bits = 1;
+  if (T) {
+    f = KeyFrame{hb[0], hb[1], hb[2], static_cast<long long>(hb[4]) - hb[1] + 1, static_cast<long long>(hb[5]) - hb[2] + 1};
+    const unsigned long long ex = static_cast<unsigned long long>(static_cast<long long>(hb[3]) - hb[0] + 1);
+    const unsigned long long span = ex * static_cast<unsigned long long>(f.ey) * static_cast<unsigned long long>(f.ez);
+    while (bits < 64 && (1ULL << bits) < span) ++bits;
+  }
+  const bool narrow = bits <= 32;
   c.keys_a.resize(static_cast<size_t>(K) + 1);
   c.keys_b.resize(static_cast<size_t>(K) + 1);
   c.vals_a.resize(static_cast<size_t>(K) + 1);
   c.vals_b.resize(static_cast<size_t>(K) + 1);
-  if (T) k_emit<<<div_up(T, 256), 256, 0, ls(c)>>>(T, c.lat.data(), c.ecount.data(), c.keys_a.data(), c.vals_a.data());
-  if (K) {
+  auto* ka32 = reinterpret_cast<uint32_t*>(c.keys_a.data());
+  auto* kb32 = reinterpret_cast<uint32_t*>(c.keys_b.data());
+  if (T) {
+    if (narrow) k_emit<uint32_t><<<div_up(T, 256), 256, 0, ls(c)>>>(T, c.lat.data(), c.ecount.data(), f, ka32, c.vals_a.data());
+    else k_emit<uint64_t><<<div_up(T, 256), 256, 0, ls(c)>>>(T, c.lat.data(), c.ecount.data(), f, c.keys_a.data(), c.vals_a.data());
+  }
+  if (K) {  // stable LSD radix sort: per-cell triangle lists stay ascending
     tmp = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, tmp, c.keys_a.data(), c.keys_b.data(), c.vals_a.data(), c.vals_b.data(),
-                                    (int)K, 0, 63, s);
-    t = scratch(c, tmp);
-    WG_CUDA(cub::DeviceRadixSort::SortPairs(t, tmp, c.keys_a.data(), c.keys_b.data(), c.vals_a.data(),
-                                            c.vals_b.data(), (int)K, 0, 63, s));
+    if (narrow) {
+      cub::DeviceRadixSort::SortPairs(nullptr, tmp, ka32, kb32, c.vals_a.data(), c.vals_b.data(), (int)K, 0, bits, s);
+      t = scratch(c, tmp);
+      WG_CUDA(cub::DeviceRadixSort::SortPairs(t, tmp, ka32, kb32, c.vals_a.data(), c.vals_b.data(), (int)K, 0, bits, s));
+    } else {
+      cub::DeviceRadixSort::SortPairs(nullptr, tmp, c.keys_a.data(), c.keys_b.data(), c.vals_a.data(), c.vals_b.data(),
+                                      (int)K, 0, bits, s);
+      t = scratch(c, tmp);
+      WG_CUDA(cub::DeviceRadixSort::SortPairs(t, tmp, c.keys_a.data(), c.keys_b.data(), c.vals_a.data(),
+                                              c.vals_b.data(), (int)K, 0, bits, s));
+    }
   }
   // run-length cells
   c.cell_flag.resize(static_cast<size_t>(K) + 1);
-  if (K) k_cell_flags<<<div_up(K, 256), 256, 0, ls(c)>>>(K, c.keys_b.data(), c.cell_flag.data());
+  if (K) {
+    if (narrow) k_cell_flags<uint32_t><<<div_up(K, 256), 256, 0, ls(c)>>>(K, kb32, c.cell_flag.data());
+    else k_cell_flags<uint64_t><<<div_up(K, 256), 256, 0, ls(c)>>>(K, c.keys_b.data(), c.cell_flag.data());
+  }
   WG_CUDA(cudaMemsetAsync(c.cell_flag.data() + K, 0, sizeof(int32_t), s));
   tmp = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, tmp, c.cell_flag.data(), c.cell_flag.data(), K + 1, s);
@@ -368,7 +559,10 @@ void build_grid(Ctx& c, const double* x0, const double* x1, int mode, double thi
   c.cell_keys.resize(static_cast<size_t>(cells) + 1);
   c.cell_off.resize(static_cast<size_t>(cells) + 1);
   c.wprefix.resize(static_cast<size_t>(cells) + 1);
-  if (K) k_cells<<<div_up(K, 256), 256, 0, ls(c)>>>(K, c.keys_b.data(), c.cell_flag.data(), c.cell_keys.data(), c.cell_off.data());
+  if (K) {
+    if (narrow) k_cells<uint32_t><<<div_up(K, 256), 256, 0, ls(c)>>>(K, kb32, c.cell_flag.data(), f, c.cell_keys.data(), c.cell_off.data());
+    else k_cells<uint64_t><<<div_up(K, 256), 256, 0, ls(c)>>>(K, c.keys_b.data(), c.cell_flag.data(), f, c.cell_keys.data(), c.cell_off.data());
+  }
   WG_CUDA(cudaMemcpyAsync(c.cell_off.data() + cells, &K, sizeof(int64_t), cudaMemcpyHostToDevice, s));
   if (cells) k_pair_counts<<<div_up(cells, 256), 256, 0, ls(c)>>>(cells, c.cell_off.data(), c.wprefix.data());
   WG_CUDA(cudaMemsetAsync(c.wprefix.data() + cells, 0, sizeof(int64_t), s));
@@ -387,8 +581,18 @@ void build_grid(Ctx& c, const double* x0, const double* x1, int mode, double thi
 // ---------------------------------------------------------------------------
 // candidate walk
 // ---------------------------------------------------------------------------
+// One warp per occupied cell. The cell's pair range intersected with
+// [begin, end) is enumerated in the reference's flattened (i, j) order with
+// lane l taking local index base + l; a pair is a candidate iff the smallest
+// common cell of the two lattice boxes, (max lo_x, max lo_y, max lo_z), is
+// this cell (collision.cpp:205-210, 366-369) — only the lo corners are read,
+// staged in shared memory. Hits are compacted with a warp ballot, so pass 2
+// writes them in exactly the reference's walk order.
+constexpr int kWalkWarps = 8;
+constexpr int kWalkStage = 384;
+
 struct WalkArgs {
-  int64_t begin, end, chunk, cells;
+  int64_t begin, end, cells;
   const int64_t* __restrict__ prefix;
   const int64_t* __restrict__ cell_off;
   const int32_t* __restrict__ cell_tris;
@@ -396,75 +600,93 @@ struct WalkArgs {
   const int* __restrict__ lat;
 };
 
-// Walks this thread's chunk; calls emit(t1, t2) for each candidate.
-template <class F>
-__device__ __forceinline__ void walk_chunk(const WalkArgs& w, int64_t g0, int64_t g1, F&& emit) {
-  // cell = upper_bound(prefix, g0) - 1
-  int64_t lo = 0, hi = w.cells + 1;
-  while (lo < hi) {
-    const int64_t mid = (lo + hi) >> 1;
-    if (w.prefix[mid] <= g0) lo = mid + 1;
-    else hi = mid;
-  }
-  int64_t cell = lo - 1;
-  int64_t s = w.cell_off[cell + 1] - w.cell_off[cell];
-  // decode local pair index k -> (i, j), rows of length s-1-i
-  const int64_t k = g0 - w.prefix[cell];
-  auto start = [&](int64_t i) { return i * s - i * (i + 1) / 2; };
-  const double b = 2.0 * s - 1.0;
-  int64_t i = static_cast<int64_t>(floor((b - sqrt(fmax(b * b - 8.0 * (double)k, 0.0))) * 0.5));
-  if (i < 0) i = 0;
-  while (i > 0 && start(i) > k) --i;
-  while (start(i + 1) <= k) ++i;
-  int64_t j = i + 1 + (k - start(i));
-  int64_t next = w.prefix[cell + 1];
-  const int32_t* tl = w.cell_tris + w.cell_off[cell];
-  uint64_t key = w.cell_keys[cell];
-  for (int64_t g = g0; g < g1; ++g) {
-    while (g >= next) {
-      ++cell;
-      s = w.cell_off[cell + 1] - w.cell_off[cell];
-      tl = w.cell_tris + w.cell_off[cell];
-      key = w.cell_keys[cell];
-      next = w.prefix[cell + 1];
-      i = 0;
-      j = 1;
-    }
-    const int t1 = tl[i], t2 = tl[j];
-    const int* a = w.lat + 6 * t1;
-    const int* bb = w.lat + 6 * t2;
-    const uint64_t mc = pack_cell(max(a[0], bb[0]), max(a[1], bb[1]), max(a[2], bb[2]));
-    if (mc == key) emit(t1, t2);
-    if (++j >= s) {
-      ++i;
-      j = i + 1;
-    }
-  }
-}
+// row i of the upper triangle starts at local index i*s - i(i+1)/2
+__device__ __forceinline__ int64_t tri_start(int64_t i, int64_t s) { return i * s - i * (i + 1) / 2; }
 
-__global__ void k_walk_count(WalkArgs w, int64_t nthreads, int64_t* __restrict__ counts) {
-  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (tid >= nthreads) return;
-  const int64_t g0 = w.begin + tid * w.chunk;
-  const int64_t g1 = min(g0 + w.chunk, w.end);
+template <bool kWrite>
+__global__ void __launch_bounds__(kWalkWarps * 32) k_cell_walk(WalkArgs w, int64_t* __restrict__ counts,
+                                                               const int64_t* __restrict__ offs,
+                                                               int2* __restrict__ out) {
+  __shared__ int3 sm_lo[kWalkWarps][kWalkStage];
+  __shared__ int sm_id[kWalkWarps][kWalkStage];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t cell = blockIdx.x * (int64_t)kWalkWarps + warp;
+  if (cell >= w.cells) return;  // warp-uniform
+  const int64_t p0 = w.prefix[cell], p1 = w.prefix[cell + 1];
+  const int64_t lo = max(p0, w.begin), hi = min(p1, w.end);
   int64_t n = 0;
-  if (g0 < g1) walk_chunk(w, g0, g1, [&](int, int) { ++n; });
-  counts[tid] = n;
-}
-
-__global__ void k_walk_write(WalkArgs w, int64_t nthreads, const int64_t* __restrict__ offs,
-                             int32_t* __restrict__ pairs) {
-  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (tid >= nthreads) return;
-  const int64_t g0 = w.begin + tid * w.chunk;
-  const int64_t g1 = min(g0 + w.chunk, w.end);
-  int64_t o = offs[tid];
-  if (g0 < g1)
-    walk_chunk(w, g0, g1, [&](int t1, int t2) {
-      pairs[2 * o] = t1;
-      pairs[2 * o + 1] = t2;
-      ++o;
-    });
+  int64_t o = kWrite ? offs[cell] : 0;
+  if (lo < hi) {
+    const int64_t cbase = w.cell_off[cell];
+    const int64_t s = w.cell_off[cell + 1] - cbase;
+    const int32_t* tl = w.cell_tris + cbase;
+    const uint64_t key = w.cell_keys[cell];
+    const int cx = static_cast<int>(key >> 42) - static_cast<int>(kLatBias);
+    const int cy = static_cast<int>((key >> 21) & 0x1FFFFF) - static_cast<int>(kLatBias);
+    const int cz = static_cast<int>(key & 0x1FFFFF) - static_cast<int>(kLatBias);
+    const bool staged = s <= kWalkStage;
+    if (staged) {
+      for (int i = lane; i < s; i += 32) {
+        const int t = tl[i];
+        sm_id[warp][i] = t;
+        sm_lo[warp][i] = make_int3(w.lat[6 * t], w.lat[6 * t + 1], w.lat[6 * t + 2]);
+      }
+    }
+    __syncwarp();
+    auto load = [&](int64_t i, int& t, int3& l) {
+      if (staged) {
+        t = sm_id[warp][i];
+        l = sm_lo[warp][i];
+      } else {
+        t = tl[i];
+        l = make_int3(w.lat[6 * t], w.lat[6 * t + 1], w.lat[6 * t + 2]);
+      }
+    };
+    // decode this lane's first local index
+    const int64_t l0 = lo - p0, l1 = hi - p0;
+    int64_t k = l0 + lane;
+    int64_t i = 0, j = 0;
+    if (k < l1) {
+      const double b = 2.0 * s - 1.0;
+      i = static_cast<int64_t>(floor((b - sqrt(fmax(b * b - 8.0 * static_cast<double>(k), 0.0))) * 0.5));
+      if (i < 0) i = 0;
+      while (i > 0 && tri_start(i, s) > k) --i;
+      while (tri_start(i + 1, s) <= k) ++i;
+      j = i + 1 + (k - tri_start(i, s));
+    }
+    for (int64_t kb = l0; kb < l1; kb += 32) {
+      const bool act = k < l1;
+      bool hit = false;
+      int t1 = 0, t2 = 0;
+      if (act) {
+        int3 a, c;
+        load(i, t1, a);
+        load(j, t2, c);
+        hit = max(a.x, c.x) == cx && max(a.y, c.y) == cy && max(a.z, c.z) == cz;
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, hit);
+      if (kWrite && hit) out[o + __popc(m & ((1u << lane) - 1u))] = make_int2(t1, t2);
+      o += __popc(m);
+      n += __popc(m);
+      // advance this lane by 32 local indices
+      k += 32;
+      if (k < l1) {
+        int64_t adv = 32;
+        while (adv > 0) {
+          const int64_t room = s - j;
+          if (adv < room) {
+            j += adv;
+            adv = 0;
+          } else {
+            adv -= room;
+            ++i;
+            j = i + 1;
+          }
+        }
+      }
+    }
+  }
+  if (!kWrite && lane == 0) counts[cell] = n;
 }
 
 // Returns the candidate count of [begin, end); when pairs_out is non-null
@@ -476,24 +698,23 @@ int64_t candidates(Ctx& c, int64_t begin, int64_t end, int32_t* pairs_out) {
   end = std::min<int64_t>(end, c.grid_total);
   if (begin >= end) return 0;
   cudaStream_t s = c.stream;
-  const int64_t W = end - begin;
-  const int64_t target_threads = 148LL * 1024;
-  const int64_t chunk = std::max<int64_t>(32, (W + target_threads - 1) / target_threads);
-  const int64_t nthreads = (W + chunk - 1) / chunk;
-  WalkArgs w{begin, end, chunk, c.grid_cells, c.wprefix.data(), c.cell_off.data(), c.vals_b.data(),
-             c.cell_keys.data(), c.lat.data()};
-  c.cand_count.resize(static_cast<size_t>(nthreads) + 1);
-  WG_CUDA(cudaMemsetAsync(c.cand_count.data() + nthreads, 0, sizeof(int64_t), s));
-  k_walk_count<<<div_up(nthreads, 256), 256, 0, ls(c)>>>(w, nthreads, c.cand_count.data());
+  const int64_t cells = c.grid_cells;
+  WalkArgs w{begin, end, cells, c.wprefix.data(), c.cell_off.data(), c.vals_b.data(), c.cell_keys.data(),
+             c.lat.data()};
+  c.cand_count.resize(static_cast<size_t>(cells) + 1);
+  WG_CUDA(cudaMemsetAsync(c.cand_count.data() + cells, 0, sizeof(int64_t), s));
+  const int blocks = div_up(cells, kWalkWarps);
+  k_cell_walk<false><<<blocks, kWalkWarps * 32, 0, ls(c)>>>(w, c.cand_count.data(), nullptr, nullptr);
   size_t tmp = 0;
-  cub::DeviceScan::ExclusiveSum(nullptr, tmp, c.cand_count.data(), c.cand_count.data(), nthreads + 1, s);
+  cub::DeviceScan::ExclusiveSum(nullptr, tmp, c.cand_count.data(), c.cand_count.data(), cells + 1, s);
   void* t = scratch(c, tmp);
-  WG_CUDA(cub::DeviceScan::ExclusiveSum(t, tmp, c.cand_count.data(), c.cand_count.data(), nthreads + 1, s));
+  WG_CUDA(cub::DeviceScan::ExclusiveSum(t, tmp, c.cand_count.data(), c.cand_count.data(), cells + 1, s));
   int64_t n = 0;
-  WG_CUDA(cudaMemcpyAsync(&n, c.cand_count.data() + nthreads, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  WG_CUDA(cudaMemcpyAsync(&n, c.cand_count.data() + cells, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
   WG_CUDA(cudaStreamSynchronize(s));
   c.cand_pairs.resize(2 * static_cast<size_t>(n) + 2);
-  k_walk_write<<<div_up(nthreads, 256), 256, 0, ls(c)>>>(w, nthreads, c.cand_count.data(), c.cand_pairs.data());
+  k_cell_walk<true><<<blocks, kWalkWarps * 32, 0, ls(c)>>>(w, nullptr, c.cand_count.data(),
+                                                           reinterpret_cast<int2*>(c.cand_pairs.data()));
   WG_CUDA(cudaGetLastError());
   if (pairs_out && n)
     WG_CUDA(cudaMemcpyAsync(pairs_out, c.cand_pairs.data(), 2 * sizeof(int32_t) * n, cudaMemcpyDefault, s));
@@ -502,11 +723,11 @@ int64_t candidates(Ctx& c, int64_t begin, int64_t end, int32_t* pairs_out) {
 }
 
 // Test hook: exact parallel serial-order sum vs a one-thread serial loop.
-void serial_sum(Ctx& c, int n, const double* d_host, double* exact, double* naive) {
+void serial_sum(Ctx& c, int n, const double* d_host, double* exact, double* naive, int fast) {
   DBuf<double> d, o;
   d.upload(d_host, static_cast<size_t>(n), c.stream);
   o.resize(2);
-  launch_cell_size(c, n, d.data(), 1.0, o.data());  // cell = max(sum / n, 1e-9)
+  launch_cell_size(c, n, d.data(), 1.0, o.data(), fast != 0);  // cell = max(sum / n, 1e-9)
   k_serial_sum_naive<<<1, 1, 0, ls(c)>>>(n, d.data(), o.data() + 1);
   WG_CUDA(cudaGetLastError());
   double h[2];

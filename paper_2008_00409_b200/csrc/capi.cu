@@ -280,9 +280,9 @@ weft_status weft_gpu_stats(weft_gpu_ctx* ctx, weft_gpu_stats_t* out) {
   });
 }
 
-weft_status weft_gpu_test_serial_sum(weft_gpu_ctx* ctx, int32_t n, const double* d, double* mean_exact,
-                                     double* sum_naive) {
-  return guard(ctx, [&] { weft_gpu::serial_sum(ctx->c, n, d, mean_exact, sum_naive); });
+weft_status weft_gpu_test_serial_sum(weft_gpu_ctx* ctx, int32_t n, const double* d, int32_t fast,
+                                     double* mean_exact, double* sum_naive) {
+  return guard(ctx, [&] { weft_gpu::serial_sum(ctx->c, n, d, mean_exact, sum_naive, fast); });
 }
 
 weft_status weft_gpu_get_stream(weft_gpu_ctx* ctx, void** stream) {

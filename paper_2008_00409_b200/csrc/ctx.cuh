@@ -94,6 +94,8 @@ struct Ctx {
   DBuf<int64_t> cell_off;      // cells + 1
   DBuf<int64_t> wprefix;       // cells + 1
   DBuf<int32_t> cell_flag;
+  DBuf<double> sum_approx;
+  DBuf<unsigned char> sum_maps;
   int64_t grid_entries = 0, grid_cells = 0, grid_total = 0;
   double grid_cell_size = 0.0;
   DBuf<int64_t> cand_count;
@@ -144,7 +146,7 @@ void set_soup(Ctx& c, int verts, int ntris, const int32_t* tris);
 void build_grid(Ctx& c, const double* x0_dev, const double* x1_dev, int mode, double thickness, double cell_scale);
 int64_t candidates(Ctx& c, int64_t begin, int64_t end, int32_t* pairs_dev_or_null);
 
-void serial_sum(Ctx& c, int n, const double* d_host, double* exact, double* naive);
+void serial_sum(Ctx& c, int n, const double* d_host, double* exact, double* naive, int fast);
 
 // CUB scratch helper
 void* scratch(Ctx& c, size_t bytes);

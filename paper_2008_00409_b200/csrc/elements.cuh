@@ -37,14 +37,6 @@ __device__ __forceinline__ double comp(V3 a, int i) { return i == 0 ? a.x : (i =
 
 constexpr double kDeg = 1e-24;  // kDegenerateNormal2, elements.cpp:9
 
-// Row-a result of one element instance. J[b][9] row-major blocks (a, b).
-struct RowEval {
-  double f[3];      // element_force(x_adv).f[a] + element_friction_force(v).f[a]
-  double J[4][9];   // element_jacobian(x_cur).block[a][b]
-  double D[4][9];   // element_velocity_damping block[a][b] (if damped)
-  bool damped;
-};
-
 // ---------------------------------------------------------------- stretch
 // stretch_state (elements.cpp:133-141)
 struct StretchSt {
@@ -80,15 +72,16 @@ __device__ __forceinline__ void stretch_force_row(const double* d, V3 x0, V3 x1,
   f[2] = 0.0 + ((su * gu.z - sv * gv.z) - ss * gs.z);
 }
 
-// stretch_jacobian blocks (i, j), j = 0..2 (elements.cpp:183-230).
-__device__ __forceinline__ void stretch_jac_row(const double* d, V3 x0, V3 x1, V3 x2, int i, bool exact,
-                                                double J[4][9]) {
+// stretch_jacobian blocks (i, j), j = 0..2 (elements.cpp:183-230), streamed
+// to emit(j, block) one block at a time (keeps the 3x3 block in registers).
+template <class F>
+__device__ __forceinline__ void stretch_jac_row(const double* d, V3 x0, V3 x1, V3 x2, int i, bool exact, F&& emit) {
   const StretchSt st = stretch_state(d, x0, x1, x2);
+  double J[9];
   if (!st.ok) {
 #pragma unroll
-    for (int j = 0; j < 3; ++j)
-#pragma unroll
-      for (int q = 0; q < 9; ++q) J[j][q] = 0.0;
+    for (int q = 0; q < 9; ++q) J[q] = 0.0;
+    for (int j = 0; j < 3; ++j) emit(j, J);
     return;
   }
   const V3 wu_hat = divs(st.wu, st.wu_len), wv_hat = divs(st.wv, st.wv_len);
@@ -98,7 +91,6 @@ __device__ __forceinline__ void stretch_jac_row(const double* d, V3 x0, V3 x1, V
   const double ui = d[i], vi = d[3 + i];
   const V3 gui = scl(a * ui, wu_hat), gvi = scl(a * vi, wv_hat);
   const V3 gsi = scl(a, add(scl(ui, st.wv), scl(vi, st.wu)));
-#pragma unroll
   for (int j = 0; j < 3; ++j) {
     const double uj = d[j], vj = d[3 + j];
     const V3 guj = scl(a * uj, wu_hat), gvj = scl(a * vj, wv_hat);
@@ -118,8 +110,9 @@ __device__ __forceinline__ void stretch_jac_row(const double* d, V3 x0, V3 x1, V
         if (keep_u2) m = m - su2 * (id - comp(wu_hat, r) * comp(wu_hat, c));
         if (keep_v2) m = m - sv2 * (id - comp(wv_hat, r) * comp(wv_hat, c));
         if (keep_s2) m = m - ss2 * id;
-        J[j][r * 3 + c] = 0.0 + m;
+        J[r * 3 + c] = 0.0 + m;
       }
+    emit(j, J);
   }
 }
 
@@ -224,7 +217,7 @@ __device__ __noinline__ void dihedral_gradient_dual(const double xs[12], int j, 
 // Exact-mode bend blocks (a, b): -k g_a g_b^T - (k dtheta) H_ab with the
 // symmetrized dual Hessian (elements.cpp:131-159, 244-267).
 __device__ __noinline__ void bend_jac_exact_row(const double* d, V3 x0, V3 x1, V3 x2, V3 x3, int a,
-                                                double J[4][9]) {
+                                                double (*J)[9]) {
   V3 g[4];
   dihedral_gradient(x0, x1, x2, x3, g);
   const double dtheta = dihedral_angle(x0, x1, x2, x3) - d[0];
@@ -258,21 +251,23 @@ __device__ __noinline__ void bend_jac_exact_row(const double* d, V3 x0, V3 x1, V
 }
 
 // ---------------------------------------------------------------- evaluate
+// One element instance, stencil row a. Returns f = element_force(x_adv).f[a]
+// + element_friction_force(v).f[a] (assembly.hpp:185) and streams the row's
+// Jacobian blocks J_ab (x_cur) with the velocity-damping blocks D_ab (or
+// nullptr when the element has none) to emit(b, J, D, add) in ascending b;
+// add = false marks a block whose matrix contribution is exactly -0.
 // Payload layout per kind: include/weft_gpu.h.
+template <bool exact, class F>
 __device__ __forceinline__ void eval_row(int kind, int ss, const int st[4], const double* __restrict__ d, int a,
                                          const double* __restrict__ xc, const double* __restrict__ xa,
-                                         const double* __restrict__ vel, bool exact, RowEval& out) {
-  out.f[0] = out.f[1] = out.f[2] = 0.0;
-  out.damped = false;
-#pragma unroll
-  for (int b = 0; b < 4; ++b)
-#pragma unroll
-    for (int q = 0; q < 9; ++q) out.J[b][q] = 0.0;
+                                         const double* __restrict__ vel, double f[3], F&& emit) {
+  f[0] = f[1] = f[2] = 0.0;
   double fr[3] = {0.0, 0.0, 0.0};
   switch (kind) {
     case WEFT_STRETCH: {
-      stretch_force_row(d, ld3(xa, st[0]), ld3(xa, st[1]), ld3(xa, st[2]), a, out.f);
-      stretch_jac_row(d, ld3(xc, st[0]), ld3(xc, st[1]), ld3(xc, st[2]), a, exact, out.J);
+      stretch_force_row(d, ld3(xa, st[0]), ld3(xa, st[1]), ld3(xa, st[2]), a, f);
+      stretch_jac_row(d, ld3(xc, st[0]), ld3(xc, st[1]), ld3(xc, st[2]), a, exact,
+                      [&](int b, const double* J) { emit(b, J, nullptr, true); });
       break;
     }
     case WEFT_BEND: {
@@ -283,24 +278,29 @@ __device__ __forceinline__ void eval_row(int kind, int ss, const int st[4], cons
         dihedral_gradient(p0, p1, p2, p3, g);
         const double coeff = -d[1] * (theta - d[0]);
         const V3 ga = g[a];
-        out.f[0] = 0.0 + coeff * ga.x;
-        out.f[1] = 0.0 + coeff * ga.y;
-        out.f[2] = 0.0 + coeff * ga.z;
+        f[0] = 0.0 + coeff * ga.x;
+        f[1] = 0.0 + coeff * ga.y;
+        f[2] = 0.0 + coeff * ga.z;
       }
       const V3 p0 = ld3(xc, st[0]), p1 = ld3(xc, st[1]), p2 = ld3(xc, st[2]), p3 = ld3(xc, st[3]);
-      if (exact) {
-        bend_jac_exact_row(d, p0, p1, p2, p3, a, out.J);
+      if constexpr (exact) {
+        double J[4][9];
+        bend_jac_exact_row(d, p0, p1, p2, p3, a, J);
+        for (int b = 0; b < 4; ++b) emit(b, J[b], nullptr, true);
       } else {  // bend_jacobian SpdProjected (elements.cpp:244-267)
         V3 g[4];
         dihedral_gradient(p0, p1, p2, p3, g);
         const double nk = -d[1];
         const V3 ga = g[a];
 #pragma unroll
-        for (int b = 0; b < 4; ++b)
+        for (int b = 0; b < 4; ++b) {
+          double J[9];
 #pragma unroll
           for (int r = 0; r < 3; ++r)
 #pragma unroll
-            for (int c = 0; c < 3; ++c) out.J[b][r * 3 + c] = 0.0 + nk * (comp(ga, r) * comp(g[b], c));
+            for (int c = 0; c < 3; ++c) J[r * 3 + c] = 0.0 + nk * (comp(ga, r) * comp(g[b], c));
+          emit(b, J, nullptr, true);
+        }
       }
       break;
     }
@@ -312,20 +312,21 @@ __device__ __forceinline__ void eval_row(int kind, int ss, const int st[4], cons
           const V3 dir = divs(dd, len);
           const V3 fa = scl(d[1] * (len - d[0]), dir);
           if (a == 0) {
-            out.f[0] = 0.0 + fa.x;
-            out.f[1] = 0.0 + fa.y;
-            out.f[2] = 0.0 + fa.z;
-          } else if (a == 1) {
-            out.f[0] = 0.0 - fa.x;
-            out.f[1] = 0.0 - fa.y;
-            out.f[2] = 0.0 - fa.z;
+            f[0] = 0.0 + fa.x;
+            f[1] = 0.0 + fa.y;
+            f[2] = 0.0 + fa.z;
+          } else {
+            f[0] = 0.0 - fa.x;
+            f[1] = 0.0 - fa.y;
+            f[2] = 0.0 - fa.z;
           }
         }
       }
-      {  // spring_jacobian (elements.cpp:281-293)
+      {  // spring_jacobian (elements.cpp:281-293): blocks (a,0), (a,1)
         const V3 dd = sub(ld3(xc, st[1]), ld3(xc, st[0]));
         const double len = norm(dd);
-        if (len >= 1e-12 && a < 2) {
+        double K[9];
+        if (len >= 1e-12) {
           const V3 dir = divs(dd, len);
           double lateral = 1.0 - d[0] / len;
           if (!exact) lateral = lateral > 0.0 ? lateral : 0.0;
@@ -334,34 +335,48 @@ __device__ __forceinline__ void eval_row(int kind, int ss, const int st[4], cons
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
               const double oo = comp(dir, r) * comp(dir, c);
-              const double k = d[1] * (oo + lateral * ((r == c ? 1.0 : 0.0) - oo));
-              out.J[a][r * 3 + c] = 0.0 - k;      // (a, a)
-              out.J[1 - a][r * 3 + c] = 0.0 + k;  // (a, 1-a)
+              K[r * 3 + c] = d[1] * (oo + lateral * ((r == c ? 1.0 : 0.0) - oo));
             }
+        } else {
+#pragma unroll
+          for (int q = 0; q < 9; ++q) K[q] = 0.0;  // blocks stay zero
+        }
+        double J[9];
+        const bool live = len >= 1e-12;
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+#pragma unroll
+          for (int q = 0; q < 9; ++q) J[q] = !live ? 0.0 : (b == a ? 0.0 - K[q] : 0.0 + K[q]);
+          emit(b, J, nullptr, true);
         }
       }
       break;
     }
-    case WEFT_EXTERNAL: {
-      if (a == 0) {  // element_force assigns (elements.cpp:335-337)
-        out.f[0] = d[0];
-        out.f[1] = d[1];
-        out.f[2] = d[2];
-        if (d[3] > 0.0) {  // drag friction (elements.cpp:364-368) and damping (:390-393)
-          const V3 v = ld3(vel, st[0]);
-          fr[0] = -d[3] * v.x;
-          fr[1] = -d[3] * v.y;
-          fr[2] = -d[3] * v.z;
-          out.damped = true;
+    case WEFT_EXTERNAL: {  // constant force; drag friction + damping (elements.cpp:335-337, 364-368, 390-393)
+      f[0] = d[0];
+      f[1] = d[1];
+      f[2] = d[2];
+      if (d[3] > 0.0) {
+        const V3 v = ld3(vel, st[0]);
+        fr[0] = -d[3] * v.x;
+        fr[1] = -d[3] * v.y;
+        fr[2] = -d[3] * v.z;
+        double J[9], D[9];
 #pragma unroll
-          for (int b = 0; b < 4; ++b)
+        for (int r = 0; r < 3; ++r)
 #pragma unroll
-            for (int q = 0; q < 9; ++q) out.D[b][q] = 0.0;
+          for (int c = 0; c < 3; ++c) {
+            J[r * 3 + c] = 0.0;
+            D[r * 3 + c] = 0.0 + d[3] * (r == c ? 1.0 : 0.0);
+          }
+        emit(0, J, D, true);
+      } else {
+        // (-scale) * 0 = -0 never changes a sum: only the damping product
+        // J v (exactly 0 or -0) is needed.
+        double J[9];
 #pragma unroll
-          for (int r = 0; r < 3; ++r)
-#pragma unroll
-            for (int c = 0; c < 3; ++c) out.D[0][r * 3 + c] = 0.0 + d[3] * (r == c ? 1.0 : 0.0);
-        }
+        for (int q = 0; q < 9; ++q) J[q] = 0.0;
+        emit(0, J, nullptr, false);
       }
       break;
     }
@@ -373,25 +388,13 @@ __device__ __forceinline__ void eval_row(int kind, int ss, const int st[4], cons
         if (gap < d[8]) {
           const double mag = d[9] * (d[8] - gap);
           const double s = mag * d[3 + a];
-          out.f[0] = 0.0 + s * n.x;
-          out.f[1] = 0.0 + s * n.y;
-          out.f[2] = 0.0 + s * n.z;
+          f[0] = 0.0 + s * n.x;
+          f[1] = 0.0 + s * n.y;
+          f[2] = 0.0 + s * n.z;
         }
       }
-      {  // contact_jacobian (elements.cpp:305-316) at x_cur
-        double gap = d[7];
-        for (int i = 0; i < ss; ++i) gap = gap + d[3 + i] * dot(n, ld3(xc, st[i]));
-        if (gap < d[8]) {
-          for (int j = 0; j < ss; ++j) {
-            const double k = (d[9] * d[3 + a]) * d[3 + j];
-#pragma unroll
-            for (int r = 0; r < 3; ++r)
-#pragma unroll
-              for (int c = 0; c < 3; ++c) out.J[j][r * 3 + c] = 0.0 - k * (comp(n, r) * comp(n, c));
-          }
-        }
-      }
-      if (d[11] > 0.0) {  // friction (elements.cpp:370-381) and damping (:395-402)
+      const bool damped = d[11] > 0.0;
+      if (damped) {  // friction (elements.cpp:370-381)
         V3 rel = v3(d[13], d[14], d[15]);
         for (int i = 0; i < ss; ++i) rel = add(rel, scl(d[3 + i], ld3(vel, st[i])));
         const double rn = dot(n, rel);
@@ -400,29 +403,32 @@ __device__ __forceinline__ void eval_row(int kind, int ss, const int st[4], cons
         fr[0] = d[3 + a] * frv.x;
         fr[1] = d[3 + a] * frv.y;
         fr[2] = d[3 + a] * frv.z;
-        out.damped = true;
+      }
+      double gap = d[7];  // contact_jacobian (elements.cpp:305-316) at x_cur
+      for (int i = 0; i < ss; ++i) gap = gap + d[3 + i] * dot(n, ld3(xc, st[i]));
+      const bool active = gap < d[8];
+      for (int j = 0; j < ss; ++j) {
+        double J[9], D[9];
+        const double k = (d[9] * d[3 + a]) * d[3 + j];
+        const double kd = (d[11] * d[3 + a]) * d[3 + j];
 #pragma unroll
-        for (int b = 0; b < 4; ++b)
+        for (int r = 0; r < 3; ++r)
 #pragma unroll
-          for (int q = 0; q < 9; ++q) out.D[b][q] = 0.0;
-        for (int j = 0; j < ss; ++j) {
-          const double k = (d[11] * d[3 + a]) * d[3 + j];
-#pragma unroll
-          for (int r = 0; r < 3; ++r)
-#pragma unroll
-            for (int c = 0; c < 3; ++c)
-              out.D[j][r * 3 + c] = 0.0 + k * ((r == c ? 1.0 : 0.0) - comp(n, r) * comp(n, c));
-        }
+          for (int c = 0; c < 3; ++c) {
+            const double nn = comp(n, r) * comp(n, c);
+            J[r * 3 + c] = active ? 0.0 - k * nn : 0.0;
+            D[r * 3 + c] = 0.0 + kd * ((r == c ? 1.0 : 0.0) - nn);
+          }
+        emit(j, J, damped ? D : nullptr, true);
       }
       break;
     }
     default:
       break;
   }
-  // Vec3 f = force.f[a] + friction.f[a] (assembly.hpp:185)
-  out.f[0] = out.f[0] + fr[0];
-  out.f[1] = out.f[1] + fr[1];
-  out.f[2] = out.f[2] + fr[2];
+  f[0] = f[0] + fr[0];
+  f[1] = f[1] + fr[1];
+  f[2] = f[2] + fr[2];
 }
 
 }  // namespace weft_gpu

@@ -130,12 +130,50 @@ __device__ __forceinline__ void row_product(const SellView& A, int r, int ngroup
   }
 }
 
+// Single accumulation group (n = 1 or interior rows): the column of slot
+// k+1 is fetched while slot k is processed, so the x gather of a slot only
+// waits on its own round trip; matrix words are streamed with evict-first
+// loads (ld.global.cs) so the gathered vectors stay resident in L2.
+template <int PMode>
+__device__ __forceinline__ void row_product_1(const SellView& A, int r, const double* __restrict__ x,
+                                              const double* __restrict__ pold, double beta, double& y0, double& y1,
+                                              double& y2) {
+  const int len = A.rowlen[r];
+  const int64_t base = A.slice_off[r >> 5] + (r & 31);
+  const int64_t T = A.total;
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+  int cn = len > 0 ? (__ldcs(A.cols + base) & kColMask) : 0;
+#pragma unroll 2
+  for (int k = 0; k < len; ++k) {
+    const int64_t at = base + (int64_t)k * kSlice;
+    const int c = cn;
+    if (k + 1 < len) cn = __ldcs(A.cols + at + kSlice) & kColMask;
+    const double* v = A.vals + at;
+    const double v0 = __ldcs(v), v1 = __ldcs(v + T), v2 = __ldcs(v + 2 * T);
+    const double v3 = __ldcs(v + 3 * T), v4 = __ldcs(v + 4 * T), v5 = __ldcs(v + 5 * T);
+    const double v6 = __ldcs(v + 6 * T), v7 = __ldcs(v + 7 * T), v8 = __ldcs(v + 8 * T);
+    double x0 = x[3 * c], x1 = x[3 * c + 1], x2 = x[3 * c + 2];
+    if (PMode == 2) {
+      x0 = x0 + beta * pold[3 * c];
+      x1 = x1 + beta * pold[3 * c + 1];
+      x2 = x2 + beta * pold[3 * c + 2];
+    }
+    a0 = a0 + ((v0 * x0 + v1 * x1) + v2 * x2);
+    a1 = a1 + ((v3 * x0 + v4 * x1) + v5 * x2);
+    a2 = a2 + ((v6 * x0 + v7 * x1) + v8 * x2);
+  }
+  y0 = a0;
+  y1 = a1;
+  y2 = a2;
+}
+
 __global__ void __launch_bounds__(256) k_spmv(SellView A, int ngroups, const double* __restrict__ x,
                                               double* __restrict__ y) {
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= A.rows) return;
   double y0, y1, y2;
-  row_product<0>(A, r, ngroups, x, nullptr, 0.0, y0, y1, y2);
+  if (ngroups == 1) row_product_1<0>(A, r, x, nullptr, 0.0, y0, y1, y2);
+  else row_product<0>(A, r, ngroups, x, nullptr, 0.0, y0, y1, y2);
   y[3 * r] = y0;
   y[3 * r + 1] = y1;
   y[3 * r + 2] = y2;
@@ -431,6 +469,7 @@ __global__ void k_pcg_init(int rows, const double* __restrict__ b, const double*
 
 // Iteration kernel 1: q = A p with p = z (+ beta p) formed on the fly;
 // p.q partials; last block: curvature checks and alpha = rho / pq.
+template <bool kSingle>
 __global__ void __launch_bounds__(256) k_pcg_spmv(SellView A, PartBlocks pb, int ngroups, const double* __restrict__ z,
                                                   const double* __restrict__ p, double* __restrict__ q,
                                                   double* partials, PcgState* st) {
@@ -443,8 +482,13 @@ __global__ void __launch_bounds__(256) k_pcg_spmv(SellView A, PartBlocks pb, int
   double s[1] = {0.0};
   if (r < rend) {
     double y0, y1, y2;
-    if (first) row_product<1>(A, r, ngroups, z, p, beta, y0, y1, y2);
-    else row_product<2>(A, r, ngroups, z, p, beta, y0, y1, y2);
+    if constexpr (kSingle) {
+      if (first) row_product_1<1>(A, r, z, p, beta, y0, y1, y2);
+      else row_product_1<2>(A, r, z, p, beta, y0, y1, y2);
+    } else {
+      if (first) row_product<1>(A, r, ngroups, z, p, beta, y0, y1, y2);
+      else row_product<2>(A, r, ngroups, z, p, beta, y0, y1, y2);
+    }
     q[3 * r] = y0;
     q[3 * r + 1] = y1;
     q[3 * r + 2] = y2;
@@ -616,7 +660,7 @@ PcgResult pcg_solve(Ctx& c, const double* b_dev, const weft_pcg_config& cfg, dou
     }
     for (int k = 0; k < chunk; ++k) {
       if (c.profile) WG_CUDA(cudaEventRecord(c.prof_ev[2 * k], s));
-      k_pcg_spmv<<<nblocks, threads, 0, ls(c)>>>(A, pb, c.go.n, c.z.data(), c.pv.data(), c.q.data(), c.partials.data(),
+      (c.go.n == 1 ? k_pcg_spmv<true> : k_pcg_spmv<false>)<<<nblocks, threads, 0, ls(c)>>>(A, pb, c.go.n, c.z.data(), c.pv.data(), c.q.data(), c.partials.data(),
                                              c.pcg);
       if (c.profile) WG_CUDA(cudaEventRecord(c.prof_ev[2 * k + 1], s));
       k_pcg_update<<<nblocks, threads, 0, ls(c)>>>(pb, c.dinv.data(), bj, c.xs.data(), c.r.data(), c.z.data(),

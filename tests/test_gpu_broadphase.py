@@ -124,11 +124,12 @@ def test_exact_serial_sum(weft, case):
     with weft.Engine(1) as eng:
         for d in ds:
             d = np.ascontiguousarray(d, np.float64)
-            me, sn = C.c_double(), C.c_double()
-            assert weft.LIB.weft_gpu_test_serial_sum(eng._ctx, C.c_int32(len(d)), d.ctypes.data_as(C.c_void_p),
-                                                      C.byref(me), C.byref(sn)) == 0
             s = _serial(d)
-            assert (sn.value == s) or (np.isnan(sn.value) and np.isnan(s))
             mean = s / len(d) if len(d) else 1.0
             want = 1e-9 if mean < 1e-9 else mean
-            assert (me.value == want) or (np.isnan(me.value) and np.isnan(want)), (len(d), me.value, want)
+            for fast in (0, 1):
+                me, sn = C.c_double(), C.c_double()
+                assert weft.LIB.weft_gpu_test_serial_sum(eng._ctx, C.c_int32(len(d)), d.ctypes.data_as(C.c_void_p),
+                                                          C.c_int32(fast), C.byref(me), C.byref(sn)) == 0
+                assert (sn.value == s) or (np.isnan(sn.value) and np.isnan(s))
+                assert (me.value == want) or (np.isnan(me.value) and np.isnan(want)), (fast, len(d), me.value, want)
