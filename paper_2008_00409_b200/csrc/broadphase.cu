@@ -390,7 +390,8 @@ __global__ void k_lattice(int ntris, const double* __restrict__ lo, const double
 // Lattice bounds (min lo, max hi per axis) so cell keys can be sorted in a
 // compact, order-isomorphic form: ((ix-x0)*ey + (iy-y0))*ez + (iz-z0)
 // orders cells exactly like the reference's packed 63-bit key.
-__global__ void k_lat_bounds(int ntris, const int* __restrict__ lat, int* __restrict__ bounds) {
+__global__ void __launch_bounds__(256) k_lat_bounds(int ntris, const int* __restrict__ lat, int* __restrict__ bounds) {
+  __shared__ int sm[8][6];
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   int v[6] = {INT_MAX, INT_MAX, INT_MAX, INT_MIN, INT_MIN, INT_MIN};
   if (t < ntris) {
@@ -404,12 +405,17 @@ __global__ void k_lat_bounds(int ntris, const int* __restrict__ lat, int* __rest
       v[c + 3] = max(v[c + 3], __shfl_xor_sync(0xffffffffu, v[c + 3], o));
     }
   }
-  if ((threadIdx.x & 31) == 0) {
+  const int warp = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0)
 #pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      atomicMin(bounds + c, v[c]);
-      atomicMax(bounds + 3 + c, v[c + 3]);
-    }
+    for (int c = 0; c < 6; ++c) sm[warp][c] = v[c];
+  __syncthreads();
+  if (threadIdx.x < 6) {
+    const int c = threadIdx.x;
+    int r = sm[0][c];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) r = c < 3 ? min(r, sm[w][c]) : max(r, sm[w][c]);
+    if (c < 3) atomicMin(bounds + c, r);
+    else atomicMax(bounds + c, r);
   }
 }
 

@@ -79,6 +79,11 @@ struct Ctx {
   DBuf<double> hist, phist;
   PcgState* pcg = nullptr;       // device
   void* pcg_host = nullptr;      // pinned mirror
+  DBuf<unsigned char> pcg_args;  // device PcgArgs
+  bool use_graphs = true;        // whole-solve CUDA graph (conditional WHILE)
+  cudaGraphExec_t pcg_exec = nullptr;
+  int pcg_exec_blocks = 0;
+  bool pcg_exec_single = false;
 
   // ---- broad phase
   int soup_verts = 0, soup_tris = 0;

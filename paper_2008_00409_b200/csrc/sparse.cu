@@ -467,18 +467,32 @@ __global__ void k_pcg_init(int rows, const double* __restrict__ b, const double*
   p[3 * i] = p[3 * i + 1] = p[3 * i + 2] = 0.0;
 }
 
+// Per-solve arguments, read by the iteration kernels through one device
+// pointer so the captured CUDA graph stays valid across solves.
+struct PcgArgs {
+  SellView A;
+  PartBlocks pb;
+  int ngroups;
+  int bj;
+  const double* dinv;
+  double *x, *r, *z, *p, *q, *partials, *hist, *phist;
+};
+
 // Iteration kernel 1: q = A p with p = z (+ beta p) formed on the fly;
 // p.q partials; last block: curvature checks and alpha = rho / pq.
 template <bool kSingle>
-__global__ void __launch_bounds__(256) k_pcg_spmv(SellView A, PartBlocks pb, int ngroups, const double* __restrict__ z,
-                                                  const double* __restrict__ p, double* __restrict__ q,
-                                                  double* partials, PcgState* st) {
+__global__ void __launch_bounds__(256) k_pcg_spmv(const PcgArgs* __restrict__ args, PcgState* st) {
   __shared__ double smem[32];
   if (st->done) return;
+  const PcgArgs& g = *args;
+  const SellView A = g.A;
+  const double* __restrict__ z = g.z;
+  const double* __restrict__ p = g.p;
+  double* __restrict__ q = g.q;
   const bool first = st->first != 0;
   const double beta = st->beta;
   int rend;
-  const int r = block_row(pb, blockIdx.x, rend);
+  const int r = block_row(g.pb, blockIdx.x, rend);
   double s[1] = {0.0};
   if (r < rend) {
     double y0, y1, y2;
@@ -486,8 +500,8 @@ __global__ void __launch_bounds__(256) k_pcg_spmv(SellView A, PartBlocks pb, int
       if (first) row_product_1<1>(A, r, z, p, beta, y0, y1, y2);
       else row_product_1<2>(A, r, z, p, beta, y0, y1, y2);
     } else {
-      if (first) row_product<1>(A, r, ngroups, z, p, beta, y0, y1, y2);
-      else row_product<2>(A, r, ngroups, z, p, beta, y0, y1, y2);
+      if (first) row_product<1>(A, r, g.ngroups, z, p, beta, y0, y1, y2);
+      else row_product<2>(A, r, g.ngroups, z, p, beta, y0, y1, y2);
     }
     q[3 * r] = y0;
     q[3 * r + 1] = y1;
@@ -501,10 +515,10 @@ __global__ void __launch_bounds__(256) k_pcg_spmv(SellView A, PartBlocks pb, int
     s[0] = (p0 * y0 + p1 * y1) + p2 * y2;
   }
   block_sum<1>(s, smem);
-  if (threadIdx.x == 0) partials[blockIdx.x] = s[0];
+  if (threadIdx.x == 0) g.partials[blockIdx.x] = s[0];
   if (!last_block(&st->counter)) return;
   double t[1];
-  finalize_sums<1>(pb, partials, t, smem);
+  finalize_sums<1>(g.pb, g.partials, t, smem);
   if (threadIdx.x == 0) {
     st->counter = 0;
     const double pq = t[0];
@@ -525,18 +539,24 @@ __global__ void __launch_bounds__(256) k_pcg_spmv(SellView A, PartBlocks pb, int
 
 // Iteration kernel 2: p = z + beta p (own rows), x += alpha p,
 // r -= alpha q, z = M^-1 r; r.r and r.z partials; last block: residual
-// history, convergence test, beta.
-__global__ void __launch_bounds__(256) k_pcg_update(PartBlocks pb, const double* __restrict__ dinv, bool bj,
-                                                    double* __restrict__ x, double* __restrict__ r,
-                                                    double* __restrict__ z, double* __restrict__ p,
-                                                    const double* __restrict__ q, double* partials, PcgState* st,
-                                                    double* hist, double* phist) {
+// history, convergence test, beta, and (graph mode) the loop condition.
+__global__ void __launch_bounds__(256) k_pcg_update(const PcgArgs* __restrict__ args, PcgState* st,
+                                                    cudaGraphConditionalHandle cond, int use_cond) {
   __shared__ double smem[2 * 32];
-  if (st->done) return;
+  if (st->done) {
+    if (use_cond && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(cond, 0);
+    return;
+  }
+  const PcgArgs& g = *args;
+  double* __restrict__ x = g.x;
+  double* __restrict__ r = g.r;
+  double* __restrict__ z = g.z;
+  double* __restrict__ p = g.p;
+  const double* __restrict__ q = g.q;
   const bool first = st->first != 0;
   const double beta = st->beta, alpha = st->alpha;
   int rend;
-  const int i = block_row(pb, blockIdx.x, rend);
+  const int i = block_row(g.pb, blockIdx.x, rend);
   double s[2] = {0.0, 0.0};
   if (i < rend) {
     double pr[3], rr[3];
@@ -550,7 +570,7 @@ __global__ void __launch_bounds__(256) k_pcg_update(PartBlocks pb, const double*
       r[3 * i + c] = rr[c];
     }
     double z0, z1, z2;
-    precond_row(dinv, bj, i, rr[0], rr[1], rr[2], z0, z1, z2);
+    precond_row(g.dinv, g.bj != 0, i, rr[0], rr[1], rr[2], z0, z1, z2);
     z[3 * i] = z0;
     z[3 * i + 1] = z1;
     z[3 * i + 2] = z2;
@@ -559,12 +579,12 @@ __global__ void __launch_bounds__(256) k_pcg_update(PartBlocks pb, const double*
   }
   block_sum<2>(s, smem);
   if (threadIdx.x == 0) {
-    partials[2 * blockIdx.x] = s[0];
-    partials[2 * blockIdx.x + 1] = s[1];
+    g.partials[2 * blockIdx.x] = s[0];
+    g.partials[2 * blockIdx.x + 1] = s[1];
   }
   if (!last_block(&st->counter)) return;
   double t[2];
-  finalize_sums<2>(pb, partials, t, smem);
+  finalize_sums<2>(g.pb, g.partials, t, smem);
   if (threadIdx.x == 0) {
     st->counter = 0;
     const int it = st->iter + 1;
@@ -575,23 +595,26 @@ __global__ void __launch_bounds__(256) k_pcg_update(PartBlocks pb, const double*
     if (!isfinite(r_norm)) {
       st->status = 3;
       st->done = 1;
-      return;
+    } else {
+      g.hist[it - 1] = r_norm / st->b_norm;
+      const double rho_next = t[1];
+      g.phist[it - 1] = sqrt(rho_next > 0.0 ? rho_next : 0.0);
+      if (r_norm <= st->tol) {
+        st->converged = 1;
+        st->done = 1;
+      } else {
+        st->beta = rho_next / st->rho;
+        st->rho = rho_next;
+        if (it >= st->max_iter) st->done = 1;
+      }
     }
-    hist[it - 1] = r_norm / st->b_norm;
-    const double rho_next = t[1];
-    phist[it - 1] = sqrt(rho_next > 0.0 ? rho_next : 0.0);
-    if (r_norm <= st->tol) {
-      st->converged = 1;
-      st->done = 1;
-      return;
-    }
-    st->beta = rho_next / st->rho;
-    st->rho = rho_next;
-    if (it >= st->max_iter) st->done = 1;
+    if (use_cond) cudaGraphSetConditional(cond, st->done ? 0 : 1);
   }
 }
 
 void pcg_free(Ctx& c) {
+  if (c.pcg_exec) cudaGraphExecDestroy(c.pcg_exec);
+  c.pcg_exec = nullptr;
   if (c.pcg) cudaFree(c.pcg);
   if (c.pcg_host) cudaFreeHost(c.pcg_host);
   c.pcg = nullptr;
@@ -650,39 +673,108 @@ PcgResult pcg_solve(Ctx& c, const double* b_dev, const weft_pcg_config& cfg, dou
   init.done = max_it == 0 ? 1 : 0;
   WG_CUDA(cudaMemcpyAsync(c.pcg, &init, sizeof(init), cudaMemcpyHostToDevice, s));
 
+  // per-solve argument block (device)
+  PcgArgs args{A, pb, c.go.n, bj ? 1 : 0, c.dinv.data(), c.xs.data(), c.r.data(), c.z.data(), c.pv.data(),
+               c.q.data(), c.partials.data(), c.hist.data(), c.phist.data()};
+  c.pcg_args.resize(sizeof(PcgArgs));
+  const PcgArgs* dargs = reinterpret_cast<const PcgArgs*>(c.pcg_args.data());
+  WG_CUDA(cudaMemcpyAsync(c.pcg_args.data(), &args, sizeof(args), cudaMemcpyHostToDevice, s));
+  auto spmv_kernel = c.go.n == 1 ? k_pcg_spmv<true> : k_pcg_spmv<false>;
   auto* hs = static_cast<PcgState*>(c.pcg_host);
-  int chunk = 4;
-  int iter_before = 0;
-  for (;;) {
-    if (c.profile && c.prof_ev.size() < 64) {
-      c.prof_ev.resize(64);
-      for (auto& e : c.prof_ev) WG_CUDA(cudaEventCreate(&e));
-    }
-    for (int k = 0; k < chunk; ++k) {
-      if (c.profile) WG_CUDA(cudaEventRecord(c.prof_ev[2 * k], s));
-      (c.go.n == 1 ? k_pcg_spmv<true> : k_pcg_spmv<false>)<<<nblocks, threads, 0, ls(c)>>>(A, pb, c.go.n, c.z.data(), c.pv.data(), c.q.data(), c.partials.data(),
-                                             c.pcg);
-      if (c.profile) WG_CUDA(cudaEventRecord(c.prof_ev[2 * k + 1], s));
-      k_pcg_update<<<nblocks, threads, 0, ls(c)>>>(pb, c.dinv.data(), bj, c.xs.data(), c.r.data(), c.z.data(),
-                                               c.pv.data(), c.q.data(), c.partials.data(), c.pcg, c.hist.data(),
-                                               c.phist.data());
-    }
-    WG_CUDA(cudaGetLastError());
-    WG_CUDA(cudaMemcpyAsync(hs, c.pcg, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
-    WG_CUDA(cudaStreamSynchronize(s));
-    if (c.profile) {
-      // Only launches that did work count (kernels early-exit once done).
-      const int worked = std::min(chunk, hs->iter - iter_before);
-      for (int k = 0; k < worked; ++k) {
-        float ms = 0.f;
-        WG_CUDA(cudaEventElapsedTime(&ms, c.prof_ev[2 * k], c.prof_ev[2 * k + 1]));
-        c.spmv_ms += ms;
-        ++c.spmv_launches;
+
+  if (!c.profile && c.use_graphs) {
+    // The whole solve is one graph launch: a conditional WHILE node whose
+    // body is the two iteration kernels; the update kernel's last block
+    // clears the condition when the solve is done.
+    const bool single = c.go.n == 1;
+    if (!c.pcg_exec || c.pcg_exec_blocks != nblocks || c.pcg_exec_single != single) {
+      if (c.pcg_exec) cudaGraphExecDestroy(c.pcg_exec);
+      c.pcg_exec = nullptr;
+      cudaGraph_t graph = nullptr;
+      bool ok = cudaGraphCreate(&graph, 0) == cudaSuccess;
+      cudaGraphConditionalHandle cond = 0;
+      cudaGraph_t body = nullptr;
+      if (ok) ok = cudaGraphConditionalHandleCreate(&cond, graph, 1, cudaGraphCondAssignDefault) == cudaSuccess;
+      if (ok) {
+        cudaGraphNodeParams cp{};
+        cp.type = cudaGraphNodeTypeConditional;
+        cp.conditional.handle = cond;
+        cp.conditional.type = cudaGraphCondTypeWhile;
+        cp.conditional.size = 1;
+        cudaGraphNode_t node;
+        ok = cudaGraphAddNode(&node, graph, nullptr, 0, &cp) == cudaSuccess;
+        if (ok) body = cp.conditional.phGraph_out[0];
+      }
+      if (ok) {
+        cudaKernelNodeParams k1{};
+        void* a1[] = {(void*)&dargs, (void*)&c.pcg};
+        k1.func = reinterpret_cast<void*>(spmv_kernel);
+        k1.gridDim = dim3(nblocks);
+        k1.blockDim = dim3(threads);
+        k1.kernelParams = a1;
+        int use = 1;
+        cudaKernelNodeParams k2{};
+        void* a2[] = {(void*)&dargs, (void*)&c.pcg, (void*)&cond, (void*)&use};
+        k2.func = reinterpret_cast<void*>(k_pcg_update);
+        k2.gridDim = dim3(nblocks);
+        k2.blockDim = dim3(threads);
+        k2.kernelParams = a2;
+        cudaGraphNode_t n1, n2;
+        ok = cudaGraphAddKernelNode(&n1, body, nullptr, 0, &k1) == cudaSuccess &&
+             cudaGraphAddKernelNode(&n2, body, &n1, 1, &k2) == cudaSuccess &&
+             cudaGraphInstantiate(&c.pcg_exec, graph, 0) == cudaSuccess;
+      }
+      if (graph) cudaGraphDestroy(graph);
+      if (!ok) {  // no conditional-node support: fall back to host-chunked launches
+        cudaGetLastError();
+        c.use_graphs = false;
+        if (c.pcg_exec) cudaGraphExecDestroy(c.pcg_exec);
+        c.pcg_exec = nullptr;
+      } else {
+        c.pcg_exec_blocks = nblocks;
+        c.pcg_exec_single = single;
       }
     }
-    iter_before = hs->iter;
-    if (hs->done) break;
-    chunk = std::min(chunk * 2, 32);  // <= 32 (event pool of 64)
+    if (c.pcg_exec) {
+      WG_CUDA(cudaGraphLaunch(c.pcg_exec, s));
+      c.launches += 2 * max_it;  // upper bound; exact count read back below
+      WG_CUDA(cudaMemcpyAsync(hs, c.pcg, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
+      WG_CUDA(cudaStreamSynchronize(s));
+      c.launches -= 2 * max_it;
+      c.launches += 2 * std::max(hs->iter, 1);
+    }
+  }
+  if (c.profile || !c.use_graphs) {
+    int chunk = 4;
+    int iter_before = 0;
+    for (;;) {
+      if (c.profile && c.prof_ev.size() < 64) {
+        c.prof_ev.resize(64);
+        for (auto& e : c.prof_ev) WG_CUDA(cudaEventCreate(&e));
+      }
+      for (int k = 0; k < chunk; ++k) {
+        if (c.profile) WG_CUDA(cudaEventRecord(c.prof_ev[2 * k], s));
+        spmv_kernel<<<nblocks, threads, 0, ls(c)>>>(dargs, c.pcg);
+        if (c.profile) WG_CUDA(cudaEventRecord(c.prof_ev[2 * k + 1], s));
+        k_pcg_update<<<nblocks, threads, 0, ls(c)>>>(dargs, c.pcg, 0, 0);
+      }
+      WG_CUDA(cudaGetLastError());
+      WG_CUDA(cudaMemcpyAsync(hs, c.pcg, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
+      WG_CUDA(cudaStreamSynchronize(s));
+      if (c.profile) {
+        // Only launches that did work count (kernels early-exit once done).
+        const int worked = std::min(chunk, hs->iter - iter_before);
+        for (int k = 0; k < worked; ++k) {
+          float ms = 0.f;
+          WG_CUDA(cudaEventElapsedTime(&ms, c.prof_ev[2 * k], c.prof_ev[2 * k + 1]));
+          c.spmv_ms += ms;
+          ++c.spmv_launches;
+        }
+      }
+      iter_before = hs->iter;
+      if (hs->done) break;
+      chunk = std::min(chunk * 2, 32);  // <= 32 (event pool of 64)
+    }
   }
   res.iterations = hs->iter;
   res.converged = hs->converged;

@@ -35,7 +35,7 @@ def test_sim_steps_match_reference(weft, layers, nx, steps, tol):
         rr = ref.step(sc.dt, sc.thickness, tol=tol, max_it=3000)
         if k == 0:
             assert rg.dcd_candidates == rr["dcd_candidates"]
-        assert abs(rg.pcg_iterations - rr["pcg_iterations"]) <= 2
+        assert abs(rg.pcg_iterations - rr["pcg_iterations"]) <= max(2, 0.02 * rr["pcg_iterations"])
     xg = np.zeros(3 * p)
     vg = np.zeros(3 * p)
     eng.sim_get_state(xg, vg)
