@@ -245,7 +245,6 @@ def gpu_arm(args, rank, world, local):
 
     # ---- device-resident timed region
     barrier()
-    eng.profile(True)
     launches0 = eng.stats().launches
     clocks = Clocks(local)
     ev0 = torch.cuda.Event(enable_timing=True)
@@ -257,9 +256,16 @@ def gpu_arm(args, rank, world, local):
     barrier()
     clk = clocks.stop()
     ms_total = max_over_ranks(ev0.elapsed_time(ev1))
+    launches = eng.stats().launches - launches0
+    # Kernel timing for the roofline: the timed region runs the PCG as one
+    # CUDA graph, so the SpMV launches are timed with CUDA events on the
+    # context stream in a profiled replay of the same step (chunked launches,
+    # identical kernels and inputs).
+    eng.profile(True)
+    for _ in range(2):
+        replay()
     st = eng.stats()
     eng.profile(False)
-    launches = st.launches - launches0
     spmv_avg_ms = st.spmv_ms / max(st.spmv_launches, 1)
     info = eng.matrix_info()
 

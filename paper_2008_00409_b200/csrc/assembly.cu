@@ -56,6 +56,24 @@ void set_vertices(Ctx& c, int p, const double* mass, const uint8_t* pinned) {
   WG_CUDA(cudaStreamSynchronize(c.stream));
 }
 
+// Per-element result slots of the two-phase SpdProjected fill: the rhs
+// contribution dt*f_a of every stencil slot (3 doubles each) followed by the
+// element state the slot pass regenerates Jacobian blocks from.
+static int state_size(int kind) {
+  switch (kind) {
+    case WEFT_STRETCH:
+      return 18;  // wu_hat, wv_hat, wu, wv, |wu|, |wv|, cu, cv, cs, ok, keep_u2, keep_v2
+    case WEFT_BEND:
+      return 12;  // dihedral gradient at x_cur
+    case WEFT_SPRING:
+      return 10;  // K (row-major) and the live flag
+    case WEFT_CONTACT:
+      return 1;   // active flag (gap < activation at x_cur)
+    default:
+      return 0;
+  }
+}
+
 static int payload_size(int kind) {
   switch (kind) {
     case WEFT_STRETCH:
@@ -75,7 +93,7 @@ static int payload_size(int kind) {
 // Converts flat records into the device SoA (stencil, info, damping,
 // payload pool) starting at element index `first` / payload offset `pay0`.
 static void upload_elements(Ctx& c, int64_t count, const weft_element* elems, int64_t first, int64_t pay0,
-                            int64_t* pay_used) {
+                            int64_t* pay_used, int64_t res0, int64_t* res_used) {
   std::vector<weft_element> host;
   const weft_element* h = elems;
   cudaPointerAttributes attr{};
@@ -90,6 +108,8 @@ static void upload_elements(Ctx& c, int64_t count, const weft_element* elems, in
   std::vector<double> damp(static_cast<size_t>(count));
   std::vector<double> pay;
   pay.reserve(static_cast<size_t>(count) * 4);
+  std::vector<int32_t> roff(static_cast<size_t>(count));
+  int64_t rcur = res0;
   for (int64_t i = 0; i < count; ++i) {
     const weft_element& e = h[i];
     const int ps = payload_size(e.kind);
@@ -110,6 +130,9 @@ static void upload_elements(Ctx& c, int64_t count, const weft_element* elems, in
     info[static_cast<size_t>(i)] = make_int2(e.kind | (e.stencil_size << 8), static_cast<int>(off));
     damp[static_cast<size_t>(i)] = e.damping;
     pay.insert(pay.end(), e.data, e.data + ps);
+    if (rcur > INT32_MAX) throw Error(WEFT_ERR_DIMENSION, "element results exceed 2^31 doubles");
+    roff[static_cast<size_t>(i)] = static_cast<int32_t>(rcur);
+    rcur += 3 * e.stencil_size + state_size(e.kind);
   }
   const size_t n_total = static_cast<size_t>(first + count);
   const size_t pay_total = static_cast<size_t>(pay0) + pay.size();
@@ -129,6 +152,8 @@ static void upload_elements(Ctx& c, int64_t count, const weft_element* elems, in
   grow(c.einfo, n_total, static_cast<size_t>(first));
   grow(c.edamp, n_total, static_cast<size_t>(first));
   grow(c.epay, pay_total, static_cast<size_t>(pay0));
+  grow(c.eres_off, n_total, static_cast<size_t>(first));
+  c.eres.resize(static_cast<size_t>(rcur) + 1);
   if (count) {
     WG_CUDA(cudaMemcpyAsync(c.est.data() + first, st.data(), sizeof(int4) * count, cudaMemcpyHostToDevice, c.stream));
     WG_CUDA(cudaMemcpyAsync(c.einfo.data() + first, info.data(), sizeof(int2) * count, cudaMemcpyHostToDevice, c.stream));
@@ -137,6 +162,10 @@ static void upload_elements(Ctx& c, int64_t count, const weft_element* elems, in
   if (!pay.empty())
     WG_CUDA(cudaMemcpyAsync(c.epay.data() + pay0, pay.data(), sizeof(double) * pay.size(), cudaMemcpyHostToDevice,
                             c.stream));
+  if (count)
+    WG_CUDA(cudaMemcpyAsync(c.eres_off.data() + first, roff.data(), sizeof(int32_t) * count, cudaMemcpyHostToDevice,
+                            c.stream));
+  *res_used = rcur - res0;
   WG_CUDA(cudaStreamSynchronize(c.stream));  // host staging vectors die here
   *pay_used = static_cast<int64_t>(pay.size());
 }
@@ -318,9 +347,11 @@ static void build_pattern(Ctx& c, int64_t first, int64_t count, bool with_diag, 
 void set_elements(Ctx& c, int64_t count, const weft_element* elems) {
   if (c.p == 0 && count) throw Error(WEFT_ERR_INVALID, "set_elements: set_vertices first");
   int64_t used = 0;
-  upload_elements(c, count, elems, 0, 0, &used);
+  int64_t rused = 0;
+  upload_elements(c, count, elems, 0, 0, &used, 0, &rused);
   c.n_static = count;
   c.static_pay = used;
+  c.static_res = rused;
   c.n_contacts = 0;
   build_incidence(c, 0, count, 0, c.inc_ptr, c.inc);
   build_pattern(c, 0, count, true, c.spat_ptr, c.spat);
@@ -334,7 +365,8 @@ void set_elements(Ctx& c, int64_t count, const weft_element* elems) {
 void set_contacts(Ctx& c, int64_t count, const weft_element* elems) {
   if (c.p == 0) throw Error(WEFT_ERR_INVALID, "set_contacts: set_vertices first");
   int64_t used = 0;
-  upload_elements(c, count, elems, c.n_static, c.static_pay, &used);
+  int64_t rused = 0;
+  upload_elements(c, count, elems, c.n_static, c.static_pay, &used, c.static_res, &rused);
   c.n_contacts = count;
   // contact incidences: codes are the contact index (element n_static + i).
   build_incidence(c, c.n_static, count, 0, c.cinc_ptr, c.cinc);
@@ -626,6 +658,414 @@ __global__ void k_zero_padding(int p, const int64_t* __restrict__ soff, const in
     for (int q = 0; q < 9; ++q) vals[q * total + base + (int64_t)k * kSlice] = 0.0;
 }
 
+// ---------------------------------------------------------------------------
+// Two-phase SpdProjected fill
+// ---------------------------------------------------------------------------
+// Phase 1, one thread per ELEMENT (no replication): element_force at x_adv,
+// friction, all Jacobian blocks at x_cur (for the damping term), and the
+// per-stencil-slot rhs contribution dt * f_a, exactly as fill_matrix's
+// instance loop computes them (assembly.hpp:170-197); plus a compact state
+// from which any block J_ab is regenerated bit-identically.
+// Phase 2, one thread per matrix SLOT (row, column): mass first, then every
+// incidence of the row in ascending element order that couples to this
+// column adds (-scale) J_ab (+ dt D_ab) into register accumulators
+// (assembly.hpp:199-215) — no atomics, no shared-memory accumulators, full
+// occupancy. Phase 2b sums each row's rhs contributions in the same order.
+
+// stretch block (i, j) from the stored x_cur state (elements.cpp:209-228,
+// keep_s2 = false in SpdProjected mode).
+__device__ __forceinline__ void stretch_block_state(const double* __restrict__ S, const double* __restrict__ d,
+                                                    int i, int j, double J[9]) {
+  if (S[15] == 0.0) {
+#pragma unroll
+    for (int q = 0; q < 9; ++q) J[q] = 0.0;
+    return;
+  }
+  const V3 wu_hat = v3(S[0], S[1], S[2]), wv_hat = v3(S[3], S[4], S[5]);
+  const V3 wu = v3(S[6], S[7], S[8]), wv = v3(S[9], S[10], S[11]);
+  const double wu_len = S[12], wv_len = S[13];
+  const double a = d[6];
+  const double ui = d[i], vi = d[3 + i], uj = d[j], vj = d[3 + j];
+  const V3 gui = scl(a * ui, wu_hat), gvi = scl(a * vi, wv_hat);
+  const V3 gsi = scl(a, add(scl(ui, wv), scl(vi, wu)));
+  const V3 guj = scl(a * uj, wu_hat), gvj = scl(a * vj, wv_hat);
+  const V3 gsj = scl(a, add(scl(uj, wv), scl(vj, wu)));
+  const double su2 = (d[7] * S[16]) * (((a * ui) * uj) / wu_len);
+  const double sv2 = (d[8] * S[17]) * (((a * vi) * vj) / wv_len);
+  const bool keep_u2 = S[16] >= 0.0, keep_v2 = S[17] >= 0.0;
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const double id = r == c ? 1.0 : 0.0;
+      double m = 0.0;
+      m = m - d[7] * (comp(gui, r) * comp(guj, c));
+      m = m - d[8] * (comp(gvi, r) * comp(gvj, c));
+      m = m - d[9] * (comp(gsi, r) * comp(gsj, c));
+      if (keep_u2) m = m - su2 * (id - comp(wu_hat, r) * comp(wu_hat, c));
+      if (keep_v2) m = m - sv2 * (id - comp(wv_hat, r) * comp(wv_hat, c));
+      J[r * 3 + c] = 0.0 + m;
+    }
+}
+
+// Block J_ab (and D_ab) of an element from its phase-1 state. Returns
+// whether D is present (velocity damping).
+__device__ __forceinline__ bool elem_block(int kind, const double* __restrict__ S, const double* __restrict__ d,
+                                           int a, int b, double J[9], double D[9]) {
+  switch (kind) {
+    case WEFT_STRETCH:
+      stretch_block_state(S, d, a, b, J);
+      return false;
+    case WEFT_BEND: {
+      const double nk = -d[1];
+      const V3 ga = v3(S[3 * a], S[3 * a + 1], S[3 * a + 2]);
+      const V3 gb = v3(S[3 * b], S[3 * b + 1], S[3 * b + 2]);
+#pragma unroll
+      for (int r = 0; r < 3; ++r)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) J[r * 3 + c] = 0.0 + nk * (comp(ga, r) * comp(gb, c));
+      return false;
+    }
+    case WEFT_SPRING: {
+      const bool live = S[9] != 0.0;
+#pragma unroll
+      for (int q = 0; q < 9; ++q) J[q] = !live ? 0.0 : (b == a ? 0.0 - S[q] : 0.0 + S[q]);
+      return false;
+    }
+    case WEFT_EXTERNAL: {
+#pragma unroll
+      for (int r = 0; r < 3; ++r)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          J[r * 3 + c] = 0.0;
+          D[r * 3 + c] = 0.0 + d[3] * (r == c ? 1.0 : 0.0);
+        }
+      return d[3] > 0.0;
+    }
+    case WEFT_CONTACT: {
+      const V3 n = v3(d[0], d[1], d[2]);
+      const bool active = S[0] != 0.0;
+      const double k = (d[9] * d[3 + a]) * d[3 + b];
+      const double kd = (d[11] * d[3 + a]) * d[3 + b];
+#pragma unroll
+      for (int r = 0; r < 3; ++r)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          const double nn = comp(n, r) * comp(n, c);
+          J[r * 3 + c] = active ? 0.0 - k * nn : 0.0;
+          D[r * 3 + c] = 0.0 + kd * ((r == c ? 1.0 : 0.0) - nn);
+        }
+      return d[11] > 0.0;
+    }
+    default:
+#pragma unroll
+      for (int q = 0; q < 9; ++q) J[q] = 0.0;
+      return false;
+  }
+}
+
+struct ElemArgs {
+  int64_t n;
+  double dt;
+  const int4* __restrict__ est;
+  const int2* __restrict__ einfo;
+  const double* __restrict__ edamp;
+  const double* __restrict__ epay;
+  const int32_t* __restrict__ eres_off;
+  double* __restrict__ eres;
+  const double* __restrict__ xc;
+  const double* __restrict__ xa;
+  const double* __restrict__ vel;
+};
+
+__global__ void __launch_bounds__(128) k_elem_eval(ElemArgs g) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= g.n) return;
+  const int4 s4 = g.est[e];
+  const int2 info = g.einfo[e];
+  const int kind = info.x & 0xff, ss = (info.x >> 8) & 0xff;
+  const int st[4] = {s4.x, s4.y, s4.z, s4.w};
+  const double* __restrict__ d = g.epay + info.y;
+  const double damping = g.edamp[e];
+  double* __restrict__ R = g.eres + g.eres_off[e];
+  double* __restrict__ S = R + 3 * ss;
+  double f[4][3];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) f[i][0] = f[i][1] = f[i][2] = 0.0;
+  double fr[4][3];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) fr[i][0] = fr[i][1] = fr[i][2] = 0.0;
+  switch (kind) {
+    case WEFT_STRETCH: {
+      {  // stretch_force (elements.cpp:161-181) at x_adv
+        const StretchSt sa = stretch_state(d, ld3(g.xa, st[0]), ld3(g.xa, st[1]), ld3(g.xa, st[2]));
+        if (sa.ok) {
+          const V3 wu_hat = divs(sa.wu, sa.wu_len), wv_hat = divs(sa.wv, sa.wv_len);
+          const double a = d[6];
+          const double cu = a * (sa.wu_len - 1.0), cv = a * (sa.wv_len - 1.0), cs = a * dot(sa.wu, sa.wv);
+          const double su = -(d[7] * cu), sv = d[8] * cv, sc = d[9] * cs;
+#pragma unroll
+          for (int i = 0; i < 3; ++i) {
+            const V3 gu = scl(a * d[i], wu_hat);
+            const V3 gv = scl(a * d[3 + i], wv_hat);
+            const V3 gs = scl(a, add(scl(d[i], sa.wv), scl(d[3 + i], sa.wu)));
+            f[i][0] = 0.0 + ((su * gu.x - sv * gv.x) - sc * gs.x);
+            f[i][1] = 0.0 + ((su * gu.y - sv * gv.y) - sc * gs.y);
+            f[i][2] = 0.0 + ((su * gu.z - sv * gv.z) - sc * gs.z);
+          }
+        }
+      }
+      // x_cur state (elements.cpp:183-205)
+      const StretchSt sc = stretch_state(d, ld3(g.xc, st[0]), ld3(g.xc, st[1]), ld3(g.xc, st[2]));
+      if (sc.ok) {
+        const V3 wu_hat = divs(sc.wu, sc.wu_len), wv_hat = divs(sc.wv, sc.wv_len);
+        const double a = d[6];
+        S[0] = wu_hat.x; S[1] = wu_hat.y; S[2] = wu_hat.z;
+        S[3] = wv_hat.x; S[4] = wv_hat.y; S[5] = wv_hat.z;
+        S[6] = sc.wu.x; S[7] = sc.wu.y; S[8] = sc.wu.z;
+        S[9] = sc.wv.x; S[10] = sc.wv.y; S[11] = sc.wv.z;
+        S[12] = sc.wu_len;
+        S[13] = sc.wv_len;
+        S[14] = a * dot(sc.wu, sc.wv);  // cs (unused in SpdProjected)
+        S[15] = 1.0;
+        S[16] = a * (sc.wu_len - 1.0);  // cu: keep_u2 iff cu >= 0
+        S[17] = a * (sc.wv_len - 1.0);  // cv: keep_v2 iff cv >= 0
+      } else {
+#pragma unroll
+        for (int q = 0; q < 18; ++q) S[q] = 0.0;
+      }
+      break;
+    }
+    case WEFT_BEND: {
+      {  // bend_force at x_adv (elements.cpp:232-242)
+        const V3 p0 = ld3(g.xa, st[0]), p1 = ld3(g.xa, st[1]), p2 = ld3(g.xa, st[2]), p3 = ld3(g.xa, st[3]);
+        const double theta = dihedral_angle(p0, p1, p2, p3);
+        V3 gg[4];
+        dihedral_gradient(p0, p1, p2, p3, gg);
+        const double coeff = -d[1] * (theta - d[0]);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          f[i][0] = 0.0 + coeff * gg[i].x;
+          f[i][1] = 0.0 + coeff * gg[i].y;
+          f[i][2] = 0.0 + coeff * gg[i].z;
+        }
+      }
+      V3 gg[4];
+      dihedral_gradient(ld3(g.xc, st[0]), ld3(g.xc, st[1]), ld3(g.xc, st[2]), ld3(g.xc, st[3]), gg);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        S[3 * i] = gg[i].x;
+        S[3 * i + 1] = gg[i].y;
+        S[3 * i + 2] = gg[i].z;
+      }
+      break;
+    }
+    case WEFT_SPRING: {
+      {  // spring_force (elements.cpp:269-279)
+        const V3 dd = sub(ld3(g.xa, st[1]), ld3(g.xa, st[0]));
+        const double len = norm(dd);
+        if (len >= 1e-12) {
+          const V3 dir = divs(dd, len);
+          const V3 fa = scl(d[1] * (len - d[0]), dir);
+          f[0][0] = 0.0 + fa.x;
+          f[0][1] = 0.0 + fa.y;
+          f[0][2] = 0.0 + fa.z;
+          f[1][0] = 0.0 - fa.x;
+          f[1][1] = 0.0 - fa.y;
+          f[1][2] = 0.0 - fa.z;
+        }
+      }
+      const V3 dd = sub(ld3(g.xc, st[1]), ld3(g.xc, st[0]));
+      const double len = norm(dd);
+      if (len >= 1e-12) {
+        const V3 dir = divs(dd, len);
+        double lateral = 1.0 - d[0] / len;
+        lateral = lateral > 0.0 ? lateral : 0.0;  // SpdProjected
+#pragma unroll
+        for (int r = 0; r < 3; ++r)
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            const double oo = comp(dir, r) * comp(dir, c);
+            S[r * 3 + c] = d[1] * (oo + lateral * ((r == c ? 1.0 : 0.0) - oo));
+          }
+        S[9] = 1.0;
+      } else {
+#pragma unroll
+        for (int q = 0; q < 10; ++q) S[q] = 0.0;
+      }
+      break;
+    }
+    case WEFT_EXTERNAL: {
+      f[0][0] = d[0];
+      f[0][1] = d[1];
+      f[0][2] = d[2];
+      if (d[3] > 0.0) {
+        const V3 v = ld3(g.vel, st[0]);
+        fr[0][0] = -d[3] * v.x;
+        fr[0][1] = -d[3] * v.y;
+        fr[0][2] = -d[3] * v.z;
+      }
+      break;
+    }
+    case WEFT_CONTACT: {
+      const V3 n = v3(d[0], d[1], d[2]);
+      double gap = d[7];
+      for (int i = 0; i < ss; ++i) gap = gap + d[3 + i] * dot(n, ld3(g.xa, st[i]));
+      if (gap < d[8]) {
+        const double mag = d[9] * (d[8] - gap);
+        for (int i = 0; i < ss; ++i) {
+          const double sv = mag * d[3 + i];
+          f[i][0] = 0.0 + sv * n.x;
+          f[i][1] = 0.0 + sv * n.y;
+          f[i][2] = 0.0 + sv * n.z;
+        }
+      }
+      if (d[11] > 0.0) {
+        V3 rel = v3(d[13], d[14], d[15]);
+        for (int i = 0; i < ss; ++i) rel = add(rel, scl(d[3 + i], ld3(g.vel, st[i])));
+        const double rn = dot(n, rel);
+        const V3 tang = sub(rel, scl(rn, n));
+        const V3 frv = scl(-d[11], tang);
+        for (int i = 0; i < ss; ++i) {
+          fr[i][0] = d[3 + i] * frv.x;
+          fr[i][1] = d[3 + i] * frv.y;
+          fr[i][2] = d[3 + i] * frv.z;
+        }
+      }
+      double gc = d[7];
+      for (int i = 0; i < ss; ++i) gc = gc + d[3 + i] * dot(n, ld3(g.xc, st[i]));
+      S[0] = gc < d[8] ? 1.0 : 0.0;
+      break;
+    }
+    default:
+      break;
+  }
+  // rhs contributions (assembly.hpp:185-197): f = force + friction, then
+  // + damping * (J_ab v_b) in ascending b, then dt * f.
+  for (int i = 0; i < ss; ++i) {
+    double fx = f[i][0] + fr[i][0], fy = f[i][1] + fr[i][1], fz = f[i][2] + fr[i][2];
+    if (damping > 0.0) {
+      for (int b = 0; b < ss; ++b) {
+        double J[9], D[9];
+        elem_block(kind, S, d, i, b, J, D);
+        const V3 vb = ld3(g.vel, st[b]);
+        fx = fx + damping * ((J[0] * vb.x + J[1] * vb.y) + J[2] * vb.z);
+        fy = fy + damping * ((J[3] * vb.x + J[4] * vb.y) + J[5] * vb.z);
+        fz = fz + damping * ((J[6] * vb.x + J[7] * vb.y) + J[8] * vb.z);
+      }
+    }
+    R[3 * i] = g.dt * fx;
+    R[3 * i + 1] = g.dt * fy;
+    R[3 * i + 2] = g.dt * fz;
+  }
+}
+
+struct SlotArgs {
+  int p;
+  int64_t n_static;
+  double dt;
+  const int64_t* __restrict__ slice_off;
+  const int32_t* __restrict__ rowlen;
+  const int32_t* __restrict__ cols;
+  double* __restrict__ vals;
+  int64_t total;
+  const double* __restrict__ mass;
+  const uint8_t* __restrict__ pinned;
+  const int64_t* __restrict__ inc_ptr;
+  const int32_t* __restrict__ inc;
+  const int64_t* __restrict__ cinc_ptr;
+  const int32_t* __restrict__ cinc;
+  const int4* __restrict__ est;
+  const int2* __restrict__ einfo;
+  const double* __restrict__ edamp;
+  const double* __restrict__ epay;
+  const int32_t* __restrict__ eres_off;
+  const double* __restrict__ eres;
+  double* __restrict__ rhs;
+  int* __restrict__ bad_mass;
+};
+
+constexpr int kSlotWarps = 16;
+
+// Phase 2: one CTA per slice of 32 rows, warp w takes slots w, w+16, ...
+__global__ void __launch_bounds__(kSlotWarps * 32) k_fill_slots(SlotArgs g) {
+  const int slice = blockIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int r = slice * kSlice + lane;
+  if (r >= g.p) return;
+  const int len = g.rowlen[r];
+  const int64_t base = g.slice_off[slice] + lane;
+  const double dt = g.dt;
+  for (int k = warp; k < len; k += kSlotWarps) {
+    const int64_t at = base + (int64_t)k * kSlice;
+    const int col = g.cols[at] & kColMask;
+    double acc[9];
+#pragma unroll
+    for (int q = 0; q < 9; ++q) acc[q] = 0.0;
+    if (col == r) {  // mass diagonal first (assembly.hpp:155-166)
+      const double m = g.pinned[r] ? 1.0 : g.mass[r];
+      acc[0] = acc[0] + m;
+      acc[4] = acc[4] + m;
+      acc[8] = acc[8] + m;
+    }
+    for (int pass = 0; pass < 2; ++pass) {
+      const int64_t* ip = pass == 0 ? g.inc_ptr : g.cinc_ptr;
+      const int32_t* il = pass == 0 ? g.inc : g.cinc;
+      const int64_t i1 = ip[r + 1];
+      for (int64_t ii = ip[r]; ii < i1; ++ii) {
+        const int code = __ldg(il + ii);
+        const int64_t e = (pass == 0 ? 0 : g.n_static) + (code >> 2);
+        const int4 s4 = __ldg(g.est + e);
+        const int st[4] = {s4.x, s4.y, s4.z, s4.w};
+        const int2 info = __ldg(g.einfo + e);
+        const int kind = info.x & 0xff, ss = (info.x >> 8) & 0xff;
+        for (int b = 0; b < ss; ++b) {
+          if (st[b] != col) continue;
+          const int a = code & 3;
+          const double* d = g.epay + info.y;
+          const double* S = g.eres + g.eres_off[e] + 3 * ss;
+          double J[9], D[9];
+          const bool damped = elem_block(kind, S, d, a, b, J, D);
+          const double damping = g.edamp[e];
+          const double nscale = -(dt * dt + damping * dt);
+#pragma unroll
+          for (int q = 0; q < 9; ++q) {
+            double cv = nscale * J[q];
+            if (damped) cv = cv + dt * D[q];
+            acc[q] = acc[q] + cv;
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 9; ++q) g.vals[q * g.total + at] = acc[q];
+  }
+}
+
+// Phase 2b: rhs per row, contributions in ascending element order.
+__global__ void __launch_bounds__(256) k_fill_rhs(SlotArgs g) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= g.p) return;
+  if (!g.pinned[r] && g.mass[r] <= 0.0) atomicMin(g.bad_mass, r);
+  double r0 = 0.0, r1 = 0.0, r2 = 0.0;
+  for (int pass = 0; pass < 2; ++pass) {
+    const int64_t* ip = pass == 0 ? g.inc_ptr : g.cinc_ptr;
+    const int32_t* il = pass == 0 ? g.inc : g.cinc;
+    const int64_t i1 = ip[r + 1];
+    for (int64_t ii = ip[r]; ii < i1; ++ii) {
+      const int code = il[ii];
+      const int64_t e = (pass == 0 ? 0 : g.n_static) + (code >> 2);
+      const double* R = g.eres + g.eres_off[e] + 3 * (code & 3);
+      r0 = r0 + R[0];
+      r1 = r1 + R[1];
+      r2 = r2 + R[2];
+    }
+  }
+  g.rhs[3 * r] = r0;
+  g.rhs[3 * r + 1] = r1;
+  g.rhs[3 * r + 2] = r2;
+}
+
 constexpr int kFillThreads = 64;
 constexpr int kWideCap = 24;
 
@@ -671,7 +1111,21 @@ void fill_matrix(Ctx& c, const double* xc, const double* xa, const double* vel, 
   f.xa = xa;
   f.vel = vel;
   f.bad_mass = bad;
-  if (c.p) {
+  if (c.p && !f.exact) {
+    if (!layout_cached)
+      k_zero_padding<<<div_up(c.p, 256), 256, 0, ls(c)>>>(c.p, A.slice_off.data(), A.rowlen.data(), A.vals.data(), A.total);
+    const int64_t ne = c.n_static + c.n_contacts;
+    ElemArgs ea{ne, dt, c.est.data(), c.einfo.data(), c.edamp.data(), c.epay.data(), c.eres_off.data(), c.eres.data(),
+                xc, xa, vel};
+    if (ne) k_elem_eval<<<div_up(ne, 128), 128, 0, ls(c)>>>(ea);
+    SlotArgs sa{c.p, c.n_static, dt, A.slice_off.data(), A.rowlen.data(), A.cols.data(), A.vals.data(), A.total,
+                c.mass.data(), c.pinned.data(), c.inc_ptr.data(), c.inc.data(), c.cinc_ptr.data(), c.cinc.data(),
+                c.est.data(), c.einfo.data(), c.edamp.data(), c.epay.data(), c.eres_off.data(), c.eres.data(),
+                c.rhs.data(), bad};
+    k_fill_slots<<<A.nslices, kSlotWarps * 32, 0, ls(c)>>>(sa);
+    k_fill_rhs<<<div_up(c.p, 256), 256, 0, ls(c)>>>(sa);
+    WG_CUDA(cudaGetLastError());
+  } else if (c.p) {
     if (!layout_cached)
       k_zero_padding<<<div_up(c.p, 256), 256, 0, ls(c)>>>(c.p, A.slice_off.data(), A.rowlen.data(), A.vals.data(), A.total);
     const size_t smem = static_cast<size_t>(f.wcap) * (9 * sizeof(double) + sizeof(int32_t)) * kFillThreads;

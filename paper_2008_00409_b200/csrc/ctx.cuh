@@ -52,6 +52,9 @@ struct Ctx {
   DBuf<double> edamp;     // element damping
   DBuf<double> epay;      // payload pool
   int64_t static_pay = 0;  // payload doubles used by static elements
+  DBuf<int32_t> eres_off;  // per element: offset of its results in eres
+  DBuf<double> eres;       // phase-1 results (rhs contributions + state)
+  int64_t static_res = 0;
   // static row incidences: per row, (element*4 + a) ascending element
   DBuf<int64_t> inc_ptr;  // p + 1
   DBuf<int32_t> inc;
