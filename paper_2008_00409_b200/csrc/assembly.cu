@@ -913,11 +913,14 @@ __global__ void __launch_bounds__(128) k_elem_eval(ElemArgs g) {
       for (int i = 0; i < ss; ++i) gap = gap + d[3 + i] * dot(n, ld3(g.xa, st[i]));
       if (gap < d[8]) {
         const double mag = d[9] * (d[8] - gap);
-        for (int i = 0; i < ss; ++i) {
-          const double sv = mag * d[3 + i];
-          f[i][0] = 0.0 + sv * n.x;
-          f[i][1] = 0.0 + sv * n.y;
-          f[i][2] = 0.0 + sv * n.z;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          if (i < ss) {
+            const double sv = mag * d[3 + i];
+            f[i][0] = 0.0 + sv * n.x;
+            f[i][1] = 0.0 + sv * n.y;
+            f[i][2] = 0.0 + sv * n.z;
+          }
         }
       }
       if (d[11] > 0.0) {
@@ -926,10 +929,13 @@ __global__ void __launch_bounds__(128) k_elem_eval(ElemArgs g) {
         const double rn = dot(n, rel);
         const V3 tang = sub(rel, scl(rn, n));
         const V3 frv = scl(-d[11], tang);
-        for (int i = 0; i < ss; ++i) {
-          fr[i][0] = d[3 + i] * frv.x;
-          fr[i][1] = d[3 + i] * frv.y;
-          fr[i][2] = d[3 + i] * frv.z;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          if (i < ss) {
+            fr[i][0] = d[3 + i] * frv.x;
+            fr[i][1] = d[3 + i] * frv.y;
+            fr[i][2] = d[3 + i] * frv.z;
+          }
         }
       }
       double gc = d[7];
@@ -942,21 +948,27 @@ __global__ void __launch_bounds__(128) k_elem_eval(ElemArgs g) {
   }
   // rhs contributions (assembly.hpp:185-197): f = force + friction, then
   // + damping * (J_ab v_b) in ascending b, then dt * f.
-  for (int i = 0; i < ss; ++i) {
-    double fx = f[i][0] + fr[i][0], fy = f[i][1] + fr[i][1], fz = f[i][2] + fr[i][2];
-    if (damping > 0.0) {
-      for (int b = 0; b < ss; ++b) {
-        double J[9], D[9];
-        elem_block(kind, S, d, i, b, J, D);
-        const V3 vb = ld3(g.vel, st[b]);
-        fx = fx + damping * ((J[0] * vb.x + J[1] * vb.y) + J[2] * vb.z);
-        fy = fy + damping * ((J[3] * vb.x + J[4] * vb.y) + J[5] * vb.z);
-        fz = fz + damping * ((J[6] * vb.x + J[7] * vb.y) + J[8] * vb.z);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    if (i < ss) {
+      double fx = f[i][0] + fr[i][0], fy = f[i][1] + fr[i][1], fz = f[i][2] + fr[i][2];
+      if (damping > 0.0) {
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          if (b < ss) {
+            double J[9], D[9];
+            elem_block(kind, S, d, i, b, J, D);
+            const V3 vb = ld3(g.vel, st[b]);
+            fx = fx + damping * ((J[0] * vb.x + J[1] * vb.y) + J[2] * vb.z);
+            fy = fy + damping * ((J[3] * vb.x + J[4] * vb.y) + J[5] * vb.z);
+            fz = fz + damping * ((J[6] * vb.x + J[7] * vb.y) + J[8] * vb.z);
+          }
+        }
       }
+      R[3 * i] = g.dt * fx;
+      R[3 * i + 1] = g.dt * fy;
+      R[3 * i + 2] = g.dt * fz;
     }
-    R[3 * i] = g.dt * fx;
-    R[3 * i + 1] = g.dt * fy;
-    R[3 * i + 2] = g.dt * fz;
   }
 }
 
@@ -985,14 +997,71 @@ struct SlotArgs {
   int* __restrict__ bad_mass;
 };
 
-constexpr int kSlotWarps = 16;
+constexpr int kSlotWarps = 8;
+constexpr int kStageCap = 1024;  // staged incidences per slice (static + contact)
 
-// Phase 2: one CTA per slice of 32 rows, warp w takes slots w, w+16, ...
-__global__ void __launch_bounds__(kSlotWarps * 32) k_fill_slots(SlotArgs g) {
+// One staged incidence of the slice (shared memory).
+struct StagedInc {
+  int4 st;        // stencil
+  int kind_ss_a;  // kind | ss << 8 | a << 16
+  int pay;        // payload offset
+  int res;        // state offset (results + 3 ss)
+  double damping;
+};
+
+// acc += (-scale) J_ab (+ dt D_ab) for one coupling, block regenerated from
+// the element's phase-1 state (bitwise the blocks fill_matrix adds).
+__device__ __forceinline__ void add_block(const StagedInc& si, int b, const double* __restrict__ epay,
+                                          const double* __restrict__ eres, double dt, double acc[9]) {
+  const int kind = si.kind_ss_a & 0xff, a = (si.kind_ss_a >> 16) & 0xff;
+  double J[9], D[9];
+  const bool damped = elem_block(kind, eres + si.res, epay + si.pay, a, b, J, D);
+  const double nscale = -(dt * dt + si.damping * dt);
+#pragma unroll
+  for (int q = 0; q < 9; ++q) {
+    double cv = nscale * J[q];
+    if (damped) cv = cv + dt * D[q];
+    acc[q] = acc[q] + cv;
+  }
+}
+
+// Phase 2: one CTA per slice of 32 rows. The slice's incidences (static then
+// contact, each ascending element per row) are staged in shared memory;
+// warp w computes slots w, w+8, ... of its lane's row.
+__global__ void __launch_bounds__(kSlotWarps * 32, 2) k_fill_slots(SlotArgs g) {
+  __shared__ int4 sm_st[kStageCap];
+  __shared__ int sm_ksa[kStageCap], sm_pay[kStageCap], sm_res[kStageCap];
+  __shared__ double sm_damp[kStageCap];
+  __shared__ int sm_row[2][kSlice + 1];  // per pass: row -> first staged entry
   const int slice = blockIdx.x;
+  const int r0 = slice * kSlice;
+  const int rows = min(kSlice, g.p - r0);
+  const int64_t s0 = g.inc_ptr[r0], s1 = g.inc_ptr[r0 + rows];
+  const int64_t c0 = g.cinc_ptr[r0], c1 = g.cinc_ptr[r0 + rows];
+  const int nstat = static_cast<int>(s1 - s0), ncont = static_cast<int>(c1 - c0);
+  const bool staged = nstat + ncont <= kStageCap;
+  if (staged) {
+    for (int i = threadIdx.x; i < nstat + ncont; i += blockDim.x) {
+      const bool cpass = i >= nstat;
+      const int code = cpass ? g.cinc[c0 + (i - nstat)] : g.inc[s0 + i];
+      const int64_t e = (cpass ? g.n_static : 0) + (code >> 2);
+      const int2 info = g.einfo[e];
+      const int ss = (info.x >> 8) & 0xff;
+      sm_st[i] = g.est[e];
+      sm_ksa[i] = info.x | ((code & 3) << 16);
+      sm_pay[i] = info.y;
+      sm_res[i] = g.eres_off[e] + 3 * ss;
+      sm_damp[i] = g.edamp[e];
+    }
+    for (int i = threadIdx.x; i <= rows; i += blockDim.x) {
+      sm_row[0][i] = static_cast<int>(g.inc_ptr[r0 + i] - s0);
+      sm_row[1][i] = nstat + static_cast<int>(g.cinc_ptr[r0 + i] - c0);
+    }
+  }
+  __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int r = slice * kSlice + lane;
-  if (r >= g.p) return;
+  const int r = r0 + lane;
+  if (lane >= rows) return;
   const int len = g.rowlen[r];
   const int64_t base = g.slice_off[slice] + lane;
   const double dt = g.dt;
@@ -1008,32 +1077,42 @@ __global__ void __launch_bounds__(kSlotWarps * 32) k_fill_slots(SlotArgs g) {
       acc[4] = acc[4] + m;
       acc[8] = acc[8] + m;
     }
-    for (int pass = 0; pass < 2; ++pass) {
-      const int64_t* ip = pass == 0 ? g.inc_ptr : g.cinc_ptr;
-      const int32_t* il = pass == 0 ? g.inc : g.cinc;
-      const int64_t i1 = ip[r + 1];
-      for (int64_t ii = ip[r]; ii < i1; ++ii) {
-        const int code = __ldg(il + ii);
-        const int64_t e = (pass == 0 ? 0 : g.n_static) + (code >> 2);
-        const int4 s4 = __ldg(g.est + e);
-        const int st[4] = {s4.x, s4.y, s4.z, s4.w};
-        const int2 info = __ldg(g.einfo + e);
-        const int kind = info.x & 0xff, ss = (info.x >> 8) & 0xff;
-        for (int b = 0; b < ss; ++b) {
-          if (st[b] != col) continue;
-          const int a = code & 3;
-          const double* d = g.epay + info.y;
-          const double* S = g.eres + g.eres_off[e] + 3 * ss;
-          double J[9], D[9];
-          const bool damped = elem_block(kind, S, d, a, b, J, D);
-          const double damping = g.edamp[e];
-          const double nscale = -(dt * dt + damping * dt);
+    if (staged) {
+      for (int pass = 0; pass < 2; ++pass) {
+        const int i1 = sm_row[pass][lane + 1];
+        for (int i = sm_row[pass][lane]; i < i1; ++i) {
+          const int4 st4 = sm_st[i];
+          const int ss = (sm_ksa[i] >> 8) & 0xff;
+          const int stv[4] = {st4.x, st4.y, st4.z, st4.w};
 #pragma unroll
-          for (int q = 0; q < 9; ++q) {
-            double cv = nscale * J[q];
-            if (damped) cv = cv + dt * D[q];
-            acc[q] = acc[q] + cv;
+          for (int b = 0; b < 4; ++b) {
+            if (b < ss && stv[b] == col) {
+              StagedInc si{st4, sm_ksa[i], sm_pay[i], sm_res[i], sm_damp[i]};
+              add_block(si, b, g.epay, g.eres, dt, acc);
+            }
           }
+        }
+      }
+    } else {
+      for (int pass = 0; pass < 2; ++pass) {
+        const int64_t* ip = pass == 0 ? g.inc_ptr : g.cinc_ptr;
+        const int32_t* il = pass == 0 ? g.inc : g.cinc;
+        const int64_t i1 = ip[r + 1];
+        for (int64_t ii = ip[r]; ii < i1; ++ii) {
+          const int code = il[ii];
+          const int64_t e = (pass == 0 ? 0 : g.n_static) + (code >> 2);
+          const int2 info = g.einfo[e];
+          const int ss = (info.x >> 8) & 0xff;
+          StagedInc si;
+          si.st = g.est[e];
+          si.kind_ss_a = info.x | ((code & 3) << 16);
+          si.pay = info.y;
+          si.res = g.eres_off[e] + 3 * ss;
+          si.damping = g.edamp[e];
+          const int stv[4] = {si.st.x, si.st.y, si.st.z, si.st.w};
+#pragma unroll
+          for (int b = 0; b < 4; ++b)
+            if (b < ss && stv[b] == col) add_block(si, b, g.epay, g.eres, dt, acc);
         }
       }
     }
