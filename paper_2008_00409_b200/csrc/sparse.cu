@@ -167,6 +167,74 @@ __device__ __forceinline__ void row_product_1(const SellView& A, int r, const do
   y2 = a2;
 }
 
+// Two threads per row (single accumulation group): lane parity q takes
+// slots k = 2j + q, so each warp load instruction moves two coalesced
+// 128-byte segments (16 rows x slots 2j and 2j+1) and twice as many rows are
+// in flight. The even lane accumulates the row in the reference's slot order
+// (P_2j from itself, P_2j+1 from its odd partner via a shuffle). All lanes of
+// the warp iterate to the warp's longest row so the shuffles stay converged.
+template <int PMode>
+__device__ __forceinline__ void row_product_pair(const SellView& A, int r, bool valid, const double* __restrict__ x,
+                                                 const double* __restrict__ pold, double beta, double& y0,
+                                                 double& y1, double& y2) {
+  const int par = threadIdx.x & 1;
+  const int len = valid ? A.rowlen[r] : 0;
+  const int kmax = __reduce_max_sync(0xffffffffu, len);
+  const int64_t base = valid ? A.slice_off[r >> 5] + (r & 31) : 0;
+  const int64_t T = A.total;
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+  int cn = par < len ? (__ldcs(A.cols + base + (int64_t)par * kSlice) & kColMask) : 0;
+  for (int k0 = 0; k0 < kmax; k0 += 2) {
+    const int k = k0 + par;
+    double p0 = 0.0, p1 = 0.0, p2 = 0.0;
+    if (k < len) {
+      const int64_t at = base + (int64_t)k * kSlice;
+      const int c = cn;
+      if (k + 2 < len) cn = __ldcs(A.cols + at + 2 * kSlice) & kColMask;
+      const double* v = A.vals + at;
+      const double v0 = __ldcs(v), v1 = __ldcs(v + T), v2 = __ldcs(v + 2 * T);
+      const double v3 = __ldcs(v + 3 * T), v4 = __ldcs(v + 4 * T), v5 = __ldcs(v + 5 * T);
+      const double v6 = __ldcs(v + 6 * T), v7 = __ldcs(v + 7 * T), v8 = __ldcs(v + 8 * T);
+      double x0 = x[3 * c], x1 = x[3 * c + 1], x2 = x[3 * c + 2];
+      if (PMode == 2) {
+        x0 = x0 + beta * pold[3 * c];
+        x1 = x1 + beta * pold[3 * c + 1];
+        x2 = x2 + beta * pold[3 * c + 2];
+      }
+      p0 = (v0 * x0 + v1 * x1) + v2 * x2;
+      p1 = (v3 * x0 + v4 * x1) + v5 * x2;
+      p2 = (v6 * x0 + v7 * x1) + v8 * x2;
+    }
+    const double q0 = __shfl_down_sync(0xffffffffu, p0, 1);
+    const double q1 = __shfl_down_sync(0xffffffffu, p1, 1);
+    const double q2 = __shfl_down_sync(0xffffffffu, p2, 1);
+    if (par == 0 && k0 < len) {
+      a0 = a0 + p0;
+      a1 = a1 + p1;
+      a2 = a2 + p2;
+      if (k0 + 1 < len) {
+        a0 = a0 + q0;
+        a1 = a1 + q1;
+        a2 = a2 + q2;
+      }
+    }
+  }
+  y0 = a0;
+  y1 = a1;
+  y2 = a2;
+}
+
+__global__ void __launch_bounds__(256) k_spmv_pair(SellView A, const double* __restrict__ x, double* __restrict__ y) {
+  const int r = blockIdx.x * (blockDim.x >> 1) + (threadIdx.x >> 1);
+  double y0, y1, y2;
+  row_product_pair<0>(A, r, r < A.rows, x, nullptr, 0.0, y0, y1, y2);
+  if (r < A.rows && (threadIdx.x & 1) == 0) {
+    y[3 * r] = y0;
+    y[3 * r + 1] = y1;
+    y[3 * r + 2] = y2;
+  }
+}
+
 __global__ void __launch_bounds__(256) k_spmv(SellView A, int ngroups, const double* __restrict__ x,
                                               double* __restrict__ y) {
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
@@ -183,7 +251,8 @@ void spmv(Ctx& c, const double* x_dev, double* y_dev) {
   if (!c.has_matrix) throw Error(WEFT_ERR_INVALID, "spmv: no matrix loaded");
   const int threads = 256;
   if (c.A.rows == 0) return;
-  k_spmv<<<div_up(c.A.rows, threads), threads, 0, ls(c)>>>(view(c.A), c.go.n, x_dev, y_dev);
+  if (c.go.n == 1) k_spmv_pair<<<div_up(c.A.rows, threads / 2), threads, 0, ls(c)>>>(view(c.A), x_dev, y_dev);
+  else k_spmv<<<div_up(c.A.rows, threads), threads, 0, ls(c)>>>(view(c.A), c.go.n, x_dev, y_dev);
   WG_CUDA(cudaGetLastError());
 }
 
@@ -472,6 +541,7 @@ __global__ void k_pcg_init(int rows, const double* __restrict__ b, const double*
 struct PcgArgs {
   SellView A;
   PartBlocks pb;
+  PartBlocks pb2;  // blocks of 128 rows (two threads per row, single partition)
   int ngroups;
   int bj;
   const double* dinv;
@@ -492,14 +562,31 @@ __global__ void __launch_bounds__(256) k_pcg_spmv(const PcgArgs* __restrict__ ar
   const bool first = st->first != 0;
   const double beta = st->beta;
   int rend;
-  const int r = block_row(g.pb, blockIdx.x, rend);
   double s[1] = {0.0};
-  if (r < rend) {
+  if constexpr (kSingle) {
+    // two threads per row (single partition: rows [0, rows))
+    const int r = blockIdx.x * (blockDim.x >> 1) + (threadIdx.x >> 1);
+    const bool valid = r < A.rows;
     double y0, y1, y2;
-    if constexpr (kSingle) {
-      if (first) row_product_1<1>(A, r, z, p, beta, y0, y1, y2);
-      else row_product_1<2>(A, r, z, p, beta, y0, y1, y2);
-    } else {
+    if (first) row_product_pair<1>(A, r, valid, z, p, beta, y0, y1, y2);
+    else row_product_pair<2>(A, r, valid, z, p, beta, y0, y1, y2);
+    if (valid && (threadIdx.x & 1) == 0) {
+      q[3 * r] = y0;
+      q[3 * r + 1] = y1;
+      q[3 * r + 2] = y2;
+      double p0 = z[3 * r], p1 = z[3 * r + 1], p2 = z[3 * r + 2];
+      if (!first) {
+        p0 = p0 + beta * p[3 * r];
+        p1 = p1 + beta * p[3 * r + 1];
+        p2 = p2 + beta * p[3 * r + 2];
+      }
+      s[0] = (p0 * y0 + p1 * y1) + p2 * y2;
+    }
+  }
+  const int r = kSingle ? -1 : block_row(g.pb, blockIdx.x, rend);
+  if (!kSingle && r < rend) {
+    double y0, y1, y2;
+    {
       if (first) row_product<1>(A, r, g.ngroups, z, p, beta, y0, y1, y2);
       else row_product<2>(A, r, g.ngroups, z, p, beta, y0, y1, y2);
     }
@@ -518,7 +605,7 @@ __global__ void __launch_bounds__(256) k_pcg_spmv(const PcgArgs* __restrict__ ar
   if (threadIdx.x == 0) g.partials[blockIdx.x] = s[0];
   if (!last_block(&st->counter)) return;
   double t[1];
-  finalize_sums<1>(g.pb, g.partials, t, smem);
+  finalize_sums<1>(kSingle ? g.pb2 : g.pb, g.partials, t, smem);
   if (threadIdx.x == 0) {
     st->counter = 0;
     const double pq = t[0];
@@ -639,7 +726,7 @@ PcgResult pcg_solve(Ctx& c, const double* b_dev, const weft_pcg_config& cfg, dou
   c.phist.resize(static_cast<size_t>(max_it) + 1);
   const PartBlocks pb = part_blocks(c.pm, threads);
   const int nblocks = pb.bstart[pb.n];
-  c.partials.resize(2 * static_cast<size_t>(nblocks) + 2);
+  c.partials.resize(4 * static_cast<size_t>(nblocks) + 4);
   const SellView A = view(c.A);
   cudaStream_t s = c.stream;
 
@@ -674,7 +761,9 @@ PcgResult pcg_solve(Ctx& c, const double* b_dev, const weft_pcg_config& cfg, dou
   WG_CUDA(cudaMemcpyAsync(c.pcg, &init, sizeof(init), cudaMemcpyHostToDevice, s));
 
   // per-solve argument block (device)
-  PcgArgs args{A, pb, c.go.n, bj ? 1 : 0, c.dinv.data(), c.xs.data(), c.r.data(), c.z.data(), c.pv.data(),
+  const PartBlocks pb2 = part_blocks(c.pm, threads / 2);
+  const int nblocks2 = pb2.bstart[pb2.n];
+  PcgArgs args{A, pb, pb2, c.go.n, bj ? 1 : 0, c.dinv.data(), c.xs.data(), c.r.data(), c.z.data(), c.pv.data(),
                c.q.data(), c.partials.data(), c.hist.data(), c.phist.data()};
   c.pcg_args.resize(sizeof(PcgArgs));
   const PcgArgs* dargs = reinterpret_cast<const PcgArgs*>(c.pcg_args.data());
@@ -709,7 +798,7 @@ PcgResult pcg_solve(Ctx& c, const double* b_dev, const weft_pcg_config& cfg, dou
         cudaKernelNodeParams k1{};
         void* a1[] = {(void*)&dargs, (void*)&c.pcg};
         k1.func = reinterpret_cast<void*>(spmv_kernel);
-        k1.gridDim = dim3(nblocks);
+        k1.gridDim = dim3(single ? nblocks2 : nblocks);
         k1.blockDim = dim3(threads);
         k1.kernelParams = a1;
         int use = 1;
@@ -754,7 +843,7 @@ PcgResult pcg_solve(Ctx& c, const double* b_dev, const weft_pcg_config& cfg, dou
       }
       for (int k = 0; k < chunk; ++k) {
         if (c.profile) WG_CUDA(cudaEventRecord(c.prof_ev[2 * k], s));
-        spmv_kernel<<<nblocks, threads, 0, ls(c)>>>(dargs, c.pcg);
+        spmv_kernel<<<c.go.n == 1 ? nblocks2 : nblocks, threads, 0, ls(c)>>>(dargs, c.pcg);
         if (c.profile) WG_CUDA(cudaEventRecord(c.prof_ev[2 * k + 1], s));
         k_pcg_update<<<nblocks, threads, 0, ls(c)>>>(dargs, c.pcg, 0, 0);
       }
