@@ -1,6 +1,7 @@
 // capi.cu — the extern "C" boundary (include/weft_gpu.h). Every entry
 // point converts exceptions into a weft_status plus a thread-local message
 // worded like the reference's exception.
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -132,6 +133,8 @@ weft_status weft_gpu_create(const weft_gpu_options* opts, weft_gpu_ctx** out) {
     WG_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
     for (auto& e : c.ev) WG_CUDA(cudaEventCreate(&e));
     c.scalars.resize(64);
+    if (const char* e = std::getenv("WEFT_SPMV_PAIR")) c.spmv_pair = std::atoi(e) != 0;
+    if (const char* e = std::getenv("WEFT_NO_GRAPHS")) c.use_graphs = std::atoi(e) == 0;
     // accumulation group order from the work queues
     const int n = c.nparts;
     c.go.n = n;

@@ -87,6 +87,8 @@ struct Ctx {
   cudaGraphExec_t pcg_exec = nullptr;
   int pcg_exec_blocks = 0;
   bool pcg_exec_single = false;
+  bool pcg_exec_pair = false;
+  bool spmv_pair = false;  // two threads per row SpMV variant (WEFT_SPMV_PAIR=1)
 
   // ---- broad phase
   int soup_verts = 0, soup_tris = 0;

@@ -251,7 +251,7 @@ void spmv(Ctx& c, const double* x_dev, double* y_dev) {
   if (!c.has_matrix) throw Error(WEFT_ERR_INVALID, "spmv: no matrix loaded");
   const int threads = 256;
   if (c.A.rows == 0) return;
-  if (c.go.n == 1) k_spmv_pair<<<div_up(c.A.rows, threads / 2), threads, 0, ls(c)>>>(view(c.A), x_dev, y_dev);
+  if (c.go.n == 1 && c.spmv_pair) k_spmv_pair<<<div_up(c.A.rows, threads / 2), threads, 0, ls(c)>>>(view(c.A), x_dev, y_dev);
   else k_spmv<<<div_up(c.A.rows, threads), threads, 0, ls(c)>>>(view(c.A), c.go.n, x_dev, y_dev);
   WG_CUDA(cudaGetLastError());
 }
@@ -550,7 +550,7 @@ struct PcgArgs {
 
 // Iteration kernel 1: q = A p with p = z (+ beta p) formed on the fly;
 // p.q partials; last block: curvature checks and alpha = rho / pq.
-template <bool kSingle>
+template <bool kSingle, bool kPair>
 __global__ void __launch_bounds__(256) k_pcg_spmv(const PcgArgs* __restrict__ args, PcgState* st) {
   __shared__ double smem[32];
   if (st->done) return;
@@ -563,7 +563,7 @@ __global__ void __launch_bounds__(256) k_pcg_spmv(const PcgArgs* __restrict__ ar
   const double beta = st->beta;
   int rend;
   double s[1] = {0.0};
-  if constexpr (kSingle) {
+  if constexpr (kSingle && kPair) {
     // two threads per row (single partition: rows [0, rows))
     const int r = blockIdx.x * (blockDim.x >> 1) + (threadIdx.x >> 1);
     const bool valid = r < A.rows;
@@ -583,10 +583,13 @@ __global__ void __launch_bounds__(256) k_pcg_spmv(const PcgArgs* __restrict__ ar
       s[0] = (p0 * y0 + p1 * y1) + p2 * y2;
     }
   }
-  const int r = kSingle ? -1 : block_row(g.pb, blockIdx.x, rend);
-  if (!kSingle && r < rend) {
+  const int r = (kSingle && kPair) ? -1 : block_row(g.pb, blockIdx.x, rend);
+  if (!(kSingle && kPair) && r < rend) {
     double y0, y1, y2;
-    {
+    if constexpr (kSingle) {
+      if (first) row_product_1<1>(A, r, z, p, beta, y0, y1, y2);
+      else row_product_1<2>(A, r, z, p, beta, y0, y1, y2);
+    } else {
       if (first) row_product<1>(A, r, g.ngroups, z, p, beta, y0, y1, y2);
       else row_product<2>(A, r, g.ngroups, z, p, beta, y0, y1, y2);
     }
@@ -605,7 +608,7 @@ __global__ void __launch_bounds__(256) k_pcg_spmv(const PcgArgs* __restrict__ ar
   if (threadIdx.x == 0) g.partials[blockIdx.x] = s[0];
   if (!last_block(&st->counter)) return;
   double t[1];
-  finalize_sums<1>(kSingle ? g.pb2 : g.pb, g.partials, t, smem);
+  finalize_sums<1>((kSingle && kPair) ? g.pb2 : g.pb, g.partials, t, smem);
   if (threadIdx.x == 0) {
     st->counter = 0;
     const double pq = t[0];
@@ -768,7 +771,8 @@ PcgResult pcg_solve(Ctx& c, const double* b_dev, const weft_pcg_config& cfg, dou
   c.pcg_args.resize(sizeof(PcgArgs));
   const PcgArgs* dargs = reinterpret_cast<const PcgArgs*>(c.pcg_args.data());
   WG_CUDA(cudaMemcpyAsync(c.pcg_args.data(), &args, sizeof(args), cudaMemcpyHostToDevice, s));
-  auto spmv_kernel = c.go.n == 1 ? k_pcg_spmv<true> : k_pcg_spmv<false>;
+  const bool pair = c.go.n == 1 && c.spmv_pair;
+  auto spmv_kernel = c.go.n == 1 ? (pair ? k_pcg_spmv<true, true> : k_pcg_spmv<true, false>) : k_pcg_spmv<false, false>;
   auto* hs = static_cast<PcgState*>(c.pcg_host);
 
   if (!c.profile && c.use_graphs) {
@@ -776,7 +780,7 @@ PcgResult pcg_solve(Ctx& c, const double* b_dev, const weft_pcg_config& cfg, dou
     // body is the two iteration kernels; the update kernel's last block
     // clears the condition when the solve is done.
     const bool single = c.go.n == 1;
-    if (!c.pcg_exec || c.pcg_exec_blocks != nblocks || c.pcg_exec_single != single) {
+    if (!c.pcg_exec || c.pcg_exec_blocks != nblocks || c.pcg_exec_single != single || c.pcg_exec_pair != pair) {
       if (c.pcg_exec) cudaGraphExecDestroy(c.pcg_exec);
       c.pcg_exec = nullptr;
       cudaGraph_t graph = nullptr;
@@ -798,7 +802,7 @@ PcgResult pcg_solve(Ctx& c, const double* b_dev, const weft_pcg_config& cfg, dou
         cudaKernelNodeParams k1{};
         void* a1[] = {(void*)&dargs, (void*)&c.pcg};
         k1.func = reinterpret_cast<void*>(spmv_kernel);
-        k1.gridDim = dim3(single ? nblocks2 : nblocks);
+        k1.gridDim = dim3(pair ? nblocks2 : nblocks);
         k1.blockDim = dim3(threads);
         k1.kernelParams = a1;
         int use = 1;
@@ -822,6 +826,7 @@ PcgResult pcg_solve(Ctx& c, const double* b_dev, const weft_pcg_config& cfg, dou
       } else {
         c.pcg_exec_blocks = nblocks;
         c.pcg_exec_single = single;
+        c.pcg_exec_pair = pair;
       }
     }
     if (c.pcg_exec) {
@@ -843,7 +848,7 @@ PcgResult pcg_solve(Ctx& c, const double* b_dev, const weft_pcg_config& cfg, dou
       }
       for (int k = 0; k < chunk; ++k) {
         if (c.profile) WG_CUDA(cudaEventRecord(c.prof_ev[2 * k], s));
-        spmv_kernel<<<c.go.n == 1 ? nblocks2 : nblocks, threads, 0, ls(c)>>>(dargs, c.pcg);
+        spmv_kernel<<<pair ? nblocks2 : nblocks, threads, 0, ls(c)>>>(dargs, c.pcg);
         if (c.profile) WG_CUDA(cudaEventRecord(c.prof_ev[2 * k + 1], s));
         k_pcg_update<<<nblocks, threads, 0, ls(c)>>>(dargs, c.pcg, 0, 0);
       }
