@@ -505,6 +505,8 @@ static void build_layout(Ctx& c) {
 // ---------------------------------------------------------------------------
 // value fill
 // ---------------------------------------------------------------------------
+constexpr int kFillThreadsConst = 64;
+
 struct FillArgs {
   int p;
   int64_t n_static;
@@ -541,7 +543,7 @@ struct Acc {
   double* gv;   // output planes (Wide)
   int64_t total, base;
   __device__ __forceinline__ double& at(int slot, int q) {
-    if (Wide) return gv[q * total + base + (int64_t)slot * kSlice];
+    if (Wide) return gv[vidx(base + (int64_t)slot * kSlice, tid & 31, q)];
     return sm[(slot * 9 + q) * bs + tid];
   }
 };
@@ -556,6 +558,7 @@ __global__ void __launch_bounds__(64) k_fill(FillArgs f) {
   const int64_t base = f.slice_off[r >> 5] + (r & 31);
   int32_t* colbuf = reinterpret_cast<int32_t*>(smem + (size_t)f.wcap * 9 * blockDim.x);
   Acc<Wide> acc{smem, (int)threadIdx.x, (int)blockDim.x, f.vals, f.total, base};
+  static_assert(kFillThreadsConst % 32 == 0, "row lanes must match threadIdx.x % 32");
   auto col_of = [&](int k) -> int {
     if (!Wide) return colbuf[k * blockDim.x + threadIdx.x];
     return f.cols[base + (int64_t)k * kSlice] & kColMask;
@@ -640,7 +643,7 @@ __global__ void __launch_bounds__(64) k_fill(FillArgs f) {
   if (!Wide) {
     for (int k = 0; k < len; ++k)
 #pragma unroll
-      for (int q = 0; q < 9; ++q) f.vals[q * f.total + base + (int64_t)k * kSlice] = acc.at(k, q);
+      for (int q = 0; q < 9; ++q) f.vals[vidx(base + (int64_t)k * kSlice, r & 31, q)] = acc.at(k, q);
   }
 }
 
@@ -655,7 +658,7 @@ __global__ void k_zero_padding(int p, const int64_t* __restrict__ soff, const in
   const int64_t base = soff[s] + (r & 31);
   for (int k = rowlen[r]; k < width; ++k)
 #pragma unroll
-    for (int q = 0; q < 9; ++q) vals[q * total + base + (int64_t)k * kSlice] = 0.0;
+    for (int q = 0; q < 9; ++q) vals[vidx(base + (int64_t)k * kSlice, r & 31, q)] = 0.0;
 }
 
 // ---------------------------------------------------------------------------
@@ -1117,7 +1120,7 @@ __global__ void __launch_bounds__(kSlotWarps * 32, 2) k_fill_slots(SlotArgs g) {
       }
     }
 #pragma unroll
-    for (int q = 0; q < 9; ++q) g.vals[q * g.total + at] = acc[q];
+    for (int q = 0; q < 9; ++q) g.vals[vidx(at, lane, q)] = acc[q];
   }
 }
 

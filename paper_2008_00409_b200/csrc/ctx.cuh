@@ -6,10 +6,12 @@
 namespace weft_gpu {
 
 // Sliced-ELL (SELL-32) 3x3-block matrix. Slot k of row r lives at
-// slice_off[r/32] + 32*k + r%32; the nine block components are nine planes
-// of `total` doubles each (the reference's nine SoA value planes,
-// proj/include/weft/bell.hpp:61-79, re-laid slot-major per warp of rows so
-// one load instruction moves 256 contiguous bytes). Per row, slots are
+// slice_off[r/32] + 32*k + r%32 (column words); its nine block components
+// sit at vidx(at, r%32, q): per (slice, slot) nine 256-byte component
+// chunks, i.e. the reference's nine SoA value planes
+// (proj/include/weft/bell.hpp:61-79) re-laid slot-major per warp of rows so
+// each load instruction moves 256 contiguous bytes and a slice is one
+// sequential stream. Per row, slots are
 // ordered by accumulation group (own partition first, then the work-queue
 // order) and by ascending column within a group; the group position is
 // packed in bits 28..30 of the column word.
@@ -26,6 +28,14 @@ struct SellMatrix {
 };
 
 constexpr int kColMask = 0x0FFFFFFF;
+
+// Value index of component q (row-major 3x3) of the slot at column-index
+// position `at` of a row with lane = row % 32: the nine components of one
+// slot of a 32-row slice are nine consecutive 256-byte chunks, so a warp
+// walking its rows' slot k streams one contiguous 2304-byte record.
+__host__ __device__ __forceinline__ int64_t vidx(int64_t at, int lane, int q) {
+  return 9 * (at - lane) + 32 * q + lane;
+}
 constexpr int kGroupShift = 28;
 
 struct PcgState;  // device scalars, see pcg.cu

@@ -101,10 +101,10 @@ __device__ __forceinline__ void row_product(const SellView& A, int r, int ngroup
       a0 = a1 = a2 = 0.0;
       ++cg;
     }
-    const double* v = A.vals + at;
-    const double v0 = __ldg(v), v1 = __ldg(v + T), v2 = __ldg(v + 2 * T);
-    const double v3 = __ldg(v + 3 * T), v4 = __ldg(v + 4 * T), v5 = __ldg(v + 5 * T);
-    const double v6 = __ldg(v + 6 * T), v7 = __ldg(v + 7 * T), v8 = __ldg(v + 8 * T);
+    const double* v = A.vals + vidx(at, r & 31, 0);
+    const double v0 = __ldg(v), v1 = __ldg(v + 32), v2 = __ldg(v + 64);
+    const double v3 = __ldg(v + 96), v4 = __ldg(v + 128), v5 = __ldg(v + 160);
+    const double v6 = __ldg(v + 192), v7 = __ldg(v + 224), v8 = __ldg(v + 256);
     double x0 = x[3 * c], x1 = x[3 * c + 1], x2 = x[3 * c + 2];
     if (PMode == 2) {
       x0 = x0 + beta * pold[3 * c];
@@ -148,10 +148,10 @@ __device__ __forceinline__ void row_product_1(const SellView& A, int r, const do
     const int64_t at = base + (int64_t)k * kSlice;
     const int c = cn;
     if (k + 1 < len) cn = __ldcs(A.cols + at + kSlice) & kColMask;
-    const double* v = A.vals + at;
-    const double v0 = __ldcs(v), v1 = __ldcs(v + T), v2 = __ldcs(v + 2 * T);
-    const double v3 = __ldcs(v + 3 * T), v4 = __ldcs(v + 4 * T), v5 = __ldcs(v + 5 * T);
-    const double v6 = __ldcs(v + 6 * T), v7 = __ldcs(v + 7 * T), v8 = __ldcs(v + 8 * T);
+    const double* v = A.vals + vidx(at, r & 31, 0);
+    const double v0 = __ldcs(v), v1 = __ldcs(v + 32), v2 = __ldcs(v + 64);
+    const double v3 = __ldcs(v + 96), v4 = __ldcs(v + 128), v5 = __ldcs(v + 160);
+    const double v6 = __ldcs(v + 192), v7 = __ldcs(v + 224), v8 = __ldcs(v + 256);
     double x0 = x[3 * c], x1 = x[3 * c + 1], x2 = x[3 * c + 2];
     if (PMode == 2) {
       x0 = x0 + beta * pold[3 * c];
@@ -191,10 +191,10 @@ __device__ __forceinline__ void row_product_pair(const SellView& A, int r, bool 
       const int64_t at = base + (int64_t)k * kSlice;
       const int c = cn;
       if (k + 2 < len) cn = __ldcs(A.cols + at + 2 * kSlice) & kColMask;
-      const double* v = A.vals + at;
-      const double v0 = __ldcs(v), v1 = __ldcs(v + T), v2 = __ldcs(v + 2 * T);
-      const double v3 = __ldcs(v + 3 * T), v4 = __ldcs(v + 4 * T), v5 = __ldcs(v + 5 * T);
-      const double v6 = __ldcs(v + 6 * T), v7 = __ldcs(v + 7 * T), v8 = __ldcs(v + 8 * T);
+      const double* v = A.vals + vidx(at, r & 31, 0);
+      const double v0 = __ldcs(v), v1 = __ldcs(v + 32), v2 = __ldcs(v + 64);
+      const double v3 = __ldcs(v + 96), v4 = __ldcs(v + 128), v5 = __ldcs(v + 160);
+      const double v6 = __ldcs(v + 192), v7 = __ldcs(v + 224), v8 = __ldcs(v + 256);
       double x0 = x[3 * c], x1 = x[3 * c + 1], x2 = x[3 * c + 2];
       if (PMode == 2) {
         x0 = x0 + beta * pold[3 * c];
@@ -302,7 +302,7 @@ void set_matrix_csr(Ctx& c, int rows, const int64_t* row_ptr, const int32_t* col
       const int64_t at = base + static_cast<int64_t>(s) * kSlice;
       const int64_t k = order[s].second;
       hc[static_cast<size_t>(at)] = cols[k] | (order[s].first << kGroupShift);
-      for (int q = 0; q < 9; ++q) hv[static_cast<size_t>(q * total + at)] = vals[9 * k + q];
+      for (int q = 0; q < 9; ++q) hv[static_cast<size_t>(vidx(at, r % kSlice, q))] = vals[9 * k + q];
     }
   }
   A.total = total;
@@ -347,7 +347,7 @@ void download_csr(Ctx& c, int64_t* row_ptr, int32_t* cols, double* vals) {
     for (const auto& [col, at] : order) {
       if (cols) cols[cursor] = col;
       if (vals)
-        for (int q = 0; q < 9; ++q) vals[9 * cursor + q] = hv[static_cast<size_t>(q * A.total + at)];
+        for (int q = 0; q < 9; ++q) vals[9 * cursor + q] = hv[static_cast<size_t>(vidx(at, r % kSlice, q))];
       ++cursor;
     }
     if (row_ptr) row_ptr[r + 1] = cursor;
@@ -477,7 +477,7 @@ __global__ void k_dinv(SellView A, double* __restrict__ dinv) {
   for (int k = 0; k < len; ++k) {
     const int64_t at = base + (int64_t)k * kSlice;
     if ((A.cols[at] & kColMask) == r) {
-      for (int q = 0; q < 9; ++q) m[q] = A.vals[at + q * A.total];
+      for (int q = 0; q < 9; ++q) m[q] = A.vals[vidx(at, r & 31, q)];
       break;
     }
   }

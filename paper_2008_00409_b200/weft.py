@@ -428,8 +428,11 @@ class ClothMesh:
         return out
 
     def __del__(self):
-        if getattr(self, "_h", None):
-            LIB.weft_mesh_destroy(self._h)
+        if getattr(self, "_h", None) and LIB is not None:
+            try:
+                LIB.weft_mesh_destroy(self._h)
+            except Exception:
+                pass
             self._h = None
 
 
