@@ -419,11 +419,12 @@ struct PcgState {
   unsigned counter;
 };
 
+// Last-block-done: thread 0 publishes the block's partial (caller wrote it
+// before), fences once, and counts arrivals; only the last block reduces.
 __device__ __forceinline__ bool last_block(unsigned* counter) {
   __shared__ bool s_last;
-  __threadfence();
-  __syncthreads();
   if (threadIdx.x == 0) {
+    __threadfence();
     const unsigned t = atomicAdd(counter, 1u);
     s_last = (t == gridDim.x - 1);
   }
@@ -649,18 +650,44 @@ __global__ void __launch_bounds__(256) k_pcg_update(const PcgArgs* __restrict__ 
   const int i = block_row(g.pb, blockIdx.x, rend);
   double s[2] = {0.0, 0.0};
   if (i < rend) {
+    // all loads first (the arrays come through a struct, so the compiler
+    // cannot prove they do not alias and would otherwise serialise them)
+    double zv[3], pv[3], xv[3], rv[3], qv[3], m[9];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      zv[c] = z[3 * i + c];
+      pv[c] = first ? 0.0 : p[3 * i + c];
+      xv[c] = x[3 * i + c];
+      rv[c] = r[3 * i + c];
+      qv[c] = q[3 * i + c];
+    }
+    if (g.bj) {
+#pragma unroll
+      for (int k = 0; k < 9; ++k) m[k] = g.dinv[9 * (size_t)i + k];
+    }
     double pr[3], rr[3];
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-      const double zc = z[3 * i + c];
-      pr[c] = first ? zc : zc + beta * p[3 * i + c];
-      p[3 * i + c] = pr[c];
-      x[3 * i + c] = x[3 * i + c] + alpha * pr[c];
-      rr[c] = r[3 * i + c] - alpha * q[3 * i + c];
-      r[3 * i + c] = rr[c];
+      pr[c] = first ? zv[c] : zv[c] + beta * pv[c];
+      xv[c] = xv[c] + alpha * pr[c];
+      rr[c] = rv[c] - alpha * qv[c];
     }
     double z0, z1, z2;
-    precond_row(g.dinv, g.bj != 0, i, rr[0], rr[1], rr[2], z0, z1, z2);
+    if (g.bj) {  // apply_precond (solver.hpp:67-89)
+      z0 = ((0.0 + m[0] * rr[0]) + m[1] * rr[1]) + m[2] * rr[2];
+      z1 = ((0.0 + m[3] * rr[0]) + m[4] * rr[1]) + m[5] * rr[2];
+      z2 = ((0.0 + m[6] * rr[0]) + m[7] * rr[1]) + m[8] * rr[2];
+    } else {
+      z0 = rr[0];
+      z1 = rr[1];
+      z2 = rr[2];
+    }
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      p[3 * i + c] = pr[c];
+      x[3 * i + c] = xv[c];
+      r[3 * i + c] = rr[c];
+    }
     z[3 * i] = z0;
     z[3 * i + 1] = z1;
     z[3 * i + 2] = z2;
