@@ -167,6 +167,21 @@ __device__ __forceinline__ void row_product_1(const SellView& A, int r, const do
   y2 = a2;
 }
 
+// Asks the TMA unit to stream a whole slice (values + column words) into L2
+// with one bulk prefetch, so the per-row loads that follow hit L2 instead of
+// each paying a DRAM round trip (SASS: UBLKPF.L2).
+__device__ __forceinline__ void prefetch_slice_l2(const SellView& A, int slice) {
+  const int64_t s0 = A.slice_off[slice], s1 = A.slice_off[slice + 1];
+  const int64_t w = s1 - s0;  // slots (32 per row-width unit)
+  if (w <= 0) return;
+  const char* vals = reinterpret_cast<const char*>(A.vals + 9 * s0);
+  const char* cols = reinterpret_cast<const char*>(A.cols + s0);
+  const unsigned vbytes = static_cast<unsigned>(72 * w);
+  const unsigned cbytes = static_cast<unsigned>(4 * w);
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(vals), "r"(vbytes) : "memory");
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(cols), "r"(cbytes) : "memory");
+}
+
 // Two threads per row (single accumulation group): lane parity q takes
 // slots k = 2j + q, so each warp load instruction moves two coalesced
 // 128-byte segments (16 rows x slots 2j and 2j+1) and twice as many rows are
@@ -238,6 +253,7 @@ __global__ void __launch_bounds__(256) k_spmv_pair(SellView A, const double* __r
 __global__ void __launch_bounds__(256) k_spmv(SellView A, int ngroups, const double* __restrict__ x,
                                               double* __restrict__ y) {
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if ((threadIdx.x & 31) == 0 && r < A.rows) prefetch_slice_l2(A, r >> 5);
   if (r >= A.rows) return;
   double y0, y1, y2;
   if (ngroups == 1) row_product_1<0>(A, r, x, nullptr, 0.0, y0, y1, y2);
@@ -585,6 +601,7 @@ __global__ void __launch_bounds__(256) k_pcg_spmv(const PcgArgs* __restrict__ ar
     }
   }
   const int r = (kSingle && kPair) ? -1 : block_row(g.pb, blockIdx.x, rend);
+  if (kSingle && !kPair && (threadIdx.x & 31) == 0 && r < rend) prefetch_slice_l2(A, r >> 5);
   if (!(kSingle && kPair) && r < rend) {
     double y0, y1, y2;
     if constexpr (kSingle) {
