@@ -130,6 +130,12 @@ __device__ __forceinline__ void row_product(const SellView& A, int r, int ngroup
   }
 }
 
+// Matrix-stream load: WEFT_LDS(p) (default __ldg; evict-first __ldcs
+// measured slower or equal on B200 for this kernel).
+#ifndef WEFT_LDS
+#define WEFT_LDS(p) __ldg(p)
+#endif
+
 // Single accumulation group (n = 1 or interior rows): the column of slot
 // k+1 is fetched while slot k is processed, so the x gather of a slot only
 // waits on its own round trip; matrix words are streamed with evict-first
@@ -142,16 +148,16 @@ __device__ __forceinline__ void row_product_1(const SellView& A, int r, const do
   const int64_t base = A.slice_off[r >> 5] + (r & 31);
   const int64_t T = A.total;
   double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-  int cn = len > 0 ? (__ldcs(A.cols + base) & kColMask) : 0;
+  int cn = len > 0 ? (WEFT_LDS(A.cols + base) & kColMask) : 0;
 #pragma unroll 2
   for (int k = 0; k < len; ++k) {
     const int64_t at = base + (int64_t)k * kSlice;
     const int c = cn;
-    if (k + 1 < len) cn = __ldcs(A.cols + at + kSlice) & kColMask;
+    if (k + 1 < len) cn = WEFT_LDS(A.cols + at + kSlice) & kColMask;
     const double* v = A.vals + vidx(at, r & 31, 0);
-    const double v0 = __ldcs(v), v1 = __ldcs(v + 32), v2 = __ldcs(v + 64);
-    const double v3 = __ldcs(v + 96), v4 = __ldcs(v + 128), v5 = __ldcs(v + 160);
-    const double v6 = __ldcs(v + 192), v7 = __ldcs(v + 224), v8 = __ldcs(v + 256);
+    const double v0 = WEFT_LDS(v), v1 = WEFT_LDS(v + 32), v2 = WEFT_LDS(v + 64);
+    const double v3 = WEFT_LDS(v + 96), v4 = WEFT_LDS(v + 128), v5 = WEFT_LDS(v + 160);
+    const double v6 = WEFT_LDS(v + 192), v7 = WEFT_LDS(v + 224), v8 = WEFT_LDS(v + 256);
     double x0 = x[3 * c], x1 = x[3 * c + 1], x2 = x[3 * c + 2];
     if (PMode == 2) {
       x0 = x0 + beta * pold[3 * c];
@@ -198,18 +204,18 @@ __device__ __forceinline__ void row_product_pair(const SellView& A, int r, bool 
   const int64_t base = valid ? A.slice_off[r >> 5] + (r & 31) : 0;
   const int64_t T = A.total;
   double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-  int cn = par < len ? (__ldcs(A.cols + base + (int64_t)par * kSlice) & kColMask) : 0;
+  int cn = par < len ? (WEFT_LDS(A.cols + base + (int64_t)par * kSlice) & kColMask) : 0;
   for (int k0 = 0; k0 < kmax; k0 += 2) {
     const int k = k0 + par;
     double p0 = 0.0, p1 = 0.0, p2 = 0.0;
     if (k < len) {
       const int64_t at = base + (int64_t)k * kSlice;
       const int c = cn;
-      if (k + 2 < len) cn = __ldcs(A.cols + at + 2 * kSlice) & kColMask;
+      if (k + 2 < len) cn = WEFT_LDS(A.cols + at + 2 * kSlice) & kColMask;
       const double* v = A.vals + vidx(at, r & 31, 0);
-      const double v0 = __ldcs(v), v1 = __ldcs(v + 32), v2 = __ldcs(v + 64);
-      const double v3 = __ldcs(v + 96), v4 = __ldcs(v + 128), v5 = __ldcs(v + 160);
-      const double v6 = __ldcs(v + 192), v7 = __ldcs(v + 224), v8 = __ldcs(v + 256);
+      const double v0 = WEFT_LDS(v), v1 = WEFT_LDS(v + 32), v2 = WEFT_LDS(v + 64);
+      const double v3 = WEFT_LDS(v + 96), v4 = WEFT_LDS(v + 128), v5 = WEFT_LDS(v + 160);
+      const double v6 = WEFT_LDS(v + 192), v7 = WEFT_LDS(v + 224), v8 = WEFT_LDS(v + 256);
       double x0 = x[3 * c], x1 = x[3 * c + 1], x2 = x[3 * c + 2];
       if (PMode == 2) {
         x0 = x0 + beta * pold[3 * c];
@@ -253,7 +259,6 @@ __global__ void __launch_bounds__(256) k_spmv_pair(SellView A, const double* __r
 __global__ void __launch_bounds__(256) k_spmv(SellView A, int ngroups, const double* __restrict__ x,
                                               double* __restrict__ y) {
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if ((threadIdx.x & 31) == 0 && r < A.rows) prefetch_slice_l2(A, r >> 5);
   if (r >= A.rows) return;
   double y0, y1, y2;
   if (ngroups == 1) row_product_1<0>(A, r, x, nullptr, 0.0, y0, y1, y2);
@@ -601,7 +606,6 @@ __global__ void __launch_bounds__(256) k_pcg_spmv(const PcgArgs* __restrict__ ar
     }
   }
   const int r = (kSingle && kPair) ? -1 : block_row(g.pb, blockIdx.x, rend);
-  if (kSingle && !kPair && (threadIdx.x & 31) == 0 && r < rend) prefetch_slice_l2(A, r >> 5);
   if (!(kSingle && kPair) && r < rend) {
     double y0, y1, y2;
     if constexpr (kSingle) {
