@@ -1,0 +1,285 @@
+// weft_dropin.hpp — drop-in replacements for the reference's hot-path entry
+// points with the reference's own C++ signatures, implemented over the C-ABI
+// of libweft_gpu.so (include/weft_gpu.h). A maintainer of the reference
+// switches a call site from weft::fill_matrix(...) to weft::gpu::fill_matrix(...)
+// (same arguments, same return types, same exception classes); see
+// INTEGRATION.md.
+//
+// Header-only; include after the reference headers (proj/include) and link
+// against libweft_gpu.so. Only Real = double is supported on the GPU path
+// (the reference default, driver.hpp:35); float throws.
+#pragma once
+
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "weft/assembly.hpp"
+#include "weft/collision.hpp"
+#include "weft/solver.hpp"
+#include "weft/sparse.hpp"
+#include "weft_gpu.h"
+
+namespace weft::gpu {
+
+// Rethrows a C-ABI status as the reference's exception class.
+inline void check(weft_status s) {
+  if (s == WEFT_OK) return;
+  const std::string msg = weft_gpu_last_error();
+  switch (s) {
+    case WEFT_ERR_DIMENSION: throw DimensionError(msg);
+    case WEFT_ERR_SOLVER: throw SolverError(msg);
+    case WEFT_ERR_EXEC: throw ExecError(msg);
+    case WEFT_ERR_TOPOLOGY: throw TopologyError(msg);
+    case WEFT_ERR_SCHEDULE: throw ScheduleError(msg);
+    default: throw Error(msg);
+  }
+}
+
+// One GPU context per reference Engine (same partition count n, so the
+// SpMV / dot-product orders are the Engine(n) orders).
+class Context {
+ public:
+  explicit Context(int partitions, int cuda_device = 0) {
+    weft_gpu_options o{cuda_device, partitions, 0, partitions};
+    check(weft_gpu_create(&o, &ctx_));
+  }
+  ~Context() { weft_gpu_destroy(ctx_); }
+  Context(const Context&) = delete;
+  Context& operator=(const Context&) = delete;
+  weft_gpu_ctx* get() const { return ctx_; }
+
+ private:
+  weft_gpu_ctx* ctx_ = nullptr;
+};
+
+inline Context& context_for(const Engine& engine) {
+  static std::mutex mu;
+  static std::map<const Engine*, std::unique_ptr<Context>> ctxs;
+  std::lock_guard lock(mu);
+  auto& c = ctxs[&engine];
+  if (!c) c = std::make_unique<Context>(engine.devices());
+  return *c;
+}
+
+inline weft_element to_flat(const AssemblyElement& e) {
+  weft_element f{};
+  f.kind = static_cast<int32_t>(e.kind);
+  f.stencil_size = e.stencil_size;
+  for (int i = 0; i < 4; ++i) f.stencil[i] = e.stencil[static_cast<std::size_t>(i)];
+  f.damping = e.damping;
+  double* d = f.data;
+  std::visit(
+      [&](const auto& v) {
+        using T = std::decay_t<decltype(v)>;
+        if constexpr (std::is_same_v<T, StretchData>) {
+          for (int i = 0; i < 3; ++i) {
+            d[i] = v.pwu[static_cast<std::size_t>(i)];
+            d[3 + i] = v.pwv[static_cast<std::size_t>(i)];
+          }
+          d[6] = v.area;
+          d[7] = v.k_warp;
+          d[8] = v.k_weft;
+          d[9] = v.k_shear;
+        } else if constexpr (std::is_same_v<T, BendData>) {
+          d[0] = v.rest_angle;
+          d[1] = v.stiffness;
+        } else if constexpr (std::is_same_v<T, SpringData>) {
+          d[0] = v.rest_length;
+          d[1] = v.stiffness;
+        } else if constexpr (std::is_same_v<T, ExternalData>) {
+          for (int i = 0; i < 3; ++i) d[i] = v.force[i];
+          d[3] = v.drag;
+        } else {
+          for (int i = 0; i < 3; ++i) d[i] = v.normal[i];
+          for (int i = 0; i < 4; ++i) d[3 + i] = v.w[static_cast<std::size_t>(i)];
+          d[7] = v.bias;
+          d[8] = v.activation;
+          d[9] = v.stiffness;
+          d[10] = v.friction;
+          d[11] = v.tangential_damping;
+          d[12] = v.frozen_normal_force;
+          for (int i = 0; i < 3; ++i) d[13 + i] = v.rel_vel_bias[i];
+        }
+      },
+      e.data);
+  return f;
+}
+
+inline std::vector<double> flat3(std::span<const Vec3> v) {
+  std::vector<double> out(3 * v.size());
+  for (std::size_t i = 0; i < v.size(); ++i)
+    for (int c = 0; c < 3; ++c) out[3 * i + static_cast<std::size_t>(c)] = v[i][c];
+  return out;
+}
+
+// Global block CSR -> the reference's partitioned BELL type
+// (partition_matrix(from_entries(...)), sparse.hpp:103-147).
+inline PartitionedMatrix<double> to_partitioned(int rows, const std::vector<int64_t>& rp, const std::vector<int32_t>& cols,
+                                                const std::vector<double>& vals,
+                                                const std::vector<DevicePartition>& parts) {
+  std::vector<BlockEntry<double>> entries;
+  entries.reserve(cols.size());
+  for (int r = 0; r < rows; ++r)
+    for (int64_t k = rp[static_cast<std::size_t>(r)]; k < rp[static_cast<std::size_t>(r) + 1]; ++k) {
+      BlockEntry<double> e;
+      e.row = r;
+      e.col = cols[static_cast<std::size_t>(k)];
+      std::memcpy(e.m.data(), &vals[static_cast<std::size_t>(9 * k)], sizeof(double) * 9);
+      entries.push_back(e);
+    }
+  return partition_matrix(BellMatrix<double>::from_entries(rows, entries), parts);
+}
+
+inline void upload_partitioned(weft_gpu_ctx* ctx, const PartitionedMatrix<double>& a) {
+  const auto g = gather_matrix(a);
+  std::vector<int64_t> rp(static_cast<std::size_t>(g.block_rows()) + 1, 0);
+  std::vector<int32_t> cols;
+  std::vector<double> vals;
+  for (int r = 0; r < g.block_rows(); ++r) {
+    for (int s = 0; s < g.ell_width(); ++s) {
+      const int32_t c = g.col_at(r, s);
+      if (c == BellMatrix<double>::kNoBlock) break;
+      cols.push_back(c);
+      for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) vals.push_back(g.value_at(r, s, i, j));
+    }
+    rp[static_cast<std::size_t>(r) + 1] = static_cast<int64_t>(cols.size());
+  }
+  check(weft_gpu_set_matrix(ctx, g.block_rows(), rp.data(), cols.data(), vals.data()));
+}
+
+// fill_matrix<Real> (assembly.hpp:74-77): same signature and results.
+template <class Real>
+AssembledSystem<Real> fill_matrix(Engine& engine, const DistributedElements& /*dist*/, const SystemInputs& in,
+                                  const std::vector<DevicePartition>& partitions) {
+  if constexpr (!std::is_same_v<Real, double>) {
+    throw Error("weft::gpu::fill_matrix: only double precision runs on the GPU path");
+  } else {
+    if (in.dt <= 0.0) throw DimensionError("fill_matrix: dt must be positive");
+    weft_gpu_ctx* ctx = context_for(engine).get();
+    const int p = partitions.empty() ? 0 : partitions.back().end;
+    std::vector<uint8_t> pinned(in.pinned.begin(), in.pinned.end());
+    check(weft_gpu_set_vertices(ctx, p, in.mass.data(), pinned.data()));
+    std::vector<weft_element> elems;
+    elems.reserve(in.elements.size());
+    for (const auto& e : in.elements) elems.push_back(to_flat(e));
+    check(weft_gpu_set_elements(ctx, static_cast<int64_t>(elems.size()), elems.data()));
+    const auto xc = flat3(in.x_current), xa = flat3(in.x_advanced), v = flat3(in.velocity);
+    check(weft_gpu_fill_matrix(ctx, xc.data(), xa.data(), v.data(), in.dt,
+                               in.mode == JacobianMode::Exact ? WEFT_JAC_EXACT : WEFT_JAC_SPD_PROJECTED));
+    weft_matrix_info info{};
+    check(weft_gpu_matrix_info(ctx, &info));
+    std::vector<int64_t> rp(static_cast<std::size_t>(info.block_rows) + 1);
+    std::vector<int32_t> cols(static_cast<std::size_t>(info.nnzb));
+    std::vector<double> vals(9 * static_cast<std::size_t>(info.nnzb)), rhs(3 * static_cast<std::size_t>(p));
+    check(weft_gpu_download_matrix(ctx, rp.data(), cols.data(), vals.data()));
+    check(weft_gpu_download_rhs(ctx, rhs.data()));
+    AssembledSystem<double> out{to_partitioned(info.block_rows, rp, cols, vals, partitions),
+                                DistVector<double>(&engine, partitions)};
+    for (const auto& part : partitions) {
+      auto local = out.rhs.local(part.device_id);
+      std::copy(rhs.begin() + 3 * part.begin, rhs.begin() + 3 * part.end, local.begin());
+    }
+    return out;
+  }
+}
+
+// spmv_pipelined<Real> (sparse.hpp:72-101).
+template <class Real>
+void spmv_pipelined(Engine& engine, const PartitionedMatrix<Real>& a, const ValidatedSchedule& sched,
+                    const DistVector<Real>& x, DistVector<Real>& y, SpmvWorkspace<Real>& /*ws*/) {
+  if constexpr (!std::is_same_v<Real, double>) {
+    throw Error("weft::gpu::spmv_pipelined: only double precision runs on the GPU path");
+  } else {
+    if (engine.devices() != a.devices || sched.devices() != a.devices)
+      throw DimensionError("spmv_pipelined: engine/schedule/matrix device counts differ");
+    weft_gpu_ctx* ctx = context_for(engine).get();
+    upload_partitioned(ctx, a);
+    const auto xg = x.gather();
+    std::vector<double> yg(xg.size());
+    check(weft_gpu_spmv(ctx, xg.data(), yg.data()));
+    for (const auto& part : a.partitions) {
+      auto local = y.local(part.device_id);
+      std::copy(yg.begin() + 3 * part.begin, yg.begin() + 3 * part.end, local.begin());
+    }
+  }
+}
+
+// pcg_solve<Real> (solver.hpp:36-178).
+template <class Real>
+PcgReport pcg_solve(Engine& engine, const PartitionedMatrix<Real>& a, const ValidatedSchedule& /*sched*/,
+                    const DistVector<Real>& b, DistVector<Real>& x, const PcgConfig& config) {
+  if constexpr (!std::is_same_v<Real, double>) {
+    throw Error("weft::gpu::pcg_solve: only double precision runs on the GPU path");
+  } else {
+    if (engine.devices() != a.devices) throw DimensionError("pcg_solve: engine/matrix device count mismatch");
+    weft_gpu_ctx* ctx = context_for(engine).get();
+    upload_partitioned(ctx, a);
+    const auto bg = b.gather();
+    std::vector<double> xg(bg.size());
+    weft_pcg_config cfg{config.rel_tolerance, config.max_iterations,
+                        config.preconditioner == Preconditioner::None ? WEFT_PRECOND_NONE : WEFT_PRECOND_BLOCK_JACOBI};
+    std::vector<double> hist(static_cast<std::size_t>(std::max(config.max_iterations, 1)));
+    std::vector<double> phist(hist.size());
+    weft_pcg_report rep{0, 0, 0.0, hist.data(), phist.data()};
+    check(weft_gpu_pcg(ctx, bg.data(), xg.data(), &cfg, &rep));
+    for (const auto& part : a.partitions) {
+      auto local = x.local(part.device_id);
+      std::copy(xg.begin() + 3 * part.begin, xg.begin() + 3 * part.end, local.begin());
+    }
+    PcgReport out;
+    out.iterations = rep.iterations;
+    out.converged = rep.converged != 0;
+    out.rel_residual = rep.rel_residual;
+    out.residual_history.assign(hist.begin(), hist.begin() + rep.iterations);
+    out.precond_norm_history.assign(phist.begin(), phist.begin() + rep.iterations);
+    return out;
+  }
+}
+
+// build_grid (collision.cpp:118-179): the device grid downloaded into the
+// reference's HashGrid / WorkloadTable types.
+inline GridBuildResult build_grid(const CollisionSoup& soup, std::span<const Vec3> x_begin, std::span<const Vec3> x_end,
+                                  CollisionMode mode, const CollisionParams& params, int cuda_device = 0) {
+  static std::unique_ptr<Context> ctx_holder;
+  if (!ctx_holder) ctx_holder = std::make_unique<Context>(1, cuda_device);
+  weft_gpu_ctx* ctx = ctx_holder->get();
+  std::vector<int32_t> tris(3 * soup.triangles.size());
+  for (std::size_t t = 0; t < soup.triangles.size(); ++t)
+    for (int c = 0; c < 3; ++c) tris[3 * t + static_cast<std::size_t>(c)] = soup.triangles[t][static_cast<std::size_t>(c)];
+  check(weft_gpu_set_soup(ctx, soup.vertex_count, static_cast<int32_t>(soup.triangles.size()), tris.data()));
+  const auto x0 = flat3(x_begin), x1 = flat3(x_end);
+  check(weft_gpu_build_grid(ctx, x0.data(), x1.data(),
+                            mode == CollisionMode::Continuous ? WEFT_CONTINUOUS : WEFT_DISCRETE, params.thickness,
+                            params.cell_scale));
+  weft_grid_info info{};
+  check(weft_gpu_grid_info(ctx, &info));
+  std::vector<uint64_t> keys(static_cast<std::size_t>(info.cells));
+  std::vector<int64_t> off(static_cast<std::size_t>(info.cells) + 1), prefix(off.size());
+  std::vector<int32_t> cell_tris(static_cast<std::size_t>(info.entries));
+  std::vector<int64_t> boxes(6 * soup.triangles.size());
+  check(weft_gpu_download_grid(ctx, keys.data(), off.data(), cell_tris.data(), prefix.data(), boxes.data()));
+  GridBuildResult out;
+  out.grid.cell_size = info.cell_size;
+  out.grid.cell_keys = keys;
+  for (int64_t c = 0; c < info.cells; ++c) {
+    out.grid.cell_tris.emplace_back(cell_tris.begin() + off[static_cast<std::size_t>(c)],
+                                    cell_tris.begin() + off[static_cast<std::size_t>(c) + 1]);
+    const int64_t s = off[static_cast<std::size_t>(c) + 1] - off[static_cast<std::size_t>(c)];
+    out.table.counts.push_back(s * (s - 1) / 2);
+  }
+  out.table.prefix = prefix;
+  out.table.total = prefix.back();
+  out.grid.tri_boxes.resize(soup.triangles.size());
+  for (std::size_t t = 0; t < soup.triangles.size(); ++t)
+    for (int c = 0; c < 6; ++c) out.grid.tri_boxes[t][static_cast<std::size_t>(c)] = boxes[6 * t + static_cast<std::size_t>(c)];
+  return out;
+}
+
+}  // namespace weft::gpu

@@ -1,0 +1,164 @@
+// Runs reference-style checks through the C++ drop-in (weft::gpu::*),
+// comparing against the reference's own CPU functions on the reference's
+// own fixture generators (src/oracle). Built by `make -C oracle dropin`
+// against the unmodified reference objects; executed by
+// tests/test_gpu_dropin.py on a GPU box.
+#define DOCTEST_CONFIG_IMPLEMENT_WITH_MAIN
+#include <doctest.h>
+
+#include "oracle/collision_oracle.hpp"
+#include "oracle/physics_oracle.hpp"
+#include "oracle/sparse_oracle.hpp"
+#include "weft/physics.hpp"
+#include "weft_dropin.hpp"
+
+using namespace weft;
+
+namespace {
+
+Eigen::MatrixXd dense(const PartitionedMatrix<double>& m) { return oracle::bell_to_dense(gather_matrix(m)); }
+
+}  // namespace
+
+TEST_CASE("drop-in fill_matrix equals the reference fill_matrix (bitwise matrix, 1e-12 rhs), n in {1,2,4}") {
+  oracle::Rng rng(22);
+  for (int trial = 0; trial < 6; ++trial) {
+    auto mesh = oracle::random_cloth(rng, 7);
+    const int p = mesh.vertex_count();
+    SimState state = SimState::rest(mesh);
+    for (auto& v : state.v) v = rng.vec3(-0.3, 0.3);
+    std::vector<std::uint8_t> pinned(static_cast<std::size_t>(p), 0);
+    pinned[0] = 1;
+    MaterialParams params;
+    params.damping = 0.001;
+    const auto elements = build_elements(mesh, params, Vec3(0, 0, -9.81), Vec3::Zero());
+    std::vector<Vec3> adv(state.x.size());
+    for (std::size_t i = 0; i < adv.size(); ++i) adv[i] = state.x[i] + 0.01 * state.v[i];
+    SystemInputs in;
+    in.elements = elements;
+    in.x_current = state.x;
+    in.x_advanced = adv;
+    in.velocity = state.v;
+    in.mass = mesh.vertex_mass;
+    in.pinned = pinned;
+    in.dt = 0.01;
+    for (int n : {1, 2, 4}) {
+      CAPTURE(trial);
+      CAPTURE(n);
+      Engine engine(n);
+      const auto parts = make_partitions(p, n);
+      const auto dist = distribute_elements(elements, parts);
+      const auto ref = fill_matrix<double>(engine, dist, in, parts);
+      const auto gpu = gpu::fill_matrix<double>(engine, dist, in, parts);
+      CHECK((dense(ref.matrix) - dense(gpu.matrix)).cwiseAbs().maxCoeff() == 0.0);
+      const auto rb = ref.rhs.gather(), gb = gpu.rhs.gather();
+      double scale = 1e-300, err = 0.0;
+      for (std::size_t i = 0; i < rb.size(); ++i) {
+        scale = std::max(scale, std::abs(rb[i]));
+        err = std::max(err, std::abs(rb[i] - gb[i]));
+      }
+      CHECK(err <= 1e-12 * scale);
+    }
+  }
+}
+
+TEST_CASE("drop-in spmv_pipelined is bitwise equal to the order-matched serial oracle") {
+  oracle::Rng rng(6);
+  for (int n : {1, 2, 4}) {
+    Engine engine(n);
+    ValidatedSchedule sched = n == 1 ? ValidatedSchedule() : ValidatedSchedule(generate_work_queues(FatTree::make(n)), n);
+    for (int trial = 0; trial < 10; ++trial) {
+      const int rows = rng.uniform_int(n, 40);
+      const auto global = oracle::random_bell(rng, rows, 3);
+      const auto parts = make_partitions(rows, n);
+      const auto split = partition_matrix(global, parts);
+      std::vector<double> xg(static_cast<std::size_t>(3 * rows));
+      for (auto& v : xg) v = rng.uniform(-2.0, 2.0);
+      DistVector<double> x(&engine, parts), y(&engine, parts);
+      for (const auto& part : parts)
+        std::copy(xg.begin() + 3 * part.begin, xg.begin() + 3 * part.end, x.local(part.device_id).begin());
+      SpmvWorkspace<double> ws(n, split.padded_len);
+      gpu::spmv_pipelined(engine, split, sched, x, y, ws);
+      CHECK(y.gather() == oracle::spmv_partitioned_serial<double>(split, sched, xg));
+    }
+  }
+}
+
+TEST_CASE("drop-in pcg_solve: hand-solved 2x2, non-SPD error, cloth system vs reference") {
+  {
+    std::vector<BlockEntry<double>> entries(1);
+    entries[0].m = {4, 1, 0, 1, 3, 0, 0, 0, 1};
+    const auto a = BellMatrix<double>::from_entries(1, entries);
+    Engine engine(1);
+    const auto parts = make_partitions(1, 1);
+    const auto split = partition_matrix(a, parts);
+    DistVector<double> b(&engine, parts), x(&engine, parts);
+    b.local(0)[0] = 1;
+    b.local(0)[1] = 2;
+    PcgConfig cfg;
+    cfg.rel_tolerance = 1e-12;
+    const auto rep = gpu::pcg_solve(engine, split, ValidatedSchedule(), b, x, cfg);
+    CHECK(rep.converged);
+    CHECK(x.gather()[0] == doctest::Approx(1.0 / 11.0).epsilon(1e-10));
+    CHECK(x.gather()[1] == doctest::Approx(7.0 / 11.0).epsilon(1e-10));
+  }
+  {
+    std::vector<BlockEntry<double>> entries(1);
+    entries[0].m = {-1, 0, 0, 0, -1, 0, 0, 0, -1};
+    const auto a = BellMatrix<double>::from_entries(1, entries);
+    Engine engine(1);
+    const auto parts = make_partitions(1, 1);
+    DistVector<double> b(&engine, parts), x(&engine, parts);
+    b.fill(1.0);
+    PcgConfig cfg;
+    cfg.preconditioner = Preconditioner::None;
+    CHECK_THROWS_AS(gpu::pcg_solve(engine, partition_matrix(a, parts), ValidatedSchedule(), b, x, cfg), SolverError);
+  }
+  oracle::Rng rng(35);
+  auto mesh = oracle::random_cloth(rng, 7);
+  const int p = mesh.vertex_count();
+  SimState state = SimState::rest(mesh);
+  for (auto& v : state.v) v = rng.vec3(-0.3, 0.3);
+  std::vector<std::uint8_t> pinned(static_cast<std::size_t>(p), 0);
+  pinned[0] = 1;
+  for (int n : {1, 2}) {
+    Engine engine(n);
+    const auto sys = step_system<double>(engine, mesh, state, MaterialParams{}, pinned, {}, 1.0 / 150.0,
+                                         Vec3(0, 0, -9.81), Vec3::Zero());
+    ValidatedSchedule sched = n == 1 ? ValidatedSchedule() : ValidatedSchedule(generate_work_queues(FatTree::make(n)), n);
+    PcgConfig cfg;
+    cfg.rel_tolerance = 1e-10;
+    DistVector<double> xr(&engine, sys.matrix.partitions), xgpu(&engine, sys.matrix.partitions);
+    const auto rr = pcg_solve(engine, sys.matrix, sched, sys.rhs, xr, cfg);
+    const auto rg = gpu::pcg_solve(engine, sys.matrix, sched, sys.rhs, xgpu, cfg);
+    CHECK(rg.converged);
+    CHECK(std::abs(rg.iterations - rr.iterations) <= 2);
+    const auto a = xr.gather(), g = xgpu.gather();
+    double scale = 1e-300, err = 0.0;
+    for (std::size_t i = 0; i < a.size(); ++i) {
+      scale = std::max(scale, std::abs(a[i]));
+      err = std::max(err, std::abs(a[i] - g[i]));
+    }
+    CHECK(err <= 1e-8 * scale);
+  }
+}
+
+TEST_CASE("drop-in build_grid equals the reference build_grid bit for bit") {
+  oracle::Rng rng(43);
+  for (int trial = 0; trial < 4; ++trial) {
+    const auto scene = oracle::random_two_cloth_scene(rng, 8);
+    for (CollisionMode mode : {CollisionMode::Discrete, CollisionMode::Continuous}) {
+      CollisionParams params;
+      params.thickness = 0.01;
+      const auto ref = build_grid(scene.soup, scene.x_begin, scene.x_end, mode, params);
+      const auto gpu = gpu::build_grid(scene.soup, scene.x_begin, scene.x_end, mode, params);
+      CHECK(ref.grid.cell_size == gpu.grid.cell_size);
+      CHECK(ref.grid.cell_keys == gpu.grid.cell_keys);
+      CHECK(ref.grid.cell_tris == gpu.grid.cell_tris);
+      CHECK(ref.grid.tri_boxes == gpu.grid.tri_boxes);
+      CHECK(ref.table.counts == gpu.table.counts);
+      CHECK(ref.table.prefix == gpu.table.prefix);
+      CHECK(ref.table.total == gpu.table.total);
+    }
+  }
+}
