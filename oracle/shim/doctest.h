@@ -145,6 +145,7 @@ inline int run_all() {
   auto& s = state();
   std::printf("[doctest-shim] test cases: %zu | failed: %d | assertions: %d | failed assertions: %d\n",
               registry().size(), failed_cases, s.checks, s.failures);
+  std::fflush(stdout);
   return failed_cases;
 }
 

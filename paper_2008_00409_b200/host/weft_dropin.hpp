@@ -58,11 +58,15 @@ class Context {
   weft_gpu_ctx* ctx_ = nullptr;
 };
 
+// Contexts are cached per partition count (an Engine's only property the
+// GPU path depends on), so short-lived Engines reuse device state.
 inline Context& context_for(const Engine& engine) {
+  // Intentionally leaked: contexts must not be torn down during static
+  // destruction, after the CUDA runtime itself may already be gone.
   static std::mutex mu;
-  static std::map<const Engine*, std::unique_ptr<Context>> ctxs;
+  static auto* ctxs = new std::map<int, std::unique_ptr<Context>>();
   std::lock_guard lock(mu);
-  auto& c = ctxs[&engine];
+  auto& c = (*ctxs)[engine.devices()];
   if (!c) c = std::make_unique<Context>(engine.devices());
   return *c;
 }
@@ -247,8 +251,7 @@ PcgReport pcg_solve(Engine& engine, const PartitionedMatrix<Real>& a, const Vali
 // reference's HashGrid / WorkloadTable types.
 inline GridBuildResult build_grid(const CollisionSoup& soup, std::span<const Vec3> x_begin, std::span<const Vec3> x_end,
                                   CollisionMode mode, const CollisionParams& params, int cuda_device = 0) {
-  static std::unique_ptr<Context> ctx_holder;
-  if (!ctx_holder) ctx_holder = std::make_unique<Context>(1, cuda_device);
+  static Context* ctx_holder = new Context(1, cuda_device);  // leaked on purpose (see context_for)
   weft_gpu_ctx* ctx = ctx_holder->get();
   std::vector<int32_t> tris(3 * soup.triangles.size());
   for (std::size_t t = 0; t < soup.triangles.size(); ++t)
