@@ -101,6 +101,32 @@ weft_status weft_gpu_create(const weft_gpu_options* opts, weft_gpu_ctx** out);
 weft_status weft_gpu_destroy(weft_gpu_ctx* ctx);
 
 /* ---------------------------------------------------------------------- */
+/* Rank group: one process per GPU (replaces the in-process interconnect  */
+/* of Engine::run_pipelined / all_reduce_sum, proj/src/exec.cpp:170-307)   */
+/* ---------------------------------------------------------------------- */
+
+/* A context whose partition range [part_begin, part_end) is a proper subset
+ * of [0, partitions) is one rank of a group: ranks own equal contiguous
+ * partition ranges (rank = part_begin / (part_end - part_begin)), hold only
+ * their rows of the matrix, assemble only their rows, and exchange halo
+ * vectors, reduction partials and state rows through peer memory.
+ * Protocol: every rank calls weft_gpu_set_vertices (or weft_gpu_set_matrix),
+ * then weft_gpu_comm_export, shares the handle bytes with all ranks (any
+ * transport, e.g. torch.distributed.all_gather_object), then
+ * weft_gpu_comm_attach with all handles in rank order. Afterwards every
+ * collective entry point (spmv, pcg, sim_step) must be called by all ranks
+ * in the same order. Destroy only after a host barrier. */
+enum { WEFT_IPC_HANDLE_BYTES = 64 };
+weft_status weft_gpu_comm_export(weft_gpu_ctx* ctx, void* handle_out /* WEFT_IPC_HANDLE_BYTES */);
+weft_status weft_gpu_comm_attach(weft_gpu_ctx* ctx, const void* handles /* world * WEFT_IPC_HANDLE_BYTES */);
+typedef struct weft_rank_info {
+  int32_t world, rank;
+  int32_t first_row, rows; /* global block rows [first_row, first_row + rows) held here */
+  int32_t global_rows;
+} weft_rank_info;
+weft_status weft_gpu_rank_info(weft_gpu_ctx* ctx, weft_rank_info* info);
+
+/* ---------------------------------------------------------------------- */
 /* Partitions and schedule (proj/src/exec.cpp:10-27, proj/src/topology.cpp)*/
 /* ---------------------------------------------------------------------- */
 
@@ -122,8 +148,10 @@ weft_status weft_gpu_set_matrix(weft_gpu_ctx* ctx, int32_t block_rows, const int
 
 /* y = A x with the pipelined order of spmv_pipelined (sparse.hpp:72-101):
  * per row the own-partition sub-block sum first, then the other sub-blocks
- * in work-queue order. x, y: 3*block_rows doubles. Bitwise equal to
- * oracle::spmv_partitioned_serial (src/oracle/sparse_oracle.hpp:12-42). */
+ * in work-queue order. x, y: 3*global_rows doubles. Bitwise equal to
+ * oracle::spmv_partitioned_serial (src/oracle/sparse_oracle.hpp:12-42).
+ * In a rank group only this rank's rows of x are read (the others are
+ * gathered from their owners) and only its rows of y are written. */
 weft_status weft_gpu_spmv(weft_gpu_ctx* ctx, const double* x, double* y);
 
 /* Matrix shape of the context's current system (assembled or loaded). */
@@ -135,10 +163,12 @@ typedef struct weft_matrix_info {
 } weft_matrix_info;
 weft_status weft_gpu_matrix_info(weft_gpu_ctx* ctx, weft_matrix_info* info);
 
-/* Downloads the current system as global block CSR, ascending columns
- * (gather_matrix, sparse.hpp:149-173). Any pointer may be NULL. */
+/* Downloads the current system as block CSR, ascending columns
+ * (gather_matrix, sparse.hpp:149-173): all rows, or this rank's rows in a
+ * rank group (weft_gpu_rank_info). Any pointer may be NULL. */
 weft_status weft_gpu_download_matrix(weft_gpu_ctx* ctx, int64_t* row_ptr, int32_t* cols, double* vals);
-/* Downloads the assembled right-hand side (3*block_rows doubles). */
+/* Downloads the assembled right-hand side of the held rows
+ * (3*block_rows doubles). */
 weft_status weft_gpu_download_rhs(weft_gpu_ctx* ctx, double* rhs);
 
 /* ---------------------------------------------------------------------- */
@@ -164,7 +194,9 @@ typedef struct weft_pcg_report { /* PcgReport, solver.hpp:23-29 */
 
 /* Solves A x = b for the context's current matrix (pcg_solve,
  * solver.hpp:36-178). b may be NULL to use the assembled rhs. x receives the
- * solution (3*block_rows doubles; NULL keeps it on the device). Returns
+ * solution (3*global_rows doubles; NULL keeps it on the device). In a rank
+ * group b and x are full-length, only this rank's rows are read/written,
+ * and the result is bitwise that of one context with the same partitions. Returns
  * WEFT_ERR_SOLVER with the reference's message on non-finite/non-positive
  * curvature or divergence; non-convergence is only flagged. */
 weft_status weft_gpu_pcg(weft_gpu_ctx* ctx, const double* b, double* x, const weft_pcg_config* config,

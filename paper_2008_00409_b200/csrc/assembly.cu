@@ -44,7 +44,7 @@ void set_vertices(Ctx& c, int p, const double* mass, const uint8_t* pinned) {
   if (p >= (1 << 28)) throw Error(WEFT_ERR_DIMENSION, "more than 2^28 vertices");
   if (p < c.nparts) throw Error(WEFT_ERR_DIMENSION, "fewer vertices than partitions");
   c.p = p;
-  c.pm = PartMap::make(p, c.nparts);
+  set_rows(c, p);
   c.mass.upload(mass, static_cast<size_t>(p), c.stream);
   c.pinned.upload(pinned, static_cast<size_t>(p), c.stream);
   c.n_static = c.n_contacts = 0;
@@ -407,12 +407,12 @@ __device__ __forceinline__ void for_union(const MergeIn& m, int r, F&& f) {
   }
 }
 
-__global__ void k_merge_len(int p, MergeIn m, int32_t* __restrict__ len) {
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= p) return;
+__global__ void k_merge_len(int row0, int nloc, MergeIn m, int32_t* __restrict__ len) {
+  const int lr = blockIdx.x * blockDim.x + threadIdx.x;
+  if (lr >= nloc) return;
   int n = 0;
-  for_union(m, r, [&](int) { ++n; });
-  len[r] = n;
+  for_union(m, row0 + lr, [&](int) { ++n; });
+  len[lr] = n;
 }
 
 __global__ void k_slice_width(int p, int nslices, const int32_t* __restrict__ len, int64_t* __restrict__ w) {
@@ -426,12 +426,14 @@ __global__ void k_slice_width(int p, int nslices, const int32_t* __restrict__ le
 // Writes the row's columns grouped by accumulation order: own partition
 // first, then the work-queue order (sparse.hpp:89-95); ascending inside a
 // group. Padding slots get -1.
-__global__ void k_merge_fill(int p, MergeIn m, PartMap pm, GroupOrder go, const int64_t* __restrict__ soff,
-                             const int32_t* __restrict__ len, int32_t* __restrict__ cols) {
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= p) return;
-  const int s = r >> 5;
-  const int64_t base = soff[s] + (r & 31);
+__global__ void k_merge_fill(int row0, int nloc, MergeIn m, PartMap pm, GroupOrder go,
+                             const int64_t* __restrict__ soff, const int32_t* __restrict__ len,
+                             int32_t* __restrict__ cols) {
+  const int lr = blockIdx.x * blockDim.x + threadIdx.x;
+  if (lr >= nloc) return;
+  const int r = row0 + lr;
+  const int s = lr >> 5;
+  const int64_t base = soff[s] + (lr & 31);
   const int width = static_cast<int>((soff[s + 1] - soff[s]) / kSlice);
   const int d = pm.owner(r);
   int k = 0;
@@ -460,13 +462,15 @@ static void build_layout(Ctx& c) {
     m.ccol = ccol.data();
   }
   SellMatrix& A = c.A;
-  A.rows = p;
-  A.nslices = div_up(p, kSlice);
-  A.rowlen.resize(static_cast<size_t>(p) + 1);
+  const int nloc = c.row1 - c.row0;  // this rank's rows (all rows when world == 1)
+  A.rows = nloc;
+  A.row0 = c.row0;
+  A.nslices = div_up(nloc, kSlice);
+  A.rowlen.resize(static_cast<size_t>(nloc) + 1);
   A.slice_off.resize(static_cast<size_t>(A.nslices) + 1);
-  if (p) {
-    k_merge_len<<<div_up(p, 256), 256, 0, ls(c)>>>(p, m, A.rowlen.data());
-    k_slice_width<<<div_up(A.nslices, 256), 256, 0, ls(c)>>>(p, A.nslices, A.rowlen.data(), A.slice_off.data());
+  if (nloc) {
+    k_merge_len<<<div_up(nloc, 256), 256, 0, ls(c)>>>(c.row0, nloc, m, A.rowlen.data());
+    k_slice_width<<<div_up(A.nslices, 256), 256, 0, ls(c)>>>(nloc, A.nslices, A.rowlen.data(), A.slice_off.data());
   }
   WG_CUDA(cudaMemsetAsync(A.slice_off.data() + A.nslices, 0, sizeof(int64_t), s));
   size_t tmp = 0;
@@ -480,14 +484,14 @@ static void build_layout(Ctx& c) {
   red.resize(2);
   int* lenp = A.rowlen.data();
   size_t t1 = 0, t2 = 0;
-  cub::DeviceReduce::Sum(nullptr, t1, lenp, red.data(), p, s);
-  cub::DeviceReduce::Max(nullptr, t2, lenp, reinterpret_cast<int*>(red.data() + 1), p, s);
+  cub::DeviceReduce::Sum(nullptr, t1, lenp, red.data(), nloc, s);
+  cub::DeviceReduce::Max(nullptr, t2, lenp, reinterpret_cast<int*>(red.data() + 1), nloc, s);
   t = scratch(c, std::max(t1, t2));
   int64_t hr[2] = {0, 0};
-  if (p) {
-    WG_CUDA(cub::DeviceReduce::Sum(t, t1, lenp, red.data(), p, s));
+  if (nloc) {
+    WG_CUDA(cub::DeviceReduce::Sum(t, t1, lenp, red.data(), nloc, s));
     WG_CUDA(cudaMemsetAsync(red.data() + 1, 0, sizeof(int64_t), s));
-    WG_CUDA(cub::DeviceReduce::Max(t, t2, lenp, reinterpret_cast<int*>(red.data() + 1), p, s));
+    WG_CUDA(cub::DeviceReduce::Max(t, t2, lenp, reinterpret_cast<int*>(red.data() + 1), nloc, s));
     WG_CUDA(cudaMemcpyAsync(hr, red.data(), sizeof(hr), cudaMemcpyDeviceToHost, s));
   }
   WG_CUDA(cudaStreamSynchronize(s));
@@ -496,8 +500,9 @@ static void build_layout(Ctx& c) {
   A.max_len = static_cast<int>(hr[1] & 0xffffffff);
   A.cols.resize(static_cast<size_t>(total) + 1);
   A.vals.resize(9 * static_cast<size_t>(total) + 9);
-  if (p)
-    k_merge_fill<<<div_up(p, 256), 256, 0, ls(c)>>>(p, m, c.pm, c.go, A.slice_off.data(), A.rowlen.data(), A.cols.data());
+  if (nloc)
+    k_merge_fill<<<div_up(nloc, 256), 256, 0, ls(c)>>>(c.row0, nloc, m, c.pm, c.go, A.slice_off.data(), A.rowlen.data(),
+                                                      A.cols.data());
   WG_CUDA(cudaGetLastError());
   WG_CUDA(cudaStreamSynchronize(s));  // cptr/ccol die here
 }
@@ -508,7 +513,8 @@ static void build_layout(Ctx& c) {
 constexpr int kFillThreadsConst = 64;
 
 struct FillArgs {
-  int p;
+  int p;     // held rows (local row lr = global row - row0)
+  int row0;
   int64_t n_static;
   double dt;
   bool exact;
@@ -551,11 +557,12 @@ struct Acc {
 template <bool Wide, bool Exact>
 __global__ void __launch_bounds__(64) k_fill(FillArgs f) {
   extern __shared__ double smem[];
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  const int len = r < f.p ? f.rowlen[r] : 0;
-  const bool mine = r < f.p && (Wide ? len > f.wcap : len <= f.wcap);
+  const int lr = blockIdx.x * blockDim.x + threadIdx.x;
+  const int len = lr < f.p ? f.rowlen[lr] : 0;
+  const bool mine = lr < f.p && (Wide ? len > f.wcap : len <= f.wcap);
   if (!mine) return;
-  const int64_t base = f.slice_off[r >> 5] + (r & 31);
+  const int r = f.row0 + lr;
+  const int64_t base = f.slice_off[lr >> 5] + (lr & 31);
   int32_t* colbuf = reinterpret_cast<int32_t*>(smem + (size_t)f.wcap * 9 * blockDim.x);
   Acc<Wide> acc{smem, (int)threadIdx.x, (int)blockDim.x, f.vals, f.total, base};
   static_assert(kFillThreadsConst % 32 == 0, "row lanes must match threadIdx.x % 32");
@@ -643,7 +650,7 @@ __global__ void __launch_bounds__(64) k_fill(FillArgs f) {
   if (!Wide) {
     for (int k = 0; k < len; ++k)
 #pragma unroll
-      for (int q = 0; q < 9; ++q) f.vals[vidx(base + (int64_t)k * kSlice, r & 31, q)] = acc.at(k, q);
+      for (int q = 0; q < 9; ++q) f.vals[vidx(base + (int64_t)k * kSlice, lr & 31, q)] = acc.at(k, q);
   }
 }
 
@@ -769,6 +776,7 @@ __device__ __forceinline__ bool elem_block(int kind, const double* __restrict__ 
 
 struct ElemArgs {
   int64_t n;
+  const int64_t* __restrict__ list;  // element ids to evaluate (null: 0..n-1)
   double dt;
   const int4* __restrict__ est;
   const int2* __restrict__ einfo;
@@ -782,8 +790,9 @@ struct ElemArgs {
 };
 
 __global__ void __launch_bounds__(128) k_elem_eval(ElemArgs g) {
-  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (e >= g.n) return;
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= g.n) return;
+  const int64_t e = g.list ? g.list[i] : i;
   const int4 s4 = g.est[e];
   const int2 info = g.einfo[e];
   const int kind = info.x & 0xff, ss = (info.x >> 8) & 0xff;
@@ -976,7 +985,8 @@ __global__ void __launch_bounds__(128) k_elem_eval(ElemArgs g) {
 }
 
 struct SlotArgs {
-  int p;
+  int p;     // held rows
+  int row0;  // global index of the first
   int64_t n_static;
   double dt;
   const int64_t* __restrict__ slice_off;
@@ -1037,8 +1047,8 @@ __global__ void __launch_bounds__(kSlotWarps * 32, 2) k_fill_slots(SlotArgs g) {
   __shared__ double sm_damp[kStageCap];
   __shared__ int sm_row[2][kSlice + 1];  // per pass: row -> first staged entry
   const int slice = blockIdx.x;
-  const int r0 = slice * kSlice;
-  const int rows = min(kSlice, g.p - r0);
+  const int r0 = g.row0 + slice * kSlice;  // global row of lane 0
+  const int rows = min(kSlice, g.p - slice * kSlice);
   const int64_t s0 = g.inc_ptr[r0], s1 = g.inc_ptr[r0 + rows];
   const int64_t c0 = g.cinc_ptr[r0], c1 = g.cinc_ptr[r0 + rows];
   const int nstat = static_cast<int>(s1 - s0), ncont = static_cast<int>(c1 - c0);
@@ -1065,7 +1075,7 @@ __global__ void __launch_bounds__(kSlotWarps * 32, 2) k_fill_slots(SlotArgs g) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int r = r0 + lane;
   if (lane >= rows) return;
-  const int len = g.rowlen[r];
+  const int len = g.rowlen[slice * kSlice + lane];
   const int64_t base = g.slice_off[slice] + lane;
   const double dt = g.dt;
   for (int k = warp; k < len; k += kSlotWarps) {
@@ -1126,8 +1136,9 @@ __global__ void __launch_bounds__(kSlotWarps * 32, 2) k_fill_slots(SlotArgs g) {
 
 // Phase 2b: rhs per row, contributions in ascending element order.
 __global__ void __launch_bounds__(256) k_fill_rhs(SlotArgs g) {
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= g.p) return;
+  const int lr = blockIdx.x * blockDim.x + threadIdx.x;
+  if (lr >= g.p) return;
+  const int r = g.row0 + lr;
   if (!g.pinned[r] && g.mass[r] <= 0.0) atomicMin(g.bad_mass, r);
   double r0 = 0.0, r1 = 0.0, r2 = 0.0;
   for (int pass = 0; pass < 2; ++pass) {
@@ -1151,6 +1162,45 @@ __global__ void __launch_bounds__(256) k_fill_rhs(SlotArgs g) {
 constexpr int kFillThreads = 64;
 constexpr int kWideCap = 24;
 
+// 1 for elements with a non-pinned stencil vertex in [row0, row1): the
+// element instances distribute_elements hands this rank (assembly.cpp:28-51).
+__global__ void k_elem_mine(int64_t n, const int4* __restrict__ est, const int2* __restrict__ einfo,
+                            const uint8_t* __restrict__ pinned, int row0, int row1, uint8_t* __restrict__ flag) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  const int4 s4 = est[e];
+  const int ss = (einfo[e].x >> 8) & 0xff;
+  const int sv[4] = {s4.x, s4.y, s4.z, s4.w};
+  uint8_t mine = 0;
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+    if (a < ss && sv[a] >= row0 && sv[a] < row1 && !pinned[sv[a]]) mine = 1;
+  flag[e] = mine;
+}
+
+// Compacts this rank's element ids (ascending) into c.elist; returns count.
+static int64_t select_rank_elements(Ctx& c) {
+  const int64_t ne = c.n_static + c.n_contacts;
+  cudaStream_t s = c.stream;
+  DBuf<uint8_t> flag;
+  flag.resize(static_cast<size_t>(ne) + 1);
+  c.elist.resize(static_cast<size_t>(ne) + 1);
+  DBuf<int64_t> cnt;
+  cnt.resize(1);
+  if (!ne) return 0;
+  k_elem_mine<<<div_up(ne, 256), 256, 0, ls(c)>>>(ne, c.est.data(), c.einfo.data(), c.pinned.data(), c.row0, c.row1,
+                                                   flag.data());
+  cub::CountingInputIterator<int64_t> ids(0);
+  size_t tmp = 0;
+  cub::DeviceSelect::Flagged(nullptr, tmp, ids, flag.data(), c.elist.data(), cnt.data(), ne, s);
+  void* t = scratch(c, tmp);
+  WG_CUDA(cub::DeviceSelect::Flagged(t, tmp, ids, flag.data(), c.elist.data(), cnt.data(), ne, s));
+  int64_t h = 0;
+  WG_CUDA(cudaMemcpyAsync(&h, cnt.data(), sizeof(h), cudaMemcpyDeviceToHost, s));
+  WG_CUDA(cudaStreamSynchronize(s));
+  return h;
+}
+
 void fill_matrix(Ctx& c, const double* xc, const double* xa, const double* vel, double dt, int mode) {
   if (!(dt > 0.0)) throw Error(WEFT_ERR_DIMENSION, "fill_matrix: dt must be positive");
   if (c.p == 0 && c.n_static == 0) throw Error(WEFT_ERR_INVALID, "fill_matrix: set_vertices/set_elements first");
@@ -1167,8 +1217,10 @@ void fill_matrix(Ctx& c, const double* xc, const double* xa, const double* vel, 
   int* bad = reinterpret_cast<int*>(c.scalars.data() + 8);
   const int big = INT32_MAX;
   WG_CUDA(cudaMemcpyAsync(bad, &big, sizeof(int), cudaMemcpyHostToDevice, s));
+  const int nloc = c.row1 - c.row0;
   FillArgs f{};
-  f.p = c.p;
+  f.p = nloc;
+  f.row0 = c.row0;
   f.n_static = c.n_static;
   f.dt = dt;
   f.exact = mode == WEFT_JAC_EXACT;
@@ -1193,31 +1245,40 @@ void fill_matrix(Ctx& c, const double* xc, const double* xa, const double* vel, 
   f.xa = xa;
   f.vel = vel;
   f.bad_mass = bad;
-  if (c.p && !f.exact) {
+  if (nloc && !f.exact) {
     if (!layout_cached)
-      k_zero_padding<<<div_up(c.p, 256), 256, 0, ls(c)>>>(c.p, A.slice_off.data(), A.rowlen.data(), A.vals.data(), A.total);
-    const int64_t ne = c.n_static + c.n_contacts;
-    ElemArgs ea{ne, dt, c.est.data(), c.einfo.data(), c.edamp.data(), c.epay.data(), c.eres_off.data(), c.eres.data(),
-                xc, xa, vel};
+      k_zero_padding<<<div_up(nloc, 256), 256, 0, ls(c)>>>(nloc, A.slice_off.data(), A.rowlen.data(), A.vals.data(),
+                                                         A.total);
+    // phase 1 over every element (one rank) or over the elements coupled to
+    // this rank's rows (distribute_elements, assembly.cpp:28-51)
+    int64_t ne = c.n_static + c.n_contacts;
+    const int64_t* list = nullptr;
+    if (c.world > 1) {
+      ne = select_rank_elements(c);
+      list = c.elist.data();
+    }
+    ElemArgs ea{ne, list, dt, c.est.data(), c.einfo.data(), c.edamp.data(), c.epay.data(), c.eres_off.data(),
+                c.eres.data(), xc, xa, vel};
     if (ne) k_elem_eval<<<div_up(ne, 128), 128, 0, ls(c)>>>(ea);
-    SlotArgs sa{c.p, c.n_static, dt, A.slice_off.data(), A.rowlen.data(), A.cols.data(), A.vals.data(), A.total,
-                c.mass.data(), c.pinned.data(), c.inc_ptr.data(), c.inc.data(), c.cinc_ptr.data(), c.cinc.data(),
-                c.est.data(), c.einfo.data(), c.edamp.data(), c.epay.data(), c.eres_off.data(), c.eres.data(),
-                c.rhs.data(), bad};
+    SlotArgs sa{nloc, c.row0, c.n_static, dt, A.slice_off.data(), A.rowlen.data(), A.cols.data(), A.vals.data(),
+                A.total, c.mass.data(), c.pinned.data(), c.inc_ptr.data(), c.inc.data(), c.cinc_ptr.data(),
+                c.cinc.data(), c.est.data(), c.einfo.data(), c.edamp.data(), c.epay.data(), c.eres_off.data(),
+                c.eres.data(), c.rhs.data(), bad};
     k_fill_slots<<<A.nslices, kSlotWarps * 32, 0, ls(c)>>>(sa);
-    k_fill_rhs<<<div_up(c.p, 256), 256, 0, ls(c)>>>(sa);
+    k_fill_rhs<<<div_up(nloc, 256), 256, 0, ls(c)>>>(sa);
     WG_CUDA(cudaGetLastError());
-  } else if (c.p) {
+  } else if (nloc) {
     if (!layout_cached)
-      k_zero_padding<<<div_up(c.p, 256), 256, 0, ls(c)>>>(c.p, A.slice_off.data(), A.rowlen.data(), A.vals.data(), A.total);
+      k_zero_padding<<<div_up(nloc, 256), 256, 0, ls(c)>>>(nloc, A.slice_off.data(), A.rowlen.data(), A.vals.data(),
+                                                         A.total);
     const size_t smem = static_cast<size_t>(f.wcap) * (9 * sizeof(double) + sizeof(int32_t)) * kFillThreads;
     auto narrow = f.exact ? k_fill<false, true> : k_fill<false, false>;
     auto wide = f.exact ? k_fill<true, true> : k_fill<true, false>;
     WG_CUDA(cudaFuncSetAttribute(narrow, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    narrow<<<div_up(c.p, kFillThreads), kFillThreads, smem, ls(c)>>>(f);
+    narrow<<<div_up(nloc, kFillThreads), kFillThreads, smem, ls(c)>>>(f);
     if (A.max_len > kWideCap) {
       // rows wider than the shared-memory budget accumulate in place
-      wide<<<div_up(c.p, kFillThreads), kFillThreads, 0, ls(c)>>>(f);
+      wide<<<div_up(nloc, kFillThreads), kFillThreads, 0, ls(c)>>>(f);
     }
     WG_CUDA(cudaGetLastError());
   }

@@ -123,8 +123,14 @@ weft_status weft_gpu_create(const weft_gpu_options* opts, weft_gpu_ctx** out) {
     if (!is_pow2(c.nparts))
       throw weft_gpu::Error(WEFT_ERR_TOPOLOGY,
                             "fat-tree requires a power-of-two device count, got " + std::to_string(c.nparts));
-    if (c.part_begin != 0 || c.part_end != c.nparts)
-      throw weft_gpu::Error(WEFT_ERR_INVALID, "multi-process partition ranges are created through weft_gpu_create_dist");
+    const int span = c.part_end - c.part_begin;
+    if (span < 1 || c.part_begin < 0 || c.part_end > c.nparts || c.nparts % span != 0 || c.part_begin % span != 0)
+      throw weft_gpu::Error(WEFT_ERR_TOPOLOGY, "partition range [" + std::to_string(c.part_begin) + ", " +
+                                                   std::to_string(c.part_end) +
+                                                   ") is not one of equal contiguous rank ranges of " +
+                                                   std::to_string(c.nparts) + " partitions");
+    c.world = c.nparts / span;
+    c.rank = c.part_begin / span;
     int count = 0;
     WG_CUDA(cudaGetDeviceCount(&count));
     if (c.device < 0 || c.device >= count)
@@ -164,6 +170,7 @@ weft_status weft_gpu_destroy(weft_gpu_ctx* ctx) {
     auto& c = ctx->c;
     weft_gpu::pcg_free(c);
     WG_CUDA(cudaStreamSynchronize(c.stream));
+    weft_gpu::comm_free(c);
     for (auto& e : c.ev) cudaEventDestroy(e);
     cudaStreamDestroy(c.stream);
   });
@@ -193,13 +200,25 @@ weft_status weft_gpu_spmv(weft_gpu_ctx* ctx, const double* x, double* y) {
   return guard(ctx, [&] {
     auto& c = ctx->c;
     need(c.has_matrix, WEFT_ERR_INVALID, "spmv: no matrix");
-    const size_t len = 3 * static_cast<size_t>(c.A.rows);
-    c.r.resize(len);
+    const size_t len = 3 * static_cast<size_t>(c.pm.p);
     c.q.resize(len);
-    WG_CUDA(cudaMemcpyAsync(c.r.data(), x, len * sizeof(double), cudaMemcpyDefault, c.stream));
-    weft_gpu::spmv(c, c.r.data(), c.q.data());
-    WG_CUDA(cudaMemcpyAsync(y, c.q.data(), len * sizeof(double), cudaMemcpyDefault, c.stream));
+    if (c.world == 1) {
+      c.r.resize(len);
+      WG_CUDA(cudaMemcpyAsync(c.r.data(), x, len * sizeof(double), cudaMemcpyDefault, c.stream));
+      weft_gpu::spmv(c, c.r.data(), c.q.data());
+      WG_CUDA(cudaMemcpyAsync(y, c.q.data(), len * sizeof(double), cudaMemcpyDefault, c.stream));
+    } else {
+      // own rows of x into the window; peers gather the rest from their owners
+      weft_gpu::comm_need(c, "spmv");
+      const size_t o = 3 * static_cast<size_t>(c.row0), m = 3 * static_cast<size_t>(c.A.rows);
+      WG_CUDA(cudaMemcpyAsync(c.z.data() + o, x + o, m * sizeof(double), cudaMemcpyDefault, c.stream));
+      weft_gpu::publish_vectors(c);
+      weft_gpu::spmv(c, c.z.data(), c.q.data());
+      weft_gpu::rank_barrier(c);  // peers finished reading this rank's x rows
+      WG_CUDA(cudaMemcpyAsync(y + o, c.q.data() + o, m * sizeof(double), cudaMemcpyDefault, c.stream));
+    }
     WG_CUDA(cudaStreamSynchronize(c.stream));
+    weft_gpu::comm_check(c);
   });
 }
 
@@ -225,7 +244,8 @@ weft_status weft_gpu_download_rhs(weft_gpu_ctx* ctx, double* rhs) {
   return guard(ctx, [&] {
     auto& c = ctx->c;
     need(c.has_rhs, WEFT_ERR_INVALID, "download_rhs: no assembled system");
-    WG_CUDA(cudaMemcpyAsync(rhs, c.rhs.data(), 3 * sizeof(double) * c.A.rows, cudaMemcpyDefault, c.stream));
+    WG_CUDA(cudaMemcpyAsync(rhs, c.rhs.data() + 3 * static_cast<size_t>(c.row0), 3 * sizeof(double) * c.A.rows,
+                            cudaMemcpyDefault, c.stream));
     WG_CUDA(cudaStreamSynchronize(c.stream));
   });
 }
@@ -236,7 +256,7 @@ weft_status weft_gpu_pcg(weft_gpu_ctx* ctx, const double* b, double* x, const we
     auto& c = ctx->c;
     need(c.has_matrix, WEFT_ERR_INVALID, "pcg: no matrix");
     need(config != nullptr, WEFT_ERR_INVALID, "pcg: config is NULL");
-    const size_t len = 3 * static_cast<size_t>(c.A.rows);
+    const size_t len = 3 * static_cast<size_t>(c.pm.p);
     const double* bdev = nullptr;
     if (b) {
       c.bvec.resize(len);
@@ -260,10 +280,36 @@ weft_status weft_gpu_pcg(weft_gpu_ctx* ctx, const double* b, double* x, const we
       report->rel_residual = r.rel_residual;
     }
     if (x) {
-      if (r.iterations == 0) WG_CUDA(cudaMemsetAsync(c.xs.data(), 0, len * sizeof(double), c.stream));
-      WG_CUDA(cudaMemcpyAsync(x, c.xs.data(), len * sizeof(double), cudaMemcpyDefault, c.stream));
+      const size_t o = 3 * static_cast<size_t>(c.row0), m = 3 * static_cast<size_t>(c.A.rows);
+      if (r.iterations == 0) WG_CUDA(cudaMemsetAsync(c.xs.data() + o, 0, m * sizeof(double), c.stream));
+      WG_CUDA(cudaMemcpyAsync(x + o, c.xs.data() + o, m * sizeof(double), cudaMemcpyDefault, c.stream));
       WG_CUDA(cudaStreamSynchronize(c.stream));
     }
+  });
+}
+
+weft_status weft_gpu_comm_export(weft_gpu_ctx* ctx, void* handle_out) {
+  return guard(ctx, [&] {
+    need(handle_out != nullptr, WEFT_ERR_INVALID, "comm_export: handle_out is NULL");
+    weft_gpu::comm_export(ctx->c, handle_out);
+  });
+}
+
+weft_status weft_gpu_comm_attach(weft_gpu_ctx* ctx, const void* handles) {
+  return guard(ctx, [&] {
+    need(handles != nullptr, WEFT_ERR_INVALID, "comm_attach: handles is NULL");
+    weft_gpu::comm_attach(ctx->c, handles);
+  });
+}
+
+weft_status weft_gpu_rank_info(weft_gpu_ctx* ctx, weft_rank_info* info) {
+  return guard(ctx, [&] {
+    auto& c = ctx->c;
+    info->world = c.world;
+    info->rank = c.rank;
+    info->first_row = c.row0;
+    info->rows = c.row1 - c.row0;
+    info->global_rows = c.pm.p;
   });
 }
 

@@ -47,14 +47,23 @@ struct DBuf {
   T* ptr = nullptr;
   size_t cap = 0;
   size_t n = 0;
+  bool ext = false;  // view of memory owned elsewhere (the peer window)
   DBuf() = default;
   DBuf(const DBuf&) = delete;
   DBuf& operator=(const DBuf&) = delete;
   ~DBuf() {
-    if (ptr) cudaFree(ptr);
+    if (ptr && !ext) cudaFree(ptr);
+  }
+  // Turns the buffer into a fixed-capacity view of `count` elements at p.
+  void attach(T* p, size_t count) {
+    if (ptr && !ext) cudaFree(ptr);
+    ptr = p;
+    cap = n = count;
+    ext = true;
   }
   void resize(size_t count) {
     if (count > cap) {
+      if (ext) throw std::runtime_error("window buffer too small (vertex count changed after weft_gpu_comm_export)");
       if (ptr) WG_CUDA(cudaFree(ptr));
       ptr = nullptr;
       size_t c = count + count / 8 + 16;
@@ -110,5 +119,63 @@ struct GroupOrder {
 };
 
 inline int div_up(long long a, long long b) { return static_cast<int>((a + b - 1) / b); }
+
+// ---------------------------------------------------------------------------
+// Peer-memory synchronisation between ranks (one process per GPU, windows
+// mapped through CUDA IPC; NVLink P2P on a multi-GPU node). Flags are
+// monotonically increasing 64-bit sequence numbers written by their owner
+// rank with a system-scope release and polled with a system-scope acquire.
+// ---------------------------------------------------------------------------
+constexpr int kMaxRanks = 8;
+constexpr unsigned long long kSpinTimeoutNs = 30ull * 1000 * 1000 * 1000;  // 30 s
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Spins until *flag >= target; false after kSpinTimeoutNs (a dead peer must
+// not hang the GPU: the caller records the failure and the host throws).
+__device__ __forceinline__ bool wait_flag(const unsigned long long* flag, unsigned long long target) {
+  if (ld_acquire_sys(flag) >= target) return true;
+  const unsigned long long t0 = global_ns();
+  for (;;) {
+    __nanosleep(64);
+    if (ld_acquire_sys(flag) >= target) return true;
+    if (global_ns() - t0 > kSpinTimeoutNs) return false;
+  }
+}
+
+// The peer-visible part of a rank's context (one cudaMalloc, exported as a
+// CUDA IPC handle). Written remotely by peers: the ready flags (slot = the
+// writer's rank) and the reduction slots of the writer's partitions.
+struct CommHeader {
+  unsigned long long vec_ready[kMaxRanks];    // PCG / SpMV gather vectors published
+  unsigned long long red_ready[kMaxRanks];    // reduction partials published
+  unsigned long long state_ready[kMaxRanks];  // sim state (v, x_cand) rows published
+  double red[2][kMaxParts][4];                // [sequence parity][partition][value]
+};
+
+// Kernel-side view of the rank group (by value in kernel arguments).
+struct CommView {
+  int world = 1, rank = 0;
+  int ppr = 1;                            // partitions per rank
+  CommHeader* hdr[kMaxRanks] = {};        // every rank's header (own = local)
+  const double* z[kMaxRanks] = {};        // every rank's gather vectors (global row index)
+  const double* p[kMaxRanks] = {};
+  char* base[kMaxRanks] = {};             // every rank's window base
+  unsigned long long* seq = nullptr;      // own counters: [0] vec, [1] red, [2] state, [3] error
+};
 
 }  // namespace weft_gpu

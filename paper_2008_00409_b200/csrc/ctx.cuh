@@ -16,7 +16,8 @@ namespace weft_gpu {
 // order) and by ascending column within a group; the group position is
 // packed in bits 28..30 of the column word.
 struct SellMatrix {
-  int rows = 0;
+  int rows = 0;       // block rows held (the rank's rows)
+  int row0 = 0;       // global index of the first held row
   int nslices = 0;
   int64_t total = 0;  // slots incl. padding
   int64_t nnzb = 0;
@@ -44,6 +45,18 @@ struct Ctx {
   int device = 0;
   int nparts = 1;
   int part_begin = 0, part_end = 1;
+  // Rank group (one process per GPU): this context owns partitions
+  // [part_begin, part_end) = global rows [row0, row1); world ranks own
+  // equal contiguous partition ranges. world == 1: everything local.
+  int world = 1, rank = 0;
+  int row0 = 0, row1 = 0;
+  void* win = nullptr;          // own peer-visible window (cudaMalloc, IPC-exported)
+  size_t win_bytes = 0;
+  int win_p = 0;                // vertex count the window was sized for
+  void* peer_win[kMaxRanks] = {};  // mapped peer windows (own = win)
+  bool attached = false;
+  DBuf<unsigned long long> seq;    // [0] vec, [1] red, [2] state, [3] error
+  CommView comm;                   // kernel view (valid once attached)
   cudaStream_t stream = nullptr;
   cudaEvent_t ev[8] = {};
 
@@ -64,6 +77,7 @@ struct Ctx {
   int64_t static_pay = 0;  // payload doubles used by static elements
   DBuf<int32_t> eres_off;  // per element: offset of its results in eres
   DBuf<double> eres;       // phase-1 results (rhs contributions + state)
+  DBuf<int64_t> elist;     // rank group: ids of the elements coupled to held rows
   int64_t static_res = 0;
   // static row incidences: per row, (element*4 + a) ascending element
   DBuf<int64_t> inc_ptr;  // p + 1
@@ -167,6 +181,17 @@ void build_grid(Ctx& c, const double* x0_dev, const double* x1_dev, int mode, do
 int64_t candidates(Ctx& c, int64_t begin, int64_t end, int32_t* pairs_dev_or_null);
 
 void serial_sum(Ctx& c, int n, const double* d_host, double* exact, double* naive, int fast);
+
+// rank group (comm.cu, sparse.cu)
+void set_rows(Ctx& c, int p);  // partition map + this rank's row window
+void comm_need(Ctx& c, const char* what);
+void comm_check(Ctx& c);
+void comm_export(Ctx& c, void* handle_out);
+void comm_attach(Ctx& c, const void* handles);
+void comm_free(Ctx& c);
+void publish_vectors(Ctx& c);  // z/p rows of this rank are final
+void rank_barrier(Ctx& c);
+void exchange_state(Ctx& c);   // sim: publish own v/x_cand rows, pull the peers'
 
 // CUB scratch helper
 void* scratch(Ctx& c, size_t bytes);

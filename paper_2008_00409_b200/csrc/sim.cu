@@ -2,6 +2,7 @@
 // hot-path step (Simulator::step_impl stages 1-4 plus the CCD broad phase,
 // proj/src/driver.cpp:96-215; narrow phase and impact zones are out of
 // scope for this tier).
+#include <algorithm>
 #include <string>
 
 #include "ctx.cuh"
@@ -16,11 +17,12 @@ __global__ void k_advance(int64_t n, const double* __restrict__ x, const double*
   if (i < n) out[i] = x[i] + dt * v[i];
 }
 
-// v += dv; x_cand = x + dt v (driver.cpp:165-176)
-__global__ void k_candidate(int64_t n, const double* __restrict__ x, double* __restrict__ v,
+// v += dv; x_cand = x + dt v (driver.cpp:165-176) over entries [i0, i1)
+// (this rank's rows)
+__global__ void k_candidate(int64_t i0, int64_t i1, const double* __restrict__ x, double* __restrict__ v,
                             const double* __restrict__ dv, double dt, double* __restrict__ xc) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n) return;
+  const int64_t i = i0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= i1) return;
   const double vi = v[i] + dv[i];
   v[i] = vi;
   xc[i] = x[i] + dt * vi;
@@ -156,6 +158,10 @@ weft_status weft_gpu_sim_set_state(weft_gpu_ctx* ctx, const double* x, const dou
     if (c.p == 0 || c.n_static == 0) throw Error(WEFT_ERR_INVALID, "sim_set_state: set vertices and elements first");
     if (c.soup_verts != c.p) throw Error(WEFT_ERR_INVALID, "sim_set_state: soup must be the cloth (soup_verts == p)");
     const size_t n = 3 * static_cast<size_t>(c.p);
+    if (c.world > 1) {
+      weft_gpu::comm_need(c, "sim_set_state");
+      weft_gpu::rank_barrier(c);  // no peer may still be reading the state being replaced
+    }
     weft_gpu::upload_vec(c, c.sim_x, x, n);
     weft_gpu::upload_vec(c, c.sim_v, v, n);
     c.sim_xc.resize(n);
@@ -173,8 +179,17 @@ weft_status weft_gpu_sim_step(weft_gpu_ctx* ctx, const weft_sim_params* prm, wef
     cudaEvent_t* ev = c.ev;
     // 1. proximity broad phase (DCD) on the current configuration
     WG_CUDA(cudaEventRecord(ev[0], s));
+    // the grid is replicated on every rank (collision.cpp:397-399); each
+    // rank walks its split_workload share of the pair space (:181-192)
+    auto share = [&](int64_t total, int64_t& b, int64_t& e) {
+      const int64_t base = total / c.world, extra = total % c.world;
+      b = c.rank * base + std::min<int64_t>(c.rank, extra);
+      e = b + base + (c.rank < extra ? 1 : 0);
+    };
+    int64_t wb = 0, we = 0;
     weft_gpu::build_grid(c, c.sim_x.data(), c.sim_x.data(), WEFT_DISCRETE, prm->thickness, prm->cell_scale);
-    const int64_t dcd = weft_gpu::candidates(c, 0, c.grid_total, nullptr);
+    share(c.grid_total, wb, we);
+    const int64_t dcd = weft_gpu::candidates(c, wb, we, nullptr);
     WG_CUDA(cudaEventRecord(ev[1], s));
     // 2. assembly of step_system at (x, v)
     c.x_adv.resize(static_cast<size_t>(n));
@@ -188,13 +203,16 @@ weft_status weft_gpu_sim_step(weft_gpu_ctx* ctx, const weft_sim_params* prm, wef
     if (!pr.converged)  // driver.cpp:158-161
       throw Error(WEFT_ERR_SOLVER, "PCG did not converge (residual " + std::to_string(pr.rel_residual) + ")");
     // 4. candidate update
-    if (pr.iterations == 0) WG_CUDA(cudaMemsetAsync(c.xs.data(), 0, n * sizeof(double), s));
-    weft_gpu::k_candidate<<<weft_gpu::div_up(n, 256), 256, 0, ls(c)>>>(n, c.sim_x.data(), c.sim_v.data(), c.xs.data(),
-                                                                    dt, c.sim_xc.data());
+    const int64_t i0 = 3 * static_cast<int64_t>(c.row0), i1 = 3 * static_cast<int64_t>(c.row1);
+    if (pr.iterations == 0) WG_CUDA(cudaMemsetAsync(c.xs.data() + i0, 0, (i1 - i0) * sizeof(double), s));
+    weft_gpu::k_candidate<<<weft_gpu::div_up(i1 - i0, 256), 256, 0, ls(c)>>>(i0, i1, c.sim_x.data(), c.sim_v.data(),
+                                                                          c.xs.data(), dt, c.sim_xc.data());
+    if (c.world > 1) weft_gpu::exchange_state(c);  // all rows of v and x_cand on every rank
     WG_CUDA(cudaEventRecord(ev[4], s));
     // 5. impact broad phase (CCD) over begin -> candidate
     weft_gpu::build_grid(c, c.sim_x.data(), c.sim_xc.data(), WEFT_CONTINUOUS, prm->thickness, prm->cell_scale);
-    const int64_t ccd = weft_gpu::candidates(c, 0, c.grid_total, nullptr);
+    share(c.grid_total, wb, we);
+    const int64_t ccd = weft_gpu::candidates(c, wb, we, nullptr);
     WG_CUDA(cudaEventRecord(ev[5], s));
     // 7. commit (no zone correction in this tier)
     std::swap(c.sim_x.ptr, c.sim_xc.ptr);

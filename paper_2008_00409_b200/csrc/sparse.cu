@@ -28,7 +28,8 @@ namespace weft_gpu {
 // Matrix view passed to kernels
 // ---------------------------------------------------------------------------
 struct SellView {
-  int rows;
+  int rows;  // held rows; kernel row indices below are LOCAL (global - row0)
+  int row0;
   int64_t total;
   const int64_t* __restrict__ slice_off;
   const int32_t* __restrict__ rowlen;
@@ -37,25 +38,27 @@ struct SellView {
 };
 
 static SellView view(const SellMatrix& A) {
-  return SellView{A.rows, A.total, A.slice_off.data(), A.rowlen.data(), A.cols.data(), A.vals.data()};
+  return SellView{A.rows, A.row0, A.total, A.slice_off.data(), A.rowlen.data(), A.cols.data(), A.vals.data()};
 }
 
 // Blocks are aligned to partitions so that every block's dot partial
 // belongs to exactly one partition.
 struct PartBlocks {
-  int n;
+  int n;   // partitions held by this rank
+  int d0;  // global index of the first one
   int bstart[kMaxParts + 1];
   int rbegin[kMaxParts];
   int rend[kMaxParts];
 };
 
-static PartBlocks part_blocks(const PartMap& pm, int threads) {
+static PartBlocks part_blocks(const Ctx& c, int threads) {
   PartBlocks pb{};
-  pb.n = pm.n;
+  pb.n = c.part_end - c.part_begin;
+  pb.d0 = c.part_begin;
   pb.bstart[0] = 0;
-  for (int d = 0; d < pm.n; ++d) {
-    pb.rbegin[d] = pm.begin(d);
-    pb.rend[d] = pm.end(d);
+  for (int d = 0; d < pb.n; ++d) {
+    pb.rbegin[d] = c.pm.begin(pb.d0 + d);
+    pb.rend[d] = c.pm.end(pb.d0 + d);
     pb.bstart[d + 1] = pb.bstart[d] + div_up(pb.rend[d] - pb.rbegin[d], threads);
   }
   return pb;
@@ -70,17 +73,58 @@ __device__ __forceinline__ int block_part(const PartBlocks& pb, int b) {
 // ---------------------------------------------------------------------------
 // Row product in the reference order
 // ---------------------------------------------------------------------------
+// Gathers x[c] (+ beta * pold[c] for PMode 2) for column c. Columns of
+// another rank (kRemote, only reached for accumulation groups != 0) are read
+// over peer memory once that rank has published the vectors
+// (vec_ready >= vexp); `seen` caches which ranks were already waited for.
+template <int PMode, bool kRemote>
+__device__ __forceinline__ void gather3(int c, int g, const double* __restrict__ x, const double* __restrict__ pold,
+                                        double beta, const CommView& cv, const PartMap& pm, unsigned long long vexp,
+                                        unsigned& seen, double& x0, double& x1, double& x2) {
+  if (kRemote && g != 0) {
+    const int q = pm.owner(c) / cv.ppr;
+    if (q != cv.rank) {
+      if (!(seen & (1u << q))) {
+        if (!wait_flag(&cv.hdr[cv.rank]->vec_ready[q], vexp)) atomicExch(cv.seq + 3, 1ull);
+        seen |= 1u << q;
+      }
+      const double* zq = cv.z[q];
+      x0 = __ldcg(zq + 3 * c);
+      x1 = __ldcg(zq + 3 * c + 1);
+      x2 = __ldcg(zq + 3 * c + 2);
+      if (PMode == 2) {
+        const double* pq = cv.p[q];
+        x0 = x0 + beta * __ldcg(pq + 3 * c);
+        x1 = x1 + beta * __ldcg(pq + 3 * c + 1);
+        x2 = x2 + beta * __ldcg(pq + 3 * c + 2);
+      }
+      return;
+    }
+  }
+  x0 = x[3 * c];
+  x1 = x[3 * c + 1];
+  x2 = x[3 * c + 2];
+  if (PMode == 2) {
+    x0 = x0 + beta * pold[3 * c];
+    x1 = x1 + beta * pold[3 * c + 1];
+    x2 = x2 + beta * pold[3 * c + 2];
+  }
+}
+
+// Row product of LOCAL row lr in the reference order.
 // PMode 0: x given. PMode 1: x = z (first PCG iteration, p = z).
 // PMode 2: x = z + beta * p_old on the fly (PCG p update).
-template <int PMode>
-__device__ __forceinline__ void row_product(const SellView& A, int r, int ngroups, const double* __restrict__ x,
+template <int PMode, bool kRemote = false>
+__device__ __forceinline__ void row_product(const SellView& A, int lr, int ngroups, const double* __restrict__ x,
                                             const double* __restrict__ pold, double beta, double& y0, double& y1,
-                                            double& y2) {
-  const int len = A.rowlen[r];
-  const int64_t base = A.slice_off[r >> 5] + (r & 31);
+                                            double& y2, const CommView& cv = CommView(), const PartMap& pm = PartMap(),
+                                            unsigned long long vexp = 0) {
+  const int len = A.rowlen[lr];
+  const int64_t base = A.slice_off[lr >> 5] + (lr & 31);
   const int64_t T = A.total;
   double a0 = 0.0, a1 = 0.0, a2 = 0.0;
   int cg = 0;
+  unsigned seen = 0;
   y0 = y1 = y2 = 0.0;
 #pragma unroll 2
   for (int k = 0; k < len; ++k) {
@@ -101,16 +145,12 @@ __device__ __forceinline__ void row_product(const SellView& A, int r, int ngroup
       a0 = a1 = a2 = 0.0;
       ++cg;
     }
-    const double* v = A.vals + vidx(at, r & 31, 0);
+    const double* v = A.vals + vidx(at, lr & 31, 0);
     const double v0 = __ldg(v), v1 = __ldg(v + 32), v2 = __ldg(v + 64);
     const double v3 = __ldg(v + 96), v4 = __ldg(v + 128), v5 = __ldg(v + 160);
     const double v6 = __ldg(v + 192), v7 = __ldg(v + 224), v8 = __ldg(v + 256);
-    double x0 = x[3 * c], x1 = x[3 * c + 1], x2 = x[3 * c + 2];
-    if (PMode == 2) {
-      x0 = x0 + beta * pold[3 * c];
-      x1 = x1 + beta * pold[3 * c + 1];
-      x2 = x2 + beta * pold[3 * c + 2];
-    }
+    double x0, x1, x2;
+    gather3<PMode, kRemote>(c, g, x, pold, beta, cv, pm, vexp, seen, x0, x1, x2);
     a0 = a0 + ((v0 * x0 + v1 * x1) + v2 * x2);
     a1 = a1 + ((v3 * x0 + v4 * x1) + v5 * x2);
     a2 = a2 + ((v6 * x0 + v7 * x1) + v8 * x2);
@@ -257,15 +297,86 @@ __global__ void __launch_bounds__(256) k_spmv_pair(SellView A, const double* __r
 }
 
 __global__ void __launch_bounds__(256) k_spmv(SellView A, int ngroups, const double* __restrict__ x,
-                                              double* __restrict__ y) {
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= A.rows) return;
+                                              double* __restrict__ y, CommView cv, PartMap pm) {
+  const int lr = blockIdx.x * blockDim.x + threadIdx.x;
+  if (lr >= A.rows) return;
+  const int r = A.row0 + lr;
   double y0, y1, y2;
-  if (ngroups == 1) row_product_1<0>(A, r, x, nullptr, 0.0, y0, y1, y2);
-  else row_product<0>(A, r, ngroups, x, nullptr, 0.0, y0, y1, y2);
+  if (ngroups == 1) row_product_1<0>(A, lr, x, nullptr, 0.0, y0, y1, y2);
+  else if (cv.world > 1) row_product<0, true>(A, lr, ngroups, x, nullptr, 0.0, y0, y1, y2, cv, pm, cv.seq[0]);
+  else row_product<0>(A, lr, ngroups, x, nullptr, 0.0, y0, y1, y2);
   y[3 * r] = y0;
   y[3 * r + 1] = y1;
   y[3 * r + 2] = y2;
+}
+
+// ---------------------------------------------------------------------------
+// Rank-group primitives over peer memory (world > 1)
+// ---------------------------------------------------------------------------
+// "My rows of the gather vectors (z, p) are final": one thread, after the
+// writes of the whole grid are ordered before it (kernel boundary or the
+// last-block counter with system-scope fences).
+__device__ __forceinline__ void publish_vec(const CommView& cv) {
+  __threadfence_system();
+  const unsigned long long s = cv.seq[0] + 1;
+  cv.seq[0] = s;
+  for (int q = 0; q < cv.world; ++q) st_release_sys(&cv.hdr[q]->vec_ready[cv.rank], s);
+}
+
+__global__ void k_publish_vec(CommView cv) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) publish_vec(cv);
+}
+
+// Engine::all_reduce_sum (proj/src/exec.cpp:170-174) over ranks: every rank
+// stores its partitions' values into every rank's reduction slots, releases
+// its flag, waits for all flags, and sums the n partitions in ascending
+// order — the same association as a single-rank run with n partitions, so
+// all ranks (and the 1-GPU run) get bitwise the same scalar. Thread 0 only.
+template <int NV>
+__device__ void combine(const CommView& cv, int d0, int nloc, int ntot, const double (&v)[kMaxParts][NV],
+                        double (&out)[NV]) {
+#pragma unroll
+  for (int i = 0; i < NV; ++i) out[i] = 0.0;
+  if (cv.world == 1) {
+    for (int d = 0; d < nloc; ++d)
+#pragma unroll
+      for (int i = 0; i < NV; ++i) out[i] = out[i] + v[d][i];
+    return;
+  }
+  const unsigned long long s = cv.seq[1] + 1;
+  cv.seq[1] = s;
+  const int par = static_cast<int>(s & 1);
+  for (int q = 0; q < cv.world; ++q)
+    for (int d = 0; d < nloc; ++d)
+#pragma unroll
+      for (int i = 0; i < NV; ++i) cv.hdr[q]->red[par][d0 + d][i] = v[d][i];
+  __threadfence_system();
+  for (int q = 0; q < cv.world; ++q) st_release_sys(&cv.hdr[q]->red_ready[cv.rank], s);
+  CommHeader* me = cv.hdr[cv.rank];
+  for (int q = 0; q < cv.world; ++q)
+    if (!wait_flag(&me->red_ready[q], s)) atomicExch(cv.seq + 3, 1ull);
+  for (int d = 0; d < ntot; ++d)
+#pragma unroll
+    for (int i = 0; i < NV; ++i) out[i] = out[i] + __ldcg(&me->red[par][d][i]);
+}
+
+// Rank barrier (a reduction of nothing): after it, every rank has finished
+// all work it issued before (e.g. reading this rank's window).
+__global__ void k_rank_barrier(CommView cv, int ntot) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double v[kMaxParts][1] = {};
+  double out[1];
+  combine<1>(cv, 0, 0, ntot, v, out);
+}
+
+void publish_vectors(Ctx& c) {
+  k_publish_vec<<<1, 32, 0, ls(c)>>>(c.comm);
+  WG_CUDA(cudaGetLastError());
+}
+
+void rank_barrier(Ctx& c) {
+  k_rank_barrier<<<1, 32, 0, ls(c)>>>(c.comm, c.nparts);
+  WG_CUDA(cudaGetLastError());
 }
 
 void spmv(Ctx& c, const double* x_dev, double* y_dev) {
@@ -273,42 +384,55 @@ void spmv(Ctx& c, const double* x_dev, double* y_dev) {
   const int threads = 256;
   if (c.A.rows == 0) return;
   if (c.go.n == 1 && c.spmv_pair) k_spmv_pair<<<div_up(c.A.rows, threads / 2), threads, 0, ls(c)>>>(view(c.A), x_dev, y_dev);
-  else k_spmv<<<div_up(c.A.rows, threads), threads, 0, ls(c)>>>(view(c.A), c.go.n, x_dev, y_dev);
+  else k_spmv<<<div_up(c.A.rows, threads), threads, 0, ls(c)>>>(view(c.A), c.go.n, x_dev, y_dev, c.comm, c.pm);
   WG_CUDA(cudaGetLastError());
 }
 
 // ---------------------------------------------------------------------------
 // Host construction of the SELL layout from a global CSR (set_matrix path)
 // ---------------------------------------------------------------------------
+void set_rows(Ctx& c, int p) {
+  c.pm = PartMap::make(p, c.nparts);
+  c.row0 = c.pm.begin(c.part_begin);
+  c.row1 = c.pm.end(c.part_end - 1);
+}
+
+// Takes the GLOBAL block CSR (every rank passes the same matrix) and keeps
+// this rank's rows [row0, row1) (partition_matrix, sparse.hpp:103-147).
 void set_matrix_csr(Ctx& c, int rows, const int64_t* row_ptr, const int32_t* cols, const double* vals) {
   if (rows < 0) throw Error(WEFT_ERR_DIMENSION, "set_matrix: negative row count");
   if (rows >= (1 << 28)) throw Error(WEFT_ERR_DIMENSION, "set_matrix: more than 2^28 block rows");
-  c.pm = PartMap::make(rows, c.nparts);
   if (rows < c.nparts) throw Error(WEFT_ERR_DIMENSION, "set_matrix: fewer rows than partitions");
+  set_rows(c, rows);
   SellMatrix& A = c.A;
-  A.rows = rows;
-  A.nslices = div_up(rows, kSlice);
-  std::vector<int32_t> len(static_cast<size_t>(rows));
+  const int nloc = c.row1 - c.row0;
+  A.rows = nloc;
+  A.row0 = c.row0;
+  A.nslices = div_up(nloc, kSlice);
+  std::vector<int32_t> len(static_cast<size_t>(nloc));
   std::vector<int64_t> soff(static_cast<size_t>(A.nslices) + 1, 0);
   int64_t nnzb = 0;
   int maxlen = 0;
-  for (int r = 0; r < rows; ++r) {
+  for (int r = 0; r < rows; ++r)
+    if (row_ptr[r + 1] - row_ptr[r] < 0) throw Error(WEFT_ERR_DIMENSION, "set_matrix: row_ptr not monotone");
+  for (int lr = 0; lr < nloc; ++lr) {
+    const int r = c.row0 + lr;
     const int64_t l = row_ptr[r + 1] - row_ptr[r];
-    if (l < 0) throw Error(WEFT_ERR_DIMENSION, "set_matrix: row_ptr not monotone");
-    len[static_cast<size_t>(r)] = static_cast<int32_t>(l);
+    len[static_cast<size_t>(lr)] = static_cast<int32_t>(l);
     nnzb += l;
     maxlen = std::max<int>(maxlen, static_cast<int>(l));
   }
   for (int s = 0; s < A.nslices; ++s) {
     int w = 0;
-    for (int r = s * kSlice; r < std::min(rows, (s + 1) * kSlice); ++r) w = std::max(w, len[static_cast<size_t>(r)]);
+    for (int lr = s * kSlice; lr < std::min(nloc, (s + 1) * kSlice); ++lr) w = std::max(w, len[static_cast<size_t>(lr)]);
     soff[static_cast<size_t>(s) + 1] = soff[static_cast<size_t>(s)] + static_cast<int64_t>(w) * kSlice;
   }
   const int64_t total = soff.back();
   std::vector<int32_t> hc(static_cast<size_t>(total), -1);
   std::vector<double> hv(9 * static_cast<size_t>(total), 0.0);
   std::vector<std::pair<int, int64_t>> order;  // (group, csr index)
-  for (int r = 0; r < rows; ++r) {
+  for (int lr = 0; lr < nloc; ++lr) {
+    const int r = c.row0 + lr;
     const int d = c.pm.owner(r);
     order.clear();
     for (int64_t k = row_ptr[r]; k < row_ptr[r + 1]; ++k) {
@@ -318,12 +442,12 @@ void set_matrix_csr(Ctx& c, int rows, const int64_t* row_ptr, const int32_t* col
     }
     std::stable_sort(order.begin(), order.end(),
                      [](const auto& a, const auto& b) { return a.first < b.first; });
-    const int64_t base = soff[static_cast<size_t>(r / kSlice)] + r % kSlice;
+    const int64_t base = soff[static_cast<size_t>(lr / kSlice)] + lr % kSlice;
     for (size_t s = 0; s < order.size(); ++s) {
       const int64_t at = base + static_cast<int64_t>(s) * kSlice;
       const int64_t k = order[s].second;
       hc[static_cast<size_t>(at)] = cols[k] | (order[s].first << kGroupShift);
-      for (int q = 0; q < 9; ++q) hv[static_cast<size_t>(vidx(at, r % kSlice, q))] = vals[9 * k + q];
+      for (int q = 0; q < 9; ++q) hv[static_cast<size_t>(vidx(at, lr % kSlice, q))] = vals[9 * k + q];
     }
   }
   A.total = total;
@@ -339,7 +463,8 @@ void set_matrix_csr(Ctx& c, int rows, const int64_t* row_ptr, const int32_t* col
   c.have_pattern_for_contacts = false;
 }
 
-// Global CSR with ascending columns (gather_matrix, sparse.hpp:149-173).
+// This rank's rows [row0, row1) as block CSR with ascending columns
+// (gather_matrix, sparse.hpp:149-173; all rows when world == 1).
 void download_csr(Ctx& c, int64_t* row_ptr, int32_t* cols, double* vals) {
   SellMatrix& A = c.A;
   std::vector<int64_t> soff(A.slice_off.size());
@@ -403,14 +528,14 @@ __device__ __forceinline__ void block_sum(double (&v)[NV], double* smem /* NV * 
   __syncthreads();
 }
 
-// Sums partials[b*NV + i] over blocks of each partition (fixed strided
-// order + fixed tree), then over partitions in ascending order. Called by
-// all threads of the last block; result valid in thread 0.
+// Sums partials[b*NV + i] over the blocks of each held partition (fixed
+// strided order + fixed tree), then combines the partitions in ascending
+// order across ranks. Called by all threads of the last block; result valid
+// in thread 0.
 template <int NV>
-__device__ void finalize_sums(const PartBlocks& pb, const double* partials, double (&out)[NV], double* smem) {
-  double total[NV];
-#pragma unroll
-  for (int i = 0; i < NV; ++i) total[i] = 0.0;
+__device__ void finalize_sums(const PartBlocks& pb, const double* partials, double (&out)[NV], double* smem,
+                              const CommView& cv, int ntot) {
+  double per[kMaxParts][NV];
   for (int d = 0; d < pb.n; ++d) {
     double v[NV];
 #pragma unroll
@@ -420,10 +545,9 @@ __device__ void finalize_sums(const PartBlocks& pb, const double* partials, doub
       for (int i = 0; i < NV; ++i) v[i] = v[i] + __ldcg(partials + (size_t)b * NV + i);
     block_sum<NV>(v, smem);
 #pragma unroll
-    for (int i = 0; i < NV; ++i) total[i] = total[i] + v[i];  // only thread 0's value is used
+    for (int i = 0; i < NV; ++i) per[d][i] = v[i];  // only thread 0's value is used
   }
-#pragma unroll
-  for (int i = 0; i < NV; ++i) out[i] = total[i];
+  if (threadIdx.x == 0) combine<NV>(cv, pb.d0, pb.n, ntot, per, out);
 }
 
 // ---------------------------------------------------------------------------
@@ -442,10 +566,13 @@ struct PcgState {
 
 // Last-block-done: thread 0 publishes the block's partial (caller wrote it
 // before), fences once, and counts arrivals; only the last block reduces.
-__device__ __forceinline__ bool last_block(unsigned* counter) {
+// With peers (sys), the fence is system-scope so the rows this grid wrote
+// are visible to other GPUs before the last block releases them.
+__device__ __forceinline__ bool last_block(unsigned* counter, bool sys) {
   __shared__ bool s_last;
   if (threadIdx.x == 0) {
-    __threadfence();
+    if (sys) __threadfence_system();
+    else __threadfence();
     const unsigned t = atomicAdd(counter, 1u);
     s_last = (t == gridDim.x - 1);
   }
@@ -454,7 +581,8 @@ __device__ __forceinline__ bool last_block(unsigned* counter) {
   return s_last;
 }
 
-// Row range of block b under partition-aligned blocking.
+// Global row of thread threadIdx.x in block b under partition-aligned
+// blocking (rows of the held partitions only).
 __device__ __forceinline__ int block_row(const PartBlocks& pb, int b, int& rend) {
   const int d = block_part(pb, b);
   rend = pb.rend[d];
@@ -464,7 +592,8 @@ __device__ __forceinline__ int block_row(const PartBlocks& pb, int b, int& rend)
 // dot(u, v) per partition + ascending sum into *out (used for ||b||, rho0).
 __global__ void __launch_bounds__(256) k_dot2(PartBlocks pb, const double* __restrict__ u, const double* __restrict__ v,
                                               const double* __restrict__ u2, const double* __restrict__ v2,
-                                              double* partials, unsigned* counter, double* out) {
+                                              double* partials, unsigned* counter, double* out, CommView cv,
+                                              int ntot) {
   __shared__ double smem[2 * 32];
   int rend;
   const int r = block_row(pb, blockIdx.x, rend);
@@ -478,9 +607,9 @@ __global__ void __launch_bounds__(256) k_dot2(PartBlocks pb, const double* __res
     partials[2 * blockIdx.x] = s[0];
     partials[2 * blockIdx.x + 1] = s[1];
   }
-  if (!last_block(counter)) return;
+  if (!last_block(counter, false)) return;
   double t[2];
-  finalize_sums<2>(pb, partials, t, smem);
+  finalize_sums<2>(pb, partials, t, smem, cv, ntot);
   if (threadIdx.x == 0) {
     out[0] = t[0];
     out[1] = t[1];
@@ -490,16 +619,18 @@ __global__ void __launch_bounds__(256) k_dot2(PartBlocks pb, const double* __res
 
 // Block-Jacobi inverse of the diagonal blocks (solver.hpp:49-65) with the
 // cofactor inverse of oracle/shim/Eigen/Dense; identity when absent.
+// dinv is indexed by global row.
 __global__ void k_dinv(SellView A, double* __restrict__ dinv) {
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= A.rows) return;
-  const int len = A.rowlen[r];
-  const int64_t base = A.slice_off[r >> 5] + (r & 31);
+  const int lr = blockIdx.x * blockDim.x + threadIdx.x;
+  if (lr >= A.rows) return;
+  const int r = A.row0 + lr;
+  const int len = A.rowlen[lr];
+  const int64_t base = A.slice_off[lr >> 5] + (lr & 31);
   double m[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
   for (int k = 0; k < len; ++k) {
     const int64_t at = base + (int64_t)k * kSlice;
     if ((A.cols[at] & kColMask) == r) {
-      for (int q = 0; q < 9; ++q) m[q] = A.vals[vidx(at, r & 31, q)];
+      for (int q = 0; q < 9; ++q) m[q] = A.vals[vidx(at, lr & 31, q)];
       break;
     }
   }
@@ -539,12 +670,14 @@ __device__ __forceinline__ void precond_row(const double* __restrict__ dinv, boo
   z2 = ((0.0 + m[6] * r0) + m[7] * r1) + m[8] * r2;
 }
 
-// PCG init: x = 0, r = b, z = M^-1 r (p = z is formed by the first SpMV).
-__global__ void k_pcg_init(int rows, const double* __restrict__ b, const double* __restrict__ dinv, bool bj,
-                           double* __restrict__ x, double* __restrict__ r, double* __restrict__ z,
+// PCG init over the held rows: x = 0, r = b, z = M^-1 r (p = z is formed by
+// the first SpMV).
+__global__ void k_pcg_init(int row0, int rows, const double* __restrict__ b, const double* __restrict__ dinv,
+                           bool bj, double* __restrict__ x, double* __restrict__ r, double* __restrict__ z,
                            double* __restrict__ p) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= rows) return;
+  const int lr = blockIdx.x * blockDim.x + threadIdx.x;
+  if (lr >= rows) return;
+  const int i = row0 + lr;
   const double b0 = b[3 * i], b1 = b[3 * i + 1], b2 = b[3 * i + 2];
   double z0, z1, z2;
   precond_row(dinv, bj, i, b0, b1, b2, z0, z1, z2);
@@ -568,11 +701,14 @@ struct PcgArgs {
   int bj;
   const double* dinv;
   double *x, *r, *z, *p, *q, *partials, *hist, *phist;
+  CommView cv;
+  PartMap pm;
 };
 
 // Iteration kernel 1: q = A p with p = z (+ beta p) formed on the fly;
 // p.q partials; last block: curvature checks and alpha = rho / pq.
-template <bool kSingle, bool kPair>
+// kRemote: columns of other ranks are gathered over peer memory.
+template <bool kSingle, bool kPair, bool kRemote>
 __global__ void __launch_bounds__(256) k_pcg_spmv(const PcgArgs* __restrict__ args, PcgState* st) {
   __shared__ double smem[32];
   if (st->done) return;
@@ -607,13 +743,15 @@ __global__ void __launch_bounds__(256) k_pcg_spmv(const PcgArgs* __restrict__ ar
   }
   const int r = (kSingle && kPair) ? -1 : block_row(g.pb, blockIdx.x, rend);
   if (!(kSingle && kPair) && r < rend) {
+    const int lr = r - A.row0;
     double y0, y1, y2;
     if constexpr (kSingle) {
-      if (first) row_product_1<1>(A, r, z, p, beta, y0, y1, y2);
-      else row_product_1<2>(A, r, z, p, beta, y0, y1, y2);
+      if (first) row_product_1<1>(A, lr, z, p, beta, y0, y1, y2);
+      else row_product_1<2>(A, lr, z, p, beta, y0, y1, y2);
     } else {
-      if (first) row_product<1>(A, r, g.ngroups, z, p, beta, y0, y1, y2);
-      else row_product<2>(A, r, g.ngroups, z, p, beta, y0, y1, y2);
+      const unsigned long long vexp = kRemote ? g.cv.seq[0] : 0;
+      if (first) row_product<1, kRemote>(A, lr, g.ngroups, z, p, beta, y0, y1, y2, g.cv, g.pm, vexp);
+      else row_product<2, kRemote>(A, lr, g.ngroups, z, p, beta, y0, y1, y2, g.cv, g.pm, vexp);
     }
     q[3 * r] = y0;
     q[3 * r + 1] = y1;
@@ -628,9 +766,9 @@ __global__ void __launch_bounds__(256) k_pcg_spmv(const PcgArgs* __restrict__ ar
   }
   block_sum<1>(s, smem);
   if (threadIdx.x == 0) g.partials[blockIdx.x] = s[0];
-  if (!last_block(&st->counter)) return;
+  if (!last_block(&st->counter, false)) return;
   double t[1];
-  finalize_sums<1>((kSingle && kPair) ? g.pb2 : g.pb, g.partials, t, smem);
+  finalize_sums<1>((kSingle && kPair) ? g.pb2 : g.pb, g.partials, t, smem, g.cv, g.pm.n);
   if (threadIdx.x == 0) {
     st->counter = 0;
     const double pq = t[0];
@@ -720,9 +858,13 @@ __global__ void __launch_bounds__(256) k_pcg_update(const PcgArgs* __restrict__ 
     g.partials[2 * blockIdx.x] = s[0];
     g.partials[2 * blockIdx.x + 1] = s[1];
   }
-  if (!last_block(&st->counter)) return;
+  const bool peers = g.cv.world > 1;
+  if (!last_block(&st->counter, peers)) return;
+  // z and p of the held rows are final: release them to the peers before
+  // waiting on the reduction, so their next SpMV can start gathering.
+  if (peers && threadIdx.x == 0) publish_vec(g.cv);
   double t[2];
-  finalize_sums<2>(g.pb, g.partials, t, smem);
+  finalize_sums<2>(g.pb, g.partials, t, smem, g.cv, g.pm.n);
   if (threadIdx.x == 0) {
     st->counter = 0;
     const int it = st->iter + 1;
@@ -762,20 +904,22 @@ void pcg_free(Ctx& c) {
 PcgResult pcg_solve(Ctx& c, const double* b_dev, const weft_pcg_config& cfg, double* hist_host,
                     double* phist_host) {
   if (!c.has_matrix) throw Error(WEFT_ERR_INVALID, "pcg: no matrix");
-  const int rows = c.A.rows;
-  const size_t len = 3 * static_cast<size_t>(rows);
+  comm_need(c, "pcg");
+  const int rows = c.A.rows;                               // held rows
+  const size_t len = 3 * static_cast<size_t>(c.pm.p);      // vectors: global row index
   const int threads = 256;
+  const bool peers = c.world > 1;
   if (!c.pcg) {
     WG_CUDA(cudaMalloc(&c.pcg, sizeof(PcgState)));
     WG_CUDA(cudaHostAlloc(&c.pcg_host, sizeof(PcgState), cudaHostAllocDefault));
   }
   for (auto* v : {&c.r, &c.z, &c.pv, &c.q, &c.xs}) v->resize(len);
   const bool bj = cfg.preconditioner == WEFT_PRECOND_BLOCK_JACOBI;
-  c.dinv.resize(9 * static_cast<size_t>(rows) + 9);
+  c.dinv.resize(9 * static_cast<size_t>(c.pm.p) + 9);
   const int max_it = std::max(cfg.max_iterations, 0);
   c.hist.resize(static_cast<size_t>(max_it) + 1);
   c.phist.resize(static_cast<size_t>(max_it) + 1);
-  const PartBlocks pb = part_blocks(c.pm, threads);
+  const PartBlocks pb = part_blocks(c, threads);
   const int nblocks = pb.bstart[pb.n];
   c.partials.resize(4 * static_cast<size_t>(nblocks) + 4);
   const SellView A = view(c.A);
@@ -788,16 +932,18 @@ PcgResult pcg_solve(Ctx& c, const double* b_dev, const weft_pcg_config& cfg, dou
   double* dots = reinterpret_cast<double*>(c.scalars.data());
   if (rows > 0) {
     if (bj) k_dinv<<<div_up(rows, threads), threads, 0, ls(c)>>>(A, c.dinv.data());
-    k_pcg_init<<<div_up(rows, threads), threads, 0, ls(c)>>>(rows, b_dev, c.dinv.data(), bj, c.xs.data(), c.r.data(),
-                                                         c.z.data(), c.pv.data());
+    k_pcg_init<<<div_up(rows, threads), threads, 0, ls(c)>>>(c.row0, rows, b_dev, c.dinv.data(), bj, c.xs.data(),
+                                                         c.r.data(), c.z.data(), c.pv.data());
+    if (peers) publish_vectors(c);  // z of the held rows, gathered by the first SpMV
     // ||b|| and rho = r.z (r = b)
     k_dot2<<<nblocks, threads, 0, ls(c)>>>(pb, b_dev, b_dev, c.r.data(), c.z.data(), c.partials.data(),
-                                       &c.pcg->counter, dots);
+                                       &c.pcg->counter, dots, c.comm, c.nparts);
     WG_CUDA(cudaGetLastError());
   }
   double hd[2] = {0.0, 0.0};
   if (rows > 0) WG_CUDA(cudaMemcpyAsync(hd, dots, sizeof(hd), cudaMemcpyDeviceToHost, s));
   WG_CUDA(cudaStreamSynchronize(s));
+  comm_check(c);
   PcgResult res;
   const double b_norm = std::sqrt(hd[0]);
   if (b_norm == 0.0) {
@@ -812,15 +958,16 @@ PcgResult pcg_solve(Ctx& c, const double* b_dev, const weft_pcg_config& cfg, dou
   WG_CUDA(cudaMemcpyAsync(c.pcg, &init, sizeof(init), cudaMemcpyHostToDevice, s));
 
   // per-solve argument block (device)
-  const PartBlocks pb2 = part_blocks(c.pm, threads / 2);
+  const PartBlocks pb2 = part_blocks(c, threads / 2);
   const int nblocks2 = pb2.bstart[pb2.n];
   PcgArgs args{A, pb, pb2, c.go.n, bj ? 1 : 0, c.dinv.data(), c.xs.data(), c.r.data(), c.z.data(), c.pv.data(),
-               c.q.data(), c.partials.data(), c.hist.data(), c.phist.data()};
+               c.q.data(), c.partials.data(), c.hist.data(), c.phist.data(), c.comm, c.pm};
   c.pcg_args.resize(sizeof(PcgArgs));
   const PcgArgs* dargs = reinterpret_cast<const PcgArgs*>(c.pcg_args.data());
   WG_CUDA(cudaMemcpyAsync(c.pcg_args.data(), &args, sizeof(args), cudaMemcpyHostToDevice, s));
   const bool pair = c.go.n == 1 && c.spmv_pair;
-  auto spmv_kernel = c.go.n == 1 ? (pair ? k_pcg_spmv<true, true> : k_pcg_spmv<true, false>) : k_pcg_spmv<false, false>;
+  auto spmv_kernel = c.go.n == 1 ? (pair ? k_pcg_spmv<true, true, false> : k_pcg_spmv<true, false, false>)
+                                 : (peers ? k_pcg_spmv<false, false, true> : k_pcg_spmv<false, false, false>);
   auto* hs = static_cast<PcgState*>(c.pcg_host);
 
   if (!c.profile && c.use_graphs) {
@@ -918,6 +1065,7 @@ PcgResult pcg_solve(Ctx& c, const double* b_dev, const weft_pcg_config& cfg, dou
       chunk = std::min(chunk * 2, 32);  // <= 32 (event pool of 64)
     }
   }
+  comm_check(c);
   res.iterations = hs->iter;
   res.converged = hs->converged;
   res.rel_residual = hs->r_norm / b_norm;

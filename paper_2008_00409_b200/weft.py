@@ -91,6 +91,43 @@ class MatrixInfo(C.Structure):
                 ("padded_slots", C.c_int64)]
 
 
+class RankInfo(C.Structure):
+    _fields_ = [("world", C.c_int32), ("rank", C.c_int32), ("first_row", C.c_int32), ("rows", C.c_int32),
+                ("global_rows", C.c_int32)]
+
+
+IPC_HANDLE_BYTES = 64
+
+
+def rank_partitions(partitions: int, world: int, rank: int):
+    """Partition range [begin, end) of `rank` in a group of `world` ranks
+    over `partitions` logical partitions (equal contiguous ranges)."""
+    if world < 1 or partitions % world != 0 or not 0 <= rank < world:
+        raise TopologyError(f"{partitions} partitions cannot be split over {world} ranks")
+    span = partitions // world
+    return rank * span, (rank + 1) * span
+
+
+def exchange_handles(mine: bytes, world: int, group=None) -> list:
+    """All ranks' window handles in rank order (torch.distributed
+    all_gather_object; the bytes are opaque, any backend works)."""
+    import torch.distributed as dist
+    if dist.get_world_size(group) != world:
+        raise TopologyError(f"process group has {dist.get_world_size(group)} ranks, the engine expects {world}")
+    allh = [None] * world
+    dist.all_gather_object(allh, mine, group=group)
+    return allh
+
+
+def rank_share(total: int, world: int, rank: int):
+    """This rank's range of split_workload(total, world) (collision.cpp:
+    181-192): the pair-space share a rank walks in the replicated broad
+    phase (csrc/sim.cu mirrors it)."""
+    base, extra = divmod(total, world)
+    b = rank * base + min(rank, extra)
+    return b, b + base + (1 if rank < extra else 0)
+
+
 class GridInfo(C.Structure):
     _fields_ = [("cell_size", C.c_double), ("cells", C.c_int64), ("entries", C.c_int64), ("total", C.c_int64)]
 
@@ -207,13 +244,21 @@ class HashGrid:
 
 
 class Engine:
-    """A GPU context with ``devices`` logical row partitions (weft::Engine)."""
+    """A GPU context with ``devices`` logical row partitions (weft::Engine).
 
-    def __init__(self, devices: int = 1, cuda_device: int = 0):
+    ``world``/``rank`` > 1 make it one rank of a group (one process per GPU)
+    holding partitions ``rank_partitions(devices, world, rank)``; call
+    ``attach_peers`` once the vertex count is known (after set_vertices or
+    set_matrix)."""
+
+    def __init__(self, devices: int = 1, cuda_device: int = 0, world: int = 1, rank: int = 0):
         self._ctx = C.c_void_p()
-        opts = Options(cuda_device, devices, 0, devices)
+        b, e = rank_partitions(devices, world, rank)
+        opts = Options(cuda_device, devices, b, e)
         _check(LIB.weft_gpu_create(C.byref(opts), C.byref(self._ctx)))
         self.devices = devices
+        self.world = world
+        self.rank = rank
 
     def close(self):
         if self._ctx:
@@ -232,6 +277,28 @@ class Engine:
     def __exit__(self, *exc):
         self.close()
 
+    # -- rank group ---------------------------------------------------------
+    def rank_info(self) -> RankInfo:
+        info = RankInfo()
+        _check(LIB.weft_gpu_rank_info(self._ctx, C.byref(info)))
+        return info
+
+    def comm_export(self) -> bytes:
+        h = (C.c_ubyte * IPC_HANDLE_BYTES)()
+        _check(LIB.weft_gpu_comm_export(self._ctx, h))
+        return bytes(h)
+
+    def comm_attach(self, handles):
+        if len(handles) != self.world or any(len(h) != IPC_HANDLE_BYTES for h in handles):
+            raise Error("comm_attach: need one handle per rank")
+        buf = (C.c_ubyte * (IPC_HANDLE_BYTES * self.world)).from_buffer_copy(b"".join(handles))
+        _check(LIB.weft_gpu_comm_attach(self._ctx, buf))
+
+    def attach_peers(self, group=None):
+        """Exports this rank's window and maps every peer's, exchanging the
+        handle bytes through torch.distributed (any backend)."""
+        self.comm_attach(exchange_handles(self.comm_export(), self.world, group))
+
     # -- sparse -------------------------------------------------------------
     def set_matrix(self, m: BlockCsr):
         _check(LIB.weft_gpu_set_matrix(self._ctx, C.c_int32(m.rows), _ptr(np.ascontiguousarray(m.row_ptr, np.int64)),
@@ -240,11 +307,11 @@ class Engine:
     def spmv_pipelined(self, m: BlockCsr | None, x) -> np.ndarray:
         if m is not None:
             self.set_matrix(m)
-        info = self.matrix_info()
+        rows = self.rank_info().global_rows
         x = _f64(x)
-        if len(x) != 3 * info.block_rows:
+        if len(x) != 3 * rows:
             raise DimensionError("spmv_pipelined: dim(x) != rows")
-        y = np.zeros(3 * info.block_rows)
+        y = np.zeros(3 * rows)
         _check(LIB.weft_gpu_spmv(self._ctx, _ptr(x), _ptr(y)))
         return y
 
@@ -273,8 +340,7 @@ class Engine:
         if m is not None:
             self.set_matrix(m)
         config = config or PcgConfig()
-        info = self.matrix_info()
-        n = 3 * info.block_rows
+        n = 3 * self.rank_info().global_rows
         x = np.zeros(n)
         hist = np.zeros(max(config.max_iterations, 1))
         phist = np.zeros(max(config.max_iterations, 1))
