@@ -195,17 +195,31 @@ def gpu_arm(args, rank, world, local):
     import torch
     import torch.distributed as dist
 
+    # WEFT_BENCH_ONE_GPU=1: every rank on cuda:0 with gloo plumbing — a
+    # functional check of the rank-group path on a 1-GPU box (time-sliced
+    # contexts; its timings are meaningless).
+    one_gpu = os.environ.get("WEFT_BENCH_ONE_GPU") == "1"
+    if one_gpu:
+        local = 0
     torch.cuda.set_device(local)
+    backend = "gloo" if one_gpu else "nccl"
     if world > 1 and not dist.is_initialized():
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2008_00409_b200 import weft
 
     sc = make_scene(args.config, args.seed)
     mesh = weft.ClothMesh.build(sc.verts, sc.tris, sc.density)
     elems = mesh.build_elements(sc.material, sc.gravity)
     p = mesh.vertex_count
-    eng = weft.Engine(1, cuda_device=local)
+    # one logical partition per rank: the rows of the cloth are split over
+    # the GPUs (strong scaling of the one 1.65M-triangle problem)
+    eng = weft.Engine(world, cuda_device=local, world=world, rank=rank)
     eng.set_vertices(mesh.vertex_mass, sc.pinned)
+    if world > 1:
+        eng.attach_peers()
     eng.set_elements(elems)
     eng.set_soup(p, sc.tris)
     x0 = sc.verts.reshape(-1).copy()
@@ -221,12 +235,15 @@ def gpu_arm(args, rank, world, local):
             dist.barrier()
         torch.cuda.synchronize()
 
-    def max_over_ranks(v: float) -> float:
+    def reduce_over_ranks(v: float, op) -> float:
         if world == 1:
             return v
-        t = torch.tensor([v], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t = torch.tensor([v], dtype=torch.float64, device="cpu" if backend == "gloo" else "cuda")
+        dist.all_reduce(t, op=op)
         return float(t.item())
+
+    def max_over_ranks(v: float) -> float:
+        return reduce_over_ranks(v, dist.ReduceOp.MAX)
 
     # settle: the replayed state S (device-resident copy + pinned host copy)
     for _ in range(args.settle):
@@ -288,12 +305,18 @@ def gpu_arm(args, rank, world, local):
         e1.synchronize()
         barrier()
         e2e_ms = max_over_ranks(e0.elapsed_time(e1))
-        e2e = {"value": world * args.steps / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": 2 * 8 * 3 * p,
-               "d2h_bytes_per_step": 2 * 8 * 3 * p}
+        # every rank uploads the full state (x, v) and reads it back
+        e2e = {"value": args.steps / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": world * 2 * 8 * 3 * p,
+               "d2h_bytes_per_step": world * 2 * 8 * 3 * p}
 
+    # candidate counts: each rank walks its split_workload share
+    dcd_total = int(reduce_over_ranks(float(reps[-1].dcd_candidates), dist.ReduceOp.SUM if world > 1 else None))
+    ccd_total = int(reduce_over_ranks(float(reps[-1].ccd_candidates), dist.ReduceOp.SUM if world > 1 else None))
+    barrier()  # no rank unmaps its window while a peer may still read it
     if rank != 0:
+        eng.close()
         return
-    value = world * args.steps / (ms_total / 1e3)
+    value = args.steps / (ms_total / 1e3)  # whole-job steps/s (one step = the whole cloth on all ranks)
     peak, peak_src = peaks()
     # algorithmic bytes of one k_pcg_spmv launch: 9 FP64 values + 1 int32
     # column per live block; per row: length word, z and p gathered once,
@@ -314,16 +337,18 @@ def gpu_arm(args, rank, world, local):
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_total / args.steps, "higher_is_better": True,
-        "scaling": "weak" if world > 1 else "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {
             "workload": f"config {args.config}: {sc.layers} x {sc.nx}^2 layered cloth, {sc.tri_count} tris, "
                         f"{p} verts, pinned top edges, dt={sc.dt:.6g}, PCG tol 1e-4 block-Jacobi; every step "
                         f"replays the state after {args.settle} steps from rest",
-            "parallelism": "single GPU" if world == 1 else f"{world} independent replicas (partitioned multi-GPU "
-                                                            "path not enabled in this build)",
+            "parallelism": "single GPU" if world == 1 else (
+                f"{world} ranks, one row partition each (make_partitions); PCG halos and ordered dot "
+                "reductions over peer memory (CUDA IPC / NVLink), replicated broad phase with split pair ranges"
+                + (" [WEFT_BENCH_ONE_GPU: all ranks time-sliced on one GPU, functional check only]" if one_gpu else "")),
             "l2": "inputs larger than L2 (matrix alone ~0.75 GB)",
             "pcg_iterations_mean": statistics.mean(it), "nnzb": info.nnzb, "block_rows": info.block_rows,
-            "dcd_candidates": reps[-1].dcd_candidates, "ccd_candidates": reps[-1].ccd_candidates,
+            "dcd_candidates": dcd_total, "ccd_candidates": ccd_total,
             "stage_ms_mean": {"broad": statistics.mean(r.ms_broad for r in reps),
                               "assemble": statistics.mean(r.ms_assemble for r in reps),
                               "solve": statistics.mean(r.ms_solve for r in reps)},
