@@ -274,16 +274,16 @@ def gpu_arm(args, rank, world, local):
     clk = clocks.stop()
     ms_total = max_over_ranks(ev0.elapsed_time(ev1))
     launches = eng.stats().launches - launches0
-    # Kernel timing for the roofline: the timed region runs the PCG as one
-    # CUDA graph, so the SpMV launches are timed with CUDA events on the
-    # context stream in a profiled replay of the same step (chunked launches,
-    # identical kernels and inputs).
+    # Kernel timing for the roofline, CUDA events on the context stream in a
+    # profiled replay of the same step: the one-partition solve is ONE
+    # persistent kernel (timed whole); the multi-partition solve runs as a
+    # CUDA graph, so its SpMV launches are timed one by one (chunked
+    # launches, identical kernels and inputs).
     eng.profile(True)
     for _ in range(2):
         replay()
     st = eng.stats()
     eng.profile(False)
-    spmv_avg_ms = st.spmv_ms / max(st.spmv_launches, 1)
     info = eng.matrix_info()
 
     # ---- end-to-end through the C-ABI with host buffers
@@ -318,12 +318,26 @@ def gpu_arm(args, rank, world, local):
         return
     value = args.steps / (ms_total / 1e3)  # whole-job steps/s (one step = the whole cloth on all ranks)
     peak, peak_src = peaks()
-    # algorithmic bytes of one k_pcg_spmv launch: 9 FP64 values + 1 int32
-    # column per live block; per row: length word, z and p gathered once,
-    # q written.
-    alg_bytes = info.nnzb * (9 * 8 + 4) + info.block_rows * (4 + 3 * 8 * 3)
-    achieved = alg_bytes / (spmv_avg_ms * 1e-3) / 1e9
-    traffic = traffic_per_launch(args.config)
+    if st.pcg_solves:
+        # k_pcg_persistent: per iteration, phase A streams 9
+        # FP64 values + 1 int32 column per live block and per row the length
+        # word, z and p gathered once, q and p written (4 + 4*24 B); phase B
+        # reads p, q, x, r (96 B) and D^-1 (72 B) and writes x, r, z (72 B).
+        kname = "k_pcg_persistent (whole PCG solve, one launch)"
+        it_bytes = info.nnzb * (9 * 8 + 4) + info.block_rows * (4 + 4 * 24 + 96 + 72 + 72)
+        alg_bytes = it_bytes * st.pcg_iterations / st.pcg_solves
+        launch_ms = st.pcg_ms / st.pcg_solves
+        nlaunch = st.pcg_solves
+        traffic = None
+    else:
+        # k_pcg_spmv: 9 FP64 values + 1 int32 column per live block; per
+        # row: length word, z and p gathered once, q written.
+        kname = "k_pcg_spmv"
+        alg_bytes = info.nnzb * (9 * 8 + 4) + info.block_rows * (4 + 3 * 8 * 3)
+        launch_ms = st.spmv_ms / max(st.spmv_launches, 1)
+        nlaunch = st.spmv_launches
+        traffic = traffic_per_launch(args.config)
+    achieved = alg_bytes / (launch_ms * 1e-3) / 1e9
     it = [r.pcg_iterations for r in reps]
     cpu = None
     if not args.no_cpu_baseline and world == 1:
@@ -354,9 +368,9 @@ def gpu_arm(args, rank, world, local):
                               "solve": statistics.mean(r.ms_solve for r in reps)},
             "gpu_launches_per_step": launches / args.steps,
         },
-        "roofline": {"bound": "hbm", "kernel": "k_pcg_spmv", "achieved": achieved, "peak": peak, "unit": "GB/s",
+        "roofline": {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "alg_bytes_per_launch": alg_bytes,
-                     "avg_launch_ms": spmv_avg_ms, "launches": st.spmv_launches, "peak_source": peak_src},
+                     "avg_launch_ms": launch_ms, "launches": nlaunch, "peak_source": peak_src},
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": launches,

@@ -309,12 +309,17 @@ weft_status weft_gpu_sim_get_state(weft_gpu_ctx* ctx, double* x, double* v);
 /* ---------------------------------------------------------------------- */
 
 typedef struct weft_gpu_stats_t {
-  int64_t launches;      /* kernels of this library launched by the context */
-  int64_t spmv_launches; /* PCG SpMV launches timed while profiling */
-  double spmv_ms;        /* their summed device time (CUDA events) */
+  int64_t launches;       /* kernels of this library launched by the context */
+  int64_t spmv_launches;  /* PCG SpMV launches timed while profiling (graph/launch path) */
+  double spmv_ms;         /* their summed device time (CUDA events) */
+  int64_t pcg_solves;     /* persistent PCG kernels timed while profiling */
+  int64_t pcg_iterations; /* their iterations */
+  double pcg_ms;          /* their summed device time (CUDA events) */
 } weft_gpu_stats_t;
 
-/* Enables per-launch CUDA-event timing of the PCG SpMV kernel (resets). */
+/* Enables CUDA-event timing of the PCG kernels (resets the counters):
+ * each SpMV launch on the multi-kernel path, each whole-solve persistent
+ * kernel on the one-partition path. */
 weft_status weft_gpu_profile(weft_gpu_ctx* ctx, int32_t enable);
 weft_status weft_gpu_stats(weft_gpu_ctx* ctx, weft_gpu_stats_t* out);
 /* Test hook for the exact serial-order sum behind build_grid's cell size

@@ -42,6 +42,25 @@ def _compile(src: str, verbose: bool) -> str:
     return obj
 
 
+def build_variant(tag: str, defines: list[str]) -> str:
+    """Dev only: a copy of the library compiled with extra -D flags into
+    build/variants/ (load it with WEFT_LIB=...)."""
+    out_dir = os.path.join(OBJ, "variants", tag)
+    os.makedirs(out_dir, exist_ok=True)
+    objs = []
+    for src in SOURCES:
+        obj = os.path.join(out_dir, os.path.splitext(src)[0] + ".o")
+        r = subprocess.run([NVCC, *NVCC_FLAGS, *defines, "-c", os.path.join(CSRC, src), "-o", obj],
+                           capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr}")
+        objs.append(obj)
+    out = os.path.join(out_dir, "libweft_gpu.so")
+    subprocess.run([NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", out, *objs, "-cudart",
+                    "static"], check=True)
+    return out
+
+
 def build(verbose: bool = False) -> str:
     os.makedirs(OBJ, exist_ok=True)
     srcs = [s for s in SOURCES if os.path.exists(os.path.join(CSRC, s))]

@@ -141,6 +141,7 @@ weft_status weft_gpu_create(const weft_gpu_options* opts, weft_gpu_ctx** out) {
     c.scalars.resize(64);
     if (const char* e = std::getenv("WEFT_SPMV_PAIR")) c.spmv_pair = std::atoi(e) != 0;
     if (const char* e = std::getenv("WEFT_NO_GRAPHS")) c.use_graphs = std::atoi(e) == 0;
+    if (const char* e = std::getenv("WEFT_PCG_PERSISTENT")) c.use_persistent = std::atoi(e) != 0;
     // accumulation group order from the work queues
     const int n = c.nparts;
     c.go.n = n;
@@ -318,6 +319,9 @@ weft_status weft_gpu_profile(weft_gpu_ctx* ctx, int32_t enable) {
     ctx->c.profile = enable != 0;
     ctx->c.spmv_launches = 0;
     ctx->c.spmv_ms = 0.0;
+    ctx->c.pcg_solves = 0;
+    ctx->c.pcg_iterations = 0;
+    ctx->c.pcg_ms = 0.0;
   });
 }
 
@@ -326,6 +330,9 @@ weft_status weft_gpu_stats(weft_gpu_ctx* ctx, weft_gpu_stats_t* out) {
     out->launches = ctx->c.launches;
     out->spmv_launches = ctx->c.spmv_launches;
     out->spmv_ms = ctx->c.spmv_ms;
+    out->pcg_solves = ctx->c.pcg_solves;
+    out->pcg_iterations = ctx->c.pcg_iterations;
+    out->pcg_ms = ctx->c.pcg_ms;
   });
 }
 

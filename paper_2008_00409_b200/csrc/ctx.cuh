@@ -113,6 +113,8 @@ struct Ctx {
   bool pcg_exec_single = false;
   bool pcg_exec_pair = false;
   bool spmv_pair = false;  // two threads per row SpMV variant (WEFT_SPMV_PAIR=1)
+  bool use_persistent = true;  // one-partition solves: one cooperative kernel (WEFT_PCG_PERSISTENT=0: graph)
+  DBuf<double> p2;             // its second search-direction buffer
 
   // ---- broad phase
   int soup_verts = 0, soup_tris = 0;
@@ -145,6 +147,9 @@ struct Ctx {
   bool profile = false;           // time every PCG SpMV launch with events
   int64_t spmv_launches = 0;      // PCG SpMV launches timed
   double spmv_ms = 0.0;           // their summed device time
+  int64_t pcg_solves = 0;         // persistent solves timed while profiling
+  int64_t pcg_iterations = 0;     // their iterations
+  double pcg_ms = 0.0;            // their summed device time
   std::vector<cudaEvent_t> prof_ev;
 
   // ---- resident simulation state

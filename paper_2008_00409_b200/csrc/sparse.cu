@@ -20,6 +20,8 @@
 #include <cstring>
 #include <numeric>
 
+#include <cooperative_groups.h>
+
 #include "ctx.cuh"
 
 namespace weft_gpu {
@@ -703,6 +705,7 @@ struct PcgArgs {
   double *x, *r, *z, *p, *q, *partials, *hist, *phist;
   CommView cv;
   PartMap pm;
+  double* p2;  // persistent solve: second search-direction buffer
 };
 
 // Iteration kernel 1: q = A p with p = z (+ beta p) formed on the fly;
@@ -892,6 +895,233 @@ __global__ void __launch_bounds__(256) k_pcg_update(const PcgArgs* __restrict__ 
   }
 }
 
+// ---------------------------------------------------------------------------
+// Persistent PCG (one partition, one rank): the whole solve is ONE cooperative
+// kernel. Each warp owns a fixed set of 32-row slices; an iteration is
+//   phase A  q = A p_k (p_k = z_k + beta p_{k-1} formed on the fly, two
+//            gathers), p_k of the own rows to the other p buffer, p.q
+//   grid sync, every block reduces the per-block partials in the same fixed
+//            order -> bitwise identical alpha everywhere
+//   phase B  x += alpha p, r -= alpha q, z = D^-1 r, r.r and r.z
+//   grid sync, reduce -> residual test, beta
+// No kernel boundary, no launch gap, no host round trip per iteration. The
+// vectors written inside the kernel are read with ld.global.cg (L2, never a
+// stale L1 line); the matrix stream uses the read-only path.
+// ---------------------------------------------------------------------------
+constexpr int kPersistThreads = 256;
+#ifndef WEFT_PERSIST_MINB
+#define WEFT_PERSIST_MINB 2  // 16 warps/SM, no spills (measured best on B200 vs 3-6)
+#endif
+#ifndef WEFT_MAT_LD
+#define WEFT_MAT_LD(p) __ldg(p)
+#endif
+
+template <int PMode>
+__device__ __forceinline__ void row_product_cg(const SellView& A, int r, const double* __restrict__ z,
+                                               const double* __restrict__ pold, double beta, double& y0, double& y1,
+                                               double& y2) {
+  const int len = A.rowlen[r];
+  const int64_t base = A.slice_off[r >> 5] + (r & 31);
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+  int cn = len > 0 ? (WEFT_MAT_LD(A.cols + base) & kColMask) : 0;
+#pragma unroll 2
+  for (int k = 0; k < len; ++k) {
+    const int64_t at = base + (int64_t)k * kSlice;
+    const int c = cn;
+    if (k + 1 < len) cn = WEFT_MAT_LD(A.cols + at + kSlice) & kColMask;
+    const double* v = A.vals + vidx(at, r & 31, 0);
+    const double v0 = WEFT_MAT_LD(v), v1 = WEFT_MAT_LD(v + 32), v2 = WEFT_MAT_LD(v + 64);
+    const double v3 = WEFT_MAT_LD(v + 96), v4 = WEFT_MAT_LD(v + 128), v5 = WEFT_MAT_LD(v + 160);
+    const double v6 = WEFT_MAT_LD(v + 192), v7 = WEFT_MAT_LD(v + 224), v8 = WEFT_MAT_LD(v + 256);
+    double x0 = __ldcg(z + 3 * c), x1 = __ldcg(z + 3 * c + 1), x2 = __ldcg(z + 3 * c + 2);
+    if (PMode == 2) {
+      x0 = x0 + beta * __ldcg(pold + 3 * c);
+      x1 = x1 + beta * __ldcg(pold + 3 * c + 1);
+      x2 = x2 + beta * __ldcg(pold + 3 * c + 2);
+    }
+    a0 = a0 + ((v0 * x0 + v1 * x1) + v2 * x2);
+    a1 = a1 + ((v3 * x0 + v4 * x1) + v5 * x2);
+    a2 = a2 + ((v6 * x0 + v7 * x1) + v8 * x2);
+  }
+  y0 = a0;
+  y1 = a1;
+  y2 = a2;
+}
+
+// Sum of partials[i * NV + k] over i < n in a fixed order, result in every
+// thread of the block (identical in every block).
+template <int NV>
+__device__ __forceinline__ void all_blocks_sum(const double* partials, int n, double (&out)[NV], double* smem) {
+  double v[NV];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) v[k] = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x)
+#pragma unroll
+    for (int k = 0; k < NV; ++k) v[k] = v[k] + __ldcg(partials + (size_t)i * NV + k);
+  block_sum<NV>(v, smem);
+  __shared__ double bc[NV];
+  if (threadIdx.x == 0)
+#pragma unroll
+    for (int k = 0; k < NV; ++k) bc[k] = v[k];
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < NV; ++k) out[k] = bc[k];
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kPersistThreads, WEFT_PERSIST_MINB) k_pcg_persistent(const PcgArgs* __restrict__ args, PcgState* st) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double smem[2 * 32];
+  const PcgArgs& g = *args;
+  const SellView A = g.A;
+  const int rows = A.rows;
+  const int nslices = (rows + kSlice - 1) / kSlice;
+  const int warps = blockDim.x >> 5;
+  const int gw = blockIdx.x * warps + (threadIdx.x >> 5), tw = gridDim.x * warps;
+  const int lane = threadIdx.x & 31;
+  const int G = gridDim.x;
+  const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
+  double* __restrict__ x = g.x;
+  double* __restrict__ r = g.r;
+  double* __restrict__ z = g.z;
+  double* __restrict__ q = g.q;
+  double* pcur = g.p;
+  double* pnew = g.p2;
+  const double* __restrict__ dinv = g.dinv;
+  const bool bj = g.bj != 0;
+  double rho = st->rho;
+  const double tol = st->tol, b_norm = st->b_norm;
+  const int max_it = st->max_iter;
+  double beta = 0.0, r_norm = st->r_norm;
+  int it = 0, status = 0, converged = 0;
+  bool done = st->done != 0;
+  bool first = true;
+  while (!done) {
+    // ---- phase A: q = A p, p of the own rows, p.q
+    double s1[1] = {0.0};
+    for (int sl = gw; sl < nslices; sl += tw) {
+      const int i = sl * kSlice + lane;
+      if (i < rows) {
+        double y0, y1, y2;
+        if (first) row_product_cg<1>(A, i, z, pcur, beta, y0, y1, y2);
+        else row_product_cg<2>(A, i, z, pcur, beta, y0, y1, y2);
+        double p0 = __ldcg(z + 3 * i), p1 = __ldcg(z + 3 * i + 1), p2 = __ldcg(z + 3 * i + 2);
+        if (!first) {
+          p0 = p0 + beta * __ldcg(pcur + 3 * i);
+          p1 = p1 + beta * __ldcg(pcur + 3 * i + 1);
+          p2 = p2 + beta * __ldcg(pcur + 3 * i + 2);
+        }
+        __stcg(q + 3 * i, y0);
+        __stcg(q + 3 * i + 1, y1);
+        __stcg(q + 3 * i + 2, y2);
+        __stcg(pnew + 3 * i, p0);
+        __stcg(pnew + 3 * i + 1, p1);
+        __stcg(pnew + 3 * i + 2, p2);
+        s1[0] = s1[0] + ((p0 * y0 + p1 * y1) + p2 * y2);
+      }
+    }
+    block_sum<1>(s1, smem);
+    if (threadIdx.x == 0) __stcg(g.partials + blockIdx.x, s1[0]);
+    grid.sync();
+    double pq[1];
+    all_blocks_sum<1>(g.partials, G, pq, smem);
+    if (!isfinite(pq[0])) {
+      status = 1;
+      ++it;
+      break;
+    }
+    if (pq[0] <= 0.0) {
+      status = 2;
+      ++it;
+      break;
+    }
+    const double alpha = rho / pq[0];
+    // ---- phase B: x, r, z over the same rows (own writes, read back by the same thread)
+    double s2[2] = {0.0, 0.0};
+    for (int sl = gw; sl < nslices; sl += tw) {
+      const int i = sl * kSlice + lane;
+      if (i < rows) {
+        double pv[3], qv[3], xv[3], rv[3], m[9];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          pv[c] = __ldcg(pnew + 3 * i + c);
+          qv[c] = __ldcg(q + 3 * i + c);
+          xv[c] = __ldcg(x + 3 * i + c);
+          rv[c] = __ldcg(r + 3 * i + c);
+        }
+        if (bj) {
+#pragma unroll
+          for (int k = 0; k < 9; ++k) m[k] = __ldg(dinv + 9 * (size_t)i + k);
+        }
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          xv[c] = xv[c] + alpha * pv[c];
+          rv[c] = rv[c] - alpha * qv[c];
+        }
+        double z0, z1, z2;
+        if (bj) {  // apply_precond (solver.hpp:67-89)
+          z0 = ((0.0 + m[0] * rv[0]) + m[1] * rv[1]) + m[2] * rv[2];
+          z1 = ((0.0 + m[3] * rv[0]) + m[4] * rv[1]) + m[5] * rv[2];
+          z2 = ((0.0 + m[6] * rv[0]) + m[7] * rv[1]) + m[8] * rv[2];
+        } else {
+          z0 = rv[0];
+          z1 = rv[1];
+          z2 = rv[2];
+        }
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          __stcg(x + 3 * i + c, xv[c]);
+          __stcg(r + 3 * i + c, rv[c]);
+        }
+        __stcg(z + 3 * i, z0);
+        __stcg(z + 3 * i + 1, z1);
+        __stcg(z + 3 * i + 2, z2);
+        s2[0] = s2[0] + ((rv[0] * rv[0] + rv[1] * rv[1]) + rv[2] * rv[2]);
+        s2[1] = s2[1] + ((rv[0] * z0 + rv[1] * z1) + rv[2] * z2);
+      }
+    }
+    block_sum<2>(s2, smem);
+    if (threadIdx.x == 0) {
+      __stcg(g.partials + G + 2 * blockIdx.x, s2[0]);
+      __stcg(g.partials + G + 2 * blockIdx.x + 1, s2[1]);
+    }
+    grid.sync();
+    double t[2];
+    all_blocks_sum<2>(g.partials + G, G, t, smem);
+    ++it;
+    r_norm = sqrt(t[0]);
+    if (!isfinite(r_norm)) {
+      status = 3;
+      break;
+    }
+    if (lead) {
+      g.hist[it - 1] = r_norm / b_norm;
+      g.phist[it - 1] = sqrt(t[1] > 0.0 ? t[1] : 0.0);
+    }
+    if (r_norm <= tol) {
+      converged = 1;
+      break;
+    }
+    beta = t[1] / rho;
+    rho = t[1];
+    if (it >= max_it) break;
+    double* tmp = pcur;
+    pcur = pnew;
+    pnew = tmp;
+    first = false;
+  }
+  if (lead) {
+    st->iter = it;
+    st->status = status;
+    st->converged = converged;
+    st->r_norm = r_norm;
+    st->rho = rho;
+    st->beta = beta;
+    st->done = 1;
+  }
+}
+
 void pcg_free(Ctx& c) {
   if (c.pcg_exec) cudaGraphExecDestroy(c.pcg_exec);
   c.pcg_exec = nullptr;
@@ -960,8 +1190,18 @@ PcgResult pcg_solve(Ctx& c, const double* b_dev, const weft_pcg_config& cfg, dou
   // per-solve argument block (device)
   const PartBlocks pb2 = part_blocks(c, threads / 2);
   const int nblocks2 = pb2.bstart[pb2.n];
+  const bool persistent = c.go.n == 1 && c.world == 1 && c.use_persistent;
+  int pgrid = 0;
+  if (persistent) {
+    int occ = 0, sms = 0;
+    WG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_pcg_persistent, kPersistThreads, 0));
+    WG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device));
+    pgrid = std::max(1, occ) * sms;
+    c.p2.resize(len);
+    if (c.partials.size() < 3 * static_cast<size_t>(pgrid) + 4) c.partials.resize(3 * static_cast<size_t>(pgrid) + 4);
+  }
   PcgArgs args{A, pb, pb2, c.go.n, bj ? 1 : 0, c.dinv.data(), c.xs.data(), c.r.data(), c.z.data(), c.pv.data(),
-               c.q.data(), c.partials.data(), c.hist.data(), c.phist.data(), c.comm, c.pm};
+               c.q.data(), c.partials.data(), c.hist.data(), c.phist.data(), c.comm, c.pm, c.p2.data()};
   c.pcg_args.resize(sizeof(PcgArgs));
   const PcgArgs* dargs = reinterpret_cast<const PcgArgs*>(c.pcg_args.data());
   WG_CUDA(cudaMemcpyAsync(c.pcg_args.data(), &args, sizeof(args), cudaMemcpyHostToDevice, s));
@@ -970,7 +1210,24 @@ PcgResult pcg_solve(Ctx& c, const double* b_dev, const weft_pcg_config& cfg, dou
                                  : (peers ? k_pcg_spmv<false, false, true> : k_pcg_spmv<false, false, false>);
   auto* hs = static_cast<PcgState*>(c.pcg_host);
 
-  if (!c.profile && c.use_graphs) {
+  if (persistent) {
+    // the whole solve: one cooperative launch (co-resident grid, grid syncs)
+    void* kargs[] = {(void*)&dargs, (void*)&c.pcg};
+    if (c.profile) WG_CUDA(cudaEventRecord(c.ev[6], s));
+    WG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_pcg_persistent), dim3(pgrid), dim3(kPersistThreads),
+                                        kargs, 0, s));
+    ++c.launches;
+    if (c.profile) WG_CUDA(cudaEventRecord(c.ev[7], s));
+    WG_CUDA(cudaMemcpyAsync(hs, c.pcg, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
+    WG_CUDA(cudaStreamSynchronize(s));
+    if (c.profile) {
+      float ms = 0.f;
+      WG_CUDA(cudaEventElapsedTime(&ms, c.ev[6], c.ev[7]));
+      c.pcg_ms += ms;
+      c.pcg_iterations += hs->iter;
+      ++c.pcg_solves;
+    }
+  } else if (!c.profile && c.use_graphs) {
     // The whole solve is one graph launch: a conditional WHILE node whose
     // body is the two iteration kernels; the update kernel's last block
     // clears the condition when the solve is done.
@@ -1033,7 +1290,7 @@ PcgResult pcg_solve(Ctx& c, const double* b_dev, const weft_pcg_config& cfg, dou
       c.launches += 2 * std::max(hs->iter, 1);
     }
   }
-  if (c.profile || !c.use_graphs) {
+  if (!persistent && (c.profile || !c.use_graphs)) {
     int chunk = 4;
     int iter_before = 0;
     for (;;) {

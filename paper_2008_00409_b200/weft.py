@@ -27,7 +27,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libweft_gpu.so")
+LIB_PATH = os.environ.get("WEFT_LIB") or os.path.join(_PKG, "libweft_gpu.so")  # WEFT_LIB: dev variants only
 
 STRETCH, BEND, SPRING, EXTERNAL, CONTACT = range(5)
 JAC_EXACT, JAC_SPD = 0, 1
@@ -503,7 +503,8 @@ class ClothMesh:
 
 
 class GpuStats(C.Structure):
-    _fields_ = [("launches", C.c_int64), ("spmv_launches", C.c_int64), ("spmv_ms", C.c_double)]
+    _fields_ = [("launches", C.c_int64), ("spmv_launches", C.c_int64), ("spmv_ms", C.c_double),
+                ("pcg_solves", C.c_int64), ("pcg_iterations", C.c_int64), ("pcg_ms", C.c_double)]
 
 
 def _engine_profile(self, enable: bool = True):
