@@ -427,13 +427,14 @@ __global__ void k_slice_width(int p, int nslices, const int32_t* __restrict__ le
 // first, then the work-queue order (sparse.hpp:89-95); ascending inside a
 // group. Padding slots get -1.
 __global__ void k_merge_fill(int row0, int nloc, MergeIn m, PartMap pm, GroupOrder go,
-                             const int64_t* __restrict__ soff, const int32_t* __restrict__ len,
+                             const int64_t* __restrict__ soff, const int32_t* __restrict__ pos,
                              int32_t* __restrict__ cols) {
   const int lr = blockIdx.x * blockDim.x + threadIdx.x;
   if (lr >= nloc) return;
   const int r = row0 + lr;
-  const int s = lr >> 5;
-  const int64_t base = soff[s] + (lr & 31);
+  const int mp = pos[lr];  // matrix position of the row (SELL-32-sigma)
+  const int s = mp >> 5;
+  const int64_t base = soff[s] + (mp & 31);
   const int width = static_cast<int>((soff[s + 1] - soff[s]) / kSlice);
   const int d = pm.owner(r);
   int k = 0;
@@ -466,12 +467,14 @@ static void build_layout(Ctx& c) {
   A.rows = nloc;
   A.row0 = c.row0;
   A.nslices = div_up(nloc, kSlice);
-  A.rowlen.resize(static_cast<size_t>(nloc) + 1);
   A.slice_off.resize(static_cast<size_t>(A.nslices) + 1);
-  if (nloc) {
-    k_merge_len<<<div_up(nloc, 256), 256, 0, ls(c)>>>(c.row0, nloc, m, A.rowlen.data());
+  DBuf<int32_t> len_row;
+  len_row.resize(static_cast<size_t>(nloc) + 1);
+  if (nloc) k_merge_len<<<div_up(nloc, 256), 256, 0, ls(c)>>>(c.row0, nloc, m, len_row.data());
+  build_sigma(c, len_row.data());  // A.perm / A.pos / A.rowlen (by position)
+  ++A.layout_id;
+  if (nloc)
     k_slice_width<<<div_up(A.nslices, 256), 256, 0, ls(c)>>>(nloc, A.nslices, A.rowlen.data(), A.slice_off.data());
-  }
   WG_CUDA(cudaMemsetAsync(A.slice_off.data() + A.nslices, 0, sizeof(int64_t), s));
   size_t tmp = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, tmp, A.slice_off.data(), A.slice_off.data(), A.nslices + 1, s);
@@ -501,7 +504,7 @@ static void build_layout(Ctx& c) {
   A.cols.resize(static_cast<size_t>(total) + 1);
   A.vals.resize(9 * static_cast<size_t>(total) + 9);
   if (nloc)
-    k_merge_fill<<<div_up(nloc, 256), 256, 0, ls(c)>>>(c.row0, nloc, m, c.pm, c.go, A.slice_off.data(), A.rowlen.data(),
+    k_merge_fill<<<div_up(nloc, 256), 256, 0, ls(c)>>>(c.row0, nloc, m, c.pm, c.go, A.slice_off.data(), A.pos.data(),
                                                       A.cols.data());
   WG_CUDA(cudaGetLastError());
   WG_CUDA(cudaStreamSynchronize(s));  // cptr/ccol die here
@@ -513,8 +516,9 @@ static void build_layout(Ctx& c) {
 constexpr int kFillThreadsConst = 64;
 
 struct FillArgs {
-  int p;     // held rows (local row lr = global row - row0)
+  int p;     // held rows (threads walk matrix positions; row = row0 + perm[m])
   int row0;
+  const int32_t* __restrict__ perm;
   int64_t n_static;
   double dt;
   bool exact;
@@ -557,11 +561,11 @@ struct Acc {
 template <bool Wide, bool Exact>
 __global__ void __launch_bounds__(64) k_fill(FillArgs f) {
   extern __shared__ double smem[];
-  const int lr = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lr = blockIdx.x * blockDim.x + threadIdx.x;  // matrix position
   const int len = lr < f.p ? f.rowlen[lr] : 0;
   const bool mine = lr < f.p && (Wide ? len > f.wcap : len <= f.wcap);
   if (!mine) return;
-  const int r = f.row0 + lr;
+  const int r = f.row0 + f.perm[lr];
   const int64_t base = f.slice_off[lr >> 5] + (lr & 31);
   int32_t* colbuf = reinterpret_cast<int32_t*>(smem + (size_t)f.wcap * 9 * blockDim.x);
   Acc<Wide> acc{smem, (int)threadIdx.x, (int)blockDim.x, f.vals, f.total, base};
@@ -987,6 +991,7 @@ __global__ void __launch_bounds__(128) k_elem_eval(ElemArgs g) {
 struct SlotArgs {
   int p;     // held rows
   int row0;  // global index of the first
+  const int32_t* __restrict__ perm;  // matrix position -> local row
   int64_t n_static;
   double dt;
   const int64_t* __restrict__ slice_off;
@@ -1045,18 +1050,56 @@ __global__ void __launch_bounds__(kSlotWarps * 32, 2) k_fill_slots(SlotArgs g) {
   __shared__ int4 sm_st[kStageCap];
   __shared__ int sm_ksa[kStageCap], sm_pay[kStageCap], sm_res[kStageCap];
   __shared__ double sm_damp[kStageCap];
-  __shared__ int sm_row[2][kSlice + 1];  // per pass: row -> first staged entry
+  __shared__ int sm_row[2][kSlice + 1];  // per pass: lane -> first staged entry
+  __shared__ int64_t sm_beg[2][kSlice];   // per pass: lane -> first incidence
+  __shared__ int sm_rid[kSlice];          // lane -> global row
   const int slice = blockIdx.x;
-  const int r0 = g.row0 + slice * kSlice;  // global row of lane 0
   const int rows = min(kSlice, g.p - slice * kSlice);
-  const int64_t s0 = g.inc_ptr[r0], s1 = g.inc_ptr[r0 + rows];
-  const int64_t c0 = g.cinc_ptr[r0], c1 = g.cinc_ptr[r0 + rows];
-  const int nstat = static_cast<int>(s1 - s0), ncont = static_cast<int>(c1 - c0);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // The slice's rows (SELL-32-sigma positions -> rows, not contiguous):
+  // per-lane incidence counts, warp-scanned into staging offsets.
+  if (warp == 0) {
+    int row = 0, ns = 0, nc = 0;
+    if (lane < rows) {
+      row = g.row0 + g.perm[slice * kSlice + lane];
+      const int64_t a0 = g.inc_ptr[row], c0 = g.cinc_ptr[row];
+      ns = static_cast<int>(g.inc_ptr[row + 1] - a0);
+      nc = static_cast<int>(g.cinc_ptr[row + 1] - c0);
+      sm_beg[0][lane] = a0;
+      sm_beg[1][lane] = c0;
+      sm_rid[lane] = row;
+    }
+    int ps = ns, pc = nc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int ts = __shfl_up_sync(0xffffffffu, ps, o), tc = __shfl_up_sync(0xffffffffu, pc, o);
+      if (lane >= o) {
+        ps += ts;
+        pc += tc;
+      }
+    }
+    const int tots = __shfl_sync(0xffffffffu, ps, 31);
+    sm_row[0][lane] = ps - ns;  // exclusive
+    sm_row[1][lane] = tots + pc - nc;
+    if (lane == 31) {
+      sm_row[0][32] = tots;
+      sm_row[1][32] = tots + pc;
+    }
+  }
+  __syncthreads();
+  const int nstat = sm_row[0][32], ncont = sm_row[1][32] - nstat;
   const bool staged = nstat + ncont <= kStageCap;
   if (staged) {
     for (int i = threadIdx.x; i < nstat + ncont; i += blockDim.x) {
       const bool cpass = i >= nstat;
-      const int code = cpass ? g.cinc[c0 + (i - nstat)] : g.inc[s0 + i];
+      const int* off = sm_row[cpass ? 1 : 0];
+      int l = 0;  // lane whose range holds i (ranges of lanes >= rows are empty)
+#pragma unroll
+      for (int step = 16; step > 0; step >>= 1)
+        if (l + step <= 32 && off[l + step] <= i) l += step;
+      while (l + 1 < 32 && off[l + 1] <= i) ++l;
+      const int64_t at = sm_beg[cpass ? 1 : 0][l] + (i - off[l]);
+      const int code = cpass ? g.cinc[at] : g.inc[at];
       const int64_t e = (cpass ? g.n_static : 0) + (code >> 2);
       const int2 info = g.einfo[e];
       const int ss = (info.x >> 8) & 0xff;
@@ -1066,15 +1109,10 @@ __global__ void __launch_bounds__(kSlotWarps * 32, 2) k_fill_slots(SlotArgs g) {
       sm_res[i] = g.eres_off[e] + 3 * ss;
       sm_damp[i] = g.edamp[e];
     }
-    for (int i = threadIdx.x; i <= rows; i += blockDim.x) {
-      sm_row[0][i] = static_cast<int>(g.inc_ptr[r0 + i] - s0);
-      sm_row[1][i] = nstat + static_cast<int>(g.cinc_ptr[r0 + i] - c0);
-    }
   }
   __syncthreads();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int r = r0 + lane;
   if (lane >= rows) return;
+  const int r = sm_rid[lane];
   const int len = g.rowlen[slice * kSlice + lane];
   const int64_t base = g.slice_off[slice] + lane;
   const double dt = g.dt;
@@ -1221,6 +1259,7 @@ void fill_matrix(Ctx& c, const double* xc, const double* xa, const double* vel, 
   FillArgs f{};
   f.p = nloc;
   f.row0 = c.row0;
+  f.perm = A.perm.data();
   f.n_static = c.n_static;
   f.dt = dt;
   f.exact = mode == WEFT_JAC_EXACT;
@@ -1260,7 +1299,7 @@ void fill_matrix(Ctx& c, const double* xc, const double* xa, const double* vel, 
     ElemArgs ea{ne, list, dt, c.est.data(), c.einfo.data(), c.edamp.data(), c.epay.data(), c.eres_off.data(),
                 c.eres.data(), xc, xa, vel};
     if (ne) k_elem_eval<<<div_up(ne, 128), 128, 0, ls(c)>>>(ea);
-    SlotArgs sa{nloc, c.row0, c.n_static, dt, A.slice_off.data(), A.rowlen.data(), A.cols.data(), A.vals.data(),
+    SlotArgs sa{nloc, c.row0, A.perm.data(), c.n_static, dt, A.slice_off.data(), A.rowlen.data(), A.cols.data(), A.vals.data(),
                 A.total, c.mass.data(), c.pinned.data(), c.inc_ptr.data(), c.inc.data(), c.cinc_ptr.data(),
                 c.cinc.data(), c.est.data(), c.einfo.data(), c.edamp.data(), c.epay.data(), c.eres_off.data(),
                 c.eres.data(), c.rhs.data(), bad};

@@ -23,12 +23,22 @@ struct SellMatrix {
   int64_t nnzb = 0;
   int max_len = 0;
   DBuf<int64_t> slice_off;  // nslices + 1
-  DBuf<int32_t> rowlen;     // rows
+  DBuf<int32_t> rowlen;     // rows, by matrix position
+  // SELL-32-sigma: matrix position m holds local row perm[m]; rows are
+  // sorted by descending length inside windows of kSigma rows (aligned to
+  // partition starts), so a slice's rows have (nearly) equal lengths and
+  // no padding is streamed. Per-row slot order is untouched.
+  DBuf<int32_t> perm;       // rows
+  DBuf<int32_t> pos;        // rows: local row -> matrix position
+  DBuf<int32_t> colp;       // total: column words as positions (one-partition persistent PCG)
+  int64_t layout_id = 0;    // bumped whenever the layout changes
+  int64_t colp_id = -1;     // layout colp was built for
   DBuf<int32_t> cols;       // total (packed col | group << 28; -1 padding)
   DBuf<double> vals;        // 9 * total
 };
 
 constexpr int kColMask = 0x0FFFFFFF;
+constexpr int kSigma = 256;  // sorting window of the SELL-32-sigma layout
 
 // Value index of component q (row-major 3x3) of the slot at column-index
 // position `at` of a row with lane = row % 32: the nine components of one
@@ -102,6 +112,7 @@ struct Ctx {
 
   // ---- PCG work
   DBuf<double> r, z, pv, q, xs, dinv, bvec;
+  DBuf<double> xp;  // persistent PCG: solution in position space
   DBuf<double> partials;
   DBuf<double> hist, phist;
   PcgState* pcg = nullptr;       // device
@@ -165,6 +176,11 @@ inline cudaStream_t ls(Ctx& c) {
 
 // ---- entry points implemented across the .cu files
 void set_matrix_csr(Ctx& c, int rows, const int64_t* row_ptr, const int32_t* cols, const double* vals);
+// Window starts (local rows) of the sigma sort: partition-aligned chunks.
+std::vector<int32_t> sigma_windows(const Ctx& c);
+// Device sigma layout from per-row lengths (local row order): fills A.perm,
+// A.pos and A.rowlen (by position).
+void build_sigma(Ctx& c, const int32_t* len_row);
 void spmv(Ctx& c, const double* x_dev, double* y_dev);
 void download_csr(Ctx& c, int64_t* row_ptr, int32_t* cols, double* vals);
 struct PcgResult {

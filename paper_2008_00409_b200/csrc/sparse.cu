@@ -30,17 +30,20 @@ namespace weft_gpu {
 // Matrix view passed to kernels
 // ---------------------------------------------------------------------------
 struct SellView {
-  int rows;  // held rows; kernel row indices below are LOCAL (global - row0)
+  int rows;  // held rows; the matrix is addressed by POSITION m (SELL-32-sigma),
+             // local row perm[m], global row row0 + perm[m]
   int row0;
   int64_t total;
   const int64_t* __restrict__ slice_off;
   const int32_t* __restrict__ rowlen;
   const int32_t* __restrict__ cols;
   const double* __restrict__ vals;
+  const int32_t* __restrict__ perm;  // matrix position -> local row
 };
 
 static SellView view(const SellMatrix& A) {
-  return SellView{A.rows, A.row0, A.total, A.slice_off.data(), A.rowlen.data(), A.cols.data(), A.vals.data()};
+  return SellView{A.rows,        A.row0,       A.total,       A.slice_off.data(), A.rowlen.data(),
+                  A.cols.data(), A.vals.data(), A.perm.data()};
 }
 
 // Blocks are aligned to partitions so that every block's dot partial
@@ -288,10 +291,11 @@ __device__ __forceinline__ void row_product_pair(const SellView& A, int r, bool 
 }
 
 __global__ void __launch_bounds__(256) k_spmv_pair(SellView A, const double* __restrict__ x, double* __restrict__ y) {
-  const int r = blockIdx.x * (blockDim.x >> 1) + (threadIdx.x >> 1);
+  const int m = blockIdx.x * (blockDim.x >> 1) + (threadIdx.x >> 1);
   double y0, y1, y2;
-  row_product_pair<0>(A, r, r < A.rows, x, nullptr, 0.0, y0, y1, y2);
-  if (r < A.rows && (threadIdx.x & 1) == 0) {
+  row_product_pair<0>(A, m, m < A.rows, x, nullptr, 0.0, y0, y1, y2);
+  if (m < A.rows && (threadIdx.x & 1) == 0) {
+    const int r = A.perm[m];  // one partition, one rank: row0 == 0
     y[3 * r] = y0;
     y[3 * r + 1] = y1;
     y[3 * r + 2] = y2;
@@ -300,13 +304,13 @@ __global__ void __launch_bounds__(256) k_spmv_pair(SellView A, const double* __r
 
 __global__ void __launch_bounds__(256) k_spmv(SellView A, int ngroups, const double* __restrict__ x,
                                               double* __restrict__ y, CommView cv, PartMap pm) {
-  const int lr = blockIdx.x * blockDim.x + threadIdx.x;
-  if (lr >= A.rows) return;
-  const int r = A.row0 + lr;
+  const int m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= A.rows) return;
+  const int r = A.row0 + A.perm[m];
   double y0, y1, y2;
-  if (ngroups == 1) row_product_1<0>(A, lr, x, nullptr, 0.0, y0, y1, y2);
-  else if (cv.world > 1) row_product<0, true>(A, lr, ngroups, x, nullptr, 0.0, y0, y1, y2, cv, pm, cv.seq[0]);
-  else row_product<0>(A, lr, ngroups, x, nullptr, 0.0, y0, y1, y2);
+  if (ngroups == 1) row_product_1<0>(A, m, x, nullptr, 0.0, y0, y1, y2);
+  else if (cv.world > 1) row_product<0, true>(A, m, ngroups, x, nullptr, 0.0, y0, y1, y2, cv, pm, cv.seq[0]);
+  else row_product<0>(A, m, ngroups, x, nullptr, 0.0, y0, y1, y2);
   y[3 * r] = y0;
   y[3 * r + 1] = y1;
   y[3 * r + 2] = y2;
@@ -399,6 +403,50 @@ void set_rows(Ctx& c, int p) {
   c.row1 = c.pm.end(c.part_end - 1);
 }
 
+std::vector<int32_t> sigma_windows(const Ctx& c) {
+  std::vector<int32_t> w;
+  for (int d = c.part_begin; d < c.part_end; ++d) {
+    const int b = c.pm.begin(d) - c.row0, e = c.pm.end(d) - c.row0;
+    for (int s = b; s < e; s += kSigma) w.push_back(s);
+  }
+  w.push_back(c.row1 - c.row0);
+  return w;
+}
+
+// One block per window: stable sort of its rows by descending length
+// (rank = rows that are longer, or as long and earlier).
+__global__ void __launch_bounds__(kSigma) k_sigma(const int32_t* __restrict__ wstart, const int32_t* __restrict__ len,
+                                                  int32_t* __restrict__ perm, int32_t* __restrict__ pos,
+                                                  int32_t* __restrict__ len_m) {
+  __shared__ int32_t sl[kSigma];
+  const int a = wstart[blockIdx.x], n = wstart[blockIdx.x + 1] - a;
+  const int t = threadIdx.x;
+  if (t < n) sl[t] = len[a + t];
+  __syncthreads();
+  if (t >= n) return;
+  const int L = sl[t];
+  int rank = 0;
+  for (int j = 0; j < n; ++j) rank += (sl[j] > L) || (sl[j] == L && j < t);
+  perm[a + rank] = a + t;
+  pos[a + t] = a + rank;
+  len_m[a + rank] = L;
+}
+
+void build_sigma(Ctx& c, const int32_t* len_row) {
+  SellMatrix& A = c.A;
+  const std::vector<int32_t> w = sigma_windows(c);
+  DBuf<int32_t> wd;
+  wd.upload(w.data(), w.size(), c.stream);
+  A.perm.resize(static_cast<size_t>(A.rows) + 1);
+  A.pos.resize(static_cast<size_t>(A.rows) + 1);
+  A.rowlen.resize(static_cast<size_t>(A.rows) + 1);
+  if (w.size() > 1)
+    k_sigma<<<static_cast<int>(w.size()) - 1, kSigma, 0, ls(c)>>>(wd.data(), len_row, A.perm.data(), A.pos.data(),
+                                                                  A.rowlen.data());
+  WG_CUDA(cudaGetLastError());
+  WG_CUDA(cudaStreamSynchronize(c.stream));  // wd dies here
+}
+
 // Takes the GLOBAL block CSR (every rank passes the same matrix) and keeps
 // this rank's rows [row0, row1) (partition_matrix, sparse.hpp:103-147).
 void set_matrix_csr(Ctx& c, int rows, const int64_t* row_ptr, const int32_t* cols, const double* vals) {
@@ -417,16 +465,32 @@ void set_matrix_csr(Ctx& c, int rows, const int64_t* row_ptr, const int32_t* col
   int maxlen = 0;
   for (int r = 0; r < rows; ++r)
     if (row_ptr[r + 1] - row_ptr[r] < 0) throw Error(WEFT_ERR_DIMENSION, "set_matrix: row_ptr not monotone");
-  for (int lr = 0; lr < nloc; ++lr) {
-    const int r = c.row0 + lr;
+  // SELL-32-sigma: positions sorted by descending row length per window
+  std::vector<int32_t> perm(static_cast<size_t>(nloc)), pos(static_cast<size_t>(nloc));
+  {
+    const std::vector<int32_t> w = sigma_windows(c);
+    std::vector<std::pair<int, int>> v;
+    for (size_t k = 0; k + 1 < w.size(); ++k) {
+      v.clear();
+      for (int lr = w[k]; lr < w[k + 1]; ++lr)
+        v.push_back({-static_cast<int>(row_ptr[c.row0 + lr + 1] - row_ptr[c.row0 + lr]), lr});
+      std::stable_sort(v.begin(), v.end());
+      for (size_t i = 0; i < v.size(); ++i) {
+        perm[static_cast<size_t>(w[k]) + i] = v[i].second;
+        pos[static_cast<size_t>(v[i].second)] = w[k] + static_cast<int>(i);
+      }
+    }
+  }
+  for (int m = 0; m < nloc; ++m) {
+    const int r = c.row0 + perm[static_cast<size_t>(m)];
     const int64_t l = row_ptr[r + 1] - row_ptr[r];
-    len[static_cast<size_t>(lr)] = static_cast<int32_t>(l);
+    len[static_cast<size_t>(m)] = static_cast<int32_t>(l);
     nnzb += l;
     maxlen = std::max<int>(maxlen, static_cast<int>(l));
   }
   for (int s = 0; s < A.nslices; ++s) {
     int w = 0;
-    for (int lr = s * kSlice; lr < std::min(nloc, (s + 1) * kSlice); ++lr) w = std::max(w, len[static_cast<size_t>(lr)]);
+    for (int m = s * kSlice; m < std::min(nloc, (s + 1) * kSlice); ++m) w = std::max(w, len[static_cast<size_t>(m)]);
     soff[static_cast<size_t>(s) + 1] = soff[static_cast<size_t>(s)] + static_cast<int64_t>(w) * kSlice;
   }
   const int64_t total = soff.back();
@@ -435,6 +499,7 @@ void set_matrix_csr(Ctx& c, int rows, const int64_t* row_ptr, const int32_t* col
   std::vector<std::pair<int, int64_t>> order;  // (group, csr index)
   for (int lr = 0; lr < nloc; ++lr) {
     const int r = c.row0 + lr;
+    const int mp = pos[static_cast<size_t>(lr)];
     const int d = c.pm.owner(r);
     order.clear();
     for (int64_t k = row_ptr[r]; k < row_ptr[r + 1]; ++k) {
@@ -444,12 +509,12 @@ void set_matrix_csr(Ctx& c, int rows, const int64_t* row_ptr, const int32_t* col
     }
     std::stable_sort(order.begin(), order.end(),
                      [](const auto& a, const auto& b) { return a.first < b.first; });
-    const int64_t base = soff[static_cast<size_t>(lr / kSlice)] + lr % kSlice;
+    const int64_t base = soff[static_cast<size_t>(mp / kSlice)] + mp % kSlice;
     for (size_t s = 0; s < order.size(); ++s) {
       const int64_t at = base + static_cast<int64_t>(s) * kSlice;
       const int64_t k = order[s].second;
       hc[static_cast<size_t>(at)] = cols[k] | (order[s].first << kGroupShift);
-      for (int q = 0; q < 9; ++q) hv[static_cast<size_t>(vidx(at, lr % kSlice, q))] = vals[9 * k + q];
+      for (int q = 0; q < 9; ++q) hv[static_cast<size_t>(vidx(at, mp % kSlice, q))] = vals[9 * k + q];
     }
   }
   A.total = total;
@@ -457,9 +522,12 @@ void set_matrix_csr(Ctx& c, int rows, const int64_t* row_ptr, const int32_t* col
   A.max_len = maxlen;
   A.slice_off.upload(soff.data(), soff.size(), c.stream);
   A.rowlen.upload(len.data(), len.size(), c.stream);
+  A.perm.upload(perm.data(), perm.size(), c.stream);
+  A.pos.upload(pos.data(), pos.size(), c.stream);
   A.cols.upload(hc.data(), hc.size(), c.stream);
   A.vals.upload(hv.data(), hv.size(), c.stream);
   WG_CUDA(cudaStreamSynchronize(c.stream));
+  ++A.layout_id;
   c.has_matrix = true;
   c.has_rhs = false;
   c.have_pattern_for_contacts = false;
@@ -472,8 +540,10 @@ void download_csr(Ctx& c, int64_t* row_ptr, int32_t* cols, double* vals) {
   std::vector<int64_t> soff(A.slice_off.size());
   std::vector<int32_t> len(static_cast<size_t>(A.rows));
   std::vector<int32_t> hc(static_cast<size_t>(A.total));
+  std::vector<int32_t> pos(static_cast<size_t>(A.rows));
   A.slice_off.download(soff.data(), soff.size(), c.stream);
   A.rowlen.download(len.data(), len.size(), c.stream);
+  A.pos.download(pos.data(), pos.size(), c.stream);
   A.cols.download(hc.data(), hc.size(), c.stream);
   std::vector<double> hv;
   if (vals) {
@@ -485,9 +555,10 @@ void download_csr(Ctx& c, int64_t* row_ptr, int32_t* cols, double* vals) {
   std::vector<std::pair<int, int64_t>> order;
   if (row_ptr) row_ptr[0] = 0;
   for (int r = 0; r < A.rows; ++r) {
-    const int64_t base = soff[static_cast<size_t>(r / kSlice)] + r % kSlice;
+    const int mp = pos[static_cast<size_t>(r)];
+    const int64_t base = soff[static_cast<size_t>(mp / kSlice)] + mp % kSlice;
     order.clear();
-    for (int k = 0; k < len[static_cast<size_t>(r)]; ++k) {
+    for (int k = 0; k < len[static_cast<size_t>(mp)]; ++k) {
       const int64_t at = base + static_cast<int64_t>(k) * kSlice;
       order.push_back({hc[static_cast<size_t>(at)] & kColMask, at});
     }
@@ -495,7 +566,7 @@ void download_csr(Ctx& c, int64_t* row_ptr, int32_t* cols, double* vals) {
     for (const auto& [col, at] : order) {
       if (cols) cols[cursor] = col;
       if (vals)
-        for (int q = 0; q < 9; ++q) vals[9 * cursor + q] = hv[static_cast<size_t>(vidx(at, r % kSlice, q))];
+        for (int q = 0; q < 9; ++q) vals[9 * cursor + q] = hv[static_cast<size_t>(vidx(at, mp % kSlice, q))];
       ++cursor;
     }
     if (row_ptr) row_ptr[r + 1] = cursor;
@@ -622,17 +693,18 @@ __global__ void __launch_bounds__(256) k_dot2(PartBlocks pb, const double* __res
 // Block-Jacobi inverse of the diagonal blocks (solver.hpp:49-65) with the
 // cofactor inverse of oracle/shim/Eigen/Dense; identity when absent.
 // dinv is indexed by global row.
+template <bool kPosOut>
 __global__ void k_dinv(SellView A, double* __restrict__ dinv) {
-  const int lr = blockIdx.x * blockDim.x + threadIdx.x;
-  if (lr >= A.rows) return;
-  const int r = A.row0 + lr;
-  const int len = A.rowlen[lr];
-  const int64_t base = A.slice_off[lr >> 5] + (lr & 31);
+  const int mp = blockIdx.x * blockDim.x + threadIdx.x;
+  if (mp >= A.rows) return;
+  const int r = A.row0 + A.perm[mp];
+  const int len = A.rowlen[mp];
+  const int64_t base = A.slice_off[mp >> 5] + (mp & 31);
   double m[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
   for (int k = 0; k < len; ++k) {
     const int64_t at = base + (int64_t)k * kSlice;
     if ((A.cols[at] & kColMask) == r) {
-      for (int q = 0; q < 9; ++q) m[q] = A.vals[vidx(at, lr & 31, q)];
+      for (int q = 0; q < 9; ++q) m[q] = A.vals[vidx(at, mp & 31, q)];
       break;
     }
   }
@@ -643,7 +715,7 @@ __global__ void k_dinv(SellView A, double* __restrict__ dinv) {
   const double c00 = COF(0, 0), c10 = COF(1, 0), c20 = COF(2, 0);
   const double det = (c00 * M(0, 0) + c10 * M(1, 0)) + c20 * M(2, 0);
   const double invdet = 1.0 / det;
-  double* o = dinv + 9 * (size_t)r;
+  double* o = dinv + 9 * (kPosOut ? (size_t)mp : (size_t)r);
   o[0] = c00 * invdet;
   o[1] = c10 * invdet;
   o[2] = c20 * invdet;
@@ -726,12 +798,13 @@ __global__ void __launch_bounds__(256) k_pcg_spmv(const PcgArgs* __restrict__ ar
   double s[1] = {0.0};
   if constexpr (kSingle && kPair) {
     // two threads per row (single partition: rows [0, rows))
-    const int r = blockIdx.x * (blockDim.x >> 1) + (threadIdx.x >> 1);
-    const bool valid = r < A.rows;
+    const int m = blockIdx.x * (blockDim.x >> 1) + (threadIdx.x >> 1);
+    const bool valid = m < A.rows;
     double y0, y1, y2;
-    if (first) row_product_pair<1>(A, r, valid, z, p, beta, y0, y1, y2);
-    else row_product_pair<2>(A, r, valid, z, p, beta, y0, y1, y2);
+    if (first) row_product_pair<1>(A, m, valid, z, p, beta, y0, y1, y2);
+    else row_product_pair<2>(A, m, valid, z, p, beta, y0, y1, y2);
     if (valid && (threadIdx.x & 1) == 0) {
+      const int r = A.perm[m];
       q[3 * r] = y0;
       q[3 * r + 1] = y1;
       q[3 * r + 2] = y2;
@@ -744,17 +817,20 @@ __global__ void __launch_bounds__(256) k_pcg_spmv(const PcgArgs* __restrict__ ar
       s[0] = (p0 * y0 + p1 * y1) + p2 * y2;
     }
   }
-  const int r = (kSingle && kPair) ? -1 : block_row(g.pb, blockIdx.x, rend);
-  if (!(kSingle && kPair) && r < rend) {
-    const int lr = r - A.row0;
+  // the partition-aligned block layout walks matrix positions; each
+  // position's row lies in the same sigma window, hence the same partition
+  const int mg = (kSingle && kPair) ? -1 : block_row(g.pb, blockIdx.x, rend);
+  if (!(kSingle && kPair) && mg < rend) {
+    const int m = mg - A.row0;
+    const int r = A.row0 + A.perm[m];
     double y0, y1, y2;
     if constexpr (kSingle) {
-      if (first) row_product_1<1>(A, lr, z, p, beta, y0, y1, y2);
-      else row_product_1<2>(A, lr, z, p, beta, y0, y1, y2);
+      if (first) row_product_1<1>(A, m, z, p, beta, y0, y1, y2);
+      else row_product_1<2>(A, m, z, p, beta, y0, y1, y2);
     } else {
       const unsigned long long vexp = kRemote ? g.cv.seq[0] : 0;
-      if (first) row_product<1, kRemote>(A, lr, g.ngroups, z, p, beta, y0, y1, y2, g.cv, g.pm, vexp);
-      else row_product<2, kRemote>(A, lr, g.ngroups, z, p, beta, y0, y1, y2, g.cv, g.pm, vexp);
+      if (first) row_product<1, kRemote>(A, m, g.ngroups, z, p, beta, y0, y1, y2, g.cv, g.pm, vexp);
+      else row_product<2, kRemote>(A, m, g.ngroups, z, p, beta, y0, y1, y2, g.cv, g.pm, vexp);
     }
     q[3 * r] = y0;
     q[3 * r + 1] = y1;
@@ -981,6 +1057,7 @@ __global__ void __launch_bounds__(kPersistThreads, WEFT_PERSIST_MINB) k_pcg_pers
   const int gw = blockIdx.x * warps + (threadIdx.x >> 5), tw = gridDim.x * warps;
   const int lane = threadIdx.x & 31;
   const int G = gridDim.x;
+  (void)nslices;
   const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
   double* __restrict__ x = g.x;
   double* __restrict__ r = g.r;
@@ -1001,7 +1078,7 @@ __global__ void __launch_bounds__(kPersistThreads, WEFT_PERSIST_MINB) k_pcg_pers
     // ---- phase A: q = A p, p of the own rows, p.q
     double s1[1] = {0.0};
     for (int sl = gw; sl < nslices; sl += tw) {
-      const int i = sl * kSlice + lane;
+      const int i = sl * kSlice + lane;  // matrix position == vector index (position space)
       if (i < rows) {
         double y0, y1, y2;
         if (first) row_product_cg<1>(A, i, z, pcur, beta, y0, y1, y2);
@@ -1037,11 +1114,11 @@ __global__ void __launch_bounds__(kPersistThreads, WEFT_PERSIST_MINB) k_pcg_pers
       break;
     }
     const double alpha = rho / pq[0];
-    // ---- phase B: x, r, z over the same rows (own writes, read back by the same thread)
+    // ---- phase B: x, r, z (coalesced; q and p of phase A are visible after
+    // the grid sync, read through L2)
     double s2[2] = {0.0, 0.0};
-    for (int sl = gw; sl < nslices; sl += tw) {
-      const int i = sl * kSlice + lane;
-      if (i < rows) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < rows; i += gridDim.x * blockDim.x) {
+      {
         double pv[3], qv[3], xv[3], rv[3], m[9];
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
@@ -1122,6 +1199,46 @@ __global__ void __launch_bounds__(kPersistThreads, WEFT_PERSIST_MINB) k_pcg_pers
   }
 }
 
+// Position-space column words (one partition: no group bits; padding stays -1).
+__global__ void k_colpos(int64_t total, const int32_t* __restrict__ cols, const int32_t* __restrict__ pos,
+                         int32_t* __restrict__ colp) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= total) return;
+  const int c = cols[i];
+  colp[i] = c < 0 ? c : pos[c & kColMask];
+}
+
+// PCG init in position space: r = b[perm], z = M^-1 r, x = 0, p = 0.
+__global__ void k_pcg_init_pos(int rows, const int32_t* __restrict__ perm, const double* __restrict__ b,
+                               const double* __restrict__ dinv, bool bj, double* __restrict__ x,
+                               double* __restrict__ r, double* __restrict__ z, double* __restrict__ p) {
+  const int m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= rows) return;
+  const int i = perm[m];
+  const double b0 = b[3 * i], b1 = b[3 * i + 1], b2 = b[3 * i + 2];
+  double z0, z1, z2;
+  precond_row(dinv, bj, m, b0, b1, b2, z0, z1, z2);
+  x[3 * m] = x[3 * m + 1] = x[3 * m + 2] = 0.0;
+  r[3 * m] = b0;
+  r[3 * m + 1] = b1;
+  r[3 * m + 2] = b2;
+  z[3 * m] = z0;
+  z[3 * m + 1] = z1;
+  z[3 * m + 2] = z2;
+  p[3 * m] = p[3 * m + 1] = p[3 * m + 2] = 0.0;
+}
+
+// out[perm[m]] = in[m] (3 doubles per row).
+__global__ void k_scatter_rows(int rows, const int32_t* __restrict__ perm, const double* __restrict__ in,
+                               double* __restrict__ out) {
+  const int m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= rows) return;
+  const int i = perm[m];
+  out[3 * i] = in[3 * m];
+  out[3 * i + 1] = in[3 * m + 1];
+  out[3 * i + 2] = in[3 * m + 2];
+}
+
 void pcg_free(Ctx& c) {
   if (c.pcg_exec) cudaGraphExecDestroy(c.pcg_exec);
   c.pcg_exec = nullptr;
@@ -1139,6 +1256,10 @@ PcgResult pcg_solve(Ctx& c, const double* b_dev, const weft_pcg_config& cfg, dou
   const size_t len = 3 * static_cast<size_t>(c.pm.p);      // vectors: global row index
   const int threads = 256;
   const bool peers = c.world > 1;
+  // One partition on one rank: the whole solve is one persistent kernel in
+  // POSITION space (vectors and columns permuted to the SELL-32-sigma order,
+  // b gathered in, x scattered out), so every vector access is coalesced.
+  const bool persistent = c.go.n == 1 && c.world == 1 && c.use_persistent;
   if (!c.pcg) {
     WG_CUDA(cudaMalloc(&c.pcg, sizeof(PcgState)));
     WG_CUDA(cudaHostAlloc(&c.pcg_host, sizeof(PcgState), cudaHostAllocDefault));
@@ -1161,13 +1282,30 @@ PcgResult pcg_solve(Ctx& c, const double* b_dev, const weft_pcg_config& cfg, dou
   WG_CUDA(cudaMemcpyAsync(c.pcg, &init, sizeof(init), cudaMemcpyHostToDevice, s));
   double* dots = reinterpret_cast<double*>(c.scalars.data());
   if (rows > 0) {
-    if (bj) k_dinv<<<div_up(rows, threads), threads, 0, ls(c)>>>(A, c.dinv.data());
-    k_pcg_init<<<div_up(rows, threads), threads, 0, ls(c)>>>(c.row0, rows, b_dev, c.dinv.data(), bj, c.xs.data(),
-                                                         c.r.data(), c.z.data(), c.pv.data());
-    if (peers) publish_vectors(c);  // z of the held rows, gathered by the first SpMV
-    // ||b|| and rho = r.z (r = b)
-    k_dot2<<<nblocks, threads, 0, ls(c)>>>(pb, b_dev, b_dev, c.r.data(), c.z.data(), c.partials.data(),
-                                       &c.pcg->counter, dots, c.comm, c.nparts);
+    if (persistent) {
+      if (c.A.colp_id != c.A.layout_id) {  // position-space column words, once per layout
+        c.A.colp.resize(static_cast<size_t>(c.A.total) + 1);
+        if (c.A.total)
+          k_colpos<<<div_up(c.A.total, 256), 256, 0, ls(c)>>>(c.A.total, c.A.cols.data(), c.A.pos.data(),
+                                                               c.A.colp.data());
+        c.A.colp_id = c.A.layout_id;
+      }
+      c.xp.resize(len);
+      if (bj) k_dinv<true><<<div_up(rows, threads), threads, 0, ls(c)>>>(A, c.dinv.data());
+      k_pcg_init_pos<<<div_up(rows, threads), threads, 0, ls(c)>>>(rows, c.A.perm.data(), b_dev, c.dinv.data(), bj,
+                                                                   c.xp.data(), c.r.data(), c.z.data(), c.pv.data());
+      // ||b|| and rho = r.z over the permuted r = b
+      k_dot2<<<nblocks, threads, 0, ls(c)>>>(pb, c.r.data(), c.r.data(), c.r.data(), c.z.data(), c.partials.data(),
+                                         &c.pcg->counter, dots, c.comm, c.nparts);
+    } else {
+      if (bj) k_dinv<false><<<div_up(rows, threads), threads, 0, ls(c)>>>(A, c.dinv.data());
+      k_pcg_init<<<div_up(rows, threads), threads, 0, ls(c)>>>(c.row0, rows, b_dev, c.dinv.data(), bj, c.xs.data(),
+                                                           c.r.data(), c.z.data(), c.pv.data());
+      if (peers) publish_vectors(c);  // z of the held rows, gathered by the first SpMV
+      // ||b|| and rho = r.z (r = b)
+      k_dot2<<<nblocks, threads, 0, ls(c)>>>(pb, b_dev, b_dev, c.r.data(), c.z.data(), c.partials.data(),
+                                         &c.pcg->counter, dots, c.comm, c.nparts);
+    }
     WG_CUDA(cudaGetLastError());
   }
   double hd[2] = {0.0, 0.0};
@@ -1190,7 +1328,6 @@ PcgResult pcg_solve(Ctx& c, const double* b_dev, const weft_pcg_config& cfg, dou
   // per-solve argument block (device)
   const PartBlocks pb2 = part_blocks(c, threads / 2);
   const int nblocks2 = pb2.bstart[pb2.n];
-  const bool persistent = c.go.n == 1 && c.world == 1 && c.use_persistent;
   int pgrid = 0;
   if (persistent) {
     int occ = 0, sms = 0;
@@ -1202,6 +1339,10 @@ PcgResult pcg_solve(Ctx& c, const double* b_dev, const weft_pcg_config& cfg, dou
   }
   PcgArgs args{A, pb, pb2, c.go.n, bj ? 1 : 0, c.dinv.data(), c.xs.data(), c.r.data(), c.z.data(), c.pv.data(),
                c.q.data(), c.partials.data(), c.hist.data(), c.phist.data(), c.comm, c.pm, c.p2.data()};
+  if (persistent) {
+    args.A.cols = c.A.colp.data();  // columns as positions
+    args.x = c.xp.data();
+  }
   c.pcg_args.resize(sizeof(PcgArgs));
   const PcgArgs* dargs = reinterpret_cast<const PcgArgs*>(c.pcg_args.data());
   WG_CUDA(cudaMemcpyAsync(c.pcg_args.data(), &args, sizeof(args), cudaMemcpyHostToDevice, s));
@@ -1218,6 +1359,7 @@ PcgResult pcg_solve(Ctx& c, const double* b_dev, const weft_pcg_config& cfg, dou
                                         kargs, 0, s));
     ++c.launches;
     if (c.profile) WG_CUDA(cudaEventRecord(c.ev[7], s));
+    k_scatter_rows<<<div_up(rows, threads), threads, 0, ls(c)>>>(rows, c.A.perm.data(), c.xp.data(), c.xs.data());
     WG_CUDA(cudaMemcpyAsync(hs, c.pcg, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
     WG_CUDA(cudaStreamSynchronize(s));
     if (c.profile) {
