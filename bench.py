@@ -120,6 +120,19 @@ def traffic_per_launch(config: str):
     return d.get(config)
 
 
+def pcg_traffic_per_launch(config: str, iterations: float):
+    """DRAM bytes of one k_pcg_persistent launch from the committed ncu
+    --set full capture, scaled to this run's iteration count, or None."""
+    path = os.path.join(ROOT, "profiles", "pcg_traffic.json")
+    if not os.path.exists(path):
+        return None
+    with open(path) as f:
+        d = json.load(f).get(config)
+    if not d:
+        return None
+    return d["dram_bytes_per_launch"] / d["iterations"] * iterations
+
+
 # ---------------------------------------------------------------- scene
 def make_scene(config: str, seed: int):
     from paper_2008_00409_b200 import scenes
@@ -328,7 +341,7 @@ def gpu_arm(args, rank, world, local):
         alg_bytes = it_bytes * st.pcg_iterations / st.pcg_solves
         launch_ms = st.pcg_ms / st.pcg_solves
         nlaunch = st.pcg_solves
-        traffic = None
+        traffic = pcg_traffic_per_launch(args.config, st.pcg_iterations / st.pcg_solves)
     else:
         # k_pcg_spmv: 9 FP64 values + 1 int32 column per live block; per
         # row: length word, z and p gathered once, q written.
