@@ -335,9 +335,11 @@ def gpu_arm(args, rank, world, local):
         # k_pcg_persistent: per iteration, phase A streams 9
         # FP64 values + 1 int32 column per live block and per row the length
         # word, z and p gathered once, q and p written (4 + 4*24 B); phase B
-        # reads p, q, x, r (96 B) and D^-1 (72 B) and writes x, r, z (72 B).
+        # reads q, r (48 B) and D^-1 (72 B) and writes r, z (48 B), plus on
+        # every other iteration the deferred x update (x read + written, two
+        # p read: 96 B), i.e. 216 B/row on average.
         kname = "k_pcg_persistent (whole PCG solve, one launch)"
-        it_bytes = info.nnzb * (9 * 8 + 4) + info.block_rows * (4 + 4 * 24 + 96 + 72 + 72)
+        it_bytes = info.nnzb * (9 * 8 + 4) + info.block_rows * (4 + 4 * 24 + 216)
         alg_bytes = it_bytes * st.pcg_iterations / st.pcg_solves
         launch_ms = st.pcg_ms / st.pcg_solves
         nlaunch = st.pcg_solves

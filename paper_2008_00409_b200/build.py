@@ -44,8 +44,8 @@ def _compile(src: str, verbose: bool) -> str:
 
 def build_variant(tag: str, defines: list[str]) -> str:
     """Dev only: a copy of the library compiled with extra -D flags into
-    build/variants/ (load it with WEFT_LIB=...)."""
-    out_dir = os.path.join(OBJ, "variants", tag)
+    variants/<tag>/ (load it with WEFT_LIB=...)."""
+    out_dir = os.path.join(os.path.dirname(PKG), "variants", tag)
     os.makedirs(out_dir, exist_ok=True)
     objs = []
     for src in SOURCES:

@@ -991,6 +991,16 @@ constexpr int kPersistThreads = 256;
 #ifndef WEFT_MAT_LD
 #define WEFT_MAT_LD(p) __ldg(p)
 #endif
+#ifndef WEFT_PK_UNROLL
+#define WEFT_PK_UNROLL 2
+#endif
+constexpr int kPkUnroll = WEFT_PK_UNROLL;
+#ifndef WEFT_PK_PREFETCH
+#define WEFT_PK_PREFETCH 0
+#endif
+#ifndef WEFT_PK_XDEFER
+#define WEFT_PK_XDEFER 1
+#endif
 
 template <int PMode>
 __device__ __forceinline__ void row_product_cg(const SellView& A, int r, const double* __restrict__ z,
@@ -1000,7 +1010,7 @@ __device__ __forceinline__ void row_product_cg(const SellView& A, int r, const d
   const int64_t base = A.slice_off[r >> 5] + (r & 31);
   double a0 = 0.0, a1 = 0.0, a2 = 0.0;
   int cn = len > 0 ? (WEFT_MAT_LD(A.cols + base) & kColMask) : 0;
-#pragma unroll 2
+#pragma unroll kPkUnroll
   for (int k = 0; k < len; ++k) {
     const int64_t at = base + (int64_t)k * kSlice;
     const int c = cn;
@@ -1074,10 +1084,16 @@ __global__ void __launch_bounds__(kPersistThreads, WEFT_PERSIST_MINB) k_pcg_pers
   int it = 0, status = 0, converged = 0;
   bool done = st->done != 0;
   bool first = true;
+  bool x_pending = false;  // x += alpha_prev * p (p in pnew of the last phase B) not applied yet
+  double alpha_prev = 0.0;
   while (!done) {
     // ---- phase A: q = A p, p of the own rows, p.q
     double s1[1] = {0.0};
     for (int sl = gw; sl < nslices; sl += tw) {
+#if WEFT_PK_PREFETCH
+      // stream this warp's next slice into L2 while this one computes
+      if (lane == 0 && sl + tw < nslices) prefetch_slice_l2(A, sl + tw);
+#endif
       const int i = sl * kSlice + lane;  // matrix position == vector index (position space)
       if (i < rows) {
         double y0, y1, y2;
@@ -1115,49 +1131,58 @@ __global__ void __launch_bounds__(kPersistThreads, WEFT_PERSIST_MINB) k_pcg_pers
     }
     const double alpha = rho / pq[0];
     // ---- phase B: x, r, z (coalesced; q and p of phase A are visible after
-    // the grid sync, read through L2)
+    // the grid sync, read through L2). The x update of every other iteration
+    // is deferred and applied with the next one as (x + a_k p_k) + a_k+1 p_k+1
+    // — the same two roundings in the same order, one x round trip fewer.
+    const bool x_now = !WEFT_PK_XDEFER || x_pending;
     double s2[2] = {0.0, 0.0};
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < rows; i += gridDim.x * blockDim.x) {
-      {
-        double pv[3], qv[3], xv[3], rv[3], m[9];
+      double qv[3], rv[3], m[9];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        qv[c] = __ldcg(q + 3 * i + c);
+        rv[c] = __ldcg(r + 3 * i + c);
+      }
+      if (x_now) {
+        double xv[3], pv[3];
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
           pv[c] = __ldcg(pnew + 3 * i + c);
-          qv[c] = __ldcg(q + 3 * i + c);
           xv[c] = __ldcg(x + 3 * i + c);
-          rv[c] = __ldcg(r + 3 * i + c);
         }
-        if (bj) {
+        if (WEFT_PK_XDEFER) {
 #pragma unroll
-          for (int k = 0; k < 9; ++k) m[k] = __ldg(dinv + 9 * (size_t)i + k);
-        }
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          xv[c] = xv[c] + alpha * pv[c];
-          rv[c] = rv[c] - alpha * qv[c];
-        }
-        double z0, z1, z2;
-        if (bj) {  // apply_precond (solver.hpp:67-89)
-          z0 = ((0.0 + m[0] * rv[0]) + m[1] * rv[1]) + m[2] * rv[2];
-          z1 = ((0.0 + m[3] * rv[0]) + m[4] * rv[1]) + m[5] * rv[2];
-          z2 = ((0.0 + m[6] * rv[0]) + m[7] * rv[1]) + m[8] * rv[2];
-        } else {
-          z0 = rv[0];
-          z1 = rv[1];
-          z2 = rv[2];
+          for (int c = 0; c < 3; ++c) xv[c] = xv[c] + alpha_prev * __ldcg(pcur + 3 * i + c);
         }
 #pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          __stcg(x + 3 * i + c, xv[c]);
-          __stcg(r + 3 * i + c, rv[c]);
-        }
-        __stcg(z + 3 * i, z0);
-        __stcg(z + 3 * i + 1, z1);
-        __stcg(z + 3 * i + 2, z2);
-        s2[0] = s2[0] + ((rv[0] * rv[0] + rv[1] * rv[1]) + rv[2] * rv[2]);
-        s2[1] = s2[1] + ((rv[0] * z0 + rv[1] * z1) + rv[2] * z2);
+        for (int c = 0; c < 3; ++c) __stcg(x + 3 * i + c, xv[c] + alpha * pv[c]);
       }
+      if (bj) {
+#pragma unroll
+        for (int k = 0; k < 9; ++k) m[k] = __ldg(dinv + 9 * (size_t)i + k);
+      }
+#pragma unroll
+      for (int c = 0; c < 3; ++c) rv[c] = rv[c] - alpha * qv[c];
+      double z0, z1, z2;
+      if (bj) {  // apply_precond (solver.hpp:67-89)
+        z0 = ((0.0 + m[0] * rv[0]) + m[1] * rv[1]) + m[2] * rv[2];
+        z1 = ((0.0 + m[3] * rv[0]) + m[4] * rv[1]) + m[5] * rv[2];
+        z2 = ((0.0 + m[6] * rv[0]) + m[7] * rv[1]) + m[8] * rv[2];
+      } else {
+        z0 = rv[0];
+        z1 = rv[1];
+        z2 = rv[2];
+      }
+#pragma unroll
+      for (int c = 0; c < 3; ++c) __stcg(r + 3 * i + c, rv[c]);
+      __stcg(z + 3 * i, z0);
+      __stcg(z + 3 * i + 1, z1);
+      __stcg(z + 3 * i + 2, z2);
+      s2[0] = s2[0] + ((rv[0] * rv[0] + rv[1] * rv[1]) + rv[2] * rv[2]);
+      s2[1] = s2[1] + ((rv[0] * z0 + rv[1] * z1) + rv[2] * z2);
     }
+    x_pending = !x_now;
+    alpha_prev = alpha;
     block_sum<2>(s2, smem);
     if (threadIdx.x == 0) {
       __stcg(g.partials + G + 2 * blockIdx.x, s2[0]);
@@ -1187,6 +1212,13 @@ __global__ void __launch_bounds__(kPersistThreads, WEFT_PERSIST_MINB) k_pcg_pers
     pcur = pnew;
     pnew = tmp;
     first = false;
+  }
+  if (x_pending && status == 0) {
+    // the last iteration's deferred x update (its p is in pnew: the swap
+    // below the residual test is skipped on exit)
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < rows; i += gridDim.x * blockDim.x)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) __stcg(x + 3 * i + c, __ldcg(x + 3 * i + c) + alpha_prev * __ldcg(pnew + 3 * i + c));
   }
   if (lead) {
     st->iter = it;
