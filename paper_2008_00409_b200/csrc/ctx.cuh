@@ -113,6 +113,7 @@ struct Ctx {
   // ---- PCG work
   DBuf<double> r, z, pv, q, xs, dinv, bvec;
   DBuf<double> xp;  // persistent PCG: solution in position space
+  DBuf<unsigned long long> timing;  // dev instrumentation of the persistent PCG
   DBuf<double> partials;
   DBuf<double> hist, phist;
   PcgState* pcg = nullptr;       // device

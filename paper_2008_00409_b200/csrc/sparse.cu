@@ -17,6 +17,8 @@
 // partition order (Engine::all_reduce_sum, proj/src/exec.cpp:170-174).
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 
@@ -778,6 +780,7 @@ struct PcgArgs {
   CommView cv;
   PartMap pm;
   double* p2;  // persistent solve: second search-direction buffer
+  unsigned long long* timing;  // dev instrumentation (WEFT_PCG_TIMING=1): ns per phase, summed
 };
 
 // Iteration kernel 1: q = A p with p = z (+ beta p) formed on the fly;
@@ -1088,11 +1091,16 @@ __global__ void __launch_bounds__(kPersistThreads, WEFT_PERSIST_MINB) k_pcg_pers
   double alpha_prev = 0.0;
   while (!done) {
     // ---- phase A: q = A p, p of the own rows, p.q
+    unsigned long long tm0 = 0;
+    if (g.timing && lead) tm0 = global_ns();
     double s1[1] = {0.0};
     for (int sl = gw; sl < nslices; sl += tw) {
-#if WEFT_PK_PREFETCH
+#if WEFT_PK_PREFETCH == 1
       // stream this warp's next slice into L2 while this one computes
       if (lane == 0 && sl + tw < nslices) prefetch_slice_l2(A, sl + tw);
+#elif WEFT_PK_PREFETCH == 2
+      // request this slice's whole record stream at once (one bulk L2 prefetch)
+      if (lane == 0) prefetch_slice_l2(A, sl);
 #endif
       const int i = sl * kSlice + lane;  // matrix position == vector index (position space)
       if (i < rows) {
@@ -1116,7 +1124,14 @@ __global__ void __launch_bounds__(kPersistThreads, WEFT_PERSIST_MINB) k_pcg_pers
     }
     block_sum<1>(s1, smem);
     if (threadIdx.x == 0) __stcg(g.partials + blockIdx.x, s1[0]);
+    unsigned long long tm1 = 0;
+    if (g.timing && lead) tm1 = global_ns();
     grid.sync();
+    if (g.timing && lead) {
+      const unsigned long long tm2 = global_ns();
+      g.timing[0] += tm1 - tm0;  // phase A (block 0's view)
+      g.timing[1] += tm2 - tm1;  // grid sync 1
+    }
     double pq[1];
     all_blocks_sum<1>(g.partials, G, pq, smem);
     if (!isfinite(pq[0])) {
@@ -1188,7 +1203,14 @@ __global__ void __launch_bounds__(kPersistThreads, WEFT_PERSIST_MINB) k_pcg_pers
       __stcg(g.partials + G + 2 * blockIdx.x, s2[0]);
       __stcg(g.partials + G + 2 * blockIdx.x + 1, s2[1]);
     }
+    unsigned long long tm3 = 0;
+    if (g.timing && lead) tm3 = global_ns();
     grid.sync();
+    if (g.timing && lead) {
+      const unsigned long long tm4 = global_ns();
+      g.timing[2] += tm3 - tm0;  // iteration up to sync 2 (A + sync + reduce + B)
+      g.timing[3] += tm4 - tm3;  // grid sync 2
+    }
     double t[2];
     all_blocks_sum<2>(g.partials + G, G, t, smem);
     ++it;
@@ -1374,6 +1396,11 @@ PcgResult pcg_solve(Ctx& c, const double* b_dev, const weft_pcg_config& cfg, dou
   if (persistent) {
     args.A.cols = c.A.colp.data();  // columns as positions
     args.x = c.xp.data();
+    if (std::getenv("WEFT_PCG_TIMING")) {
+      c.timing.resize(8);
+      c.timing.zero(s);
+      args.timing = c.timing.data();
+    }
   }
   c.pcg_args.resize(sizeof(PcgArgs));
   const PcgArgs* dargs = reinterpret_cast<const PcgArgs*>(c.pcg_args.data());
@@ -1394,6 +1421,13 @@ PcgResult pcg_solve(Ctx& c, const double* b_dev, const weft_pcg_config& cfg, dou
     k_scatter_rows<<<div_up(rows, threads), threads, 0, ls(c)>>>(rows, c.A.perm.data(), c.xp.data(), c.xs.data());
     WG_CUDA(cudaMemcpyAsync(hs, c.pcg, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
     WG_CUDA(cudaStreamSynchronize(s));
+    if (args.timing && hs->iter) {
+      unsigned long long t[4];
+      WG_CUDA(cudaMemcpy(t, args.timing, sizeof(t), cudaMemcpyDeviceToHost));
+      std::fprintf(stderr, "[pcg timing] its %d  phaseA %.1f us  sync1 %.1f us  reduce+phaseB %.1f us  sync2 %.1f us\n",
+                   hs->iter, t[0] * 1e-3 / hs->iter, t[1] * 1e-3 / hs->iter,
+                   (t[2] - t[0] - t[1]) * 1e-3 / hs->iter, t[3] * 1e-3 / hs->iter);
+    }
     if (c.profile) {
       float ms = 0.f;
       WG_CUDA(cudaEventElapsedTime(&ms, c.ev[6], c.ev[7]));
