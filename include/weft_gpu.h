@@ -289,7 +289,8 @@ typedef struct weft_step_report {
   double pcg_residual;
   int64_t dcd_candidates;
   int64_t ccd_candidates;
-  double ms_broad;    /* device time of both broad phases */
+  double ms_broad;    /* device time of both broad phases (the DCD one runs on a
+                         side stream, overlapped with the assembly) */
   double ms_assemble; /* device time of fill_matrix */
   double ms_solve;    /* device time of the PCG */
 } weft_step_report;

@@ -32,8 +32,9 @@
 namespace weft_gpu {
 
 void* scratch(Ctx& c, size_t bytes) {
-  c.scratch.resize(bytes + 256);
-  return c.scratch.data();
+  DBuf<unsigned char>& b = c.cur == c.side ? c.scratch_side : c.scratch;
+  b.resize(bytes + 256);
+  return b.data();
 }
 
 // ---------------------------------------------------------------------------
@@ -793,7 +794,13 @@ struct ElemArgs {
   const double* __restrict__ vel;
 };
 
-__global__ void __launch_bounds__(128) k_elem_eval(ElemArgs g) {
+#ifndef WEFT_EVAL_MINB
+#define WEFT_EVAL_MINB 1
+#endif
+#ifndef WEFT_SLOT_MINB
+#define WEFT_SLOT_MINB 2
+#endif
+__global__ void __launch_bounds__(128, WEFT_EVAL_MINB) k_elem_eval(ElemArgs g) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= g.n) return;
   const int64_t e = g.list ? g.list[i] : i;
@@ -1046,7 +1053,7 @@ __device__ __forceinline__ void add_block(const StagedInc& si, int b, const doub
 // Phase 2: one CTA per slice of 32 rows. The slice's incidences (static then
 // contact, each ascending element per row) are staged in shared memory;
 // warp w computes slots w, w+8, ... of its lane's row.
-__global__ void __launch_bounds__(kSlotWarps * 32, 2) k_fill_slots(SlotArgs g) {
+__global__ void __launch_bounds__(kSlotWarps * 32, WEFT_SLOT_MINB) k_fill_slots(SlotArgs g) {
   __shared__ int4 sm_st[kStageCap];
   __shared__ int sm_ksa[kStageCap], sm_pay[kStageCap], sm_res[kStageCap];
   __shared__ double sm_damp[kStageCap];
@@ -1239,7 +1246,7 @@ static int64_t select_rank_elements(Ctx& c) {
   return h;
 }
 
-void fill_matrix(Ctx& c, const double* xc, const double* xa, const double* vel, double dt, int mode) {
+void fill_matrix(Ctx& c, const double* xc, const double* xa, const double* vel, double dt, int mode, bool finish) {
   if (!(dt > 0.0)) throw Error(WEFT_ERR_DIMENSION, "fill_matrix: dt must be positive");
   if (c.p == 0 && c.n_static == 0) throw Error(WEFT_ERR_INVALID, "fill_matrix: set_vertices/set_elements first");
   if (c.spat_ptr.size() != static_cast<size_t>(c.p) + 1) throw Error(WEFT_ERR_INVALID, "fill_matrix: set_elements first");
@@ -1321,13 +1328,22 @@ void fill_matrix(Ctx& c, const double* xc, const double* xa, const double* vel, 
     }
     WG_CUDA(cudaGetLastError());
   }
-  int hbad = big;
-  WG_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s));
-  WG_CUDA(cudaStreamSynchronize(s));
-  if (hbad != big)
-    throw Error(WEFT_ERR_DIMENSION, "fill_matrix: vertex " + std::to_string(hbad) + " has non-positive mass");
   c.has_matrix = true;
   c.has_rhs = true;
+  if (finish) fill_matrix_finish(c);
+}
+
+void fill_matrix_finish(Ctx& c) {
+  const int big = INT32_MAX;
+  int hbad = big;
+  const int* bad = reinterpret_cast<const int*>(c.scalars.data() + 8);
+  WG_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+  WG_CUDA(cudaStreamSynchronize(c.stream));
+  if (hbad != big) {
+    c.has_matrix = false;
+    c.has_rhs = false;
+    throw Error(WEFT_ERR_DIMENSION, "fill_matrix: vertex " + std::to_string(hbad) + " has non-positive mass");
+  }
 }
 
 }  // namespace weft_gpu

@@ -480,7 +480,7 @@ __global__ void k_pair_counts(int64_t cells, const int64_t* __restrict__ cell_of
 
 void build_grid(Ctx& c, const double* x0, const double* x1, int mode, double thickness, double cell_scale) {
   const int T = c.soup_tris;
-  cudaStream_t s = c.stream;
+  cudaStream_t s = c.cur;
   const bool ccd = mode == WEFT_CONTINUOUS;
   const double inflate = ccd ? 1e-9 : 0.5 * thickness;  // collision.cpp:122
   c.box_lo.resize(3 * static_cast<size_t>(T) + 3);
@@ -698,12 +698,12 @@ __global__ void __launch_bounds__(kWalkWarps * 32) k_cell_walk(WalkArgs w, int64
 // Returns the candidate count of [begin, end); when pairs_out is non-null
 // the pairs are written there (device or host pointer). Device-resident
 // pairs stay in c.cand_pairs.
-int64_t candidates(Ctx& c, int64_t begin, int64_t end, int32_t* pairs_out) {
+int64_t candidates(Ctx& c, int64_t begin, int64_t end, int32_t* pairs_out, bool count_only) {
   if (!c.has_grid) throw Error(WEFT_ERR_INVALID, "candidates: build_grid first");
   begin = std::max<int64_t>(begin, 0);
   end = std::min<int64_t>(end, c.grid_total);
   if (begin >= end) return 0;
-  cudaStream_t s = c.stream;
+  cudaStream_t s = c.cur;
   const int64_t cells = c.grid_cells;
   WalkArgs w{begin, end, cells, c.wprefix.data(), c.cell_off.data(), c.vals_b.data(), c.cell_keys.data(),
              c.lat.data()};
@@ -718,6 +718,7 @@ int64_t candidates(Ctx& c, int64_t begin, int64_t end, int32_t* pairs_out) {
   int64_t n = 0;
   WG_CUDA(cudaMemcpyAsync(&n, c.cand_count.data() + cells, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
   WG_CUDA(cudaStreamSynchronize(s));
+  if (count_only) return n;  // the walk's count pass is the whole result
   c.cand_pairs.resize(2 * static_cast<size_t>(n) + 2);
   k_cell_walk<true><<<blocks, kWalkWarps * 32, 0, ls(c)>>>(w, nullptr, c.cand_count.data(),
                                                            reinterpret_cast<int2*>(c.cand_pairs.data()));

@@ -137,7 +137,10 @@ weft_status weft_gpu_create(const weft_gpu_options* opts, weft_gpu_ctx** out) {
       throw weft_gpu::Error(WEFT_ERR_EXEC, "device " + std::to_string(c.device) + " failed: no such CUDA device");
     WG_CUDA(cudaSetDevice(c.device));
     WG_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+    WG_CUDA(cudaStreamCreateWithFlags(&c.side, cudaStreamNonBlocking));
+    c.cur = c.stream;
     for (auto& e : c.ev) WG_CUDA(cudaEventCreate(&e));
+    for (auto& e : c.ev_side) WG_CUDA(cudaEventCreate(&e));
     c.scalars.resize(64);
     if (const char* e = std::getenv("WEFT_SPMV_PAIR")) c.spmv_pair = std::atoi(e) != 0;
     if (const char* e = std::getenv("WEFT_NO_GRAPHS")) c.use_graphs = std::atoi(e) == 0;
@@ -172,7 +175,10 @@ weft_status weft_gpu_destroy(weft_gpu_ctx* ctx) {
     weft_gpu::pcg_free(c);
     WG_CUDA(cudaStreamSynchronize(c.stream));
     weft_gpu::comm_free(c);
+    WG_CUDA(cudaStreamSynchronize(c.side));
     for (auto& e : c.ev) cudaEventDestroy(e);
+    for (auto& e : c.ev_side) cudaEventDestroy(e);
+    cudaStreamDestroy(c.side);
     cudaStreamDestroy(c.stream);
   });
   delete ctx;

@@ -68,7 +68,13 @@ struct Ctx {
   DBuf<unsigned long long> seq;    // [0] vec, [1] red, [2] state, [3] error
   CommView comm;                   // kernel view (valid once attached)
   cudaStream_t stream = nullptr;
+  // side stream: the DCD broad phase runs on it concurrently with the
+  // assembly (independent work, both latency-bound); `cur` is the stream
+  // library launches currently go to (ls()).
+  cudaStream_t side = nullptr;
+  cudaStream_t cur = nullptr;
   cudaEvent_t ev[8] = {};
+  cudaEvent_t ev_side[4] = {};
 
   // ---- vertices / partitions
   int p = 0;
@@ -150,8 +156,9 @@ struct Ctx {
   DBuf<int32_t> cand_pairs;
   bool has_grid = false;
 
-  // ---- CUB scratch
+  // ---- CUB scratch (one per stream)
   DBuf<unsigned char> scratch;
+  DBuf<unsigned char> scratch_side;
   DBuf<int64_t> scalars;  // small device scratch
 
   // ---- instrumentation
@@ -172,7 +179,7 @@ struct Ctx {
 // Launch-site stream accessor: counts the launch (gpu_launches in bench.py).
 inline cudaStream_t ls(Ctx& c) {
   ++c.launches;
-  return c.stream;
+  return c.cur;
 }
 
 // ---- entry points implemented across the .cu files
@@ -196,11 +203,15 @@ void pcg_free(Ctx& c);
 void set_vertices(Ctx& c, int p, const double* mass, const uint8_t* pinned);
 void set_elements(Ctx& c, int64_t count, const weft_element* elems);
 void set_contacts(Ctx& c, int64_t count, const weft_element* elems);
-void fill_matrix(Ctx& c, const double* xc, const double* xa, const double* vel, double dt, int mode);
+// finish = false leaves the final host check (non-positive mass) to
+// fill_matrix_finish, so other streams can be fed while the kernels run.
+void fill_matrix(Ctx& c, const double* xc, const double* xa, const double* vel, double dt, int mode,
+                 bool finish = true);
+void fill_matrix_finish(Ctx& c);
 
 void set_soup(Ctx& c, int verts, int ntris, const int32_t* tris);
 void build_grid(Ctx& c, const double* x0_dev, const double* x1_dev, int mode, double thickness, double cell_scale);
-int64_t candidates(Ctx& c, int64_t begin, int64_t end, int32_t* pairs_dev_or_null);
+int64_t candidates(Ctx& c, int64_t begin, int64_t end, int32_t* pairs_dev_or_null, bool count_only = false);
 
 void serial_sum(Ctx& c, int n, const double* d_host, double* exact, double* naive, int fast);
 

@@ -3,6 +3,7 @@
 // proj/src/driver.cpp:96-215; narrow phase and impact zones are out of
 // scope for this tier).
 #include <algorithm>
+#include <cstdlib>
 #include <string>
 
 #include "ctx.cuh"
@@ -177,8 +178,6 @@ weft_status weft_gpu_sim_step(weft_gpu_ctx* ctx, const weft_sim_params* prm, wef
     const int64_t n = 3 * static_cast<int64_t>(c.p);
     const double dt = prm->dt;
     cudaEvent_t* ev = c.ev;
-    // 1. proximity broad phase (DCD) on the current configuration
-    WG_CUDA(cudaEventRecord(ev[0], s));
     // the grid is replicated on every rank (collision.cpp:397-399); each
     // rank walks its split_workload share of the pair space (:181-192)
     auto share = [&](int64_t total, int64_t& b, int64_t& e) {
@@ -187,16 +186,39 @@ weft_status weft_gpu_sim_step(weft_gpu_ctx* ctx, const weft_sim_params* prm, wef
       e = b + base + (c.rank < extra ? 1 : 0);
     };
     int64_t wb = 0, we = 0;
-    weft_gpu::build_grid(c, c.sim_x.data(), c.sim_x.data(), WEFT_DISCRETE, prm->thickness, prm->cell_scale);
-    share(c.grid_total, wb, we);
-    const int64_t dcd = weft_gpu::candidates(c, wb, we, nullptr);
-    WG_CUDA(cudaEventRecord(ev[1], s));
-    // 2. assembly of step_system at (x, v)
+    // 1 + 2. The proximity broad phase (DCD) on x and the assembly of
+    // step_system at (x, v) are independent (contacts come from the narrow
+    // phase, out of this tier): the assembly is enqueued on the main stream,
+    // the broad phase runs on the side stream at the same time (both are
+    // latency-bound kernels that leave most of the GPU idle alone).
+    WG_CUDA(cudaEventRecord(ev[0], s));  // state ready
     c.x_adv.resize(static_cast<size_t>(n));
     weft_gpu::k_advance<<<weft_gpu::div_up(n, 256), 256, 0, ls(c)>>>(n, c.sim_x.data(), c.sim_v.data(), dt,
                                                                   c.x_adv.data());
-    weft_gpu::fill_matrix(c, c.sim_x.data(), c.x_adv.data(), c.sim_v.data(), dt, prm->jac_mode);
+    weft_gpu::fill_matrix(c, c.sim_x.data(), c.x_adv.data(), c.sim_v.data(), dt, prm->jac_mode, /*finish=*/false);
     WG_CUDA(cudaEventRecord(ev[2], s));
+    // A/B knob (WEFT_SIM_OVERLAP=1): measured no gain on B200 — the
+    // assembly's grids fill every SM, so the side-stream broad phase only
+    // runs in their gaps — hence serial by default.
+    static const bool serial = std::getenv("WEFT_SIM_OVERLAP") == nullptr;
+    if (serial) weft_gpu::fill_matrix_finish(c);
+    WG_CUDA(cudaStreamWaitEvent(c.side, serial ? ev[2] : ev[0], 0));
+    WG_CUDA(cudaEventRecord(c.ev_side[0], c.side));
+    int64_t dcd = 0;
+    c.cur = c.side;
+    try {
+      weft_gpu::build_grid(c, c.sim_x.data(), c.sim_x.data(), WEFT_DISCRETE, prm->thickness, prm->cell_scale);
+      share(c.grid_total, wb, we);
+      dcd = weft_gpu::candidates(c, wb, we, nullptr, /*count_only=*/true);
+    } catch (...) {
+      c.cur = c.stream;
+      throw;
+    }
+    c.cur = c.stream;
+    WG_CUDA(cudaEventRecord(c.ev_side[1], c.side));
+    weft_gpu::fill_matrix_finish(c);
+    WG_CUDA(cudaStreamWaitEvent(s, c.ev_side[1], 0));  // the cooperative PCG gets the whole GPU
+    WG_CUDA(cudaEventRecord(ev[1], s));
     // 3. PCG for dv
     const weft_gpu::PcgResult pr = weft_gpu::pcg_solve(c, c.rhs.data(), prm->pcg, nullptr, nullptr);
     WG_CUDA(cudaEventRecord(ev[3], s));
@@ -212,16 +234,16 @@ weft_status weft_gpu_sim_step(weft_gpu_ctx* ctx, const weft_sim_params* prm, wef
     // 5. impact broad phase (CCD) over begin -> candidate
     weft_gpu::build_grid(c, c.sim_x.data(), c.sim_xc.data(), WEFT_CONTINUOUS, prm->thickness, prm->cell_scale);
     share(c.grid_total, wb, we);
-    const int64_t ccd = weft_gpu::candidates(c, wb, we, nullptr);
+    const int64_t ccd = weft_gpu::candidates(c, wb, we, nullptr, /*count_only=*/true);
     WG_CUDA(cudaEventRecord(ev[5], s));
     // 7. commit (no zone correction in this tier)
     std::swap(c.sim_x.ptr, c.sim_xc.ptr);
     std::swap(c.sim_x.cap, c.sim_xc.cap);
     WG_CUDA(cudaEventSynchronize(ev[5]));
-    float t01 = 0, t12 = 0, t23 = 0, t45 = 0;
-    cudaEventElapsedTime(&t01, ev[0], ev[1]);
-    cudaEventElapsedTime(&t12, ev[1], ev[2]);
-    cudaEventElapsedTime(&t23, ev[2], ev[3]);
+    float tdcd = 0, tasm = 0, t13 = 0, t45 = 0;
+    cudaEventElapsedTime(&tdcd, c.ev_side[0], c.ev_side[1]);  // overlapped with the assembly
+    cudaEventElapsedTime(&tasm, ev[0], ev[2]);
+    cudaEventElapsedTime(&t13, ev[1], ev[3]);
     cudaEventElapsedTime(&t45, ev[4], ev[5]);
     if (rep) {
       rep->pcg_iterations = pr.iterations;
@@ -229,9 +251,9 @@ weft_status weft_gpu_sim_step(weft_gpu_ctx* ctx, const weft_sim_params* prm, wef
       rep->pcg_residual = pr.rel_residual;
       rep->dcd_candidates = dcd;
       rep->ccd_candidates = ccd;
-      rep->ms_broad = t01 + t45;
-      rep->ms_assemble = t12;
-      rep->ms_solve = t23;
+      rep->ms_broad = tdcd + t45;
+      rep->ms_assemble = tasm;
+      rep->ms_solve = t13;
     }
   });
 }
