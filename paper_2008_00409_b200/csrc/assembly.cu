@@ -1038,15 +1038,66 @@ struct StagedInc {
 // the element's phase-1 state (bitwise the blocks fill_matrix adds).
 __device__ __forceinline__ void add_block(const StagedInc& si, int b, const double* __restrict__ epay,
                                           const double* __restrict__ eres, double dt, double acc[9]) {
+  // acc += (-scale) J_ab (+ dt D_ab), entry by entry with elem_block's exact
+  // expressions but no 3x3 temporaries (register pressure of k_fill_slots)
   const int kind = si.kind_ss_a & 0xff, a = (si.kind_ss_a >> 16) & 0xff;
-  double J[9], D[9];
-  const bool damped = elem_block(kind, eres + si.res, epay + si.pay, a, b, J, D);
+  const double* __restrict__ S = eres + si.res;
+  const double* __restrict__ d = epay + si.pay;
   const double nscale = -(dt * dt + si.damping * dt);
+  switch (kind) {
+    case WEFT_STRETCH: {
+      if (S[15] == 0.0) {
 #pragma unroll
-  for (int q = 0; q < 9; ++q) {
-    double cv = nscale * J[q];
-    if (damped) cv = cv + dt * D[q];
-    acc[q] = acc[q] + cv;
+        for (int q = 0; q < 9; ++q) acc[q] = acc[q] + nscale * 0.0;
+        return;
+      }
+      const V3 wu_hat = v3(S[0], S[1], S[2]), wv_hat = v3(S[3], S[4], S[5]);
+      const V3 wu = v3(S[6], S[7], S[8]), wv = v3(S[9], S[10], S[11]);
+      const double wu_len = S[12], wv_len = S[13];
+      const double ar = d[6];
+      const double ui = d[a], vi = d[3 + a], uj = d[b], vj = d[3 + b];
+      const V3 gui = scl(ar * ui, wu_hat), gvi = scl(ar * vi, wv_hat);
+      const V3 gsi = scl(ar, add(scl(ui, wv), scl(vi, wu)));
+      const V3 guj = scl(ar * uj, wu_hat), gvj = scl(ar * vj, wv_hat);
+      const V3 gsj = scl(ar, add(scl(uj, wv), scl(vj, wu)));
+      const double su2 = (d[7] * S[16]) * (((ar * ui) * uj) / wu_len);
+      const double sv2 = (d[8] * S[17]) * (((ar * vi) * vj) / wv_len);
+      const bool keep_u2 = S[16] >= 0.0, keep_v2 = S[17] >= 0.0;
+#pragma unroll
+      for (int r = 0; r < 3; ++r)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          const double id = r == c ? 1.0 : 0.0;
+          double m = 0.0;
+          m = m - d[7] * (comp(gui, r) * comp(guj, c));
+          m = m - d[8] * (comp(gvi, r) * comp(gvj, c));
+          m = m - d[9] * (comp(gsi, r) * comp(gsj, c));
+          if (keep_u2) m = m - su2 * (id - comp(wu_hat, r) * comp(wu_hat, c));
+          if (keep_v2) m = m - sv2 * (id - comp(wv_hat, r) * comp(wv_hat, c));
+          acc[r * 3 + c] = acc[r * 3 + c] + nscale * (0.0 + m);
+        }
+      return;
+    }
+    case WEFT_BEND: {
+      const double nk = -d[1];
+      const V3 ga = v3(S[3 * a], S[3 * a + 1], S[3 * a + 2]);
+      const V3 gb = v3(S[3 * b], S[3 * b + 1], S[3 * b + 2]);
+#pragma unroll
+      for (int r = 0; r < 3; ++r)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) acc[r * 3 + c] = acc[r * 3 + c] + nscale * (0.0 + nk * (comp(ga, r) * comp(gb, c)));
+      return;
+    }
+    default: {
+      double J[9], D[9];
+      const bool damped = elem_block(kind, S, d, a, b, J, D);
+#pragma unroll
+      for (int q = 0; q < 9; ++q) {
+        double cv = nscale * J[q];
+        if (damped) cv = cv + dt * D[q];
+        acc[q] = acc[q] + cv;
+      }
+    }
   }
 }
 
