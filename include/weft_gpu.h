@@ -267,6 +267,26 @@ weft_status weft_gpu_download_grid(weft_gpu_ctx* ctx, uint64_t* cell_keys, int64
 weft_status weft_gpu_candidates(weft_gpu_ctx* ctx, int64_t begin, int64_t end, int64_t* count,
                                 int32_t* pairs);
 
+/* Narrow phase (collision.cpp:214-309, collision_geom.cpp:35-317). The soup
+ * edge table (CollisionSoup::build, collision.cpp:95-116) is built by
+ * weft_gpu_set_soup; movable flags default to all movable (NULL resets). */
+weft_status weft_gpu_set_soup_movable(weft_gpu_ctx* ctx, const uint8_t* movable);
+
+/* collide (collision.cpp:391-417): build_grid, the candidate walk and the
+ * elementary DCD (vertex-face / edge-edge proximity within `thickness`) or
+ * CCD (coplanarity cubic + bisection, earliest contact) tests of every
+ * candidate pair, merged, sorted and deduplicated by (kind, a, b) like
+ * sync_shared_cells. VertexFace: a = vertex, b = triangle, weights = (1,
+ * bary0..2); EdgeEdge: a < b edge ids, weights = (1-s, s, 1-t, t). The
+ * result stays on the device; *count = number of hits. In a rank group each
+ * rank returns the hits of its split_workload share. */
+weft_status weft_gpu_collide(weft_gpu_ctx* ctx, const double* x_begin, const double* x_end, int32_t mode,
+                             double thickness, double cell_scale, int64_t* count);
+/* The last collide result: kind_ab = 3 int32 per hit (kind 0 = VertexFace,
+ * 1 = EdgeEdge, a, b); vals = 8 doubles per hit (gap or toi, normal xyz,
+ * weights 0..3). Either pointer may be NULL. */
+weft_status weft_gpu_download_contacts(weft_gpu_ctx* ctx, int32_t* kind_ab, double* vals);
+
 /* split_workload (collision.cpp:181-192). */
 weft_status weft_split_workload(int64_t total, int32_t devices, int64_t* begin, int64_t* end);
 

@@ -548,6 +548,53 @@ int64_t ref_grid_candidates(void* h, int64_t begin, int64_t end, int32_t* pairs)
 
 void ref_grid_free(void* h) { delete static_cast<GridHandle*>(h); }
 
+// collide (collision.cpp:391-417) with Engine(devices): broad phase, narrow
+// phase over every device's pair range, sync_shared_cells. Returns the hit
+// count; fills (kind, a, b) triples and (gap | toi, normal, weights) octets
+// for up to `cap` hits. movable: NULL = all movable.
+int64_t ref_collide(int32_t vertex_count, int32_t tri_count, const int32_t* tris, const uint8_t* movable,
+                    const double* x0, const double* x1, int32_t mode, double thickness, double cell_scale,
+                    int32_t devices, int64_t cap, int32_t* kab, double* vals) {
+  try {
+    std::vector<std::array<int, 3>> t(static_cast<std::size_t>(tri_count));
+    for (int i = 0; i < tri_count; ++i) t[static_cast<std::size_t>(i)] = {tris[3 * i], tris[3 * i + 1], tris[3 * i + 2]};
+    std::vector<std::uint8_t> mv(static_cast<std::size_t>(vertex_count), 1);
+    if (movable) mv.assign(movable, movable + vertex_count);
+    const auto soup = CollisionSoup::build(std::move(t), vertex_count, std::move(mv));
+    const auto xb = to_vec3(x0, vertex_count);
+    const auto xe = to_vec3(x1 ? x1 : x0, vertex_count);
+    CollisionParams params;
+    params.thickness = thickness;
+    params.cell_scale = cell_scale;
+    Engine engine(devices);
+    const bool ccd = mode == WEFT_CONTINUOUS;
+    const auto r = collide(engine, soup, xb, xe, ccd ? CollisionMode::Continuous : CollisionMode::Discrete, params);
+    auto emit = [&](const auto& items, auto scalar) -> int64_t {
+      const int64_t n = static_cast<int64_t>(items.size());
+      for (int64_t i = 0; i < std::min(n, cap); ++i) {
+        const auto& h = items[static_cast<std::size_t>(i)];
+        if (kab) {
+          kab[3 * i] = static_cast<int32_t>(h.kind);
+          kab[3 * i + 1] = h.a;
+          kab[3 * i + 2] = h.b;
+        }
+        if (vals) {
+          double* o = vals + 8 * i;
+          o[0] = scalar(h);
+          for (int c = 0; c < 3; ++c) o[1 + c] = h.normal[c];
+          for (int c = 0; c < 4; ++c) o[4 + c] = h.weights[static_cast<std::size_t>(c)];
+        }
+      }
+      return n;
+    };
+    if (ccd) return emit(r.impacts, [](const Impact& h) { return h.toi; });
+    return emit(r.proximities, [](const Proximity& h) { return h.gap; });
+  } catch (const std::exception& e) {
+    set_error(e);
+    return -1;
+  }
+}
+
 // oracle::random_two_cloth_scene (src/oracle/collision_oracle.cpp:110-138).
 // Returns vertex count; fills tris (cap) / x_begin / x_end when non-NULL.
 int32_t ref_two_cloth_scene(uint64_t seed, int32_t max_side, int32_t* tri_count, int32_t* tris, double* x0,

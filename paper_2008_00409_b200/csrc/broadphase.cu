@@ -55,6 +55,7 @@ void set_soup(Ctx& c, int verts, int ntris, const int32_t* tris) {
   c.soup_tris = ntris;
   c.tris.upload(h.data(), h.size(), c.stream);
   WG_CUDA(cudaStreamSynchronize(c.stream));
+  build_soup_edges(c, h);  // CollisionSoup::build's edge table (narrow phase)
   c.has_grid = false;
 }
 

@@ -156,6 +156,15 @@ struct Ctx {
   DBuf<int32_t> cand_pairs;
   bool has_grid = false;
 
+  // ---- narrow phase (narrow.cu)
+  DBuf<int2> soup_edges;          // CollisionSoup::edges (sorted vertex pairs)
+  DBuf<int32_t> soup_tri_edges;   // 3 edge ids per triangle
+  DBuf<uint8_t> soup_movable;     // per soup vertex
+  DBuf<unsigned long long> hit_count, hit_keys, hit_keys_sorted, contact_keys;
+  DBuf<double> hit_vals, contact_vals;  // 8 per hit: gap | toi, normal, weights
+  DBuf<int64_t> hit_idx, hit_idx_sorted, hit_flag;
+  int64_t n_contacts_found = 0, narrow_pairs = 0, narrow_raw_hits = 0;
+
   // ---- CUB scratch (one per stream)
   DBuf<unsigned char> scratch;
   DBuf<unsigned char> scratch_side;
@@ -214,6 +223,13 @@ void build_grid(Ctx& c, const double* x0_dev, const double* x1_dev, int mode, do
 int64_t candidates(Ctx& c, int64_t begin, int64_t end, int32_t* pairs_dev_or_null, bool count_only = false);
 
 void serial_sum(Ctx& c, int n, const double* d_host, double* exact, double* naive, int fast);
+
+// narrow phase (narrow.cu)
+void build_soup_edges(Ctx& c, const std::vector<int32_t>& tris);
+void set_soup_movable(Ctx& c, const uint8_t* movable);
+int64_t narrow_phase(Ctx& c, const double* x0, const double* x1, int mode, double thickness, int64_t begin,
+                     int64_t end);
+void download_contacts(Ctx& c, int32_t* kab, double* vals);
 
 // rank group (comm.cu, sparse.cu)
 void set_rows(Ctx& c, int p);  // partition map + this rank's row window

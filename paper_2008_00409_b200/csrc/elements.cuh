@@ -167,7 +167,7 @@ __device__ __forceinline__ Dual dsqrt(Dual a) {
 
 // dihedral_gradient_t<Dual>: derivative of the gradient along coordinate j.
 // Returns the 12 derivative components (gradient index i = 3*vertex+comp).
-__device__ __noinline__ void dihedral_gradient_dual(const double xs[12], int j, double out[12]) {
+static __device__ __noinline__ void dihedral_gradient_dual(const double xs[12], int j, double out[12]) {
   Dual x[4][3];
 #pragma unroll
   for (int v = 0; v < 4; ++v)
@@ -216,7 +216,7 @@ __device__ __noinline__ void dihedral_gradient_dual(const double xs[12], int j, 
 
 // Exact-mode bend blocks (a, b): -k g_a g_b^T - (k dtheta) H_ab with the
 // symmetrized dual Hessian (elements.cpp:131-159, 244-267).
-__device__ __noinline__ void bend_jac_exact_row(const double* d, V3 x0, V3 x1, V3 x2, V3 x3, int a,
+static __device__ __noinline__ void bend_jac_exact_row(const double* d, V3 x0, V3 x1, V3 x2, V3 x3, int a,
                                                 double (*J)[9]) {
   V3 g[4];
   dihedral_gradient(x0, x1, x2, x3, g);

@@ -1,0 +1,639 @@
+// narrow.cu — the narrow phase: elementary DCD / CCD
+// feature tests on the broad phase's candidate triangle pairs, merged and
+// deduplicated like sync_shared_cells.
+//
+// Reference: narrow_phase_pair (proj/src/collision.cpp:214-309), the
+// elementary tests and the cubic solver (proj/src/collision_geom.cpp:
+// 35-317), sort_dedup / sync_shared_cells (collision.cpp:313-325,380-389),
+// collide (:391-417). Every expression keeps the reference's association
+// (Vec3 algebra of oracle/shim/Eigen/Dense: strict left-to-right 3-term
+// reductions) and the library is built with -fmad=false; the operations are
+// IEEE +, -, *, /, sqrt, so hits are bitwise the reference's.
+//
+// Device pipeline: build_grid -> candidate walk (pairs written) -> one
+// thread per candidate pair runs the 6 vertex-face and 9 edge-edge tests
+// and appends hits (key = kind<<62 | a<<31 | b, 8 doubles) -> CUB radix sort
+// by key -> keep the first of equal keys (duplicates come from different
+// triangle pairs sharing a feature pair and are identical).
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <unordered_map>
+#include <vector>
+
+#include "ctx.cuh"
+#include "elements.cuh"
+
+namespace weft_gpu {
+namespace {
+
+constexpr double kBaryEps = 1e-8;        // collision_geom.cpp:9
+constexpr double kRootClampEps = 1e-12;  // collision_geom.cpp:10
+
+__device__ __forceinline__ double dmin(double a, double b) { return b < a ? b : a; }  // std::min
+__device__ __forceinline__ double dmax(double a, double b) { return a < b ? b : a; }  // std::max
+__device__ __forceinline__ double dclamp(double v, double lo, double hi) {            // std::clamp
+  return v < lo ? lo : (hi < v ? hi : v);
+}
+__device__ __forceinline__ V3 neg(V3 a) { return V3{-a.x, -a.y, -a.z}; }
+__device__ __forceinline__ double sqn(V3 a) { return dot(a, a); }
+__device__ __forceinline__ V3 lerp3(V3 a, V3 b, double t) { return add(a, scl(t, sub(b, a))); }
+__device__ __forceinline__ V3 ldx(const double* __restrict__ x, int v) {
+  return V3{x[3 * v], x[3 * v + 1], x[3 * v + 2]};
+}
+
+// Eigen's unitOrthogonal for 3-vectors, as oracle/shim/Eigen/Dense.
+__device__ __forceinline__ V3 unit_orthogonal(V3 s) {
+  const double prec = 1e-12;
+  if (!(fabs(s.x) <= fabs(s.z) * prec) || !(fabs(s.y) <= fabs(s.z) * prec)) {
+    const double invnm = 1.0 / sqrt(s.x * s.x + s.y * s.y);
+    return V3{-s.y * invnm, s.x * invnm, 0.0};
+  }
+  const double invnm = 1.0 / sqrt(s.y * s.y + s.z * s.z);
+  return V3{0.0, -s.z * invnm, s.y * invnm};
+}
+
+struct Hit {
+  double s;  // gap (DCD) or toi (CCD)
+  V3 n;
+  double w[4];
+};
+
+__device__ __forceinline__ double poly_eval(double c3, double c2, double c1, double c0, double t) {
+  return ((c3 * t + c2) * t + c1) * t + c0;
+}
+
+// bisect_root (collision_geom.cpp:17-31).
+__device__ double bisect_root(double c3, double c2, double c1, double c0, double lo, double hi) {
+  double flo = poly_eval(c3, c2, c1, c0, lo);
+  for (int it = 0; it < 90; ++it) {
+    const double mid = 0.5 * (lo + hi);
+    const double fm = poly_eval(c3, c2, c1, c0, mid);
+    if (fm == 0.0) return mid;
+    if ((flo < 0.0) == (fm < 0.0)) {
+      lo = mid;
+      flo = fm;
+    } else {
+      hi = mid;
+    }
+  }
+  return 0.5 * (lo + hi);
+}
+
+// cubic_roots_in_unit_interval (collision_geom.cpp:35-88). -1 = identically zero.
+__device__ int cubic_roots(double c3, double c2, double c1, double c0, double roots[3]) {
+  const double scale = dmax(dmax(dmax(fabs(c3), fabs(c2)), fabs(c1)), fabs(c0));
+  if (scale == 0.0) return -1;
+  c3 = c3 / scale;
+  c2 = c2 / scale;
+  c1 = c1 / scale;
+  c0 = c0 / scale;
+  double bp[4] = {0.0, 1.0, 0.0, 0.0};
+  int nbp = 2;
+  const double qa = 3.0 * c3, qb = 2.0 * c2, qc = c1;
+  if (fabs(qa) > 1e-14) {
+    const double disc = qb * qb - 4.0 * qa * qc;
+    if (disc > 0.0) {
+      const double sq = sqrt(disc);
+      const double q = -0.5 * (qb + (qb >= 0.0 ? sq : -sq));
+      const double t0 = q / qa, t1 = qc / q;
+      if (t0 > 0.0 && t0 < 1.0) bp[nbp++] = t0;
+      if (t1 > 0.0 && t1 < 1.0) bp[nbp++] = t1;
+    }
+  } else if (fabs(qb) > 1e-14) {
+    const double t = -qc / qb;
+    if (t > 0.0 && t < 1.0) bp[nbp++] = t;
+  }
+  for (int i = 1; i < nbp; ++i)  // std::sort of <= 4 breakpoints
+    for (int j = i; j > 0 && bp[j] < bp[j - 1]; --j) {
+      const double t = bp[j];
+      bp[j] = bp[j - 1];
+      bp[j - 1] = t;
+    }
+  int count = 0;
+  for (int k = 0; k + 1 < nbp; ++k) {
+    const double lo = bp[k], hi = bp[k + 1];
+    if (hi - lo < 1e-15) continue;
+    const double flo = poly_eval(c3, c2, c1, c0, lo);
+    const double fhi = poly_eval(c3, c2, c1, c0, hi);
+    double root = -1.0;
+    if (flo == 0.0) {
+      root = lo;
+    } else if ((flo < 0.0) != (fhi <= 0.0)) {
+      root = bisect_root(c3, c2, c1, c0, lo, hi);
+    } else if (fhi == 0.0 && k + 2 == nbp) {
+      root = hi;
+    }
+    if (root >= -kRootClampEps && root <= 1.0 + kRootClampEps) {
+      root = dmin(1.0, dmax(0.0, root));
+      if (count == 0 || fabs(roots[count - 1] - root) > 1e-14) roots[count++] = root;
+    }
+  }
+  return count;
+}
+
+// dcd_vertex_face (collision_geom.cpp:90-162): closest point on the
+// triangle (Ericson), hit iff the distance is < h.
+__device__ bool dcd_vf(V3 v, V3 a, V3 b, V3 c, double h, Hit& hit) {
+  const V3 ab = sub(b, a), ac = sub(c, a), av = sub(v, a);
+  const double d1 = dot(ab, av), d2 = dot(ac, av);
+  V3 cp;
+  double b0, b1, b2;
+  if (d1 <= 0.0 && d2 <= 0.0) {
+    cp = a;
+    b0 = 1;
+    b1 = 0;
+    b2 = 0;
+  } else {
+    const V3 bv = sub(v, b);
+    const double d3 = dot(ab, bv), d4 = dot(ac, bv);
+    if (d3 >= 0.0 && d4 <= d3) {
+      cp = b;
+      b0 = 0;
+      b1 = 1;
+      b2 = 0;
+    } else {
+      const double vc = d1 * d4 - d3 * d2;
+      if (vc <= 0.0 && d1 >= 0.0 && d3 <= 0.0) {
+        const double w = d1 / (d1 - d3);
+        cp = add(a, scl(w, ab));
+        b0 = 1 - w;
+        b1 = w;
+        b2 = 0;
+      } else {
+        const V3 cv = sub(v, c);
+        const double d5 = dot(ab, cv), d6 = dot(ac, cv);
+        if (d6 >= 0.0 && d5 <= d6) {
+          cp = c;
+          b0 = 0;
+          b1 = 0;
+          b2 = 1;
+        } else {
+          const double vb = d5 * d2 - d1 * d6;
+          if (vb <= 0.0 && d2 >= 0.0 && d6 <= 0.0) {
+            const double w = d2 / (d2 - d6);
+            cp = add(a, scl(w, ac));
+            b0 = 1 - w;
+            b1 = 0;
+            b2 = w;
+          } else {
+            const double va = d3 * d6 - d5 * d4;
+            if (va <= 0.0 && (d4 - d3) >= 0.0 && (d5 - d6) >= 0.0) {
+              const double w = (d4 - d3) / ((d4 - d3) + (d5 - d6));
+              cp = add(b, scl(w, sub(c, b)));
+              b0 = 0;
+              b1 = 1 - w;
+              b2 = w;
+            } else {
+              const double denom = 1.0 / ((va + vb) + vc);
+              const double wb = vb * denom, wc = vc * denom;
+              cp = add(add(a, scl(wb, ab)), scl(wc, ac));
+              b0 = (1.0 - wb) - wc;
+              b1 = wb;
+              b2 = wc;
+            }
+          }
+        }
+      }
+    }
+  }
+  const V3 diff = sub(v, cp);
+  const double dist = norm(diff);
+  if (!(dist < h)) return false;  // dist >= h (NaN never hits either way)
+  hit.s = dist;
+  if (dist > 1e-12) {
+    hit.n = divs(diff, dist);
+  } else {
+    const V3 n = cross(ab, ac);
+    const double len = norm(n);
+    if (len > 1e-16) {
+      hit.n = divs(n, len);
+    } else {
+      const V3 d = sqn(ab) > sqn(ac) ? ab : ac;
+      hit.n = unit_orthogonal(d);
+    }
+  }
+  hit.w[0] = 1.0;
+  hit.w[1] = b0;
+  hit.w[2] = b1;
+  hit.w[3] = b2;
+  return true;
+}
+
+// dcd_edge_edge (collision_geom.cpp:164-213).
+__device__ bool dcd_ee(V3 p1, V3 p2, V3 q1, V3 q2, double h, Hit& hit) {
+  const V3 d1 = sub(p2, p1), d2 = sub(q2, q1), r = sub(p1, q1);
+  const double a = sqn(d1), e = sqn(d2), f = dot(d2, r);
+  double s = 0.0, t = 0.0;
+  if (a <= 1e-18 && e <= 1e-18) {
+  } else if (a <= 1e-18) {
+    t = dclamp(f / e, 0.0, 1.0);
+  } else {
+    const double c = dot(d1, r);
+    if (e <= 1e-18) {
+      s = dclamp(-c / a, 0.0, 1.0);
+    } else {
+      const double b = dot(d1, d2);
+      const double denom = a * e - b * b;
+      s = denom > 1e-18 ? dclamp((b * f - c * e) / denom, 0.0, 1.0) : 0.0;
+      t = (b * s + f) / e;
+      if (t < 0.0) {
+        t = 0.0;
+        s = dclamp(-c / a, 0.0, 1.0);
+      } else if (t > 1.0) {
+        t = 1.0;
+        s = dclamp((b - c) / a, 0.0, 1.0);
+      }
+    }
+  }
+  const V3 cp = add(p1, scl(s, d1));
+  const V3 cq = add(q1, scl(t, d2));
+  const V3 diff = sub(cp, cq);
+  const double dist = norm(diff);
+  if (!(dist < h)) return false;
+  hit.s = dist;
+  if (dist > 1e-12) {
+    hit.n = divs(diff, dist);
+  } else {
+    const V3 n = cross(d1, d2);
+    const double len = norm(n);
+    if (len > 1e-16) {
+      hit.n = divs(n, len);
+    } else {
+      const V3 d = sqn(d1) > sqn(d2) ? d1 : d2;
+      hit.n = sqn(d) > 1e-18 ? unit_orthogonal(d) : V3{1, 0, 0};
+    }
+  }
+  hit.w[0] = 1.0 - s;
+  hit.w[1] = s;
+  hit.w[2] = 1.0 - t;
+  hit.w[3] = t;
+  return true;
+}
+
+// triple_product_cubic (collision_geom.cpp:219-227).
+__device__ __forceinline__ void triple_cubic(V3 u0, V3 du, V3 v0, V3 dv, V3 w0, V3 dw, double& c3, double& c2,
+                                             double& c1, double& c0) {
+  c0 = dot(cross(u0, v0), w0);
+  c1 = (dot(cross(du, v0), w0) + dot(cross(u0, dv), w0)) + dot(cross(u0, v0), dw);
+  c2 = (dot(cross(du, dv), w0) + dot(cross(du, v0), dw)) + dot(cross(u0, dv), dw);
+  c3 = dot(cross(du, dv), dw);
+}
+
+// ccd_vertex_face (collision_geom.cpp:231-272).
+__device__ bool ccd_vf(V3 v0, V3 v1, V3 a0, V3 a1, V3 b0, V3 b1, V3 c0v, V3 c1v, Hit& out) {
+  const V3 u0 = sub(b0, a0), du = sub(sub(b1, a1), u0);
+  const V3 w0 = sub(c0v, a0), dw = sub(sub(c1v, a1), w0);
+  const V3 q0 = sub(v0, a0), dq = sub(sub(v1, a1), q0);
+  double c3, c2, c1, c0;
+  triple_cubic(u0, du, w0, dw, q0, dq, c3, c2, c1, c0);
+  double roots[3];
+  int count = cubic_roots(c3, c2, c1, c0, roots);
+  if (count < 0) {
+    roots[0] = 0.0;
+    roots[1] = 0.5;
+    roots[2] = 1.0;
+    count = 3;
+  }
+  for (int k = 0; k < count; ++k) {
+    const double t = roots[k];
+    const V3 v = lerp3(v0, v1, t), a = lerp3(a0, a1, t), b = lerp3(b0, b1, t), c = lerp3(c0v, c1v, t);
+    Hit hit;
+    if (!dcd_vf(v, a, b, c, 1e100, hit)) continue;
+    const double scale = dmax(dmax(norm(sub(b, a)), norm(sub(c, a))), 1e-12);
+    if (hit.s > 1e-9 * scale) continue;
+    V3 n = cross(sub(b, a), sub(c, a));
+    const double len = norm(n);
+    n = len > 1e-16 ? divs(n, len) : hit.n;
+    const V3 cp0 = add(add(scl(hit.w[1], a0), scl(hit.w[2], b0)), scl(hit.w[3], c0v));
+    if (dot(n, sub(v0, cp0)) < 0.0) n = neg(n);
+    out.s = t;
+    out.n = n;
+    for (int q = 0; q < 4; ++q) out.w[q] = hit.w[q];
+    return true;
+  }
+  return false;
+}
+
+// ccd_edge_edge (collision_geom.cpp:274-317).
+__device__ bool ccd_ee(V3 p10, V3 p11, V3 p20, V3 p21, V3 q10, V3 q11, V3 q20, V3 q21, Hit& out) {
+  const V3 u0 = sub(p20, p10), du = sub(sub(p21, p11), u0);
+  const V3 v0 = sub(q20, q10), dv = sub(sub(q21, q11), v0);
+  const V3 w0 = sub(q10, p10), dw = sub(sub(q11, p11), w0);
+  double c3, c2, c1, c0;
+  triple_cubic(u0, du, v0, dv, w0, dw, c3, c2, c1, c0);
+  double roots[3];
+  int count = cubic_roots(c3, c2, c1, c0, roots);
+  if (count < 0) {
+    roots[0] = 0.0;
+    roots[1] = 0.5;
+    roots[2] = 1.0;
+    count = 3;
+  }
+  for (int k = 0; k < count; ++k) {
+    const double t = roots[k];
+    const V3 p1 = lerp3(p10, p11, t), p2 = lerp3(p20, p21, t);
+    const V3 q1 = lerp3(q10, q11, t), q2 = lerp3(q20, q21, t);
+    Hit hit;
+    if (!dcd_ee(p1, p2, q1, q2, 1e100, hit)) continue;
+    const double scale = dmax(dmax(norm(sub(p2, p1)), norm(sub(q2, q1))), 1e-12);
+    if (hit.s > 1e-9 * scale) continue;
+    const double s = hit.w[1], u = hit.w[3];
+    if (s < -kBaryEps || s > 1.0 + kBaryEps || u < -kBaryEps || u > 1.0 + kBaryEps) continue;
+    V3 n = cross(sub(p2, p1), sub(q2, q1));
+    const double len = norm(n);
+    if (len < 1e-16) n = hit.n;
+    else n = divs(n, len);
+    const V3 cp0 = add(scl(1.0 - s, p10), scl(s, p20));
+    const V3 cq0 = add(scl(1.0 - u, q10), scl(u, q20));
+    if (dot(n, sub(cp0, cq0)) < 0.0) n = neg(n);
+    out.s = t;
+    out.n = n;
+    for (int q = 0; q < 4; ++q) out.w[q] = hit.w[q];
+    return true;
+  }
+  return false;
+}
+
+struct NarrowArgs {
+  int64_t npairs;
+  const int2* __restrict__ pairs;
+  const int32_t* __restrict__ tris;       // 3 per triangle
+  const int32_t* __restrict__ tri_edges;  // 3 per triangle
+  const int2* __restrict__ edges;
+  const uint8_t* __restrict__ movable;
+  const double* __restrict__ x0;
+  const double* __restrict__ x1;
+  bool ccd;
+  double thickness;
+  unsigned long long* __restrict__ keys;  // kind << 62 | a << 31 | b
+  double* __restrict__ vals;              // 8 per hit
+  unsigned long long* __restrict__ count;
+  unsigned long long cap;
+};
+
+__device__ __forceinline__ void emit(const NarrowArgs& g, int kind, int a, int b, const Hit& h) {
+  const unsigned long long slot = atomicAdd(g.count, 1ull);
+  if (slot >= g.cap) return;  // host re-runs with the exact capacity
+  g.keys[slot] = (static_cast<unsigned long long>(kind) << 62) | (static_cast<unsigned long long>(a) << 31) |
+                 static_cast<unsigned long long>(b);
+  double* o = g.vals + 8 * slot;
+  o[0] = h.s;
+  o[1] = h.n.x;
+  o[2] = h.n.y;
+  o[3] = h.n.z;
+  o[4] = h.w[0];
+  o[5] = h.w[1];
+  o[6] = h.w[2];
+  o[7] = h.w[3];
+}
+
+// feature_apart (collision.cpp:226-254): box separation beyond the margin on
+// some axis, over begin (and, for CCD, end) positions.
+template <int NA, int NB>
+__device__ __forceinline__ bool feature_apart(const NarrowArgs& g, const int (&fa)[NA], const int (&fb)[NB],
+                                              double margin) {
+  for (int axis = 0; axis < 3; ++axis) {
+    double lo_a = 1e300, hi_a = -1e300, lo_b = 1e300, hi_b = -1e300;
+#pragma unroll
+    for (int k = 0; k < NA; ++k) {
+      const double p0 = g.x0[3 * fa[k] + axis];
+      lo_a = dmin(lo_a, p0);
+      hi_a = dmax(hi_a, p0);
+      if (g.ccd) {
+        const double p1 = g.x1[3 * fa[k] + axis];
+        lo_a = dmin(lo_a, p1);
+        hi_a = dmax(hi_a, p1);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < NB; ++k) {
+      const double p0 = g.x0[3 * fb[k] + axis];
+      lo_b = dmin(lo_b, p0);
+      hi_b = dmax(hi_b, p0);
+      if (g.ccd) {
+        const double p1 = g.x1[3 * fb[k] + axis];
+        lo_b = dmin(lo_b, p1);
+        hi_b = dmax(hi_b, p1);
+      }
+    }
+    if (lo_a > hi_b + margin || lo_b > hi_a + margin) return true;
+  }
+  return false;
+}
+
+// narrow_phase_pair (collision.cpp:214-309), one thread per candidate pair.
+__global__ void __launch_bounds__(128) k_narrow(NarrowArgs g) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= g.npairs) return;
+  const int2 pr = g.pairs[i];
+  const int t1 = pr.x, t2 = pr.y;
+  const int tri1[3] = {g.tris[3 * t1], g.tris[3 * t1 + 1], g.tris[3 * t1 + 2]};
+  const int tri2[3] = {g.tris[3 * t2], g.tris[3 * t2 + 1], g.tris[3 * t2 + 2]};
+  const double margin = g.ccd ? 1e-9 : g.thickness;
+  // vertex-face, both directions; shared vertices are exempt
+  for (int dir = 0; dir < 2; ++dir) {
+    const int* vt = dir == 0 ? tri1 : tri2;
+    const int* ft = dir == 0 ? tri2 : tri1;
+    const int face_id = dir == 0 ? t2 : t1;
+    for (int k = 0; k < 3; ++k) {
+      const int v = vt[k];
+      if (ft[0] == v || ft[1] == v || ft[2] == v) continue;
+      if (!g.movable[v] && !g.movable[ft[0]] && !g.movable[ft[1]] && !g.movable[ft[2]]) continue;
+      const int fa[1] = {v};
+      const int fb[3] = {ft[0], ft[1], ft[2]};
+      if (feature_apart(g, fa, fb, margin)) continue;
+      Hit h;
+      bool hit;
+      if (!g.ccd) {
+        hit = dcd_vf(ldx(g.x0, v), ldx(g.x0, ft[0]), ldx(g.x0, ft[1]), ldx(g.x0, ft[2]), g.thickness, h);
+      } else {
+        hit = ccd_vf(ldx(g.x0, v), ldx(g.x1, v), ldx(g.x0, ft[0]), ldx(g.x1, ft[0]), ldx(g.x0, ft[1]),
+                     ldx(g.x1, ft[1]), ldx(g.x0, ft[2]), ldx(g.x1, ft[2]), h);
+      }
+      if (hit) emit(g, 0, v, face_id, h);
+    }
+  }
+  // edge-edge in canonical (min id, max id) orientation
+  for (int ka = 0; ka < 3; ++ka) {
+    const int ea = g.tri_edges[3 * t1 + ka];
+    for (int kb = 0; kb < 3; ++kb) {
+      const int eb = g.tri_edges[3 * t2 + kb];
+      if (ea == eb) continue;
+      const int lo = ea < eb ? ea : eb, hi = ea < eb ? eb : ea;
+      const int2 e1 = g.edges[lo], e2 = g.edges[hi];
+      if (e1.x == e2.x || e1.x == e2.y || e1.y == e2.x || e1.y == e2.y) continue;
+      if (!g.movable[e1.x] && !g.movable[e1.y] && !g.movable[e2.x] && !g.movable[e2.y]) continue;
+      const int fa[2] = {e1.x, e1.y};
+      const int fb[2] = {e2.x, e2.y};
+      if (feature_apart(g, fa, fb, margin)) continue;
+      Hit h;
+      bool hit;
+      if (!g.ccd) {
+        hit = dcd_ee(ldx(g.x0, e1.x), ldx(g.x0, e1.y), ldx(g.x0, e2.x), ldx(g.x0, e2.y), g.thickness, h);
+      } else {
+        hit = ccd_ee(ldx(g.x0, e1.x), ldx(g.x1, e1.x), ldx(g.x0, e1.y), ldx(g.x1, e1.y), ldx(g.x0, e2.x),
+                     ldx(g.x1, e2.x), ldx(g.x0, e2.y), ldx(g.x1, e2.y), h);
+      }
+      if (hit) emit(g, 1, lo, hi, h);
+    }
+  }
+}
+
+__global__ void k_iota(int64_t n, int64_t* __restrict__ v) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) v[i] = i;
+}
+
+// sort_dedup (collision.cpp:313-325): keep the first of each run of equal keys.
+__global__ void k_unique_flags(int64_t n, const unsigned long long* __restrict__ keys, int64_t* __restrict__ flag) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) flag[i] = (i == 0 || keys[i] != keys[i - 1]) ? 1 : 0;
+}
+
+__global__ void k_compact_hits(int64_t n, const unsigned long long* __restrict__ keys,
+                               const int64_t* __restrict__ idx, const int64_t* __restrict__ pos,
+                               const double* __restrict__ vals, unsigned long long* __restrict__ out_keys,
+                               double* __restrict__ out_vals) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (!(i == 0 || keys[i] != keys[i - 1])) return;
+  const int64_t o = pos[i];
+  out_keys[o] = keys[i];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) out_vals[8 * o + q] = vals[8 * idx[i] + q];
+}
+
+}  // namespace
+
+// CollisionSoup::build (collision.cpp:95-116): unique sorted edges with ids in
+// order of first appearance (triangle order, k = 0, 1, 2), per-triangle edge
+// ids. Host, once per soup.
+void build_soup_edges(Ctx& c, const std::vector<int32_t>& tris) {
+  const size_t T = tris.size() / 3;
+  std::unordered_map<uint64_t, int32_t> ids;
+  ids.reserve(3 * T);
+  std::vector<int2> edges;
+  std::vector<int32_t> te(3 * T);
+  for (size_t t = 0; t < T; ++t)
+    for (int k = 0; k < 3; ++k) {
+      int a = tris[3 * t + k], b = tris[3 * t + (k + 1) % 3];
+      if (a > b) std::swap(a, b);
+      const uint64_t key = (static_cast<uint64_t>(static_cast<uint32_t>(a)) << 32) | static_cast<uint32_t>(b);
+      auto it = ids.find(key);
+      if (it == ids.end()) {
+        it = ids.emplace(key, static_cast<int32_t>(edges.size())).first;
+        edges.push_back(make_int2(a, b));
+      }
+      te[3 * t + k] = it->second;
+    }
+  c.soup_edges.upload(edges.data(), edges.size(), c.stream);
+  c.soup_tri_edges.upload(te.data(), te.size(), c.stream);
+  std::vector<uint8_t> mv(static_cast<size_t>(c.soup_verts), 1);
+  c.soup_movable.upload(mv.data(), mv.size(), c.stream);
+  WG_CUDA(cudaStreamSynchronize(c.stream));
+}
+
+void set_soup_movable(Ctx& c, const uint8_t* movable) {
+  std::vector<uint8_t> mv(static_cast<size_t>(c.soup_verts), 1);
+  if (movable && c.soup_verts)
+    WG_CUDA(cudaMemcpy(mv.data(), movable, mv.size(), cudaMemcpyDefault));
+  for (auto& m : mv) m = m ? 1 : 0;
+  c.soup_movable.upload(mv.data(), mv.size(), c.stream);
+  WG_CUDA(cudaStreamSynchronize(c.stream));
+}
+
+// collide (collision.cpp:391-417) for this rank's pair range on the current
+// grid: narrow phase of every candidate pair, sorted and deduplicated.
+int64_t narrow_phase(Ctx& c, const double* x0, const double* x1, int mode, double thickness, int64_t begin,
+                     int64_t end) {
+  cudaStream_t s = c.stream;
+  const int64_t npairs = candidates(c, begin, end, nullptr, /*count_only=*/false);
+  const bool ccd = mode == WEFT_CONTINUOUS;
+  NarrowArgs g{npairs,
+               reinterpret_cast<const int2*>(c.cand_pairs.data()),
+               c.tris.data(),
+               c.soup_tri_edges.data(),
+               c.soup_edges.data(),
+               c.soup_movable.data(),
+               x0,
+               ccd ? x1 : x0,
+               ccd,
+               thickness,
+               nullptr,
+               nullptr,
+               nullptr,
+               0};
+  c.hit_count.resize(1);
+  unsigned long long nh = 0;
+  if (npairs) {
+    size_t cap = std::max<size_t>(c.hit_keys.cap, static_cast<size_t>(1) << 20);
+    for (int attempt = 0; attempt < 2; ++attempt) {
+      c.hit_keys.resize(cap);
+      c.hit_vals.resize(8 * cap);
+      g.keys = c.hit_keys.data();
+      g.vals = c.hit_vals.data();
+      g.count = c.hit_count.data();
+      g.cap = cap;
+      WG_CUDA(cudaMemsetAsync(c.hit_count.data(), 0, sizeof(unsigned long long), s));
+      k_narrow<<<div_up(npairs, 128), 128, 0, ls(c)>>>(g);
+      WG_CUDA(cudaGetLastError());
+      WG_CUDA(cudaMemcpyAsync(&nh, c.hit_count.data(), sizeof(nh), cudaMemcpyDeviceToHost, s));
+      WG_CUDA(cudaStreamSynchronize(s));
+      if (nh <= cap) break;
+      cap = static_cast<size_t>(nh);  // exact capacity, run once more
+    }
+  }
+  const int64_t n = static_cast<int64_t>(nh);
+  c.hit_keys_sorted.resize(static_cast<size_t>(n) + 1);
+  c.hit_idx.resize(static_cast<size_t>(n) + 1);
+  c.hit_idx_sorted.resize(static_cast<size_t>(n) + 1);
+  c.hit_flag.resize(static_cast<size_t>(n) + 1);
+  int64_t nu = 0;
+  if (n) {
+    k_iota<<<div_up(n, 256), 256, 0, ls(c)>>>(n, c.hit_idx.data());
+    size_t tmp = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tmp, c.hit_keys.data(), c.hit_keys_sorted.data(), c.hit_idx.data(),
+                                    c.hit_idx_sorted.data(), n, 0, 63, s);
+    size_t tmp2 = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tmp2, c.hit_flag.data(), c.hit_flag.data(), n + 1, s);
+    void* t = scratch(c, std::max(tmp, tmp2));
+    WG_CUDA(cub::DeviceRadixSort::SortPairs(t, tmp, c.hit_keys.data(), c.hit_keys_sorted.data(), c.hit_idx.data(),
+                                            c.hit_idx_sorted.data(), n, 0, 63, s));
+    k_unique_flags<<<div_up(n, 256), 256, 0, ls(c)>>>(n, c.hit_keys_sorted.data(), c.hit_flag.data());
+    WG_CUDA(cudaMemsetAsync(c.hit_flag.data() + n, 0, sizeof(int64_t), s));
+    WG_CUDA(cub::DeviceScan::ExclusiveSum(t, tmp2, c.hit_flag.data(), c.hit_flag.data(), n + 1, s));
+    WG_CUDA(cudaMemcpyAsync(&nu, c.hit_flag.data() + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    WG_CUDA(cudaStreamSynchronize(s));
+    c.contact_keys.resize(static_cast<size_t>(nu) + 1);
+    c.contact_vals.resize(8 * static_cast<size_t>(nu) + 8);
+    k_compact_hits<<<div_up(n, 256), 256, 0, ls(c)>>>(n, c.hit_keys_sorted.data(), c.hit_idx_sorted.data(),
+                                                      c.hit_flag.data(), c.hit_vals.data(), c.contact_keys.data(),
+                                                      c.contact_vals.data());
+    WG_CUDA(cudaGetLastError());
+    WG_CUDA(cudaStreamSynchronize(s));
+  }
+  c.n_contacts_found = nu;
+  c.narrow_pairs = npairs;
+  c.narrow_raw_hits = n;
+  return nu;
+}
+
+void download_contacts(Ctx& c, int32_t* kab, double* vals) {
+  const int64_t n = c.n_contacts_found;
+  if (n <= 0) return;
+  cudaStream_t s = c.stream;
+  std::vector<unsigned long long> keys(static_cast<size_t>(n));
+  WG_CUDA(cudaMemcpyAsync(keys.data(), c.contact_keys.data(), 8 * n, cudaMemcpyDeviceToHost, s));
+  if (vals) WG_CUDA(cudaMemcpyAsync(vals, c.contact_vals.data(), 64 * n, cudaMemcpyDefault, s));
+  WG_CUDA(cudaStreamSynchronize(s));
+  if (kab)
+    for (int64_t i = 0; i < n; ++i) {
+      const unsigned long long k = keys[static_cast<size_t>(i)];
+      kab[3 * i] = static_cast<int32_t>(k >> 62);
+      kab[3 * i + 1] = static_cast<int32_t>((k >> 31) & 0x7FFFFFFFull);
+      kab[3 * i + 2] = static_cast<int32_t>(k & 0x7FFFFFFFull);
+    }
+}
+
+}  // namespace weft_gpu

@@ -117,6 +117,36 @@ weft_status weft_gpu_build_grid(weft_gpu_ctx* ctx, const double* x_begin, const 
   });
 }
 
+weft_status weft_gpu_set_soup_movable(weft_gpu_ctx* ctx, const uint8_t* movable) {
+  return guard2(ctx, [&](Ctx& c) { weft_gpu::set_soup_movable(c, movable); });
+}
+
+weft_status weft_gpu_collide(weft_gpu_ctx* ctx, const double* x_begin, const double* x_end, int32_t mode,
+                             double thickness, double cell_scale, int64_t* count) {
+  return guard2(ctx, [&](Ctx& c) {
+    const size_t n = 3 * static_cast<size_t>(c.soup_verts);
+    if (!x_begin) throw Error(WEFT_ERR_INVALID, "collide: x_begin is NULL");
+    weft_gpu::upload_vec(c, c.x_cur, x_begin, n);
+    const bool ccd = mode == WEFT_CONTINUOUS;
+    if (ccd) {
+      if (!x_end) throw Error(WEFT_ERR_INVALID, "collide: continuous mode needs x_end");
+      weft_gpu::upload_vec(c, c.x_adv, x_end, n);
+    }
+    const double* x1 = ccd ? c.x_adv.data() : c.x_cur.data();
+    weft_gpu::build_grid(c, c.x_cur.data(), x1, mode, thickness, cell_scale);
+    // a rank of a group walks its split_workload share (collision.cpp:402)
+    const int64_t total = c.grid_total, base = total / c.world, extra = total % c.world;
+    const int64_t b = c.rank * base + std::min<int64_t>(c.rank, extra);
+    const int64_t e = b + base + (c.rank < extra ? 1 : 0);
+    const int64_t nh = weft_gpu::narrow_phase(c, c.x_cur.data(), x1, mode, thickness, b, e);
+    if (count) *count = nh;
+  });
+}
+
+weft_status weft_gpu_download_contacts(weft_gpu_ctx* ctx, int32_t* kind_ab, double* vals) {
+  return guard2(ctx, [&](Ctx& c) { weft_gpu::download_contacts(c, kind_ab, vals); });
+}
+
 weft_status weft_gpu_grid_info(weft_gpu_ctx* ctx, weft_grid_info* info) {
   return guard2(ctx, [&](Ctx& c) {
     if (!c.has_grid) throw Error(WEFT_ERR_INVALID, "grid_info: build_grid first");

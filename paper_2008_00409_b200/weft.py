@@ -411,6 +411,26 @@ class Engine:
         _check(LIB.weft_gpu_candidates(self._ctx, C.c_int64(begin), C.c_int64(end), C.byref(n), _ptr(pairs)))
         return pairs[: 2 * n.value].reshape(-1, 2)
 
+    # -- narrow phase ----------------------------------------
+    def set_soup_movable(self, movable=None):
+        m = None if movable is None else np.ascontiguousarray(movable, np.uint8)
+        _check(LIB.weft_gpu_set_soup_movable(self._ctx, _ptr(m)))
+
+    def collide(self, x_begin, x_end=None, mode: int = DISCRETE, thickness: float = 0.005, cell_scale: float = 1.5):
+        """collide (collision.cpp:391-417): broad + narrow phase, sorted and
+        deduplicated by (kind, a, b). Returns (kab (n, 3) int32: kind 0 =
+        VertexFace / 1 = EdgeEdge, a, b; vals (n, 8): gap|toi, normal xyz,
+        weights 0..3)."""
+        xb = _f64(x_begin)
+        xe = None if x_end is None else _f64(x_end)
+        n = C.c_int64()
+        _check(LIB.weft_gpu_collide(self._ctx, _ptr(xb), _ptr(xe), C.c_int32(mode), C.c_double(thickness),
+                                    C.c_double(cell_scale), C.byref(n)))
+        kab = np.zeros((max(n.value, 1), 3), np.int32)
+        vals = np.zeros((max(n.value, 1), 8))
+        _check(LIB.weft_gpu_download_contacts(self._ctx, _ptr(kab), _ptr(vals)))
+        return kab[: n.value], vals[: n.value]
+
     # -- device-resident step -----------------------------------------------
     def sim_set_state(self, x, v):
         _check(LIB.weft_gpu_sim_set_state(self._ctx, _ptr(_f64(x) if isinstance(x, np.ndarray) else x),

@@ -44,6 +44,28 @@ def main():
             out[f"{tag}_pairs"] = REF.candidates(g)
             REF.free_grid(g)
         np.savez_compressed(os.path.join(HERE, f"grid_{k}.npz"), **out)
+    # narrow phase: collide (collision.cpp:391-417) on random_two_cloth_scene
+    # (DCD at two thicknesses, CCD) and on a pinned layered cloth.
+    k = 0
+    for seed, mode, th in [(41, DISCRETE, 0.05), (43, DISCRETE, 0.2), (41, CONTINUOUS, 0.01), (43, CONTINUOUS, 0.01)]:
+        nv, tris, x0, x1 = REF.two_cloth_scene(seed, 8)
+        kab, vals = REF.collide(nv, tris, x0, x1, mode, th)
+        np.savez_compressed(os.path.join(HERE, f"narrow_{k}.npz"), nv=np.array(nv), tris=tris, x0=x0, x1=x1,
+                            mode=np.array(mode), thickness=np.array(th), movable=np.ones(nv, np.uint8), kab=kab,
+                            vals=vals)
+        k += 1
+    sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+    from paper_2008_00409_b200 import scenes
+    sc = scenes.layered_cloth(2, 10, seed=8)
+    x0 = sc.verts.reshape(-1)
+    x1 = x0 + np.random.default_rng(4).uniform(-0.6, 0.6, x0.shape) * sc.spacing
+    mv = (1 - sc.pinned).astype(np.uint8)
+    for mode in (DISCRETE, CONTINUOUS):
+        kab, vals = REF.collide(len(sc.verts), sc.tris, x0, x1, mode, 2 * sc.thickness, movable=mv)
+        np.savez_compressed(os.path.join(HERE, f"narrow_{k}.npz"), nv=np.array(len(sc.verts)), tris=sc.tris, x0=x0,
+                            x1=x1, mode=np.array(mode), thickness=np.array(2 * sc.thickness), movable=mv, kab=kab,
+                            vals=vals)
+        k += 1
     # SpMV: oracle::random_bell (sparse_oracle.cpp:7-23), pipelined at n = 1, 2, 4.
     for k, (seed, rows) in enumerate([(5, 7), (6, 40)]):
         s = REF.random_bell(seed, rows, 3)

@@ -239,6 +239,7 @@ class Ref:
         L.ref_last_error.restype = C.c_char_p
         L.ref_build_elements.restype = C.c_int64
         L.ref_grid_candidates.restype = C.c_int64
+        L.ref_collide.restype = C.c_int64
         L.ref_spmv.restype = C.c_int32
         L.ref_pcg.restype = C.c_int32
         L.ref_two_cloth_scene.restype = C.c_int32
@@ -385,6 +386,24 @@ class Ref:
 
     def free_grid(self, g: Grid):
         self.lib.ref_grid_free(C.c_void_p(g._handle))
+
+    def collide(self, vertex_count, tris, x0, x1=None, mode=DISCRETE, thickness=0.005, cell_scale=1.5, devices=2,
+                movable=None):
+        """collide (collision.cpp:391-417) -> (kab (n, 3) int32: kind, a, b; vals (n, 8): gap|toi,
+        normal xyz, weights 0..3), sorted and deduplicated by (kind, a, b)."""
+        tris = np.ascontiguousarray(tris, np.int32)
+        x0 = np.ascontiguousarray(x0, np.float64)
+        x1 = None if x1 is None else np.ascontiguousarray(x1, np.float64)
+        mv = None if movable is None else np.ascontiguousarray(movable, np.uint8)
+        args = (C.c_int32(vertex_count), C.c_int32(len(tris)), ptr(tris), ptr(mv), ptr(x0), ptr(x1), C.c_int32(mode),
+                C.c_double(thickness), C.c_double(cell_scale), C.c_int32(devices))
+        n = self.lib.ref_collide(*args, C.c_int64(0), None, None)
+        if n < 0:
+            raise RuntimeError(self.lib.ref_last_error().decode())
+        kab = np.zeros((max(n, 1), 3), np.int32)
+        vals = np.zeros((max(n, 1), 8))
+        self.lib.ref_collide(*args, C.c_int64(n), ptr(kab), ptr(vals))
+        return kab[:n], vals[:n]
 
     def two_cloth_scene(self, seed, max_side):
         tc = C.c_int32()
