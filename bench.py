@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--settle", type=int, default=2, help="steps from rest that define the replayed state S")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-narrow", action="store_true", help="skip the narrow-phase timing")
     ap.add_argument("--ref-budget-s", type=float, default=150.0, help="wall budget of the reference arm")
     return ap.parse_args()
 
@@ -322,6 +323,31 @@ def gpu_arm(args, rank, world, local):
         e2e = {"value": args.steps / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": world * 2 * 8 * 3 * p,
                "d2h_bytes_per_step": world * 2 * 8 * 3 * p}
 
+    # narrow phase (not part of the hot-path step): collide()
+    # = broad phase + elementary DCD / CCD tests + dedup on the replayed state
+    narrow = None
+    if world == 1 and not args.no_narrow:
+        eng.set_soup_movable(1 - sc.pinned)
+        xe = xs + sc.dt * vs
+        narrow = {}
+        for name, mode, x1 in (("dcd", weft.DISCRETE, None), ("ccd", weft.CONTINUOUS, xe)):
+            eng.collide(xs, x1, mode, sc.thickness)  # warm-up (buffers)
+            times = []
+            for _ in range(3):
+                n0 = torch.cuda.Event(enable_timing=True)
+                n1 = torch.cuda.Event(enable_timing=True)
+                n0.record(stream)
+                kab, _ = eng.collide(xs, x1, mode, sc.thickness)
+                n1.record(stream)
+                n1.synchronize()
+                times.append(n0.elapsed_time(n1))
+            g = eng.grid_info()
+            narrow[name] = {"ms": statistics.median(times), "ms_all": times, "raw_pairs": g.total, "hits": int(len(kab)),
+                            "vertex_face": int((kab[:, 0] == 0).sum()), "edge_edge": int((kab[:, 0] == 1).sum())}
+        narrow["note"] = ("weft_gpu_collide on the replayed state (x_end = x + dt v for CCD): grid, candidate walk, "
+                          "6 VF + 9 EE tests per candidate pair, radix-sorted dedup; device time incl. the hit "
+                          "download; not part of the timed step (out of the hot-path scope in both arms)")
+
     # candidate counts: each rank walks its split_workload share
     dcd_total = int(reduce_over_ranks(float(reps[-1].dcd_candidates), dist.ReduceOp.SUM if world > 1 else None))
     ccd_total = int(reduce_over_ranks(float(reps[-1].ccd_candidates), dist.ReduceOp.SUM if world > 1 else None))
@@ -382,6 +408,7 @@ def gpu_arm(args, rank, world, local):
                               "assemble": statistics.mean(r.ms_assemble for r in reps),
                               "solve": statistics.mean(r.ms_solve for r in reps)},
             "gpu_launches_per_step": launches / args.steps,
+            "narrow_phase": narrow,
         },
         "roofline": {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "alg_bytes_per_launch": alg_bytes,

@@ -421,8 +421,8 @@ class Engine:
         deduplicated by (kind, a, b). Returns (kab (n, 3) int32: kind 0 =
         VertexFace / 1 = EdgeEdge, a, b; vals (n, 8): gap|toi, normal xyz,
         weights 0..3)."""
-        xb = _f64(x_begin)
-        xe = None if x_end is None else _f64(x_end)
+        xb = x_begin if hasattr(x_begin, "data_ptr") else _f64(x_begin)
+        xe = None if x_end is None else (x_end if hasattr(x_end, "data_ptr") else _f64(x_end))
         n = C.c_int64()
         _check(LIB.weft_gpu_collide(self._ctx, _ptr(xb), _ptr(xe), C.c_int32(mode), C.c_double(thickness),
                                     C.c_double(cell_scale), C.byref(n)))
