@@ -285,4 +285,36 @@ inline GridBuildResult build_grid(const CollisionSoup& soup, std::span<const Vec
   return out;
 }
 
+// collide (collision.cpp:391-417): broad + narrow phase on the GPU, results
+// in the reference's NarrowPhaseResult (sorted, deduplicated). The soup's
+// movable flags are honoured; `engine` only selects the context.
+inline NarrowPhaseResult collide(Engine& engine, const CollisionSoup& soup, std::span<const Vec3> x_begin,
+                                 std::span<const Vec3> x_end, CollisionMode mode, const CollisionParams& params,
+                                 CollideTimes* /*times*/ = nullptr) {
+  weft_gpu_ctx* ctx = context_for(engine).get();
+  std::vector<int32_t> tris(3 * soup.triangles.size());
+  for (std::size_t t = 0; t < soup.triangles.size(); ++t)
+    for (int c = 0; c < 3; ++c) tris[3 * t + static_cast<std::size_t>(c)] = soup.triangles[t][static_cast<std::size_t>(c)];
+  check(weft_gpu_set_soup(ctx, soup.vertex_count, static_cast<int32_t>(soup.triangles.size()), tris.data()));
+  check(weft_gpu_set_soup_movable(ctx, soup.movable.data()));
+  const auto x0 = flat3(x_begin), x1 = flat3(x_end);
+  const bool ccd = mode == CollisionMode::Continuous;
+  int64_t n = 0;
+  check(weft_gpu_collide(ctx, x0.data(), x1.data(), ccd ? WEFT_CONTINUOUS : WEFT_DISCRETE, params.thickness,
+                         params.cell_scale, &n));
+  std::vector<int32_t> kab(3 * static_cast<std::size_t>(n));
+  std::vector<double> vals(8 * static_cast<std::size_t>(n));
+  check(weft_gpu_download_contacts(ctx, kab.data(), vals.data()));
+  NarrowPhaseResult out;
+  for (int64_t i = 0; i < n; ++i) {
+    const auto kind = kab[3 * i] == 0 ? FeatureKind::VertexFace : FeatureKind::EdgeEdge;
+    const double* v = &vals[8 * i];
+    const Vec3 nrm(v[1], v[2], v[3]);
+    const std::array<double, 4> w{v[4], v[5], v[6], v[7]};
+    if (ccd) out.impacts.push_back(Impact{kind, kab[3 * i + 1], kab[3 * i + 2], v[0], nrm, w});
+    else out.proximities.push_back(Proximity{kind, kab[3 * i + 1], kab[3 * i + 2], v[0], nrm, w});
+  }
+  return out;
+}
+
 }  // namespace weft::gpu

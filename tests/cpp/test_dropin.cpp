@@ -162,3 +162,31 @@ TEST_CASE("drop-in build_grid equals the reference build_grid bit for bit") {
     }
   }
 }
+
+TEST_CASE("drop-in collide equals the reference collide (hits, bitwise values)") {
+  oracle::Rng rng(44);
+  for (int trial = 0; trial < 4; ++trial) {
+    const auto scene = oracle::random_two_cloth_scene(rng, 8);
+    for (CollisionMode mode : {CollisionMode::Discrete, CollisionMode::Continuous}) {
+      CollisionParams params;
+      params.thickness = mode == CollisionMode::Discrete ? 0.1 : 0.01;
+      for (int n : {1, 2}) {
+        Engine engine(n);
+        const auto ref = collide(engine, scene.soup, scene.x_begin, scene.x_end, mode, params);
+        const auto gpu = gpu::collide(engine, scene.soup, scene.x_begin, scene.x_end, mode, params);
+        REQUIRE(ref.proximities.size() == gpu.proximities.size());
+        REQUIRE(ref.impacts.size() == gpu.impacts.size());
+        for (std::size_t i = 0; i < ref.proximities.size(); ++i) {
+          const auto &a = ref.proximities[i], &b = gpu.proximities[i];
+          CHECK((a.kind == b.kind && a.a == b.a && a.b == b.b && a.gap == b.gap && a.normal == b.normal &&
+                 a.weights == b.weights));
+        }
+        for (std::size_t i = 0; i < ref.impacts.size(); ++i) {
+          const auto &a = ref.impacts[i], &b = gpu.impacts[i];
+          CHECK((a.kind == b.kind && a.a == b.a && a.b == b.b && a.toi == b.toi && a.normal == b.normal &&
+                 a.weights == b.weights));
+        }
+      }
+    }
+  }
+}
