@@ -352,6 +352,26 @@ void set_elements(Ctx& c, int64_t count, const weft_element* elems) {
   upload_elements(c, count, elems, 0, 0, &used, 0, &rused);
   c.n_static = count;
   c.static_pay = used;
+  // same-kind runs of the static list (k_elem_eval is compiled per kind)
+  c.kind_runs.clear();
+  {
+    std::vector<weft_element> host;
+    const weft_element* h = elems;
+    cudaPointerAttributes attr{};
+    if (count && cudaPointerGetAttributes(&attr, elems) == cudaSuccess && attr.type == cudaMemoryTypeDevice) {
+      host.resize(static_cast<size_t>(count));
+      WG_CUDA(cudaMemcpy(host.data(), elems, sizeof(weft_element) * count, cudaMemcpyDeviceToHost));
+      h = host.data();
+    }
+    cudaGetLastError();
+    for (int64_t i = 0; i < count;) {
+      int64_t j = i + 1;
+      while (j < count && h[j].kind == h[i].kind) ++j;
+      c.kind_runs.push_back(Ctx::KindRun{h[i].kind, i, j});
+      i = j;
+    }
+    if (c.kind_runs.size() > 16) c.kind_runs.clear();  // unsorted list: one generic launch
+  }
   c.static_res = rused;
   c.n_contacts = 0;
   build_incidence(c, 0, count, 0, c.inc_ptr, c.inc);
@@ -781,7 +801,7 @@ __device__ __forceinline__ bool elem_block(int kind, const double* __restrict__ 
 
 struct ElemArgs {
   int64_t n;
-  const int64_t* __restrict__ list;  // element ids to evaluate (null: 0..n-1)
+  const int64_t* __restrict__ list;  // element ids to evaluate (null: first .. first+n-1)
   double dt;
   const int4* __restrict__ est;
   const int2* __restrict__ einfo;
@@ -792,6 +812,7 @@ struct ElemArgs {
   const double* __restrict__ xc;
   const double* __restrict__ xa;
   const double* __restrict__ vel;
+  int64_t first;  // first element id (list == null)
 };
 
 #ifndef WEFT_EVAL_MINB
@@ -800,13 +821,18 @@ struct ElemArgs {
 #ifndef WEFT_SLOT_MINB
 #define WEFT_SLOT_MINB 2
 #endif
+// KIND >= 0: every element of the launch has that kind (runs of the static
+// list, which build_elements orders triangles -> hinges -> vertices), so the
+// kernel is compiled for one element kind — no divergence, and the register
+// allocation of that kind only. KIND < 0: any kind (contacts, rank lists).
+template <int KIND>
 __global__ void __launch_bounds__(128, WEFT_EVAL_MINB) k_elem_eval(ElemArgs g) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= g.n) return;
-  const int64_t e = g.list ? g.list[i] : i;
+  const int64_t e = g.list ? g.list[i] : g.first + i;
   const int4 s4 = g.est[e];
   const int2 info = g.einfo[e];
-  const int kind = info.x & 0xff, ss = (info.x >> 8) & 0xff;
+  const int kind = KIND >= 0 ? KIND : (info.x & 0xff), ss = (info.x >> 8) & 0xff;
   const int st[4] = {s4.x, s4.y, s4.z, s4.w};
   const double* __restrict__ d = g.epay + info.y;
   const double damping = g.edamp[e];
@@ -1355,8 +1381,31 @@ void fill_matrix(Ctx& c, const double* xc, const double* xa, const double* vel, 
       list = c.elist.data();
     }
     ElemArgs ea{ne, list, dt, c.est.data(), c.einfo.data(), c.edamp.data(), c.epay.data(), c.eres_off.data(),
-                c.eres.data(), xc, xa, vel};
-    if (ne) k_elem_eval<<<div_up(ne, 128), 128, 0, ls(c)>>>(ea);
+                c.eres.data(), xc, xa, vel, 0};
+    if (list || c.kind_runs.empty()) {
+      if (ne) k_elem_eval<-1><<<div_up(ne, 128), 128, 0, ls(c)>>>(ea);
+    } else {
+      // one launch per same-kind run of the static list, then the contacts
+      for (const auto& run : c.kind_runs) {
+        ElemArgs er = ea;
+        er.first = run.begin;
+        er.n = run.end - run.begin;
+        if (!er.n) continue;
+        const int blocks = div_up(er.n, 128);
+        switch (run.kind) {
+          case WEFT_STRETCH: k_elem_eval<WEFT_STRETCH><<<blocks, 128, 0, ls(c)>>>(er); break;
+          case WEFT_BEND: k_elem_eval<WEFT_BEND><<<blocks, 128, 0, ls(c)>>>(er); break;
+          case WEFT_EXTERNAL: k_elem_eval<WEFT_EXTERNAL><<<blocks, 128, 0, ls(c)>>>(er); break;
+          default: k_elem_eval<-1><<<blocks, 128, 0, ls(c)>>>(er); break;
+        }
+      }
+      if (c.n_contacts) {
+        ElemArgs er = ea;
+        er.first = c.n_static;
+        er.n = c.n_contacts;
+        k_elem_eval<-1><<<div_up(er.n, 128), 128, 0, ls(c)>>>(er);
+      }
+    }
     SlotArgs sa{nloc, c.row0, A.perm.data(), c.n_static, dt, A.slice_off.data(), A.rowlen.data(), A.cols.data(), A.vals.data(),
                 A.total, c.mass.data(), c.pinned.data(), c.inc_ptr.data(), c.inc.data(), c.cinc_ptr.data(),
                 c.cinc.data(), c.est.data(), c.einfo.data(), c.edamp.data(), c.epay.data(), c.eres_off.data(),

@@ -94,6 +94,11 @@ struct Ctx {
   DBuf<int32_t> eres_off;  // per element: offset of its results in eres
   DBuf<double> eres;       // phase-1 results (rhs contributions + state)
   DBuf<int64_t> elist;     // rank group: ids of the elements coupled to held rows
+  struct KindRun {
+    int kind;
+    int64_t begin, end;
+  };
+  std::vector<KindRun> kind_runs;  // same-kind runs of the static list
   int64_t static_res = 0;
   // static row incidences: per row, (element*4 + a) ascending element
   DBuf<int64_t> inc_ptr;  // p + 1
