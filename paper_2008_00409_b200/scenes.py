@@ -15,6 +15,12 @@ CONFIGS = {
     "B": (3, 309),    # Zoey-scale, 569,184 triangles
     "C": (2, 501),    # Kimono-scale, 1,000,000 triangles
     "D": (3, 525),    # Kneel-scale, 1,647,456 triangles
+    # E: the 0.5M-10M triangle sweep (BASELINE.json configs[4])
+    "E05": (1, 501),  # 500,000 triangles, one layer
+    "E1": (1, 708),   # 1,000,416 triangles, one layer
+    "E3": (3, 708),   # 3,001,248 triangles
+    "E5": (4, 792),   # 5,004,504 triangles
+    "E10": (4, 1119), # 9,999,392 triangles
 }
 
 
