@@ -301,6 +301,15 @@ typedef struct weft_sim_params {
   double cell_scale; /* CollisionParams::cell_scale */
   weft_pcg_config pcg;
   int32_t jac_mode;
+  /* 1: Simulator::step_impl stages 1-2 in full (driver.cpp:132-149): the DCD
+   * narrow phase, proximities_to_elements (response.cpp:43-106) on the
+   * device and the contact elements assembled with the static ones; the CCD
+   * narrow phase counts impacts (impact zones are not resolved). One rank
+   * only. 0: the hot-path step (candidate pairs counted, no contacts). */
+  int32_t contacts;
+  double stiffness_scale; /* ContactParams (response.hpp:13-21); contact thickness = thickness */
+  double friction;
+  double contact_damping;
 } weft_sim_params;
 
 typedef struct weft_step_report {
@@ -313,6 +322,9 @@ typedef struct weft_step_report {
                          side stream, overlapped with the assembly) */
   double ms_assemble; /* device time of fill_matrix */
   double ms_solve;    /* device time of the PCG */
+  int64_t proximities;      /* contacts mode: DCD hits */
+  int64_t contact_elements; /* contacts mode: elements built from them */
+  int64_t impacts;          /* contacts mode: CCD hits */
 } weft_step_report;
 
 /* Uploads the state (x, v: 3*p doubles each; the soup positions of the

@@ -21,6 +21,7 @@
 #include "weft/collision.hpp"
 #include "weft/mesh.hpp"
 #include "weft/physics.hpp"
+#include "weft/response.hpp"
 #include "weft/solver.hpp"
 
 #include "../include/weft_gpu.h"
@@ -747,6 +748,58 @@ int32_t ref_sim_step(void* h, const double* params, double* out) {
     out[5] = ms(tb0, tb1) + ms(tc0, tc1);
     out[6] = ms(tb1, ta);
     out[7] = ms(ta, tsol);
+    return 0;
+  } catch (const std::exception& e) {
+    return set_error(e);
+  }
+}
+
+// Simulator::step_impl (driver.cpp:96-215) without impact zones: DCD collide
+// (broad + narrow phase), proximities_to_elements, step_system with the
+// contacts, pcg_solve, candidate update, CCD collide (impacts counted, not
+// resolved), commit. params: dt, thickness, cell_scale, pcg tol, pcg max
+// its, contact stiffness_scale, friction, contact damping. out: pcg its,
+// converged, residual, proximities, contacts, impacts.
+int32_t ref_sim_step_contacts(void* h, const double* params, double* out) {
+  auto* s = static_cast<RefSim*>(h);
+  try {
+    const double dt = params[0];
+    CollisionParams cp;
+    cp.thickness = params[1];
+    cp.cell_scale = params[2];
+    PcgConfig pc;
+    pc.rel_tolerance = params[3];
+    pc.max_iterations = static_cast<int>(params[4]);
+    ContactParams kp;
+    kp.thickness = params[1];
+    kp.stiffness_scale = params[5];
+    kp.friction = params[6];
+    kp.damping = params[7];
+    const int p = s->mesh.vertex_count();
+    const auto dcd = collide(*s->engine, s->soup, s->state.x, s->state.x, CollisionMode::Discrete, cp);
+    auto contacts = proximities_to_elements(dcd.proximities, s->soup, s->state.x, s->state.v, s->mesh.vertex_mass,
+                                            dt, kp);
+    const auto ncontacts = contacts.size();
+    auto system = step_system<double>(*s->engine, s->mesh, s->state, s->material, s->pinned, std::move(contacts), dt,
+                                      Vec3(0, 0, -9.81), Vec3::Zero());
+    DistVector<double> dv(s->engine.get(), system.matrix.partitions);
+    const auto rep = pcg_solve(*s->engine, system.matrix, s->sched, system.rhs, dv, pc);
+    if (!rep.converged) throw SolverError("PCG did not converge (residual " + std::to_string(rep.rel_residual) + ")");
+    const auto dvg = dv.gather();
+    std::vector<Vec3> cand(static_cast<std::size_t>(p));
+    for (int i = 0; i < p; ++i) {
+      for (int c = 0; c < 3; ++c) s->state.v[static_cast<std::size_t>(i)][c] += dvg[static_cast<std::size_t>(3 * i + c)];
+      cand[static_cast<std::size_t>(i)] = s->state.x[static_cast<std::size_t>(i)] + dt * s->state.v[static_cast<std::size_t>(i)];
+    }
+    const auto ccd = collide(*s->engine, s->soup, s->state.x, cand, CollisionMode::Continuous, cp);
+    s->state.x = std::move(cand);
+    s->state.time += dt;
+    out[0] = rep.iterations;
+    out[1] = rep.converged ? 1 : 0;
+    out[2] = rep.rel_residual;
+    out[3] = static_cast<double>(dcd.proximities.size());
+    out[4] = static_cast<double>(ncontacts);
+    out[5] = static_cast<double>(ccd.impacts.size());
     return 0;
   } catch (const std::exception& e) {
     return set_error(e);

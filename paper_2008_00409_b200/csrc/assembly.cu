@@ -394,6 +394,38 @@ void set_contacts(Ctx& c, int64_t count, const weft_element* elems) {
   c.have_pattern_for_contacts = false;
 }
 
+// Device-generated contacts (proximities_to_elements on the GPU, narrow.cu):
+// room for `count` contact elements after the static list — 16 payload
+// doubles and 13 result doubles (3 * 4 rhs + 1 state) each — keeping the
+// static prefix. The caller's kernel fills the records.
+void reserve_contacts(Ctx& c, int64_t count) {
+  auto grow = [&](auto& buf, size_t need, size_t keep) {
+    using T = std::remove_reference_t<decltype(*buf.data())>;
+    if (need > buf.cap) {
+      DBuf<T> tmp;
+      tmp.resize(need);
+      if (keep) WG_CUDA(cudaMemcpyAsync(tmp.data(), buf.data(), keep * sizeof(T), cudaMemcpyDeviceToDevice, c.stream));
+      std::swap(tmp.ptr, buf.ptr);
+      std::swap(tmp.cap, buf.cap);
+    }
+    buf.n = need;
+  };
+  const size_t n_total = static_cast<size_t>(c.n_static + count);
+  grow(c.est, n_total + 1, static_cast<size_t>(c.n_static));
+  grow(c.einfo, n_total + 1, static_cast<size_t>(c.n_static));
+  grow(c.edamp, n_total + 1, static_cast<size_t>(c.n_static));
+  grow(c.eres_off, n_total + 1, static_cast<size_t>(c.n_static));
+  grow(c.epay, static_cast<size_t>(c.static_pay + kContactPay * count) + 1, static_cast<size_t>(c.static_pay));
+  c.eres.resize(static_cast<size_t>(c.static_res + kContactRes * count) + 1);
+  WG_CUDA(cudaStreamSynchronize(c.stream));
+}
+
+void finish_contacts(Ctx& c, int64_t count) {
+  c.n_contacts = count;
+  build_incidence(c, c.n_static, count, 0, c.cinc_ptr, c.cinc);
+  c.have_pattern_for_contacts = false;
+}
+
 // ---------------------------------------------------------------------------
 // merged pattern -> sliced-ELL layout in accumulation-group order
 // ---------------------------------------------------------------------------

@@ -169,6 +169,8 @@ struct Ctx {
   DBuf<double> hit_vals, contact_vals;  // 8 per hit: gap | toi, normal, weights
   DBuf<int64_t> hit_idx, hit_idx_sorted, hit_flag;
   int64_t n_contacts_found = 0, narrow_pairs = 0, narrow_raw_hits = 0;
+  DBuf<int> contact_active;      // proximities_to_elements: active count per vertex
+  DBuf<int64_t> contact_flag;    // per proximity: element flag, then position
 
   // ---- CUB scratch (one per stream)
   DBuf<unsigned char> scratch;
@@ -235,6 +237,15 @@ void set_soup_movable(Ctx& c, const uint8_t* movable);
 int64_t narrow_phase(Ctx& c, const double* x0, const double* x1, int mode, double thickness, int64_t begin,
                      int64_t end);
 void download_contacts(Ctx& c, int32_t* kab, double* vals);
+// proximities_to_elements on the device (response.cpp:43-106): contact
+// elements from the last DCD narrow phase, written after the static list.
+constexpr int kContactPay = 16, kContactRes = 13;
+struct ContactParamsDev {
+  double thickness, stiffness_scale, friction, damping;
+};
+int64_t contacts_from_proximities(Ctx& c, const double* x, const double* v, double dt, const ContactParamsDev& kp);
+void reserve_contacts(Ctx& c, int64_t count);
+void finish_contacts(Ctx& c, int64_t count);
 
 // rank group (comm.cu, sparse.cu)
 void set_rows(Ctx& c, int p);  // partition map + this rank's row window

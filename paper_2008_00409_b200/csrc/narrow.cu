@@ -504,7 +504,178 @@ __global__ void k_compact_hits(int64_t n, const unsigned long long* __restrict__
   for (int q = 0; q < 8; ++q) out_vals[8 * o + q] = vals[8 * idx[i] + q];
 }
 
+// ---- proximities_to_elements (response.cpp:43-106) ------------------------
+struct ContactArgs {
+  int64_t n;
+  const unsigned long long* __restrict__ keys;
+  const double* __restrict__ vals;
+  const int32_t* __restrict__ tris;
+  const int2* __restrict__ edges;
+  const uint8_t* __restrict__ movable;
+  const double* __restrict__ mass;
+  const double* __restrict__ x;
+  const double* __restrict__ v;
+  double dt;
+  ContactParamsDev kp;
+  int* __restrict__ active;  // per vertex
+  int64_t* __restrict__ flag;  // per proximity (then exclusive positions)
+  // element records (after the static list)
+  int64_t n_static, static_pay, static_res;
+  int4* __restrict__ est;
+  int2* __restrict__ einfo;
+  double* __restrict__ edamp;
+  double* __restrict__ epay;
+  int32_t* __restrict__ eres_off;
+};
+
+// participants (response.cpp:21-39): four (vertex, signed weight) pairs.
+__device__ __forceinline__ void participants(const ContactArgs& g, int64_t i, int vtx[4], double w[4]) {
+  const unsigned long long k = g.keys[i];
+  const int kind = static_cast<int>(k >> 62);
+  const int a = static_cast<int>((k >> 31) & 0x7FFFFFFFull), b = static_cast<int>(k & 0x7FFFFFFFull);
+  const double* hw = g.vals + 8 * i + 4;
+  if (kind == 0) {
+    vtx[0] = a;
+    w[0] = 1.0;
+    for (int q = 0; q < 3; ++q) {
+      vtx[q + 1] = g.tris[3 * b + q];
+      w[q + 1] = -hw[q + 1];
+    }
+  } else {
+    const int2 e1 = g.edges[a], e2 = g.edges[b];
+    vtx[0] = e1.x;
+    w[0] = hw[0];
+    vtx[1] = e1.y;
+    w[1] = hw[1];
+    vtx[2] = e2.x;
+    w[2] = -hw[2];
+    vtx[3] = e2.y;
+    w[3] = -hw[3];
+  }
+}
+
+__global__ void k_contact_active(ContactArgs g) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= g.n) return;
+  if (g.vals[8 * i] >= g.kp.thickness) return;
+  int vtx[4];
+  double w[4];
+  participants(g, i, vtx, w);
+  for (int q = 0; q < 4; ++q)
+    if (g.movable[vtx[q]]) atomicAdd(g.active + vtx[q], 1);
+}
+
+// kEmit false: flag[i] = 1 iff proximity i becomes an element; true: write
+// it at n_static + flag[i] (flag scanned to positions).
+template <bool kEmit>
+__global__ void k_contact_elems(ContactArgs g) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= g.n) return;
+  const double gap = g.vals[8 * i];
+  if (gap >= g.kp.thickness) {
+    if (!kEmit) g.flag[i] = 0;
+    return;
+  }
+  int vtx[4];
+  double w[4];
+  participants(g, i, vtx, w);
+  const V3 nrm = v3(g.vals[8 * i + 1], g.vals[8 * i + 2], g.vals[8 * i + 3]);
+  int count = 0, overlap = 1;
+  int st[4] = {-1, -1, -1, -1};
+  double cw[4] = {0.0, 0.0, 0.0, 0.0};
+  V3 rel_vel = v3(0.0, 0.0, 0.0), rel_bias = v3(0.0, 0.0, 0.0);
+  double inv_mass = 0.0, bias = 0.0;
+  for (int q = 0; q < 4; ++q) {
+    const V3 vq = ldx(g.v, vtx[q]);
+    rel_vel = add(rel_vel, scl(w[q], vq));
+    if (g.movable[vtx[q]]) {
+      st[count] = vtx[q];
+      cw[count] = w[q];
+      inv_mass = inv_mass + (w[q] * w[q]) / g.mass[vtx[q]];
+      const int ac = g.active[vtx[q]];
+      overlap = overlap < ac ? ac : overlap;  // std::max
+      ++count;
+    } else {
+      bias = bias + w[q] * dot(nrm, ldx(g.x, vtx[q]));
+      rel_bias = add(rel_bias, scl(w[q], vq));
+    }
+  }
+  const bool live = count > 0 && !(inv_mass <= 0.0);
+  if (!kEmit) {
+    g.flag[i] = live ? 1 : 0;
+    return;
+  }
+  if (!live) return;
+  const double stiffness = g.kp.stiffness_scale / (((inv_mass * g.dt) * g.dt) * static_cast<double>(overlap));
+  const double pen = g.kp.thickness - gap;
+  const double frozen = stiffness * (0.0 < pen ? pen : 0.0);
+  double tdamp = 0.0;
+  if (g.kp.friction > 0.0) {
+    const V3 vt = sub(rel_vel, scl(dot(nrm, rel_vel), nrm));
+    const double vn = norm(vt);
+    tdamp = (g.kp.friction * frozen) / (vn < 0.05 ? 0.05 : vn);
+  }
+  const int64_t k = g.flag[i];
+  const int64_t e = g.n_static + k;
+  const int64_t pay = g.static_pay + static_cast<int64_t>(kContactPay) * k;
+  g.est[e] = make_int4(st[0], st[1], st[2], st[3]);
+  g.einfo[e] = make_int2(WEFT_CONTACT | (count << 8), static_cast<int>(pay));
+  g.edamp[e] = g.kp.damping;
+  g.eres_off[e] = static_cast<int32_t>(g.static_res + static_cast<int64_t>(kContactRes) * k);
+  double* d = g.epay + pay;  // ContactData layout of weft_element.data (weft_gpu.h)
+  d[0] = nrm.x;
+  d[1] = nrm.y;
+  d[2] = nrm.z;
+  for (int q = 0; q < 4; ++q) d[3 + q] = cw[q];
+  d[7] = bias;
+  d[8] = g.kp.thickness;
+  d[9] = stiffness;
+  d[10] = g.kp.friction;
+  d[11] = tdamp;
+  d[12] = frozen;
+  d[13] = rel_bias.x;
+  d[14] = rel_bias.y;
+  d[15] = rel_bias.z;
+}
+
 }  // namespace
+
+int64_t contacts_from_proximities(Ctx& c, const double* x, const double* v, double dt, const ContactParamsDev& kp) {
+  cudaStream_t s = c.stream;
+  const int64_t n = c.n_contacts_found;
+  if (c.static_res + static_cast<int64_t>(kContactRes) * n > INT32_MAX)
+    throw Error(WEFT_ERR_DIMENSION, "contact element results exceed 2^31 doubles");
+  c.contact_active.resize(static_cast<size_t>(c.soup_verts) + 1);
+  c.contact_active.zero(s);
+  c.contact_flag.resize(static_cast<size_t>(n) + 1);
+  ContactArgs g{n,  c.contact_keys.data(), c.contact_vals.data(), c.tris.data(), c.soup_edges.data(),
+                c.soup_movable.data(), c.mass.data(), x, v, dt, kp, c.contact_active.data(), c.contact_flag.data(),
+                c.n_static, c.static_pay, c.static_res, nullptr, nullptr, nullptr, nullptr, nullptr};
+  int64_t count = 0;
+  if (n) {
+    k_contact_active<<<div_up(n, 256), 256, 0, ls(c)>>>(g);
+    k_contact_elems<false><<<div_up(n, 256), 256, 0, ls(c)>>>(g);
+    WG_CUDA(cudaMemsetAsync(c.contact_flag.data() + n, 0, sizeof(int64_t), s));
+    size_t tmp = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tmp, c.contact_flag.data(), c.contact_flag.data(), n + 1, s);
+    void* t = scratch(c, tmp);
+    WG_CUDA(cub::DeviceScan::ExclusiveSum(t, tmp, c.contact_flag.data(), c.contact_flag.data(), n + 1, s));
+    WG_CUDA(cudaMemcpyAsync(&count, c.contact_flag.data() + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    WG_CUDA(cudaStreamSynchronize(s));
+    reserve_contacts(c, count);
+    g.est = c.est.data();
+    g.einfo = c.einfo.data();
+    g.edamp = c.edamp.data();
+    g.epay = c.epay.data();
+    g.eres_off = c.eres_off.data();
+    k_contact_elems<true><<<div_up(n, 256), 256, 0, ls(c)>>>(g);
+    WG_CUDA(cudaGetLastError());
+  } else {
+    reserve_contacts(c, 0);
+  }
+  finish_contacts(c, count);
+  return count;
+}
 
 // CollisionSoup::build (collision.cpp:95-116): unique sorted edges with ids in
 // order of first appearance (triangle order, k = 0, 1, 2), per-triangle edge

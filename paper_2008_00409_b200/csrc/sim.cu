@@ -29,6 +29,11 @@ __global__ void k_candidate(int64_t i0, int64_t i1, const double* __restrict__ x
   xc[i] = x[i] + dt * vi;
 }
 
+__global__ void k_movable(int p, const uint8_t* __restrict__ pinned, uint8_t* __restrict__ movable) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < p) movable[i] = pinned[i] ? 0 : 1;
+}
+
 void upload_vec(Ctx& c, DBuf<double>& dst, const double* src, size_t n) {
   dst.resize(n);
   if (n) WG_CUDA(cudaMemcpyAsync(dst.data(), src, n * sizeof(double), cudaMemcpyDefault, c.stream));
@@ -196,6 +201,9 @@ weft_status weft_gpu_sim_set_state(weft_gpu_ctx* ctx, const double* x, const dou
     weft_gpu::upload_vec(c, c.sim_x, x, n);
     weft_gpu::upload_vec(c, c.sim_v, v, n);
     c.sim_xc.resize(n);
+    // the soup is the cloth: movable = !pinned (driver.cpp:73-85)
+    c.soup_movable.resize(static_cast<size_t>(c.p));
+    weft_gpu::k_movable<<<weft_gpu::div_up(c.p, 256), 256, 0, ls(c)>>>(c.p, c.pinned.data(), c.soup_movable.data());
     WG_CUDA(cudaStreamSynchronize(c.stream));
     c.has_state = true;
   });
@@ -216,6 +224,29 @@ weft_status weft_gpu_sim_step(weft_gpu_ctx* ctx, const weft_sim_params* prm, wef
       e = b + base + (c.rank < extra ? 1 : 0);
     };
     int64_t wb = 0, we = 0;
+    int64_t dcd = 0, nprox = 0, ncont = 0, nimp = 0;
+    const bool contacts = prm->contacts != 0;
+    if (contacts) {
+      // Simulator::step_impl stages 1-2 in full (driver.cpp:132-149): DCD
+      // collide, proximities_to_elements, step_system with the contacts.
+      if (c.world > 1) throw Error(WEFT_ERR_INVALID, "sim_step: contacts mode runs on one rank");
+      WG_CUDA(cudaEventRecord(c.ev_side[0], s));
+      weft_gpu::build_grid(c, c.sim_x.data(), c.sim_x.data(), WEFT_DISCRETE, prm->thickness, prm->cell_scale);
+      nprox = weft_gpu::narrow_phase(c, c.sim_x.data(), c.sim_x.data(), WEFT_DISCRETE, prm->thickness, 0,
+                                     c.grid_total);
+      dcd = c.narrow_pairs;
+      WG_CUDA(cudaEventRecord(c.ev_side[1], s));
+      WG_CUDA(cudaEventRecord(ev[0], s));
+      const weft_gpu::ContactParamsDev kp{prm->thickness, prm->stiffness_scale, prm->friction, prm->contact_damping};
+      ncont = weft_gpu::contacts_from_proximities(c, c.sim_x.data(), c.sim_v.data(), dt, kp);
+      c.x_adv.resize(static_cast<size_t>(n));
+      weft_gpu::k_advance<<<weft_gpu::div_up(n, 256), 256, 0, ls(c)>>>(n, c.sim_x.data(), c.sim_v.data(), dt,
+                                                                    c.x_adv.data());
+      weft_gpu::fill_matrix(c, c.sim_x.data(), c.x_adv.data(), c.sim_v.data(), dt, prm->jac_mode);
+      WG_CUDA(cudaEventRecord(ev[2], s));
+      WG_CUDA(cudaEventRecord(ev[1], s));
+    } else {
+    if (c.n_contacts) weft_gpu::finish_contacts(c, 0);  // no stale contacts from a contacts-mode step
     // 1 + 2. The proximity broad phase (DCD) on x and the assembly of
     // step_system at (x, v) are independent (contacts come from the narrow
     // phase, out of this tier): the assembly is enqueued on the main stream,
@@ -234,7 +265,6 @@ weft_status weft_gpu_sim_step(weft_gpu_ctx* ctx, const weft_sim_params* prm, wef
     if (serial) weft_gpu::fill_matrix_finish(c);
     WG_CUDA(cudaStreamWaitEvent(c.side, serial ? ev[2] : ev[0], 0));
     WG_CUDA(cudaEventRecord(c.ev_side[0], c.side));
-    int64_t dcd = 0;
     c.cur = c.side;
     try {
       weft_gpu::build_grid(c, c.sim_x.data(), c.sim_x.data(), WEFT_DISCRETE, prm->thickness, prm->cell_scale);
@@ -249,6 +279,7 @@ weft_status weft_gpu_sim_step(weft_gpu_ctx* ctx, const weft_sim_params* prm, wef
     weft_gpu::fill_matrix_finish(c);
     WG_CUDA(cudaStreamWaitEvent(s, c.ev_side[1], 0));  // the cooperative PCG gets the whole GPU
     WG_CUDA(cudaEventRecord(ev[1], s));
+    }
     // 3. PCG for dv
     const weft_gpu::PcgResult pr = weft_gpu::pcg_solve(c, c.rhs.data(), prm->pcg, nullptr, nullptr);
     WG_CUDA(cudaEventRecord(ev[3], s));
@@ -264,7 +295,13 @@ weft_status weft_gpu_sim_step(weft_gpu_ctx* ctx, const weft_sim_params* prm, wef
     // 5. impact broad phase (CCD) over begin -> candidate
     weft_gpu::build_grid(c, c.sim_x.data(), c.sim_xc.data(), WEFT_CONTINUOUS, prm->thickness, prm->cell_scale);
     share(c.grid_total, wb, we);
-    const int64_t ccd = weft_gpu::candidates(c, wb, we, nullptr, /*count_only=*/true);
+    int64_t ccd = 0;
+    if (contacts) {  // impacts found, not resolved (impact zones are out of scope)
+      nimp = weft_gpu::narrow_phase(c, c.sim_x.data(), c.sim_xc.data(), WEFT_CONTINUOUS, prm->thickness, wb, we);
+      ccd = c.narrow_pairs;
+    } else {
+      ccd = weft_gpu::candidates(c, wb, we, nullptr, /*count_only=*/true);
+    }
     WG_CUDA(cudaEventRecord(ev[5], s));
     // 7. commit (no zone correction in this tier)
     std::swap(c.sim_x.ptr, c.sim_xc.ptr);
@@ -284,6 +321,9 @@ weft_status weft_gpu_sim_step(weft_gpu_ctx* ctx, const weft_sim_params* prm, wef
       rep->ms_broad = tdcd + t45;
       rep->ms_assemble = tasm;
       rep->ms_solve = t13;
+      rep->proximities = nprox;
+      rep->contact_elements = ncont;
+      rep->impacts = nimp;
     }
   });
 }

@@ -134,13 +134,22 @@ class GridInfo(C.Structure):
 
 class SimParams(C.Structure):
     _fields_ = [("dt", C.c_double), ("thickness", C.c_double), ("cell_scale", C.c_double), ("pcg", PcgConfig),
-                ("jac_mode", C.c_int32)]
+                ("jac_mode", C.c_int32), ("contacts", C.c_int32), ("stiffness_scale", C.c_double),
+                ("friction", C.c_double), ("contact_damping", C.c_double)]
+
+    def __init__(self, dt=1.0 / 240.0, thickness=0.005, cell_scale=1.5, pcg=None, jac_mode=1, contacts=0,
+                 stiffness_scale=4.0, friction=0.2, contact_damping=0.0):
+        """SimConfig subset (driver.hpp:30-45): collision and ContactParams
+        (response.hpp:13-21) defaults of the reference."""
+        super().__init__(dt, thickness, cell_scale, pcg if pcg is not None else PcgConfig(), jac_mode, contacts,
+                         stiffness_scale, friction, contact_damping)
 
 
 class StepReport(C.Structure):
     _fields_ = [("pcg_iterations", C.c_int32), ("pcg_converged", C.c_int32), ("pcg_residual", C.c_double),
                 ("dcd_candidates", C.c_int64), ("ccd_candidates", C.c_int64), ("ms_broad", C.c_double),
-                ("ms_assemble", C.c_double), ("ms_solve", C.c_double)]
+                ("ms_assemble", C.c_double), ("ms_solve", C.c_double), ("proximities", C.c_int64),
+                ("contact_elements", C.c_int64), ("impacts", C.c_int64)]
 
 
 def _load():

@@ -459,6 +459,19 @@ class RefSim:
                 "ms_assemble", "ms_solve")
         return dict(zip(keys, out.tolist()))
 
+    def step_contacts(self, dt, thickness, cell_scale=1.5, tol=1e-4, max_it=400, stiffness_scale=4.0,
+                      friction=0.2, damping=0.0):
+        """Simulator::step_impl without impact zones (ref_sim_step_contacts)."""
+        L = self.ref.lib
+        L.ref_sim_step_contacts.restype = C.c_int32
+        prm = np.array([dt, thickness, cell_scale, tol, max_it, stiffness_scale, friction, damping], np.float64)
+        out = np.zeros(8)
+        st = L.ref_sim_step_contacts(C.c_void_p(self.h), ptr(prm), ptr(out))
+        if st:
+            raise RuntimeError(L.ref_last_error().decode())
+        keys = ("pcg_iterations", "pcg_converged", "pcg_residual", "proximities", "contacts", "impacts")
+        return dict(zip(keys, out.tolist()))
+
     def close(self):
         if self.h:
             self.ref.lib.ref_sim_free(C.c_void_p(self.h))
