@@ -348,6 +348,36 @@ def gpu_arm(args, rank, world, local):
                           "6 VF + 9 EE tests per candidate pair, radix-sorted dedup; device time incl. the hit "
                           "download; not part of the timed step (out of the hot-path scope in both arms)")
 
+    # Simulator::step_impl minus impact zones (contacts mode): DCD narrow phase
+    # -> proximities_to_elements -> assembly with contacts -> PCG -> CCD
+    # narrow phase; informational, the headline step is the hot path above
+    full = None
+    if world == 1 and not args.no_narrow:
+        fp = weft.SimParams(sc.dt, sc.thickness, 1.5, weft.PcgConfig(1e-4, 400, weft.PRECOND_BLOCK_JACOBI),
+                            weft.JAC_SPD, contacts=1)
+        ftimes, frep = [], None
+        try:
+            for k in range(4):
+                eng.sim_set_state(xs, vs)
+                f0 = torch.cuda.Event(enable_timing=True)
+                f1 = torch.cuda.Event(enable_timing=True)
+                f0.record(stream)
+                frep = eng.sim_step(fp)
+                f1.record(stream)
+                f1.synchronize()
+                if k:
+                    ftimes.append(f0.elapsed_time(f1))
+            full = {"ms": statistics.median(ftimes), "steps_per_s": 1e3 / statistics.median(ftimes),
+                    "proximities": frep.proximities, "contact_elements": frep.contact_elements,
+                    "impacts": frep.impacts, "pcg_iterations": frep.pcg_iterations,
+                    "stage_ms": {"broad_and_narrow": frep.ms_broad, "contacts_and_assemble": frep.ms_assemble,
+                                 "solve": frep.ms_solve},
+                    "note": "weft_gpu_sim_step(contacts=1) on the replayed state: Simulator::step_impl "
+                            "(driver.cpp:96-215) without impact-zone resolution, device-resident; median of 3"}
+        except weft.Error as e:
+            full = {"error": str(e)}
+        eng.sim_step(params)  # back to the hot-path step (drops the contacts)
+
     # candidate counts: each rank walks its split_workload share
     dcd_total = int(reduce_over_ranks(float(reps[-1].dcd_candidates), dist.ReduceOp.SUM if world > 1 else None))
     ccd_total = int(reduce_over_ranks(float(reps[-1].ccd_candidates), dist.ReduceOp.SUM if world > 1 else None))
@@ -409,6 +439,7 @@ def gpu_arm(args, rank, world, local):
                               "solve": statistics.mean(r.ms_solve for r in reps)},
             "gpu_launches_per_step": launches / args.steps,
             "narrow_phase": narrow,
+            "full_step_contacts": full,
         },
         "roofline": {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "alg_bytes_per_launch": alg_bytes,

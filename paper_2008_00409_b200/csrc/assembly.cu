@@ -206,13 +206,14 @@ static void build_incidence(Ctx& c, int64_t first, int64_t count, int64_t code_b
                             DBuf<int32_t>& list) {
   const int p = c.p;
   cudaStream_t s = c.stream;
-  DBuf<int> cnt;
+  DBuf<int>& cnt = c.sc_inc_cnt;
   cnt.resize(static_cast<size_t>(p) + 1);
   cnt.zero(s);
   ptr.resize(static_cast<size_t>(p) + 1);
   const int64_t m = 4 * count;
-  DBuf<uint32_t> k1, k2;
-  DBuf<int32_t> v1;
+  DBuf<uint32_t>& k1 = c.sc_inc_k1;
+  DBuf<uint32_t>& k2 = c.sc_inc_k2;
+  DBuf<int32_t>& v1 = c.sc_inc_v1;
   k1.resize(static_cast<size_t>(m) + 1);
   k2.resize(static_cast<size_t>(m) + 1);
   v1.resize(static_cast<size_t>(m) + 1);
@@ -293,7 +294,7 @@ static void build_pattern(Ctx& c, int64_t first, int64_t count, bool with_diag, 
                           DBuf<int32_t>& cols) {
   const int p = c.p;
   cudaStream_t s = c.stream;
-  DBuf<int64_t> pc;
+  DBuf<int64_t>& pc = c.sc_pat_pc;
   pc.resize(static_cast<size_t>(count) + 1);
   int64_t npairs = 0;
   if (count) {
@@ -309,7 +310,8 @@ static void build_pattern(Ctx& c, int64_t first, int64_t count, bool with_diag, 
     WG_CUDA(cudaStreamSynchronize(s));
   }
   const int64_t nk = npairs + (with_diag ? p : 0);
-  DBuf<uint64_t> k1, k2;
+  DBuf<uint64_t>& k1 = c.sc_pat_k1;
+  DBuf<uint64_t>& k2 = c.sc_pat_k2;
   k1.resize(static_cast<size_t>(nk) + 1);
   k2.resize(static_cast<size_t>(nk) + 1);
   if (count)
@@ -318,7 +320,7 @@ static void build_pattern(Ctx& c, int64_t first, int64_t count, bool with_diag, 
   if (with_diag && p) k_diag_keys<<<div_up(p, 256), 256, 0, ls(c)>>>(p, k1.data() + npairs);
   WG_CUDA(cudaGetLastError());
   const int end_bit = 32 + bits_for(p);
-  DBuf<int64_t> nsel;
+  DBuf<int64_t>& nsel = c.sc_pat_nsel;
   nsel.resize(1);
   int64_t nu = 0;
   if (nk) {
@@ -332,7 +334,7 @@ static void build_pattern(Ctx& c, int64_t first, int64_t count, bool with_diag, 
     WG_CUDA(cudaMemcpyAsync(&nu, nsel.data(), sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     WG_CUDA(cudaStreamSynchronize(s));
   }
-  DBuf<int> cnt;
+  DBuf<int>& cnt = c.sc_pat_cnt;
   cnt.resize(static_cast<size_t>(p) + 1);
   cnt.zero(s);
   cols.resize(static_cast<size_t>(nu) + 1);
@@ -507,8 +509,8 @@ __global__ void k_merge_fill(int row0, int nloc, MergeIn m, PartMap pm, GroupOrd
 static void build_layout(Ctx& c) {
   cudaStream_t s = c.stream;
   const int p = c.p;
-  DBuf<int64_t> cptr;
-  DBuf<int32_t> ccol;
+  DBuf<int64_t>& cptr = c.sc_lay_cptr;
+  DBuf<int32_t>& ccol = c.sc_lay_ccol;
   MergeIn m{c.spat_ptr.data(), c.spat.data(), nullptr, nullptr};
   if (c.n_contacts) {
     build_pattern(c, c.n_static, c.n_contacts, false, cptr, ccol);
@@ -521,7 +523,7 @@ static void build_layout(Ctx& c) {
   A.row0 = c.row0;
   A.nslices = div_up(nloc, kSlice);
   A.slice_off.resize(static_cast<size_t>(A.nslices) + 1);
-  DBuf<int32_t> len_row;
+  DBuf<int32_t>& len_row = c.sc_lay_len;
   len_row.resize(static_cast<size_t>(nloc) + 1);
   if (nloc) k_merge_len<<<div_up(nloc, 256), 256, 0, ls(c)>>>(c.row0, nloc, m, len_row.data());
   build_sigma(c, len_row.data());  // A.perm / A.pos / A.rowlen (by position)
@@ -536,7 +538,7 @@ static void build_layout(Ctx& c) {
   // totals: slots, nnzb, max row length
   int64_t total = 0;
   WG_CUDA(cudaMemcpyAsync(&total, A.slice_off.data() + A.nslices, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-  DBuf<int64_t> red;
+  DBuf<int64_t>& red = c.sc_lay_red;
   red.resize(2);
   int* lenp = A.rowlen.data();
   size_t t1 = 0, t2 = 0;
@@ -1336,10 +1338,10 @@ __global__ void k_elem_mine(int64_t n, const int4* __restrict__ est, const int2*
 static int64_t select_rank_elements(Ctx& c) {
   const int64_t ne = c.n_static + c.n_contacts;
   cudaStream_t s = c.stream;
-  DBuf<uint8_t> flag;
+  DBuf<uint8_t>& flag = c.sc_sel_flag;
   flag.resize(static_cast<size_t>(ne) + 1);
   c.elist.resize(static_cast<size_t>(ne) + 1);
-  DBuf<int64_t> cnt;
+  DBuf<int64_t>& cnt = c.sc_sel_cnt;
   cnt.resize(1);
   if (!ne) return 0;
   k_elem_mine<<<div_up(ne, 256), 256, 0, ls(c)>>>(ne, c.est.data(), c.einfo.data(), c.pinned.data(), c.row0, c.row1,

@@ -172,6 +172,15 @@ struct Ctx {
   DBuf<int> contact_active;      // proximities_to_elements: active count per vertex
   DBuf<int64_t> contact_flag;    // per proximity: element flag, then position
 
+  // ---- persistent scratch of the pattern / layout builds (they run every
+  // step in contacts mode: no cudaMalloc / cudaFree per step)
+  DBuf<int> sc_inc_cnt, sc_pat_cnt;
+  DBuf<uint32_t> sc_inc_k1, sc_inc_k2;
+  DBuf<int32_t> sc_inc_v1, sc_lay_ccol, sc_lay_len, sc_sigma_w;
+  DBuf<int64_t> sc_pat_pc, sc_pat_nsel, sc_lay_cptr, sc_lay_red, sc_sel_cnt;
+  DBuf<uint64_t> sc_pat_k1, sc_pat_k2;
+  DBuf<uint8_t> sc_sel_flag;
+
   // ---- CUB scratch (one per stream)
   DBuf<unsigned char> scratch;
   DBuf<unsigned char> scratch_side;

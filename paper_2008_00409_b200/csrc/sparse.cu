@@ -437,7 +437,7 @@ __global__ void __launch_bounds__(kSigma) k_sigma(const int32_t* __restrict__ ws
 void build_sigma(Ctx& c, const int32_t* len_row) {
   SellMatrix& A = c.A;
   const std::vector<int32_t> w = sigma_windows(c);
-  DBuf<int32_t> wd;
+  DBuf<int32_t>& wd = c.sc_sigma_w;
   wd.upload(w.data(), w.size(), c.stream);
   A.perm.resize(static_cast<size_t>(A.rows) + 1);
   A.pos.resize(static_cast<size_t>(A.rows) + 1);
@@ -1089,15 +1089,22 @@ __global__ void __launch_bounds__(kPersistThreads, WEFT_PERSIST_MINB) k_pcg_pers
   bool first = true;
   bool x_pending = false;  // x += alpha_prev * p (p in pnew of the last phase B) not applied yet
   double alpha_prev = 0.0;
+  // Phase A work split: each warp takes a contiguous run of slices. A run
+  // spans whole sigma windows, so every warp gets the same mix of long and
+  // short rows (a strided assignment, with tw a multiple of the 8 slices
+  // per window, gave some warps only the long window heads). Splitting by
+  // equal slot counts instead measured slower on the hot path.
+  const int sl_begin = static_cast<int>((static_cast<int64_t>(gw) * nslices) / tw);
+  const int sl_end = static_cast<int>((static_cast<int64_t>(gw + 1) * nslices) / tw);
   while (!done) {
     // ---- phase A: q = A p, p of the own rows, p.q
     unsigned long long tm0 = 0;
     if (g.timing && lead) tm0 = global_ns();
     double s1[1] = {0.0};
-    for (int sl = gw; sl < nslices; sl += tw) {
+    for (int sl = sl_begin; sl < sl_end; ++sl) {
 #if WEFT_PK_PREFETCH == 1
       // stream this warp's next slice into L2 while this one computes
-      if (lane == 0 && sl + tw < nslices) prefetch_slice_l2(A, sl + tw);
+      if (lane == 0 && sl + 1 < sl_end) prefetch_slice_l2(A, sl + 1);
 #elif WEFT_PK_PREFETCH == 2
       // request this slice's whole record stream at once (one bulk L2 prefetch)
       if (lane == 0) prefetch_slice_l2(A, sl);
