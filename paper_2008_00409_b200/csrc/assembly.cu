@@ -853,7 +853,7 @@ struct ElemArgs {
 #define WEFT_EVAL_MINB 1
 #endif
 #ifndef WEFT_SLOT_MINB
-#define WEFT_SLOT_MINB 2
+#define WEFT_SLOT_MINB 4
 #endif
 // KIND >= 0: every element of the launch has that kind (runs of the static
 // list, which build_elements orders triangles -> hinges -> vertices), so the
@@ -1082,7 +1082,10 @@ struct SlotArgs {
   int* __restrict__ bad_mass;
 };
 
-constexpr int kSlotWarps = 8;
+#ifndef WEFT_SLOT_WARPS
+#define WEFT_SLOT_WARPS 4  // 4 warps x 4 CTAs/SM measured best (3, 8, 13 slower)
+#endif
+constexpr int kSlotWarps = WEFT_SLOT_WARPS;
 constexpr int kStageCap = 1024;  // staged incidences per slice (static + contact)
 
 // One staged incidence of the slice (shared memory).
