@@ -388,15 +388,11 @@ def gpu_arm(args, rank, world, local):
     value = args.steps / (ms_total / 1e3)  # whole-job steps/s (one step = the whole cloth on all ranks)
     peak, peak_src = peaks()
     if st.pcg_solves:
-        # k_pcg_persistent: per iteration, phase A streams 9
-        # FP64 values + 1 int32 column per live block and per row the length
-        # word, z and p gathered once, q and p written (4 + 4*24 B); phase B
-        # reads q, r (48 B) and D^-1 (72 B) and writes r, z (48 B), plus on
-        # every other iteration the deferred x update (x read + written, two
-        # p read: 96 B), i.e. 216 B/row on average.
+        # k_pcg_persistent: per iteration 76 B per streamed
+        # live block (9 FP64 values + int32 column) and per row 268 B (q kept
+        # in shared memory) or 316 B (q through HBM), counted by the library.
         kname = "k_pcg_persistent (whole PCG solve, one launch)"
-        it_bytes = info.nnzb * (9 * 8 + 4) + info.block_rows * (4 + 4 * 24 + 216)
-        alg_bytes = it_bytes * st.pcg_iterations / st.pcg_solves
+        alg_bytes = st.pcg_bytes / st.pcg_solves  # the library's per-solve algorithmic bytes
         launch_ms = st.pcg_ms / st.pcg_solves
         nlaunch = st.pcg_solves
         traffic = pcg_traffic_per_launch(args.config, st.pcg_iterations / st.pcg_solves)

@@ -348,6 +348,7 @@ typedef struct weft_gpu_stats_t {
   int64_t pcg_solves;     /* persistent PCG kernels timed while profiling */
   int64_t pcg_iterations; /* their iterations */
   double pcg_ms;          /* their summed device time (CUDA events) */
+  double pcg_bytes;       /* their summed algorithmic HBM bytes */
 } weft_gpu_stats_t;
 
 /* Enables CUDA-event timing of the PCG kernels (resets the counters):

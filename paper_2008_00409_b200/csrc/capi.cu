@@ -328,6 +328,7 @@ weft_status weft_gpu_profile(weft_gpu_ctx* ctx, int32_t enable) {
     ctx->c.pcg_solves = 0;
     ctx->c.pcg_iterations = 0;
     ctx->c.pcg_ms = 0.0;
+    ctx->c.pcg_bytes = 0.0;
   });
 }
 
@@ -339,6 +340,7 @@ weft_status weft_gpu_stats(weft_gpu_ctx* ctx, weft_gpu_stats_t* out) {
     out->pcg_solves = ctx->c.pcg_solves;
     out->pcg_iterations = ctx->c.pcg_iterations;
     out->pcg_ms = ctx->c.pcg_ms;
+    out->pcg_bytes = ctx->c.pcg_bytes;
   });
 }
 

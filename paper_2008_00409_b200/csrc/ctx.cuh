@@ -194,6 +194,7 @@ struct Ctx {
   int64_t pcg_solves = 0;         // persistent solves timed while profiling
   int64_t pcg_iterations = 0;     // their iterations
   double pcg_ms = 0.0;            // their summed device time
+  double pcg_bytes = 0.0;         // their summed algorithmic bytes
   std::vector<cudaEvent_t> prof_ev;
 
   // ---- resident simulation state

@@ -780,6 +780,7 @@ struct PcgArgs {
   CommView cv;
   PartMap pm;
   double* p2;  // persistent solve: second search-direction buffer
+  int q_msw;   // persistent solve with q in shared memory: max slices per warp
   unsigned long long* timing;  // dev instrumentation (WEFT_PCG_TIMING=1): ns per phase, summed
 };
 
@@ -1058,10 +1059,14 @@ __device__ __forceinline__ void all_blocks_sum(const double* partials, int n, do
   __syncthreads();
 }
 
+// kQs: q = A p of the warp's rows stays in shared memory between phase A
+// and phase B (phase B then walks the same slice runs): q never touches HBM.
+template <bool kQs>
 __global__ void __launch_bounds__(kPersistThreads, WEFT_PERSIST_MINB) k_pcg_persistent(const PcgArgs* __restrict__ args, PcgState* st) {
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
   __shared__ double smem[2 * 32];
+  extern __shared__ double q_s[];  // kQs: [warp][slice of the run][component][lane]
   const PcgArgs& g = *args;
   const SellView A = g.A;
   const int rows = A.rows;
@@ -1096,6 +1101,7 @@ __global__ void __launch_bounds__(kPersistThreads, WEFT_PERSIST_MINB) k_pcg_pers
   // equal slot counts instead measured slower on the hot path.
   const int sl_begin = static_cast<int>((static_cast<int64_t>(gw) * nslices) / tw);
   const int sl_end = static_cast<int>((static_cast<int64_t>(gw + 1) * nslices) / tw);
+  double* const qw = q_s + static_cast<size_t>(threadIdx.x >> 5) * g.q_msw * 96 + lane;  // kQs: this warp's rows
   while (!done) {
     // ---- phase A: q = A p, p of the own rows, p.q
     unsigned long long tm0 = 0;
@@ -1120,9 +1126,16 @@ __global__ void __launch_bounds__(kPersistThreads, WEFT_PERSIST_MINB) k_pcg_pers
           p1 = p1 + beta * __ldcg(pcur + 3 * i + 1);
           p2 = p2 + beta * __ldcg(pcur + 3 * i + 2);
         }
-        __stcg(q + 3 * i, y0);
-        __stcg(q + 3 * i + 1, y1);
-        __stcg(q + 3 * i + 2, y2);
+        if constexpr (kQs) {
+          double* qq = qw + (sl - sl_begin) * 96;
+          qq[0] = y0;
+          qq[32] = y1;
+          qq[64] = y2;
+        } else {
+          __stcg(q + 3 * i, y0);
+          __stcg(q + 3 * i + 1, y1);
+          __stcg(q + 3 * i + 2, y2);
+        }
         __stcg(pnew + 3 * i, p0);
         __stcg(pnew + 3 * i + 1, p1);
         __stcg(pnew + 3 * i + 2, p2);
@@ -1158,11 +1171,17 @@ __global__ void __launch_bounds__(kPersistThreads, WEFT_PERSIST_MINB) k_pcg_pers
     // — the same two roundings in the same order, one x round trip fewer.
     const bool x_now = !WEFT_PK_XDEFER || x_pending;
     double s2[2] = {0.0, 0.0};
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < rows; i += gridDim.x * blockDim.x) {
+    // kQs: the rows of this warp's slice run (q from shared memory);
+    // otherwise row-linear over the grid
+    const int pb_begin = kQs ? sl_begin * kSlice + lane : blockIdx.x * blockDim.x + threadIdx.x;
+    const int pb_end = kQs ? min(rows, sl_end * kSlice) : rows;
+    const int pb_step = kQs ? kSlice : gridDim.x * blockDim.x;
+    for (int i = pb_begin; i < pb_end; i += pb_step) {
       double qv[3], rv[3], m[9];
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
-        qv[c] = __ldcg(q + 3 * i + c);
+        if constexpr (kQs) qv[c] = qw[((i - lane) / kSlice - sl_begin) * 96 + 32 * c];
+        else qv[c] = __ldcg(q + 3 * i + c);
         rv[c] = __ldcg(r + 3 * i + c);
       }
       if (x_now) {
@@ -1244,8 +1263,11 @@ __global__ void __launch_bounds__(kPersistThreads, WEFT_PERSIST_MINB) k_pcg_pers
   }
   if (x_pending && status == 0) {
     // the last iteration's deferred x update (its p is in pnew: the swap
-    // below the residual test is skipped on exit)
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < rows; i += gridDim.x * blockDim.x)
+    // below the residual test is skipped on exit), over phase B's rows
+    const int pb_begin = kQs ? sl_begin * kSlice + lane : blockIdx.x * blockDim.x + threadIdx.x;
+    const int pb_end = kQs ? min(rows, sl_end * kSlice) : rows;
+    const int pb_step = kQs ? kSlice : gridDim.x * blockDim.x;
+    for (int i = pb_begin; i < pb_end; i += pb_step)
 #pragma unroll
       for (int c = 0; c < 3; ++c) __stcg(x + 3 * i + c, __ldcg(x + 3 * i + c) + alpha_prev * __ldcg(pnew + 3 * i + c));
   }
@@ -1389,12 +1411,30 @@ PcgResult pcg_solve(Ctx& c, const double* b_dev, const weft_pcg_config& cfg, dou
   // per-solve argument block (device)
   const PartBlocks pb2 = part_blocks(c, threads / 2);
   const int nblocks2 = pb2.bstart[pb2.n];
-  int pgrid = 0;
+  int pgrid = 0, msw = 0;
+  size_t qs_bytes = 0;
+  auto pkern = k_pcg_persistent<false>;
   if (persistent) {
-    int occ = 0, sms = 0;
-    WG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_pcg_persistent, kPersistThreads, 0));
+    // q in shared memory when the warps' slice runs fit at two CTAs per SM
+    int sms = 0;
     WG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device));
+    const int warps_per_cta = kPersistThreads / 32;
+    const int nsl = div_up(rows, kSlice);
+    msw = div_up(nsl, static_cast<int64_t>(sms) * WEFT_PERSIST_MINB * warps_per_cta);
+    qs_bytes = static_cast<size_t>(warps_per_cta) * msw * 96 * sizeof(double);
+    static const bool qs_off = std::getenv("WEFT_PCG_QSMEM") && std::atoi(std::getenv("WEFT_PCG_QSMEM")) == 0;
+    const bool qs = !qs_off && qs_bytes <= 100 * 1024;
+    if (qs) {
+      pkern = k_pcg_persistent<true>;
+      WG_CUDA(cudaFuncSetAttribute(pkern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(qs_bytes)));
+    } else {
+      qs_bytes = 0;
+    }
+    int occ = 0;
+    WG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pkern, kPersistThreads, qs_bytes));
     pgrid = std::max(1, occ) * sms;
+    if (qs && static_cast<int64_t>(pgrid) * warps_per_cta * msw < nsl)
+      throw Error(WEFT_ERR_EXEC, "pcg: persistent grid smaller than planned (" + std::to_string(pgrid) + " CTAs)");
     c.p2.resize(len);
     if (c.partials.size() < 3 * static_cast<size_t>(pgrid) + 4) c.partials.resize(3 * static_cast<size_t>(pgrid) + 4);
   }
@@ -1403,6 +1443,7 @@ PcgResult pcg_solve(Ctx& c, const double* b_dev, const weft_pcg_config& cfg, dou
   if (persistent) {
     args.A.cols = c.A.colp.data();  // columns as positions
     args.x = c.xp.data();
+    args.q_msw = msw;
     if (std::getenv("WEFT_PCG_TIMING")) {
       c.timing.resize(8);
       c.timing.zero(s);
@@ -1421,8 +1462,8 @@ PcgResult pcg_solve(Ctx& c, const double* b_dev, const weft_pcg_config& cfg, dou
     // the whole solve: one cooperative launch (co-resident grid, grid syncs)
     void* kargs[] = {(void*)&dargs, (void*)&c.pcg};
     if (c.profile) WG_CUDA(cudaEventRecord(c.ev[6], s));
-    WG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_pcg_persistent), dim3(pgrid), dim3(kPersistThreads),
-                                        kargs, 0, s));
+    WG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(pkern), dim3(pgrid), dim3(kPersistThreads), kargs,
+                                        qs_bytes, s));
     ++c.launches;
     if (c.profile) WG_CUDA(cudaEventRecord(c.ev[7], s));
     k_scatter_rows<<<div_up(rows, threads), threads, 0, ls(c)>>>(rows, c.A.perm.data(), c.xp.data(), c.xs.data());
@@ -1441,6 +1482,13 @@ PcgResult pcg_solve(Ctx& c, const double* b_dev, const weft_pcg_config& cfg, dou
       c.pcg_ms += ms;
       c.pcg_iterations += hs->iter;
       ++c.pcg_solves;
+      // algorithmic bytes per iteration: 76 per streamed live
+      // block; per row phase A 4 + 2*24 gathered + 24 p written (+ 24 q
+      // written unless q stays in shared memory), phase B 24 r + 72 D^-1
+      // read, 48 r, z written, 48 for x / p every other iteration (+ 24 q
+      // read unless shared)
+      const double per_row = 4.0 + 48.0 + 24.0 + 24.0 + 72.0 + 48.0 + 48.0 + (qs_bytes ? 0.0 : 48.0);
+      c.pcg_bytes += hs->iter * (76.0 * static_cast<double>(c.A.nnzb) + per_row * rows);
     }
   } else if (!c.profile && c.use_graphs) {
     // The whole solve is one graph launch: a conditional WHILE node whose

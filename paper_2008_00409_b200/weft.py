@@ -533,7 +533,8 @@ class ClothMesh:
 
 class GpuStats(C.Structure):
     _fields_ = [("launches", C.c_int64), ("spmv_launches", C.c_int64), ("spmv_ms", C.c_double),
-                ("pcg_solves", C.c_int64), ("pcg_iterations", C.c_int64), ("pcg_ms", C.c_double)]
+                ("pcg_solves", C.c_int64), ("pcg_iterations", C.c_int64), ("pcg_ms", C.c_double),
+                ("pcg_bytes", C.c_double)]
 
 
 def _engine_profile(self, enable: bool = True):

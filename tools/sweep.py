@@ -59,8 +59,7 @@ def run(cfg: str, steps: int = 6, warmup: int = 3):
     st = eng.stats()
     eng.profile(False)
     info = eng.matrix_info()
-    it_bytes = info.nnzb * 76 + info.block_rows * (4 + 4 * 24 + 216)
-    pcg_gbs = it_bytes * st.pcg_iterations / (st.pcg_ms * 1e-3) / 1e9 if st.pcg_solves else None
+    pcg_gbs = st.pcg_bytes / (st.pcg_ms * 1e-3) / 1e9 if st.pcg_solves else None
     eng.set_soup_movable(1 - sc.pinned)
     eng.collide(xs, None, weft.DISCRETE, sc.thickness)
     n0, n1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
