@@ -124,6 +124,7 @@ struct Ctx {
   // ---- PCG work
   DBuf<double> r, z, pv, q, xs, dinv, bvec;
   DBuf<double> xp;  // persistent PCG: solution in position space
+  DBuf<double> dinv6;  // persistent PCG: packed symmetric block-Jacobi inverses
   DBuf<unsigned long long> timing;  // dev instrumentation of the persistent PCG
   DBuf<double> partials;
   DBuf<double> hist, phist;

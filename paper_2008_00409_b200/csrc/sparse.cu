@@ -695,8 +695,12 @@ __global__ void __launch_bounds__(256) k_dot2(PartBlocks pb, const double* __res
 // Block-Jacobi inverse of the diagonal blocks (solver.hpp:49-65) with the
 // cofactor inverse of oracle/shim/Eigen/Dense; identity when absent.
 // dinv is indexed by global row.
+// kPosOut (persistent solve): position order, plus the packed upper
+// triangle d6 (6 doubles) and *asym = 1 if any inverse is not bitwise
+// symmetric (then the solve reads the 9-double form).
 template <bool kPosOut>
-__global__ void k_dinv(SellView A, double* __restrict__ dinv) {
+__global__ void k_dinv(SellView A, double* __restrict__ dinv, double* __restrict__ d6 = nullptr,
+                       int* __restrict__ asym = nullptr) {
   const int mp = blockIdx.x * blockDim.x + threadIdx.x;
   if (mp >= A.rows) return;
   const int r = A.row0 + A.perm[mp];
@@ -727,6 +731,19 @@ __global__ void k_dinv(SellView A, double* __restrict__ dinv) {
   o[6] = COF(0, 2) * invdet;
   o[7] = COF(1, 2) * invdet;
   o[8] = COF(2, 2) * invdet;
+  if (kPosOut && d6) {
+    // SpdProjected / contact / mass diagonal blocks are bitwise symmetric
+    // (sums of outer products in one order), and so are their cofactor
+    // inverses: 6 doubles carry the block exactly.
+    if (o[1] != o[3] || o[2] != o[6] || o[5] != o[7]) atomicOr(asym, 1);
+    double* h = d6 + 6 * (size_t)mp;
+    h[0] = o[0];
+    h[1] = o[1];
+    h[2] = o[2];
+    h[3] = o[4];
+    h[4] = o[5];
+    h[5] = o[8];
+  }
 #undef COF
 #undef M
 }
@@ -781,6 +798,7 @@ struct PcgArgs {
   PartMap pm;
   double* p2;  // persistent solve: second search-direction buffer
   int q_msw;   // persistent solve with q in shared memory: max slices per warp
+  const double* dinv6;  // persistent solve: packed symmetric D^-1 (null: 9-double form)
   unsigned long long* timing;  // dev instrumentation (WEFT_PCG_TIMING=1): ns per phase, summed
 };
 
@@ -1199,8 +1217,18 @@ __global__ void __launch_bounds__(kPersistThreads, WEFT_PERSIST_MINB) k_pcg_pers
         for (int c = 0; c < 3; ++c) __stcg(x + 3 * i + c, xv[c] + alpha * pv[c]);
       }
       if (bj) {
+        if (g.dinv6) {  // bitwise-symmetric inverses: 48 instead of 72 bytes per row
+          const double* h = g.dinv6 + 6 * (size_t)i;
+          m[0] = __ldg(h);
+          m[1] = m[3] = __ldg(h + 1);
+          m[2] = m[6] = __ldg(h + 2);
+          m[4] = __ldg(h + 3);
+          m[5] = m[7] = __ldg(h + 4);
+          m[8] = __ldg(h + 5);
+        } else {
 #pragma unroll
-        for (int k = 0; k < 9; ++k) m[k] = __ldg(dinv + 9 * (size_t)i + k);
+          for (int k = 0; k < 9; ++k) m[k] = __ldg(dinv + 9 * (size_t)i + k);
+        }
       }
 #pragma unroll
       for (int c = 0; c < 3; ++c) rv[c] = rv[c] - alpha * qv[c];
@@ -1364,6 +1392,7 @@ PcgResult pcg_solve(Ctx& c, const double* b_dev, const weft_pcg_config& cfg, dou
   init.first = 1;
   WG_CUDA(cudaMemcpyAsync(c.pcg, &init, sizeof(init), cudaMemcpyHostToDevice, s));
   double* dots = reinterpret_cast<double*>(c.scalars.data());
+  int* dinv_asym = reinterpret_cast<int*>(c.scalars.data() + 12);
   if (rows > 0) {
     if (persistent) {
       if (c.A.colp_id != c.A.layout_id) {  // position-space column words, once per layout
@@ -1374,7 +1403,9 @@ PcgResult pcg_solve(Ctx& c, const double* b_dev, const weft_pcg_config& cfg, dou
         c.A.colp_id = c.A.layout_id;
       }
       c.xp.resize(len);
-      if (bj) k_dinv<true><<<div_up(rows, threads), threads, 0, ls(c)>>>(A, c.dinv.data());
+      c.dinv6.resize(6 * static_cast<size_t>(rows) + 6);
+      WG_CUDA(cudaMemsetAsync(dinv_asym, 0, sizeof(int), s));
+      if (bj) k_dinv<true><<<div_up(rows, threads), threads, 0, ls(c)>>>(A, c.dinv.data(), c.dinv6.data(), dinv_asym);
       k_pcg_init_pos<<<div_up(rows, threads), threads, 0, ls(c)>>>(rows, c.A.perm.data(), b_dev, c.dinv.data(), bj,
                                                                    c.xp.data(), c.r.data(), c.z.data(), c.pv.data());
       // ||b|| and rho = r.z over the permuted r = b
@@ -1392,7 +1423,9 @@ PcgResult pcg_solve(Ctx& c, const double* b_dev, const weft_pcg_config& cfg, dou
     WG_CUDA(cudaGetLastError());
   }
   double hd[2] = {0.0, 0.0};
+  int asym = 1;
   if (rows > 0) WG_CUDA(cudaMemcpyAsync(hd, dots, sizeof(hd), cudaMemcpyDeviceToHost, s));
+  if (rows > 0 && persistent && bj) WG_CUDA(cudaMemcpyAsync(&asym, dinv_asym, sizeof(int), cudaMemcpyDeviceToHost, s));
   WG_CUDA(cudaStreamSynchronize(s));
   comm_check(c);
   PcgResult res;
@@ -1444,6 +1477,8 @@ PcgResult pcg_solve(Ctx& c, const double* b_dev, const weft_pcg_config& cfg, dou
     args.A.cols = c.A.colp.data();  // columns as positions
     args.x = c.xp.data();
     args.q_msw = msw;
+    static const bool d6_off = std::getenv("WEFT_PCG_DINV6") && std::atoi(std::getenv("WEFT_PCG_DINV6")) == 0;
+    args.dinv6 = (bj && !asym && !d6_off) ? c.dinv6.data() : nullptr;
     if (std::getenv("WEFT_PCG_TIMING")) {
       c.timing.resize(8);
       c.timing.zero(s);
@@ -1487,7 +1522,8 @@ PcgResult pcg_solve(Ctx& c, const double* b_dev, const weft_pcg_config& cfg, dou
       // written unless q stays in shared memory), phase B 24 r + 72 D^-1
       // read, 48 r, z written, 48 for x / p every other iteration (+ 24 q
       // read unless shared)
-      const double per_row = 4.0 + 48.0 + 24.0 + 24.0 + 72.0 + 48.0 + 48.0 + (qs_bytes ? 0.0 : 48.0);
+      const double per_row =
+          4.0 + 48.0 + 24.0 + 24.0 + (args.dinv6 ? 48.0 : 72.0) + 48.0 + 48.0 + (qs_bytes ? 0.0 : 48.0);
       c.pcg_bytes += hs->iter * (76.0 * static_cast<double>(c.A.nnzb) + per_row * rows);
     }
   } else if (!c.profile && c.use_graphs) {
