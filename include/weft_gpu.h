@@ -42,7 +42,8 @@ typedef enum weft_status {
   WEFT_ERR_EXEC = 3,      /* weft::ExecError: CUDA/NCCL failure, names the GPU */
   WEFT_ERR_TOPOLOGY = 4,  /* weft::TopologyError  */
   WEFT_ERR_SCHEDULE = 5,  /* weft::ScheduleError  */
-  WEFT_ERR_INVALID = 6    /* invalid argument or call order */
+  WEFT_ERR_INVALID = 6,   /* invalid argument or call order */
+  WEFT_ERR_ZONE = 7       /* weft::ZoneFailure (response.hpp:8-11) */
 } weft_status;
 
 /* Message of the last failed call on this thread ("" if none). */
@@ -287,6 +288,54 @@ weft_status weft_gpu_collide(weft_gpu_ctx* ctx, const double* x_begin, const dou
  * weights 0..3). Either pointer may be NULL. */
 weft_status weft_gpu_download_contacts(weft_gpu_ctx* ctx, int32_t* kind_ab, double* vals);
 
+/* ---------------------------------------------------------------------- */
+/* Impact zones (proj/src/response.cpp:108-400)                           */
+/* ---------------------------------------------------------------------- */
+
+typedef struct weft_zone_params { /* ZoneSolveParams, response.hpp:46-60 */
+  double clearance;               /* h' (Simulator: clearance_fraction * thickness) */
+  double initial_penalty;         /* mu, in units of the mean zone vertex mass */
+  double inner_tolerance;
+  int32_t al_iterations;
+  int32_t inner_iterations;
+  int32_t outer_cap;
+  int32_t retry_cap;
+  double max_correction_factor;
+} weft_zone_params;
+
+typedef struct weft_zone_report { /* ZoneResolveReport, response.hpp:62-68 */
+  int32_t outer_iterations;
+  int32_t zone_count;
+  int32_t max_zone_vertices;
+  int64_t impacts_resolved;
+  int64_t first_round_impacts;
+} weft_zone_report;
+
+/* build_zones (response.cpp:108-162) over n impacts given as (kind, a, b)
+ * triples on the soup set with weft_gpu_set_soup (+ set_soup_movable):
+ * connected components of the impact graph (impacts adjacent iff they share
+ * a participant vertex), zones numbered by their first impact.
+ * impact_zone: n int32 (may be NULL); *zone_count; *vertex_total = movable
+ * zone vertices over all zones. Fetch the vertex lists with
+ * weft_gpu_zone_vertices. */
+weft_status weft_gpu_build_zones(weft_gpu_ctx* ctx, int64_t n, const int32_t* kind_ab, int32_t* impact_zone,
+                                 int32_t* zone_count, int64_t* vertex_total);
+/* The last build_zones: vert_off = zone_count + 1 offsets into verts
+ * (each zone's movable vertices, ascending). */
+weft_status weft_gpu_zone_vertices(weft_gpu_ctx* ctx, int32_t* vert_off, int32_t* verts);
+/* distribute_zones (response.cpp:164-182): device_of[z] for zones of the
+ * given vertex counts (greedy, descending size, least-loaded device). */
+weft_status weft_distribute_zones(int32_t zone_count, const int32_t* sizes, int32_t devices, int32_t* device_of);
+/* resolve_zones (response.cpp:338-400) on the soup set with set_soup (+
+ * set_soup_movable): CCD over x_begin -> x_candidate, impact zones built and
+ * solved (augmented Lagrangian, Armijo gradient descent) until clean.
+ * x_candidate (3 * soup vertices, host or device) is updated in place;
+ * vertex_mass has one entry per soup vertex. WEFT_ERR_ZONE with the
+ * reference's message when the outer cap is reached or a zone diverges. */
+weft_status weft_gpu_resolve_zones(weft_gpu_ctx* ctx, const double* x_begin, double* x_candidate,
+                                   const double* vertex_mass, double thickness, double cell_scale,
+                                   const weft_zone_params* params, weft_zone_report* report);
+
 /* split_workload (collision.cpp:181-192). */
 weft_status weft_split_workload(int64_t total, int32_t devices, int64_t* begin, int64_t* end);
 
@@ -310,6 +359,10 @@ typedef struct weft_sim_params {
   double stiffness_scale; /* ContactParams (response.hpp:13-21); contact thickness = thickness */
   double friction;
   double contact_damping;
+  /* contacts mode only — 1: resolve_zones after the CCD (driver.cpp:181-191)
+   * and the commit's velocity correction (:195-204): the full step_impl. */
+  int32_t zones;
+  weft_zone_params zone;
 } weft_sim_params;
 
 typedef struct weft_step_report {
@@ -324,7 +377,10 @@ typedef struct weft_step_report {
   double ms_solve;    /* device time of the PCG */
   int64_t proximities;      /* contacts mode: DCD hits */
   int64_t contact_elements; /* contacts mode: elements built from them */
-  int64_t impacts;          /* contacts mode: CCD hits */
+  int64_t impacts;          /* contacts mode: CCD hits (first round) */
+  int32_t zone_count;       /* zones mode: zones over all outer rounds */
+  int32_t zone_outer;       /* zones mode: outer rounds */
+  double ms_zones;          /* zones mode: device time of resolve_zones */
 } weft_step_report;
 
 /* Uploads the state (x, v: 3*p doubles each; the soup positions of the

@@ -189,6 +189,7 @@ int set_error(const std::exception& e) {
   if (dynamic_cast<const ExecError*>(&e)) return WEFT_ERR_EXEC;
   if (dynamic_cast<const TopologyError*>(&e)) return WEFT_ERR_TOPOLOGY;
   if (dynamic_cast<const ScheduleError*>(&e)) return WEFT_ERR_SCHEDULE;
+  if (dynamic_cast<const ZoneFailure*>(&e)) return WEFT_ERR_ZONE;
   return WEFT_ERR_INVALID;
 }
 
@@ -614,6 +615,98 @@ int32_t ref_two_cloth_scene(uint64_t seed, int32_t max_side, int32_t* tri_count,
   return s.soup.vertex_count;
 }
 
+
+static ZoneSolveParams zone_params_from(const double* zp) {
+  ZoneSolveParams z;
+  z.clearance = zp[0];
+  z.initial_penalty = zp[1];
+  z.inner_tolerance = zp[2];
+  z.al_iterations = static_cast<int>(zp[3]);
+  z.inner_iterations = static_cast<int>(zp[4]);
+  z.outer_cap = static_cast<int>(zp[5]);
+  z.retry_cap = static_cast<int>(zp[6]);
+  z.max_correction_factor = zp[7];
+  return z;
+}
+
+static CollisionSoup soup_from(int32_t vertex_count, int32_t tri_count, const int32_t* tris, const uint8_t* movable) {
+  std::vector<std::array<int, 3>> t(static_cast<std::size_t>(tri_count));
+  for (int i = 0; i < tri_count; ++i) t[static_cast<std::size_t>(i)] = {tris[3 * i], tris[3 * i + 1], tris[3 * i + 2]};
+  std::vector<std::uint8_t> mv(static_cast<std::size_t>(vertex_count), 1);
+  if (movable) mv.assign(movable, movable + vertex_count);
+  return CollisionSoup::build(std::move(t), vertex_count, std::move(mv));
+}
+
+// build_zones (response.cpp:108-162) over (kind, a, b) triples. Fills
+// impact_zone (n), vert_off (zones + 1, up to cap_off), verts (up to
+// cap_verts); returns the zone count.
+int32_t ref_build_zones(int32_t vertex_count, int32_t tri_count, const int32_t* tris, const uint8_t* movable, int64_t n,
+                        const int32_t* kab, int32_t* impact_zone, int64_t cap_off, int32_t* vert_off,
+                        int64_t cap_verts, int32_t* verts) {
+  try {
+    const auto soup = soup_from(vertex_count, tri_count, tris, movable);
+    std::vector<Impact> imps(static_cast<std::size_t>(n));
+    for (int64_t i = 0; i < n; ++i) {
+      auto& h = imps[static_cast<std::size_t>(i)];
+      h.kind = kab[3 * i] == 0 ? FeatureKind::VertexFace : FeatureKind::EdgeEdge;
+      h.a = kab[3 * i + 1];
+      h.b = kab[3 * i + 2];
+    }
+    const auto zones = build_zones(imps, soup);
+    int64_t off = 0;
+    for (std::size_t z = 0; z < zones.size(); ++z) {
+      for (int i : zones[z].impacts) impact_zone[i] = static_cast<int32_t>(z);
+      if (static_cast<int64_t>(z) < cap_off) vert_off[z] = static_cast<int32_t>(off);
+      for (int v : zones[z].vertices) {
+        if (off < cap_verts) verts[off] = v;
+        ++off;
+      }
+    }
+    if (static_cast<int64_t>(zones.size()) < cap_off) vert_off[zones.size()] = static_cast<int32_t>(off);
+    return static_cast<int32_t>(zones.size());
+  } catch (const std::exception& e) {
+    set_error(e);
+    return -1;
+  }
+}
+
+// resolve_zones (response.cpp:338-400) with Engine(devices). x_cand is
+// updated in place. zp: clearance, initial_penalty, inner_tolerance,
+// al_iterations, inner_iterations, outer_cap, retry_cap,
+// max_correction_factor. report: outer_iterations, zone_count,
+// max_zone_vertices, impacts_resolved, first_round_impacts.
+int32_t ref_resolve_zones(int32_t vertex_count, int32_t tri_count, const int32_t* tris, const uint8_t* movable,
+                          const double* mass, const double* x_begin, double* x_cand, double thickness,
+                          double cell_scale, int32_t devices, const double* zp, int64_t* report) {
+  try {
+    const auto soup = soup_from(vertex_count, tri_count, tris, movable);
+    const auto xb = to_vec3(x_begin, vertex_count);
+    auto xc = to_vec3(x_cand, vertex_count);
+    const std::vector<double> m(mass, mass + vertex_count);
+    CollisionParams cp;
+    cp.thickness = thickness;
+    cp.cell_scale = cell_scale;
+    Engine engine(devices);
+    int32_t status = 0;
+    ZoneResolveReport r;
+    try {
+      r = resolve_zones(engine, soup, xb, xc, m, cp, zone_params_from(zp));
+    } catch (const std::exception& e) {
+      status = set_error(e);
+    }
+    for (int v = 0; v < vertex_count; ++v)
+      for (int c = 0; c < 3; ++c) x_cand[3 * v + c] = xc[static_cast<std::size_t>(v)][c];
+    report[0] = r.outer_iterations;
+    report[1] = r.zone_count;
+    report[2] = r.max_zone_vertices;
+    report[3] = r.impacts_resolved;
+    report[4] = r.first_round_impacts;
+    return status;
+  } catch (const std::exception& e) {
+    return set_error(e);
+  }
+}
+
 }  // extern "C"
 
 // ---------------------------------------------------------------------------
@@ -758,8 +851,11 @@ int32_t ref_sim_step(void* h, const double* params, double* out) {
 // (broad + narrow phase), proximities_to_elements, step_system with the
 // contacts, pcg_solve, candidate update, CCD collide (impacts counted, not
 // resolved), commit. params: dt, thickness, cell_scale, pcg tol, pcg max
-// its, contact stiffness_scale, friction, contact damping. out: pcg its,
-// converged, residual, proximities, contacts, impacts.
+// its, contact stiffness_scale, friction, contact damping, zones flag, the 8
+// zone params (ref_resolve_zones); with the flag set, resolve_zones and the
+// commit's velocity correction run too (the full step_impl). out: pcg its,
+// converged, residual, proximities, contacts, impacts (first CCD round),
+// zone count, zone outer rounds.
 int32_t ref_sim_step_contacts(void* h, const double* params, double* out) {
   auto* s = static_cast<RefSim*>(h);
   try {
@@ -792,6 +888,17 @@ int32_t ref_sim_step_contacts(void* h, const double* params, double* out) {
       cand[static_cast<std::size_t>(i)] = s->state.x[static_cast<std::size_t>(i)] + dt * s->state.v[static_cast<std::size_t>(i)];
     }
     const auto ccd = collide(*s->engine, s->soup, s->state.x, cand, CollisionMode::Continuous, cp);
+    if (params[8] != 0.0) {
+      // 5-7. resolve_zones + the commit's velocity correction (driver.cpp:181-204)
+      const std::vector<Vec3> pre = cand;
+      const auto zr = resolve_zones(*s->engine, s->soup, s->state.x, cand, s->mesh.vertex_mass, cp,
+                                    zone_params_from(params + 9));
+      for (int i = 0; i < p; ++i)
+        if (cand[static_cast<std::size_t>(i)] != pre[static_cast<std::size_t>(i)])
+          s->state.v[static_cast<std::size_t>(i)] += (cand[static_cast<std::size_t>(i)] - pre[static_cast<std::size_t>(i)]) / dt;
+      out[6] = zr.zone_count;
+      out[7] = zr.outer_iterations;
+    }
     s->state.x = std::move(cand);
     s->state.time += dt;
     out[0] = rep.iterations;

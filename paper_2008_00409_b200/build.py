@@ -21,7 +21,7 @@ NVCC_FLAGS = [
     "-Xcompiler", "-fPIC,-O2,-ffp-contract=off", "--expt-relaxed-constexpr",
 ]
 
-SOURCES = ["capi.cu", "sparse.cu", "assembly.cu", "broadphase.cu", "sim.cu", "comm.cu", "narrow.cu", "mesh.cpp"]
+SOURCES = ["capi.cu", "sparse.cu", "assembly.cu", "broadphase.cu", "sim.cu", "comm.cu", "narrow.cu", "zones.cu", "mesh.cpp"]
 
 
 def _compile(src: str, verbose: bool) -> str:

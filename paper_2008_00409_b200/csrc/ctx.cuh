@@ -201,6 +201,20 @@ struct Ctx {
   // ---- resident simulation state
   DBuf<double> sim_x, sim_v, sim_xc;
   bool has_state = false;
+
+  // impact zones (zones.cu): accumulated impacts, zone structure, solver scratch
+  DBuf<unsigned long long> zn_acc_keys, zn_acc_sorted, zn_tmp_keys;
+  DBuf<double> zn_acc_vals;
+  DBuf<int64_t> zn_flag;
+  DBuf<int32_t> zn_part_v, zn_owner, zn_parent, zn_zone_of, zn_zone_of_sorted, zn_iota, zn_zimp, zn_zimp_off;
+  DBuf<double> zn_part_w;
+  DBuf<unsigned long long> zn_vkeys, zn_vkeys_sorted, zn_ikeys, zn_ikeys_sorted;
+  DBuf<int32_t> zn_voff, zn_ioff;
+  DBuf<double> zn_cn, zn_lam, zn_force, zn_tc, zn_tv, zn_grad, zn_saved, zn_prop, zn_pre;
+  DBuf<int32_t> zn_fail;
+  int64_t zn_m = 0;      // accumulated impacts
+  int32_t zn_nz = 0;     // zones of the last build
+  int64_t zn_nzv = 0;    // zone vertices of the last build
 };
 
 // Launch-site stream accessor: counts the launch (gpu_launches in bench.py).
@@ -256,6 +270,12 @@ struct ContactParamsDev {
 };
 int64_t contacts_from_proximities(Ctx& c, const double* x, const double* v, double dt, const ContactParamsDev& kp);
 void reserve_contacts(Ctx& c, int64_t count);
+int32_t build_zones(Ctx& c, const unsigned long long* keys, const double* vals, int64_t m);
+void download_zones(Ctx& c, int64_t m, int32_t* impact_zone, int32_t* vert_off, int32_t* verts);
+std::vector<std::vector<int>> distribute_zones(const std::vector<int>& sizes, int devices);
+void resolve_zones(Ctx& c, const double* xb, double* xcand, const double* mass, double thickness, double cell_scale,
+                   const weft_zone_params& zp, weft_zone_report& rep, bool have_first);
+void zone_commit(Ctx& c, const double* corrected, const double* pre, double dt, double* v);
 void finish_contacts(Ctx& c, int64_t count);
 
 // rank group (comm.cu, sparse.cu)

@@ -152,6 +152,76 @@ weft_status weft_gpu_download_contacts(weft_gpu_ctx* ctx, int32_t* kind_ab, doub
   return guard2(ctx, [&](Ctx& c) { weft_gpu::download_contacts(c, kind_ab, vals); });
 }
 
+weft_status weft_gpu_build_zones(weft_gpu_ctx* ctx, int64_t n, const int32_t* kind_ab, int32_t* impact_zone,
+                                 int32_t* zone_count, int64_t* vertex_total) {
+  return guard2(ctx, [&](Ctx& c) {
+    if (n < 0 || (n > 0 && !kind_ab)) throw Error(WEFT_ERR_INVALID, "build_zones: bad impact list");
+    if (c.soup_verts == 0 && n > 0) throw Error(WEFT_ERR_INVALID, "build_zones: set the soup first");
+    std::vector<unsigned long long> keys(static_cast<size_t>(n));
+    const int nedges = static_cast<int>(c.soup_edges.size());
+    for (int64_t i = 0; i < n; ++i) {
+      const int kind = kind_ab[3 * i], a = kind_ab[3 * i + 1], b = kind_ab[3 * i + 2];
+      const bool ok = kind == 0 ? (a >= 0 && a < c.soup_verts && b >= 0 && b < c.soup_tris)
+                                : (kind == 1 && a >= 0 && a < nedges && b >= 0 && b < nedges);
+      if (!ok) throw Error(WEFT_ERR_DIMENSION, "build_zones: impact " + std::to_string(i) + " out of range");
+      keys[static_cast<size_t>(i)] = (static_cast<unsigned long long>(kind) << 62) |
+                                     (static_cast<unsigned long long>(a) << 31) | static_cast<unsigned long long>(b);
+    }
+    weft_gpu::DBuf<unsigned long long>& kd = c.zn_tmp_keys;
+    kd.upload(keys.data(), keys.size(), c.stream);
+    weft_gpu::DBuf<double> vd;  // weights do not change the zone structure
+    vd.resize(8 * static_cast<size_t>(n) + 8);
+    vd.zero(c.stream);
+    const int32_t nz = weft_gpu::build_zones(c, kd.data(), vd.data(), n);
+    if (impact_zone) weft_gpu::download_zones(c, n, impact_zone, nullptr, nullptr);
+    WG_CUDA(cudaStreamSynchronize(c.stream));
+    if (zone_count) *zone_count = nz;
+    if (vertex_total) *vertex_total = c.zn_nzv;
+  });
+}
+
+weft_status weft_gpu_zone_vertices(weft_gpu_ctx* ctx, int32_t* vert_off, int32_t* verts) {
+  return guard2(ctx, [&](Ctx& c) { weft_gpu::download_zones(c, 0, nullptr, vert_off, verts); });
+}
+
+weft_status weft_distribute_zones(int32_t zone_count, const int32_t* sizes, int32_t devices, int32_t* device_of) {
+  if (zone_count < 0 || devices < 1 || (zone_count > 0 && (!sizes || !device_of))) return WEFT_ERR_INVALID;
+  const std::vector<int> sz(sizes, sizes + zone_count);
+  const auto asg = weft_gpu::distribute_zones(sz, devices);
+  for (int d = 0; d < devices; ++d)
+    for (int z : asg[static_cast<size_t>(d)]) device_of[z] = d;
+  return WEFT_OK;
+}
+
+weft_status weft_gpu_resolve_zones(weft_gpu_ctx* ctx, const double* x_begin, double* x_candidate,
+                                   const double* vertex_mass, double thickness, double cell_scale,
+                                   const weft_zone_params* params, weft_zone_report* report) {
+  return guard2(ctx, [&](Ctx& c) {
+    if (!x_begin || !x_candidate || !vertex_mass || !params) throw Error(WEFT_ERR_INVALID, "resolve_zones: NULL argument");
+    const size_t n = 3 * static_cast<size_t>(c.soup_verts);
+    weft_gpu::upload_vec(c, c.x_cur, x_begin, n);
+    weft_gpu::upload_vec(c, c.x_adv, x_candidate, n);
+    weft_gpu::upload_vec(c, c.vel, vertex_mass, static_cast<size_t>(c.soup_verts));
+    weft_zone_report rep{};
+    // like the reference, x_candidate holds the positions reached even when
+    // ZoneFailure is raised (resolve_zones mutates it in place)
+    auto copy_back = [&]() {
+      WG_CUDA(cudaMemcpyAsync(x_candidate, c.x_adv.data(), n * sizeof(double), cudaMemcpyDefault, c.stream));
+      WG_CUDA(cudaStreamSynchronize(c.stream));
+    };
+    try {
+      weft_gpu::resolve_zones(c, c.x_cur.data(), c.x_adv.data(), c.vel.data(), thickness, cell_scale, *params, rep,
+                              false);
+    } catch (const Error& e) {
+      if (report) *report = rep;
+      if (e.status == WEFT_ERR_ZONE) copy_back();
+      throw;
+    }
+    copy_back();
+    if (report) *report = rep;
+  });
+}
+
 weft_status weft_gpu_grid_info(weft_gpu_ctx* ctx, weft_grid_info* info) {
   return guard2(ctx, [&](Ctx& c) {
     if (!c.has_grid) throw Error(WEFT_ERR_INVALID, "grid_info: build_grid first");
@@ -296,14 +366,29 @@ weft_status weft_gpu_sim_step(weft_gpu_ctx* ctx, const weft_sim_params* prm, wef
     weft_gpu::build_grid(c, c.sim_x.data(), c.sim_xc.data(), WEFT_CONTINUOUS, prm->thickness, prm->cell_scale);
     share(c.grid_total, wb, we);
     int64_t ccd = 0;
-    if (contacts) {  // impacts found, not resolved (impact zones are out of scope)
+    weft_zone_report zr{};
+    float tz = 0;
+    if (contacts) {
       nimp = weft_gpu::narrow_phase(c, c.sim_x.data(), c.sim_xc.data(), WEFT_CONTINUOUS, prm->thickness, wb, we);
       ccd = c.narrow_pairs;
+      if (prm->zones) {
+        // 5-6. resolve_zones (driver.cpp:181-191): its first CCD round is
+        // the collide above; 7. the commit's velocity correction (:195-204)
+        WG_CUDA(cudaEventRecord(c.ev_side[2], s));
+        c.zn_pre.resize(static_cast<size_t>(n));
+        WG_CUDA(cudaMemcpyAsync(c.zn_pre.data(), c.sim_xc.data(), n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+        weft_gpu::resolve_zones(c, c.sim_x.data(), c.sim_xc.data(), c.mass.data(), prm->thickness, prm->cell_scale,
+                                prm->zone, zr, /*have_first=*/true);
+        weft_gpu::zone_commit(c, c.sim_xc.data(), c.zn_pre.data(), dt, c.sim_v.data());
+        WG_CUDA(cudaEventRecord(c.ev_side[3], s));
+        WG_CUDA(cudaEventSynchronize(c.ev_side[3]));
+        cudaEventElapsedTime(&tz, c.ev_side[2], c.ev_side[3]);
+      }
     } else {
       ccd = weft_gpu::candidates(c, wb, we, nullptr, /*count_only=*/true);
     }
     WG_CUDA(cudaEventRecord(ev[5], s));
-    // 7. commit (no zone correction in this tier)
+    // 7. commit
     std::swap(c.sim_x.ptr, c.sim_xc.ptr);
     std::swap(c.sim_x.cap, c.sim_xc.cap);
     WG_CUDA(cudaEventSynchronize(ev[5]));
@@ -324,6 +409,9 @@ weft_status weft_gpu_sim_step(weft_gpu_ctx* ctx, const weft_sim_params* prm, wef
       rep->proximities = nprox;
       rep->contact_elements = ncont;
       rep->impacts = nimp;
+      rep->zone_count = zr.zone_count;
+      rep->zone_outer = zr.outer_iterations;
+      rep->ms_zones = tz;
     }
   });
 }

@@ -64,7 +64,12 @@ class ScheduleError(Error):
     pass
 
 
-_ERRORS = {1: DimensionError, 2: SolverError, 3: ExecError, 4: TopologyError, 5: ScheduleError, 6: Error}
+class ZoneFailure(Error):
+    """weft::ZoneFailure (response.hpp:8-11)."""
+
+
+_ERRORS = {1: DimensionError, 2: SolverError, 3: ExecError, 4: TopologyError, 5: ScheduleError, 6: Error,
+           7: ZoneFailure}
 
 
 class Options(C.Structure):
@@ -132,24 +137,52 @@ class GridInfo(C.Structure):
     _fields_ = [("cell_size", C.c_double), ("cells", C.c_int64), ("entries", C.c_int64), ("total", C.c_int64)]
 
 
+class ZoneParams(C.Structure):
+    """ZoneSolveParams (response.hpp:46-60), the reference's defaults."""
+    _fields_ = [("clearance", C.c_double), ("initial_penalty", C.c_double), ("inner_tolerance", C.c_double),
+                ("al_iterations", C.c_int32), ("inner_iterations", C.c_int32), ("outer_cap", C.c_int32),
+                ("retry_cap", C.c_int32), ("max_correction_factor", C.c_double)]
+
+    def __init__(self, clearance=0.0025, initial_penalty=10.0, inner_tolerance=1e-8, al_iterations=25,
+                 inner_iterations=64, outer_cap=10, retry_cap=3, max_correction_factor=8.0):
+        super().__init__(clearance, initial_penalty, inner_tolerance, al_iterations, inner_iterations, outer_cap,
+                         retry_cap, max_correction_factor)
+
+    def as_array(self):
+        return np.array([self.clearance, self.initial_penalty, self.inner_tolerance, self.al_iterations,
+                         self.inner_iterations, self.outer_cap, self.retry_cap, self.max_correction_factor])
+
+
+class ZoneReport(C.Structure):
+    """ZoneResolveReport (response.hpp:62-68)."""
+    _fields_ = [("outer_iterations", C.c_int32), ("zone_count", C.c_int32), ("max_zone_vertices", C.c_int32),
+                ("impacts_resolved", C.c_int64), ("first_round_impacts", C.c_int64)]
+
+
 class SimParams(C.Structure):
     _fields_ = [("dt", C.c_double), ("thickness", C.c_double), ("cell_scale", C.c_double), ("pcg", PcgConfig),
                 ("jac_mode", C.c_int32), ("contacts", C.c_int32), ("stiffness_scale", C.c_double),
-                ("friction", C.c_double), ("contact_damping", C.c_double)]
+                ("friction", C.c_double), ("contact_damping", C.c_double), ("zones", C.c_int32),
+                ("zone", ZoneParams)]
 
     def __init__(self, dt=1.0 / 240.0, thickness=0.005, cell_scale=1.5, pcg=None, jac_mode=1, contacts=0,
-                 stiffness_scale=4.0, friction=0.2, contact_damping=0.0):
-        """SimConfig subset (driver.hpp:30-45): collision and ContactParams
-        (response.hpp:13-21) defaults of the reference."""
+                 stiffness_scale=4.0, friction=0.2, contact_damping=0.0, zones=0, zone=None):
+        """SimConfig subset (driver.hpp:30-45): collision, ContactParams
+        (response.hpp:13-21) and ZoneSolveParams defaults of the reference;
+        the zone clearance follows Simulator's rule clearance_fraction (0.5) *
+        thickness (driver.cpp:87-89) unless `zone` is given."""
+        if zone is None:
+            zone = ZoneParams(clearance=0.5 * thickness)
         super().__init__(dt, thickness, cell_scale, pcg if pcg is not None else PcgConfig(), jac_mode, contacts,
-                         stiffness_scale, friction, contact_damping)
+                         stiffness_scale, friction, contact_damping, zones, zone)
 
 
 class StepReport(C.Structure):
     _fields_ = [("pcg_iterations", C.c_int32), ("pcg_converged", C.c_int32), ("pcg_residual", C.c_double),
                 ("dcd_candidates", C.c_int64), ("ccd_candidates", C.c_int64), ("ms_broad", C.c_double),
                 ("ms_assemble", C.c_double), ("ms_solve", C.c_double), ("proximities", C.c_int64),
-                ("contact_elements", C.c_int64), ("impacts", C.c_int64)]
+                ("contact_elements", C.c_int64), ("impacts", C.c_int64), ("zone_count", C.c_int32),
+                ("zone_outer", C.c_int32), ("ms_zones", C.c_double)]
 
 
 def _load():
@@ -204,6 +237,18 @@ def generate_work_queues(devices: int):
     _check(LIB.weft_work_queues(C.c_int32(devices), _ptr(peer), _ptr(vec)))
     return [list(zip(peer[d * (devices - 1):(d + 1) * (devices - 1)].tolist(),
                      vec[d * (devices - 1):(d + 1) * (devices - 1)].tolist())) for d in range(devices)]
+
+
+def distribute_zones(sizes, devices: int):
+    """distribute_zones (response.cpp:164-182) -> per device list of zone ids."""
+    sz = np.ascontiguousarray(sizes, np.int32)
+    dev = np.zeros(max(len(sz), 1), np.int32)
+    _check(LIB.weft_distribute_zones(C.c_int32(len(sz)), _ptr(sz), C.c_int32(devices), _ptr(dev)))
+    out = [[] for _ in range(devices)]
+    order = sorted(range(len(sz)), key=lambda z: -int(sz[z]))  # assignment order (stable)
+    for z in order:
+        out[int(dev[z])].append(z)
+    return out
 
 
 def split_workload(total: int, devices: int):
@@ -439,6 +484,38 @@ class Engine:
         vals = np.zeros((max(n.value, 1), 8))
         _check(LIB.weft_gpu_download_contacts(self._ctx, _ptr(kab), _ptr(vals)))
         return kab[: n.value], vals[: n.value]
+
+    # -- impact zones (response.cpp:108-400) --------------------------------
+    def build_zones(self, kab):
+        """build_zones (response.cpp:108-162) over (kind, a, b) impacts on
+        the soup -> (impact_zone (n,), list of per-zone movable vertices)."""
+        kab = np.ascontiguousarray(kab, np.int32).reshape(-1, 3)
+        n = len(kab)
+        iz = np.zeros(max(n, 1), np.int32)
+        nz = C.c_int32()
+        nv = C.c_int64()
+        _check(LIB.weft_gpu_build_zones(self._ctx, C.c_int64(n), _ptr(kab), _ptr(iz), C.byref(nz), C.byref(nv)))
+        off = np.zeros(nz.value + 1, np.int32)
+        verts = np.zeros(max(nv.value, 1), np.int32)
+        _check(LIB.weft_gpu_zone_vertices(self._ctx, _ptr(off), _ptr(verts)))
+        return iz[:n], [verts[off[z]:off[z + 1]].copy() for z in range(nz.value)]
+
+    def resolve_zones(self, x_begin, x_candidate, vertex_mass, thickness: float = 0.005, cell_scale: float = 1.5,
+                      params: "ZoneParams | None" = None):
+        """resolve_zones (response.cpp:338-400): returns (corrected
+        candidate positions, ZoneReport); raises ZoneFailure like the
+        reference (with .x_candidate = the positions it left behind)."""
+        xc = _f64(x_candidate).copy()
+        rep = ZoneReport()
+        prm = params if params is not None else ZoneParams()
+        try:
+            _check(LIB.weft_gpu_resolve_zones(self._ctx, _ptr(_f64(x_begin)), _ptr(xc), _ptr(_f64(vertex_mass)),
+                                              C.c_double(thickness), C.c_double(cell_scale), C.byref(prm),
+                                              C.byref(rep)))
+        except ZoneFailure as e:  # the positions reached, as the reference leaves them
+            e.x_candidate, e.report = xc, rep
+            raise
+        return xc, rep
 
     # -- device-resident step -----------------------------------------------
     def sim_set_state(self, x, v):

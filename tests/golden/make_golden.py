@@ -17,6 +17,31 @@ from oracle_bindings import CONTINUOUS, DISCRETE, JAC_EXACT, JAC_SPD, REF  # noq
 from problems import cloth_problem  # noqa: E402
 
 
+ZONE_REPORT = ("outer_iterations", "zone_count", "max_zone_vertices", "impacts_resolved", "first_round_impacts")
+# ("two", seed, side) | ("layered", layers, nx, seed, amplitude in grid spacings)
+ZONE_CASES = [("two", 52, 6), ("two", 41, 8), ("two", 43, 8), ("layered", 2, 10, 8, 0.6), ("layered", 2, 16, 3, 0.5),
+              ("layered", 3, 12, 5, 0.4), ("layered", 3, 30, 2, 0.6)]
+
+
+def zone_case(case):
+    """Inputs of a resolve_zones case: nv, tris, x_begin, x_candidate, mass,
+    movable, thickness, the 8 ZoneSolveParams values."""
+    if case[0] == "two":
+        nv, tris, x0, x1 = REF.two_cloth_scene(case[1], case[2])
+        # test_response.cpp:218-240: mass 0.05, default parameters
+        return nv, tris, x0, x1, np.full(nv, 0.05), np.ones(nv, np.uint8), 0.005, [0.0025, 10.0, 1e-8, 25, 64, 10, 3,
+                                                                                  8.0]
+    sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+    from paper_2008_00409_b200 import scenes
+    _, layers, nx, seed, amp = case
+    sc = scenes.layered_cloth(layers, nx, seed=seed)
+    x0 = sc.verts.reshape(-1).copy()
+    x1 = x0 + np.random.default_rng(4).uniform(-amp, amp, x0.shape) * sc.spacing
+    nv = len(sc.verts)
+    return (nv, sc.tris, x0, x1, np.full(nv, 1e-3), (1 - sc.pinned).astype(np.uint8), sc.thickness,
+            [0.5 * sc.thickness, 10.0, 1e-8, 25, 64, 10, 3, 8.0])
+
+
 def main():
     assert REF is not None, "oracle/_ref/libweft_ref.so missing: make -C oracle ref"
     # assembly: random_cloth problems (test_assembly.cpp:55-71 recipe) with
@@ -66,6 +91,15 @@ def main():
                             x1=x1, mode=np.array(mode), thickness=np.array(2 * sc.thickness), movable=mv, kab=kab,
                             vals=vals)
         k += 1
+    # impact zones: resolve_zones (response.cpp:338-400) on random_two_cloth_scene
+    # (ZoneFailure cases: the positions left behind and the message are pinned
+    # too) and on pinned layered cloths with a perturbed candidate.
+    for k, case in enumerate(ZONE_CASES):
+        nv, tris, x0, x1, mass, mv, th, zp = zone_case(case)
+        st, msg, xc, rep = REF.resolve_zones(nv, tris, mass, x0, x1, thickness=th, devices=2, params=zp, movable=mv)
+        np.savez_compressed(os.path.join(HERE, f"zones_{k}.npz"), nv=np.array(nv), tris=tris, x0=x0, x1=x1,
+                            mass=mass, movable=mv, thickness=np.array(th), params=np.asarray(zp), status=np.array(st),
+                            message=np.array(msg), x_out=xc, report=np.array([rep[f] for f in ZONE_REPORT]))
     # SpMV: oracle::random_bell (sparse_oracle.cpp:7-23), pipelined at n = 1, 2, 4.
     for k, (seed, rows) in enumerate([(5, 7), (6, 40)]):
         s = REF.random_bell(seed, rows, 3)

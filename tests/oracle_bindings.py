@@ -405,6 +405,41 @@ class Ref:
         self.lib.ref_collide(*args, C.c_int64(n), ptr(kab), ptr(vals))
         return kab[:n], vals[:n]
 
+    def build_zones(self, vertex_count, tris, kab, movable=None):
+        """build_zones (response.cpp:108-162) -> (impact_zone, per-zone vertex lists)."""
+        tris = np.ascontiguousarray(tris, np.int32)
+        kab = np.ascontiguousarray(kab, np.int32).reshape(-1, 3)
+        mv = None if movable is None else np.ascontiguousarray(movable, np.uint8)
+        n = len(kab)
+        iz = np.zeros(max(n, 1), np.int32)
+        cap_off, cap_v = n + 1, 4 * n + 1
+        off = np.zeros(cap_off, np.int32)
+        verts = np.zeros(cap_v, np.int32)
+        nz = self.lib.ref_build_zones(C.c_int32(vertex_count), C.c_int32(len(tris)), ptr(tris), ptr(mv),
+                                      C.c_int64(n), ptr(kab), ptr(iz), C.c_int64(cap_off), ptr(off),
+                                      C.c_int64(cap_v), ptr(verts))
+        if nz < 0:
+            raise RuntimeError(self.lib.ref_last_error().decode())
+        return iz[:n], [verts[off[z]:off[z + 1]].copy() for z in range(nz)]
+
+    def resolve_zones(self, vertex_count, tris, mass, x_begin, x_cand, thickness=0.005, cell_scale=1.5,
+                      devices=2, params=None, movable=None):
+        """resolve_zones (response.cpp:338-400) -> (status, message, corrected
+        candidate, report dict). params: the 8 ZoneSolveParams values."""
+        tris = np.ascontiguousarray(tris, np.int32)
+        mv = None if movable is None else np.ascontiguousarray(movable, np.uint8)
+        xc = np.ascontiguousarray(x_cand, np.float64).reshape(-1).copy()
+        zp = np.asarray(params if params is not None else [0.0025, 10.0, 1e-8, 25, 64, 10, 3, 8.0], np.float64)
+        rep = np.zeros(5, np.int64)
+        st = self.lib.ref_resolve_zones(C.c_int32(vertex_count), C.c_int32(len(tris)), ptr(tris), ptr(mv),
+                                        ptr(np.ascontiguousarray(mass, np.float64)),
+                                        ptr(np.ascontiguousarray(x_begin, np.float64).reshape(-1)), ptr(xc),
+                                        C.c_double(thickness), C.c_double(cell_scale), C.c_int32(devices), ptr(zp),
+                                        ptr(rep))
+        msg = self.lib.ref_last_error().decode() if st else ""
+        keys = ("outer_iterations", "zone_count", "max_zone_vertices", "impacts_resolved", "first_round_impacts")
+        return st, msg, xc, dict(zip(keys, rep.tolist()))
+
     def two_cloth_scene(self, seed, max_side):
         tc = C.c_int32()
         nv = self.lib.ref_two_cloth_scene(C.c_uint64(seed), C.c_int32(max_side), C.byref(tc), None, None, None)
@@ -417,6 +452,12 @@ class Ref:
 
 ORACLE = Oracle() if os.path.exists(ORACLE_SO) else None
 REF = Ref() if os.path.exists(REF_SO) else None
+
+
+class RefError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(msg)
+        self.status = status
 
 
 class RefSim:
@@ -460,16 +501,21 @@ class RefSim:
         return dict(zip(keys, out.tolist()))
 
     def step_contacts(self, dt, thickness, cell_scale=1.5, tol=1e-4, max_it=400, stiffness_scale=4.0,
-                      friction=0.2, damping=0.0):
-        """Simulator::step_impl without impact zones (ref_sim_step_contacts)."""
+                      friction=0.2, damping=0.0, zones=None):
+        """Simulator::step_impl (ref_sim_step_contacts): without impact
+        zones, or with them when `zones` = the 8 zone parameters
+        (ref_resolve_zones order)."""
         L = self.ref.lib
         L.ref_sim_step_contacts.restype = C.c_int32
-        prm = np.array([dt, thickness, cell_scale, tol, max_it, stiffness_scale, friction, damping], np.float64)
+        zp = np.zeros(8) if zones is None else np.asarray(zones, np.float64)
+        prm = np.concatenate([[dt, thickness, cell_scale, tol, max_it, stiffness_scale, friction, damping,
+                               0.0 if zones is None else 1.0], zp])
         out = np.zeros(8)
         st = L.ref_sim_step_contacts(C.c_void_p(self.h), ptr(prm), ptr(out))
         if st:
-            raise RuntimeError(L.ref_last_error().decode())
-        keys = ("pcg_iterations", "pcg_converged", "pcg_residual", "proximities", "contacts", "impacts")
+            raise RefError(st, L.ref_last_error().decode())
+        keys = ("pcg_iterations", "pcg_converged", "pcg_residual", "proximities", "contacts", "impacts",
+                "zone_count", "zone_outer")
         return dict(zip(keys, out.tolist()))
 
     def close(self):
