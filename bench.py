@@ -203,6 +203,75 @@ def reference_arm(args, rank, world):
     print(json.dumps(out), flush=True)
 
 
+# ---------------------------------------------------------------- zones
+ZONE_SCENE = (3, 160, 0.1, 0.8)  # layers, nx, fraction of vertices perturbed, amplitude (grid spacings)
+
+
+def zone_case(seed: int = 7):
+    """A resolve_zones workload: a pinned layered cloth whose candidate
+    positions push a random subset of vertices through their neighbours."""
+    import numpy as np
+    from paper_2008_00409_b200 import scenes
+    layers, nx, frac, amp = ZONE_SCENE
+    sc = scenes.layered_cloth(layers, nx, seed=seed)
+    rng = np.random.default_rng(seed)
+    x0 = sc.verts.reshape(-1).copy()
+    x1 = x0.copy()
+    pick = rng.random(len(sc.verts)) < frac
+    d = rng.uniform(-amp, amp, (len(sc.verts), 3)) * sc.spacing
+    x1.reshape(-1, 3)[pick] += d[pick]
+    mv = (1 - sc.pinned).astype(np.uint8)
+    mass = np.full(len(sc.verts), 1e-3)
+    return sc, x0, x1, mv, mass
+
+
+def zone_bench(weft, stream, with_ref: bool):
+    """Impact zones: resolve_zones (CCD rounds + zone
+    solves) on the GPU vs the compiled reference on the same input; both
+    outputs must be bitwise equal."""
+    import numpy as np
+    import torch
+    sc, x0, x1, mv, mass = zone_case()
+    prm = weft.ZoneParams(clearance=0.5 * sc.thickness)
+    out = {"workload": f"{ZONE_SCENE[0]} x {ZONE_SCENE[1]}^2 layered cloth ({sc.tri_count} tris), "
+                       f"{ZONE_SCENE[2]:.0%} of the vertices displaced by up to {ZONE_SCENE[3]} grid spacings"}
+    with weft.Engine(1) as eng:
+        eng.set_soup(len(sc.verts), sc.tris)
+        eng.set_soup_movable(mv)
+        times, res = [], None
+        for k in range(4):
+            t0 = torch.cuda.Event(enable_timing=True)
+            t1 = torch.cuda.Event(enable_timing=True)
+            t0.record(stream)
+            try:
+                res = eng.resolve_zones(x0, x1, mass, sc.thickness, 1.5, prm)
+            except weft.ZoneFailure as e:
+                res = (e.x_candidate, e.report)
+                out["zone_failure"] = str(e)[:120]
+            t1.record(stream)
+            t1.synchronize()
+            if k:
+                times.append(t0.elapsed_time(t1))
+        xc, rep = res
+        out.update({"gpu_ms": statistics.median(times), "first_round_impacts": rep.first_round_impacts,
+                    "outer_iterations": rep.outer_iterations, "zones": rep.zone_count,
+                    "max_zone_vertices": rep.max_zone_vertices,
+                    "note": "weft_gpu_resolve_zones incl. its CCD rounds and host<->device copies of the positions; "
+                            "median of 3 after one warm-up"})
+    if with_ref:
+        sys.path.insert(0, os.path.join(ROOT, "tests"))
+        from oracle_bindings import REF
+        if REF is not None:
+            devices, _ = ref_devices()
+            t = time.perf_counter()
+            st, msg, rx, rrep = REF.resolve_zones(len(sc.verts), sc.tris, mass, x0, x1, thickness=sc.thickness,
+                                                  devices=devices, params=prm.as_array(), movable=mv)
+            out["reference_ms"] = 1e3 * (time.perf_counter() - t)
+            out["reference_devices"] = devices
+            out["bitwise_equal"] = bool(np.array_equal(rx, xc))
+    return out
+
+
 # ---------------------------------------------------------------- GPU arm
 def gpu_arm(args, rank, world, local):
     import numpy as np
@@ -354,7 +423,7 @@ def gpu_arm(args, rank, world, local):
     full = None
     if world == 1 and not args.no_narrow:
         fp = weft.SimParams(sc.dt, sc.thickness, 1.5, weft.PcgConfig(1e-4, 400, weft.PRECOND_BLOCK_JACOBI),
-                            weft.JAC_SPD, contacts=1)
+                            weft.JAC_SPD, contacts=1, zones=1)
         ftimes, frep = [], None
         try:
             for k in range(4):
@@ -369,14 +438,19 @@ def gpu_arm(args, rank, world, local):
                     ftimes.append(f0.elapsed_time(f1))
             full = {"ms": statistics.median(ftimes), "steps_per_s": 1e3 / statistics.median(ftimes),
                     "proximities": frep.proximities, "contact_elements": frep.contact_elements,
-                    "impacts": frep.impacts, "pcg_iterations": frep.pcg_iterations,
+                    "impacts": frep.impacts, "zones": frep.zone_count, "pcg_iterations": frep.pcg_iterations,
                     "stage_ms": {"broad_and_narrow": frep.ms_broad, "contacts_and_assemble": frep.ms_assemble,
-                                 "solve": frep.ms_solve},
-                    "note": "weft_gpu_sim_step(contacts=1) on the replayed state: Simulator::step_impl "
-                            "(driver.cpp:96-215) without impact-zone resolution, device-resident; median of 3"}
+                                 "solve": frep.ms_solve, "zones": frep.ms_zones},
+                    "note": "weft_gpu_sim_step(contacts=1, zones=1) on the replayed state: the whole "
+                            "Simulator::step_impl (driver.cpp:96-215) incl. resolve_zones, device-resident; "
+                            "median of 3"}
         except weft.Error as e:
             full = {"error": str(e)}
         eng.sim_step(params)  # back to the hot-path step (drops the contacts)
+
+    zones = None
+    if world == 1 and not args.no_narrow:
+        zones = zone_bench(weft, stream, not args.no_cpu_baseline)
 
     # candidate counts: each rank walks its split_workload share
     dcd_total = int(reduce_over_ranks(float(reps[-1].dcd_candidates), dist.ReduceOp.SUM if world > 1 else None))
@@ -436,6 +510,7 @@ def gpu_arm(args, rank, world, local):
             "gpu_launches_per_step": launches / args.steps,
             "narrow_phase": narrow,
             "full_step_contacts": full,
+            "impact_zones": zones,
         },
         "roofline": {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "alg_bytes_per_launch": alg_bytes,

@@ -1010,11 +1010,68 @@ constexpr int kPersistThreads = 256;
 #ifndef WEFT_PERSIST_MINB
 #define WEFT_PERSIST_MINB 2  // 16 warps/SM, no spills (measured best on B200 vs 3-6)
 #endif
+// L2 eviction priorities of the persistent kernel: the matrix (streamed
+// once per iteration, 0.69 GB at config D) and phase B's own-row streams (r,
+// x, D^-1) are loaded with an L2 evict_first policy, the z / p gathers with
+// evict_last, so the gathered vectors stay resident in the 126 MB L2 while
+// the matrix streams past them. Measured on B200, config D: 200 -> 168 us per
+// PCG iteration together with WEFT_PK_UNROLL 1 (tools/pcg_ab.py; knobs:
+// WEFT_MAT_EF, WEFT_VEC_EL, WEFT_PB_EF, WEFT_ZP_ST_EL = also store z / p
+// with evict_last, measured equal).
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+  uint64_t pol;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+  uint64_t pol;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ double ld_nc_hint(const double* p, uint64_t pol) {
+  double v;
+  asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ int ld_nc_hint(const int* p, uint64_t pol) {
+  int v;
+  asm volatile("ld.global.nc.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ double ld_cg_hint(const double* p, uint64_t pol) {
+  double v;
+  asm volatile("ld.global.cg.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void st_cg_hint(double* p, double v, uint64_t pol) {
+  asm volatile("st.global.cg.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
+}
+#ifndef WEFT_ZP_ST_EL
+#define WEFT_ZP_ST_EL 0  // phase A/B stores of p and z (gathered next phase A) with evict_last
+#endif
+#ifndef WEFT_PB_EF
+#define WEFT_PB_EF 1  // phase B streams (r, x, D^-1) with evict_first
+#endif
+#ifndef WEFT_MAT_EF
+#define WEFT_MAT_EF 1
+#endif
+#ifndef WEFT_VEC_EL
+#define WEFT_VEC_EL 1
+#endif
 #ifndef WEFT_MAT_LD
+#if WEFT_MAT_EF
+#define WEFT_MAT_LD(p) ld_nc_hint(p, mpol)
+#else
 #define WEFT_MAT_LD(p) __ldg(p)
 #endif
+#endif
+#if WEFT_VEC_EL
+#define WEFT_VEC_LD(p) ld_cg_hint(p, vpol)
+#else
+#define WEFT_VEC_LD(p) __ldcg(p)
+#endif
 #ifndef WEFT_PK_UNROLL
-#define WEFT_PK_UNROLL 2
+#define WEFT_PK_UNROLL 1
 #endif
 constexpr int kPkUnroll = WEFT_PK_UNROLL;
 #ifndef WEFT_PK_PREFETCH
@@ -1028,6 +1085,12 @@ template <int PMode>
 __device__ __forceinline__ void row_product_cg(const SellView& A, int r, const double* __restrict__ z,
                                                const double* __restrict__ pold, double beta, double& y0, double& y1,
                                                double& y2) {
+#if WEFT_MAT_EF
+  const uint64_t mpol = l2_policy_evict_first();
+#endif
+#if WEFT_VEC_EL
+  const uint64_t vpol = l2_policy_evict_last();
+#endif
   const int len = A.rowlen[r];
   const int64_t base = A.slice_off[r >> 5] + (r & 31);
   double a0 = 0.0, a1 = 0.0, a2 = 0.0;
@@ -1041,11 +1104,11 @@ __device__ __forceinline__ void row_product_cg(const SellView& A, int r, const d
     const double v0 = WEFT_MAT_LD(v), v1 = WEFT_MAT_LD(v + 32), v2 = WEFT_MAT_LD(v + 64);
     const double v3 = WEFT_MAT_LD(v + 96), v4 = WEFT_MAT_LD(v + 128), v5 = WEFT_MAT_LD(v + 160);
     const double v6 = WEFT_MAT_LD(v + 192), v7 = WEFT_MAT_LD(v + 224), v8 = WEFT_MAT_LD(v + 256);
-    double x0 = __ldcg(z + 3 * c), x1 = __ldcg(z + 3 * c + 1), x2 = __ldcg(z + 3 * c + 2);
+    double x0 = WEFT_VEC_LD(z + 3 * c), x1 = WEFT_VEC_LD(z + 3 * c + 1), x2 = WEFT_VEC_LD(z + 3 * c + 2);
     if (PMode == 2) {
-      x0 = x0 + beta * __ldcg(pold + 3 * c);
-      x1 = x1 + beta * __ldcg(pold + 3 * c + 1);
-      x2 = x2 + beta * __ldcg(pold + 3 * c + 2);
+      x0 = x0 + beta * WEFT_VEC_LD(pold + 3 * c);
+      x1 = x1 + beta * WEFT_VEC_LD(pold + 3 * c + 1);
+      x2 = x2 + beta * WEFT_VEC_LD(pold + 3 * c + 2);
     }
     a0 = a0 + ((v0 * x0 + v1 * x1) + v2 * x2);
     a1 = a1 + ((v3 * x0 + v4 * x1) + v5 * x2);
@@ -1120,6 +1183,15 @@ __global__ void __launch_bounds__(kPersistThreads, WEFT_PERSIST_MINB) k_pcg_pers
   const int sl_begin = static_cast<int>((static_cast<int64_t>(gw) * nslices) / tw);
   const int sl_end = static_cast<int>((static_cast<int64_t>(gw + 1) * nslices) / tw);
   double* const qw = q_s + static_cast<size_t>(threadIdx.x >> 5) * g.q_msw * 96 + lane;  // kQs: this warp's rows
+#if WEFT_ZP_ST_EL
+  const uint64_t elpol = l2_policy_evict_last();
+#endif
+#if WEFT_PB_EF
+  const uint64_t efpol = l2_policy_evict_first();
+#define PB_LD(p) ld_cg_hint(p, efpol)
+#else
+#define PB_LD(p) __ldcg(p)
+#endif
   while (!done) {
     // ---- phase A: q = A p, p of the own rows, p.q
     unsigned long long tm0 = 0;
@@ -1154,9 +1226,15 @@ __global__ void __launch_bounds__(kPersistThreads, WEFT_PERSIST_MINB) k_pcg_pers
           __stcg(q + 3 * i + 1, y1);
           __stcg(q + 3 * i + 2, y2);
         }
+#if WEFT_ZP_ST_EL
+        st_cg_hint(pnew + 3 * i, p0, elpol);
+        st_cg_hint(pnew + 3 * i + 1, p1, elpol);
+        st_cg_hint(pnew + 3 * i + 2, p2, elpol);
+#else
         __stcg(pnew + 3 * i, p0);
         __stcg(pnew + 3 * i + 1, p1);
         __stcg(pnew + 3 * i + 2, p2);
+#endif
         s1[0] = s1[0] + ((p0 * y0 + p1 * y1) + p2 * y2);
       }
     }
@@ -1200,14 +1278,14 @@ __global__ void __launch_bounds__(kPersistThreads, WEFT_PERSIST_MINB) k_pcg_pers
       for (int c = 0; c < 3; ++c) {
         if constexpr (kQs) qv[c] = qw[((i - lane) / kSlice - sl_begin) * 96 + 32 * c];
         else qv[c] = __ldcg(q + 3 * i + c);
-        rv[c] = __ldcg(r + 3 * i + c);
+        rv[c] = PB_LD(r + 3 * i + c);
       }
       if (x_now) {
         double xv[3], pv[3];
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
           pv[c] = __ldcg(pnew + 3 * i + c);
-          xv[c] = __ldcg(x + 3 * i + c);
+          xv[c] = PB_LD(x + 3 * i + c);
         }
         if (WEFT_PK_XDEFER) {
 #pragma unroll
@@ -1219,12 +1297,21 @@ __global__ void __launch_bounds__(kPersistThreads, WEFT_PERSIST_MINB) k_pcg_pers
       if (bj) {
         if (g.dinv6) {  // bitwise-symmetric inverses: 48 instead of 72 bytes per row
           const double* h = g.dinv6 + 6 * (size_t)i;
+#if WEFT_PB_EF
+          m[0] = ld_nc_hint(h, efpol);
+          m[1] = m[3] = ld_nc_hint(h + 1, efpol);
+          m[2] = m[6] = ld_nc_hint(h + 2, efpol);
+          m[4] = ld_nc_hint(h + 3, efpol);
+          m[5] = m[7] = ld_nc_hint(h + 4, efpol);
+          m[8] = ld_nc_hint(h + 5, efpol);
+#else
           m[0] = __ldg(h);
           m[1] = m[3] = __ldg(h + 1);
           m[2] = m[6] = __ldg(h + 2);
           m[4] = __ldg(h + 3);
           m[5] = m[7] = __ldg(h + 4);
           m[8] = __ldg(h + 5);
+#endif
         } else {
 #pragma unroll
           for (int k = 0; k < 9; ++k) m[k] = __ldg(dinv + 9 * (size_t)i + k);
@@ -1244,9 +1331,15 @@ __global__ void __launch_bounds__(kPersistThreads, WEFT_PERSIST_MINB) k_pcg_pers
       }
 #pragma unroll
       for (int c = 0; c < 3; ++c) __stcg(r + 3 * i + c, rv[c]);
+#if WEFT_ZP_ST_EL
+      st_cg_hint(z + 3 * i, z0, elpol);
+      st_cg_hint(z + 3 * i + 1, z1, elpol);
+      st_cg_hint(z + 3 * i + 2, z2, elpol);
+#else
       __stcg(z + 3 * i, z0);
       __stcg(z + 3 * i + 1, z1);
       __stcg(z + 3 * i + 2, z2);
+#endif
       s2[0] = s2[0] + ((rv[0] * rv[0] + rv[1] * rv[1]) + rv[2] * rv[2]);
       s2[1] = s2[1] + ((rv[0] * z0 + rv[1] * z1) + rv[2] * z2);
     }
