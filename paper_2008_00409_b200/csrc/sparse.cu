@@ -77,6 +77,60 @@ __device__ __forceinline__ int block_part(const PartBlocks& pb, int b) {
   return d;
 }
 
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+  uint64_t pol;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+  uint64_t pol;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ double ld_nc_hint(const double* p, uint64_t pol) {
+  double v;
+  asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ int ld_nc_hint(const int* p, uint64_t pol) {
+  int v;
+  asm volatile("ld.global.nc.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ double ld_cg_hint(const double* p, uint64_t pol) {
+  double v;
+  asm volatile("ld.global.cg.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void st_cg_hint(double* p, double v, uint64_t pol) {
+  asm volatile("st.global.cg.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ double ld_hint(const double* p, uint64_t pol) {
+  double v;
+  asm volatile("ld.global.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+}
+// Single-group row products of the multi-kernel path (k_spmv, k_pcg_spmv:
+// one partition, or the interior rows of a rank): the same L2 priorities as
+// the persistent kernel (matrix evict_first, gathered vector evict_last).
+// Measured on B200, config D, graph PCG: 259 -> 229 us per iteration; the
+// multi-group row product measured 3 % slower with them, so it keeps plain
+// loads (tools/pcg_ab.py, WEFT_SPMV_HINT=0 turns them off).
+#ifndef WEFT_SPMV_HINT
+#define WEFT_SPMV_HINT 1
+#endif
+#if WEFT_SPMV_HINT
+#define SP_POLICIES                                  \
+  const uint64_t mpol = l2_policy_evict_first(); \
+  const uint64_t vpol = l2_policy_evict_last();
+#define SP_MLD(p) ld_nc_hint(p, mpol)
+#define SP_XLD(p) ld_hint(p, vpol)
+#else
+#define SP_POLICIES
+#define SP_MLD(p) __ldg(p)
+#define SP_XLD(p) (*(p))
+#endif
+
 // ---------------------------------------------------------------------------
 // Row product in the reference order
 // ---------------------------------------------------------------------------
@@ -195,21 +249,22 @@ __device__ __forceinline__ void row_product_1(const SellView& A, int r, const do
   const int64_t base = A.slice_off[r >> 5] + (r & 31);
   const int64_t T = A.total;
   double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-  int cn = len > 0 ? (WEFT_LDS(A.cols + base) & kColMask) : 0;
+  SP_POLICIES
+  int cn = len > 0 ? (SP_MLD(A.cols + base) & kColMask) : 0;
 #pragma unroll 2
   for (int k = 0; k < len; ++k) {
     const int64_t at = base + (int64_t)k * kSlice;
     const int c = cn;
-    if (k + 1 < len) cn = WEFT_LDS(A.cols + at + kSlice) & kColMask;
+    if (k + 1 < len) cn = SP_MLD(A.cols + at + kSlice) & kColMask;
     const double* v = A.vals + vidx(at, r & 31, 0);
-    const double v0 = WEFT_LDS(v), v1 = WEFT_LDS(v + 32), v2 = WEFT_LDS(v + 64);
-    const double v3 = WEFT_LDS(v + 96), v4 = WEFT_LDS(v + 128), v5 = WEFT_LDS(v + 160);
-    const double v6 = WEFT_LDS(v + 192), v7 = WEFT_LDS(v + 224), v8 = WEFT_LDS(v + 256);
-    double x0 = x[3 * c], x1 = x[3 * c + 1], x2 = x[3 * c + 2];
+    const double v0 = SP_MLD(v), v1 = SP_MLD(v + 32), v2 = SP_MLD(v + 64);
+    const double v3 = SP_MLD(v + 96), v4 = SP_MLD(v + 128), v5 = SP_MLD(v + 160);
+    const double v6 = SP_MLD(v + 192), v7 = SP_MLD(v + 224), v8 = SP_MLD(v + 256);
+    double x0 = SP_XLD(x + 3 * c), x1 = SP_XLD(x + 3 * c + 1), x2 = SP_XLD(x + 3 * c + 2);
     if (PMode == 2) {
-      x0 = x0 + beta * pold[3 * c];
-      x1 = x1 + beta * pold[3 * c + 1];
-      x2 = x2 + beta * pold[3 * c + 2];
+      x0 = x0 + beta * SP_XLD(pold + 3 * c);
+      x1 = x1 + beta * SP_XLD(pold + 3 * c + 1);
+      x2 = x2 + beta * SP_XLD(pold + 3 * c + 2);
     }
     a0 = a0 + ((v0 * x0 + v1 * x1) + v2 * x2);
     a1 = a1 + ((v3 * x0 + v4 * x1) + v5 * x2);
@@ -1018,34 +1073,6 @@ constexpr int kPersistThreads = 256;
 // PCG iteration together with WEFT_PK_UNROLL 1 (tools/pcg_ab.py; knobs:
 // WEFT_MAT_EF, WEFT_VEC_EL, WEFT_PB_EF, WEFT_ZP_ST_EL = also store z / p
 // with evict_last, measured equal).
-__device__ __forceinline__ uint64_t l2_policy_evict_first() {
-  uint64_t pol;
-  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-  return pol;
-}
-__device__ __forceinline__ uint64_t l2_policy_evict_last() {
-  uint64_t pol;
-  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-  return pol;
-}
-__device__ __forceinline__ double ld_nc_hint(const double* p, uint64_t pol) {
-  double v;
-  asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
-  return v;
-}
-__device__ __forceinline__ int ld_nc_hint(const int* p, uint64_t pol) {
-  int v;
-  asm volatile("ld.global.nc.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
-  return v;
-}
-__device__ __forceinline__ double ld_cg_hint(const double* p, uint64_t pol) {
-  double v;
-  asm volatile("ld.global.cg.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
-  return v;
-}
-__device__ __forceinline__ void st_cg_hint(double* p, double v, uint64_t pol) {
-  asm volatile("st.global.cg.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
-}
 #ifndef WEFT_ZP_ST_EL
 #define WEFT_ZP_ST_EL 0  // phase A/B stores of p and z (gathered next phase A) with evict_last
 #endif

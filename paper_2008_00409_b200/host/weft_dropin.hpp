@@ -10,6 +10,7 @@
 // (the reference default, driver.hpp:35); float throws.
 #pragma once
 
+#include <algorithm>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -21,6 +22,7 @@
 
 #include "weft/assembly.hpp"
 #include "weft/collision.hpp"
+#include "weft/response.hpp"
 #include "weft/solver.hpp"
 #include "weft/sparse.hpp"
 #include "weft_gpu.h"
@@ -37,6 +39,7 @@ inline void check(weft_status s) {
     case WEFT_ERR_EXEC: throw ExecError(msg);
     case WEFT_ERR_TOPOLOGY: throw TopologyError(msg);
     case WEFT_ERR_SCHEDULE: throw ScheduleError(msg);
+    case WEFT_ERR_ZONE: throw ZoneFailure(msg);
     default: throw Error(msg);
   }
 }
@@ -314,6 +317,84 @@ inline NarrowPhaseResult collide(Engine& engine, const CollisionSoup& soup, std:
     if (ccd) out.impacts.push_back(Impact{kind, kab[3 * i + 1], kab[3 * i + 2], v[0], nrm, w});
     else out.proximities.push_back(Proximity{kind, kab[3 * i + 1], kab[3 * i + 2], v[0], nrm, w});
   }
+  return out;
+}
+
+inline void set_soup(weft_gpu_ctx* ctx, const CollisionSoup& soup) {
+  std::vector<int32_t> tris(3 * soup.triangles.size());
+  for (std::size_t t = 0; t < soup.triangles.size(); ++t)
+    for (int c = 0; c < 3; ++c) tris[3 * t + static_cast<std::size_t>(c)] = soup.triangles[t][static_cast<std::size_t>(c)];
+  check(weft_gpu_set_soup(ctx, soup.vertex_count, static_cast<int32_t>(soup.triangles.size()), tris.data()));
+  check(weft_gpu_set_soup_movable(ctx, soup.movable.data()));
+}
+
+// build_zones (response.cpp:108-162) on the GPU: same zones, same ids, same
+// impact lists and sorted movable vertex lists. Uses the context of Engine(1).
+inline std::vector<ImpactZone> build_zones(const std::vector<Impact>& impacts, const CollisionSoup& soup) {
+  weft_gpu_ctx* ctx = context_for(Engine(1)).get();
+  set_soup(ctx, soup);
+  const int64_t n = static_cast<int64_t>(impacts.size());
+  std::vector<int32_t> kab(3 * impacts.size() + 3), iz(impacts.size() + 1);
+  for (int64_t i = 0; i < n; ++i) {
+    kab[3 * i] = impacts[static_cast<std::size_t>(i)].kind == FeatureKind::VertexFace ? 0 : 1;
+    kab[3 * i + 1] = impacts[static_cast<std::size_t>(i)].a;
+    kab[3 * i + 2] = impacts[static_cast<std::size_t>(i)].b;
+  }
+  int32_t nz = 0;
+  int64_t nv = 0;
+  check(weft_gpu_build_zones(ctx, n, kab.data(), iz.data(), &nz, &nv));
+  std::vector<int32_t> off(static_cast<std::size_t>(nz) + 1), verts(static_cast<std::size_t>(nv) + 1);
+  check(weft_gpu_zone_vertices(ctx, off.data(), verts.data()));
+  std::vector<ImpactZone> zones(static_cast<std::size_t>(nz));
+  for (int32_t z = 0; z < nz; ++z) {
+    zones[static_cast<std::size_t>(z)].id = z;
+    zones[static_cast<std::size_t>(z)].vertices.assign(verts.begin() + off[static_cast<std::size_t>(z)],
+                                                        verts.begin() + off[static_cast<std::size_t>(z) + 1]);
+  }
+  for (int64_t i = 0; i < n; ++i) zones[static_cast<std::size_t>(iz[static_cast<std::size_t>(i)])].impacts.push_back(static_cast<int>(i));
+  return zones;
+}
+
+// distribute_zones (response.cpp:164-182).
+inline std::vector<std::vector<int>> distribute_zones(const std::vector<ImpactZone>& zones, int devices) {
+  std::vector<int32_t> sizes(zones.size() + 1), dev(zones.size() + 1);
+  for (std::size_t z = 0; z < zones.size(); ++z) sizes[z] = static_cast<int32_t>(zones[z].vertices.size());
+  check(weft_distribute_zones(static_cast<int32_t>(zones.size()), sizes.data(), devices, dev.data()));
+  // the assignment order of the greedy loop: descending size, stable
+  std::vector<int> order(zones.size());
+  for (std::size_t z = 0; z < zones.size(); ++z) order[z] = static_cast<int>(z);
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return sizes[static_cast<std::size_t>(a)] > sizes[static_cast<std::size_t>(b)]; });
+  std::vector<std::vector<int>> out(static_cast<std::size_t>(devices));
+  for (int z : order) out[static_cast<std::size_t>(dev[static_cast<std::size_t>(z)])].push_back(z);
+  return out;
+}
+
+// resolve_zones (response.cpp:338-400): CCD rounds and zone solves on the GPU;
+// x_candidate is updated in place (also when ZoneFailure is thrown, like the
+// reference). Bitwise the reference's positions and report.
+inline ZoneResolveReport resolve_zones(Engine& engine, const CollisionSoup& soup, std::span<const Vec3> x_begin,
+                                       std::vector<Vec3>& x_candidate, std::span<const double> vertex_mass,
+                                       const CollisionParams& cparams, const ZoneSolveParams& zparams,
+                                       CollideTimes* /*times*/ = nullptr) {
+  weft_gpu_ctx* ctx = context_for(engine).get();
+  set_soup(ctx, soup);
+  const auto xb = flat3(x_begin);
+  auto xc = flat3(x_candidate);
+  const weft_zone_params zp{zparams.clearance, zparams.initial_penalty, zparams.inner_tolerance,
+                            zparams.al_iterations, zparams.inner_iterations, zparams.outer_cap,
+                            zparams.retry_cap, zparams.max_correction_factor};
+  weft_zone_report rep{};
+  const weft_status st = weft_gpu_resolve_zones(ctx, xb.data(), xc.data(), vertex_mass.data(), cparams.thickness,
+                                                cparams.cell_scale, &zp, &rep);
+  if (st == WEFT_OK || st == WEFT_ERR_ZONE)
+    for (std::size_t v = 0; v < x_candidate.size(); ++v) x_candidate[v] = Vec3(xc[3 * v], xc[3 * v + 1], xc[3 * v + 2]);
+  check(st);
+  ZoneResolveReport out;
+  out.outer_iterations = rep.outer_iterations;
+  out.zone_count = rep.zone_count;
+  out.max_zone_vertices = rep.max_zone_vertices;
+  out.impacts_resolved = static_cast<int>(rep.impacts_resolved);
+  out.first_round_impacts = static_cast<int>(rep.first_round_impacts);
   return out;
 }
 

@@ -190,3 +190,56 @@ TEST_CASE("drop-in collide equals the reference collide (hits, bitwise values)")
     }
   }
 }
+
+TEST_CASE("drop-in build_zones / distribute_zones / resolve_zones equal the reference (bitwise positions)") {
+  // test_response.cpp:189-216 scene (resolves) and random_two_cloth_scene
+  // (test_response.cpp:218-240 recipe; the reference gives up: ZoneFailure)
+  auto soup = CollisionSoup::build({{0, 1, 2}, {3, 4, 5}}, 6, std::vector<std::uint8_t>(6, 1));
+  std::vector<Vec3> x0 = {Vec3(-1, -1, 0), Vec3(2, -1, 0), Vec3(0.2, 2, 0),
+                          Vec3(0.2, 0.2, 0.05), Vec3(1.5, 0.3, 0.5), Vec3(0.2, 1.5, 0.5)};
+  std::vector<Vec3> x1 = x0;
+  x1[3] = Vec3(0.2, 0.2, -0.08);
+  std::vector<double> mass(6, 0.1);
+  CollisionParams cparams;
+  cparams.thickness = 0.01;
+  ZoneSolveParams zparams;
+  zparams.clearance = 0.005;
+  Engine engine(2);
+  auto xr = x1, xg = x1;
+  const auto rr = resolve_zones(engine, soup, x0, xr, mass, cparams, zparams);
+  const auto rg = gpu::resolve_zones(engine, soup, x0, xg, mass, cparams, zparams);
+  CHECK(rr.outer_iterations == rg.outer_iterations);
+  CHECK(rr.zone_count == rg.zone_count);
+  CHECK(rr.first_round_impacts == rg.first_round_impacts);
+  CHECK(xr == xg);
+
+  oracle::Rng rng(52);
+  for (int trial = 0; trial < 3; ++trial) {
+    const auto scene = oracle::random_two_cloth_scene(rng, 6 + 2 * trial);
+    std::vector<double> m(static_cast<std::size_t>(scene.soup.vertex_count), 0.05);
+    const auto brute = collide(engine, scene.soup, scene.x_begin, scene.x_end, CollisionMode::Continuous,
+                               CollisionParams{});
+    const auto zr = build_zones(brute.impacts, scene.soup);
+    const auto zg = gpu::build_zones(brute.impacts, scene.soup);
+    REQUIRE(zr.size() == zg.size());
+    for (std::size_t z = 0; z < zr.size(); ++z) {
+      CHECK(zr[z].impacts == zg[z].impacts);
+      CHECK(zr[z].vertices == zg[z].vertices);
+    }
+    CHECK(distribute_zones(zr, 3) == gpu::distribute_zones(zg, 3));
+    std::string er, eg;
+    auto a = scene.x_end, b = scene.x_end;
+    try {
+      resolve_zones(engine, scene.soup, scene.x_begin, a, m, CollisionParams{}, ZoneSolveParams{});
+    } catch (const ZoneFailure& e) {
+      er = e.what();
+    }
+    try {
+      gpu::resolve_zones(engine, scene.soup, scene.x_begin, b, m, CollisionParams{}, ZoneSolveParams{});
+    } catch (const ZoneFailure& e) {
+      eg = e.what();
+    }
+    CHECK(er == eg);
+    CHECK(a == b);
+  }
+}

@@ -14,7 +14,7 @@ cfg = sys.argv[1] if len(sys.argv) > 1 else "D"
 sc = scenes.config(cfg, seed=20240810)
 mesh = weft.ClothMesh.build(sc.verts, sc.tris, sc.density)
 p = mesh.vertex_count
-eng = weft.Engine(1)
+eng = weft.Engine(int(os.environ.get("PARTS", "1")))
 eng.set_vertices(mesh.vertex_mass, sc.pinned)
 eng.set_elements(mesh.build_elements(sc.material, sc.gravity))
 eng.set_soup(p, sc.tris)
@@ -35,5 +35,5 @@ for k in range(9):
         broad.append(r.ms_broad)
         its.append(r.pcg_iterations)
 ms = statistics.median(solve)
-print(f"{os.environ.get('WEFT_LIB', 'default')}: solve {ms:.3f} ms ({1e3 * ms / its[-1]:.1f} us/it, {its[-1]} its) "
+print(f"{os.environ.get('WEFT_LIB', 'default')} parts={os.environ.get('PARTS', '1')} persistent={os.environ.get('WEFT_PCG_PERSISTENT', '1')}: solve {ms:.3f} ms ({1e3 * ms / its[-1]:.1f} us/it, {its[-1]} its) "
       f"asm {statistics.median(asm):.3f} broad {statistics.median(broad):.3f}", flush=True)
