@@ -370,7 +370,36 @@ struct NarrowArgs {
   double* __restrict__ vals;              // 8 per hit
   unsigned long long* __restrict__ count;
   unsigned long long cap;
+  const float4* __restrict__ tbox;  // per triangle: (lo xyz, -) (hi xyz, -), rounded outward
 };
+
+// Per-triangle box over the 3 vertices (begin and, for CCD, end positions),
+// rounded outward to float: a conservative stand-in for the exact box in the
+// whole-pair rejection of k_narrow (lo rounds down, hi rounds up, and
+// hi + margin rounds monotonically, so "apart" on the float boxes implies
+// apart on the exact ones).
+__global__ void k_tri_fbox(int ntris, const int32_t* __restrict__ tris, const double* __restrict__ x0,
+                           const double* __restrict__ x1, bool ccd, float4* __restrict__ out) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= ntris) return;
+  double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+  for (int k = 0; k < 3; ++k) {
+    const int v = tris[3 * t + k];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const double p0 = x0[3 * v + a];
+      lo[a] = dmin(lo[a], p0);
+      hi[a] = dmax(hi[a], p0);
+      if (ccd) {
+        const double p1 = x1[3 * v + a];
+        lo[a] = dmin(lo[a], p1);
+        hi[a] = dmax(hi[a], p1);
+      }
+    }
+  }
+  out[2 * t] = make_float4(__double2float_rd(lo[0]), __double2float_rd(lo[1]), __double2float_rd(lo[2]), 0.f);
+  out[2 * t + 1] = make_float4(__double2float_ru(hi[0]), __double2float_ru(hi[1]), __double2float_ru(hi[2]), 0.f);
+}
 
 __device__ __forceinline__ void emit(const NarrowArgs& g, int kind, int a, int b, const Hit& h) {
   const unsigned long long slot = atomicAdd(g.count, 1ull);
@@ -390,7 +419,7 @@ __device__ __forceinline__ void emit(const NarrowArgs& g, int kind, int a, int b
 
 // feature_apart (collision.cpp:226-254): box separation beyond the margin on
 // some axis, over begin (and, for CCD, end) positions.
-template <int NA, int NB>
+template <bool kCcd, int NA, int NB>
 __device__ __forceinline__ bool feature_apart(const NarrowArgs& g, const int (&fa)[NA], const int (&fb)[NB],
                                               double margin) {
   for (int axis = 0; axis < 3; ++axis) {
@@ -400,7 +429,7 @@ __device__ __forceinline__ bool feature_apart(const NarrowArgs& g, const int (&f
       const double p0 = g.x0[3 * fa[k] + axis];
       lo_a = dmin(lo_a, p0);
       hi_a = dmax(hi_a, p0);
-      if (g.ccd) {
+      if (kCcd) {
         const double p1 = g.x1[3 * fa[k] + axis];
         lo_a = dmin(lo_a, p1);
         hi_a = dmax(hi_a, p1);
@@ -411,7 +440,7 @@ __device__ __forceinline__ bool feature_apart(const NarrowArgs& g, const int (&f
       const double p0 = g.x0[3 * fb[k] + axis];
       lo_b = dmin(lo_b, p0);
       hi_b = dmax(hi_b, p0);
-      if (g.ccd) {
+      if (kCcd) {
         const double p1 = g.x1[3 * fb[k] + axis];
         lo_b = dmin(lo_b, p1);
         hi_b = dmax(hi_b, p1);
@@ -423,14 +452,31 @@ __device__ __forceinline__ bool feature_apart(const NarrowArgs& g, const int (&f
 }
 
 // narrow_phase_pair (collision.cpp:214-309), one thread per candidate pair.
+// Compiled once per mode (kCcd): the DCD instance carries none of the
+// cubic-solver registers (150 -> fewer registers, higher occupancy).
+template <bool kCcd>
 __global__ void __launch_bounds__(128) k_narrow(NarrowArgs g) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= g.npairs) return;
   const int2 pr = g.pairs[i];
   const int t1 = pr.x, t2 = pr.y;
+  const double margin0 = kCcd ? 1e-9 : g.thickness;
+  {  // whole-pair rejection on the conservative float boxes (k_tri_fbox)
+    const float4 la = __ldg(g.tbox + 2 * t1), ha = __ldg(g.tbox + 2 * t1 + 1);
+    const float4 lb = __ldg(g.tbox + 2 * t2), hb = __ldg(g.tbox + 2 * t2 + 1);
+    if ((double)la.x > (double)hb.x + margin0 || (double)lb.x > (double)ha.x + margin0 ||
+        (double)la.y > (double)hb.y + margin0 || (double)lb.y > (double)ha.y + margin0 ||
+        (double)la.z > (double)hb.z + margin0 || (double)lb.z > (double)ha.z + margin0)
+      return;
+  }
   const int tri1[3] = {g.tris[3 * t1], g.tris[3 * t1 + 1], g.tris[3 * t1 + 2]};
   const int tri2[3] = {g.tris[3 * t2], g.tris[3 * t2 + 1], g.tris[3 * t2 + 2]};
-  const double margin = g.ccd ? 1e-9 : g.thickness;
+  const double margin = kCcd ? 1e-9 : g.thickness;
+  // Whole-pair rejection: every feature of a triangle has a box inside the
+  // triangle's box (min / max are exact and x + margin rounds monotonically),
+  // so triangle boxes apart by more than the margin imply that all 15
+  // feature_apart tests below reject — same hits, far less work.
+  if (feature_apart<kCcd>(g, tri1, tri2, margin)) return;
   // vertex-face, both directions; shared vertices are exempt
   for (int dir = 0; dir < 2; ++dir) {
     const int* vt = dir == 0 ? tri1 : tri2;
@@ -442,10 +488,10 @@ __global__ void __launch_bounds__(128) k_narrow(NarrowArgs g) {
       if (!g.movable[v] && !g.movable[ft[0]] && !g.movable[ft[1]] && !g.movable[ft[2]]) continue;
       const int fa[1] = {v};
       const int fb[3] = {ft[0], ft[1], ft[2]};
-      if (feature_apart(g, fa, fb, margin)) continue;
+      if (feature_apart<kCcd>(g, fa, fb, margin)) continue;
       Hit h;
       bool hit;
-      if (!g.ccd) {
+      if (!kCcd) {
         hit = dcd_vf(ldx(g.x0, v), ldx(g.x0, ft[0]), ldx(g.x0, ft[1]), ldx(g.x0, ft[2]), g.thickness, h);
       } else {
         hit = ccd_vf(ldx(g.x0, v), ldx(g.x1, v), ldx(g.x0, ft[0]), ldx(g.x1, ft[0]), ldx(g.x0, ft[1]),
@@ -466,10 +512,10 @@ __global__ void __launch_bounds__(128) k_narrow(NarrowArgs g) {
       if (!g.movable[e1.x] && !g.movable[e1.y] && !g.movable[e2.x] && !g.movable[e2.y]) continue;
       const int fa[2] = {e1.x, e1.y};
       const int fb[2] = {e2.x, e2.y};
-      if (feature_apart(g, fa, fb, margin)) continue;
+      if (feature_apart<kCcd>(g, fa, fb, margin)) continue;
       Hit h;
       bool hit;
-      if (!g.ccd) {
+      if (!kCcd) {
         hit = dcd_ee(ldx(g.x0, e1.x), ldx(g.x0, e1.y), ldx(g.x0, e2.x), ldx(g.x0, e2.y), g.thickness, h);
       } else {
         hit = ccd_ee(ldx(g.x0, e1.x), ldx(g.x1, e1.x), ldx(g.x0, e1.y), ldx(g.x1, e1.y), ldx(g.x0, e2.x),
@@ -734,7 +780,13 @@ int64_t narrow_phase(Ctx& c, const double* x0, const double* x1, int mode, doubl
                nullptr,
                nullptr,
                nullptr,
-               0};
+               0,
+               nullptr};
+  c.zn_tbox.resize(2 * static_cast<size_t>(c.soup_tris) + 2);
+  if (c.soup_tris)
+    k_tri_fbox<<<div_up(c.soup_tris, 256), 256, 0, ls(c)>>>(c.soup_tris, c.tris.data(), x0, ccd ? x1 : x0, ccd,
+                                                            c.zn_tbox.data());
+  g.tbox = c.zn_tbox.data();
   c.hit_count.resize(1);
   unsigned long long nh = 0;
   if (npairs) {
@@ -747,7 +799,8 @@ int64_t narrow_phase(Ctx& c, const double* x0, const double* x1, int mode, doubl
       g.count = c.hit_count.data();
       g.cap = cap;
       WG_CUDA(cudaMemsetAsync(c.hit_count.data(), 0, sizeof(unsigned long long), s));
-      k_narrow<<<div_up(npairs, 128), 128, 0, ls(c)>>>(g);
+      if (ccd) k_narrow<true><<<div_up(npairs, 128), 128, 0, ls(c)>>>(g);
+      else k_narrow<false><<<div_up(npairs, 128), 128, 0, ls(c)>>>(g);
       WG_CUDA(cudaGetLastError());
       WG_CUDA(cudaMemcpyAsync(&nh, c.hit_count.data(), sizeof(nh), cudaMemcpyDeviceToHost, s));
       WG_CUDA(cudaStreamSynchronize(s));
