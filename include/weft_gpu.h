@@ -386,6 +386,13 @@ typedef struct weft_step_report {
 /* Uploads the state (x, v: 3*p doubles each; the soup positions of the
  * cloth are x). Requires vertices, elements and soup to be set. */
 weft_status weft_gpu_sim_set_state(weft_gpu_ctx* ctx, const double* x, const double* v);
+/* Kinematic obstacles (driver.cpp:113-131): when the soup holds vertices
+ * beyond the cloth's p (obstacle triangles appended after the cloth's, ids
+ * offset by p, set_soup_movable 0 for them), their positions at the step's
+ * start and end (Obstacle::positions_at(t), positions_at(t + dt); 3 doubles
+ * per obstacle vertex) must be given before every weft_gpu_sim_step; their
+ * velocities are (end - begin) / dt and their masses 1.0. */
+weft_status weft_gpu_sim_set_obstacles(weft_gpu_ctx* ctx, double dt, const double* x_begin, const double* x_end);
 /* One step on device-resident state: DCD grid + candidates on x, assembly
  * of step_system at x, PCG, v += dv, x_cand = x + dt v, CCD grid +
  * candidates on (x, x_cand), commit x = x_cand. */

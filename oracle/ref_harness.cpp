@@ -23,6 +23,8 @@
 #include "weft/physics.hpp"
 #include "weft/response.hpp"
 #include "weft/solver.hpp"
+#include "weft/scene.hpp"
+#include "weft/driver.hpp"
 
 #include "../include/weft_gpu.h"
 
@@ -914,5 +916,126 @@ int32_t ref_sim_step_contacts(void* h, const double* params, double* out) {
 }
 
 void ref_sim_free(void* h) { delete static_cast<RefSim*>(h); }
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Scenes (scene.cpp) and the reference Simulator (driver.cpp): parity of the
+// scene loader and of whole simulation runs.
+// ---------------------------------------------------------------------------
+namespace {
+struct SceneHandle {
+  Scene scene;
+  std::unique_ptr<Simulator> sim;
+};
+}  // namespace
+
+extern "C" {
+
+// load_scene (scene.cpp:167-178) from a file, or parse_scene from text when
+// `is_text` (base_dir for relative OBJ paths).
+void* ref_scene_load(const char* path_or_text, int32_t is_text, const char* base_dir) {
+  try {
+    auto* h = new SceneHandle();
+    h->scene = is_text ? parse_scene(path_or_text, base_dir ? base_dir : ".") : load_scene(path_or_text);
+    return h;
+  } catch (const std::exception& e) {
+    set_error(e);
+    return nullptr;
+  }
+}
+
+// counts: cloth verts, cloth tris, obstacles, then per obstacle (verts, tris, keyframes) up to cap_obs
+void ref_scene_info(void* hp, int32_t* counts, int32_t cap_obs) {
+  const auto& sc = static_cast<SceneHandle*>(hp)->scene;
+  counts[0] = sc.cloth.vertex_count();
+  counts[1] = static_cast<int32_t>(sc.cloth.triangles.size());
+  counts[2] = static_cast<int32_t>(sc.obstacles.size());
+  for (int o = 0; o < std::min<int>(cap_obs, static_cast<int>(sc.obstacles.size())); ++o) {
+    counts[3 + 3 * o] = static_cast<int32_t>(sc.obstacles[static_cast<std::size_t>(o)].shape.vertices.size());
+    counts[4 + 3 * o] = static_cast<int32_t>(sc.obstacles[static_cast<std::size_t>(o)].shape.triangles.size());
+    counts[5 + 3 * o] = static_cast<int32_t>(sc.obstacles[static_cast<std::size_t>(o)].keyframes.size());
+  }
+}
+
+// config doubles: dt, frames, devices, gravity xyz, wind xyz, seed, material (7: warp, weft, shear, bend,
+// density, damping, air_drag), thickness, cell_scale, stiffness_scale, friction, clearance_fraction,
+// contact damping, pcg tol, pcg max its, preconditioner, zone outer_cap, zone initial_penalty, precision
+void ref_scene_config(void* hp, double* cfg) {
+  const auto& c = static_cast<SceneHandle*>(hp)->scene.config;
+  double v[] = {c.dt, (double)c.frames, (double)c.devices, c.gravity.x(), c.gravity.y(), c.gravity.z(), c.wind.x(),
+                c.wind.y(), c.wind.z(), (double)c.seed, c.material.stretch_warp, c.material.stretch_weft,
+                c.material.shear, c.material.bend, c.material.density, c.material.damping, c.material.air_drag,
+                c.collision.thickness, c.collision.cell_scale, c.contact.stiffness_scale, c.contact.friction,
+                c.contact.clearance_fraction, c.contact.damping, c.solver.rel_tolerance,
+                (double)c.solver.max_iterations, c.solver.preconditioner == Preconditioner::BlockJacobi ? 1.0 : 0.0,
+                (double)c.zones.outer_cap, c.zones.initial_penalty,
+                c.precision == Precision::Double ? 1.0 : 0.0};
+  std::memcpy(cfg, v, sizeof(v));
+}
+
+// cloth rest positions (3 per vertex), triangles, pinned flags; obstacle o's shape
+void ref_scene_cloth(void* hp, double* verts, int32_t* tris, uint8_t* pinned) {
+  const auto& sc = static_cast<SceneHandle*>(hp)->scene;
+  for (std::size_t i = 0; i < sc.cloth.rest_positions.size(); ++i)
+    for (int c = 0; c < 3; ++c) verts[3 * i + static_cast<std::size_t>(c)] = sc.cloth.rest_positions[i][c];
+  for (std::size_t t = 0; t < sc.cloth.triangles.size(); ++t)
+    for (int c = 0; c < 3; ++c) tris[3 * t + static_cast<std::size_t>(c)] = sc.cloth.triangles[t][static_cast<std::size_t>(c)];
+  std::memcpy(pinned, sc.pinned.data(), sc.pinned.size());
+}
+
+// obstacle o: its vertex positions at time t (Obstacle::positions_at), triangles
+void ref_scene_obstacle(void* hp, int32_t o, double t, double* verts, int32_t* tris) {
+  const auto& ob = static_cast<SceneHandle*>(hp)->scene.obstacles[static_cast<std::size_t>(o)];
+  const auto pos = ob.positions_at(t);
+  for (std::size_t i = 0; i < pos.size(); ++i)
+    for (int c = 0; c < 3; ++c) verts[3 * i + static_cast<std::size_t>(c)] = pos[i][c];
+  if (tris)
+    for (std::size_t k = 0; k < ob.shape.triangles.size(); ++k)
+      for (int c = 0; c < 3; ++c) tris[3 * k + static_cast<std::size_t>(c)] = ob.shape.triangles[k][static_cast<std::size_t>(c)];
+}
+
+// Simulator(scene) with `devices` engine devices (<= 0: the scene's), then step():
+// out = frame, time, pcg its, pcg residual, proximities, contacts, impacts, zones, zone_outer, committed.
+int32_t ref_scene_step(void* hp, int32_t devices, double* out) {
+  auto* h = static_cast<SceneHandle*>(hp);
+  try {
+    if (!h->sim) {
+      SimConfig cfg = h->scene.config;
+      if (devices > 0) cfg.devices = devices;
+      h->sim = std::make_unique<Simulator>(h->scene.cloth, h->scene.pinned, h->scene.obstacles, cfg);
+    }
+    const auto r = h->sim->step();
+    const double v[] = {(double)r.frame, r.time, (double)r.pcg_iterations, r.pcg_residual, (double)r.proximities,
+                        (double)r.contacts, (double)r.impacts, (double)r.zone_count, (double)r.zone_outer,
+                        r.committed ? 1.0 : 0.0};
+    std::memcpy(out, v, sizeof(v));
+    return 0;
+  } catch (const std::exception& e) {
+    return set_error(e);
+  }
+}
+
+void ref_scene_state(void* hp, double* x, double* v) {
+  auto* h = static_cast<SceneHandle*>(hp);
+  const auto& st = h->sim->state();
+  for (std::size_t i = 0; i < st.x.size(); ++i)
+    for (int c = 0; c < 3; ++c) {
+      if (x) x[3 * i + static_cast<std::size_t>(c)] = st.x[i][c];
+      if (v) v[3 * i + static_cast<std::size_t>(c)] = st.v[i][c];
+    }
+}
+
+// save_obj (mesh.cpp:320-332) of the cloth at its current state into buf; returns the length
+int64_t ref_scene_save_obj(void* hp, char* buf, int64_t cap) {
+  auto* h = static_cast<SceneHandle*>(hp);
+  std::ostringstream os;
+  save_obj(os, h->sim ? h->sim->state().x : h->scene.cloth.rest_positions, h->scene.cloth.triangles);
+  const std::string str = os.str();
+  if (buf) std::memcpy(buf, str.data(), std::min<int64_t>(cap, static_cast<int64_t>(str.size())));
+  return static_cast<int64_t>(str.size());
+}
+
+void ref_scene_free(void* hp) { delete static_cast<SceneHandle*>(hp); }
 
 }  // extern "C"

@@ -199,8 +199,10 @@ struct Ctx {
   std::vector<cudaEvent_t> prof_ev;
 
   // ---- resident simulation state
-  DBuf<double> sim_x, sim_v, sim_xc;
+  DBuf<double> sim_x, sim_v, sim_xc;  // soup-sized: the cloth's 3p, then obstacle vertices
+  DBuf<double> soup_mass;             // cloth masses, 1.0 for obstacle vertices
   bool has_state = false;
+  bool obstacles_set = false;         // obstacle positions of this step given
 
   // impact zones (zones.cu): accumulated impacts, zone structure, solver scratch
   DBuf<unsigned long long> zn_acc_keys, zn_acc_sorted, zn_tmp_keys;

@@ -262,26 +262,63 @@ weft_status weft_gpu_candidates(weft_gpu_ctx* ctx, int64_t begin, int64_t end, i
 weft_status weft_gpu_sim_set_state(weft_gpu_ctx* ctx, const double* x, const double* v) {
   return guard2(ctx, [&](Ctx& c) {
     if (c.p == 0 || c.n_static == 0) throw Error(WEFT_ERR_INVALID, "sim_set_state: set vertices and elements first");
-    if (c.soup_verts != c.p) throw Error(WEFT_ERR_INVALID, "sim_set_state: soup must be the cloth (soup_verts == p)");
-    const size_t n = 3 * static_cast<size_t>(c.p);
+    // the soup is the cloth (vertices [0, p)) followed by the obstacles'
+    // vertices (driver.cpp:73-85), whose positions come per step from
+    // weft_gpu_sim_set_obstacles
+    if (c.soup_verts < c.p) throw Error(WEFT_ERR_INVALID, "sim_set_state: the soup must start with the cloth");
+    if (c.soup_verts > c.p && c.world > 1) throw Error(WEFT_ERR_INVALID, "sim_set_state: obstacles run on one rank");
+    const size_t n = 3 * static_cast<size_t>(c.p), ns = 3 * static_cast<size_t>(c.soup_verts);
     if (c.world > 1) {
       weft_gpu::comm_need(c, "sim_set_state");
       weft_gpu::rank_barrier(c);  // no peer may still be reading the state being replaced
     }
-    weft_gpu::upload_vec(c, c.sim_x, x, n);
-    weft_gpu::upload_vec(c, c.sim_v, v, n);
-    c.sim_xc.resize(n);
-    // the soup is the cloth: movable = !pinned (driver.cpp:73-85)
-    c.soup_movable.resize(static_cast<size_t>(c.p));
+    c.sim_x.resize(ns);
+    c.sim_v.resize(ns);
+    WG_CUDA(cudaMemcpyAsync(c.sim_x.data(), x, n * sizeof(double), cudaMemcpyDefault, c.stream));
+    WG_CUDA(cudaMemcpyAsync(c.sim_v.data(), v, n * sizeof(double), cudaMemcpyDefault, c.stream));
+    c.sim_xc.resize(ns);
+    c.sim_xc.n = ns;
+    // movable = !pinned for the cloth, 0 for obstacle vertices
+    c.soup_movable.resize(static_cast<size_t>(c.soup_verts));
+    if (c.soup_verts > c.p) WG_CUDA(cudaMemsetAsync(c.soup_movable.data() + c.p, 0, c.soup_verts - c.p, c.stream));
     weft_gpu::k_movable<<<weft_gpu::div_up(c.p, 256), 256, 0, ls(c)>>>(c.p, c.pinned.data(), c.soup_movable.data());
+    // soup masses (driver.cpp:143-144): the cloth's, 1.0 for obstacle vertices
+    c.soup_mass.resize(static_cast<size_t>(c.soup_verts));
+    WG_CUDA(cudaMemcpyAsync(c.soup_mass.data(), c.mass.data(), c.p * sizeof(double), cudaMemcpyDeviceToDevice, c.stream));
+    if (c.soup_verts > c.p) {
+      const std::vector<double> ones(static_cast<size_t>(c.soup_verts - c.p), 1.0);
+      WG_CUDA(cudaMemcpyAsync(c.soup_mass.data() + c.p, ones.data(), ones.size() * sizeof(double),
+                              cudaMemcpyHostToDevice, c.stream));
+    }
     WG_CUDA(cudaStreamSynchronize(c.stream));
     c.has_state = true;
+    c.obstacles_set = c.soup_verts == c.p;
+  });
+}
+
+weft_status weft_gpu_sim_set_obstacles(weft_gpu_ctx* ctx, double dt, const double* x_begin, const double* x_end) {
+  return guard2(ctx, [&](Ctx& c) {
+    if (!c.has_state) throw Error(WEFT_ERR_INVALID, "sim_set_obstacles: sim_set_state first");
+    const int no = c.soup_verts - c.p;
+    if (no == 0) return;
+    if (!x_begin || !x_end || !(dt > 0.0)) throw Error(WEFT_ERR_INVALID, "sim_set_obstacles: bad arguments");
+    const size_t n = 3 * static_cast<size_t>(no), o = 3 * static_cast<size_t>(c.p);
+    std::vector<double> b(n), e(n), vel(n);
+    WG_CUDA(cudaMemcpy(b.data(), x_begin, n * sizeof(double), cudaMemcpyDefault));
+    WG_CUDA(cudaMemcpy(e.data(), x_end, n * sizeof(double), cudaMemcpyDefault));
+    for (size_t i = 0; i < n; ++i) vel[i] = (e[i] - b[i]) / dt;  // driver.cpp:126-128
+    WG_CUDA(cudaMemcpyAsync(c.sim_x.data() + o, b.data(), n * sizeof(double), cudaMemcpyHostToDevice, c.stream));
+    WG_CUDA(cudaMemcpyAsync(c.sim_xc.data() + o, e.data(), n * sizeof(double), cudaMemcpyHostToDevice, c.stream));
+    WG_CUDA(cudaMemcpyAsync(c.sim_v.data() + o, vel.data(), n * sizeof(double), cudaMemcpyHostToDevice, c.stream));
+    WG_CUDA(cudaStreamSynchronize(c.stream));
+    c.obstacles_set = true;
   });
 }
 
 weft_status weft_gpu_sim_step(weft_gpu_ctx* ctx, const weft_sim_params* prm, weft_step_report* rep) {
   return guard2(ctx, [&](Ctx& c) {
     if (!c.has_state) throw Error(WEFT_ERR_INVALID, "sim_step: sim_set_state first");
+    if (!c.obstacles_set) throw Error(WEFT_ERR_INVALID, "sim_step: obstacle positions missing (sim_set_obstacles)");
     cudaStream_t s = c.stream;
     const int64_t n = 3 * static_cast<int64_t>(c.p);
     const double dt = prm->dt;
@@ -377,8 +414,8 @@ weft_status weft_gpu_sim_step(weft_gpu_ctx* ctx, const weft_sim_params* prm, wef
         WG_CUDA(cudaEventRecord(c.ev_side[2], s));
         c.zn_pre.resize(static_cast<size_t>(n));
         WG_CUDA(cudaMemcpyAsync(c.zn_pre.data(), c.sim_xc.data(), n * sizeof(double), cudaMemcpyDeviceToDevice, s));
-        weft_gpu::resolve_zones(c, c.sim_x.data(), c.sim_xc.data(), c.mass.data(), prm->thickness, prm->cell_scale,
-                                prm->zone, zr, /*have_first=*/true);
+        weft_gpu::resolve_zones(c, c.sim_x.data(), c.sim_xc.data(), c.soup_mass.data(), prm->thickness,
+                                prm->cell_scale, prm->zone, zr, /*have_first=*/true);
         weft_gpu::zone_commit(c, c.sim_xc.data(), c.zn_pre.data(), dt, c.sim_v.data());
         WG_CUDA(cudaEventRecord(c.ev_side[3], s));
         WG_CUDA(cudaEventSynchronize(c.ev_side[3]));
@@ -391,6 +428,7 @@ weft_status weft_gpu_sim_step(weft_gpu_ctx* ctx, const weft_sim_params* prm, wef
     // 7. commit
     std::swap(c.sim_x.ptr, c.sim_xc.ptr);
     std::swap(c.sim_x.cap, c.sim_xc.cap);
+    c.obstacles_set = c.soup_verts == c.p;  // obstacle positions are per step
     WG_CUDA(cudaEventSynchronize(ev[5]));
     float tdcd = 0, tasm = 0, t13 = 0, t45 = 0;
     cudaEventElapsedTime(&tdcd, c.ev_side[0], c.ev_side[1]);  // overlapped with the assembly

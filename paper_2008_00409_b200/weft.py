@@ -522,6 +522,11 @@ class Engine:
         _check(LIB.weft_gpu_sim_set_state(self._ctx, _ptr(_f64(x) if isinstance(x, np.ndarray) else x),
                                           _ptr(_f64(v) if isinstance(v, np.ndarray) else v)))
 
+    def sim_set_obstacles(self, dt: float, x_begin, x_end):
+        """Obstacle vertex positions at the step's start and end (soup
+        vertices after the cloth's; driver.cpp:113-131)."""
+        _check(LIB.weft_gpu_sim_set_obstacles(self._ctx, C.c_double(dt), _ptr(_f64(x_begin)), _ptr(_f64(x_end))))
+
     def sim_step(self, params: SimParams) -> StepReport:
         rep = StepReport()
         _check(LIB.weft_gpu_sim_step(self._ctx, C.byref(params), C.byref(rep)))

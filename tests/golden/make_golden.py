@@ -100,6 +100,21 @@ def main():
         np.savez_compressed(os.path.join(HERE, f"zones_{k}.npz"), nv=np.array(nv), tris=tris, x0=x0, x1=x1,
                             mass=mass, movable=mv, thickness=np.array(th), params=np.asarray(zp), status=np.array(st),
                             message=np.array(msg), x_out=xc, report=np.array([rep[f] for f in ZONE_REPORT]))
+    # scenes (scene.cpp) run by the reference Simulator (driver.cpp:55-215):
+    # per-frame counts and the final state (tests/scenes_gen.py scenes)
+    from oracle_bindings import RefScene
+    from scenes_gen import SCENES, scene_text
+    for name in SCENES:
+        rs = RefScene(REF, text=scene_text(name))
+        frames = []
+        for _ in range(int(rs.config()["frames"])):
+            r = rs.step()
+            frames.append([r["pcg_iterations"], r["proximities"], r["contacts"], r["impacts"], r["zone_count"],
+                           r["zone_outer"]])
+        x, v = rs.state()
+        np.savez_compressed(os.path.join(HERE, f"scene_{name}.npz"), text=np.array(scene_text(name)),
+                            frames=np.array(frames, np.int64), x=x, v=v, obj=np.array(rs.save_obj()))
+        rs.close()
     # SpMV: oracle::random_bell (sparse_oracle.cpp:7-23), pipelined at n = 1, 2, 4.
     for k, (seed, rows) in enumerate([(5, 7), (6, 40)]):
         s = REF.random_bell(seed, rows, 3)

