@@ -82,6 +82,14 @@ __device__ __forceinline__ uint64_t l2_policy_evict_first() {
   asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
   return pol;
 }
+// evict_last for a fraction of the lines (by address), evict_unchanged for
+// the rest: the gathered vectors keep at most ~60 MB of L2 pinned when they
+// are larger than that (frac < 1 from the host, PcgArgs::vec_el_frac).
+__device__ __forceinline__ uint64_t l2_policy_evict_last_frac(float frac) {
+  uint64_t pol;
+  asm("createpolicy.fractional.L2::evict_last.L2::evict_unchanged.b64 %0, %1;" : "=l"(pol) : "f"(frac));
+  return pol;
+}
 __device__ __forceinline__ uint64_t l2_policy_evict_last() {
   uint64_t pol;
   asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
@@ -854,6 +862,7 @@ struct PcgArgs {
   double* p2;  // persistent solve: second search-direction buffer
   int q_msw;   // persistent solve with q in shared memory: max slices per warp
   const double* dinv6;  // persistent solve: packed symmetric D^-1 (null: 9-double form)
+  float vec_el_frac;    // persistent solve: fraction of the gathered z / p lines kept evict_last
   unsigned long long* timing;  // dev instrumentation (WEFT_PCG_TIMING=1): ns per phase, summed
 };
 
@@ -1111,12 +1120,12 @@ constexpr int kPkUnroll = WEFT_PK_UNROLL;
 template <int PMode>
 __device__ __forceinline__ void row_product_cg(const SellView& A, int r, const double* __restrict__ z,
                                                const double* __restrict__ pold, double beta, double& y0, double& y1,
-                                               double& y2) {
+                                               double& y2, float vec_frac) {
 #if WEFT_MAT_EF
   const uint64_t mpol = l2_policy_evict_first();
 #endif
 #if WEFT_VEC_EL
-  const uint64_t vpol = l2_policy_evict_last();
+  const uint64_t vpol = l2_policy_evict_last_frac(vec_frac);
 #endif
   const int len = A.rowlen[r];
   const int64_t base = A.slice_off[r >> 5] + (r & 31);
@@ -1235,8 +1244,8 @@ __global__ void __launch_bounds__(kPersistThreads, WEFT_PERSIST_MINB) k_pcg_pers
       const int i = sl * kSlice + lane;  // matrix position == vector index (position space)
       if (i < rows) {
         double y0, y1, y2;
-        if (first) row_product_cg<1>(A, i, z, pcur, beta, y0, y1, y2);
-        else row_product_cg<2>(A, i, z, pcur, beta, y0, y1, y2);
+        if (first) row_product_cg<1>(A, i, z, pcur, beta, y0, y1, y2, g.vec_el_frac);
+        else row_product_cg<2>(A, i, z, pcur, beta, y0, y1, y2, g.vec_el_frac);
         double p0 = __ldcg(z + 3 * i), p1 = __ldcg(z + 3 * i + 1), p2 = __ldcg(z + 3 * i + 2);
         if (!first) {
           p0 = p0 + beta * __ldcg(pcur + 3 * i);
@@ -1597,6 +1606,11 @@ PcgResult pcg_solve(Ctx& c, const double* b_dev, const weft_pcg_config& cfg, dou
     args.A.cols = c.A.colp.data();  // columns as positions
     args.x = c.xp.data();
     args.q_msw = msw;
+    // z and p (48 B per row) are gathered every iteration: pin them in L2
+    // while they fit in ~60 MB of its 126 MB, a proportional fraction beyond
+    // (the 5-10 M triangle sweep configs)
+    static const double el_budget = std::getenv("WEFT_PCG_EL_MB") ? std::atof(std::getenv("WEFT_PCG_EL_MB")) : 60.0;
+    args.vec_el_frac = static_cast<float>(std::min(1.0, el_budget * 1e6 / (48.0 * std::max(rows, 1))));
     static const bool d6_off = std::getenv("WEFT_PCG_DINV6") && std::atoi(std::getenv("WEFT_PCG_DINV6")) == 0;
     args.dinv6 = (bj && !asym && !d6_off) ? c.dinv6.data() : nullptr;
     if (std::getenv("WEFT_PCG_TIMING")) {
