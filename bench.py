@@ -477,7 +477,8 @@ def gpu_arm(args, rank, world, local):
         alg_bytes = info.nnzb * (9 * 8 + 4) + info.block_rows * (4 + 3 * 8 * 3)
         launch_ms = st.spmv_ms / max(st.spmv_launches, 1)
         nlaunch = st.spmv_launches
-        traffic = traffic_per_launch(args.config)
+        # the committed capture is of the one-partition kernel: no per-rank figure
+        traffic = traffic_per_launch(args.config) if world == 1 else None
     achieved = alg_bytes / (launch_ms * 1e-3) / 1e9
     it = [r.pcg_iterations for r in reps]
     # The assembly against the same HBM roofline (SURVEY §8(d) algorithmic
