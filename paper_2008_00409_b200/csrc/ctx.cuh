@@ -139,6 +139,7 @@ struct Ctx {
   bool spmv_pair = false;  // two threads per row SpMV variant (WEFT_SPMV_PAIR=1)
   bool use_persistent = true;  // one-partition solves: one cooperative kernel (WEFT_PCG_PERSISTENT=0: graph)
   DBuf<double> p2;             // its second search-direction buffer
+  DBuf<double> z4, p4a, p4b;   // its z / p at 32 bytes per row (WEFT_PK_V4)
 
   // ---- broad phase
   int soup_verts = 0, soup_tris = 0;

@@ -1117,6 +1117,46 @@ constexpr int kPkUnroll = WEFT_PK_UNROLL;
 #define WEFT_PK_XDEFER 1
 #endif
 
+// WEFT_PK_V4=1: inside the persistent solve the gathered vectors z and p are
+// stored 32 bytes per row (xyz + pad), so a column gather is ONE 256-bit
+// load (LDG.256, one sector) instead of three 8-byte loads.
+#ifndef WEFT_PK_V4
+#define WEFT_PK_V4 1
+#endif
+constexpr int kPkVs = WEFT_PK_V4 ? 4 : 3;  // doubles per row of z / p in the persistent solve
+__device__ __forceinline__ void ld4_cg(const double* p, uint64_t pol, double& a, double& b, double& c) {
+  double d;
+  asm volatile("ld.global.cg.L2::cache_hint.v4.f64 {%0,%1,%2,%3}, [%4], %5;"
+               : "=d"(a), "=d"(b), "=d"(c), "=d"(d)
+               : "l"(p), "l"(pol));
+}
+__device__ __forceinline__ void ld4_cg(const double* p, double& a, double& b, double& c) {
+  double d;
+  asm volatile("ld.global.cg.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p));
+}
+__device__ __forceinline__ void st4_cg(double* p, double a, double b, double c) {
+  asm volatile("st.global.cg.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(0.0) : "memory");
+}
+// own-row / gathered vector access of the persistent solve (stride kPkVs)
+__device__ __forceinline__ void vload3(const double* v, int i, double& a, double& b, double& c) {
+  if constexpr (kPkVs == 4) {
+    ld4_cg(v + 4 * (size_t)i, a, b, c);
+  } else {
+    a = __ldcg(v + 3 * (size_t)i);
+    b = __ldcg(v + 3 * (size_t)i + 1);
+    c = __ldcg(v + 3 * (size_t)i + 2);
+  }
+}
+__device__ __forceinline__ void vstore3(double* v, int i, double a, double b, double c) {
+  if constexpr (kPkVs == 4) {
+    st4_cg(v + 4 * (size_t)i, a, b, c);
+  } else {
+    __stcg(v + 3 * (size_t)i, a);
+    __stcg(v + 3 * (size_t)i + 1, b);
+    __stcg(v + 3 * (size_t)i + 2, c);
+  }
+}
+
 template <int PMode>
 __device__ __forceinline__ void row_product_cg(const SellView& A, int r, const double* __restrict__ z,
                                                const double* __restrict__ pold, double beta, double& y0, double& y1,
@@ -1140,12 +1180,24 @@ __device__ __forceinline__ void row_product_cg(const SellView& A, int r, const d
     const double v0 = WEFT_MAT_LD(v), v1 = WEFT_MAT_LD(v + 32), v2 = WEFT_MAT_LD(v + 64);
     const double v3 = WEFT_MAT_LD(v + 96), v4 = WEFT_MAT_LD(v + 128), v5 = WEFT_MAT_LD(v + 160);
     const double v6 = WEFT_MAT_LD(v + 192), v7 = WEFT_MAT_LD(v + 224), v8 = WEFT_MAT_LD(v + 256);
-    double x0 = WEFT_VEC_LD(z + 3 * c), x1 = WEFT_VEC_LD(z + 3 * c + 1), x2 = WEFT_VEC_LD(z + 3 * c + 2);
+#if WEFT_PK_V4 && WEFT_VEC_EL
+    double x0, x1, x2;
+    ld4_cg(z + 4 * (size_t)c, vpol, x0, x1, x2);
     if (PMode == 2) {
-      x0 = x0 + beta * WEFT_VEC_LD(pold + 3 * c);
-      x1 = x1 + beta * WEFT_VEC_LD(pold + 3 * c + 1);
-      x2 = x2 + beta * WEFT_VEC_LD(pold + 3 * c + 2);
+      double q0, q1, q2;
+      ld4_cg(pold + 4 * (size_t)c, vpol, q0, q1, q2);
+      x0 = x0 + beta * q0;
+      x1 = x1 + beta * q1;
+      x2 = x2 + beta * q2;
     }
+#else
+    double x0 = WEFT_VEC_LD(z + kPkVs * c), x1 = WEFT_VEC_LD(z + kPkVs * c + 1), x2 = WEFT_VEC_LD(z + kPkVs * c + 2);
+    if (PMode == 2) {
+      x0 = x0 + beta * WEFT_VEC_LD(pold + kPkVs * c);
+      x1 = x1 + beta * WEFT_VEC_LD(pold + kPkVs * c + 1);
+      x2 = x2 + beta * WEFT_VEC_LD(pold + kPkVs * c + 2);
+    }
+#endif
     a0 = a0 + ((v0 * x0 + v1 * x1) + v2 * x2);
     a1 = a1 + ((v3 * x0 + v4 * x1) + v5 * x2);
     a2 = a2 + ((v6 * x0 + v7 * x1) + v8 * x2);
@@ -1246,11 +1298,14 @@ __global__ void __launch_bounds__(kPersistThreads, WEFT_PERSIST_MINB) k_pcg_pers
         double y0, y1, y2;
         if (first) row_product_cg<1>(A, i, z, pcur, beta, y0, y1, y2, g.vec_el_frac);
         else row_product_cg<2>(A, i, z, pcur, beta, y0, y1, y2, g.vec_el_frac);
-        double p0 = __ldcg(z + 3 * i), p1 = __ldcg(z + 3 * i + 1), p2 = __ldcg(z + 3 * i + 2);
+        double p0, p1, p2;
+        vload3(z, i, p0, p1, p2);
         if (!first) {
-          p0 = p0 + beta * __ldcg(pcur + 3 * i);
-          p1 = p1 + beta * __ldcg(pcur + 3 * i + 1);
-          p2 = p2 + beta * __ldcg(pcur + 3 * i + 2);
+          double o0, o1, o2;
+          vload3(pcur, i, o0, o1, o2);
+          p0 = p0 + beta * o0;
+          p1 = p1 + beta * o1;
+          p2 = p2 + beta * o2;
         }
         if constexpr (kQs) {
           double* qq = qw + (sl - sl_begin) * 96;
@@ -1262,15 +1317,7 @@ __global__ void __launch_bounds__(kPersistThreads, WEFT_PERSIST_MINB) k_pcg_pers
           __stcg(q + 3 * i + 1, y1);
           __stcg(q + 3 * i + 2, y2);
         }
-#if WEFT_ZP_ST_EL
-        st_cg_hint(pnew + 3 * i, p0, elpol);
-        st_cg_hint(pnew + 3 * i + 1, p1, elpol);
-        st_cg_hint(pnew + 3 * i + 2, p2, elpol);
-#else
-        __stcg(pnew + 3 * i, p0);
-        __stcg(pnew + 3 * i + 1, p1);
-        __stcg(pnew + 3 * i + 2, p2);
-#endif
+        vstore3(pnew, i, p0, p1, p2);
         s1[0] = s1[0] + ((p0 * y0 + p1 * y1) + p2 * y2);
       }
     }
@@ -1318,14 +1365,14 @@ __global__ void __launch_bounds__(kPersistThreads, WEFT_PERSIST_MINB) k_pcg_pers
       }
       if (x_now) {
         double xv[3], pv[3];
+        vload3(pnew, i, pv[0], pv[1], pv[2]);
 #pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          pv[c] = __ldcg(pnew + 3 * i + c);
-          xv[c] = PB_LD(x + 3 * i + c);
-        }
+        for (int c = 0; c < 3; ++c) xv[c] = PB_LD(x + 3 * i + c);
         if (WEFT_PK_XDEFER) {
+          double po[3];
+          vload3(pcur, i, po[0], po[1], po[2]);
 #pragma unroll
-          for (int c = 0; c < 3; ++c) xv[c] = xv[c] + alpha_prev * __ldcg(pcur + 3 * i + c);
+          for (int c = 0; c < 3; ++c) xv[c] = xv[c] + alpha_prev * po[c];
         }
 #pragma unroll
         for (int c = 0; c < 3; ++c) __stcg(x + 3 * i + c, xv[c] + alpha * pv[c]);
@@ -1367,15 +1414,7 @@ __global__ void __launch_bounds__(kPersistThreads, WEFT_PERSIST_MINB) k_pcg_pers
       }
 #pragma unroll
       for (int c = 0; c < 3; ++c) __stcg(r + 3 * i + c, rv[c]);
-#if WEFT_ZP_ST_EL
-      st_cg_hint(z + 3 * i, z0, elpol);
-      st_cg_hint(z + 3 * i + 1, z1, elpol);
-      st_cg_hint(z + 3 * i + 2, z2, elpol);
-#else
-      __stcg(z + 3 * i, z0);
-      __stcg(z + 3 * i + 1, z1);
-      __stcg(z + 3 * i + 2, z2);
-#endif
+      vstore3(z, i, z0, z1, z2);
       s2[0] = s2[0] + ((rv[0] * rv[0] + rv[1] * rv[1]) + rv[2] * rv[2]);
       s2[1] = s2[1] + ((rv[0] * z0 + rv[1] * z1) + rv[2] * z2);
     }
@@ -1424,9 +1463,12 @@ __global__ void __launch_bounds__(kPersistThreads, WEFT_PERSIST_MINB) k_pcg_pers
     const int pb_begin = kQs ? sl_begin * kSlice + lane : blockIdx.x * blockDim.x + threadIdx.x;
     const int pb_end = kQs ? min(rows, sl_end * kSlice) : rows;
     const int pb_step = kQs ? kSlice : gridDim.x * blockDim.x;
-    for (int i = pb_begin; i < pb_end; i += pb_step)
+    for (int i = pb_begin; i < pb_end; i += pb_step) {
+      double pv[3];
+      vload3(pnew, i, pv[0], pv[1], pv[2]);
 #pragma unroll
-      for (int c = 0; c < 3; ++c) __stcg(x + 3 * i + c, __ldcg(x + 3 * i + c) + alpha_prev * __ldcg(pnew + 3 * i + c));
+      for (int c = 0; c < 3; ++c) __stcg(x + 3 * i + c, __ldcg(x + 3 * i + c) + alpha_prev * pv[c]);
+    }
   }
   if (lead) {
     st->iter = it;
@@ -1451,7 +1493,8 @@ __global__ void k_colpos(int64_t total, const int32_t* __restrict__ cols, const 
 // PCG init in position space: r = b[perm], z = M^-1 r, x = 0, p = 0.
 __global__ void k_pcg_init_pos(int rows, const int32_t* __restrict__ perm, const double* __restrict__ b,
                                const double* __restrict__ dinv, bool bj, double* __restrict__ x,
-                               double* __restrict__ r, double* __restrict__ z, double* __restrict__ p) {
+                               double* __restrict__ r, double* __restrict__ z, double* __restrict__ p,
+                               double* __restrict__ z4, double* __restrict__ p4) {
   const int m = blockIdx.x * blockDim.x + threadIdx.x;
   if (m >= rows) return;
   const int i = perm[m];
@@ -1466,6 +1509,13 @@ __global__ void k_pcg_init_pos(int rows, const int32_t* __restrict__ perm, const
   z[3 * m + 1] = z1;
   z[3 * m + 2] = z2;
   p[3 * m] = p[3 * m + 1] = p[3 * m + 2] = 0.0;
+  if (z4) {  // the persistent solve's 32-byte-per-row copies (kPkVs == 4)
+    z4[4 * (size_t)m] = z0;
+    z4[4 * (size_t)m + 1] = z1;
+    z4[4 * (size_t)m + 2] = z2;
+    z4[4 * (size_t)m + 3] = 0.0;
+    p4[4 * (size_t)m] = p4[4 * (size_t)m + 1] = p4[4 * (size_t)m + 2] = p4[4 * (size_t)m + 3] = 0.0;
+  }
 }
 
 // out[perm[m]] = in[m] (3 doubles per row).
@@ -1535,8 +1585,14 @@ PcgResult pcg_solve(Ctx& c, const double* b_dev, const weft_pcg_config& cfg, dou
       c.dinv6.resize(6 * static_cast<size_t>(rows) + 6);
       WG_CUDA(cudaMemsetAsync(dinv_asym, 0, sizeof(int), s));
       if (bj) k_dinv<true><<<div_up(rows, threads), threads, 0, ls(c)>>>(A, c.dinv.data(), c.dinv6.data(), dinv_asym);
-      k_pcg_init_pos<<<div_up(rows, threads), threads, 0, ls(c)>>>(rows, c.A.perm.data(), b_dev, c.dinv.data(), bj,
-                                                                   c.xp.data(), c.r.data(), c.z.data(), c.pv.data());
+      if (kPkVs == 4) {
+        c.z4.resize(4 * static_cast<size_t>(rows) + 4);
+        c.p4a.resize(4 * static_cast<size_t>(rows) + 4);
+        c.p4b.resize(4 * static_cast<size_t>(rows) + 4);
+      }
+      k_pcg_init_pos<<<div_up(rows, threads), threads, 0, ls(c)>>>(
+          rows, c.A.perm.data(), b_dev, c.dinv.data(), bj, c.xp.data(), c.r.data(), c.z.data(), c.pv.data(),
+          kPkVs == 4 ? c.z4.data() : nullptr, kPkVs == 4 ? c.p4a.data() : nullptr);
       // ||b|| and rho = r.z over the permuted r = b
       k_dot2<<<nblocks, threads, 0, ls(c)>>>(pb, c.r.data(), c.r.data(), c.r.data(), c.z.data(), c.partials.data(),
                                          &c.pcg->counter, dots, c.comm, c.nparts);
@@ -1609,6 +1665,11 @@ PcgResult pcg_solve(Ctx& c, const double* b_dev, const weft_pcg_config& cfg, dou
   if (persistent) {
     args.A.cols = c.A.colp.data();  // columns as positions
     args.x = c.xp.data();
+    if (kPkVs == 4) {  // gathered vectors 32 bytes per row
+      args.z = c.z4.data();
+      args.p = c.p4a.data();
+      args.p2 = c.p4b.data();
+    }
     args.q_msw = msw;
     // z and p (48 B per row) are gathered every iteration: pin them in L2
     // while they fit in ~60 MB of its 126 MB, a proportional fraction beyond
