@@ -38,7 +38,8 @@ struct SellMatrix {
 };
 
 constexpr int kColMask = 0x0FFFFFFF;
-constexpr int kSigma = 256;  // sorting window of the SELL-32-sigma layout
+constexpr int kSigma = 256;         // sorting window of the SELL-32-sigma layout
+constexpr int kSigmaContacts = 512; // ... of a system with contact elements (longer rows to group)
 
 // Value index of component q (row-major 3x3) of the slot at column-index
 // position `at` of a row with lane = row % 32: the nine components of one
@@ -230,7 +231,7 @@ inline cudaStream_t ls(Ctx& c) {
 // ---- entry points implemented across the .cu files
 void set_matrix_csr(Ctx& c, int rows, const int64_t* row_ptr, const int32_t* cols, const double* vals);
 // Window starts (local rows) of the sigma sort: partition-aligned chunks.
-std::vector<int32_t> sigma_windows(const Ctx& c);
+std::vector<int32_t> sigma_windows(const Ctx& c, int win = kSigma);
 // Device sigma layout from per-row lengths (local row order): fills A.perm,
 // A.pos and A.rowlen (by position).
 void build_sigma(Ctx& c, const int32_t* len_row);

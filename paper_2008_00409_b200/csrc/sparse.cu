@@ -468,11 +468,11 @@ void set_rows(Ctx& c, int p) {
   c.row1 = c.pm.end(c.part_end - 1);
 }
 
-std::vector<int32_t> sigma_windows(const Ctx& c) {
+std::vector<int32_t> sigma_windows(const Ctx& c, int win) {
   std::vector<int32_t> w;
   for (int d = c.part_begin; d < c.part_end; ++d) {
     const int b = c.pm.begin(d) - c.row0, e = c.pm.end(d) - c.row0;
-    for (int s = b; s < e; s += kSigma) w.push_back(s);
+    for (int s = b; s < e; s += win) w.push_back(s);
   }
   w.push_back(c.row1 - c.row0);
   return w;
@@ -480,10 +480,11 @@ std::vector<int32_t> sigma_windows(const Ctx& c) {
 
 // One block per window: stable sort of its rows by descending length
 // (rank = rows that are longer, or as long and earlier).
-__global__ void __launch_bounds__(kSigma) k_sigma(const int32_t* __restrict__ wstart, const int32_t* __restrict__ len,
-                                                  int32_t* __restrict__ perm, int32_t* __restrict__ pos,
-                                                  int32_t* __restrict__ len_m) {
-  __shared__ int32_t sl[kSigma];
+template <int W>
+__global__ void __launch_bounds__(W) k_sigma(const int32_t* __restrict__ wstart, const int32_t* __restrict__ len,
+                                             int32_t* __restrict__ perm, int32_t* __restrict__ pos,
+                                             int32_t* __restrict__ len_m) {
+  __shared__ int32_t sl[W];
   const int a = wstart[blockIdx.x], n = wstart[blockIdx.x + 1] - a;
   const int t = threadIdx.x;
   if (t < n) sl[t] = len[a + t];
@@ -499,15 +500,24 @@ __global__ void __launch_bounds__(kSigma) k_sigma(const int32_t* __restrict__ ws
 
 void build_sigma(Ctx& c, const int32_t* len_row) {
   SellMatrix& A = c.A;
-  const std::vector<int32_t> w = sigma_windows(c);
+  // Contact rows carry up to 3x the slots of grid rows: a wider sorting
+  // window groups them into fewer, fuller slices (config D contacts-mode
+  // solve 49.0 -> 44.5 ms; the contact-free matrix is best at 256).
+  const int win = c.n_contacts > 0 ? kSigmaContacts : kSigma;
+  const std::vector<int32_t> w = sigma_windows(c, win);
   DBuf<int32_t>& wd = c.sc_sigma_w;
   wd.upload(w.data(), w.size(), c.stream);
   A.perm.resize(static_cast<size_t>(A.rows) + 1);
   A.pos.resize(static_cast<size_t>(A.rows) + 1);
   A.rowlen.resize(static_cast<size_t>(A.rows) + 1);
-  if (w.size() > 1)
-    k_sigma<<<static_cast<int>(w.size()) - 1, kSigma, 0, ls(c)>>>(wd.data(), len_row, A.perm.data(), A.pos.data(),
-                                                                  A.rowlen.data());
+  if (w.size() > 1) {
+    if (win == kSigmaContacts)
+      k_sigma<kSigmaContacts><<<static_cast<int>(w.size()) - 1, kSigmaContacts, 0, ls(c)>>>(
+          wd.data(), len_row, A.perm.data(), A.pos.data(), A.rowlen.data());
+    else
+      k_sigma<kSigma><<<static_cast<int>(w.size()) - 1, kSigma, 0, ls(c)>>>(wd.data(), len_row, A.perm.data(),
+                                                                           A.pos.data(), A.rowlen.data());
+  }
   WG_CUDA(cudaGetLastError());
   WG_CUDA(cudaStreamSynchronize(c.stream));  // wd dies here
 }
