@@ -1167,7 +1167,7 @@ __device__ __forceinline__ void vstore3(double* v, int i, double a, double b, do
   }
 }
 
-template <int PMode>
+template <int PMode, int kUnroll>
 __device__ __forceinline__ void row_product_cg(const SellView& A, int r, const double* __restrict__ z,
                                                const double* __restrict__ pold, double beta, double& y0, double& y1,
                                                double& y2, float vec_frac) {
@@ -1181,7 +1181,7 @@ __device__ __forceinline__ void row_product_cg(const SellView& A, int r, const d
   const int64_t base = A.slice_off[r >> 5] + (r & 31);
   double a0 = 0.0, a1 = 0.0, a2 = 0.0;
   int cn = len > 0 ? (WEFT_MAT_LD(A.cols + base) & kColMask) : 0;
-#pragma unroll kPkUnroll
+#pragma unroll kUnroll
   for (int k = 0; k < len; ++k) {
     const int64_t at = base + (int64_t)k * kSlice;
     const int c = cn;
@@ -1240,7 +1240,10 @@ __device__ __forceinline__ void all_blocks_sum(const double* partials, int n, do
 
 // kQs: q = A p of the warp's rows stays in shared memory between phase A
 // and phase B (phase B then walks the same slice runs): q never touches HBM.
-template <bool kQs>
+// kUnroll: slots per row-loop trip. Grid rows (<= 13 slots) run best at 1;
+// the long contact rows (up to ~40 slots) need the deeper unroll to keep
+// enough gathers in flight (config D contacts mode: 44.1 -> 36.9 ms at 4).
+template <bool kQs, int kUnroll>
 __global__ void __launch_bounds__(kPersistThreads, WEFT_PERSIST_MINB) k_pcg_persistent(const PcgArgs* __restrict__ args, PcgState* st) {
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
@@ -1306,8 +1309,8 @@ __global__ void __launch_bounds__(kPersistThreads, WEFT_PERSIST_MINB) k_pcg_pers
       const int i = sl * kSlice + lane;  // matrix position == vector index (position space)
       if (i < rows) {
         double y0, y1, y2;
-        if (first) row_product_cg<1>(A, i, z, pcur, beta, y0, y1, y2, g.vec_el_frac);
-        else row_product_cg<2>(A, i, z, pcur, beta, y0, y1, y2, g.vec_el_frac);
+        if (first) row_product_cg<1, kUnroll>(A, i, z, pcur, beta, y0, y1, y2, g.vec_el_frac);
+        else row_product_cg<2, kUnroll>(A, i, z, pcur, beta, y0, y1, y2, g.vec_el_frac);
         double p0, p1, p2;
         vload3(z, i, p0, p1, p2);
         if (!first) {
@@ -1641,7 +1644,11 @@ PcgResult pcg_solve(Ctx& c, const double* b_dev, const weft_pcg_config& cfg, dou
   const int nblocks2 = pb2.bstart[pb2.n];
   int pgrid = 0, msw = 0;
   size_t qs_bytes = 0;
-  auto pkern = k_pcg_persistent<false>;
+  static const int unroll_env = std::getenv("WEFT_PCG_UNROLL") ? std::atoi(std::getenv("WEFT_PCG_UNROLL")) : 0;
+  const int unroll = unroll_env ? unroll_env : (c.n_contacts > 0 ? 4 : kPkUnroll);
+  auto pkern = unroll == 8 ? k_pcg_persistent<false, 8>
+                           : (unroll == 4 ? k_pcg_persistent<false, 4>
+                                          : (unroll == 2 ? k_pcg_persistent<false, 2> : k_pcg_persistent<false, 1>));
   if (persistent) {
     // q in shared memory when the warps' slice runs fit at two CTAs per SM
     int sms = 0;
@@ -1657,7 +1664,9 @@ PcgResult pcg_solve(Ctx& c, const double* b_dev, const weft_pcg_config& cfg, dou
     // memory (29.2 -> 28.0 ms).
     const bool qs = !qs_off && c.n_contacts == 0 && qs_bytes <= 100 * 1024;
     if (qs) {
-      pkern = k_pcg_persistent<true>;
+      pkern = unroll == 8 ? k_pcg_persistent<true, 8>
+                          : (unroll == 4 ? k_pcg_persistent<true, 4>
+                                         : (unroll == 2 ? k_pcg_persistent<true, 2> : k_pcg_persistent<true, 1>));
       WG_CUDA(cudaFuncSetAttribute(pkern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(qs_bytes)));
     } else {
       qs_bytes = 0;
