@@ -80,3 +80,15 @@ def test_reference_scene_files_first_frames(S, path):
         assert rel(x.reshape(-1), xr) <= 1e-8
     rs.close()
     sim.close()
+
+
+def test_obstacle_positions_required_each_step(S):
+    """weft_gpu_sim_set_obstacles is per step: a step without it is refused
+    (WEFT_ERR_INVALID), like a Simulator that never moved its obstacles."""
+    from paper_2008_00409_b200 import weft
+    sc = S.parse_scene(scene_text("drape_sphere"))
+    sim = S.Simulator(sc)
+    sim.step()
+    with pytest.raises(weft.Error, match="obstacle positions missing"):
+        sim.engine.sim_step(sim.params)
+    sim.close()
