@@ -180,6 +180,11 @@ __device__ __forceinline__ void gather3(int c, int g, const double* __restrict__
   }
 }
 
+#ifndef WEFT_MG_UNROLL
+#define WEFT_MG_UNROLL 2
+#endif
+constexpr int kMgUnroll = WEFT_MG_UNROLL;  // slots per trip of the multi-group row loop
+
 // Row product of LOCAL row lr in the reference order.
 // PMode 0: x given. PMode 1: x = z (first PCG iteration, p = z).
 // PMode 2: x = z + beta * p_old on the fly (PCG p update).
@@ -195,7 +200,7 @@ __device__ __forceinline__ void row_product(const SellView& A, int lr, int ngrou
   int cg = 0;
   unsigned seen = 0;
   y0 = y1 = y2 = 0.0;
-#pragma unroll 2
+#pragma unroll kMgUnroll
   for (int k = 0; k < len; ++k) {
     const int64_t at = base + (int64_t)k * kSlice;
     const int packed = __ldg(A.cols + at);
