@@ -64,11 +64,45 @@ def dist_env():
 
 # ---------------------------------------------------------------- clocks
 class Clocks:
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+    """SM clocks and throttle reasons sampled DURING the timed region: NVML
+    every 10 ms in a background thread (short timed regions still get many
+    samples), `nvidia-smi -lms 100` when NVML is unavailable."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks.mem,power.draw,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
+    # nvmlClocksEventReason* bits
+    BITS = {"sw_power_cap": 0x4, "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40}
 
     def __init__(self, device: int):
+        import threading
+        self.p = None
+        self.sm, self.mx, self.reasons = [], [], set()
+        self.stop_evt = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            get_reasons = getattr(pynvml, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                pynvml.nvmlDeviceGetCurrentClocksThrottleReasons
+
+            def run():
+                while not self.stop_evt.is_set():
+                    self.sm.append(float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)))
+                    self.mx.append(float(mx))
+                    bits = get_reasons(h)
+                    for name, b in self.BITS.items():
+                        if bits & b:
+                            self.reasons.add(name)
+                    self.stop_evt.wait(0.01)
+
+            self.t = threading.Thread(target=run, daemon=True)
+            self.t.start()
+            self.nvml = True
+            return
+        except Exception:
+            self.nvml = False
         self.f = tempfile.NamedTemporaryFile("w+", delete=False)
         try:
             self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
@@ -77,6 +111,12 @@ class Clocks:
             self.p = None
 
     def stop(self) -> dict:
+        if self.nvml:
+            self.stop_evt.set()
+            self.t.join()
+            return {"sm_mhz": statistics.median(self.sm) if self.sm else None,
+                    "sm_max_mhz": max(self.mx) if self.mx else None, "reasons": sorted(self.reasons),
+                    "samples": len(self.sm), "source": "nvml 10 ms"}
         if self.p is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         time.sleep(0.15)
@@ -99,7 +139,7 @@ class Clocks:
                     reasons.add(name)
         os.unlink(self.f.name)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm), "source": "nvidia-smi 100 ms"}
 
 
 def peaks():
