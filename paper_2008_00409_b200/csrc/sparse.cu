@@ -1132,13 +1132,10 @@ constexpr int kPkUnroll = WEFT_PK_UNROLL;
 #define WEFT_PK_XDEFER 1
 #endif
 
-// WEFT_PK_V4=1: inside the persistent solve the gathered vectors z and p are
-// stored 32 bytes per row (xyz + pad), so a column gather is ONE 256-bit
-// load (LDG.256, one sector) instead of three 8-byte loads.
-#ifndef WEFT_PK_V4
-#define WEFT_PK_V4 1
-#endif
-constexpr int kPkVs = WEFT_PK_V4 ? 4 : 3;  // doubles per row of z / p in the persistent solve
+// Vs = 4: inside the persistent solve the gathered vectors z and p are stored
+// 32 bytes per row (xyz + pad), so a column gather is ONE 256-bit load
+// (LDG.256, one sector) instead of three 8-byte loads (chosen per solve,
+// pcg_solve's v4).
 __device__ __forceinline__ void ld4_cg(const double* p, uint64_t pol, double& a, double& b, double& c) {
   double d;
   asm volatile("ld.global.cg.L2::cache_hint.v4.f64 {%0,%1,%2,%3}, [%4], %5;"
@@ -1152,9 +1149,10 @@ __device__ __forceinline__ void ld4_cg(const double* p, double& a, double& b, do
 __device__ __forceinline__ void st4_cg(double* p, double a, double b, double c) {
   asm volatile("st.global.cg.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(0.0) : "memory");
 }
-// own-row / gathered vector access of the persistent solve (stride kPkVs)
+// own-row / gathered vector access of the persistent solve (stride Vs)
+template <int Vs>
 __device__ __forceinline__ void vload3(const double* v, int i, double& a, double& b, double& c) {
-  if constexpr (kPkVs == 4) {
+  if constexpr (Vs == 4) {
     ld4_cg(v + 4 * (size_t)i, a, b, c);
   } else {
     a = __ldcg(v + 3 * (size_t)i);
@@ -1162,8 +1160,9 @@ __device__ __forceinline__ void vload3(const double* v, int i, double& a, double
     c = __ldcg(v + 3 * (size_t)i + 2);
   }
 }
+template <int Vs>
 __device__ __forceinline__ void vstore3(double* v, int i, double a, double b, double c) {
-  if constexpr (kPkVs == 4) {
+  if constexpr (Vs == 4) {
     st4_cg(v + 4 * (size_t)i, a, b, c);
   } else {
     __stcg(v + 3 * (size_t)i, a);
@@ -1172,7 +1171,7 @@ __device__ __forceinline__ void vstore3(double* v, int i, double a, double b, do
   }
 }
 
-template <int PMode, int kUnroll>
+template <int PMode, int kUnroll, int Vs>
 __device__ __forceinline__ void row_product_cg(const SellView& A, int r, const double* __restrict__ z,
                                                const double* __restrict__ pold, double beta, double& y0, double& y1,
                                                double& y2, float vec_frac) {
@@ -1195,9 +1194,10 @@ __device__ __forceinline__ void row_product_cg(const SellView& A, int r, const d
     const double v0 = WEFT_MAT_LD(v), v1 = WEFT_MAT_LD(v + 32), v2 = WEFT_MAT_LD(v + 64);
     const double v3 = WEFT_MAT_LD(v + 96), v4 = WEFT_MAT_LD(v + 128), v5 = WEFT_MAT_LD(v + 160);
     const double v6 = WEFT_MAT_LD(v + 192), v7 = WEFT_MAT_LD(v + 224), v8 = WEFT_MAT_LD(v + 256);
-#if WEFT_PK_V4 && WEFT_VEC_EL
+#if WEFT_VEC_EL
     double x0, x1, x2;
-    ld4_cg(z + 4 * (size_t)c, vpol, x0, x1, x2);
+    if constexpr (Vs == 4) {
+      ld4_cg(z + 4 * (size_t)c, vpol, x0, x1, x2);
     if (PMode == 2) {
       double q0, q1, q2;
       ld4_cg(pold + 4 * (size_t)c, vpol, q0, q1, q2);
@@ -1205,12 +1205,22 @@ __device__ __forceinline__ void row_product_cg(const SellView& A, int r, const d
       x1 = x1 + beta * q1;
       x2 = x2 + beta * q2;
     }
+    } else {
+      x0 = WEFT_VEC_LD(z + 3 * c);
+      x1 = WEFT_VEC_LD(z + 3 * c + 1);
+      x2 = WEFT_VEC_LD(z + 3 * c + 2);
+      if (PMode == 2) {
+        x0 = x0 + beta * WEFT_VEC_LD(pold + 3 * c);
+        x1 = x1 + beta * WEFT_VEC_LD(pold + 3 * c + 1);
+        x2 = x2 + beta * WEFT_VEC_LD(pold + 3 * c + 2);
+      }
+    }
 #else
-    double x0 = WEFT_VEC_LD(z + kPkVs * c), x1 = WEFT_VEC_LD(z + kPkVs * c + 1), x2 = WEFT_VEC_LD(z + kPkVs * c + 2);
+    double x0 = WEFT_VEC_LD(z + Vs * c), x1 = WEFT_VEC_LD(z + Vs * c + 1), x2 = WEFT_VEC_LD(z + Vs * c + 2);
     if (PMode == 2) {
-      x0 = x0 + beta * WEFT_VEC_LD(pold + kPkVs * c);
-      x1 = x1 + beta * WEFT_VEC_LD(pold + kPkVs * c + 1);
-      x2 = x2 + beta * WEFT_VEC_LD(pold + kPkVs * c + 2);
+      x0 = x0 + beta * WEFT_VEC_LD(pold + Vs * c);
+      x1 = x1 + beta * WEFT_VEC_LD(pold + Vs * c + 1);
+      x2 = x2 + beta * WEFT_VEC_LD(pold + Vs * c + 2);
     }
 #endif
     a0 = a0 + ((v0 * x0 + v1 * x1) + v2 * x2);
@@ -1248,7 +1258,7 @@ __device__ __forceinline__ void all_blocks_sum(const double* partials, int n, do
 // kUnroll: slots per row-loop trip. Grid rows (<= 13 slots) run best at 1;
 // the long contact rows (up to ~40 slots) need the deeper unroll to keep
 // enough gathers in flight (config D contacts mode: 44.1 -> 36.9 ms at 4).
-template <bool kQs, int kUnroll>
+template <bool kQs, int kUnroll, int Vs>
 __global__ void __launch_bounds__(kPersistThreads, WEFT_PERSIST_MINB) k_pcg_persistent(const PcgArgs* __restrict__ args, PcgState* st) {
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
@@ -1314,13 +1324,13 @@ __global__ void __launch_bounds__(kPersistThreads, WEFT_PERSIST_MINB) k_pcg_pers
       const int i = sl * kSlice + lane;  // matrix position == vector index (position space)
       if (i < rows) {
         double y0, y1, y2;
-        if (first) row_product_cg<1, kUnroll>(A, i, z, pcur, beta, y0, y1, y2, g.vec_el_frac);
-        else row_product_cg<2, kUnroll>(A, i, z, pcur, beta, y0, y1, y2, g.vec_el_frac);
+        if (first) row_product_cg<1, kUnroll, Vs>(A, i, z, pcur, beta, y0, y1, y2, g.vec_el_frac);
+        else row_product_cg<2, kUnroll, Vs>(A, i, z, pcur, beta, y0, y1, y2, g.vec_el_frac);
         double p0, p1, p2;
-        vload3(z, i, p0, p1, p2);
+        vload3<Vs>(z, i, p0, p1, p2);
         if (!first) {
           double o0, o1, o2;
-          vload3(pcur, i, o0, o1, o2);
+          vload3<Vs>(pcur, i, o0, o1, o2);
           p0 = p0 + beta * o0;
           p1 = p1 + beta * o1;
           p2 = p2 + beta * o2;
@@ -1335,7 +1345,7 @@ __global__ void __launch_bounds__(kPersistThreads, WEFT_PERSIST_MINB) k_pcg_pers
           __stcg(q + 3 * i + 1, y1);
           __stcg(q + 3 * i + 2, y2);
         }
-        vstore3(pnew, i, p0, p1, p2);
+        vstore3<Vs>(pnew, i, p0, p1, p2);
         s1[0] = s1[0] + ((p0 * y0 + p1 * y1) + p2 * y2);
       }
     }
@@ -1383,12 +1393,12 @@ __global__ void __launch_bounds__(kPersistThreads, WEFT_PERSIST_MINB) k_pcg_pers
       }
       if (x_now) {
         double xv[3], pv[3];
-        vload3(pnew, i, pv[0], pv[1], pv[2]);
+        vload3<Vs>(pnew, i, pv[0], pv[1], pv[2]);
 #pragma unroll
         for (int c = 0; c < 3; ++c) xv[c] = PB_LD(x + 3 * i + c);
         if (WEFT_PK_XDEFER) {
           double po[3];
-          vload3(pcur, i, po[0], po[1], po[2]);
+          vload3<Vs>(pcur, i, po[0], po[1], po[2]);
 #pragma unroll
           for (int c = 0; c < 3; ++c) xv[c] = xv[c] + alpha_prev * po[c];
         }
@@ -1432,7 +1442,7 @@ __global__ void __launch_bounds__(kPersistThreads, WEFT_PERSIST_MINB) k_pcg_pers
       }
 #pragma unroll
       for (int c = 0; c < 3; ++c) __stcg(r + 3 * i + c, rv[c]);
-      vstore3(z, i, z0, z1, z2);
+      vstore3<Vs>(z, i, z0, z1, z2);
       s2[0] = s2[0] + ((rv[0] * rv[0] + rv[1] * rv[1]) + rv[2] * rv[2]);
       s2[1] = s2[1] + ((rv[0] * z0 + rv[1] * z1) + rv[2] * z2);
     }
@@ -1483,7 +1493,7 @@ __global__ void __launch_bounds__(kPersistThreads, WEFT_PERSIST_MINB) k_pcg_pers
     const int pb_step = kQs ? kSlice : gridDim.x * blockDim.x;
     for (int i = pb_begin; i < pb_end; i += pb_step) {
       double pv[3];
-      vload3(pnew, i, pv[0], pv[1], pv[2]);
+      vload3<Vs>(pnew, i, pv[0], pv[1], pv[2]);
 #pragma unroll
       for (int c = 0; c < 3; ++c) __stcg(x + 3 * i + c, __ldcg(x + 3 * i + c) + alpha_prev * pv[c]);
     }
@@ -1527,7 +1537,7 @@ __global__ void k_pcg_init_pos(int rows, const int32_t* __restrict__ perm, const
   z[3 * m + 1] = z1;
   z[3 * m + 2] = z2;
   p[3 * m] = p[3 * m + 1] = p[3 * m + 2] = 0.0;
-  if (z4) {  // the persistent solve's 32-byte-per-row copies (kPkVs == 4)
+  if (z4) {  // the persistent solve's 32-byte-per-row copies (v4)
     z4[4 * (size_t)m] = z0;
     z4[4 * (size_t)m + 1] = z1;
     z4[4 * (size_t)m + 2] = z2;
@@ -1568,6 +1578,11 @@ PcgResult pcg_solve(Ctx& c, const double* b_dev, const weft_pcg_config& cfg, dou
   // POSITION space (vectors and columns permuted to the SELL-32-sigma order,
   // b gathered in, x scattered out), so every vector access is coalesced.
   const bool persistent = c.go.n == 1 && c.world == 1 && c.use_persistent;
+  // z / p at 32 bytes per row inside the persistent solve (one LDG.256 per
+  // gather) while 64 B per row of them fit ~100 MB of L2; beyond (the 5-10 M
+  // triangle configs) the 24-byte rows move fewer bytes (E5: 97.5 vs 103.6 ms)
+  static const int vs_env = std::getenv("WEFT_PCG_VS") ? std::atoi(std::getenv("WEFT_PCG_VS")) : 0;
+  const bool v4 = vs_env ? vs_env == 4 : (64.0 * rows <= 100e6);
   if (!c.pcg) {
     WG_CUDA(cudaMalloc(&c.pcg, sizeof(PcgState)));
     WG_CUDA(cudaHostAlloc(&c.pcg_host, sizeof(PcgState), cudaHostAllocDefault));
@@ -1603,14 +1618,14 @@ PcgResult pcg_solve(Ctx& c, const double* b_dev, const weft_pcg_config& cfg, dou
       c.dinv6.resize(6 * static_cast<size_t>(rows) + 6);
       WG_CUDA(cudaMemsetAsync(dinv_asym, 0, sizeof(int), s));
       if (bj) k_dinv<true><<<div_up(rows, threads), threads, 0, ls(c)>>>(A, c.dinv.data(), c.dinv6.data(), dinv_asym);
-      if (kPkVs == 4) {
+      if (v4) {
         c.z4.resize(4 * static_cast<size_t>(rows) + 4);
         c.p4a.resize(4 * static_cast<size_t>(rows) + 4);
         c.p4b.resize(4 * static_cast<size_t>(rows) + 4);
       }
       k_pcg_init_pos<<<div_up(rows, threads), threads, 0, ls(c)>>>(
           rows, c.A.perm.data(), b_dev, c.dinv.data(), bj, c.xp.data(), c.r.data(), c.z.data(), c.pv.data(),
-          kPkVs == 4 ? c.z4.data() : nullptr, kPkVs == 4 ? c.p4a.data() : nullptr);
+          v4 ? c.z4.data() : nullptr, v4 ? c.p4a.data() : nullptr);
       // ||b|| and rho = r.z over the permuted r = b
       k_dot2<<<nblocks, threads, 0, ls(c)>>>(pb, c.r.data(), c.r.data(), c.r.data(), c.z.data(), c.partials.data(),
                                          &c.pcg->counter, dots, c.comm, c.nparts);
@@ -1650,10 +1665,16 @@ PcgResult pcg_solve(Ctx& c, const double* b_dev, const weft_pcg_config& cfg, dou
   int pgrid = 0, msw = 0;
   size_t qs_bytes = 0;
   static const int unroll_env = std::getenv("WEFT_PCG_UNROLL") ? std::atoi(std::getenv("WEFT_PCG_UNROLL")) : 0;
-  const int unroll = unroll_env ? unroll_env : (c.n_contacts > 0 ? 4 : kPkUnroll);
-  auto pkern = unroll == 8 ? k_pcg_persistent<false, 8>
-                           : (unroll == 4 ? k_pcg_persistent<false, 4>
-                                          : (unroll == 2 ? k_pcg_persistent<false, 2> : k_pcg_persistent<false, 1>));
+  const int unroll = (unroll_env ? unroll_env : (c.n_contacts > 0 ? 4 : kPkUnroll)) >= 4 ? 4 : 1;
+  auto pick = [&](bool q) -> decltype(&k_pcg_persistent<false, 1, 3>) {
+    if (v4) {
+      if (unroll == 4) return q ? k_pcg_persistent<true, 4, 4> : k_pcg_persistent<false, 4, 4>;
+      return q ? k_pcg_persistent<true, 1, 4> : k_pcg_persistent<false, 1, 4>;
+    }
+    if (unroll == 4) return q ? k_pcg_persistent<true, 4, 3> : k_pcg_persistent<false, 4, 3>;
+    return q ? k_pcg_persistent<true, 1, 3> : k_pcg_persistent<false, 1, 3>;
+  };
+  auto pkern = pick(false);
   if (persistent) {
     // q in shared memory when the warps' slice runs fit at two CTAs per SM
     int sms = 0;
@@ -1669,9 +1690,7 @@ PcgResult pcg_solve(Ctx& c, const double* b_dev, const weft_pcg_config& cfg, dou
     // memory (29.2 -> 28.0 ms).
     const bool qs = !qs_off && c.n_contacts == 0 && qs_bytes <= 100 * 1024;
     if (qs) {
-      pkern = unroll == 8 ? k_pcg_persistent<true, 8>
-                          : (unroll == 4 ? k_pcg_persistent<true, 4>
-                                         : (unroll == 2 ? k_pcg_persistent<true, 2> : k_pcg_persistent<true, 1>));
+      pkern = pick(true);
       WG_CUDA(cudaFuncSetAttribute(pkern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(qs_bytes)));
     } else {
       qs_bytes = 0;
@@ -1689,7 +1708,7 @@ PcgResult pcg_solve(Ctx& c, const double* b_dev, const weft_pcg_config& cfg, dou
   if (persistent) {
     args.A.cols = c.A.colp.data();  // columns as positions
     args.x = c.xp.data();
-    if (kPkVs == 4) {  // gathered vectors 32 bytes per row
+    if (v4) {  // gathered vectors 32 bytes per row
       args.z = c.z4.data();
       args.p = c.p4a.data();
       args.p2 = c.p4b.data();
