@@ -508,7 +508,6 @@ __global__ void k_merge_fill(int row0, int nloc, MergeIn m, PartMap pm, GroupOrd
 // Pattern of the contact elements (rows/cols among non-pinned vertices).
 static void build_layout(Ctx& c) {
   cudaStream_t s = c.stream;
-  const int p = c.p;
   DBuf<int64_t>& cptr = c.sc_lay_cptr;
   DBuf<int32_t>& ccol = c.sc_lay_ccol;
   MergeIn m{c.spat_ptr.data(), c.spat.data(), nullptr, nullptr};

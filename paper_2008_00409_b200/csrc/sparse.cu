@@ -195,7 +195,6 @@ __device__ __forceinline__ void row_product(const SellView& A, int lr, int ngrou
                                             unsigned long long vexp = 0) {
   const int len = A.rowlen[lr];
   const int64_t base = A.slice_off[lr >> 5] + (lr & 31);
-  const int64_t T = A.total;
   double a0 = 0.0, a1 = 0.0, a2 = 0.0;
   int cg = 0;
   unsigned seen = 0;
@@ -260,7 +259,6 @@ __device__ __forceinline__ void row_product_1(const SellView& A, int r, const do
                                               double& y2) {
   const int len = A.rowlen[r];
   const int64_t base = A.slice_off[r >> 5] + (r & 31);
-  const int64_t T = A.total;
   double a0 = 0.0, a1 = 0.0, a2 = 0.0;
   SP_POLICIES
   int cn = len > 0 ? (SP_MLD(A.cols + base) & kColMask) : 0;
@@ -317,7 +315,6 @@ __device__ __forceinline__ void row_product_pair(const SellView& A, int r, bool 
   const int len = valid ? A.rowlen[r] : 0;
   const int kmax = __reduce_max_sync(0xffffffffu, len);
   const int64_t base = valid ? A.slice_off[r >> 5] + (r & 31) : 0;
-  const int64_t T = A.total;
   double a0 = 0.0, a1 = 0.0, a2 = 0.0;
   int cn = par < len ? (WEFT_LDS(A.cols + base + (int64_t)par * kSlice) & kColMask) : 0;
   for (int k0 = 0; k0 < kmax; k0 += 2) {
@@ -1136,16 +1133,20 @@ constexpr int kPkUnroll = WEFT_PK_UNROLL;
 // 32 bytes per row (xyz + pad), so a column gather is ONE 256-bit load
 // (LDG.256, one sector) instead of three 8-byte loads (chosen per solve,
 // pcg_solve's v4).
+#pragma nv_diag_suppress 550  // the pad lane of the 256-bit loads is never read
 __device__ __forceinline__ void ld4_cg(const double* p, uint64_t pol, double& a, double& b, double& c) {
-  double d;
+  double d;  // the pad lane
   asm volatile("ld.global.cg.L2::cache_hint.v4.f64 {%0,%1,%2,%3}, [%4], %5;"
                : "=d"(a), "=d"(b), "=d"(c), "=d"(d)
                : "l"(p), "l"(pol));
+  (void)d;
 }
 __device__ __forceinline__ void ld4_cg(const double* p, double& a, double& b, double& c) {
-  double d;
+  double d;  // the pad lane
   asm volatile("ld.global.cg.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p));
+  (void)d;
 }
+#pragma nv_diag_default 550
 __device__ __forceinline__ void st4_cg(double* p, double a, double b, double c) {
   asm volatile("st.global.cg.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(0.0) : "memory");
 }
