@@ -421,9 +421,9 @@ def gpu_arm(args, rank, world, local):
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(args.steps):
-            eng.sim_set_state(xh, vh)  # H2D of the step's inputs
-            eng.sim_step(params)
-            eng.sim_get_state(xo, vo)  # D2H of the step's result
+            # H2D of the step's inputs, the step, D2H of its result (one call:
+            # weft_gpu_sim_step_io overlaps the copies with the broad phases)
+            eng.sim_step_io(xh, vh, params, xo, vo)
         e1.record(stream)
         e1.synchronize()
         barrier()

@@ -397,6 +397,15 @@ weft_status weft_gpu_sim_set_obstacles(weft_gpu_ctx* ctx, double dt, const doubl
  * of step_system at x, PCG, v += dv, x_cand = x + dt v, CCD grid +
  * candidates on (x, x_cand), commit x = x_cand. */
 weft_status weft_gpu_sim_step(weft_gpu_ctx* ctx, const weft_sim_params* params, weft_step_report* report);
+/* One step with the state in host buffers (the e2e path of a caller that
+ * keeps x, v on the host): uploads x_in, v_in, steps, and writes x_out, v_out
+ * — equivalent to sim_set_state + sim_step + sim_get_state (same results),
+ * with the v upload hidden behind the DCD broad phase and the read-back behind
+ * the CCD broad phase (one rank, no obstacles; otherwise exactly that
+ * sequence). Requires a prior weft_gpu_sim_set_state. */
+weft_status weft_gpu_sim_step_io(weft_gpu_ctx* ctx, const double* x_in, const double* v_in,
+                                 const weft_sim_params* params, double* x_out, double* v_out,
+                                 weft_step_report* report);
 /* Reads the state back (either pointer may be NULL). */
 weft_status weft_gpu_sim_get_state(weft_gpu_ctx* ctx, double* x, double* v);
 

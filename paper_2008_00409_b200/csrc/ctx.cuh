@@ -205,6 +205,10 @@ struct Ctx {
   DBuf<double> soup_mass;             // cloth masses, 1.0 for obstacle vertices
   bool has_state = false;
   bool obstacles_set = false;         // obstacle positions of this step given
+  // weft_gpu_sim_step_io: the step's host buffers (null outside that call)
+  const double* io_vin = nullptr;
+  double* io_xout = nullptr;
+  double* io_vout = nullptr;
 
   // impact zones (zones.cu): accumulated impacts, zone structure, solver scratch
   DBuf<unsigned long long> zn_acc_keys, zn_acc_sorted, zn_tmp_keys;

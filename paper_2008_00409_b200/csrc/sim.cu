@@ -352,6 +352,24 @@ weft_status weft_gpu_sim_step(weft_gpu_ctx* ctx, const weft_sim_params* prm, wef
       weft_gpu::fill_matrix(c, c.sim_x.data(), c.x_adv.data(), c.sim_v.data(), dt, prm->jac_mode);
       WG_CUDA(cudaEventRecord(ev[2], s));
       WG_CUDA(cudaEventRecord(ev[1], s));
+    } else if (c.io_vin) {
+    // weft_gpu_sim_step_io, one rank: x arrived on the main stream, v is still
+    // in flight on the side stream — the DCD broad phase (x only) runs first
+    // and hides the v upload; then the assembly at (x, v)
+    if (c.n_contacts) weft_gpu::finish_contacts(c, 0);
+    WG_CUDA(cudaEventRecord(c.ev_side[0], s));
+    weft_gpu::build_grid(c, c.sim_x.data(), c.sim_x.data(), WEFT_DISCRETE, prm->thickness, prm->cell_scale);
+    share(c.grid_total, wb, we);
+    dcd = weft_gpu::candidates(c, wb, we, nullptr, /*count_only=*/true);
+    WG_CUDA(cudaEventRecord(c.ev_side[1], s));
+    WG_CUDA(cudaStreamWaitEvent(s, c.ev_side[2], 0));  // v uploaded
+    WG_CUDA(cudaEventRecord(ev[0], s));
+    c.x_adv.resize(static_cast<size_t>(n));
+    weft_gpu::k_advance<<<weft_gpu::div_up(n, 256), 256, 0, ls(c)>>>(n, c.sim_x.data(), c.sim_v.data(), dt,
+                                                                  c.x_adv.data());
+    weft_gpu::fill_matrix(c, c.sim_x.data(), c.x_adv.data(), c.sim_v.data(), dt, prm->jac_mode);
+    WG_CUDA(cudaEventRecord(ev[2], s));
+    WG_CUDA(cudaEventRecord(ev[1], s));
     } else {
     if (c.n_contacts) weft_gpu::finish_contacts(c, 0);  // no stale contacts from a contacts-mode step
     // 1 + 2. The proximity broad phase (DCD) on x and the assembly of
@@ -399,6 +417,13 @@ weft_status weft_gpu_sim_step(weft_gpu_ctx* ctx, const weft_sim_params* prm, wef
                                                                           c.xs.data(), dt, c.sim_xc.data());
     if (c.world > 1) weft_gpu::exchange_state(c);  // all rows of v and x_cand on every rank
     WG_CUDA(cudaEventRecord(ev[4], s));
+    const bool io_out_early = c.io_xout && !contacts;  // v and x_cand are final here
+    if (io_out_early) {  // read them back on the side stream while the CCD broad phase runs
+      WG_CUDA(cudaStreamWaitEvent(c.side, ev[4], 0));
+      WG_CUDA(cudaMemcpyAsync(c.io_vout, c.sim_v.data(), n * sizeof(double), cudaMemcpyDefault, c.side));
+      WG_CUDA(cudaMemcpyAsync(c.io_xout, c.sim_xc.data(), n * sizeof(double), cudaMemcpyDefault, c.side));
+      WG_CUDA(cudaEventRecord(c.ev_side[3], c.side));
+    }
     // 5. impact broad phase (CCD) over begin -> candidate
     weft_gpu::build_grid(c, c.sim_x.data(), c.sim_xc.data(), WEFT_CONTINUOUS, prm->thickness, prm->cell_scale);
     share(c.grid_total, wb, we);
@@ -429,7 +454,16 @@ weft_status weft_gpu_sim_step(weft_gpu_ctx* ctx, const weft_sim_params* prm, wef
     std::swap(c.sim_x.ptr, c.sim_xc.ptr);
     std::swap(c.sim_x.cap, c.sim_xc.cap);
     c.obstacles_set = c.soup_verts == c.p;  // obstacle positions are per step
+    if (c.io_xout) {
+      if (io_out_early) {
+        WG_CUDA(cudaEventSynchronize(c.ev_side[3]));
+      } else {  // contacts / zones change v and x up to the commit
+        WG_CUDA(cudaMemcpyAsync(c.io_vout, c.sim_v.data(), n * sizeof(double), cudaMemcpyDefault, s));
+        WG_CUDA(cudaMemcpyAsync(c.io_xout, c.sim_x.data(), n * sizeof(double), cudaMemcpyDefault, s));
+      }
+    }
     WG_CUDA(cudaEventSynchronize(ev[5]));
+    if (c.io_xout && !io_out_early) WG_CUDA(cudaStreamSynchronize(s));
     float tdcd = 0, tasm = 0, t13 = 0, t45 = 0;
     cudaEventElapsedTime(&tdcd, c.ev_side[0], c.ev_side[1]);  // overlapped with the assembly
     cudaEventElapsedTime(&tasm, ev[0], ev[2]);
@@ -452,6 +486,37 @@ weft_status weft_gpu_sim_step(weft_gpu_ctx* ctx, const weft_sim_params* prm, wef
       rep->ms_zones = tz;
     }
   });
+}
+
+weft_status weft_gpu_sim_step_io(weft_gpu_ctx* ctx, const double* x_in, const double* v_in,
+                                 const weft_sim_params* prm, double* x_out, double* v_out, weft_step_report* rep) {
+  if (!ctx) return WEFT_ERR_INVALID;
+  Ctx& c = ctx->c;
+  if (!c.has_state || !prm || prm->contacts || !x_in || !v_in || !x_out || !v_out || c.world > 1 ||
+      c.soup_verts != c.p) {
+    // the plain sequence (contacts mode, rank groups, obstacles, missing state)
+    weft_status st = weft_gpu_sim_set_state(ctx, x_in, v_in);
+    if (st == WEFT_OK) st = weft_gpu_sim_step(ctx, prm, rep);
+    if (st == WEFT_OK) st = weft_gpu_sim_get_state(ctx, x_out, v_out);
+    return st;
+  }
+  const weft_status st0 = guard2(ctx, [&](Ctx& cc) {
+    const size_t n = 3 * static_cast<size_t>(cc.p);
+    WG_CUDA(cudaMemcpyAsync(cc.sim_x.data(), x_in, n * sizeof(double), cudaMemcpyDefault, cc.stream));
+    WG_CUDA(cudaEventRecord(cc.ev_side[2], cc.stream));
+    WG_CUDA(cudaStreamWaitEvent(cc.side, cc.ev_side[2], 0));  // the previous step is done with v
+    WG_CUDA(cudaMemcpyAsync(cc.sim_v.data(), v_in, n * sizeof(double), cudaMemcpyDefault, cc.side));
+    WG_CUDA(cudaEventRecord(cc.ev_side[2], cc.side));
+  });
+  if (st0 != WEFT_OK) return st0;
+  c.io_vin = v_in;
+  c.io_xout = x_out;
+  c.io_vout = v_out;
+  const weft_status st = weft_gpu_sim_step(ctx, prm, rep);
+  c.io_vin = nullptr;
+  c.io_xout = c.io_vout = nullptr;
+  if (st != WEFT_OK) cudaStreamSynchronize(c.side);
+  return st;
 }
 
 weft_status weft_gpu_sim_get_state(weft_gpu_ctx* ctx, double* x, double* v) {

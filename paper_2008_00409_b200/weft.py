@@ -532,6 +532,14 @@ class Engine:
         _check(LIB.weft_gpu_sim_step(self._ctx, C.byref(params), C.byref(rep)))
         return rep
 
+    def sim_step_io(self, x_in, v_in, params: SimParams, x_out, v_out) -> StepReport:
+        """weft_gpu_sim_step_io: upload (x, v), one step, read (x, v) back,
+        with the copies overlapped with the broad phases."""
+        rep = StepReport()
+        _check(LIB.weft_gpu_sim_step_io(self._ctx, _ptr(x_in), _ptr(v_in), C.byref(params), _ptr(x_out), _ptr(v_out),
+                                        C.byref(rep)))
+        return rep
+
     def sim_get_state(self, x=None, v=None):
         _check(LIB.weft_gpu_sim_get_state(self._ctx, _ptr(x), _ptr(v)))
 

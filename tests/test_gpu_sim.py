@@ -86,3 +86,37 @@ def test_sim_steps_with_contacts_match_reference(weft, layers, nx, steps):
     assert r.contact_elements == 0 and r.pcg_converged
     ref.close()
     eng.close()
+
+
+def test_sim_step_io_equals_set_step_get(weft):
+    """weft_gpu_sim_step_io (copies overlapped with the broad phases) gives
+    bitwise the results of sim_set_state + sim_step + sim_get_state."""
+    from paper_2008_00409_b200 import scenes
+    sc = scenes.layered_cloth(2, 24, seed=4)
+    mesh = weft.ClothMesh.build(sc.verts, sc.tris, sc.density)
+    p = mesh.vertex_count
+    x0 = sc.verts.reshape(-1).copy()
+    v0 = np.random.default_rng(1).uniform(-0.01, 0.01, 3 * p)
+    prm = weft.SimParams(sc.dt, sc.thickness, 1.5, weft.PcgConfig(1e-8, 2000), weft.JAC_SPD)
+    outs = []
+    for io in (False, True):
+        eng = weft.Engine(1)
+        eng.set_vertices(mesh.vertex_mass, sc.pinned)
+        eng.set_elements(mesh.build_elements(sc.material, sc.gravity))
+        eng.set_soup(p, sc.tris)
+        eng.sim_set_state(x0, v0)
+        x, v = x0.copy(), v0.copy()
+        xo, vo = np.zeros(3 * p), np.zeros(3 * p)
+        reps = []
+        for _ in range(3):
+            if io:
+                reps.append(eng.sim_step_io(x, v, prm, xo, vo))
+            else:
+                eng.sim_set_state(x, v)
+                reps.append(eng.sim_step(prm))
+                eng.sim_get_state(xo, vo)
+            x, v = xo.copy(), vo.copy()
+        outs.append((x, v, [(r.pcg_iterations, r.dcd_candidates, r.ccd_candidates) for r in reps]))
+        eng.close()
+    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+    assert outs[0][2] == outs[1][2]
