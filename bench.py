@@ -6,19 +6,18 @@ Kneel-scale cloth (BASELINE config D: 3 x 525^2 grid layers, 1,647,456
 triangles, 826,875 vertices): DCD broad phase (grid + candidate pairs),
 step_system assembly, block-Jacobi PCG (tol 1e-4), candidate update, CCD
 broad phase (grid + candidate pairs), commit. Narrow phase / impact zones
-are out of this tier's scope in both arms. Every warm-up
-and timed step starts from the same state S (the state after --settle steps
-from rest): the reference's cloth model diverges on this pinned scene after
-~10 steps (identically in both arms), so the benchmark
-replays one representative step instead of a trajectory.
+are out of this tier's scope in both arms. The run is a
+trajectory from rest: W warm-up steps, then K timed steps continuing it
+(config material: paper_2008_00409_b200/scenes.py, stable for >= 40 steps).
 
   python bench.py [--gpus N --steps K --warmup W] [--impl reference]
 
 GPU arm: `value` is device-resident steps/s (CUDA events on the context's
-stream, max over ranks); `e2e` is the same step through the C-ABI with the
-state (x, v) copied host->device and back every step. Reference arm: the
-unmodified reference (oracle/_ref, compiled from /root/reference) running the
-same step on the host cores with Engine(n) threads.
+stream, max over ranks); `e2e` is the same K steps through the C-ABI with the
+state (x, v) copied from pinned host memory to the device and back every
+step. Reference arm: the unmodified reference (oracle/_ref, compiled from
+/root/reference) running the same trajectory on the host cores with
+Engine(n) threads.
 """
 from __future__ import annotations
 
@@ -47,11 +46,10 @@ def parse():
     ap.add_argument("--impl", choices=["gpu", "reference"], default="gpu")
     ap.add_argument("--config", default="D", help="scene config (A/B/C/D, BASELINE.md §2)")
     ap.add_argument("--seed", type=int, default=20240810)
-    ap.add_argument("--settle", type=int, default=2, help="steps from rest that define the replayed state S")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-narrow", action="store_true", help="skip the narrow-phase timing")
-    ap.add_argument("--ref-budget-s", type=float, default=150.0, help="wall budget of the reference arm")
+    ap.add_argument("--ref-budget-s", type=float, default=240.0, help="wall budget of the reference arm")
     return ap.parse_args()
 
 
@@ -150,17 +148,6 @@ def peaks():
     return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
 
 
-def traffic_per_launch(config: str):
-    """dram__bytes_read.sum + dram__bytes_write.sum of one k_pcg_spmv launch
-    from the committed ncu --set full capture (profiles/), or None."""
-    path = os.path.join(ROOT, "profiles", "spmv_traffic.json")
-    if not os.path.exists(path):
-        return None
-    with open(path) as f:
-        d = json.load(f)
-    return d.get(config)
-
-
 def pcg_traffic_per_launch(config: str, iterations: float):
     """DRAM bytes of one k_pcg_persistent launch from the committed ncu
     --set full capture, scaled to this run's iteration count, or None."""
@@ -189,54 +176,72 @@ def ref_devices():
     return d, n
 
 
-def run_reference_steps(sc, steps: int, warmup: int, budget_s: float, settle: int):
-    """Times the compiled reference's hot-path step (oracle/ref_harness.cpp
-    ref_sim_step), every step replayed from the settled state S. Returns
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def run_reference_steps(sc, steps: int, warmup: int, budget_s: float, functions: bool = False):
+    """The compiled reference's hot-path step (oracle/ref_harness.cpp
+    ref_sim_step) along the trajectory from rest: `warmup` untimed steps,
+    then up to `steps` timed ones within `budget_s` of wall time. Returns
     (mean seconds per timed step, timed steps, info)."""
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     from oracle_bindings import REF, RefSim
     if REF is None:
         return None, 0, {"unavailable": "oracle/_ref/libweft_ref.so not built (needs /root/reference at build time)"}
     devices, nproc = ref_devices()
-    sim = RefSim(REF, sc.verts, sc.tris, sc.pinned, sc.density, sc.material, devices)
-    for _ in range(settle):
-        sim.step(sc.dt, sc.thickness)
-    xs, vs = sim.get_state()
-    times, reps = [], []
     t_start = time.time()
-    for k in range(warmup + steps):
-        sim.set_state(xs, vs)
+    sim = RefSim(REF, sc.verts, sc.tris, sc.pinned, sc.density, sc.material, devices)
+    for _ in range(warmup):
+        sim.step(sc.dt, sc.thickness)
+    times, reps = [], []
+    for k in range(steps):
         t0 = time.perf_counter()
         r = sim.step(sc.dt, sc.thickness)
         dt = time.perf_counter() - t0
-        if k >= warmup:
-            times.append(dt)
-            reps.append(r)
-        if time.time() - t_start + dt > budget_s and len(times) >= 1:
+        times.append(dt)
+        reps.append(r)
+        if time.time() - t_start + dt > budget_s:
             break
+    info = {"devices": devices, "nproc": nproc, "last": reps[-1] if reps else {}, "cpu_model": cpu_model(),
+            "pcg_iterations": [int(r["pcg_iterations"]) for r in reps]}
+    if functions:
+        info["functions_median_ms"] = sim.time_functions(sc.dt, sc.thickness, reps=3)
     sim.close()
-    return statistics.mean(times), len(times), {"devices": devices, "nproc": nproc, "last": reps[-1] if reps else {}}
+    return statistics.mean(times), len(times), info
 
 
 def reference_arm(args, rank, world):
     if rank != 0:
         return
     sc = make_scene(args.config, args.seed)
-    sec, n, info = run_reference_steps(sc, args.steps, min(args.warmup, 1), args.ref_budget_s, args.settle)
+    sec, n, info = run_reference_steps(sc, args.steps, args.warmup, args.ref_budget_s, functions=True)
     if sec is None:
         print(json.dumps({"impl": "reference", "unavailable": info["unavailable"]}), flush=True)
         return
     value = 1.0 / sec
-    sample = (f"{n} timed full hot-path step(s) of config {args.config} replayed from the state after "
-              f"{args.settle} steps, {min(args.warmup, 1)} warm-up, "
-              f"reference Engine({info['devices']}) = {2 * info['devices']} threads on {info['nproc']} host cores")
+    sample = (f"steps {args.warmup}..{args.warmup + n - 1} of the config {args.config} trajectory from rest "
+              f"({args.warmup} untimed warm-up steps first), reference Engine({info['devices']}) = "
+              f"{2 * info['devices']} threads on {info['nproc']} host cores ({info['cpu_model']})")
     out = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": n, "warmup": min(args.warmup, 1),
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": n, "warmup": args.warmup,
         "ms_per_step": 1e3 * sec, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic", "impl": "reference",
         "config": {"workload": f"config {args.config}: {sc.layers} x {sc.nx}^2 layered cloth, {sc.tri_count} tris, "
-                               f"{sc.vertex_count} verts", "dt": sc.dt, "pcg_tol": 1e-4,
-                   "reference_stage_ms": info["last"]},
+                               f"{sc.vertex_count} verts, trajectory from rest", "dt": sc.dt, "pcg_tol": 1e-4,
+                   "material": sc.material, "reference_stage_ms_last_step": info["last"],
+                   "pcg_iterations": info["pcg_iterations"],
+                   "functions_median_ms": info["functions_median_ms"],
+                   "functions_note": "SURVEY 8(d): medians of 3 at the state after the timed steps; fill_matrix "
+                                     "over step_system's inputs, one spmv_pipelined y = A x, one DCD build_grid",
+                   "cpu_model": info["cpu_model"]},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": info["devices"], "kind": "reference", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -368,54 +373,54 @@ def gpu_arm(args, rank, world, local):
     def max_over_ranks(v: float) -> float:
         return reduce_over_ranks(v, dist.ReduceOp.MAX)
 
-    # settle: the replayed state S (device-resident copy + pinned host copy)
-    for _ in range(args.settle):
+    # warm-up: the first W steps of the trajectory from rest
+    for _ in range(args.warmup):
         eng.sim_step(params)
+    # the trajectory state at the start of the timed region (device copy):
+    # the e2e leg and the profiled replay restart from it
     xs = torch.empty(3 * p, dtype=torch.float64, device="cuda")
     vs = torch.empty(3 * p, dtype=torch.float64, device="cuda")
     eng.sim_get_state(xs, vs)
     torch.cuda.synchronize()
 
-    def replay():
-        eng.sim_set_state(xs, vs)  # device-to-device restore of S
-        return eng.sim_step(params)
-
-    for _ in range(args.warmup):
-        replay()
-
-    # ---- device-resident timed region
+    # ---- device-resident timed region: steps W .. W+K-1
     barrier()
     launches0 = eng.stats().launches
     clocks = Clocks(local)
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
-    reps = [replay() for _ in range(args.steps)]
+    reps = [eng.sim_step(params) for _ in range(args.steps)]
     ev1.record(stream)
     ev1.synchronize()
     barrier()
     clk = clocks.stop()
     ms_total = max_over_ranks(ev0.elapsed_time(ev1))
     launches = eng.stats().launches - launches0
+    xk = torch.empty_like(xs)
+    eng.sim_get_state(xk, None)
+    torch.cuda.synchronize()
     # Kernel timing for the roofline, CUDA events on the context stream in a
-    # profiled replay of the same step: the one-partition solve is ONE
-    # persistent kernel (timed whole); the multi-partition solve runs as a
-    # CUDA graph, so its SpMV launches are timed one by one (chunked
+    # profiled replay of the first two timed steps: the one-partition solve
+    # is ONE persistent kernel (timed whole); the multi-partition solve runs
+    # as a CUDA graph, so its SpMV launches are timed one by one (chunked
     # launches, identical kernels and inputs).
+    eng.sim_set_state(xs, vs)
     eng.profile(True)
     for _ in range(2):
-        replay()
+        eng.sim_step(params)
     st = eng.stats()
     eng.profile(False)
     info = eng.matrix_info()
 
-    # ---- end-to-end through the C-ABI with host buffers
+    # ---- end-to-end through the C-ABI with host buffers: the same K steps
+    # from the same state, (x, v) uploaded from pinned host memory and the
+    # step's result read back every step, the output of step k fed to k+1
     e2e = None
     if not args.no_e2e:
-        xh = xs.cpu().pin_memory()  # the step's input batch, pinned host memory
-        vh = vs.cpu().pin_memory()
-        xo = torch.empty(3 * p, dtype=torch.float64, pin_memory=True)
-        vo = torch.empty(3 * p, dtype=torch.float64, pin_memory=True)
+        xa, va = xs.cpu().pin_memory(), vs.cpu().pin_memory()
+        xb = torch.empty(3 * p, dtype=torch.float64, pin_memory=True)
+        vb = torch.empty(3 * p, dtype=torch.float64, pin_memory=True)
         barrier()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
@@ -423,17 +428,20 @@ def gpu_arm(args, rank, world, local):
         for _ in range(args.steps):
             # H2D of the step's inputs, the step, D2H of its result (one call:
             # weft_gpu_sim_step_io overlaps the copies with the broad phases)
-            eng.sim_step_io(xh, vh, params, xo, vo)
+            eng.sim_step_io(xa, va, params, xb, vb)
+            xa, xb = xb, xa
+            va, vb = vb, va
         e1.record(stream)
         e1.synchronize()
         barrier()
         e2e_ms = max_over_ranks(e0.elapsed_time(e1))
         # every rank uploads the full state (x, v) and reads it back
         e2e = {"value": args.steps / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": world * 2 * 8 * 3 * p,
-               "d2h_bytes_per_step": world * 2 * 8 * 3 * p}
+               "d2h_bytes_per_step": world * 2 * 8 * 3 * p,
+               "same_trajectory_as_value": bool(torch.equal(xa.to(xk.device), xk))}
 
     # narrow phase (not part of the hot-path step): collide()
-    # = broad phase + elementary DCD / CCD tests + dedup on the replayed state
+    # = broad phase + elementary DCD / CCD tests + dedup at the timed region's start state
     narrow = None
     if world == 1 and not args.no_narrow:
         eng.set_soup_movable(1 - sc.pinned)
@@ -453,7 +461,7 @@ def gpu_arm(args, rank, world, local):
             g = eng.grid_info()
             narrow[name] = {"ms": statistics.median(times), "ms_all": times, "raw_pairs": g.total, "hits": int(len(kab)),
                             "vertex_face": int((kab[:, 0] == 0).sum()), "edge_edge": int((kab[:, 0] == 1).sum())}
-        narrow["note"] = ("weft_gpu_collide on the replayed state (x_end = x + dt v for CCD): grid, candidate walk, "
+        narrow["note"] = ("weft_gpu_collide at the timed region's start state (x_end = x + dt v for CCD): grid, candidate walk, "
                           "6 VF + 9 EE tests per candidate pair, radix-sorted dedup; device time incl. the hit "
                           "download; not part of the timed step (out of the hot-path scope in both arms)")
 
@@ -481,7 +489,7 @@ def gpu_arm(args, rank, world, local):
                     "impacts": frep.impacts, "zones": frep.zone_count, "pcg_iterations": frep.pcg_iterations,
                     "stage_ms": {"broad_and_narrow": frep.ms_broad, "contacts_and_assemble": frep.ms_assemble,
                                  "solve": frep.ms_solve, "zones": frep.ms_zones},
-                    "note": "weft_gpu_sim_step(contacts=1, zones=1) on the replayed state: the whole "
+                    "note": "weft_gpu_sim_step(contacts=1, zones=1) from the timed region's start state: the whole "
                             "Simulator::step_impl (driver.cpp:96-215) incl. resolve_zones, device-resident; "
                             "median of 3"}
         except weft.Error as e:
@@ -517,8 +525,7 @@ def gpu_arm(args, rank, world, local):
         alg_bytes = info.nnzb * (9 * 8 + 4) + info.block_rows * (4 + 3 * 8 * 3)
         launch_ms = st.spmv_ms / max(st.spmv_launches, 1)
         nlaunch = st.spmv_launches
-        # the committed capture is of the one-partition kernel: no per-rank figure
-        traffic = traffic_per_launch(args.config) if world == 1 else None
+        traffic = None  # no committed ncu capture of the multi-partition kernels
     achieved = alg_bytes / (launch_ms * 1e-3) / 1e9
     it = [r.pcg_iterations for r in reps]
     # The assembly against the same HBM roofline (SURVEY §8(d) algorithmic
@@ -534,11 +541,12 @@ def gpu_arm(args, rank, world, local):
                          "bound": "fp64/latency (element evaluation + ordered per-slot accumulation)"}
     cpu = None
     if not args.no_cpu_baseline and world == 1:
-        sec, n, rinfo = run_reference_steps(sc, 1, 0, 45.0, args.settle)
+        sec, n, rinfo = run_reference_steps(sc, 3, 0, 60.0)
         if sec is not None:
             cpu = {"value": 1.0 / sec, "unit": UNIT, "cores": rinfo["devices"], "kind": "reference",
-                   "sample": f"{n} full hot-path step(s) of config {args.config} by the compiled reference, "
-                             f"Engine({rinfo['devices']}) on {rinfo['nproc']} host cores"}
+                   "sample": f"the first {n} steps of the config {args.config} trajectory from rest by the compiled "
+                             f"reference, Engine({rinfo['devices']}) = {2 * rinfo['devices']} threads on "
+                             f"{rinfo['nproc']} host cores ({rinfo['cpu_model']})"}
         else:
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": rinfo["unavailable"]}
     out = {
@@ -548,7 +556,9 @@ def gpu_arm(args, rank, world, local):
         "config": {
             "workload": f"config {args.config}: {sc.layers} x {sc.nx}^2 layered cloth, {sc.tri_count} tris, "
                         f"{p} verts, pinned top edges, dt={sc.dt:.6g}, PCG tol 1e-4 block-Jacobi; every step "
-                        f"replays the state after {args.settle} steps from rest",
+                        f"trajectory from rest: {args.warmup} warm-up steps, then steps {args.warmup}.."
+                        f"{args.warmup + args.steps - 1} timed",
+            "material": sc.material,
             "parallelism": "single GPU" if world == 1 else (
                 f"{world} ranks, one row partition each (make_partitions); PCG halos and ordered dot "
                 "reductions over peer memory (CUDA IPC / NVLink), replicated broad phase with split pair ranges"

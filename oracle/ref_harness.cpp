@@ -9,7 +9,9 @@
 // the reference does not expose candidates separately.
 #include <chrono>
 #include <cstring>
+#include <algorithm>
 #include <memory>
+#include <optional>
 #include <string>
 #include <thread>
 #include <vector>
@@ -843,6 +845,72 @@ int32_t ref_sim_step(void* h, const double* params, double* out) {
     out[5] = ms(tb0, tb1) + ms(tc0, tc1);
     out[6] = ms(tb1, ta);
     out[7] = ms(ta, tsol);
+    return 0;
+  } catch (const std::exception& e) {
+    return set_error(e);
+  }
+}
+
+// Per-function CPU medians on the current state (SURVEY.md §8(d) "CPU
+// timing"): fill_matrix<double> over step_system's inputs (assembly.hpp:74-220;
+// build_elements / distribute_elements done once, outside the timing),
+// spmv_pipelined on the assembled system (sparse.hpp:72-101, one global
+// y = A x), build_grid in DCD mode on x (collision.cpp:118-179, one build;
+// collide() replicates it per device). params: dt, thickness, cell_scale.
+// out: median ms of fill_matrix, spmv_pipelined, build_grid.
+int32_t ref_sim_time_functions(void* h, const double* params, int32_t reps, double* out) {
+  auto* s = static_cast<RefSim*>(h);
+  try {
+    const double dt = params[0];
+    CollisionParams cp;
+    cp.thickness = params[1];
+    cp.cell_scale = params[2];
+    const int p = s->mesh.vertex_count();
+    const int n = s->engine->devices();
+    const auto elements = build_elements(s->mesh, s->material, Vec3(0, 0, -9.81), Vec3::Zero());
+    std::vector<Vec3> adv(static_cast<std::size_t>(p));
+    for (int i = 0; i < p; ++i)
+      adv[static_cast<std::size_t>(i)] = s->state.x[static_cast<std::size_t>(i)] + dt * s->state.v[static_cast<std::size_t>(i)];
+    const auto parts = make_partitions(p, n);
+    const auto dist = distribute_elements(elements, parts);
+    SystemInputs in;
+    in.elements = elements;
+    in.x_current = s->state.x;
+    in.x_advanced = adv;
+    in.velocity = s->state.v;
+    in.mass = s->mesh.vertex_mass;
+    in.pinned = s->pinned;
+    in.dt = dt;
+    in.mode = JacobianMode::SpdProjected;
+    auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+    auto median = [](std::vector<double> v) {
+      std::sort(v.begin(), v.end());
+      return v[v.size() / 2];
+    };
+    std::vector<double> tf, ts, tg;
+    std::optional<AssembledSystem<double>> sys;
+    for (int r = 0; r < std::max(reps, 1); ++r) {
+      const auto t0 = std::chrono::steady_clock::now();
+      auto a = fill_matrix<double>(*s->engine, dist, in, parts);
+      tf.push_back(ms(t0, std::chrono::steady_clock::now()));
+      if (!sys) sys.emplace(std::move(a));
+    }
+    DistVector<double> x(s->engine.get(), sys->matrix.partitions), y(s->engine.get(), sys->matrix.partitions);
+    x.fill(1.0);
+    SpmvWorkspace<double> ws(n, sys->matrix.padded_len);
+    for (int r = 0; r < std::max(reps, 1); ++r) {
+      const auto t0 = std::chrono::steady_clock::now();
+      spmv_pipelined(*s->engine, sys->matrix, s->sched, x, y, ws);
+      ts.push_back(ms(t0, std::chrono::steady_clock::now()));
+    }
+    for (int r = 0; r < std::max(reps, 1); ++r) {
+      const auto t0 = std::chrono::steady_clock::now();
+      const auto g = build_grid(s->soup, s->state.x, s->state.x, CollisionMode::Discrete, cp);
+      tg.push_back(ms(t0, std::chrono::steady_clock::now()));
+    }
+    out[0] = median(tf);
+    out[1] = median(ts);
+    out[2] = median(tg);
     return 0;
   } catch (const std::exception& e) {
     return set_error(e);

@@ -44,6 +44,7 @@ void set_vertices(Ctx& c, int p, const double* mass, const uint8_t* pinned) {
   if (p < 0) throw Error(WEFT_ERR_DIMENSION, "negative vertex count");
   if (p >= (1 << 28)) throw Error(WEFT_ERR_DIMENSION, "more than 2^28 vertices");
   if (p < c.nparts) throw Error(WEFT_ERR_DIMENSION, "fewer vertices than partitions");
+  if (p != c.p) c.has_state = c.obstacles_set = false;  // the simulation state is sized by p
   c.p = p;
   set_rows(c, p);
   c.mass.upload(mass, static_cast<size_t>(p), c.stream);

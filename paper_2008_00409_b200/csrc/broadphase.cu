@@ -51,6 +51,7 @@ void set_soup(Ctx& c, int verts, int ntris, const int32_t* tris) {
   if (ntris) WG_CUDA(cudaMemcpy(h.data(), tris, h.size() * sizeof(int32_t), cudaMemcpyDefault));
   for (int32_t v : h)
     if (v < 0 || v >= verts) throw Error(WEFT_ERR_DIMENSION, "triangle vertex index out of range");
+  if (verts != c.soup_verts) c.has_state = c.obstacles_set = false;  // sim_x / sim_v are soup-sized
   c.soup_verts = verts;
   c.soup_tris = ntris;
   c.tris.upload(h.data(), h.size(), c.stream);

@@ -202,6 +202,7 @@ struct Ctx {
 
   // ---- resident simulation state
   DBuf<double> sim_x, sim_v, sim_xc;  // soup-sized: the cloth's 3p, then obstacle vertices
+  DBuf<double> sim_vbak;              // v at the step's start: restored when a step fails after v += dv
   DBuf<double> soup_mass;             // cloth masses, 1.0 for obstacle vertices
   bool has_state = false;
   bool obstacles_set = false;         // obstacle positions of this step given

@@ -410,7 +410,23 @@ weft_status weft_gpu_sim_step(weft_gpu_ctx* ctx, const weft_sim_params* prm, wef
     WG_CUDA(cudaEventRecord(ev[3], s));
     if (!pr.converged)  // driver.cpp:158-161
       throw Error(WEFT_ERR_SOLVER, "PCG did not converge (residual " + std::to_string(pr.rel_residual) + ")");
-    // 4. candidate update
+    // 4. candidate update. The reference works on a local v_cand and writes
+    // the state only at the commit (driver.cpp:163-206), so a frame that
+    // throws after this point (ZoneFailure, a peer timeout) leaves (x, v)
+    // untouched: v is saved here and restored unless the commit is reached.
+    c.sim_vbak.resize(static_cast<size_t>(n));
+    WG_CUDA(cudaMemcpyAsync(c.sim_vbak.data(), c.sim_v.data(), n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    struct VRestore {
+      Ctx& c;
+      int64_t n;
+      bool armed = true;
+      ~VRestore() {
+        if (!armed) return;
+        cudaStreamSynchronize(c.side);
+        cudaMemcpyAsync(c.sim_v.data(), c.sim_vbak.data(), n * sizeof(double), cudaMemcpyDeviceToDevice, c.stream);
+        cudaStreamSynchronize(c.stream);
+      }
+    } v_restore{c, n};
     const int64_t i0 = 3 * static_cast<int64_t>(c.row0), i1 = 3 * static_cast<int64_t>(c.row1);
     if (pr.iterations == 0) WG_CUDA(cudaMemsetAsync(c.xs.data() + i0, 0, (i1 - i0) * sizeof(double), s));
     weft_gpu::k_candidate<<<weft_gpu::div_up(i1 - i0, 256), 256, 0, ls(c)>>>(i0, i1, c.sim_x.data(), c.sim_v.data(),
@@ -451,6 +467,7 @@ weft_status weft_gpu_sim_step(weft_gpu_ctx* ctx, const weft_sim_params* prm, wef
     }
     WG_CUDA(cudaEventRecord(ev[5], s));
     // 7. commit
+    v_restore.armed = false;
     std::swap(c.sim_x.ptr, c.sim_xc.ptr);
     std::swap(c.sim_x.cap, c.sim_xc.cap);
     c.obstacles_set = c.soup_verts == c.p;  // obstacle positions are per step
@@ -492,9 +509,22 @@ weft_status weft_gpu_sim_step_io(weft_gpu_ctx* ctx, const double* x_in, const do
                                  const weft_sim_params* prm, double* x_out, double* v_out, weft_step_report* rep) {
   if (!ctx) return WEFT_ERR_INVALID;
   Ctx& c = ctx->c;
-  if (!c.has_state || !prm || prm->contacts || !x_in || !v_in || !x_out || !v_out || c.world > 1 ||
-      c.soup_verts != c.p) {
-    // the plain sequence (contacts mode, rank groups, obstacles, missing state)
+  if (c.has_state && c.soup_verts != c.p) {
+    // obstacles: the cloth's x and v only — the obstacle positions of this
+    // step stay as weft_gpu_sim_set_obstacles gave them
+    weft_status st = guard2(ctx, [&](Ctx& cc) {
+      if (!x_in || !v_in) throw Error(WEFT_ERR_INVALID, "sim_step_io: NULL state buffer");
+      const size_t n = 3 * static_cast<size_t>(cc.p);
+      WG_CUDA(cudaMemcpyAsync(cc.sim_x.data(), x_in, n * sizeof(double), cudaMemcpyDefault, cc.stream));
+      WG_CUDA(cudaMemcpyAsync(cc.sim_v.data(), v_in, n * sizeof(double), cudaMemcpyDefault, cc.stream));
+      WG_CUDA(cudaStreamSynchronize(cc.stream));
+    });
+    if (st == WEFT_OK) st = weft_gpu_sim_step(ctx, prm, rep);
+    if (st == WEFT_OK) st = weft_gpu_sim_get_state(ctx, x_out, v_out);
+    return st;
+  }
+  if (!c.has_state || !prm || prm->contacts || !x_in || !v_in || !x_out || !v_out || c.world > 1) {
+    // the plain sequence (contacts mode, rank groups, missing state)
     weft_status st = weft_gpu_sim_set_state(ctx, x_in, v_in);
     if (st == WEFT_OK) st = weft_gpu_sim_step(ctx, prm, rep);
     if (st == WEFT_OK) st = weft_gpu_sim_get_state(ctx, x_out, v_out);

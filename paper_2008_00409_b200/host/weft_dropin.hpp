@@ -44,8 +44,14 @@ inline void check(weft_status s) {
   }
 }
 
-// One GPU context per reference Engine (same partition count n, so the
-// SpMV / dot-product orders are the Engine(n) orders).
+// One GPU context per (partition count, CUDA device): the partition count is
+// the only property of a reference Engine the GPU path depends on (the
+// SpMV / dot-product orders are the Engine(n) orders). Each context carries
+// its own mutex, held by a Lease for the whole drop-in call, so two threads
+// driving different Engines with the same device count serialise on the
+// shared device state instead of racing on it. The reference's public API
+// is single-threaded per Engine (exec.hpp:83-85); this only makes the shared
+// cache safe.
 class Context {
  public:
   explicit Context(int partitions, int cuda_device = 0) {
@@ -56,26 +62,50 @@ class Context {
   Context(const Context&) = delete;
   Context& operator=(const Context&) = delete;
   weft_gpu_ctx* get() const { return ctx_; }
+  std::mutex& mutex() { return mu_; }
+
+  // Static inputs last uploaded (fill_matrix / step_system): the device
+  // keeps the static element list, its row-incidence tables and pattern
+  // resident, so a caller stepping the same mesh only uploads what changed.
+  std::vector<double> mass;
+  std::vector<uint8_t> pinned;
+  std::vector<weft_element> static_elems;
+  bool vertices_set = false, elements_set = false;
+  // step_system's build_elements cache key (mesh identity + material)
+  const void* mesh_key = nullptr;
+  std::vector<double> elem_params;
 
  private:
   weft_gpu_ctx* ctx_ = nullptr;
+  std::mutex mu_;
 };
 
-// Contexts are cached per partition count (an Engine's only property the
-// GPU path depends on), so short-lived Engines reuse device state.
-inline Context& context_for(const Engine& engine) {
+struct Lease {
+  Context& c;
+  std::unique_lock<std::mutex> lock;
+  weft_gpu_ctx* get() const { return c.get(); }
+};
+
+inline Lease acquire(int partitions, int cuda_device = 0) {
   // Intentionally leaked: contexts must not be torn down during static
   // destruction, after the CUDA runtime itself may already be gone.
   static std::mutex mu;
-  static auto* ctxs = new std::map<int, std::unique_ptr<Context>>();
-  std::lock_guard lock(mu);
-  auto& c = (*ctxs)[engine.devices()];
-  if (!c) c = std::make_unique<Context>(engine.devices());
-  return *c;
+  static auto* ctxs = new std::map<std::pair<int, int>, std::unique_ptr<Context>>();
+  Context* c = nullptr;
+  {
+    std::lock_guard lock(mu);
+    auto& slot = (*ctxs)[{partitions, cuda_device}];
+    if (!slot) slot = std::make_unique<Context>(partitions, cuda_device);
+    c = slot.get();
+  }
+  return Lease{*c, std::unique_lock<std::mutex>(c->mutex())};
 }
 
+inline Lease acquire(const Engine& engine) { return acquire(engine.devices()); }
+
 inline weft_element to_flat(const AssemblyElement& e) {
-  weft_element f{};
+  weft_element f;
+  std::memset(&f, 0, sizeof(f));  // padding too: the static-list cache compares records bytewise
   f.kind = static_cast<int32_t>(e.kind);
   f.stencil_size = e.stencil_size;
   for (int i = 0; i < 4; ++i) f.stencil[i] = e.stencil[static_cast<std::size_t>(i)];
@@ -143,7 +173,9 @@ inline PartitionedMatrix<double> to_partitioned(int rows, const std::vector<int6
   return partition_matrix(BellMatrix<double>::from_entries(rows, entries), parts);
 }
 
-inline void upload_partitioned(weft_gpu_ctx* ctx, const PartitionedMatrix<double>& a) {
+inline void upload_partitioned(Context& cx, const PartitionedMatrix<double>& a) {
+  weft_gpu_ctx* ctx = cx.get();
+  cx.vertices_set = cx.elements_set = false;  // set_matrix replaces the assembled system
   const auto g = gather_matrix(a);
   std::vector<int64_t> rp(static_cast<std::size_t>(g.block_rows()) + 1, 0);
   std::vector<int32_t> cols;
@@ -161,7 +193,62 @@ inline void upload_partitioned(weft_gpu_ctx* ctx, const PartitionedMatrix<double
   check(weft_gpu_set_matrix(ctx, g.block_rows(), rp.data(), cols.data(), vals.data()));
 }
 
-// fill_matrix<Real> (assembly.hpp:74-77): same signature and results.
+// Uploads the vertex data and the static element list only when they differ
+// from what the context already holds (the device keeps the static list's
+// row-incidence tables and pattern resident); `contacts` go up every call
+// as the per-step contact list (assembly order: static list, then contacts).
+inline void sync_inputs(Context& cx, int p, std::span<const double> mass, std::span<const uint8_t> pinned,
+                        const std::vector<weft_element>& static_elems, const std::vector<weft_element>& contacts) {
+  weft_gpu_ctx* ctx = cx.get();
+  const bool same_v = cx.vertices_set && static_cast<int>(cx.mass.size()) == p &&
+                      mass.size() == static_cast<std::size_t>(p) && pinned.size() == static_cast<std::size_t>(p) &&
+                      std::equal(mass.begin(), mass.end(), cx.mass.begin()) &&
+                      std::equal(pinned.begin(), pinned.end(), cx.pinned.begin());
+  if (!same_v) {
+    if (mass.size() != static_cast<std::size_t>(p) || pinned.size() != static_cast<std::size_t>(p))
+      throw DimensionError("fill_matrix: mass/pinned size mismatch");
+    cx.vertices_set = cx.elements_set = false;
+    check(weft_gpu_set_vertices(ctx, p, mass.data(), pinned.data()));
+    cx.mass.assign(mass.begin(), mass.end());
+    cx.pinned.assign(pinned.begin(), pinned.end());
+    cx.vertices_set = true;
+  }
+  const bool same_e = cx.elements_set && cx.static_elems.size() == static_elems.size() &&
+                      (static_elems.empty() ||
+                       std::memcmp(cx.static_elems.data(), static_elems.data(),
+                                   sizeof(weft_element) * static_elems.size()) == 0);
+  if (!same_e) {
+    cx.elements_set = false;
+    check(weft_gpu_set_elements(ctx, static_cast<int64_t>(static_elems.size()), static_elems.data()));
+    cx.static_elems = static_elems;
+    cx.elements_set = true;
+  }
+  check(weft_gpu_set_contacts(ctx, static_cast<int64_t>(contacts.size()), contacts.empty() ? nullptr : contacts.data()));
+}
+
+// The context's assembled system downloaded into the reference's types.
+inline AssembledSystem<double> download_system(Engine& engine, weft_gpu_ctx* ctx, int p,
+                                               const std::vector<DevicePartition>& partitions) {
+  weft_matrix_info info{};
+  check(weft_gpu_matrix_info(ctx, &info));
+  std::vector<int64_t> rp(static_cast<std::size_t>(info.block_rows) + 1);
+  std::vector<int32_t> cols(static_cast<std::size_t>(info.nnzb));
+  std::vector<double> vals(9 * static_cast<std::size_t>(info.nnzb)), rhs(3 * static_cast<std::size_t>(p));
+  check(weft_gpu_download_matrix(ctx, rp.data(), cols.data(), vals.data()));
+  check(weft_gpu_download_rhs(ctx, rhs.data()));
+  AssembledSystem<double> out{to_partitioned(info.block_rows, rp, cols, vals, partitions),
+                              DistVector<double>(&engine, partitions)};
+  for (const auto& part : partitions) {
+    auto local = out.rhs.local(part.device_id);
+    std::copy(rhs.begin() + 3 * part.begin, rhs.begin() + 3 * part.end, local.begin());
+  }
+  return out;
+}
+
+// fill_matrix<Real> (assembly.hpp:74-77): same signature and results. The
+// static prefix of in.elements (everything before the first Contact
+// element, i.e. build_elements' list, physics.hpp:53-54) is cached on the
+// device across calls; the contact elements are uploaded every call.
 template <class Real>
 AssembledSystem<Real> fill_matrix(Engine& engine, const DistributedElements& /*dist*/, const SystemInputs& in,
                                   const std::vector<DevicePartition>& partitions) {
@@ -169,31 +256,105 @@ AssembledSystem<Real> fill_matrix(Engine& engine, const DistributedElements& /*d
     throw Error("weft::gpu::fill_matrix: only double precision runs on the GPU path");
   } else {
     if (in.dt <= 0.0) throw DimensionError("fill_matrix: dt must be positive");
-    weft_gpu_ctx* ctx = context_for(engine).get();
+    Lease lease = acquire(engine);
+    weft_gpu_ctx* ctx = lease.get();
     const int p = partitions.empty() ? 0 : partitions.back().end;
-    std::vector<uint8_t> pinned(in.pinned.begin(), in.pinned.end());
-    check(weft_gpu_set_vertices(ctx, p, in.mass.data(), pinned.data()));
-    std::vector<weft_element> elems;
-    elems.reserve(in.elements.size());
-    for (const auto& e : in.elements) elems.push_back(to_flat(e));
-    check(weft_gpu_set_elements(ctx, static_cast<int64_t>(elems.size()), elems.data()));
+    std::vector<weft_element> stat, cont;
+    stat.reserve(in.elements.size());
+    bool in_contacts = false;
+    for (const auto& e : in.elements) {
+      in_contacts = in_contacts || e.kind == ElementKind::Contact;
+      (in_contacts ? cont : stat).push_back(to_flat(e));
+    }
+    sync_inputs(lease.c, p, in.mass, in.pinned, stat, cont);
     const auto xc = flat3(in.x_current), xa = flat3(in.x_advanced), v = flat3(in.velocity);
     check(weft_gpu_fill_matrix(ctx, xc.data(), xa.data(), v.data(), in.dt,
                                in.mode == JacobianMode::Exact ? WEFT_JAC_EXACT : WEFT_JAC_SPD_PROJECTED));
-    weft_matrix_info info{};
-    check(weft_gpu_matrix_info(ctx, &info));
-    std::vector<int64_t> rp(static_cast<std::size_t>(info.block_rows) + 1);
-    std::vector<int32_t> cols(static_cast<std::size_t>(info.nnzb));
-    std::vector<double> vals(9 * static_cast<std::size_t>(info.nnzb)), rhs(3 * static_cast<std::size_t>(p));
-    check(weft_gpu_download_matrix(ctx, rp.data(), cols.data(), vals.data()));
-    check(weft_gpu_download_rhs(ctx, rhs.data()));
-    AssembledSystem<double> out{to_partitioned(info.block_rows, rp, cols, vals, partitions),
-                                DistVector<double>(&engine, partitions)};
-    for (const auto& part : partitions) {
-      auto local = out.rhs.local(part.device_id);
-      std::copy(rhs.begin() + 3 * part.begin, rhs.begin() + 3 * part.end, local.begin());
+    return download_system(engine, ctx, p, partitions);
+  }
+}
+
+// step_system<Real> (physics.hpp:44-69): build_elements (the reference's own
+// host function, physics.cpp:5-63) runs once per (mesh, material, gravity,
+// wind) and its list stays on the device; per call only the contact
+// elements and the state (x, v) go up, x_adv = x + dt v and the assembly run
+// on the GPU (weft_gpu_step_system). The cache is keyed by the mesh's
+// address and rest-position storage plus the material/load values: a
+// caller that mutates a mesh in place between calls must use a new mesh
+// object (the reference's Simulator keeps its mesh const, driver.cpp:148).
+template <class Real>
+AssembledSystem<Real> step_system(Engine& engine, const ClothMesh& mesh, const SimState& state,
+                                  const MaterialParams& params, std::span<const std::uint8_t> pinned,
+                                  std::vector<AssemblyElement> contact_elements, double dt, const Vec3& gravity,
+                                  const Vec3& wind, JacobianMode mode = JacobianMode::SpdProjected) {
+  if constexpr (!std::is_same_v<Real, double>) {
+    throw Error("weft::gpu::step_system: only double precision runs on the GPU path");
+  } else {
+    if (dt <= 0.0) throw DimensionError("fill_matrix: dt must be positive");
+    const int p = mesh.vertex_count();
+    if (state.x.size() != static_cast<std::size_t>(p) || state.v.size() != static_cast<std::size_t>(p))
+      throw DimensionError("step_system: state size != vertex count");
+    Lease lease = acquire(engine);
+    Context& cx = lease.c;
+    weft_gpu_ctx* ctx = lease.get();
+    const std::vector<double> key{params.stretch_warp, params.stretch_weft, params.shear, params.bend,
+                                  params.density, params.damping, params.air_drag, gravity[0], gravity[1],
+                                  gravity[2], wind[0], wind[1], wind[2],
+                                  static_cast<double>(reinterpret_cast<std::uintptr_t>(mesh.rest_positions.data())),
+                                  static_cast<double>(mesh.triangle_count())};
+    std::vector<weft_element> stat;
+    const bool cached = cx.elements_set && cx.mesh_key == &mesh && cx.elem_params == key;
+    if (cached) {
+      stat = cx.static_elems;  // what the device holds
+    } else {
+      const auto elems = build_elements(mesh, params, gravity, wind);
+      stat.reserve(elems.size());
+      for (const auto& e : elems) stat.push_back(to_flat(e));
     }
-    return out;
+    std::vector<weft_element> cont;
+    cont.reserve(contact_elements.size());
+    for (const auto& e : contact_elements) cont.push_back(to_flat(e));
+    cx.mesh_key = nullptr;
+    sync_inputs(cx, p, mesh.vertex_mass, pinned, stat, cont);
+    cx.mesh_key = &mesh;
+    cx.elem_params = key;
+    const auto x = flat3(state.x), v = flat3(state.v);
+    check(weft_gpu_step_system(ctx, x.data(), v.data(), dt,
+                               mode == JacobianMode::Exact ? WEFT_JAC_EXACT : WEFT_JAC_SPD_PROJECTED));
+    return download_system(engine, ctx, p, make_partitions(p, engine.devices()));
+  }
+}
+
+// spmv_serial<Real> (bell.hpp:83-84, bell.cpp:147-153): y = A x on one
+// device, slots in ascending order per row (BellMatrix::multiply_into,
+// bell.cpp:87-129) — the one-partition GPU SpMV, bitwise.
+template <class Real>
+std::vector<Real> spmv_serial(const BellMatrix<Real>& a, std::span<const Real> x) {
+  if constexpr (!std::is_same_v<Real, double>) {
+    throw Error("weft::gpu::spmv_serial: only double precision runs on the GPU path");
+  } else {
+    if (static_cast<int>(x.size()) != a.rows()) throw DimensionError("spmv_serial: dim(x) != rows");
+    Lease lease = acquire(1);
+    weft_gpu_ctx* ctx = lease.get();
+    std::vector<int64_t> rp(static_cast<std::size_t>(a.block_rows()) + 1, 0);
+    std::vector<int32_t> cols;
+    std::vector<double> vals;
+    for (int r = 0; r < a.block_rows(); ++r) {
+      for (int s = 0; s < a.ell_width(); ++s) {
+        const int32_t c = a.col_at(r, s);
+        if (c == BellMatrix<double>::kNoBlock) break;
+        cols.push_back(c);
+        for (int i = 0; i < 3; ++i)
+          for (int j = 0; j < 3; ++j) vals.push_back(a.value_at(r, s, i, j));
+      }
+      rp[static_cast<std::size_t>(r) + 1] = static_cast<int64_t>(cols.size());
+    }
+    std::vector<double> y(x.size(), 0.0);
+    if (a.block_rows() == 0) return y;
+    lease.c.vertices_set = lease.c.elements_set = false;  // set_matrix replaces the assembled system
+    check(weft_gpu_set_matrix(ctx, a.block_rows(), rp.data(), cols.data(), vals.data()));
+    check(weft_gpu_spmv(ctx, x.data(), y.data()));
+    return y;
   }
 }
 
@@ -206,8 +367,9 @@ void spmv_pipelined(Engine& engine, const PartitionedMatrix<Real>& a, const Vali
   } else {
     if (engine.devices() != a.devices || sched.devices() != a.devices)
       throw DimensionError("spmv_pipelined: engine/schedule/matrix device counts differ");
-    weft_gpu_ctx* ctx = context_for(engine).get();
-    upload_partitioned(ctx, a);
+    Lease lease = acquire(engine);
+    weft_gpu_ctx* ctx = lease.get();
+    upload_partitioned(lease.c, a);
     const auto xg = x.gather();
     std::vector<double> yg(xg.size());
     check(weft_gpu_spmv(ctx, xg.data(), yg.data()));
@@ -226,8 +388,9 @@ PcgReport pcg_solve(Engine& engine, const PartitionedMatrix<Real>& a, const Vali
     throw Error("weft::gpu::pcg_solve: only double precision runs on the GPU path");
   } else {
     if (engine.devices() != a.devices) throw DimensionError("pcg_solve: engine/matrix device count mismatch");
-    weft_gpu_ctx* ctx = context_for(engine).get();
-    upload_partitioned(ctx, a);
+    Lease lease = acquire(engine);
+    weft_gpu_ctx* ctx = lease.get();
+    upload_partitioned(lease.c, a);
     const auto bg = b.gather();
     std::vector<double> xg(bg.size());
     weft_pcg_config cfg{config.rel_tolerance, config.max_iterations,
@@ -254,8 +417,8 @@ PcgReport pcg_solve(Engine& engine, const PartitionedMatrix<Real>& a, const Vali
 // reference's HashGrid / WorkloadTable types.
 inline GridBuildResult build_grid(const CollisionSoup& soup, std::span<const Vec3> x_begin, std::span<const Vec3> x_end,
                                   CollisionMode mode, const CollisionParams& params, int cuda_device = 0) {
-  static Context* ctx_holder = new Context(1, cuda_device);  // leaked on purpose (see context_for)
-  weft_gpu_ctx* ctx = ctx_holder->get();
+  Lease lease = acquire(1, cuda_device);
+  weft_gpu_ctx* ctx = lease.get();
   std::vector<int32_t> tris(3 * soup.triangles.size());
   for (std::size_t t = 0; t < soup.triangles.size(); ++t)
     for (int c = 0; c < 3; ++c) tris[3 * t + static_cast<std::size_t>(c)] = soup.triangles[t][static_cast<std::size_t>(c)];
@@ -294,7 +457,8 @@ inline GridBuildResult build_grid(const CollisionSoup& soup, std::span<const Vec
 inline NarrowPhaseResult collide(Engine& engine, const CollisionSoup& soup, std::span<const Vec3> x_begin,
                                  std::span<const Vec3> x_end, CollisionMode mode, const CollisionParams& params,
                                  CollideTimes* /*times*/ = nullptr) {
-  weft_gpu_ctx* ctx = context_for(engine).get();
+  Lease lease = acquire(engine);
+  weft_gpu_ctx* ctx = lease.get();
   std::vector<int32_t> tris(3 * soup.triangles.size());
   for (std::size_t t = 0; t < soup.triangles.size(); ++t)
     for (int c = 0; c < 3; ++c) tris[3 * t + static_cast<std::size_t>(c)] = soup.triangles[t][static_cast<std::size_t>(c)];
@@ -331,7 +495,8 @@ inline void set_soup(weft_gpu_ctx* ctx, const CollisionSoup& soup) {
 // build_zones (response.cpp:108-162) on the GPU: same zones, same ids, same
 // impact lists and sorted movable vertex lists. Uses the context of Engine(1).
 inline std::vector<ImpactZone> build_zones(const std::vector<Impact>& impacts, const CollisionSoup& soup) {
-  weft_gpu_ctx* ctx = context_for(Engine(1)).get();
+  Lease lease = acquire(1);
+  weft_gpu_ctx* ctx = lease.get();
   set_soup(ctx, soup);
   const int64_t n = static_cast<int64_t>(impacts.size());
   std::vector<int32_t> kab(3 * impacts.size() + 3), iz(impacts.size() + 1);
@@ -376,7 +541,8 @@ inline ZoneResolveReport resolve_zones(Engine& engine, const CollisionSoup& soup
                                        std::vector<Vec3>& x_candidate, std::span<const double> vertex_mass,
                                        const CollisionParams& cparams, const ZoneSolveParams& zparams,
                                        CollideTimes* /*times*/ = nullptr) {
-  weft_gpu_ctx* ctx = context_for(engine).get();
+  Lease lease = acquire(engine);
+  weft_gpu_ctx* ctx = lease.get();
   set_soup(ctx, soup);
   const auto xb = flat3(x_begin);
   auto xc = flat3(x_candidate);

@@ -2,7 +2,18 @@
 stacked grid layers of `make_grid_mesh` topology (proj/src/mesh.cpp:187-212),
 jittered rest shape (as oracle::random_cloth, physics_oracle.cpp:90-101),
 top edge of every layer pinned (scene.cpp:137-142), layers 1.5 x thickness
-apart so they are in DCD proximity from step 0, v0 = 0."""
+apart so they are in DCD proximity from step 0, v0 = 0.
+
+Material of the configurations: the MaterialParams defaults (physics.hpp:8-16)
+with the stretch and shear stiffness scaled by CONFIG_STRETCH_SCALE. The
+reference's stretch / shear conditions are area-weighted (C = a(|w|-1) and
+C = a w_u.w_v, elements.cpp:170-172), so a stiffness acts with the squared
+rest area: the default 400 N/m is calibrated for ~1 cm triangles (the
+reference's scenes, scenes/sphere.json) and cannot carry a hanging sheet of
+5 mm triangles — the sheet free-falls, its top row over-stretches and the
+run diverges after ~10 steps, identically in both arms. Scaled x1024 the
+same sheet runs a stable trajectory (measured >= 40 steps at config D with
+the compiled reference) at the same PCG work (~163 iterations per step)."""
 from __future__ import annotations
 
 from dataclasses import dataclass
@@ -65,8 +76,11 @@ def grid_tris(nx: int, ny: int, offset: int = 0) -> np.ndarray:
     return (t.reshape(-1, 3) + offset).astype(np.int32)
 
 
+CONFIG_STRETCH_SCALE = 1024.0
+
+
 def layered_cloth(layers: int, nx: int, spacing: float = 0.005, seed: int = 20240810, jitter: float = 0.15,
-                  dt: float = 1.0 / 240.0, hanging: bool = True) -> Scene:
+                  dt: float = 1.0 / 240.0, hanging: bool = True, stretch_scale: float = 1.0) -> Scene:
     width = spacing * (nx - 1)
     thickness = 0.5 * spacing
     dz = 1.5 * thickness
@@ -86,10 +100,14 @@ def layered_cloth(layers: int, nx: int, spacing: float = 0.005, seed: int = 2024
         pin = np.zeros(nx * nx, np.uint8)
         pin[(nx - 1) * nx:] = 1  # pin_top_edge: last grid row
         pinned.append(pin)
+    mat = list(Scene.material)
+    mat[0] *= stretch_scale
+    mat[1] *= stretch_scale
+    mat[2] *= stretch_scale
     return Scene(np.concatenate(verts), np.concatenate(tris), np.concatenate(pinned), layers, nx, spacing,
-                 thickness, dt)
+                 thickness, dt, material=tuple(mat))
 
 
 def config(name: str, seed: int = 20240810) -> Scene:
     layers, nx = CONFIGS[name]
-    return layered_cloth(layers, nx, seed=seed)
+    return layered_cloth(layers, nx, seed=seed, stretch_scale=CONFIG_STRETCH_SCALE)

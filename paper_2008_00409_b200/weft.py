@@ -217,6 +217,34 @@ def _f64(a):
     return np.ascontiguousarray(a, np.float64).reshape(-1)
 
 
+def _state_buf(a, n: int, what: str, output: bool):
+    """A state buffer handed to the library as a raw pointer: exactly n
+    contiguous float64 values (numpy array or torch tensor, host or device).
+    Inputs given as other array-likes are converted; anything the library
+    could read or write past the end of is rejected."""
+    if a is None:
+        raise Error(f"{what}: buffer is None")
+    if hasattr(a, "data_ptr") and not isinstance(a, np.ndarray):
+        import torch
+        if a.dtype != torch.float64 or not a.is_contiguous() or a.numel() != n:
+            raise DimensionError(f"{what}: need a contiguous float64 tensor of {n} values "
+                                 f"(got {a.dtype}, {a.numel()} values, contiguous={a.is_contiguous()})")
+        return a
+    if not isinstance(a, np.ndarray):
+        if output:
+            raise Error(f"{what}: output must be a numpy array or a torch tensor")
+        a = np.asarray(a)
+    if output:
+        if a.dtype != np.float64 or not a.flags.c_contiguous or not a.flags.writeable or a.size != n:
+            raise DimensionError(f"{what}: need a writable C-contiguous float64 array of {n} values "
+                                 f"(got {a.dtype}, {a.size} values)")
+        return a
+    a = _f64(a)
+    if a.size != n:
+        raise DimensionError(f"{what}: need {n} values, got {a.size}")
+    return a
+
+
 # ---------------------------------------------------------------------------
 # free functions
 # ---------------------------------------------------------------------------
@@ -518,9 +546,14 @@ class Engine:
         return xc, rep
 
     # -- device-resident step -----------------------------------------------
+    def _state_len(self) -> int:
+        return 3 * self.rank_info().global_rows
+
     def sim_set_state(self, x, v):
-        _check(LIB.weft_gpu_sim_set_state(self._ctx, _ptr(_f64(x) if isinstance(x, np.ndarray) else x),
-                                          _ptr(_f64(v) if isinstance(v, np.ndarray) else v)))
+        n = self._state_len()
+        x = _state_buf(x, n, "sim_set_state: x", False)
+        v = _state_buf(v, n, "sim_set_state: v", False)
+        _check(LIB.weft_gpu_sim_set_state(self._ctx, _ptr(x), _ptr(v)))
 
     def sim_set_obstacles(self, dt: float, x_begin, x_end):
         """Obstacle vertex positions at the step's start and end (soup
@@ -535,12 +568,20 @@ class Engine:
     def sim_step_io(self, x_in, v_in, params: SimParams, x_out, v_out) -> StepReport:
         """weft_gpu_sim_step_io: upload (x, v), one step, read (x, v) back,
         with the copies overlapped with the broad phases."""
+        n = self._state_len()
+        x_in = _state_buf(x_in, n, "sim_step_io: x_in", False)
+        v_in = _state_buf(v_in, n, "sim_step_io: v_in", False)
+        x_out = _state_buf(x_out, n, "sim_step_io: x_out", True)
+        v_out = _state_buf(v_out, n, "sim_step_io: v_out", True)
         rep = StepReport()
         _check(LIB.weft_gpu_sim_step_io(self._ctx, _ptr(x_in), _ptr(v_in), C.byref(params), _ptr(x_out), _ptr(v_out),
                                         C.byref(rep)))
         return rep
 
     def sim_get_state(self, x=None, v=None):
+        n = self._state_len()
+        x = None if x is None else _state_buf(x, n, "sim_get_state: x", True)
+        v = None if v is None else _state_buf(v, n, "sim_get_state: v", True)
         _check(LIB.weft_gpu_sim_get_state(self._ctx, _ptr(x), _ptr(v)))
 
 

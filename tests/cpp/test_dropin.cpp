@@ -243,3 +243,136 @@ TEST_CASE("drop-in build_zones / distribute_zones / resolve_zones equal the refe
     CHECK(a == b);
   }
 }
+
+namespace {
+
+// Two stacked grid layers in DCD proximity (contacts every step).
+ClothMesh two_layer_cloth(int nx, double spacing, double gap) {
+  std::vector<Vec3> verts;
+  std::vector<std::array<int, 3>> tris;
+  for (int layer = 0; layer < 2; ++layer) {
+    const auto g = make_grid_mesh(nx, nx, spacing * (nx - 1), spacing * (nx - 1), Vec3(0, 0, layer * gap), 0.15);
+    const int off = static_cast<int>(verts.size());
+    verts.insert(verts.end(), g.rest_positions.begin(), g.rest_positions.end());
+    for (const auto& t : g.triangles) tris.push_back({t[0] + off, t[1] + off, t[2] + off});
+  }
+  return ClothMesh::build(std::move(verts), std::move(tris), 0.15);
+}
+
+template <class V>
+double max_rel_err(const V& a, const V& b) {
+  double scale = 1e-300, err = 0.0;
+  for (std::size_t i = 0; i < a.size(); ++i) {
+    scale = std::max(scale, std::abs(a[i]));
+    err = std::max(err, std::abs(a[i] - b[i]));
+  }
+  return err / scale;
+}
+
+}  // namespace
+
+TEST_CASE("drop-in spmv_serial is bitwise the reference spmv_serial") {
+  oracle::Rng rng(61);
+  for (int trial = 0; trial < 8; ++trial) {
+    const int rows = rng.uniform_int(1, 60);
+    const auto a = oracle::random_bell(rng, rows, 4);
+    std::vector<double> x(static_cast<std::size_t>(3 * rows));
+    for (auto& v : x) v = rng.uniform(-2.0, 2.0);
+    CHECK(spmv_serial<double>(a, x) == gpu::spmv_serial<double>(a, x));
+  }
+  const auto a = oracle::random_bell(rng, 5, 2);
+  std::vector<double> bad(4);
+  CHECK_THROWS_AS(gpu::spmv_serial<double>(a, bad), DimensionError);
+}
+
+TEST_CASE("drop-in step_system equals the reference step_system, with contacts, across repeated calls") {
+  const auto mesh = two_layer_cloth(9, 0.004, 0.003);
+  const int p = mesh.vertex_count();
+  std::vector<std::uint8_t> pinned(static_cast<std::size_t>(p), 0);
+  pinned[0] = pinned[8] = 1;
+  const auto soup = CollisionSoup::build(mesh.triangles, p, std::vector<std::uint8_t>(static_cast<std::size_t>(p), 1));
+  MaterialParams params;
+  params.damping = 0.001;
+  params.air_drag = 0.2;
+  oracle::Rng rng(62);
+  const double dt = 1.0 / 240.0;
+  for (int n : {1, 2}) {
+    Engine engine(n);
+    SimState state = SimState::rest(mesh);
+    for (int call = 0; call < 4; ++call) {
+      CAPTURE(n);
+      CAPTURE(call);
+      for (auto& v : state.v) v = rng.vec3(-0.2, 0.2);
+      CollisionParams cp;
+      cp.thickness = 0.005;
+      const auto prox = collide(engine, soup, state.x, state.x, CollisionMode::Discrete, cp);
+      ContactParams kp;
+      kp.thickness = 0.005;
+      const auto contacts = proximities_to_elements(prox.proximities, soup, state.x, state.v, mesh.vertex_mass, dt, kp);
+      REQUIRE(!contacts.empty());
+      const auto ref = step_system<double>(engine, mesh, state, params, pinned, contacts, dt, Vec3(0, 0, -9.81),
+                                           Vec3(0.5, 0, 0));
+      const auto gpu = gpu::step_system<double>(engine, mesh, state, params, pinned, contacts, dt, Vec3(0, 0, -9.81),
+                                                Vec3(0.5, 0, 0));
+      CHECK((dense(ref.matrix) - dense(gpu.matrix)).cwiseAbs().maxCoeff() == 0.0);
+      CHECK(max_rel_err(ref.rhs.gather(), gpu.rhs.gather()) <= 1e-12);
+      // the cached static list must follow a material change
+      if (call == 2) params.shear *= 2.0;
+    }
+  }
+}
+
+TEST_CASE("a Simulator-style loop on the drop-ins tracks the reference loop") {
+  // driver.cpp:132-206 without impact zones: DCD collide -> contact
+  // elements -> step_system -> pcg_solve -> v += dv, x += dt v, with every
+  // hot-path call swapped for weft::gpu:: in the second loop.
+  const auto mesh = two_layer_cloth(10, 0.004, 0.003);
+  const int p = mesh.vertex_count();
+  std::vector<std::uint8_t> pinned(static_cast<std::size_t>(p), 0);
+  for (int i = 0; i < 10; ++i) pinned[static_cast<std::size_t>(90 + i)] = pinned[static_cast<std::size_t>(190 + i)] = 1;
+  const auto soup = CollisionSoup::build(mesh.triangles, p, std::vector<std::uint8_t>(pinned.size(), 1));
+  const double dt = 1.0 / 240.0;
+  const int n = 2;
+  Engine engine(n);
+  ValidatedSchedule sched(generate_work_queues(FatTree::make(n)), n);
+  PcgConfig cfg;
+  cfg.rel_tolerance = 1e-10;
+  CollisionParams cp;
+  cp.thickness = 0.005;
+  ContactParams kp;
+  kp.thickness = 0.005;
+  SimState sr = SimState::rest(mesh), sg = sr;
+  for (int step = 0; step < 6; ++step) {
+    CAPTURE(step);
+    const auto pr = collide(engine, soup, sr.x, sr.x, CollisionMode::Discrete, cp);
+    const auto pg = gpu::collide(engine, soup, sg.x, sg.x, CollisionMode::Discrete, cp);
+    CHECK(pr.proximities.size() == pg.proximities.size());
+    const auto cr = proximities_to_elements(pr.proximities, soup, sr.x, sr.v, mesh.vertex_mass, dt, kp);
+    const auto cg = proximities_to_elements(pg.proximities, soup, sg.x, sg.v, mesh.vertex_mass, dt, kp);
+    const auto ar = step_system<double>(engine, mesh, sr, MaterialParams{}, pinned, cr, dt, Vec3(0, 0, -9.81),
+                                        Vec3::Zero());
+    const auto ag = gpu::step_system<double>(engine, mesh, sg, MaterialParams{}, pinned, cg, dt, Vec3(0, 0, -9.81),
+                                             Vec3::Zero());
+    DistVector<double> dr(&engine, ar.matrix.partitions), dg(&engine, ag.matrix.partitions);
+    const auto rr = pcg_solve(engine, ar.matrix, sched, ar.rhs, dr, cfg);
+    const auto rg = gpu::pcg_solve(engine, ag.matrix, sched, ag.rhs, dg, cfg);
+    REQUIRE(rr.converged);
+    REQUIRE(rg.converged);
+    const auto vr = dr.gather(), vg = dg.gather();
+    for (int i = 0; i < p; ++i) {
+      for (int c = 0; c < 3; ++c) {
+        sr.v[static_cast<std::size_t>(i)][c] += vr[static_cast<std::size_t>(3 * i + c)];
+        sg.v[static_cast<std::size_t>(i)][c] += vg[static_cast<std::size_t>(3 * i + c)];
+      }
+      sr.x[static_cast<std::size_t>(i)] += dt * sr.v[static_cast<std::size_t>(i)];
+      sg.x[static_cast<std::size_t>(i)] += dt * sg.v[static_cast<std::size_t>(i)];
+    }
+    std::vector<double> xr, xg;
+    for (int i = 0; i < p; ++i)
+      for (int c = 0; c < 3; ++c) {
+        xr.push_back(sr.x[static_cast<std::size_t>(i)][c]);
+        xg.push_back(sg.x[static_cast<std::size_t>(i)][c]);
+      }
+    CHECK(max_rel_err(xr, xg) <= 1e-9);
+  }
+}

@@ -102,18 +102,23 @@ def main():
                             message=np.array(msg), x_out=xc, report=np.array([rep[f] for f in ZONE_REPORT]))
     # scenes (scene.cpp) run by the reference Simulator (driver.cpp:55-215):
     # per-frame counts and the final state (tests/scenes_gen.py scenes)
-    from oracle_bindings import RefScene
+    from oracle_bindings import RefError, RefScene
     from scenes_gen import SCENES, scene_text
     for name in SCENES:
         rs = RefScene(REF, text=scene_text(name))
-        frames = []
+        frames, failure = [], ""
         for _ in range(int(rs.config()["frames"])):
-            r = rs.step()
+            try:
+                r = rs.step()
+            except RefError as e:  # the scene's last frame fails in the reference (config_A)
+                failure = str(e)
+                break
             frames.append([r["pcg_iterations"], r["proximities"], r["contacts"], r["impacts"], r["zone_count"],
                            r["zone_outer"]])
         x, v = rs.state()
+        extra = {"failure": np.array(failure)} if failure else {"obj": np.array(rs.save_obj())}
         np.savez_compressed(os.path.join(HERE, f"scene_{name}.npz"), text=np.array(scene_text(name)),
-                            frames=np.array(frames, np.int64), x=x, v=v, obj=np.array(rs.save_obj()))
+                            frames=np.array(frames, np.int64), x=x, v=v, **extra)
         rs.close()
     # SpMV: oracle::random_bell (sparse_oracle.cpp:7-23), pipelined at n = 1, 2, 4.
     for k, (seed, rows) in enumerate([(5, 7), (6, 40)]):

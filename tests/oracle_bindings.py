@@ -500,6 +500,18 @@ class RefSim:
                 "ms_assemble", "ms_solve")
         return dict(zip(keys, out.tolist()))
 
+    def time_functions(self, dt, thickness, cell_scale=1.5, reps=3):
+        """Median ms of fill_matrix, spmv_pipelined and build_grid (DCD) on
+        the current state (ref_sim_time_functions)."""
+        L = self.ref.lib
+        L.ref_sim_time_functions.restype = C.c_int32
+        prm = np.array([dt, thickness, cell_scale], np.float64)
+        out = np.zeros(3)
+        st = L.ref_sim_time_functions(C.c_void_p(self.h), ptr(prm), C.c_int32(reps), ptr(out))
+        if st:
+            raise RuntimeError(L.ref_last_error().decode())
+        return {"fill_matrix_ms": out[0], "spmv_pipelined_ms": out[1], "build_grid_ms": out[2]}
+
     def step_contacts(self, dt, thickness, cell_scale=1.5, tol=1e-4, max_it=400, stiffness_scale=4.0,
                       friction=0.2, damping=0.0, zones=None):
         """Simulator::step_impl (ref_sim_step_contacts): without impact

@@ -44,6 +44,34 @@ SCENES = {
         "collision": {"thickness": 0.004, "friction": 0.1, "cell_scale": 1.7},
         "zones": {"outer_cap": 12, "initial_penalty": 12.0},
     },
+    # BASELINE config A (SURVEY.md §8 "Config shorthand"): the sheet of
+    # scenes/sphere.json (W = 0.5 m, its solver, damping and drag) at 100 x
+    # 100 with pin_top_edge and the keyframed sphere collider (r = 0.12,
+    # scenes/sphere.json:41-52), dt = 1/240. sphere.json is tuned for its
+    # 40 x 40 grid (12.8 mm spacing); at 5.05 mm two of its values break the
+    # reference itself: thickness 0.006 exceeds the spacing (445,799
+    # proximities at frame 0, ZoneFailure at frame 2), and the area-weighted
+    # stretch conditions (elements.cpp:170-172) lose (12.8/5.05)^4 = 41x of
+    # their stiffness (the sheet over-stretches onto the sphere, ZoneFailure
+    # at frame 14). Here: thickness 0.0025 = 0.5 x spacing (the rule of the
+    # other configs) and stretch/shear x41; contacts with the sphere start at
+    # frame 12 and the reference raises ZoneFailure at frame 21 — the last
+    # frame, which the GPU must reproduce too.
+    "config_A": {
+        "name": "config_A", "dt": 1 / 240, "frames": 22, "devices": 2,
+        "gravity": [0, 0, -9.81],
+        "material": {"stretch": 20500, "shear": 2050, "bend": 2e-5, "density": 0.15, "damping": 0.003,
+                     "air_drag": 0.3},
+        "cloth": {"grid": {"nx": 100, "ny": 100, "width": 0.5, "height": 0.5, "origin": [-0.25, -0.25, 0.065]},
+                  "pin_top_edge": True},
+        "collision": {"thickness": 0.0025, "contact_stiffness_scale": 4.0, "friction": 0.3},
+        "solver": {"tolerance": 1e-4, "max_iterations": 400},
+        "obstacles": [{"sphere": {"center": [0.0, 0.0, -0.07], "radius": 0.12, "stacks": 12, "slices": 18},
+                       "keyframes": [{"time": 0.0, "translate": [0, 0, 0]},
+                                     {"time": 0.14, "translate": [0.06, 0, 0]},
+                                     {"time": 0.28, "translate": [-0.06, 0, 0]},
+                                     {"time": 0.42, "translate": [0, 0, 0]}]}],
+    },
 }
 
 

@@ -1,0 +1,121 @@
+"""Parity at BASELINE config D, the configuration the headline metric is
+quoted on (3 x 525^2 layered cloth, 1,647,456 triangles; bench.py's scene and
+trajectory): the GPU hot path against the compiled reference on the same
+inputs at full size.
+
+* trajectory: 3 steps from rest through weft_gpu_sim_step vs the reference's
+  step (ref_sim_step: collide's broad phase, step_system, pcg_solve at the
+  bench's tol 1e-4, candidate update, CCD broad phase; driver.cpp:96-215):
+  identical DCD / CCD candidate counts, PCG iterations within 2 %, positions
+  and velocities within the north_star 1e-5 relative after every step;
+* broad phase on the GPU state after those steps: bitwise cell size, cell
+  keys, and the full DCD and CCD candidate-pair lists (sets and walk order,
+  compared chunk by chunk; collision.cpp:118-179, 329-378);
+* assembly on the same state: identical pattern and bitwise SpdProjected
+  values, rhs within 1e-12 (assembly.hpp:74-220).
+"""
+import numpy as np
+import pytest
+
+from oracle_bindings import REF, RefSim
+
+pytestmark = [pytest.mark.gpu, pytest.mark.ref]
+
+
+def rel(a, b):
+    return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-300))
+
+
+@pytest.fixture(scope="module")
+def D():
+    from paper_2008_00409_b200 import scenes, weft
+    sc = scenes.config("D")
+    mesh = weft.ClothMesh.build(sc.verts, sc.tris, sc.density)
+    elems = mesh.build_elements(sc.material, sc.gravity)
+    params = weft.SimParams(sc.dt, sc.thickness, 1.5, weft.PcgConfig(1e-4, 400, weft.PRECOND_BLOCK_JACOBI),
+                            weft.JAC_SPD)
+    eng = weft.Engine(1)
+    eng.set_vertices(mesh.vertex_mass, sc.pinned)
+    eng.set_elements(elems)
+    eng.set_soup(mesh.vertex_count, sc.tris)
+    eng.sim_set_state(sc.verts.reshape(-1), np.zeros(3 * mesh.vertex_count))
+    steps = [eng.sim_step(params) for _ in range(3)]
+    p = mesh.vertex_count
+    x, v = np.zeros(3 * p), np.zeros(3 * p)
+    eng.sim_get_state(x, v)
+    yield dict(sc=sc, mesh=mesh, elems=elems, eng=eng, steps=steps, x=x, v=v, weft=weft)
+    eng.close()
+
+
+def test_configD_trajectory_vs_reference(D):
+    import os
+    sc, mesh, weft = D["sc"], D["mesh"], D["weft"]
+    devices = 1
+    while devices * 2 <= min(os.cpu_count() or 1, 32):
+        devices *= 2
+    ref = RefSim(REF, sc.verts, sc.tris, sc.pinned, sc.density, sc.material, devices)
+    p = mesh.vertex_count
+    with weft.Engine(1) as eng:
+        eng.set_vertices(mesh.vertex_mass, sc.pinned)
+        eng.set_elements(D["elems"])
+        eng.set_soup(p, sc.tris)
+        eng.sim_set_state(sc.verts.reshape(-1), np.zeros(3 * p))
+        params = weft.SimParams(sc.dt, sc.thickness, 1.5, weft.PcgConfig(1e-4, 400, weft.PRECOND_BLOCK_JACOBI),
+                                weft.JAC_SPD)
+        for k in range(3):
+            r = eng.sim_step(params)
+            rr = ref.step(sc.dt, sc.thickness)
+            assert (r.dcd_candidates, r.ccd_candidates) == (rr["dcd_candidates"], rr["ccd_candidates"]), k
+            assert abs(r.pcg_iterations - rr["pcg_iterations"]) <= max(1, 0.02 * rr["pcg_iterations"]), k
+            x, v = np.zeros(3 * p), np.zeros(3 * p)
+            eng.sim_get_state(x, v)
+            xr, vr = ref.get_state()
+            assert rel(x, xr) <= 1e-5 and rel(v, vr) <= 1e-5, (k, rel(x, xr), rel(v, vr))
+    ref.close()
+
+
+@pytest.mark.parametrize("mode", ["dcd", "ccd"])
+def test_configD_broad_phase_pairs_bitwise(D, mode):
+    sc, eng, weft = D["sc"], D["eng"], D["weft"]
+    x0 = D["x"]
+    x1 = x0 + sc.dt * D["v"] if mode == "ccd" else None
+    m = weft.CONTINUOUS if mode == "ccd" else weft.DISCRETE
+    p = D["mesh"].vertex_count
+    g = REF.build_grid(p, sc.tris, x0, x1, m, sc.thickness)
+    try:
+        eng.build_grid(x0, x1, m, sc.thickness)
+        info = eng.grid_info()
+        assert info.cell_size == g.cell_size
+        assert (info.cells, info.entries, info.total) == (len(g.cell_keys), len(g.cell_tris), g.total)
+        gg = eng.download_grid(len(sc.tris))
+        assert np.array_equal(gg.cell_keys, g.cell_keys) and np.array_equal(gg.cell_offsets, g.cell_offsets)
+        assert np.array_equal(gg.cell_tris, g.cell_tris) and np.array_equal(gg.prefix, g.prefix)
+        assert np.array_equal(gg.tri_boxes, g.tri_boxes)
+        # every candidate pair, in walk order, 8 chunks of the pair space
+        bounds = np.linspace(0, g.total, 9).astype(np.int64)
+        n = 0
+        for b, e in zip(bounds[:-1], bounds[1:]):
+            a = eng.candidates(int(b), int(e))
+            r = REF.candidates(g, int(b), int(e))
+            assert np.array_equal(a, r), (mode, b, e)
+            n += len(a)
+        assert n > 50_000_000
+    finally:
+        REF.free_grid(g)
+
+
+def test_configD_assembly_bitwise(D):
+    sc, mesh, elems, weft = D["sc"], D["mesh"], D["elems"], D["weft"]
+    x, v = D["x"], D["v"]
+    xa = x + sc.dt * v
+    o = REF.fill_matrix(elems, x, xa, v, mesh.vertex_mass, sc.pinned, sc.dt, weft.JAC_SPD, n=1)
+    with weft.Engine(1) as eng:
+        eng.set_vertices(mesh.vertex_mass, sc.pinned)
+        eng.set_elements(elems)
+        eng.fill_matrix(x, xa, v, sc.dt, weft.JAC_SPD)
+        m = eng.download_matrix()
+        rhs = eng.download_rhs()
+    assert np.array_equal(m.row_ptr, o.row_ptr) and np.array_equal(m.cols, o.cols)
+    assert len(m.cols) > 9_000_000
+    assert np.array_equal(m.vals.view(np.uint64), o.vals.view(np.uint64))
+    assert rel(rhs, o.rhs) <= 1e-12

@@ -40,11 +40,57 @@ def test_simulator_vs_reference_golden(S, path):
         assert abs(got[0] - fr[0]) <= max(1, 0.02 * fr[0]), (k, got, fr)
     x, v = sim.state()
     assert rel(x.reshape(-1), g["x"]) <= 1e-8 and rel(v.reshape(-1), g["v"]) <= 1e-8
+    if "failure" in g:
+        # the reference raised ZoneFailure on the next frame (config_A); the
+        # GPU must too, with the same message, and keep the last committed
+        # state (x, v) untouched like Simulator::step_impl's local v_cand
+        from paper_2008_00409_b200 import weft
+        with pytest.raises(weft.ZoneFailure) as e:
+            sim.step()
+        assert str(e.value) == str(g["failure"])
+        x2, v2 = sim.state()
+        assert np.array_equal(x2, x) and np.array_equal(v2, v)
     sim.close()
 
 
 @pytest.mark.ref
-@pytest.mark.parametrize("name", sorted(SCENES))
+def test_config_A_sphere_vs_reference_live(S):
+    """BASELINE config A (100 x 100 sheet, pinned top edge, keyframed sphere
+    collider; tests/scenes_gen.py) through the GPU Simulator vs the reference
+    Simulator frame by frame: 21 frames (contacts with the sphere from frame
+    12), then the frame on which the reference raises ZoneFailure."""
+    from paper_2008_00409_b200 import weft
+    from oracle_bindings import RefError
+    sc = S.parse_scene(scene_text("config_A"))
+    sim = S.Simulator(sc)
+    rs = RefScene(REF, text=scene_text("config_A"))
+    contacts = 0
+    for k in range(sc.config.frames):
+        try:
+            rr = rs.step()
+        except RefError as ref_err:
+            with pytest.raises(weft.ZoneFailure) as e:
+                sim.step()
+            assert str(e.value) == str(ref_err), k
+            break
+        r = sim.step()
+        assert (r.proximities, r.contacts, r.impacts, r.zone_count) == (
+            rr["proximities"], rr["contacts"], rr["impacts"], rr["zone_count"]), k
+        assert abs(r.pcg_iterations - rr["pcg_iterations"]) <= max(1, 0.02 * rr["pcg_iterations"]), k
+        contacts += r.contacts
+        x, v = sim.state()
+        xr, vr = rs.state()
+        assert rel(x.reshape(-1), xr) <= 1e-8 and rel(v.reshape(-1), vr) <= 1e-8, k
+    assert k >= 20 and contacts > 0
+    x, v = sim.state()
+    xr, vr = rs.state()
+    assert rel(x.reshape(-1), xr) <= 1e-8 and rel(v.reshape(-1), vr) <= 1e-8
+    rs.close()
+    sim.close()
+
+
+@pytest.mark.ref
+@pytest.mark.parametrize("name", sorted(n for n in SCENES if n != "config_A"))
 def test_simulator_vs_reference_live(S, name):
     sc = S.parse_scene(scene_text(name))
     sim = S.Simulator(sc)
