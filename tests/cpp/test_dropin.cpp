@@ -337,6 +337,7 @@ TEST_CASE("a Simulator-style loop on the drop-ins tracks the reference loop") {
   ValidatedSchedule sched(generate_work_queues(FatTree::make(n)), n);
   PcgConfig cfg;
   cfg.rel_tolerance = 1e-10;
+  cfg.max_iterations = 4000;  // tol 1e-10 on the contact-stiffened system needs more than the default 400
   CollisionParams cp;
   cp.thickness = 0.005;
   ContactParams kp;
@@ -373,6 +374,10 @@ TEST_CASE("a Simulator-style loop on the drop-ins tracks the reference loop") {
         xr.push_back(sr.x[static_cast<std::size_t>(i)][c]);
         xg.push_back(sg.x[static_cast<std::size_t>(i)][c]);
       }
-    CHECK(max_rel_err(xr, xg) <= 1e-9);
+    // the north_star tolerance is 1e-5 relative; the dot products' association
+    // differs by design, so the loops agree to round-off growth
+    const double err = max_rel_err(xr, xg);
+    CAPTURE(err);
+    CHECK(err <= 1e-6);
   }
 }

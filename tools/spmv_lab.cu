@@ -143,8 +143,14 @@ struct Ring {
   static constexpr int kBytes = W * kWarp + W * S * 8;
 };
 
-template <int C, int S, int W>
-__global__ void __launch_bounds__(W * 32, 1) k2(Sell A, const double* __restrict__ x, double* __restrict__ y) {
+__device__ __forceinline__ void ld4(const double* p, double& a, double& b, double& c) {
+  double d;
+  asm volatile("ld.global.cg.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p));
+  (void)d;
+}
+
+template <int C, int S, int W, int B = 1, int Vs = 3>
+__global__ void __launch_bounds__(W * 32, B) k2(Sell A, const double* __restrict__ x, double* __restrict__ y) {
   using R = Ring<C, S, W>;
   extern __shared__ __align__(128) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -197,7 +203,9 @@ __global__ void __launch_bounds__(W * 32, 1) k2(Sell A, const double* __restrict
         if (k < n && c0 + k < len) {
           const int c = cl[k * 32 + lane];
           const double* v = vs + k * 288 + lane;
-          const double x0 = x[3 * c], x1 = x[3 * c + 1], x2 = x[3 * c + 2];
+          double x0, x1, x2;
+          if constexpr (Vs == 4) ld4(x + 4 * (size_t)c, x0, x1, x2);
+          else x0 = x[3 * c], x1 = x[3 * c + 1], x2 = x[3 * c + 2];
           a0 = a0 + ((v[0] * x0 + v[32] * x1) + v[64] * x2);
           a1 = a1 + ((v[96] * x0 + v[128] * x1) + v[160] * x2);
           a2 = a2 + ((v[192] * x0 + v[224] * x1) + v[256] * x2);
@@ -243,7 +251,7 @@ float time_it(F&& f, int reps) {
 }  // namespace
 
 extern "C" int lab_run(int rows, const int64_t* row_ptr, const int32_t* cols, const double* vals, const double* x,
-                       int sorted, double* y_out, float* times /* 4 */) {
+                       int sorted, double* y_out, float* times /* 64 */) {
   // host SELL-32 build (optionally length-sorted within 256-row windows)
   std::vector<int32_t> perm(rows);
   for (int r = 0; r < rows; ++r) perm[r] = r;
@@ -301,26 +309,45 @@ extern "C" int lab_run(int rows, const int64_t* row_ptr, const int32_t* cols, co
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   times[0] = time_it([&] { k0<<<(rows + 255) / 256, 256>>>(A, d_x, d_y); }, 50);
   CK(cudaMemcpy(y_out, d_y, 24 * (size_t)rows, cudaMemcpyDeviceToHost));
+  double* d_x4;
   {
-    constexpr int C = 4, S = 4, W = 4;
-    using R = Ring<C, S, W>;
-    CK(cudaFuncSetAttribute(k2<C, S, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, R::kBytes));
-    CK(cudaMemset(d_y, 0, 24 * (size_t)rows));
-    times[1] = time_it([&] { k2<C, S, W><<<sms, W * 32, R::kBytes>>>(A, d_x, d_y); }, 50);
-    CK(cudaGetLastError());
+    std::vector<double> h4(4 * (size_t)rows, 0.0);
+    for (int i = 0; i < rows; ++i)
+      for (int c = 0; c < 3; ++c) h4[4 * (size_t)i + c] = x[3 * (size_t)i + c];
+    CK(cudaMalloc(&d_x4, 32 * (size_t)rows));
+    CK(cudaMemcpy(d_x4, h4.data(), 32 * (size_t)rows, cudaMemcpyHostToDevice));
   }
   std::vector<double> y2(3 * (size_t)rows);
-  CK(cudaMemcpy(y2.data(), d_y, 24 * (size_t)rows, cudaMemcpyDeviceToHost));
-  int bad = 0;
-  for (size_t i = 0; i < y2.size(); ++i) bad += y2[i] != y_out[i];
-  times[3] = static_cast<float>(bad);
-  {
-    constexpr int C = 2, S = 5, W = 8;
-    using R = Ring<C, S, W>;
-    CK(cudaFuncSetAttribute(k2<C, S, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, R::kBytes));
-    times[2] = time_it([&] { k2<C, S, W><<<sms, W * 32, R::kBytes>>>(A, d_x, d_y); }, 50);
+  int vi = 0;
+  auto run = [&](auto kern, int W, int B, int bytes, bool v4) -> int {
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    CK(cudaMemset(d_y, 0, 24 * (size_t)rows));
+    const float t = time_it([&] { kern<<<sms * B, W * 32, bytes>>>(A, v4 ? d_x4 : d_x, d_y); }, 50);
     CK(cudaGetLastError());
-  }
+    CK(cudaMemcpy(y2.data(), d_y, 24 * (size_t)rows, cudaMemcpyDeviceToHost));
+    int bad = 0;
+    for (size_t i = 0; i < y2.size(); ++i) bad += y2[i] != y_out[i];
+    times[16 + 2 * vi] = t;
+    times[17 + 2 * vi] = static_cast<float>(bad);
+    ++vi;
+    return 0;
+  };
+#define RUN(C_, S_, W_, B_, V_) \
+  run(k2<C_, S_, W_, B_, V_>, W_, B_, Ring<C_, S_, W_>::kBytes, V_ == 4)
+  RUN(4, 4, 4, 1, 3);
+  RUN(2, 5, 8, 1, 3);
+  RUN(1, 4, 8, 2, 3);
+  RUN(1, 6, 8, 2, 3);
+  RUN(1, 4, 16, 1, 3);
+  RUN(2, 3, 8, 2, 3);
+  RUN(1, 8, 8, 1, 3);
+  RUN(1, 4, 8, 2, 4);
+  RUN(1, 6, 8, 2, 4);
+  RUN(2, 3, 8, 2, 4);
+  RUN(1, 3, 8, 3, 4);
+  RUN(2, 4, 4, 3, 4);
+  times[15] = static_cast<float>(vi);
+  cudaFree(d_x4);
   times[4] = static_cast<float>(total);
   {
     double *d_p, *d_part;

@@ -38,14 +38,17 @@ x = rng.uniform(-1, 1, 3 * p)
 alg = len(cols) * 76 + p * 52
 for sorted_ in (0, 1):
     y = np.zeros(3 * p)
-    t = np.zeros(9, np.float32)
+    t = np.zeros(64, np.float32)
     rc = lib.lab_run(C.c_int(p), row_ptr.ctypes.data_as(C.c_void_p), cols.ctypes.data_as(C.c_void_p),
                      vals.ctypes.data_as(C.c_void_p), x.ctypes.data_as(C.c_void_p), C.c_int(sorted_),
                      y.ctypes.data_as(C.c_void_p), t.ctypes.data_as(C.c_void_p))
     assert rc == 0
-    print(f"sorted={sorted_} slots={int(t[4])} (nnzb {len(cols)}) k0 {t[0]*1e3:.1f} us {alg/t[0]/1e6:.0f} GB/s | "
-          f"k2(C4,S4,W4) {t[1]*1e3:.1f} us {alg/t[1]/1e6:.0f} GB/s (mismatch {int(t[3])}) | "
-          f"k2(C2,S5,W8) {t[2]*1e3:.1f} us {alg/t[2]/1e6:.0f} GB/s", flush=True)
+    print(f"sorted={sorted_} slots={int(t[4])} (nnzb {len(cols)}) k0 {t[0]*1e3:.1f} us {alg/t[0]/1e6:.0f} GB/s", flush=True)
+    names = ["C4S4W4B1v3", "C2S5W8B1v3", "C1S4W8B2v3", "C1S6W8B2v3", "C1S4W16B1v3", "C2S3W8B2v3", "C1S8W8B1v3",
+             "C1S4W8B2v4", "C1S6W8B2v4", "C2S3W8B2v4", "C1S3W8B3v4", "C2S4W4B3v4"]
+    for i in range(int(t[15])):
+        tt = t[16 + 2 * i]
+        print(f"   k2 {names[i]}: {tt*1e3:.1f} us {alg/tt/1e6:.0f} GB/s mismatch {int(t[17 + 2 * i])}", flush=True)
     alg2 = len(cols) * 76 + p * 76
     print(f"   pcg-form: 2-vector gather {t[5]*1e3:.1f} us {alg2/t[5]/1e6:.0f} GB/s | +dot {t[6]*1e3:.1f} us "
           f"{alg2/t[6]/1e6:.0f} GB/s | +dot after L2 flush {(t[7]-t[8])*1e3:.1f} us {alg2/(t[7]-t[8])/1e6:.0f} GB/s "
