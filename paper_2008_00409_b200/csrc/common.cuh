@@ -164,6 +164,9 @@ struct CommHeader {
   unsigned long long vec_ready[kMaxRanks];    // PCG / SpMV gather vectors published
   unsigned long long red_ready[kMaxRanks];    // reduction partials published
   unsigned long long state_ready[kMaxRanks];  // sim state (v, x_cand) rows published
+  unsigned long long hits_ready[kMaxRanks];   // narrow-phase hits of the writer's share published
+  long long hit_count[kMaxRanks];             // ... their count (unique within the share)
+  long long pair_count[kMaxRanks];            // ... and the share's candidate pairs
   double red[2][kMaxParts][4];                // [sequence parity][partition][value]
 };
 
@@ -175,7 +178,7 @@ struct CommView {
   const double* z[kMaxRanks] = {};        // every rank's gather vectors (global row index)
   const double* p[kMaxRanks] = {};
   char* base[kMaxRanks] = {};             // every rank's window base
-  unsigned long long* seq = nullptr;      // own counters: [0] vec, [1] red, [2] state, [3] error
+  unsigned long long* seq = nullptr;      // own counters: [0] vec, [1] red, [2] state, [3] error, [4] hits
 };
 
 }  // namespace weft_gpu

@@ -170,6 +170,7 @@ struct Ctx {
   DBuf<uint8_t> soup_movable;     // per soup vertex
   DBuf<unsigned long long> hit_count, hit_keys, hit_keys_sorted, contact_keys;
   DBuf<double> hit_vals, contact_vals;  // 8 per hit: gap | toi, normal, weights
+  DBuf<long long> hit_counts;           // rank group: every rank's hit / pair counts
   DBuf<int64_t> hit_idx, hit_idx_sorted, hit_flag;
   int64_t n_contacts_found = 0, narrow_pairs = 0, narrow_raw_hits = 0;
   DBuf<int> contact_active;      // proximities_to_elements: active count per vertex
@@ -298,6 +299,14 @@ void comm_free(Ctx& c);
 void publish_vectors(Ctx& c);  // z/p rows of this rank are final
 void rank_barrier(Ctx& c);
 void exchange_state(Ctx& c);   // sim: publish own v/x_cand rows, pull the peers'
+// collide's merge over ranks: the union of every rank's unique hits
+// (contact_keys / contact_vals), sorted and deduplicated, on every rank
+int64_t merge_hits(Ctx& c);
+// sort + dedup of n raw hits in hit_keys / hit_vals -> contact_keys / vals
+int64_t dedup_hits(Ctx& c, int64_t n);
+// collide (collision.cpp:391-417): build_grid + the narrow phase of this
+// rank's split_workload share, merged over the rank group
+int64_t collide(Ctx& c, const double* x0, const double* x1, int mode, double thickness, double cell_scale);
 
 // CUB scratch helper
 void* scratch(Ctx& c, size_t bytes);

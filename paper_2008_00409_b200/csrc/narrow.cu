@@ -808,7 +808,16 @@ int64_t narrow_phase(Ctx& c, const double* x0, const double* x1, int mode, doubl
       cap = static_cast<size_t>(nh);  // exact capacity, run once more
     }
   }
-  const int64_t n = static_cast<int64_t>(nh);
+  c.narrow_pairs = npairs;
+  c.narrow_raw_hits = static_cast<int64_t>(nh);
+  return dedup_hits(c, static_cast<int64_t>(nh));
+}
+
+// sort_dedup (collision.cpp:313-325): radix sort by key, the first of every
+// equal-key run kept (duplicates — one feature pair reached from several
+// triangle pairs — carry identical values).
+int64_t dedup_hits(Ctx& c, int64_t n) {
+  cudaStream_t s = c.stream;
   c.hit_keys_sorted.resize(static_cast<size_t>(n) + 1);
   c.hit_idx.resize(static_cast<size_t>(n) + 1);
   c.hit_idx_sorted.resize(static_cast<size_t>(n) + 1);
@@ -838,9 +847,17 @@ int64_t narrow_phase(Ctx& c, const double* x0, const double* x1, int mode, doubl
     WG_CUDA(cudaStreamSynchronize(s));
   }
   c.n_contacts_found = nu;
-  c.narrow_pairs = npairs;
-  c.narrow_raw_hits = n;
   return nu;
+}
+
+int64_t collide(Ctx& c, const double* x0, const double* x1, int mode, double thickness, double cell_scale) {
+  build_grid(c, x0, x1, mode, thickness, cell_scale);
+  // a rank of a group walks its split_workload share (collision.cpp:402)
+  const int64_t total = c.grid_total, base = total / c.world, extra = total % c.world;
+  const int64_t b = c.rank * base + std::min<int64_t>(c.rank, extra);
+  const int64_t e = b + base + (c.rank < extra ? 1 : 0);
+  const int64_t n = narrow_phase(c, x0, x1, mode, thickness, b, e);
+  return c.world > 1 ? merge_hits(c) : n;
 }
 
 void download_contacts(Ctx& c, int32_t* kab, double* vals) {

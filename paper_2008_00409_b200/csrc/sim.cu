@@ -138,12 +138,8 @@ weft_status weft_gpu_collide(weft_gpu_ctx* ctx, const double* x_begin, const dou
       weft_gpu::upload_vec(c, c.x_adv, x_end, n);
     }
     const double* x1 = ccd ? c.x_adv.data() : c.x_cur.data();
-    weft_gpu::build_grid(c, c.x_cur.data(), x1, mode, thickness, cell_scale);
-    // a rank of a group walks its split_workload share (collision.cpp:402)
-    const int64_t total = c.grid_total, base = total / c.world, extra = total % c.world;
-    const int64_t b = c.rank * base + std::min<int64_t>(c.rank, extra);
-    const int64_t e = b + base + (c.rank < extra ? 1 : 0);
-    const int64_t nh = weft_gpu::narrow_phase(c, c.x_cur.data(), x1, mode, thickness, b, e);
+    // replicated grid, this rank's share, merged over the group
+    const int64_t nh = weft_gpu::collide(c, c.x_cur.data(), x1, mode, thickness, cell_scale);
     if (count) *count = nh;
   });
 }
@@ -335,12 +331,13 @@ weft_status weft_gpu_sim_step(weft_gpu_ctx* ctx, const weft_sim_params* prm, wef
     const bool contacts = prm->contacts != 0;
     if (contacts) {
       // Simulator::step_impl stages 1-2 in full (driver.cpp:132-149): DCD
-      // collide, proximities_to_elements, step_system with the contacts.
-      if (c.world > 1) throw Error(WEFT_ERR_INVALID, "sim_step: contacts mode runs on one rank");
+      // collide, proximities_to_elements, step_system with the contacts. A
+      // rank group narrow-phases its shares and merges the hits, so every
+      // rank holds all contact elements; each assembles its own rows, whose
+      // contact columns may belong to any rank (the PCG pulls them over
+      // peer memory: the dynamic contact halo).
       WG_CUDA(cudaEventRecord(c.ev_side[0], s));
-      weft_gpu::build_grid(c, c.sim_x.data(), c.sim_x.data(), WEFT_DISCRETE, prm->thickness, prm->cell_scale);
-      nprox = weft_gpu::narrow_phase(c, c.sim_x.data(), c.sim_x.data(), WEFT_DISCRETE, prm->thickness, 0,
-                                     c.grid_total);
+      nprox = weft_gpu::collide(c, c.sim_x.data(), c.sim_x.data(), WEFT_DISCRETE, prm->thickness, prm->cell_scale);
       dcd = c.narrow_pairs;
       WG_CUDA(cudaEventRecord(c.ev_side[1], s));
       WG_CUDA(cudaEventRecord(ev[0], s));
@@ -441,13 +438,11 @@ weft_status weft_gpu_sim_step(weft_gpu_ctx* ctx, const weft_sim_params* prm, wef
       WG_CUDA(cudaEventRecord(c.ev_side[3], c.side));
     }
     // 5. impact broad phase (CCD) over begin -> candidate
-    weft_gpu::build_grid(c, c.sim_x.data(), c.sim_xc.data(), WEFT_CONTINUOUS, prm->thickness, prm->cell_scale);
-    share(c.grid_total, wb, we);
     int64_t ccd = 0;
     weft_zone_report zr{};
     float tz = 0;
     if (contacts) {
-      nimp = weft_gpu::narrow_phase(c, c.sim_x.data(), c.sim_xc.data(), WEFT_CONTINUOUS, prm->thickness, wb, we);
+      nimp = weft_gpu::collide(c, c.sim_x.data(), c.sim_xc.data(), WEFT_CONTINUOUS, prm->thickness, prm->cell_scale);
       ccd = c.narrow_pairs;
       if (prm->zones) {
         // 5-6. resolve_zones (driver.cpp:181-191): its first CCD round is
@@ -463,6 +458,8 @@ weft_status weft_gpu_sim_step(weft_gpu_ctx* ctx, const weft_sim_params* prm, wef
         cudaEventElapsedTime(&tz, c.ev_side[2], c.ev_side[3]);
       }
     } else {
+      weft_gpu::build_grid(c, c.sim_x.data(), c.sim_xc.data(), WEFT_CONTINUOUS, prm->thickness, prm->cell_scale);
+      share(c.grid_total, wb, we);
       ccd = weft_gpu::candidates(c, wb, we, nullptr, /*count_only=*/true);
     }
     WG_CUDA(cudaEventRecord(ev[5], s));

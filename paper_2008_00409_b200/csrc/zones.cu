@@ -586,16 +586,15 @@ std::vector<std::vector<int>> distribute_zones(const std::vector<int>& sizes, in
 // contact_keys/vals hold collide(CCD, x_begin, x_cand)).
 void resolve_zones(Ctx& c, const double* xb, double* xcand, const double* mass, double thickness, double cell_scale,
                    const weft_zone_params& zp, weft_zone_report& rep, bool have_first) {
-  if (c.world > 1) throw Error(WEFT_ERR_INVALID, "resolve_zones runs on one rank");
+  // A rank group runs the zone solve replicated (every rank holds all
+  // rows of x_begin / x_cand and, after the merged collide, all impacts):
+  // identical zones, positions and failures on every rank.
   cudaStream_t s = c.stream;
   rep = weft_zone_report{};
   const int64_t nverts = c.soup_verts;
   c.zn_prop.resize(3 * static_cast<size_t>(nverts) + 3);
   c.zn_m = 0;
-  auto collide_ccd = [&]() -> int64_t {
-    build_grid(c, xb, xcand, WEFT_CONTINUOUS, thickness, cell_scale);
-    return narrow_phase(c, xb, xcand, WEFT_CONTINUOUS, thickness, 0, c.grid_total);
-  };
+  auto collide_ccd = [&]() -> int64_t { return collide(c, xb, xcand, WEFT_CONTINUOUS, thickness, cell_scale); };
   const double max_move = zp.max_correction_factor * (zp.clearance < 1e-9 ? 1e-9 : zp.clearance);
   for (int outer = 0; outer < zp.outer_cap; ++outer) {
     const int64_t nf = (outer == 0 && have_first) ? c.n_contacts_found : collide_ccd();

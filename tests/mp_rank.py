@@ -11,6 +11,7 @@ from __future__ import annotations
 
 import os
 import sys
+import time
 
 import numpy as np
 
@@ -97,6 +98,36 @@ def run(eng_factory, world, rank, attach, steps=3):
     eng.sim_get_state(xg, vg)
     out["sim_x"], out["sim_v"] = xg, vg
     out["sim_dcd"], out["sim_ccd"], out["sim_its"] = np.array(dcd), np.array(ccd), np.array(its)
+    engines.append(eng)
+    # -- the whole Simulator::step_impl (driver.cpp:96-215): DCD collide
+    # (shares merged over the ranks), contact elements, step_system with the
+    # contacts (inter-layer contact columns cross the partition cut: the
+    # dynamic contact halo of the PCG), CCD collide, impact zones
+    eng = eng_factory()
+    eng.set_vertices(mesh.vertex_mass, sc.pinned)
+    attach(eng)
+    eng.set_elements(mesh.build_elements(sc.material, sc.gravity))
+    eng.set_soup(p, sc.tris)
+    # from rest: the pinned layers stay untangled (WEFT_CON_V0=1: the
+    # jittered v0, whose tangled layers end in ZoneFailure — the error path)
+    eng.sim_set_state(x0, v0 if os.environ.get("WEFT_CON_V0") == "1" else np.zeros_like(x0))
+    params = weft.SimParams(sc.dt, 2 * sc.thickness, 1.5, weft.PcgConfig(1e-8, 3000), weft.JAC_SPD, contacts=1,
+                            zones=1)
+    rows, wall = [], []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        try:
+            r = eng.sim_step(params)
+        except weft.Error as e:
+            out["con_error"] = np.array(str(e))
+            wall.append(time.perf_counter() - t0)
+            break
+        wall.append(time.perf_counter() - t0)
+        rows.append([r.proximities, r.contact_elements, r.impacts, r.zone_count, r.pcg_iterations,
+                     r.dcd_candidates, r.ccd_candidates])
+    eng.sim_get_state(xg, vg)
+    out["con_x"], out["con_v"], out["con_counts"] = xg.copy(), vg.copy(), np.array(rows, dtype=np.int64)
+    out["con_wall_s"] = np.array(wall)
     engines.append(eng)
     return out, engines
 

@@ -101,3 +101,16 @@ def test_rank_group_matches_single_process(weft, tmp_path, world, parts):
         assert np.array_equal(res["sim_its"], single["sim_its"])
     assert np.array_equal(sum(r["sim_dcd"] for r in ranks), single["sim_dcd"])
     assert np.array_equal(sum(r["sim_ccd"] for r in ranks), single["sim_ccd"])
+    # whole steps with contacts and impact zones: the merged collide gives
+    # every rank the single-process proximities / impacts, and the contact
+    # columns that cross the cut go through the PCG's peer-memory halo
+    assert single["con_counts"].shape[0] >= 2 and single["con_counts"][:, 1].min() > 50, \
+        (single["con_counts"], str(single.get("con_error")))
+    for res in ranks:
+        if "con_error" in single:
+            assert str(res.get("con_error")) == str(single["con_error"])
+        else:
+            assert "con_error" not in res, str(res["con_error"])
+        assert np.array_equal(res["con_counts"], single["con_counts"])
+        assert np.array_equal(res["con_x"], single["con_x"])
+        assert np.array_equal(res["con_v"], single["con_v"])
