@@ -146,7 +146,7 @@ __device__ __forceinline__ double ld_hint(const double* p, uint64_t pol) {
 // another rank (kRemote, only reached for accumulation groups != 0) are read
 // over peer memory once that rank has published the vectors
 // (vec_ready >= vexp); `seen` caches which ranks were already waited for.
-template <int PMode, bool kRemote>
+template <int PMode, bool kRemote, bool kCg = false>
 __device__ __forceinline__ void gather3(int c, int g, const double* __restrict__ x, const double* __restrict__ pold,
                                         double beta, const CommView& cv, const PartMap& pm, unsigned long long vexp,
                                         unsigned& seen, double& x0, double& x1, double& x2) {
@@ -170,6 +170,17 @@ __device__ __forceinline__ void gather3(int c, int g, const double* __restrict__
       return;
     }
   }
+  if constexpr (kCg) {  // vectors written earlier in the same (persistent) kernel
+    x0 = __ldcg(x + 3 * c);
+    x1 = __ldcg(x + 3 * c + 1);
+    x2 = __ldcg(x + 3 * c + 2);
+    if (PMode == 2) {
+      x0 = x0 + beta * __ldcg(pold + 3 * c);
+      x1 = x1 + beta * __ldcg(pold + 3 * c + 1);
+      x2 = x2 + beta * __ldcg(pold + 3 * c + 2);
+    }
+    return;
+  }
   x0 = x[3 * c];
   x1 = x[3 * c + 1];
   x2 = x[3 * c + 2];
@@ -188,7 +199,7 @@ constexpr int kMgUnroll = WEFT_MG_UNROLL;  // slots per trip of the multi-group 
 // Row product of LOCAL row lr in the reference order.
 // PMode 0: x given. PMode 1: x = z (first PCG iteration, p = z).
 // PMode 2: x = z + beta * p_old on the fly (PCG p update).
-template <int PMode, bool kRemote = false>
+template <int PMode, bool kRemote = false, bool kCg = false>
 __device__ __forceinline__ void row_product(const SellView& A, int lr, int ngroups, const double* __restrict__ x,
                                             const double* __restrict__ pold, double beta, double& y0, double& y1,
                                             double& y2, const CommView& cv = CommView(), const PartMap& pm = PartMap(),
@@ -223,7 +234,7 @@ __device__ __forceinline__ void row_product(const SellView& A, int lr, int ngrou
     const double v3 = __ldg(v + 96), v4 = __ldg(v + 128), v5 = __ldg(v + 160);
     const double v6 = __ldg(v + 192), v7 = __ldg(v + 224), v8 = __ldg(v + 256);
     double x0, x1, x2;
-    gather3<PMode, kRemote>(c, g, x, pold, beta, cv, pm, vexp, seen, x0, x1, x2);
+    gather3<PMode, kRemote, kCg>(c, g, x, pold, beta, cv, pm, vexp, seen, x0, x1, x2);
     a0 = a0 + ((v0 * x0 + v1 * x1) + v2 * x2);
     a1 = a1 + ((v3 * x0 + v4 * x1) + v5 * x2);
     a2 = a2 + ((v6 * x0 + v7 * x1) + v8 * x2);
@@ -1069,6 +1080,253 @@ __global__ void __launch_bounds__(256) k_pcg_update(const PcgArgs* __restrict__ 
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Persistent multi-partition / rank-group PCG: the graph path's two
+// iteration kernels (k_pcg_spmv, k_pcg_update) fused into ONE cooperative
+// kernel per rank. Each CTA walks the same partition-aligned 256-row
+// "virtual blocks" the two kernels use (blockIdx.x, + grid, ...), so every
+// block partial, every per-partition sum and every reduction is bitwise the
+// graph path's; the kernel boundaries become grid syncs and the last-block
+// reductions become redundant per-CTA reductions over the partials. Across
+// ranks: block 0 posts this rank's partition sums into every rank's
+// reduction slots and releases its flag, every CTA waits for all flags and
+// adds the n partitions in ascending order (Engine::all_reduce_sum,
+// exec.cpp:170-174), and block 0 publishes z / p after each update so the
+// peers' next SpMV can gather the halo columns (dynamic contact columns
+// included). Per iteration: 2 grid syncs, 2 flag rounds, no launch.
+// ---------------------------------------------------------------------------
+template <int NV>
+__device__ void partition_sums(const PartBlocks& pb, const double* partials, double (&per)[kMaxParts][NV],
+                               double* smem) {
+  for (int d = 0; d < pb.n; ++d) {
+    double v[NV];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) v[i] = 0.0;
+    for (int b = pb.bstart[d] + threadIdx.x; b < pb.bstart[d + 1]; b += blockDim.x)
+#pragma unroll
+      for (int i = 0; i < NV; ++i) v[i] = v[i] + __ldcg(partials + (size_t)b * NV + i);
+    block_sum<NV>(v, smem);
+#pragma unroll
+    for (int i = 0; i < NV; ++i) per[d][i] = v[i];  // thread 0's value is the sum
+  }
+}
+
+// combine() split over the CTAs of a persistent grid: `post` (block 0,
+// thread 0) stores and releases, every CTA's thread 0 waits and sums. The
+// reduction sequence number s is tracked per CTA (identical everywhere).
+template <int NV>
+__device__ void combine_split(const CommView& cv, int d0, int nloc, int ntot, const double (&v)[kMaxParts][NV],
+                              unsigned long long s, bool post, double (&out)[NV]) {
+#pragma unroll
+  for (int i = 0; i < NV; ++i) out[i] = 0.0;
+  if (cv.world == 1) {
+    for (int d = 0; d < nloc; ++d)
+#pragma unroll
+      for (int i = 0; i < NV; ++i) out[i] = out[i] + v[d][i];
+    return;
+  }
+  const int par = static_cast<int>(s & 1);
+  if (post) {
+    cv.seq[1] = s;
+    for (int q = 0; q < cv.world; ++q)
+      for (int d = 0; d < nloc; ++d)
+#pragma unroll
+        for (int i = 0; i < NV; ++i) cv.hdr[q]->red[par][d0 + d][i] = v[d][i];
+    __threadfence_system();
+    for (int q = 0; q < cv.world; ++q) st_release_sys(&cv.hdr[q]->red_ready[cv.rank], s);
+  }
+  CommHeader* me = cv.hdr[cv.rank];
+  for (int q = 0; q < cv.world; ++q)
+    if (!wait_flag(&me->red_ready[q], s)) atomicExch(cv.seq + 3, 1ull);
+  for (int d = 0; d < ntot; ++d)
+#pragma unroll
+    for (int i = 0; i < NV; ++i) out[i] = out[i] + __ldcg(&me->red[par][d][i]);
+}
+
+template <bool kRemote>
+__global__ void __launch_bounds__(256, 2) k_pcg_persistent_rows(const PcgArgs* __restrict__ args, PcgState* st) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double smem[2 * 32];
+  __shared__ double bc[2];
+  const PcgArgs& g = *args;
+  const SellView A = g.A;
+  const PartBlocks& pb = g.pb;
+  const int nvb = pb.bstart[pb.n];  // virtual blocks (256 rows of one partition)
+  double* __restrict__ x = g.x;
+  double* __restrict__ r = g.r;
+  double* __restrict__ z = g.z;
+  double* __restrict__ p = g.p;
+  double* __restrict__ q = g.q;
+  const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
+  const CommView cv = g.cv;
+  unsigned long long vseq = kRemote ? cv.seq[0] : 0;  // z / p publications seen so far
+  unsigned long long rseq = kRemote ? cv.seq[1] : 0;   // reductions so far (no counters on one rank)
+  double rho = st->rho, beta = st->beta;
+  const double tol = st->tol, b_norm = st->b_norm;
+  const int max_it = st->max_iter;
+  int it = st->iter, status = 0, converged = 0;
+  bool first = st->first != 0;
+  bool done = st->done != 0;
+  double r_norm = st->r_norm;
+  grid.sync();  // every CTA has read the starting sequence numbers
+  while (!done) {
+    // ---- k_pcg_spmv: q = A p with p = z (+ beta p) formed on the fly
+    for (int vb = blockIdx.x; vb < nvb; vb += gridDim.x) {
+      int rend;
+      const int mg = block_row(pb, vb, rend);
+      double s1[1] = {0.0};
+      if (mg < rend) {
+        const int m = mg - A.row0;
+        const int row = A.row0 + A.perm[m];
+        double y0, y1, y2;
+        if (first) row_product<1, kRemote, true>(A, m, g.ngroups, z, p, beta, y0, y1, y2, cv, g.pm, vseq);
+        else row_product<2, kRemote, true>(A, m, g.ngroups, z, p, beta, y0, y1, y2, cv, g.pm, vseq);
+        __stcg(q + 3 * row, y0);
+        __stcg(q + 3 * row + 1, y1);
+        __stcg(q + 3 * row + 2, y2);
+        double p0 = __ldcg(z + 3 * row), p1 = __ldcg(z + 3 * row + 1), p2 = __ldcg(z + 3 * row + 2);
+        if (!first) {
+          p0 = p0 + beta * __ldcg(p + 3 * row);
+          p1 = p1 + beta * __ldcg(p + 3 * row + 1);
+          p2 = p2 + beta * __ldcg(p + 3 * row + 2);
+        }
+        s1[0] = (p0 * y0 + p1 * y1) + p2 * y2;
+      }
+      block_sum<1>(s1, smem);
+      if (threadIdx.x == 0) __stcg(g.partials + vb, s1[0]);
+    }
+    grid.sync();
+    if (kRemote && __ldcg(cv.seq + 3)) break;  // a peer timed out: stop everywhere
+    {
+      double per[kMaxParts][1];
+      partition_sums<1>(pb, g.partials, per, smem);
+      ++rseq;
+      if (threadIdx.x == 0) {
+        double t[1];
+        combine_split<1>(cv, pb.d0, pb.n, g.pm.n, per, rseq, blockIdx.x == 0, t);
+        bc[0] = t[0];
+      }
+      __syncthreads();
+    }
+    const double pq = bc[0];
+    if (!isfinite(pq)) {
+      status = 1;
+      ++it;
+      break;
+    }
+    if (pq <= 0.0) {
+      status = 2;
+      ++it;
+      break;
+    }
+    const double alpha = rho / pq;
+    // ---- k_pcg_update: p, x, r, z of the held rows; r.r and r.z
+    for (int vb = blockIdx.x; vb < nvb; vb += gridDim.x) {
+      int rend;
+      const int i = block_row(pb, vb, rend);
+      double s2[2] = {0.0, 0.0};
+      if (i < rend) {
+        double zv[3], pv[3], xv[3], rv[3], qv[3], m[9];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          zv[c] = __ldcg(z + 3 * i + c);
+          pv[c] = first ? 0.0 : __ldcg(p + 3 * i + c);
+          xv[c] = __ldcg(x + 3 * i + c);
+          rv[c] = __ldcg(r + 3 * i + c);
+          qv[c] = __ldcg(q + 3 * i + c);
+        }
+        if (g.bj) {
+#pragma unroll
+          for (int k = 0; k < 9; ++k) m[k] = __ldg(g.dinv + 9 * (size_t)i + k);
+        }
+        double pr[3], rr[3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          pr[c] = first ? zv[c] : zv[c] + beta * pv[c];
+          xv[c] = xv[c] + alpha * pr[c];
+          rr[c] = rv[c] - alpha * qv[c];
+        }
+        double z0, z1, z2;
+        if (g.bj) {  // apply_precond (solver.hpp:67-89)
+          z0 = ((0.0 + m[0] * rr[0]) + m[1] * rr[1]) + m[2] * rr[2];
+          z1 = ((0.0 + m[3] * rr[0]) + m[4] * rr[1]) + m[5] * rr[2];
+          z2 = ((0.0 + m[6] * rr[0]) + m[7] * rr[1]) + m[8] * rr[2];
+        } else {
+          z0 = rr[0];
+          z1 = rr[1];
+          z2 = rr[2];
+        }
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          __stcg(p + 3 * i + c, pr[c]);
+          __stcg(x + 3 * i + c, xv[c]);
+          __stcg(r + 3 * i + c, rr[c]);
+        }
+        __stcg(z + 3 * i, z0);
+        __stcg(z + 3 * i + 1, z1);
+        __stcg(z + 3 * i + 2, z2);
+        s2[0] = (rr[0] * rr[0] + rr[1] * rr[1]) + rr[2] * rr[2];
+        s2[1] = (rr[0] * z0 + rr[1] * z1) + rr[2] * z2;
+      }
+      block_sum<2>(s2, smem);
+      if (threadIdx.x == 0) {
+        __stcg(g.partials + 2 * vb, s2[0]);
+        __stcg(g.partials + 2 * vb + 1, s2[1]);
+      }
+    }
+    grid.sync();
+    if (kRemote && __ldcg(cv.seq + 3)) break;
+    // z and p of the held rows are final: release them to the peers
+    if (kRemote) {
+      if (lead) publish_vec(cv);
+      ++vseq;
+    }
+    {
+      double per[kMaxParts][2];
+      partition_sums<2>(pb, g.partials, per, smem);
+      ++rseq;
+      if (threadIdx.x == 0) {
+        double t[2];
+        combine_split<2>(cv, pb.d0, pb.n, g.pm.n, per, rseq, blockIdx.x == 0, t);
+        bc[0] = t[0];
+        bc[1] = t[1];
+      }
+      __syncthreads();
+    }
+    ++it;
+    first = false;
+    r_norm = sqrt(bc[0]);
+    if (!isfinite(r_norm)) {
+      status = 3;
+      break;
+    }
+    const double rho_next = bc[1];
+    if (lead) {
+      g.hist[it - 1] = r_norm / b_norm;
+      g.phist[it - 1] = sqrt(rho_next > 0.0 ? rho_next : 0.0);
+    }
+    if (r_norm <= tol) {
+      converged = 1;
+      break;
+    }
+    beta = rho_next / rho;
+    rho = rho_next;
+    if (it >= max_it) break;
+  }
+  if (lead) {
+    st->iter = it;
+    st->status = status;
+    st->converged = converged;
+    st->r_norm = r_norm;
+    st->rho = rho;
+    st->beta = beta;
+    st->first = first ? 1 : 0;
+    st->done = 1;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Persistent PCG (one partition, one rank): the whole solve is ONE cooperative
 // kernel. Each warp owns a fixed set of 32-row slices; an iteration is
@@ -1579,6 +1837,10 @@ PcgResult pcg_solve(Ctx& c, const double* b_dev, const weft_pcg_config& cfg, dou
   // POSITION space (vectors and columns permuted to the SELL-32-sigma order,
   // b gathered in, x scattered out), so every vector access is coalesced.
   const bool persistent = c.go.n == 1 && c.world == 1 && c.use_persistent;
+  // otherwise (several partitions or ranks) one cooperative kernel per rank
+  // too, in row space (WEFT_PCG_ROWS=0: the graph of two kernels per iteration)
+  static const bool rows_off = std::getenv("WEFT_PCG_ROWS") && std::atoi(std::getenv("WEFT_PCG_ROWS")) == 0;
+  const bool prows = !persistent && c.use_persistent && !rows_off;
   // z / p at 32 bytes per row inside the persistent solve (one LDG.256 per
   // gather) while 64 B per row of them fit ~100 MB of L2; beyond (the 5-10 M
   // triangle configs) the 24-byte rows move fewer bytes (E5: 97.5 vs 103.6 ms)
@@ -1769,6 +2031,31 @@ PcgResult pcg_solve(Ctx& c, const double* b_dev, const weft_pcg_config& cfg, dou
           4.0 + 48.0 + 24.0 + 24.0 + (args.dinv6 ? 48.0 : 72.0) + 48.0 + 48.0 + (qs_bytes ? 0.0 : 48.0);
       c.pcg_bytes += hs->iter * (76.0 * static_cast<double>(c.A.nnzb) + per_row * rows);
     }
+  } else if (prows) {
+    // several partitions and/or ranks: the two iteration kernels fused into
+    // one cooperative launch per rank (bitwise the graph path's iterates)
+    auto k = peers ? k_pcg_persistent_rows<true> : k_pcg_persistent_rows<false>;
+    int sms = 0, occ = 0;
+    WG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device));
+    WG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, threads, 0));
+    const int grid = std::max(1, std::min(std::max(1, occ) * sms, nblocks));
+    void* kargs[] = {(void*)&dargs, (void*)&c.pcg};
+    if (c.profile) WG_CUDA(cudaEventRecord(c.ev[6], s));
+    WG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k), dim3(grid), dim3(threads), kargs, 0, s));
+    ++c.launches;
+    if (c.profile) WG_CUDA(cudaEventRecord(c.ev[7], s));
+    WG_CUDA(cudaMemcpyAsync(hs, c.pcg, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
+    WG_CUDA(cudaStreamSynchronize(s));
+    if (c.profile) {
+      float ms = 0.f;
+      WG_CUDA(cudaEventElapsedTime(&ms, c.ev[6], c.ev[7]));
+      c.pcg_ms += ms;
+      c.pcg_iterations += hs->iter;
+      ++c.pcg_solves;
+      // SpMV 76 B per streamed block + 4 length + 48 gathered z, p + 24 q
+      // written per row; update 288 B per row
+      c.pcg_bytes += hs->iter * (76.0 * static_cast<double>(c.A.nnzb) + (76.0 + 288.0) * rows);
+    }
   } else if (!c.profile && c.use_graphs) {
     // The whole solve is one graph launch: a conditional WHILE node whose
     // body is the two iteration kernels; the update kernel's last block
@@ -1832,7 +2119,7 @@ PcgResult pcg_solve(Ctx& c, const double* b_dev, const weft_pcg_config& cfg, dou
       c.launches += 2 * std::max(hs->iter, 1);
     }
   }
-  if (!persistent && (c.profile || !c.use_graphs)) {
+  if (!persistent && !prows && (c.profile || !c.use_graphs)) {
     int chunk = 4;
     int iter_before = 0;
     for (;;) {

@@ -126,3 +126,39 @@ def test_pcg_bitwise_deterministic(weft):
         x1, _ = eng.pcg_solve(csr(weft, s), b)
         x2, _ = eng.pcg_solve(None, b)
     assert np.array_equal(x1, x2)
+
+
+_SOLVE_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1]); sys.path.insert(0, sys.argv[1] + "/tests")
+from gen import random_spd
+from paper_2008_00409_b200 import weft
+rng = np.random.default_rng(31)
+s = random_spd(rng, 300)
+b = rng.uniform(-1, 1, 3 * s.rows)
+out = {}
+for n in (2, 4, 8):
+    with weft.Engine(n) as eng:
+        x, rep = eng.pcg_solve(weft.BlockCsr(s.rows, s.row_ptr, s.cols, s.vals), b, weft.PcgConfig(1e-10, 2000))
+    out[f"x{n}"], out[f"it{n}"], out[f"h{n}"] = x, np.array(rep.iterations), rep.residual_history
+np.savez(sys.argv[2], **out)
+"""
+
+
+def test_pcg_persistent_rows_equals_graph(weft, tmp_path):
+    """The multi-partition solve as one cooperative kernel per rank
+    (k_pcg_persistent_rows) walks the graph path's virtual blocks: iterates,
+    residual histories and solutions are bitwise the two-kernel graph's
+    (WEFT_PCG_ROWS=0)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for flag in ("0", "1"):
+        out = tmp_path / f"rows{flag}.npz"
+        subprocess.run([sys.executable, "-c", _SOLVE_SCRIPT, root, str(out)], check=True,
+                       env=dict(os.environ, WEFT_PCG_ROWS=flag), timeout=300)
+        res[flag] = dict(np.load(out))
+    for k in res["0"]:
+        assert np.array_equal(res["0"][k], res["1"][k]), k

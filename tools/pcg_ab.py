@@ -1,6 +1,7 @@
 """A/B timing of library variants (WEFT_LIB=...): config D, the bench's
 replayed state (2 steps from rest), median device time of the PCG stage over
 8 replayed steps. Prints one line per run."""
+import hashlib
 import os
 import statistics
 import sys
@@ -35,5 +36,8 @@ for k in range(9):
         broad.append(r.ms_broad)
         its.append(r.pcg_iterations)
 ms = statistics.median(solve)
-print(f"{os.environ.get('WEFT_LIB', 'default')} parts={os.environ.get('PARTS', '1')} persistent={os.environ.get('WEFT_PCG_PERSISTENT', '1')}: solve {ms:.3f} ms ({1e3 * ms / its[-1]:.1f} us/it, {its[-1]} its) "
-      f"asm {statistics.median(asm):.3f} broad {statistics.median(broad):.3f}", flush=True)
+xo, vo = np.zeros(3 * p), np.zeros(3 * p)
+eng.sim_get_state(xo, vo)
+digest = hashlib.sha1(xo.tobytes() + vo.tobytes()).hexdigest()[:12]
+print(f"{os.environ.get('WEFT_LIB', 'default')} parts={os.environ.get('PARTS', '1')} persistent={os.environ.get('WEFT_PCG_PERSISTENT', '1')} rows={os.environ.get('WEFT_PCG_ROWS', '1')}: solve {ms:.3f} ms ({1e3 * ms / its[-1]:.1f} us/it, {its[-1]} its) "
+      f"asm {statistics.median(asm):.3f} broad {statistics.median(broad):.3f} state {digest}", flush=True)
