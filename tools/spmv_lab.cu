@@ -224,6 +224,94 @@ __global__ void __launch_bounds__(W * 32, B) k2(Sell A, const double* __restrict
   }
 }
 
+
+// ---------------------------------------------------------------- K3: gather layouts of the PCG SpMV
+// q = A (z + beta p) in position order with the persistent kernel's L2
+// priorities (matrix evict_first, vectors evict_last) and 256-bit gathers:
+//   M = 0  one vector z (32 B rows)                      — the 1-gather floor
+//   M = 1  z and p in two arrays (32 B rows each)        — the product today
+//   M = 2  z and p interleaved in one 64 B record per row
+// p_new of the own row is stored like the product does.
+__device__ __forceinline__ uint64_t pol_ef() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t pol_el() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ double ldm(const double* p, uint64_t pol) {
+  double v;
+  asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ int ldm(const int* p, uint64_t pol) {
+  int v;
+  asm volatile("ld.global.nc.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void ldv4(const double* p, uint64_t pol, double& a, double& b, double& c) {
+  double d;
+  asm volatile("ld.global.cg.L2::cache_hint.v4.f64 {%0,%1,%2,%3}, [%4], %5;"
+               : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p), "l"(pol));
+  (void)d;
+}
+__device__ __forceinline__ void stv4(double* p, double a, double b, double c) {
+  asm volatile("st.global.cg.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(0.0) : "memory");
+}
+template <int M>
+__global__ void __launch_bounds__(256) k3(Sell A, const int32_t* __restrict__ colp, const double* __restrict__ z,
+                                          const double* __restrict__ pv, double beta, double* __restrict__ q,
+                                          double* __restrict__ pnew) {
+  const int m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= A.rows) return;
+  const uint64_t ef = pol_ef(), el = pol_el();
+  const int len = A.len[m];
+  const int64_t base = A.soff[m >> 5] + (m & 31);
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+  for (int k = 0; k < len; ++k) {
+    const int64_t at = base + (int64_t)k * 32;
+    const int c = ldm(colp + at, ef);
+    const double* v = A.vals + vidx(at, m & 31, 0);
+    const double v0 = ldm(v, ef), v1 = ldm(v + 32, ef), v2 = ldm(v + 64, ef);
+    const double v3 = ldm(v + 96, ef), v4 = ldm(v + 128, ef), v5 = ldm(v + 160, ef);
+    const double v6 = ldm(v + 192, ef), v7 = ldm(v + 224, ef), v8 = ldm(v + 256, ef);
+    double x0, x1, x2;
+    if constexpr (M == 0) {
+      ldv4(z + 4 * (size_t)c, el, x0, x1, x2);
+    } else if constexpr (M == 1) {
+      double p0, p1, p2;
+      ldv4(z + 4 * (size_t)c, el, x0, x1, x2);
+      ldv4(pv + 4 * (size_t)c, el, p0, p1, p2);
+      x0 = x0 + beta * p0, x1 = x1 + beta * p1, x2 = x2 + beta * p2;
+    } else {
+      double p0, p1, p2;
+      ldv4(z + 8 * (size_t)c, el, x0, x1, x2);
+      ldv4(z + 8 * (size_t)c + 4, el, p0, p1, p2);
+      x0 = x0 + beta * p0, x1 = x1 + beta * p1, x2 = x2 + beta * p2;
+    }
+    a0 = a0 + ((v0 * x0 + v1 * x1) + v2 * x2);
+    a1 = a1 + ((v3 * x0 + v4 * x1) + v5 * x2);
+    a2 = a2 + ((v6 * x0 + v7 * x1) + v8 * x2);
+  }
+  __stcg(q + 3 * m, a0);
+  __stcg(q + 3 * m + 1, a1);
+  __stcg(q + 3 * m + 2, a2);
+  if constexpr (M == 1) {
+    double z0, z1, z2, p0, p1, p2;
+    ldv4(z + 4 * (size_t)m, el, z0, z1, z2);
+    ldv4(pv + 4 * (size_t)m, el, p0, p1, p2);
+    stv4(pnew + 4 * (size_t)m, z0 + beta * p0, z1 + beta * p1, z2 + beta * p2);
+  } else if constexpr (M == 2) {
+    double z0, z1, z2, p0, p1, p2;
+    ldv4(z + 8 * (size_t)m, el, z0, z1, z2);
+    ldv4(z + 8 * (size_t)m + 4, el, p0, p1, p2);
+    stv4(pnew + 8 * (size_t)m + 4, z0 + beta * p0, z1 + beta * p1, z2 + beta * p2);
+  }
+}
+
 #define CK(x)                                                                    \
   do {                                                                           \
     cudaError_t e = (x);                                                         \
@@ -368,6 +456,32 @@ extern "C" int lab_run(int rows, const int64_t* row_ptr, const int32_t* cols, co
     cudaFree(d_p);
     cudaFree(d_part);
     cudaFree(d_cnt);
+  }
+  {  // K3: gather layouts (sorted layout only: columns as positions)
+    std::vector<int32_t> pos(rows);
+    for (int m = 0; m < rows; ++m) pos[perm[m]] = m;
+    std::vector<int32_t> hcp(total);
+    for (int64_t i = 0; i < total; ++i) hcp[i] = pos[hc[i]];
+    int32_t* d_colp;
+    double *d_z, *d_p, *d_q, *d_pn;
+    CK(cudaMalloc(&d_colp, 4 * total));
+    CK(cudaMemcpy(d_colp, hcp.data(), 4 * total, cudaMemcpyHostToDevice));
+    CK(cudaMalloc(&d_z, 64 * (size_t)rows));
+    CK(cudaMalloc(&d_p, 64 * (size_t)rows));
+    CK(cudaMalloc(&d_q, 24 * (size_t)rows));
+    CK(cudaMalloc(&d_pn, 64 * (size_t)rows));
+    CK(cudaMemset(d_z, 0, 64 * (size_t)rows));
+    CK(cudaMemset(d_p, 0, 64 * (size_t)rows));
+    const int nb = (rows + 255) / 256;
+    times[9] = time_it([&] { k3<0><<<nb, 256>>>(A, d_colp, d_z, d_p, 0.5, d_q, d_pn); }, 50);
+    times[10] = time_it([&] { k3<1><<<nb, 256>>>(A, d_colp, d_z, d_p, 0.5, d_q, d_pn); }, 50);
+    times[11] = time_it([&] { k3<2><<<nb, 256>>>(A, d_colp, d_z, d_p, 0.5, d_q, d_pn); }, 50);
+    CK(cudaGetLastError());
+    cudaFree(d_colp);
+    cudaFree(d_z);
+    cudaFree(d_p);
+    cudaFree(d_q);
+    cudaFree(d_pn);
   }
   cudaFree(d_soff);
   cudaFree(d_len);

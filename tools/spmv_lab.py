@@ -53,3 +53,6 @@ for sorted_ in (0, 1):
     print(f"   pcg-form: 2-vector gather {t[5]*1e3:.1f} us {alg2/t[5]/1e6:.0f} GB/s | +dot {t[6]*1e3:.1f} us "
           f"{alg2/t[6]/1e6:.0f} GB/s | +dot after L2 flush {(t[7]-t[8])*1e3:.1f} us {alg2/(t[7]-t[8])/1e6:.0f} GB/s "
           f"(flush {t[8]*1e3:.1f} us)", flush=True)
+    if sorted_:
+        print(f"   gather layouts (L2 hints, 256-bit): z only {t[9]*1e3:.1f} us | z, p two arrays {t[10]*1e3:.1f} us | "
+              f"z|p 64-byte records {t[11]*1e3:.1f} us", flush=True)
