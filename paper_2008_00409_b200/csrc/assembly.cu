@@ -739,7 +739,7 @@ __global__ void k_zero_padding(int p, const int64_t* __restrict__ soff, const in
 // incidence of the row in ascending element order that couples to this
 // column adds (-scale) J_ab (+ dt D_ab) into register accumulators
 // (assembly.hpp:199-215) — no atomics, no shared-memory accumulators, full
-// occupancy. Phase 2b sums each row's rhs contributions in the same order.
+// occupancy; the same kernel sums each row's rhs contributions in that order.
 
 // stretch block (i, j) from the stored x_cur state (elements.cpp:209-228,
 // keep_s2 = false in SpdProjected mode).
@@ -1297,31 +1297,42 @@ __global__ void __launch_bounds__(kSlotWarps * 32, WEFT_SLOT_MINB) k_fill_slots(
 #pragma unroll
     for (int q = 0; q < 9; ++q) g.vals[vidx(at, lane, q)] = acc[q];
   }
-}
-
-// Phase 2b: rhs per row, contributions in ascending element order.
-__global__ void __launch_bounds__(256) k_fill_rhs(SlotArgs g) {
-  const int lr = blockIdx.x * blockDim.x + threadIdx.x;
-  if (lr >= g.p) return;
-  const int r = g.row0 + lr;
-  if (!g.pinned[r] && g.mass[r] <= 0.0) atomicMin(g.bad_mass, r);
-  double r0 = 0.0, r1 = 0.0, r2 = 0.0;
-  for (int pass = 0; pass < 2; ++pass) {
-    const int64_t* ip = pass == 0 ? g.inc_ptr : g.cinc_ptr;
-    const int32_t* il = pass == 0 ? g.inc : g.cinc;
-    const int64_t i1 = ip[r + 1];
-    for (int64_t ii = ip[r]; ii < i1; ++ii) {
-      const int code = il[ii];
-      const int64_t e = (pass == 0 ? 0 : g.n_static) + (code >> 2);
-      const double* R = g.eres + g.eres_off[e] + 3 * (code & 3);
-      r0 = r0 + R[0];
-      r1 = r1 + R[1];
-      r2 = r2 + R[2];
+  // rhs of the lane's row (assembly.hpp:182-197): the phase-1 contributions
+  // dt f_a of its incidences in ascending element order. Each sits right
+  // before the element state the slot loop above just read, so it comes out
+  // of L2 (a separate row pass re-read them from DRAM: 1.9 GB per step at D).
+  // Done by the last warp, which has the fewest slots.
+  if (warp == kSlotWarps - 1) {
+    if (!g.pinned[r] && g.mass[r] <= 0.0) atomicMin(g.bad_mass, r);
+    double r0 = 0.0, r1 = 0.0, r2 = 0.0;
+    for (int pass = 0; pass < 2; ++pass) {
+      if (staged) {
+        const int i1 = sm_row[pass][lane + 1];
+        for (int i = sm_row[pass][lane]; i < i1; ++i) {
+          const int ksa = sm_ksa[i];
+          const double* R = g.eres + sm_res[i] - 3 * ((ksa >> 8) & 0xff) + 3 * ((ksa >> 16) & 0xff);
+          r0 = r0 + R[0];
+          r1 = r1 + R[1];
+          r2 = r2 + R[2];
+        }
+      } else {
+        const int64_t* ip = pass == 0 ? g.inc_ptr : g.cinc_ptr;
+        const int32_t* il = pass == 0 ? g.inc : g.cinc;
+        const int64_t i1 = ip[r + 1];
+        for (int64_t ii = ip[r]; ii < i1; ++ii) {
+          const int code = il[ii];
+          const int64_t e = (pass == 0 ? 0 : g.n_static) + (code >> 2);
+          const double* R = g.eres + g.eres_off[e] + 3 * (code & 3);
+          r0 = r0 + R[0];
+          r1 = r1 + R[1];
+          r2 = r2 + R[2];
+        }
+      }
     }
+    g.rhs[3 * r] = r0;
+    g.rhs[3 * r + 1] = r1;
+    g.rhs[3 * r + 2] = r2;
   }
-  g.rhs[3 * r] = r0;
-  g.rhs[3 * r + 1] = r1;
-  g.rhs[3 * r + 2] = r2;
 }
 
 constexpr int kFillThreads = 64;
@@ -1455,7 +1466,6 @@ void fill_matrix(Ctx& c, const double* xc, const double* xa, const double* vel, 
                 c.eres.data(), c.rhs.data(), bad};
     if (c.n_contacts > 0) k_fill_slots<kStageCapContacts><<<A.nslices, kSlotWarps * 32, 0, ls(c)>>>(sa);
     else k_fill_slots<kStageCap><<<A.nslices, kSlotWarps * 32, 0, ls(c)>>>(sa);
-    k_fill_rhs<<<div_up(nloc, 256), 256, 0, ls(c)>>>(sa);
     WG_CUDA(cudaGetLastError());
   } else if (nloc) {
     if (!layout_cached)

@@ -119,6 +119,7 @@ __device__ __forceinline__ ParityMap compose(ParityMap f, ParityMap g) {  // f, 
 constexpr int kSumThreads = 1024;
 constexpr int kSumItems = 16;
 constexpr int kSumChunk = kSumThreads * kSumItems;
+constexpr int kSerialHead = 2048;
 constexpr long long kTwo53 = 1LL << 53;
 
 // Parity map of one term d in the binade with 1/u = inv_u.
@@ -148,7 +149,30 @@ __device__ void sum_range(const double* __restrict__ diag, int k, const int kend
                           ParityMap* sm_warp, int* sm_event, long long* sm_M) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   while (k < kend) {
-    if (s == 0.0 || !(s >= 0x1p-1000) || !isfinite(s)) {
+    if (s == 0.0) {
+      // the start: the running sum crosses a binade every time the term
+      // count doubles, so the first kSerialHead terms are added serially by
+      // one thread (a window pass per crossing would cost far more)
+      const int n = min(kSerialHead, kend - k);
+      if (tid == 0) {
+        double t = 0.0;
+        for (int i = 0; i < n; i += 8) {
+          double v[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) v[u] = i + u < n ? __ldcg(diag + k + i + u) : 0.0;
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if (i + u < n) t = t + v[u];
+        }
+        sm_d[0] = t;
+      }
+      __syncthreads();
+      s = sm_d[0];
+      __syncthreads();
+      k += n;
+      continue;
+    }
+    if (!(s >= 0x1p-1000) || !isfinite(s)) {
       // start, tiny or non-finite running sums: plain serial adds
       s = s + diag[k];
       ++k;
@@ -243,58 +267,110 @@ __device__ void sum_range(const double* __restrict__ diag, int k, const int kend
   }
 }
 
-// Fast path, pass 1: approximate chunk sums (any order; only used to
-// predict the binade the exact running sum will be in at each chunk).
-__global__ void __launch_bounds__(256) k_chunk_approx(int n, const double* __restrict__ d, double* __restrict__ approx) {
-  __shared__ double sm[8];
-  const int c = blockIdx.x;
-  const int k0 = c * kSumChunk, k1 = min(n, k0 + kSumChunk);
-  double v = 0.0;
-  for (int i = k0 + threadIdx.x; i < k1; i += blockDim.x) v += d[i];
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = v;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double t = 0.0;
-    for (int w = 0; w < 8; ++w) t += sm[w];
-    approx[c] = t;
+// Fast path. The running sum crosses a binade ~log2(sum / first term)
+// times (config D: 21 times over 1.65 M terms); only those places need the
+// exact scan, everything else is a composed parity map per segment.
+//  1. an approximate prefix of the terms (any order) predicts where the
+//     exact running sum crosses each power of two;
+//  2. the terms are cut into segments: up to kSumChunk terms in one
+//     predicted binade, and a serial segment of 2 * kCrossPad terms around
+//     every predicted crossing (overlapping ones merged: the dense early
+//     crossings become one serial head);
+//  3. one CTA per segment composes its parity map in the predicted binade;
+//  4. one CTA applies the segments in order: map segments in O(1) when the
+//     exact sum is in the predicted binade and stays there, serial segments
+//     by one thread, and anything mispredicted by the exact window scan
+//     (sum_range) — so the result is exact whatever the prediction did.
+constexpr int kCrossPad = 32;
+constexpr int kMaxCross = 256;
+
+struct SumSeg {
+  int k0, k1;
+  int serial;   // 1: added term by term by one thread
+  int e;        // predicted binade of the running sum at k0 (map segments)
+  long long a0, a1;
+  int ok;       // map usable
+  int pad;
+};
+
+// Predicted crossings: term i where the approximate prefix enters a new binade.
+__global__ void k_cross_find(int n, const double* __restrict__ pre, int* __restrict__ xs, int* __restrict__ nx) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < 1 || i >= n) return;
+  const double a = pre[i - 1], b = pre[i];
+  if (a > 0.0 && isfinite(b) && ilogb(a) != ilogb(b)) {
+    const int k = atomicAdd(nx, 1);
+    if (k < kMaxCross) xs[k] = i;
   }
 }
 
-struct ChunkMap {
-  long long a0, a1;
-  int e;
-  int ok;
-};
+// Segment list (one thread; a few hundred entries).
+__global__ void k_seg_build(int n, const int* __restrict__ xs_in,
+                            const int* __restrict__ nx_in, SumSeg* __restrict__ seg, int* __restrict__ nseg) {
+  __shared__ int xs[kMaxCross], raw[kMaxCross];
+  const int nx = min(*nx_in, kMaxCross);
+  for (int i = threadIdx.x; i < nx; i += blockDim.x) raw[i] = xs_in[i];
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  for (int i = 0; i < nx; ++i) {  // insertion sort (atomic order is arbitrary)
+    const int v = raw[i];
+    int j = i;
+    while (j > 0 && xs[j - 1] > v) {
+      xs[j] = xs[j - 1];
+      --j;
+    }
+    xs[j] = v;
+  }
+  int k = 0, xi = 0, ns = 0;
+  while (k < n) {
+    while (xi < nx && xs[xi] + kCrossPad <= k) ++xi;
+    SumSeg sg{};
+    sg.k0 = k;
+    if (k == 0 || (xi < nx && xs[xi] - kCrossPad <= k)) {
+      // serial: the first term (the sum starts at 0) and the crossings near k
+      int e = k == 0 ? 1 : k;
+      while (xi < nx && xs[xi] - kCrossPad <= e) {
+        e = max(e, xs[xi] + kCrossPad);
+        ++xi;
+      }
+      sg.k1 = min(n, e);
+      sg.serial = 1;
+    } else {
+      int r = min(n, k + kSumChunk);
+      if (xi < nx) r = min(r, xs[xi] - kCrossPad);
+      sg.k1 = r;  // binade and map: k_seg_maps
+    }
+    seg[ns++] = sg;
+    k = sg.k1;
+  }
+  *nseg = ns;
+}
 
-// Fast path, pass 2: each chunk's composed parity map in the binade
-// predicted from the approximate prefix.
-__global__ void __launch_bounds__(kSumThreads) k_chunk_maps(int n, const double* __restrict__ d,
-                                                            const double* __restrict__ approx,
-                                                            ChunkMap* __restrict__ maps) {
-  __shared__ double sm_r[32];
+// Parity map of each map segment in its predicted binade.
+__global__ void __launch_bounds__(kSumThreads) k_seg_maps(const double* __restrict__ d, const double* __restrict__ pre,
+                                                          SumSeg* __restrict__ seg, const int* __restrict__ nseg) {
   __shared__ ParityMap sm_w[32];
   __shared__ int sm_huge;
   const int c = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  double pre = 0.0;
-  for (int i = tid; i < c; i += kSumThreads) pre += approx[i];
-  for (int o = 16; o > 0; o >>= 1) pre += __shfl_xor_sync(0xffffffffu, pre, o);
-  if (lane == 0) sm_r[warp] = pre;
+  if (c >= *nseg) return;
+  SumSeg sg = seg[c];
+  if (sg.serial) return;
+  const double a = pre[sg.k0 - 1];  // predicted running sum before the segment
+  if (!(a > 0x1p-1000 && isfinite(a))) {
+    if (tid == 0) seg[c].ok = 0;
+    return;
+  }
+  sg.e = ilogb(a);
   if (tid == 0) sm_huge = 0;
   __syncthreads();
-  double start = 0.0;
-  for (int w = 0; w < 32; ++w) start += sm_r[w];
-  const bool usable = start > 0x1p-1000 && isfinite(start);
-  const int e = usable ? ilogb(start) : 0;
-  const double inv_u = ldexp(1.0, 52 - e);
-  const int k0 = c * kSumChunk;
-  const int len = min(kSumChunk, n - k0);
+  const double inv_u = ldexp(1.0, 52 - sg.e);
+  const int len = sg.k1 - sg.k0;
   ParityMap acc{0, 0};
   bool huge = false;
 #pragma unroll
   for (int i = 0; i < kSumItems; ++i) {
     const int j = tid * kSumItems + i;
-    if (j < len && usable) acc = compose(acc, term_map(__ldg(d + k0 + j), inv_u, huge));
+    if (j < len) acc = compose(acc, term_map(__ldg(d + sg.k0 + j), inv_u, huge));
   }
   if (huge) sm_huge = 1;
   // ordered reduction: lanes, then warps
@@ -310,37 +386,63 @@ __global__ void __launch_bounds__(kSumThreads) k_chunk_maps(int n, const double*
   if (tid == 0) {
     ParityMap t{0, 0};
     for (int w = 0; w < 32; ++w) t = compose(t, sm_w[w]);
-    maps[c] = ChunkMap{t.a0, t.a1, e, (usable && !sm_huge) ? 1 : 0};
+    seg[c].a0 = t.a0;
+    seg[c].a1 = t.a1;
+    seg[c].e = sg.e;
+    seg[c].ok = sm_huge ? 0 : 1;
   }
 }
 
-// cell = max(cell_scale * mean, 1e-9): combine chunk maps in order with the
-// exact running sum; a chunk whose binade was mispredicted or that leaves
-// its binade is summed by the exact window scan instead.
+// cell = max(cell_scale * mean, 1e-9) over the segments, in order.
 __global__ void __launch_bounds__(kSumThreads) k_cell_size(int ntris, const double* __restrict__ diag,
-                                                           const ChunkMap* __restrict__ maps, int nchunks,
+                                                           const SumSeg* __restrict__ seg, const int* __restrict__ nsegp,
                                                            double cell_scale, double* __restrict__ out) {
   extern __shared__ double sm_d[];
   __shared__ ParityMap sm_warp[32];
   __shared__ int sm_event;
   __shared__ long long sm_M;
+  constexpr int kSegBatch = 256;  // segments staged per batch
+  __shared__ SumSeg sm_seg[kSegBatch];
   double s = 0.0;
-  for (int c = 0; c < nchunks; ++c) {
-    const int k0 = c * kSumChunk, k1 = min(ntris, k0 + kSumChunk);
-    bool fast = false;
-    if (maps) {
-      const ChunkMap cm = maps[c];
-      if (cm.ok && s >= 0x1p-1000 && isfinite(s) && ilogb(s) == cm.e) {
-        const double inv_u = ldexp(1.0, 52 - cm.e);
+  if (seg) {
+    const int nseg = *nsegp;
+    for (int c = 0; c < nseg; ++c) {
+      if (c % kSegBatch == 0) {
+        __syncthreads();
+        for (int i = threadIdx.x; i < kSegBatch && c + i < nseg; i += blockDim.x) sm_seg[i] = seg[c + i];
+        __syncthreads();
+      }
+      const SumSeg sg = sm_seg[c % kSegBatch];
+      if (sg.serial) {  // staged by all threads, added in order by one
+        for (int b = sg.k0; b < sg.k1; b += kSumChunk) {
+          const int len = min(kSumChunk, sg.k1 - b);
+          for (int i = threadIdx.x; i < len; i += blockDim.x) sm_d[i] = __ldcg(diag + b + i);
+          __syncthreads();
+          if (threadIdx.x == 0) {
+            double t = s;
+            for (int i = 0; i < len; ++i) t = t + sm_d[i];
+            sm_M = __double_as_longlong(t);
+          }
+          __syncthreads();
+          s = __longlong_as_double(sm_M);
+          __syncthreads();
+        }
+        continue;
+      }
+      bool fast = false;
+      if (sg.ok && s >= 0x1p-1000 && isfinite(s) && ilogb(s) == sg.e) {
+        const double inv_u = ldexp(1.0, 52 - sg.e);
         const long long ms = static_cast<long long>(s * inv_u);
-        const long long M = ms + ((ms & 1) ? cm.a1 : cm.a0);
+        const long long M = ms + ((ms & 1) ? sg.a1 : sg.a0);
         if (M < kTwo53) {
-          s = ldexp(static_cast<double>(M), cm.e - 52);
+          s = ldexp(static_cast<double>(M), sg.e - 52);
           fast = true;
         }
       }
+      if (!fast) sum_range(diag, sg.k0, sg.k1, s, sm_d, sm_warp, &sm_event, &sm_M);
     }
-    if (!fast) sum_range(diag, k0, k1, s, sm_d, sm_warp, &sm_event, &sm_M);
+  } else {
+    sum_range(diag, 0, ntris, s, sm_d, sm_warp, &sm_event, &sm_M);
   }
   if (threadIdx.x == 0) {
     const double mean = ntris > 0 ? s / ntris : 1.0;
@@ -359,17 +461,27 @@ __global__ void k_serial_sum_naive(int n, const double* __restrict__ d, double* 
 constexpr size_t kSumSmem = sizeof(double) * kSumThreads * kSumItems;
 
 static void launch_cell_size(Ctx& c, int n, const double* d, double scale, double* out, bool fast = true) {
-  const int nch = div_up(n, kSumChunk);
-  ChunkMap* maps = nullptr;
-  if (fast && nch > 0) {
-    c.sum_approx.resize(static_cast<size_t>(nch));
-    c.sum_maps.resize(static_cast<size_t>(nch) * sizeof(ChunkMap));
-    maps = reinterpret_cast<ChunkMap*>(c.sum_maps.data());
-    k_chunk_approx<<<nch, 256, 0, ls(c)>>>(n, d, c.sum_approx.data());
-    k_chunk_maps<<<nch, kSumThreads, 0, ls(c)>>>(n, d, c.sum_approx.data(), maps);
+  SumSeg* seg = nullptr;
+  int* nseg = nullptr;
+  if (fast && n > 0) {
+    const int max_seg = div_up(n, kSumChunk) + 2 * kMaxCross + 2;
+    c.sum_approx.resize(static_cast<size_t>(n));
+    c.sum_maps.resize(static_cast<size_t>(max_seg) * sizeof(SumSeg) + (kMaxCross + 4) * sizeof(int));
+    seg = reinterpret_cast<SumSeg*>(c.sum_maps.data());
+    int* xs = reinterpret_cast<int*>(c.sum_maps.data() + static_cast<size_t>(max_seg) * sizeof(SumSeg));
+    int* nx = xs + kMaxCross;
+    nseg = nx + 1;
+    size_t tmp = 0;
+    cub::DeviceScan::InclusiveSum(nullptr, tmp, d, c.sum_approx.data(), n, c.cur);
+    void* t = scratch(c, tmp);
+    WG_CUDA(cub::DeviceScan::InclusiveSum(t, tmp, d, c.sum_approx.data(), n, c.cur));
+    WG_CUDA(cudaMemsetAsync(nx, 0, sizeof(int), c.cur));
+    k_cross_find<<<div_up(n, 256), 256, 0, ls(c)>>>(n, c.sum_approx.data(), xs, nx);
+    k_seg_build<<<1, 32, 0, ls(c)>>>(n, xs, nx, seg, nseg);
+    k_seg_maps<<<max_seg, kSumThreads, 0, ls(c)>>>(d, c.sum_approx.data(), seg, nseg);
   }
   WG_CUDA(cudaFuncSetAttribute(k_cell_size, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSumSmem));
-  k_cell_size<<<1, kSumThreads, kSumSmem, ls(c)>>>(n, d, maps, nch, scale, out);
+  k_cell_size<<<1, kSumThreads, kSumSmem, ls(c)>>>(n, d, seg, nseg, scale, out);
 }
 
 
