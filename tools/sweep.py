@@ -1,9 +1,12 @@
 """Size sweep on one GPU (BASELINE.json configs[4]: 0.5M-10M triangles): for
-each config, the bench's replayed hot-path step (DCD + count, assembly,
-PCG, CCD + count) timed with CUDA events, the persistent PCG kernel's HBM
-roofline, and the narrow-phase DCD time. Writes one JSON line per config.
+each config, the bench's hot-path step (DCD + count, assembly, PCG, CCD +
+count) along the trajectory from rest (3 warm-up steps, then 6 timed with
+CUDA events), the persistent PCG kernel's HBM roofline, the narrow-phase
+DCD time, and the compiled reference's CPU step on the same trajectory
+(oracle/_ref, Engine(largest power of two <= host cores); 1 warm-up step,
+up to 2 timed within a wall budget). One JSON line per config.
 
-    python tools/sweep.py [A E05 B ...] > profiles/r01_sweep_1gpu.jsonl
+    python tools/sweep.py [A E05 B ...] > profiles/r02_sweep_1gpu.jsonl
 """
 import json
 import os
@@ -34,30 +37,23 @@ def run(cfg: str, steps: int = 6, warmup: int = 3):
     x0 = sc.verts.reshape(-1).copy()
     eng.sim_set_state(x0, np.zeros_like(x0))
     prm = weft.SimParams(sc.dt, sc.thickness, 1.5, weft.PcgConfig(1e-4, 400), weft.JAC_SPD)
-    for _ in range(2):
-        eng.sim_step(prm)
-    xs = torch.empty(3 * p, dtype=torch.float64, device="cuda")
-    vs = torch.empty(3 * p, dtype=torch.float64, device="cuda")
-    eng.sim_get_state(xs, vs)
     stream = torch.cuda.ExternalStream(eng.stream())
-
-    def replay():
-        eng.sim_set_state(xs, vs)
-        return eng.sim_step(prm)
-
     for _ in range(warmup):
-        replay()
+        eng.sim_step(prm)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    reps = [replay() for _ in range(steps)]
+    reps = [eng.sim_step(prm) for _ in range(steps)]
     e1.record(stream)
     e1.synchronize()
     ms = e0.elapsed_time(e1) / steps
     eng.profile(True)
-    replay()
+    eng.sim_step(prm)
     st = eng.stats()
     eng.profile(False)
+    xs = torch.empty(3 * p, dtype=torch.float64, device="cuda")
+    vs = torch.empty(3 * p, dtype=torch.float64, device="cuda")
+    eng.sim_get_state(xs, vs)
     info = eng.matrix_info()
     pcg_gbs = st.pcg_bytes / (st.pcg_ms * 1e-3) / 1e9 if st.pcg_solves else None
     eng.set_soup_movable(1 - sc.pinned)
@@ -79,8 +75,20 @@ def run(cfg: str, steps: int = 6, warmup: int = 3):
         "gpu_mem_gb": torch.cuda.mem_get_info()[1] / 1e9 - torch.cuda.mem_get_info()[0] / 1e9,
     }
     eng.close()
+    if REF_BUDGET > 0:
+        from bench import run_reference_steps
+        sec, n, rinfo = run_reference_steps(sc, 2, 1, REF_BUDGET)
+        if sec:
+            out["cpu_reference"] = {"steps_per_s": 1.0 / sec, "timed_steps": n, "threads": 2 * rinfo["devices"],
+                                    "engine_devices": rinfo["devices"], "cpu_model": rinfo["cpu_model"],
+                                    "pcg_iterations": rinfo["pcg_iterations"]}
+            out["gpu_over_cpu_reference"] = (1e3 / ms) * sec
+        else:
+            out["cpu_reference"] = rinfo
     return out
 
+
+REF_BUDGET = float(os.environ.get("SWEEP_REF_BUDGET_S", "150"))
 
 if __name__ == "__main__":
     cfgs = sys.argv[1:] or ["A", "E05", "B", "C", "D", "E3", "E5", "E10"]
