@@ -270,6 +270,69 @@ def zone_case(seed: int = 7):
     return sc, x0, x1, mv, mass
 
 
+def body_proxy_bench(weft, stream, steps: int = 12):
+    """BASELINE.json configs[2] as written: the Kimono-scale layered cloth
+    (config C, 2 x 501^2, 1 M triangles) on a body proxy — a uv-sphere
+    obstacle (mesh.cpp:214-237) pressed into the hanging layers at 0.5 m/s —
+    through the whole Simulator::step_impl on the device (contacts, CCD, impact
+    zones, the kinematic obstacle given per step as driver.cpp:113-131 does).
+    Informational (not the headline config); one GPU."""
+    import numpy as np
+    import torch
+    from paper_2008_00409_b200 import scene as S
+    from paper_2008_00409_b200 import scenes
+    sc = scenes.config("C")
+    mesh = weft.ClothMesh.build(sc.verts, sc.tris, sc.density)
+    p = mesh.vertex_count
+    xs = sc.verts
+    radius = 0.4
+    ycl = float(xs[:, 1].max())
+    center = (float(xs[:, 0].mean()), ycl + radius + 1.5 * sc.thickness, float(xs[:, 2].mean()))
+    body = S.make_uv_sphere(center, radius, 48, 96)
+    bv = np.asarray(body.vertices, np.float64).reshape(-1, 3)
+    bt = np.asarray(body.triangles, np.int32).reshape(-1, 3) + p
+    speed = 0.2  # m/s toward the cloth (-y): within the contact thickness from the start
+    out = {"workload": f"config C ({sc.layers} x {sc.nx}^2, {sc.tri_count} tris) + uv-sphere body proxy "
+                       f"r = {radius} m ({len(bt)} tris) moving into the cloth at {speed} m/s",
+           "note": "weft_gpu_sim_step(contacts=1, zones=1) after weft_gpu_sim_set_obstacles, trajectory from rest; "
+                   "median device time of steps 2..; informational"}
+    times, reps = [], []
+    try:
+        with weft.Engine(1) as eng:
+            eng.set_vertices(mesh.vertex_mass, sc.pinned)
+            eng.set_elements(mesh.build_elements(sc.material, sc.gravity))
+            eng.set_soup(p + len(bv), np.concatenate([sc.tris, bt]))
+            x0 = sc.verts.reshape(-1).copy()
+            eng.sim_set_state(x0, np.zeros_like(x0))
+            prm = weft.SimParams(sc.dt, sc.thickness, 1.5, weft.PcgConfig(1e-4, 400), weft.JAC_SPD, contacts=1,
+                                 zones=1)
+            st = torch.cuda.ExternalStream(eng.stream())
+            for k in range(steps):
+                b0 = bv - np.array([0.0, speed * sc.dt * k, 0.0])
+                b1 = bv - np.array([0.0, speed * sc.dt * (k + 1), 0.0])
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(st)
+                eng.sim_set_obstacles(sc.dt, b0.reshape(-1), b1.reshape(-1))
+                r = eng.sim_step(prm)
+                e1.record(st)
+                e1.synchronize()
+                times.append(e0.elapsed_time(e1))
+                reps.append(r)
+            out.update({"ms": statistics.median(times[2:]), "ms_all": times,
+                        "proximities": [int(r.proximities) for r in reps],
+                        "contact_elements": [int(r.contact_elements) for r in reps],
+                        "impacts": [int(r.impacts) for r in reps], "zones": [int(r.zone_count) for r in reps],
+                        "pcg_iterations": [int(r.pcg_iterations) for r in reps]})
+    except weft.Error as e:
+        out["error"] = f"step {len(times)}: {e}"
+        if len(times) > 2:
+            out.update({"ms": statistics.median(times[2:]), "ms_all": times,
+                        "proximities": [int(r.proximities) for r in reps],
+                        "contact_elements": [int(r.contact_elements) for r in reps],
+                        "impacts": [int(r.impacts) for r in reps], "zones": [int(r.zone_count) for r in reps]})
+    return out
+
+
 def zone_bench(weft, stream, with_ref: bool):
     """Impact zones: resolve_zones (CCD rounds + zone
     solves) on the GPU vs the compiled reference on the same input; both
@@ -499,6 +562,9 @@ def gpu_arm(args, rank, world, local):
     zones = None
     if world == 1 and not args.no_narrow:
         zones = zone_bench(weft, stream, not args.no_cpu_baseline)
+    proxy = None
+    if world == 1 and not args.no_narrow:
+        proxy = body_proxy_bench(weft, stream)
 
     # candidate counts: each rank walks its split_workload share
     dcd_total = int(reduce_over_ranks(float(reps[-1].dcd_candidates), dist.ReduceOp.SUM if world > 1 else None))
@@ -573,6 +639,7 @@ def gpu_arm(args, rank, world, local):
             "narrow_phase": narrow,
             "full_step_contacts": full,
             "impact_zones": zones,
+            "body_proxy": proxy,
             "assembly_roofline": assembly_roofline,
         },
         "roofline": {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak, "unit": "GB/s",
