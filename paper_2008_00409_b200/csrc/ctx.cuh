@@ -33,6 +33,8 @@ struct SellMatrix {
   DBuf<int32_t> colp;       // total: column words as positions (one-partition persistent PCG)
   int64_t layout_id = 0;    // bumped whenever the layout changes
   int64_t colp_id = -1;     // layout colp was built for
+  DBuf<int16_t> colp16;     // total: colp as offsets from the row position (when all fit 16 bits)
+  bool colp16_ok = false;   // ... for the layout colp_id
   DBuf<int32_t> cols;       // total (packed col | group << 28; -1 padding)
   DBuf<double> vals;        // 9 * total
 };

@@ -105,6 +105,11 @@ __device__ __forceinline__ int ld_nc_hint(const int* p, uint64_t pol) {
   asm volatile("ld.global.nc.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
   return v;
 }
+__device__ __forceinline__ int ld_nc_hint(const int16_t* p, uint64_t pol) {
+  short v;
+  asm volatile("ld.global.nc.L2::cache_hint.s16 %0, [%1], %2;" : "=h"(v) : "l"(p), "l"(pol));
+  return v;
+}
 __device__ __forceinline__ double ld_cg_hint(const double* p, uint64_t pol) {
   double v;
   asm volatile("ld.global.cg.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
@@ -886,6 +891,7 @@ struct PcgArgs {
   int q_msw;   // persistent solve with q in shared memory: max slices per warp
   const double* dinv6;  // persistent solve: packed symmetric D^-1 (null: 9-double form)
   float vec_el_frac;    // persistent solve: fraction of the gathered z / p lines kept evict_last
+  const int16_t* colp16;  // persistent solve: 16-bit column offsets (null: A.cols)
   unsigned long long* timing;  // dev instrumentation (WEFT_PCG_TIMING=1): ns per phase, summed
 };
 
@@ -1430,10 +1436,13 @@ __device__ __forceinline__ void vstore3(double* v, int i, double a, double b, do
   }
 }
 
-template <int PMode, int kUnroll, int Vs>
+// kC16: the column words as 16-bit offsets from the row's own position
+// (c16, built per layout when every column of the system is within +-32767
+// positions: 2 instead of 4 streamed bytes per block).
+template <int PMode, int kUnroll, int Vs, bool kC16>
 __device__ __forceinline__ void row_product_cg(const SellView& A, int r, const double* __restrict__ z,
                                                const double* __restrict__ pold, double beta, double& y0, double& y1,
-                                               double& y2, float vec_frac) {
+                                               double& y2, float vec_frac, const int16_t* __restrict__ c16) {
 #if WEFT_MAT_EF
   const uint64_t mpol = l2_policy_evict_first();
 #endif
@@ -1443,12 +1452,16 @@ __device__ __forceinline__ void row_product_cg(const SellView& A, int r, const d
   const int len = A.rowlen[r];
   const int64_t base = A.slice_off[r >> 5] + (r & 31);
   double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-  int cn = len > 0 ? (WEFT_MAT_LD(A.cols + base) & kColMask) : 0;
+  auto col = [&](int64_t at) -> int {
+    if constexpr (kC16) return r + WEFT_MAT_LD(c16 + at);
+    else return WEFT_MAT_LD(A.cols + at) & kColMask;
+  };
+  int cn = len > 0 ? col(base) : 0;
 #pragma unroll kUnroll
   for (int k = 0; k < len; ++k) {
     const int64_t at = base + (int64_t)k * kSlice;
     const int c = cn;
-    if (k + 1 < len) cn = WEFT_MAT_LD(A.cols + at + kSlice) & kColMask;
+    if (k + 1 < len) cn = col(at + kSlice);
     const double* v = A.vals + vidx(at, r & 31, 0);
     const double v0 = WEFT_MAT_LD(v), v1 = WEFT_MAT_LD(v + 32), v2 = WEFT_MAT_LD(v + 64);
     const double v3 = WEFT_MAT_LD(v + 96), v4 = WEFT_MAT_LD(v + 128), v5 = WEFT_MAT_LD(v + 160);
@@ -1517,7 +1530,7 @@ __device__ __forceinline__ void all_blocks_sum(const double* partials, int n, do
 // kUnroll: slots per row-loop trip. Grid rows (<= 13 slots) run best at 1;
 // the long contact rows (up to ~40 slots) need the deeper unroll to keep
 // enough gathers in flight (config D contacts mode: 44.1 -> 36.9 ms at 4).
-template <bool kQs, int kUnroll, int Vs>
+template <bool kQs, int kUnroll, int Vs, bool kC16>
 __global__ void __launch_bounds__(kPersistThreads, WEFT_PERSIST_MINB) k_pcg_persistent(const PcgArgs* __restrict__ args, PcgState* st) {
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
@@ -1583,8 +1596,8 @@ __global__ void __launch_bounds__(kPersistThreads, WEFT_PERSIST_MINB) k_pcg_pers
       const int i = sl * kSlice + lane;  // matrix position == vector index (position space)
       if (i < rows) {
         double y0, y1, y2;
-        if (first) row_product_cg<1, kUnroll, Vs>(A, i, z, pcur, beta, y0, y1, y2, g.vec_el_frac);
-        else row_product_cg<2, kUnroll, Vs>(A, i, z, pcur, beta, y0, y1, y2, g.vec_el_frac);
+        if (first) row_product_cg<1, kUnroll, Vs, kC16>(A, i, z, pcur, beta, y0, y1, y2, g.vec_el_frac, g.colp16);
+        else row_product_cg<2, kUnroll, Vs, kC16>(A, i, z, pcur, beta, y0, y1, y2, g.vec_el_frac, g.colp16);
         double p0, p1, p2;
         vload3<Vs>(z, i, p0, p1, p2);
         if (!first) {
@@ -1777,6 +1790,21 @@ __global__ void k_colpos(int64_t total, const int32_t* __restrict__ cols, const 
   colp[i] = c < 0 ? c : pos[c & kColMask];
 }
 
+// 16-bit position offsets of the column words (slot at of slice s, lane l:
+// row position s * 32 + l); *bad = 1 if any live column is out of range.
+__global__ void k_colpos16(int nslices, const int64_t* __restrict__ soff, const int32_t* __restrict__ rowlen,
+                           const int32_t* __restrict__ colp, int16_t* __restrict__ c16, int* __restrict__ bad) {
+  const int m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= nslices * kSlice) return;
+  const int len = rowlen[m];
+  const int64_t base = soff[m >> 5] + (m & 31);
+  for (int k = 0; k < len; ++k) {
+    const int d = colp[base + (int64_t)k * kSlice] - m;
+    if (d < -32768 || d > 32767) atomicOr(bad, 1);
+    c16[base + (int64_t)k * kSlice] = static_cast<int16_t>(d);
+  }
+}
+
 // PCG init in position space: r = b[perm], z = M^-1 r, x = 0, p = 0.
 __global__ void k_pcg_init_pos(int rows, const int32_t* __restrict__ perm, const double* __restrict__ b,
                                const double* __restrict__ dinv, bool bj, double* __restrict__ x,
@@ -1875,6 +1903,21 @@ PcgResult pcg_solve(Ctx& c, const double* b_dev, const weft_pcg_config& cfg, dou
         if (c.A.total)
           k_colpos<<<div_up(c.A.total, 256), 256, 0, ls(c)>>>(c.A.total, c.A.cols.data(), c.A.pos.data(),
                                                                c.A.colp.data());
+        // 16-bit offsets when every column is within +-32767 positions of its
+        // row (grid meshes: the row bandwidth 2 nx + 1 plus the sigma window)
+        static const bool c16_off = std::getenv("WEFT_PCG_C16") && std::atoi(std::getenv("WEFT_PCG_C16")) == 0;
+        c.A.colp16_ok = false;
+        if (!c16_off && c.A.total) {
+          c.A.colp16.resize(static_cast<size_t>(c.A.total) + 1);
+          int* bad = reinterpret_cast<int*>(c.scalars.data() + 13);
+          WG_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), s));
+          k_colpos16<<<div_up(c.A.nslices * kSlice, 256), 256, 0, ls(c)>>>(
+              c.A.nslices, c.A.slice_off.data(), c.A.rowlen.data(), c.A.colp.data(), c.A.colp16.data(), bad);
+          int hbad = 1;
+          WG_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s));
+          WG_CUDA(cudaStreamSynchronize(s));
+          c.A.colp16_ok = hbad == 0;
+        }
         c.A.colp_id = c.A.layout_id;
       }
       c.xp.resize(len);
@@ -1929,14 +1972,24 @@ PcgResult pcg_solve(Ctx& c, const double* b_dev, const weft_pcg_config& cfg, dou
   size_t qs_bytes = 0;
   static const int unroll_env = std::getenv("WEFT_PCG_UNROLL") ? std::atoi(std::getenv("WEFT_PCG_UNROLL")) : 0;
   const int unroll = (unroll_env ? unroll_env : (c.n_contacts > 0 ? 4 : kPkUnroll)) >= 4 ? 4 : 1;
-  auto pick = [&](bool q) -> decltype(&k_pcg_persistent<false, 1, 3>) {
-    if (v4) {
-      if (unroll == 4) return q ? k_pcg_persistent<true, 4, 4> : k_pcg_persistent<false, 4, 4>;
-      return q ? k_pcg_persistent<true, 1, 4> : k_pcg_persistent<false, 1, 4>;
+  const bool c16 = persistent && c.A.colp16_ok;
+  auto pick = [&](bool q) -> decltype(&k_pcg_persistent<false, 1, 3, false>) {
+    if (c16) {
+      if (v4) {
+        if (unroll == 4) return q ? k_pcg_persistent<true, 4, 4, true> : k_pcg_persistent<false, 4, 4, true>;
+        return q ? k_pcg_persistent<true, 1, 4, true> : k_pcg_persistent<false, 1, 4, true>;
+      }
+      if (unroll == 4) return q ? k_pcg_persistent<true, 4, 3, true> : k_pcg_persistent<false, 4, 3, true>;
+      return q ? k_pcg_persistent<true, 1, 3, true> : k_pcg_persistent<false, 1, 3, true>;
     }
-    if (unroll == 4) return q ? k_pcg_persistent<true, 4, 3> : k_pcg_persistent<false, 4, 3>;
-    return q ? k_pcg_persistent<true, 1, 3> : k_pcg_persistent<false, 1, 3>;
+    if (v4) {
+      if (unroll == 4) return q ? k_pcg_persistent<true, 4, 4, false> : k_pcg_persistent<false, 4, 4, false>;
+      return q ? k_pcg_persistent<true, 1, 4, false> : k_pcg_persistent<false, 1, 4, false>;
+    }
+    if (unroll == 4) return q ? k_pcg_persistent<true, 4, 3, false> : k_pcg_persistent<false, 4, 3, false>;
+    return q ? k_pcg_persistent<true, 1, 3, false> : k_pcg_persistent<false, 1, 3, false>;
   };
+
   auto pkern = pick(false);
   if (persistent) {
     // q in shared memory when the warps' slice runs fit at two CTAs per SM
@@ -1970,6 +2023,7 @@ PcgResult pcg_solve(Ctx& c, const double* b_dev, const weft_pcg_config& cfg, dou
                c.q.data(), c.partials.data(), c.hist.data(), c.phist.data(), c.comm, c.pm, c.p2.data()};
   if (persistent) {
     args.A.cols = c.A.colp.data();  // columns as positions
+    args.colp16 = c16 ? c.A.colp16.data() : nullptr;
     args.x = c.xp.data();
     if (v4) {  // gathered vectors 32 bytes per row
       args.z = c.z4.data();
