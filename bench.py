@@ -584,6 +584,9 @@ def gpu_arm(args, rank, world, local):
         launch_ms = st.pcg_ms / st.pcg_solves
         nlaunch = st.pcg_solves
         traffic = pcg_traffic_per_launch(args.config, st.pcg_iterations / st.pcg_solves)
+        if world > 1:  # the rank group's solver: one cooperative launch per rank (its rows only)
+            kname = "k_pcg_persistent_rows (rank-group PCG, one cooperative launch per rank)"
+            traffic = None  # no ncu capture of the multi-rank kernel (one GPU per gpurun call)
     else:
         # k_pcg_spmv: 9 FP64 values + 1 int32 column per live block; per
         # row: length word, z and p gathered once, q written.
