@@ -51,7 +51,7 @@ def weft():
     return w
 
 
-@pytest.mark.parametrize("world,parts", [(2, 2), (2, 4)])
+@pytest.mark.parametrize("world,parts", [(2, 2), (2, 4), (4, 4)])
 def test_rank_group_matches_single_process(weft, tmp_path, world, parts):
     import mp_rank
 
