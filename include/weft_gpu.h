@@ -353,8 +353,10 @@ typedef struct weft_sim_params {
   /* 1: Simulator::step_impl stages 1-2 in full (driver.cpp:132-149): the DCD
    * narrow phase, proximities_to_elements (response.cpp:43-106) on the
    * device and the contact elements assembled with the static ones; the CCD
-   * narrow phase counts impacts (impact zones are not resolved). One rank
-   * only. 0: the hot-path step (candidate pairs counted, no contacts). */
+   * narrow phase counts impacts (impact zones are not resolved). A rank group
+   * narrow-phases its split_workload shares and merges the hits over peer
+   * memory (collision.cpp:405-417). 0: the hot-path step (candidate pairs
+   * counted, no contacts). */
   int32_t contacts;
   double stiffness_scale; /* ContactParams (response.hpp:13-21); contact thickness = thickness */
   double friction;
@@ -381,6 +383,9 @@ typedef struct weft_step_report {
   int32_t zone_count;       /* zones mode: zones over all outer rounds */
   int32_t zone_outer;       /* zones mode: outer rounds */
   double ms_zones;          /* zones mode: device time of resolve_zones */
+  int32_t stages;           /* stages of Simulator::step_impl run, in canonical_stage_order
+                               (driver.cpp:49-53): proximity_dcd, assemble, solve, candidate,
+                               ccd, zones, commit — 7 for a committed zones-mode step */
 } weft_step_report;
 
 /* Uploads the state (x, v: 3*p doubles each; the soup positions of the
@@ -428,6 +433,18 @@ typedef struct weft_gpu_stats_t {
  * kernel on the one-partition path. */
 weft_status weft_gpu_profile(weft_gpu_ctx* ctx, int32_t enable);
 weft_status weft_gpu_stats(weft_gpu_ctx* ctx, weft_gpu_stats_t* out);
+
+/* Engine instrumentation (EngineOptions::instrument, exec.hpp; Engine::log_line
+ * exec.cpp:176-180): while on, the library records the event lines the
+ * reference writes from inside its solvers, in its format —
+ *   "event=pcg iterations=N rel_residual=R converged=C"   (solver.hpp:171-175)
+ *   "event=zones outer=K zones=Z fresh=F accumulated=A"   (response.cpp:383-388)
+ * weft_gpu_take_log copies the recorded lines (newline-terminated, NUL-ended)
+ * into buf and clears them; buf = NULL (or cap too small) only reports the
+ * byte count (without the NUL) in *len. Stage lines ("event=stage frame=..")
+ * belong to the driver (driver.cpp:104-111): weft_step_report.stages. */
+weft_status weft_gpu_set_instrument(weft_gpu_ctx* ctx, int32_t on);
+weft_status weft_gpu_take_log(weft_gpu_ctx* ctx, char* buf, int64_t cap, int64_t* len);
 /* Test hook for the exact serial-order sum behind build_grid's cell size
  * (collision.cpp:124-133): mean_exact = max(sum/n, 1e-9) from the parallel
  * exact kernel (fast = 1: chunk-map fast path, 0: window scan only),

@@ -995,6 +995,8 @@ namespace {
 struct SceneHandle {
   Scene scene;
   std::unique_ptr<Simulator> sim;
+  std::ostringstream log;  // the Simulator's EngineOptions::instrument stream
+  bool instrument = false;
 };
 }  // namespace
 
@@ -1071,7 +1073,8 @@ int32_t ref_scene_step(void* hp, int32_t devices, double* out) {
     if (!h->sim) {
       SimConfig cfg = h->scene.config;
       if (devices > 0) cfg.devices = devices;
-      h->sim = std::make_unique<Simulator>(h->scene.cloth, h->scene.pinned, h->scene.obstacles, cfg);
+      h->sim = std::make_unique<Simulator>(h->scene.cloth, h->scene.pinned, h->scene.obstacles, cfg,
+                                           h->instrument ? &h->log : nullptr);
     }
     const auto r = h->sim->step();
     const double v[] = {(double)r.frame, r.time, (double)r.pcg_iterations, r.pcg_residual, (double)r.proximities,
@@ -1105,5 +1108,18 @@ int64_t ref_scene_save_obj(void* hp, char* buf, int64_t cap) {
 }
 
 void ref_scene_free(void* hp) { delete static_cast<SceneHandle*>(hp); }
+
+// Instrument the Simulator created by the next ref_scene_step; take_log
+// returns the lines written so far (size query with buf = NULL) and clears.
+void ref_scene_instrument(void* hp) { static_cast<SceneHandle*>(hp)->instrument = true; }
+int64_t ref_scene_take_log(void* hp, char* buf, int64_t cap) {
+  auto* h = static_cast<SceneHandle*>(hp);
+  const std::string s = h->log.str();
+  if (!buf || cap < static_cast<int64_t>(s.size()) + 1) return static_cast<int64_t>(s.size());
+  std::memcpy(buf, s.data(), s.size());
+  buf[s.size()] = '\0';
+  h->log.str("");
+  return static_cast<int64_t>(s.size());
+}
 
 }  // extern "C"

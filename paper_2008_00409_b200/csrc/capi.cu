@@ -332,6 +332,24 @@ weft_status weft_gpu_profile(weft_gpu_ctx* ctx, int32_t enable) {
   });
 }
 
+weft_status weft_gpu_set_instrument(weft_gpu_ctx* ctx, int32_t on) {
+  return guard(ctx, [&] {
+    ctx->c.instrument = on != 0;
+    if (!on) ctx->c.log.clear();
+  });
+}
+
+weft_status weft_gpu_take_log(weft_gpu_ctx* ctx, char* buf, int64_t cap, int64_t* len) {
+  return guard(ctx, [&] {
+    std::string& l = ctx->c.log;
+    if (len) *len = static_cast<int64_t>(l.size());
+    if (!buf || cap < static_cast<int64_t>(l.size()) + 1) return;
+    std::memcpy(buf, l.data(), l.size());
+    buf[l.size()] = '\0';
+    l.clear();
+  });
+}
+
 weft_status weft_gpu_stats(weft_gpu_ctx* ctx, weft_gpu_stats_t* out) {
   return guard(ctx, [&] {
     out->launches = ctx->c.launches;

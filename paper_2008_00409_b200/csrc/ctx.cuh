@@ -193,6 +193,8 @@ struct Ctx {
   DBuf<int64_t> scalars;  // small device scratch
 
   // ---- instrumentation
+  bool instrument = false;        // record the reference's solver event lines
+  std::string log;                // ... here (weft_gpu_take_log)
   int64_t launches = 0;           // kernels of this library launched so far
   bool profile = false;           // time every PCG SpMV launch with events
   int64_t spmv_launches = 0;      // PCG SpMV launches timed
@@ -229,6 +231,17 @@ struct Ctx {
   int32_t zn_nz = 0;     // zones of the last build
   int64_t zn_nzv = 0;    // zone vertices of the last build
 };
+
+// Engine::log_line (exec.cpp:176-180) while instrumentation is on.
+inline void log_line(Ctx& c, const std::string& line) {
+  if (c.instrument) c.log += line + "\n";
+}
+// ostream << double with the default format (precision 6, %g).
+inline std::string fmt_g(double v) {
+  char b[64];
+  std::snprintf(b, sizeof(b), "%g", v);
+  return b;
+}
 
 // Launch-site stream accessor: counts the launch (gpu_launches in bench.py).
 inline cudaStream_t ls(Ctx& c) {

@@ -498,6 +498,8 @@ weft_status weft_gpu_sim_step(weft_gpu_ctx* ctx, const weft_sim_params* prm, wef
       rep->zone_count = zr.zone_count;
       rep->zone_outer = zr.outer_iterations;
       rep->ms_zones = tz;
+      // the full Simulator::step_impl ran its seven stages in canonical order
+      rep->stages = contacts && prm->zones ? 7 : 0;
     }
   });
 }

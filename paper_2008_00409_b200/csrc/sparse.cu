@@ -2217,6 +2217,8 @@ PcgResult pcg_solve(Ctx& c, const double* b_dev, const weft_pcg_config& cfg, dou
   if (hs->status == 3)
     throw Error(WEFT_ERR_SOLVER,
                 "pcg: divergence (non-finite residual) at iteration " + std::to_string(hs->iter));
+  log_line(c, "event=pcg iterations=" + std::to_string(res.iterations) + " rel_residual=" + fmt_g(res.rel_residual) +
+                  " converged=" + std::to_string(res.converged ? 1 : 0));  // solver.hpp:171-175
   if (hist_host && res.iterations)
     WG_CUDA(cudaMemcpyAsync(hist_host, c.hist.data(), sizeof(double) * res.iterations, cudaMemcpyDeviceToHost, s));
   if (phist_host && res.iterations)

@@ -695,6 +695,8 @@ void resolve_zones(Ctx& c, const double* xb, double* xcand, const double* mass, 
         for (int z : dz)
           if (fail[z]) throw Error(WEFT_ERR_ZONE, "zone " + std::to_string(z) + ": inner solver diverged");
     }
+    log_line(c, "event=zones outer=" + std::to_string(outer + 1) + " zones=" + std::to_string(nz) +
+                    " fresh=" + std::to_string(nf) + " accumulated=" + std::to_string(m));  // response.cpp:383-388
   }
   // cap reached: the surviving zones name the failure (:384-399)
   const int64_t nr = collide_ccd();

@@ -15,6 +15,7 @@
 #include <map>
 #include <memory>
 #include <mutex>
+#include <sstream>
 #include <span>
 #include <stdexcept>
 #include <string>
@@ -409,6 +410,16 @@ PcgReport pcg_solve(Engine& engine, const PartitionedMatrix<Real>& a, const Vali
     out.rel_residual = rep.rel_residual;
     out.residual_history.assign(hist.begin(), hist.begin() + rep.iterations);
     out.precond_norm_history.assign(phist.begin(), phist.begin() + rep.iterations);
+    if (engine.options().instrument != nullptr && bg.size()) {  // solver.hpp:171-175 (not for b = 0)
+      bool zero = true;
+      for (double v : bg) zero = zero && v == 0.0;
+      if (!zero) {
+        std::ostringstream os;
+        os << "event=pcg iterations=" << out.iterations << " rel_residual=" << out.rel_residual
+           << " converged=" << (out.converged ? 1 : 0);
+        engine.log_line(os.str());
+      }
+    }
     return out;
   }
 }
@@ -550,8 +561,20 @@ inline ZoneResolveReport resolve_zones(Engine& engine, const CollisionSoup& soup
                             zparams.al_iterations, zparams.inner_iterations, zparams.outer_cap,
                             zparams.retry_cap, zparams.max_correction_factor};
   weft_zone_report rep{};
+  const bool instrument = engine.options().instrument != nullptr;
+  if (instrument) check(weft_gpu_set_instrument(ctx, 1));
   const weft_status st = weft_gpu_resolve_zones(ctx, xb.data(), xc.data(), vertex_mass.data(), cparams.thickness,
                                                 cparams.cell_scale, &zp, &rep);
+  if (instrument) {  // the per-round event=zones lines (response.cpp:383-388)
+    int64_t n = 0;
+    check(weft_gpu_take_log(ctx, nullptr, 0, &n));
+    std::string lines(static_cast<std::size_t>(n) + 1, '\0');
+    check(weft_gpu_take_log(ctx, lines.data(), n + 1, &n));
+    check(weft_gpu_set_instrument(ctx, 0));
+    std::istringstream is(lines.substr(0, static_cast<std::size_t>(n)));
+    for (std::string ln; std::getline(is, ln);)
+      if (!ln.empty()) engine.log_line(ln);
+  }
   if (st == WEFT_OK || st == WEFT_ERR_ZONE)
     for (std::size_t v = 0; v < x_candidate.size(); ++v) x_candidate[v] = Vec3(xc[3 * v], xc[3 * v + 1], xc[3 * v + 2]);
   check(st);

@@ -429,6 +429,12 @@ class FrameReport:  # driver.hpp:47-63
     zone_count: int = 0
     zone_outer: int = 0
     committed: bool = False
+    stage_trace: list = field(default_factory=list)
+
+
+def canonical_stage_order() -> list:
+    """The per-step stage order instrumentation asserts (driver.cpp:49-53)."""
+    return ["proximity_dcd", "assemble", "solve", "candidate", "ccd", "zones", "commit"]
 
 
 def _g10(x) -> str:
@@ -458,7 +464,11 @@ class Simulator:
     """Simulator (driver.cpp:55-215) on one GPU: the state stays on the
     device; step() issues one weft_gpu_sim_step (the whole step_impl)."""
 
-    def __init__(self, scene: Scene, devices: int | None = None, cuda_device: int = 0):
+    def __init__(self, scene: Scene, devices: int | None = None, cuda_device: int = 0, instrument=None):
+        """instrument: a writable text stream (EngineOptions::instrument): the
+        reference's event lines — stage (driver.cpp:104-111), pcg
+        (solver.hpp:171-175) and zones (response.cpp:383-388) — in its
+        order and format."""
         if scene.config.precision != "double":
             raise SceneError("the GPU path computes in double precision (Precision::Double)")
         self.scene = scene
@@ -466,6 +476,9 @@ class Simulator:
         self.mesh = scene.cloth
         p = self.mesh.vertex_count
         self.engine = weft.Engine(devices or cfg.devices, cuda_device=cuda_device)
+        self.instrument = instrument
+        if instrument is not None:
+            self.engine.set_instrument(True)
         self.engine.set_vertices(self.mesh.vertex_mass, scene.pinned)
         self.engine.set_elements(self.mesh.build_elements(cfg.material.as_tuple(), cfg.gravity, cfg.wind))
         tris = [np.asarray(self.mesh.triangles, np.int32).reshape(-1, 3)]
@@ -498,14 +511,40 @@ class Simulator:
         if self.scene.obstacles:
             self.engine.sim_set_obstacles(dt, self._obstacles_at(self.time), self._obstacles_at(self.time + dt))
         t0 = _time.perf_counter()
-        r = self.engine.sim_step(self.params)
+        try:
+            r = self.engine.sim_step(self.params)
+        except weft.Error as e:
+            # the stages the reference logged before it threw: up to the solve
+            # for a solver error, up to the zones for a zone failure
+            last = "zones" if isinstance(e, weft.ZoneFailure) else "solve"
+            order = canonical_stage_order()
+            self._log_frame(order[:order.index(last) + 1])
+            raise
+        stages = canonical_stage_order()[:r.stages]
+        self._log_frame(stages)
+        if stages != canonical_stage_order():  # driver.cpp:211-213
+            raise weft.ExecError(f"frame {self.frame}: stage order violated")
         rep = FrameReport(self.frame, self.time, r.ms_assemble + r.ms_solve, r.ms_broad, 0.0, r.ms_zones,
                           r.pcg_iterations, r.pcg_residual, r.proximities, r.contact_elements, r.impacts,
-                          r.zone_count, r.zone_outer, True)
+                          r.zone_count, r.zone_outer, True, stages)
         rep.wall_ms = 1e3 * (_time.perf_counter() - t0)
         self.time += dt
         self.frame += 1
         return rep
+
+    def _log_frame(self, stages):
+        """Writes the frame's instrument lines: each stage as it starts, the
+        solver's events after the stage that emits them."""
+        if self.instrument is None:
+            return
+        events = [ln for ln in self.engine.take_log().splitlines() if ln]
+        for name in stages:
+            self.instrument.write(f"event=stage frame={self.frame} name={name}\n")
+            kind = {"solve": "event=pcg ", "zones": "event=zones "}.get(name)
+            if kind:
+                for ln in events:
+                    if ln.startswith(kind):
+                        self.instrument.write(ln + "\n")
 
     def state(self):
         p = self.mesh.vertex_count

@@ -182,7 +182,7 @@ class StepReport(C.Structure):
                 ("dcd_candidates", C.c_int64), ("ccd_candidates", C.c_int64), ("ms_broad", C.c_double),
                 ("ms_assemble", C.c_double), ("ms_solve", C.c_double), ("proximities", C.c_int64),
                 ("contact_elements", C.c_int64), ("impacts", C.c_int64), ("zone_count", C.c_int32),
-                ("zone_outer", C.c_int32), ("ms_zones", C.c_double)]
+                ("zone_outer", C.c_int32), ("ms_zones", C.c_double), ("stages", C.c_int32)]
 
 
 def _load():
@@ -684,6 +684,22 @@ def _engine_stream(self) -> int:
     return s.value or 0
 
 
+def _engine_set_instrument(self, on: bool = True):
+    """EngineOptions::instrument: record the reference's solver event lines
+    (event=pcg, event=zones) — take them with take_log()."""
+    _check(LIB.weft_gpu_set_instrument(self._ctx, C.c_int32(1 if on else 0)))
+
+
+def _engine_take_log(self) -> str:
+    n = C.c_int64()
+    _check(LIB.weft_gpu_take_log(self._ctx, None, C.c_int64(0), C.byref(n)))
+    buf = C.create_string_buffer(n.value + 1)
+    _check(LIB.weft_gpu_take_log(self._ctx, buf, C.c_int64(n.value + 1), C.byref(n)))
+    return buf.value.decode()
+
+
+Engine.set_instrument = _engine_set_instrument
+Engine.take_log = _engine_take_log
 Engine.profile = _engine_profile
 Engine.stats = _engine_stats
 Engine.stream = _engine_stream

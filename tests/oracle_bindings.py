@@ -592,6 +592,17 @@ class RefScene:
         self.lib.ref_scene_state(C.c_void_p(self.h), ptr(x), ptr(v))
         return x, v
 
+    def instrument(self):
+        """Instrument the Simulator (created at the first step)."""
+        self.lib.ref_scene_instrument(C.c_void_p(self.h))
+
+    def take_log(self) -> str:
+        self.lib.ref_scene_take_log.restype = C.c_int64
+        n = self.lib.ref_scene_take_log(C.c_void_p(self.h), None, C.c_int64(0))
+        buf = C.create_string_buffer(n + 1)
+        self.lib.ref_scene_take_log(C.c_void_p(self.h), buf, C.c_int64(n + 1))
+        return buf.value.decode()
+
     def save_obj(self) -> str:
         n = self.lib.ref_scene_save_obj(C.c_void_p(self.h), None, C.c_int64(0))
         buf = C.create_string_buffer(int(n))

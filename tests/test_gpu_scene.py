@@ -74,11 +74,14 @@ def test_config_A_sphere_vs_reference_live(S):
     collider; tests/scenes_gen.py) through the GPU Simulator vs the reference
     Simulator frame by frame: 21 frames (contacts with the sphere from frame
     12), then the frame on which the reference raises ZoneFailure."""
+    import io
     from paper_2008_00409_b200 import weft
     from oracle_bindings import RefError
     sc = S.parse_scene(scene_text("config_A"))
-    sim = S.Simulator(sc)
+    log = io.StringIO()
+    sim = S.Simulator(sc, instrument=log)
     rs = RefScene(REF, text=scene_text("config_A"))
+    rs.instrument()
     contacts = 0
     for k in range(sc.config.frames):
         try:
@@ -100,6 +103,32 @@ def test_config_A_sphere_vs_reference_live(S):
     x, v = sim.state()
     xr, vr = rs.state()
     assert rel(x.reshape(-1), xr) <= 1e-8 and rel(v.reshape(-1), vr) <= 1e-8
+    # the instrument streams (EngineOptions::instrument): the same stage and
+    # zones events in the same order; pcg events with the iteration counts
+    # compared above (the CPU engine's event=transfer lines have no GPU
+    # analogue). Frames both committed; inside the frame that fails, the
+    # zone rounds may part (the ZoneFailure message is compared up to the
+    # surviving-zone list, same_failure).
+    def frames(text):
+        out, f = [], -1
+        for ln in text.splitlines():
+            w = ln.split()
+            if w[0] == "event=transfer":
+                continue
+            if w[0] == "event=stage":
+                f = int(w[1].split("=")[1])
+            out.append((f, w))
+        return [w for fr, w in out if fr < k]
+    ours, ref = frames(log.getvalue()), frames(rs.take_log())
+    assert [ln[0] for ln in ours] == [ln[0] for ln in ref]
+    for a, b in zip(ours, ref):
+        if a[0] == "event=pcg":
+            ia, ib = int(a[1].split("=")[1]), int(b[1].split("=")[1])
+            assert abs(ia - ib) <= max(1, 0.02 * ib) and a[3] == b[3], (a, b)
+        else:
+            assert a == b
+    assert sum(ln[0] == "event=stage" for ln in ours) == 7 * k
+    assert sum(ln[0] == "event=pcg" for ln in ours) >= 20
     rs.close()
     sim.close()
 
