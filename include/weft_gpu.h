@@ -203,6 +203,18 @@ typedef struct weft_pcg_report { /* PcgReport, solver.hpp:23-29 */
 weft_status weft_gpu_pcg(weft_gpu_ctx* ctx, const double* b, double* x, const weft_pcg_config* config,
                          weft_pcg_report* report);
 
+/* Precision::Single (driver.hpp:13, Real = float; one rank): the same entry
+ * points over float values — BellMatrix<float> and spmv_serial /
+ * spmv_pipelined<float> (bell.cpp:87-129, float products and sums in the
+ * same order), pcg_solve<float> (solver.hpp:36-178: float vectors, double
+ * dot products and block-Jacobi inverses, alpha / beta cast to float). */
+weft_status weft_gpu_set_matrix_f32(weft_gpu_ctx* ctx, int32_t block_rows, const int64_t* row_ptr,
+                                    const int32_t* cols, const float* vals);
+weft_status weft_gpu_spmv_f32(weft_gpu_ctx* ctx, const float* x, float* y);
+weft_status weft_gpu_pcg_f32(weft_gpu_ctx* ctx, const float* b, float* x, const weft_pcg_config* config,
+                             weft_pcg_report* report);
+weft_status weft_gpu_download_matrix_f32(weft_gpu_ctx* ctx, int64_t* row_ptr, int32_t* cols, float* vals);
+
 /* ---------------------------------------------------------------------- */
 /* Assembly (proj/include/weft/assembly.hpp:48-220, physics.hpp:44-69)    */
 /* ---------------------------------------------------------------------- */

@@ -168,18 +168,19 @@ Csr from_bell(const BellMatrix<double>& a) {
   return c;
 }
 
-BellMatrix<double> to_bell(int rows, const int64_t* row_ptr, const int32_t* cols, const double* vals) {
-  std::vector<BlockEntry<double>> entries;
+template <class Real = double>
+BellMatrix<Real> to_bell(int rows, const int64_t* row_ptr, const int32_t* cols, const Real* vals) {
+  std::vector<BlockEntry<Real>> entries;
   for (int r = 0; r < rows; ++r) {
     for (int64_t k = row_ptr[r]; k < row_ptr[r + 1]; ++k) {
-      BlockEntry<double> e;
+      BlockEntry<Real> e;
       e.row = r;
       e.col = cols[k];
       for (int i = 0; i < 9; ++i) e.m[static_cast<std::size_t>(i)] = vals[9 * k + i];
       entries.push_back(e);
     }
   }
-  return BellMatrix<double>::from_entries(rows, entries);
+  return BellMatrix<Real>::from_entries(rows, entries);
 }
 
 ValidatedSchedule schedule_for(int n) {
@@ -323,20 +324,22 @@ void* ref_random_bell(uint64_t seed, int32_t rows, int32_t extra) {
 }
 
 // ---------------------------------------------------------------- SpMV/PCG
-int32_t ref_spmv(int32_t rows, const int64_t* row_ptr, const int32_t* cols, const double* vals, int32_t n,
-                 const double* x, double* y) {
+}  // extern "C"
+template <class Real>
+int32_t ref_spmv_t(int32_t rows, const int64_t* row_ptr, const int32_t* cols, const Real* vals, int32_t n,
+                   const Real* x, Real* y) {
   try {
-    const auto global = to_bell(rows, row_ptr, cols, vals);
+    const auto global = to_bell<Real>(rows, row_ptr, cols, vals);
     const auto parts = make_partitions(rows, n);
     const auto split = partition_matrix(global, parts);
     Engine engine(n);
     const auto sched = schedule_for(n);
-    DistVector<double> xv(&engine, parts), yv(&engine, parts);
+    DistVector<Real> xv(&engine, parts), yv(&engine, parts);
     for (int d = 0; d < n; ++d) {
       const auto& part = parts[static_cast<std::size_t>(d)];
       std::copy(x + 3 * part.begin, x + 3 * part.end, xv.local(d).begin());
     }
-    SpmvWorkspace<double> ws(n, split.padded_len);
+    SpmvWorkspace<Real> ws(n, split.padded_len);
     spmv_pipelined(engine, split, sched, xv, yv, ws);
     const auto yg = yv.gather();
     std::copy(yg.begin(), yg.end(), y);
@@ -346,15 +349,16 @@ int32_t ref_spmv(int32_t rows, const int64_t* row_ptr, const int32_t* cols, cons
   }
 }
 
-int32_t ref_pcg(int32_t rows, const int64_t* row_ptr, const int32_t* cols, const double* vals, int32_t n,
-                const double* b, double* x, const weft_pcg_config* cfg, weft_pcg_report* rep) {
+template <class Real>
+int32_t ref_pcg_t(int32_t rows, const int64_t* row_ptr, const int32_t* cols, const Real* vals, int32_t n,
+                  const Real* b, Real* x, const weft_pcg_config* cfg, weft_pcg_report* rep) {
   try {
-    const auto global = to_bell(rows, row_ptr, cols, vals);
+    const auto global = to_bell<Real>(rows, row_ptr, cols, vals);
     const auto parts = make_partitions(rows, n);
     const auto split = partition_matrix(global, parts);
     Engine engine(n);
     const auto sched = schedule_for(n);
-    DistVector<double> bv(&engine, parts), xv(&engine, parts);
+    DistVector<Real> bv(&engine, parts), xv(&engine, parts);
     for (int d = 0; d < n; ++d) {
       const auto& part = parts[static_cast<std::size_t>(d)];
       std::copy(b + 3 * part.begin, b + 3 * part.end, bv.local(d).begin());
@@ -378,6 +382,25 @@ int32_t ref_pcg(int32_t rows, const int64_t* row_ptr, const int32_t* cols, const
   } catch (const std::exception& e) {
     return set_error(e);
   }
+}
+
+extern "C" {
+int32_t ref_spmv(int32_t rows, const int64_t* row_ptr, const int32_t* cols, const double* vals, int32_t n,
+                 const double* x, double* y) {
+  return ref_spmv_t<double>(rows, row_ptr, cols, vals, n, x, y);
+}
+int32_t ref_pcg(int32_t rows, const int64_t* row_ptr, const int32_t* cols, const double* vals, int32_t n,
+                const double* b, double* x, const weft_pcg_config* cfg, weft_pcg_report* rep) {
+  return ref_pcg_t<double>(rows, row_ptr, cols, vals, n, b, x, cfg, rep);
+}
+// Precision::Single: spmv_pipelined<float>, pcg_solve<float>
+int32_t ref_spmv_f32(int32_t rows, const int64_t* row_ptr, const int32_t* cols, const float* vals, int32_t n,
+                     const float* x, float* y) {
+  return ref_spmv_t<float>(rows, row_ptr, cols, vals, n, x, y);
+}
+int32_t ref_pcg_f32(int32_t rows, const int64_t* row_ptr, const int32_t* cols, const float* vals, int32_t n,
+                    const float* b, float* x, const weft_pcg_config* cfg, weft_pcg_report* rep) {
+  return ref_pcg_t<float>(rows, row_ptr, cols, vals, n, b, x, cfg, rep);
 }
 
 // ---------------------------------------------------------------- meshes

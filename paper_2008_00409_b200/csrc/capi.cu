@@ -203,6 +203,86 @@ weft_status weft_gpu_set_matrix(weft_gpu_ctx* ctx, int32_t rows, const int64_t* 
   });
 }
 
+// ---- Precision::Single (driver.hpp:13; Real = float), one rank
+weft_status weft_gpu_set_matrix_f32(weft_gpu_ctx* ctx, int32_t rows, const int64_t* row_ptr, const int32_t* cols,
+                                    const float* vals) {
+  return guard(ctx, [&] {
+    need(row_ptr != nullptr, WEFT_ERR_INVALID, "set_matrix: row_ptr is NULL");
+    need(ctx->c.world == 1, WEFT_ERR_INVALID, "set_matrix: Precision::Single runs on one rank");
+    std::vector<int64_t> rp(static_cast<size_t>(rows) + 1);
+    WG_CUDA(cudaMemcpy(rp.data(), row_ptr, rp.size() * sizeof(int64_t), cudaMemcpyDefault));
+    const int64_t nnzb = rp.back();
+    std::vector<int32_t> cl(static_cast<size_t>(nnzb));
+    std::vector<float> vl(9 * static_cast<size_t>(nnzb));
+    if (nnzb) {
+      WG_CUDA(cudaMemcpy(cl.data(), cols, cl.size() * sizeof(int32_t), cudaMemcpyDefault));
+      WG_CUDA(cudaMemcpy(vl.data(), vals, vl.size() * sizeof(float), cudaMemcpyDefault));
+    }
+    weft_gpu::set_matrix_csr_f32(ctx->c, rows, rp.data(), cl.data(), vl.data());
+  });
+}
+
+weft_status weft_gpu_spmv_f32(weft_gpu_ctx* ctx, const float* x, float* y) {
+  return guard(ctx, [&] {
+    auto& c = ctx->c;
+    need(c.has_matrix && c.A.f32, WEFT_ERR_INVALID, "spmv: no single-precision matrix");
+    const size_t len = 3 * static_cast<size_t>(c.pm.p);
+    c.q.resize(len);
+    c.r.resize(len);
+    float* xd = reinterpret_cast<float*>(c.r.data());
+    float* yd = reinterpret_cast<float*>(c.q.data());
+    WG_CUDA(cudaMemcpyAsync(xd, x, len * sizeof(float), cudaMemcpyDefault, c.stream));
+    weft_gpu::spmv_f32(c, xd, yd);
+    WG_CUDA(cudaMemcpyAsync(y, yd, len * sizeof(float), cudaMemcpyDefault, c.stream));
+    WG_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+
+weft_status weft_gpu_pcg_f32(weft_gpu_ctx* ctx, const float* b, float* x, const weft_pcg_config* config,
+                             weft_pcg_report* report) {
+  return guard(ctx, [&] {
+    auto& c = ctx->c;
+    need(c.has_matrix && c.A.f32, WEFT_ERR_INVALID, "pcg: no single-precision matrix");
+    need(config != nullptr, WEFT_ERR_INVALID, "pcg: config is NULL");
+    const size_t len = 3 * static_cast<size_t>(c.pm.p);
+    const float* bdev = nullptr;
+    if (b) {
+      c.bvec.resize(len);
+      WG_CUDA(cudaMemcpyAsync(c.bvec.data(), b, len * sizeof(float), cudaMemcpyDefault, c.stream));
+      bdev = reinterpret_cast<const float*>(c.bvec.data());
+    } else {
+      need(c.has_rhs, WEFT_ERR_INVALID, "pcg: b is NULL and no assembled rhs");
+      bdev = reinterpret_cast<const float*>(c.rhs.data());
+    }
+    weft_gpu::PcgResult r;
+    try {
+      r = weft_gpu::pcg_solve_f32(c, bdev, *config, report ? report->residual_history : nullptr,
+                                  report ? report->precond_norm_history : nullptr);
+    } catch (...) {
+      if (report) report->iterations = 0;
+      throw;
+    }
+    if (report) {
+      report->iterations = r.iterations;
+      report->converged = r.converged;
+      report->rel_residual = r.rel_residual;
+    }
+    if (x) {
+      float* xs = reinterpret_cast<float*>(c.xs.data());
+      if (r.iterations == 0) WG_CUDA(cudaMemsetAsync(xs, 0, len * sizeof(float), c.stream));
+      WG_CUDA(cudaMemcpyAsync(x, xs, len * sizeof(float), cudaMemcpyDefault, c.stream));
+      WG_CUDA(cudaStreamSynchronize(c.stream));
+    }
+  });
+}
+
+weft_status weft_gpu_download_matrix_f32(weft_gpu_ctx* ctx, int64_t* row_ptr, int32_t* cols, float* vals) {
+  return guard(ctx, [&] {
+    need(ctx->c.has_matrix, WEFT_ERR_INVALID, "download_matrix: no matrix");
+    weft_gpu::download_csr_f32(ctx->c, row_ptr, cols, vals);
+  });
+}
+
 weft_status weft_gpu_spmv(weft_gpu_ctx* ctx, const double* x, double* y) {
   return guard(ctx, [&] {
     auto& c = ctx->c;

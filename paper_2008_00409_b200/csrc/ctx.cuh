@@ -37,6 +37,8 @@ struct SellMatrix {
   bool colp16_ok = false;   // ... for the layout colp_id
   DBuf<int32_t> cols;       // total (packed col | group << 28; -1 padding)
   DBuf<double> vals;        // 9 * total
+  DBuf<float> vals32;       // 9 * total: the values of a Precision::Single system
+  bool f32 = false;         // the system is single precision (vals32 holds the values)
 };
 
 constexpr int kColMask = 0x0FFFFFFF;
@@ -257,7 +259,12 @@ std::vector<int32_t> sigma_windows(const Ctx& c, int win = kSigma);
 // A.pos and A.rowlen (by position).
 void build_sigma(Ctx& c, const int32_t* len_row);
 void spmv(Ctx& c, const double* x_dev, double* y_dev);
+// Precision::Single (driver.hpp:13): float systems on one rank
+void spmv_f32(Ctx& c, const float* x_dev, float* y_dev);
+void set_matrix_csr_f32(Ctx& c, int rows, const int64_t* row_ptr, const int32_t* cols, const float* vals);
+void narrow_to_f32(Ctx& c);  // the current double values -> vals32 (exact when they came from floats)
 void download_csr(Ctx& c, int64_t* row_ptr, int32_t* cols, double* vals);
+void download_csr_f32(Ctx& c, int64_t* row_ptr, int32_t* cols, float* vals);
 struct PcgResult {
   int iterations = 0;
   int converged = 0;
@@ -266,6 +273,8 @@ struct PcgResult {
 PcgResult pcg_solve(Ctx& c, const double* b_dev, const weft_pcg_config& cfg, double* hist_host,
                     double* phist_host);
 void pcg_free(Ctx& c);
+PcgResult pcg_solve_f32(Ctx& c, const float* b_dev, const weft_pcg_config& cfg, double* hist_host,
+                        double* phist_host);
 
 void set_vertices(Ctx& c, int p, const double* mass, const uint8_t* pinned);
 void set_elements(Ctx& c, int64_t count, const weft_element* elems);

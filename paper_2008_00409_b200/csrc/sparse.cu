@@ -24,6 +24,8 @@
 
 #include <cooperative_groups.h>
 
+#include <type_traits>
+
 #include "ctx.cuh"
 
 namespace weft_gpu {
@@ -41,11 +43,20 @@ struct SellView {
   const int32_t* __restrict__ cols;
   const double* __restrict__ vals;
   const int32_t* __restrict__ perm;  // matrix position -> local row
+  const float* __restrict__ vals32;  // Precision::Single systems: the values as float
 };
 
 static SellView view(const SellMatrix& A) {
   return SellView{A.rows,        A.row0,       A.total,       A.slice_off.data(), A.rowlen.data(),
-                  A.cols.data(), A.vals.data(), A.perm.data()};
+                  A.cols.data(), A.vals.data(), A.perm.data(), A.vals32.data()};
+}
+
+// The value planes of a system in Real = T (driver.hpp:13: Precision::Double
+// runs on doubles, Precision::Single on floats).
+template <class T>
+__device__ __forceinline__ const T* sell_vals(const SellView& A) {
+  if constexpr (std::is_same_v<T, float>) return A.vals32;
+  else return A.vals;
 }
 
 // Blocks are aligned to partitions so that every block's dot partial
@@ -151,11 +162,12 @@ __device__ __forceinline__ double ld_hint(const double* p, uint64_t pol) {
 // another rank (kRemote, only reached for accumulation groups != 0) are read
 // over peer memory once that rank has published the vectors
 // (vec_ready >= vexp); `seen` caches which ranks were already waited for.
-template <int PMode, bool kRemote, bool kCg = false>
-__device__ __forceinline__ void gather3(int c, int g, const double* __restrict__ x, const double* __restrict__ pold,
-                                        double beta, const CommView& cv, const PartMap& pm, unsigned long long vexp,
-                                        unsigned& seen, double& x0, double& x1, double& x2) {
-  if (kRemote && g != 0) {
+template <int PMode, bool kRemote, bool kCg = false, class T = double>
+__device__ __forceinline__ void gather3(int c, int g, const T* __restrict__ x, const T* __restrict__ pold,
+                                        T beta, const CommView& cv, const PartMap& pm, unsigned long long vexp,
+                                        unsigned& seen, T& x0, T& x1, T& x2) {
+  if constexpr (kRemote && std::is_same_v<T, double>) {
+   if (g != 0) {
     const int q = pm.owner(c) / cv.ppr;
     if (q != cv.rank) {
       if (!(seen & (1u << q))) {
@@ -174,6 +186,7 @@ __device__ __forceinline__ void gather3(int c, int g, const double* __restrict__
       }
       return;
     }
+   }
   }
   if constexpr (kCg) {  // vectors written earlier in the same (persistent) kernel
     x0 = __ldcg(x + 3 * c);
@@ -204,14 +217,18 @@ constexpr int kMgUnroll = WEFT_MG_UNROLL;  // slots per trip of the multi-group 
 // Row product of LOCAL row lr in the reference order.
 // PMode 0: x given. PMode 1: x = z (first PCG iteration, p = z).
 // PMode 2: x = z + beta * p_old on the fly (PCG p update).
-template <int PMode, bool kRemote = false, bool kCg = false>
-__device__ __forceinline__ void row_product(const SellView& A, int lr, int ngroups, const double* __restrict__ x,
-                                            const double* __restrict__ pold, double beta, double& y0, double& y1,
-                                            double& y2, const CommView& cv = CommView(), const PartMap& pm = PartMap(),
+// T = float: Precision::Single (bell.cpp:87-129 with Real = float; beta is
+// cast to Real as the p update of solver.hpp:166 does).
+template <int PMode, bool kRemote = false, bool kCg = false, class T = double>
+__device__ __forceinline__ void row_product(const SellView& A, int lr, int ngroups, const T* __restrict__ x,
+                                            const T* __restrict__ pold, double beta_d, T& y0, T& y1,
+                                            T& y2, const CommView& cv = CommView(), const PartMap& pm = PartMap(),
                                             unsigned long long vexp = 0) {
+  const T beta = static_cast<T>(beta_d);
   const int len = A.rowlen[lr];
   const int64_t base = A.slice_off[lr >> 5] + (lr & 31);
-  double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+  const T* __restrict__ vals = sell_vals<T>(A);
+  T a0 = 0, a1 = 0, a2 = 0;
   int cg = 0;
   unsigned seen = 0;
   y0 = y1 = y2 = 0.0;
@@ -231,15 +248,15 @@ __device__ __forceinline__ void row_product(const SellView& A, int lr, int ngrou
         y1 = y1 + a1;
         y2 = y2 + a2;
       }
-      a0 = a1 = a2 = 0.0;
+      a0 = a1 = a2 = 0;
       ++cg;
     }
-    const double* v = A.vals + vidx(at, lr & 31, 0);
-    const double v0 = __ldg(v), v1 = __ldg(v + 32), v2 = __ldg(v + 64);
-    const double v3 = __ldg(v + 96), v4 = __ldg(v + 128), v5 = __ldg(v + 160);
-    const double v6 = __ldg(v + 192), v7 = __ldg(v + 224), v8 = __ldg(v + 256);
-    double x0, x1, x2;
-    gather3<PMode, kRemote, kCg>(c, g, x, pold, beta, cv, pm, vexp, seen, x0, x1, x2);
+    const T* v = vals + vidx(at, lr & 31, 0);
+    const T v0 = __ldg(v), v1 = __ldg(v + 32), v2 = __ldg(v + 64);
+    const T v3 = __ldg(v + 96), v4 = __ldg(v + 128), v5 = __ldg(v + 160);
+    const T v6 = __ldg(v + 192), v7 = __ldg(v + 224), v8 = __ldg(v + 256);
+    T x0, x1, x2;
+    gather3<PMode, kRemote, kCg, T>(c, g, x, pold, beta, cv, pm, vexp, seen, x0, x1, x2);
     a0 = a0 + ((v0 * x0 + v1 * x1) + v2 * x2);
     a1 = a1 + ((v3 * x0 + v4 * x1) + v5 * x2);
     a2 = a2 + ((v6 * x0 + v7 * x1) + v8 * x2);
@@ -385,15 +402,20 @@ __global__ void __launch_bounds__(256) k_spmv_pair(SellView A, const double* __r
   }
 }
 
-__global__ void __launch_bounds__(256) k_spmv(SellView A, int ngroups, const double* __restrict__ x,
-                                              double* __restrict__ y, CommView cv, PartMap pm) {
+template <class T = double>
+__global__ void __launch_bounds__(256) k_spmv(SellView A, int ngroups, const T* __restrict__ x,
+                                              T* __restrict__ y, CommView cv, PartMap pm) {
   const int m = blockIdx.x * blockDim.x + threadIdx.x;
   if (m >= A.rows) return;
   const int r = A.row0 + A.perm[m];
-  double y0, y1, y2;
-  if (ngroups == 1) row_product_1<0>(A, m, x, nullptr, 0.0, y0, y1, y2);
-  else if (cv.world > 1) row_product<0, true>(A, m, ngroups, x, nullptr, 0.0, y0, y1, y2, cv, pm, cv.seq[0]);
-  else row_product<0>(A, m, ngroups, x, nullptr, 0.0, y0, y1, y2);
+  T y0, y1, y2;
+  if constexpr (std::is_same_v<T, float>) {  // Precision::Single: one rank
+    row_product<0, false, false, float>(A, m, ngroups, x, nullptr, 0.0, y0, y1, y2);
+  } else {
+    if (ngroups == 1) row_product_1<0>(A, m, x, nullptr, 0.0, y0, y1, y2);
+    else if (cv.world > 1) row_product<0, true, false, double>(A, m, ngroups, x, nullptr, 0.0, y0, y1, y2, cv, pm, cv.seq[0]);
+    else row_product<0, false, false, double>(A, m, ngroups, x, nullptr, 0.0, y0, y1, y2);
+  }
   y[3 * r] = y0;
   y[3 * r + 1] = y1;
   y[3 * r + 2] = y2;
@@ -468,8 +490,16 @@ void rank_barrier(Ctx& c) {
   WG_CUDA(cudaGetLastError());
 }
 
+void spmv_f32(Ctx& c, const float* x_dev, float* y_dev) {
+  if (!c.has_matrix || !c.A.f32) throw Error(WEFT_ERR_INVALID, "spmv: no single-precision matrix loaded");
+  if (c.A.rows == 0) return;
+  k_spmv<float><<<div_up(c.A.rows, 256), 256, 0, ls(c)>>>(view(c.A), c.go.n, x_dev, y_dev, c.comm, c.pm);
+  WG_CUDA(cudaGetLastError());
+}
+
 void spmv(Ctx& c, const double* x_dev, double* y_dev) {
   if (!c.has_matrix) throw Error(WEFT_ERR_INVALID, "spmv: no matrix loaded");
+  if (c.A.f32) throw Error(WEFT_ERR_INVALID, "spmv: single-precision system (use the f32 entry)");
   const int threads = 256;
   if (c.A.rows == 0) return;
   if (c.go.n == 1 && c.spmv_pair) k_spmv_pair<<<div_up(c.A.rows, threads / 2), threads, 0, ls(c)>>>(view(c.A), x_dev, y_dev);
@@ -543,6 +573,7 @@ void build_sigma(Ctx& c, const int32_t* len_row) {
 // Takes the GLOBAL block CSR (every rank passes the same matrix) and keeps
 // this rank's rows [row0, row1) (partition_matrix, sparse.hpp:103-147).
 void set_matrix_csr(Ctx& c, int rows, const int64_t* row_ptr, const int32_t* cols, const double* vals) {
+  c.A.f32 = false;
   if (rows < 0) throw Error(WEFT_ERR_DIMENSION, "set_matrix: negative row count");
   if (rows >= (1 << 28)) throw Error(WEFT_ERR_DIMENSION, "set_matrix: more than 2^28 block rows");
   if (rows < c.nparts) throw Error(WEFT_ERR_DIMENSION, "set_matrix: fewer rows than partitions");
@@ -628,7 +659,8 @@ void set_matrix_csr(Ctx& c, int rows, const int64_t* row_ptr, const int32_t* col
 
 // This rank's rows [row0, row1) as block CSR with ascending columns
 // (gather_matrix, sparse.hpp:149-173; all rows when world == 1).
-void download_csr(Ctx& c, int64_t* row_ptr, int32_t* cols, double* vals) {
+template <class T>
+static void download_csr_t(Ctx& c, int64_t* row_ptr, int32_t* cols, T* vals) {
   SellMatrix& A = c.A;
   std::vector<int64_t> soff(A.slice_off.size());
   std::vector<int32_t> len(static_cast<size_t>(A.rows));
@@ -638,10 +670,11 @@ void download_csr(Ctx& c, int64_t* row_ptr, int32_t* cols, double* vals) {
   A.rowlen.download(len.data(), len.size(), c.stream);
   A.pos.download(pos.data(), pos.size(), c.stream);
   A.cols.download(hc.data(), hc.size(), c.stream);
-  std::vector<double> hv;
+  std::vector<T> hv;
   if (vals) {
     hv.resize(9 * static_cast<size_t>(A.total));
-    A.vals.download(hv.data(), hv.size(), c.stream);
+    if constexpr (std::is_same_v<T, float>) A.vals32.download(hv.data(), hv.size(), c.stream);
+    else A.vals.download(hv.data(), hv.size(), c.stream);
   }
   WG_CUDA(cudaStreamSynchronize(c.stream));
   int64_t cursor = 0;
@@ -664,6 +697,15 @@ void download_csr(Ctx& c, int64_t* row_ptr, int32_t* cols, double* vals) {
     }
     if (row_ptr) row_ptr[r + 1] = cursor;
   }
+}
+
+void download_csr(Ctx& c, int64_t* row_ptr, int32_t* cols, double* vals) {
+  if (c.A.f32 && vals) throw Error(WEFT_ERR_INVALID, "download_matrix: single-precision system (use the f32 entry)");
+  download_csr_t<double>(c, row_ptr, cols, vals);
+}
+void download_csr_f32(Ctx& c, int64_t* row_ptr, int32_t* cols, float* vals) {
+  if (!c.A.f32 && vals) throw Error(WEFT_ERR_INVALID, "download_matrix: double-precision system");
+  download_csr_t<float>(c, row_ptr, cols, vals);
 }
 
 // ---------------------------------------------------------------------------
@@ -756,17 +798,21 @@ __device__ __forceinline__ int block_row(const PartBlocks& pb, int b, int& rend)
 }
 
 // dot(u, v) per partition + ascending sum into *out (used for ||b||, rho0).
-__global__ void __launch_bounds__(256) k_dot2(PartBlocks pb, const double* __restrict__ u, const double* __restrict__ v,
-                                              const double* __restrict__ u2, const double* __restrict__ v2,
+// Products of Real values taken in double (solver.hpp:91-100).
+template <class T = double>
+__global__ void __launch_bounds__(256) k_dot2(PartBlocks pb, const T* __restrict__ u, const T* __restrict__ v,
+                                              const T* __restrict__ u2, const T* __restrict__ v2,
                                               double* partials, unsigned* counter, double* out, CommView cv,
                                               int ntot) {
   __shared__ double smem[2 * 32];
   int rend;
   const int r = block_row(pb, blockIdx.x, rend);
   double s[2] = {0.0, 0.0};
+  auto d = [](T a) { return static_cast<double>(a); };
   if (r < rend) {
-    s[0] = (u[3 * r] * v[3 * r] + u[3 * r + 1] * v[3 * r + 1]) + u[3 * r + 2] * v[3 * r + 2];
-    if (u2) s[1] = (u2[3 * r] * v2[3 * r] + u2[3 * r + 1] * v2[3 * r + 1]) + u2[3 * r + 2] * v2[3 * r + 2];
+    s[0] = (d(u[3 * r]) * d(v[3 * r]) + d(u[3 * r + 1]) * d(v[3 * r + 1])) + d(u[3 * r + 2]) * d(v[3 * r + 2]);
+    if (u2)
+      s[1] = (d(u2[3 * r]) * d(v2[3 * r]) + d(u2[3 * r + 1]) * d(v2[3 * r + 1])) + d(u2[3 * r + 2]) * d(v2[3 * r + 2]);
   }
   block_sum<2>(s, smem);
   if (threadIdx.x == 0) {
@@ -789,7 +835,7 @@ __global__ void __launch_bounds__(256) k_dot2(PartBlocks pb, const double* __res
 // kPosOut (persistent solve): position order, plus the packed upper
 // triangle d6 (6 doubles) and *asym = 1 if any inverse is not bitwise
 // symmetric (then the solve reads the 9-double form).
-template <bool kPosOut>
+template <bool kPosOut, class T = double>
 __global__ void k_dinv(SellView A, double* __restrict__ dinv, double* __restrict__ d6 = nullptr,
                        int* __restrict__ asym = nullptr) {
   const int mp = blockIdx.x * blockDim.x + threadIdx.x;
@@ -801,7 +847,7 @@ __global__ void k_dinv(SellView A, double* __restrict__ dinv, double* __restrict
   for (int k = 0; k < len; ++k) {
     const int64_t at = base + (int64_t)k * kSlice;
     if ((A.cols[at] & kColMask) == r) {
-      for (int q = 0; q < 9; ++q) m[q] = A.vals[vidx(at, mp & 31, q)];
+      for (int q = 0; q < 9; ++q) m[q] = static_cast<double>(sell_vals<T>(A)[vidx(at, mp & 31, q)]);
       break;
     }
   }
@@ -840,8 +886,10 @@ __global__ void k_dinv(SellView A, double* __restrict__ dinv, double* __restrict
 }
 
 // apply_precond (solver.hpp:67-89): acc = 0; acc += m(i,j) * src[j].
-__device__ __forceinline__ void precond_row(const double* __restrict__ dinv, bool bj, int r, double r0, double r1,
-                                            double r2, double& z0, double& z1, double& z2) {
+// acc in double, the result cast to Real (solver.hpp:80-86).
+template <class T = double>
+__device__ __forceinline__ void precond_row(const double* __restrict__ dinv, bool bj, int r, T r0, T r1, T r2,
+                                            T& z0, T& z1, T& z2) {
   if (!bj) {
     z0 = r0;
     z1 = r1;
@@ -849,30 +897,32 @@ __device__ __forceinline__ void precond_row(const double* __restrict__ dinv, boo
     return;
   }
   const double* m = dinv + 9 * (size_t)r;
-  z0 = ((0.0 + m[0] * r0) + m[1] * r1) + m[2] * r2;
-  z1 = ((0.0 + m[3] * r0) + m[4] * r1) + m[5] * r2;
-  z2 = ((0.0 + m[6] * r0) + m[7] * r1) + m[8] * r2;
+  const double d0 = r0, d1 = r1, d2 = r2;
+  z0 = static_cast<T>(((0.0 + m[0] * d0) + m[1] * d1) + m[2] * d2);
+  z1 = static_cast<T>(((0.0 + m[3] * d0) + m[4] * d1) + m[5] * d2);
+  z2 = static_cast<T>(((0.0 + m[6] * d0) + m[7] * d1) + m[8] * d2);
 }
 
 // PCG init over the held rows: x = 0, r = b, z = M^-1 r (p = z is formed by
 // the first SpMV).
-__global__ void k_pcg_init(int row0, int rows, const double* __restrict__ b, const double* __restrict__ dinv,
-                           bool bj, double* __restrict__ x, double* __restrict__ r, double* __restrict__ z,
-                           double* __restrict__ p) {
+template <class T = double>
+__global__ void k_pcg_init(int row0, int rows, const T* __restrict__ b, const double* __restrict__ dinv,
+                           bool bj, T* __restrict__ x, T* __restrict__ r, T* __restrict__ z,
+                           T* __restrict__ p) {
   const int lr = blockIdx.x * blockDim.x + threadIdx.x;
   if (lr >= rows) return;
   const int i = row0 + lr;
-  const double b0 = b[3 * i], b1 = b[3 * i + 1], b2 = b[3 * i + 2];
-  double z0, z1, z2;
-  precond_row(dinv, bj, i, b0, b1, b2, z0, z1, z2);
-  x[3 * i] = x[3 * i + 1] = x[3 * i + 2] = 0.0;
+  const T b0 = b[3 * i], b1 = b[3 * i + 1], b2 = b[3 * i + 2];
+  T z0, z1, z2;
+  precond_row<T>(dinv, bj, i, b0, b1, b2, z0, z1, z2);
+  x[3 * i] = x[3 * i + 1] = x[3 * i + 2] = 0;
   r[3 * i] = b0;
   r[3 * i + 1] = b1;
   r[3 * i + 2] = b2;
   z[3 * i] = z0;
   z[3 * i + 1] = z1;
   z[3 * i + 2] = z2;
-  p[3 * i] = p[3 * i + 1] = p[3 * i + 2] = 0.0;
+  p[3 * i] = p[3 * i + 1] = p[3 * i + 2] = 0;
 }
 
 // Per-solve arguments, read by the iteration kernels through one device
@@ -1150,7 +1200,7 @@ __device__ void combine_split(const CommView& cv, int d0, int nloc, int ntot, co
     for (int i = 0; i < NV; ++i) out[i] = out[i] + __ldcg(&me->red[par][d][i]);
 }
 
-template <bool kRemote>
+template <bool kRemote, class T = double>
 __global__ void __launch_bounds__(256, 2) k_pcg_persistent_rows(const PcgArgs* __restrict__ args, PcgState* st) {
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
@@ -1160,11 +1210,13 @@ __global__ void __launch_bounds__(256, 2) k_pcg_persistent_rows(const PcgArgs* _
   const SellView A = g.A;
   const PartBlocks& pb = g.pb;
   const int nvb = pb.bstart[pb.n];  // virtual blocks (256 rows of one partition)
-  double* __restrict__ x = g.x;
-  double* __restrict__ r = g.r;
-  double* __restrict__ z = g.z;
-  double* __restrict__ p = g.p;
-  double* __restrict__ q = g.q;
+  // T = float: Precision::Single — Real vectors and matrix, double scalars
+  // and dot products, alpha / beta cast to Real in the updates (solver.hpp)
+  T* __restrict__ x = reinterpret_cast<T*>(g.x);
+  T* __restrict__ r = reinterpret_cast<T*>(g.r);
+  T* __restrict__ z = reinterpret_cast<T*>(g.z);
+  T* __restrict__ p = reinterpret_cast<T*>(g.p);
+  T* __restrict__ q = reinterpret_cast<T*>(g.q);
   const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
   const CommView cv = g.cv;
   unsigned long long vseq = kRemote ? cv.seq[0] : 0;  // z / p publications seen so far
@@ -1186,19 +1238,21 @@ __global__ void __launch_bounds__(256, 2) k_pcg_persistent_rows(const PcgArgs* _
       if (mg < rend) {
         const int m = mg - A.row0;
         const int row = A.row0 + A.perm[m];
-        double y0, y1, y2;
-        if (first) row_product<1, kRemote, true>(A, m, g.ngroups, z, p, beta, y0, y1, y2, cv, g.pm, vseq);
-        else row_product<2, kRemote, true>(A, m, g.ngroups, z, p, beta, y0, y1, y2, cv, g.pm, vseq);
+        T y0, y1, y2;
+        if (first) row_product<1, kRemote, true, T>(A, m, g.ngroups, z, p, beta, y0, y1, y2, cv, g.pm, vseq);
+        else row_product<2, kRemote, true, T>(A, m, g.ngroups, z, p, beta, y0, y1, y2, cv, g.pm, vseq);
         __stcg(q + 3 * row, y0);
         __stcg(q + 3 * row + 1, y1);
         __stcg(q + 3 * row + 2, y2);
-        double p0 = __ldcg(z + 3 * row), p1 = __ldcg(z + 3 * row + 1), p2 = __ldcg(z + 3 * row + 2);
+        T p0 = __ldcg(z + 3 * row), p1 = __ldcg(z + 3 * row + 1), p2 = __ldcg(z + 3 * row + 2);
         if (!first) {
-          p0 = p0 + beta * __ldcg(p + 3 * row);
-          p1 = p1 + beta * __ldcg(p + 3 * row + 1);
-          p2 = p2 + beta * __ldcg(p + 3 * row + 2);
+          const T bt = static_cast<T>(beta);
+          p0 = p0 + bt * __ldcg(p + 3 * row);
+          p1 = p1 + bt * __ldcg(p + 3 * row + 1);
+          p2 = p2 + bt * __ldcg(p + 3 * row + 2);
         }
-        s1[0] = (p0 * y0 + p1 * y1) + p2 * y2;
+        const double dp0 = p0, dp1 = p1, dp2 = p2, dy0 = y0, dy1 = y1, dy2 = y2;
+        s1[0] = (dp0 * dy0 + dp1 * dy1) + dp2 * dy2;
       }
       block_sum<1>(s1, smem);
       if (threadIdx.x == 0) __stcg(g.partials + vb, s1[0]);
@@ -1234,11 +1288,12 @@ __global__ void __launch_bounds__(256, 2) k_pcg_persistent_rows(const PcgArgs* _
       const int i = block_row(pb, vb, rend);
       double s2[2] = {0.0, 0.0};
       if (i < rend) {
-        double zv[3], pv[3], xv[3], rv[3], qv[3], m[9];
+        T zv[3], pv[3], xv[3], rv[3], qv[3];
+        double m[9];
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
           zv[c] = __ldcg(z + 3 * i + c);
-          pv[c] = first ? 0.0 : __ldcg(p + 3 * i + c);
+          pv[c] = first ? T(0) : __ldcg(p + 3 * i + c);
           xv[c] = __ldcg(x + 3 * i + c);
           rv[c] = __ldcg(r + 3 * i + c);
           qv[c] = __ldcg(q + 3 * i + c);
@@ -1247,18 +1302,20 @@ __global__ void __launch_bounds__(256, 2) k_pcg_persistent_rows(const PcgArgs* _
 #pragma unroll
           for (int k = 0; k < 9; ++k) m[k] = __ldg(g.dinv + 9 * (size_t)i + k);
         }
-        double pr[3], rr[3];
+        T pr[3], rr[3];
+        const T at = static_cast<T>(alpha), bt = static_cast<T>(beta);
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-          pr[c] = first ? zv[c] : zv[c] + beta * pv[c];
-          xv[c] = xv[c] + alpha * pr[c];
-          rr[c] = rv[c] - alpha * qv[c];
+          pr[c] = first ? zv[c] : zv[c] + bt * pv[c];
+          xv[c] = xv[c] + at * pr[c];
+          rr[c] = rv[c] - at * qv[c];
         }
-        double z0, z1, z2;
-        if (g.bj) {  // apply_precond (solver.hpp:67-89)
-          z0 = ((0.0 + m[0] * rr[0]) + m[1] * rr[1]) + m[2] * rr[2];
-          z1 = ((0.0 + m[3] * rr[0]) + m[4] * rr[1]) + m[5] * rr[2];
-          z2 = ((0.0 + m[6] * rr[0]) + m[7] * rr[1]) + m[8] * rr[2];
+        T z0, z1, z2;
+        if (g.bj) {  // apply_precond (solver.hpp:67-89): double acc, cast to Real
+          const double d0 = rr[0], d1 = rr[1], d2 = rr[2];
+          z0 = static_cast<T>(((0.0 + m[0] * d0) + m[1] * d1) + m[2] * d2);
+          z1 = static_cast<T>(((0.0 + m[3] * d0) + m[4] * d1) + m[5] * d2);
+          z2 = static_cast<T>(((0.0 + m[6] * d0) + m[7] * d1) + m[8] * d2);
         } else {
           z0 = rr[0];
           z1 = rr[1];
@@ -1273,8 +1330,9 @@ __global__ void __launch_bounds__(256, 2) k_pcg_persistent_rows(const PcgArgs* _
         __stcg(z + 3 * i, z0);
         __stcg(z + 3 * i + 1, z1);
         __stcg(z + 3 * i + 2, z2);
-        s2[0] = (rr[0] * rr[0] + rr[1] * rr[1]) + rr[2] * rr[2];
-        s2[1] = (rr[0] * z0 + rr[1] * z1) + rr[2] * z2;
+        const double e0 = rr[0], e1 = rr[1], e2 = rr[2], f0 = z0, f1 = z1, f2 = z2;
+        s2[0] = (e0 * e0 + e1 * e1) + e2 * e2;
+        s2[1] = (e0 * f0 + e1 * f1) + e2 * f2;
       }
       block_sum<2>(s2, smem);
       if (threadIdx.x == 0) {
@@ -1856,6 +1914,7 @@ void pcg_free(Ctx& c) {
 PcgResult pcg_solve(Ctx& c, const double* b_dev, const weft_pcg_config& cfg, double* hist_host,
                     double* phist_host) {
   if (!c.has_matrix) throw Error(WEFT_ERR_INVALID, "pcg: no matrix");
+  if (c.A.f32) throw Error(WEFT_ERR_INVALID, "pcg: single-precision system (use the f32 entry)");
   comm_need(c, "pcg");
   const int rows = c.A.rows;                               // held rows
   const size_t len = 3 * static_cast<size_t>(c.pm.p);      // vectors: global row index
@@ -2225,6 +2284,123 @@ PcgResult pcg_solve(Ctx& c, const double* b_dev, const weft_pcg_config& cfg, dou
     WG_CUDA(cudaMemcpyAsync(phist_host, c.phist.data(), sizeof(double) * res.iterations, cudaMemcpyDeviceToHost, s));
   WG_CUDA(cudaStreamSynchronize(s));
   return res;
+}
+
+
+// pcg_solve<float> (solver.hpp:36-178 with Real = float): the rows solver in
+// single precision (one rank; any partition count) — float vectors and
+// matrix, double dots, double block-Jacobi inverses of the float diagonal
+// blocks, alpha / beta cast to float in the updates.
+PcgResult pcg_solve_f32(Ctx& c, const float* b_dev, const weft_pcg_config& cfg, double* hist_host,
+                        double* phist_host) {
+  if (!c.has_matrix || !c.A.f32) throw Error(WEFT_ERR_INVALID, "pcg: no single-precision matrix");
+  if (c.world > 1) throw Error(WEFT_ERR_INVALID, "pcg: Precision::Single runs on one rank");
+  const int rows = c.A.rows;
+  const size_t len = 3 * static_cast<size_t>(c.pm.p);
+  const int threads = 256;
+  if (!c.pcg) {
+    WG_CUDA(cudaMalloc(&c.pcg, sizeof(PcgState)));
+    WG_CUDA(cudaHostAlloc(&c.pcg_host, sizeof(PcgState), cudaHostAllocDefault));
+  }
+  for (auto* v : {&c.r, &c.z, &c.pv, &c.q, &c.xs}) v->resize(len);  // float views of these
+  auto f = [](DBuf<double>& d) { return reinterpret_cast<float*>(d.data()); };
+  const bool bj = cfg.preconditioner == WEFT_PRECOND_BLOCK_JACOBI;
+  c.dinv.resize(9 * static_cast<size_t>(c.pm.p) + 9);
+  const int max_it = std::max(cfg.max_iterations, 0);
+  c.hist.resize(static_cast<size_t>(max_it) + 1);
+  c.phist.resize(static_cast<size_t>(max_it) + 1);
+  const PartBlocks pb = part_blocks(c, threads);
+  const int nblocks = pb.bstart[pb.n];
+  c.partials.resize(4 * static_cast<size_t>(nblocks) + 4);
+  const SellView A = view(c.A);
+  cudaStream_t s = c.stream;
+  PcgState init{};
+  init.max_iter = max_it;
+  init.first = 1;
+  WG_CUDA(cudaMemcpyAsync(c.pcg, &init, sizeof(init), cudaMemcpyHostToDevice, s));
+  double* dots = reinterpret_cast<double*>(c.scalars.data());
+  if (rows > 0) {
+    if (bj) k_dinv<false, float><<<div_up(rows, threads), threads, 0, ls(c)>>>(A, c.dinv.data());
+    k_pcg_init<float><<<div_up(rows, threads), threads, 0, ls(c)>>>(c.row0, rows, b_dev, c.dinv.data(), bj, f(c.xs),
+                                                                    f(c.r), f(c.z), f(c.pv));
+    k_dot2<float><<<nblocks, threads, 0, ls(c)>>>(pb, b_dev, b_dev, f(c.r), f(c.z), c.partials.data(),
+                                                  &c.pcg->counter, dots, c.comm, c.nparts);
+    WG_CUDA(cudaGetLastError());
+  }
+  double hd[2] = {0.0, 0.0};
+  if (rows > 0) WG_CUDA(cudaMemcpyAsync(hd, dots, sizeof(hd), cudaMemcpyDeviceToHost, s));
+  WG_CUDA(cudaStreamSynchronize(s));
+  PcgResult res;
+  const double b_norm = std::sqrt(hd[0]);
+  if (b_norm == 0.0) {
+    res.converged = 1;
+    return res;
+  }
+  init.b_norm = b_norm;
+  init.tol = cfg.rel_tolerance * b_norm;
+  init.rho = hd[1];
+  init.r_norm = b_norm;
+  init.done = max_it == 0 ? 1 : 0;
+  WG_CUDA(cudaMemcpyAsync(c.pcg, &init, sizeof(init), cudaMemcpyHostToDevice, s));
+  PcgArgs args{A, pb, pb, c.go.n, bj ? 1 : 0, c.dinv.data(), c.xs.data(), c.r.data(), c.z.data(), c.pv.data(),
+               c.q.data(), c.partials.data(), c.hist.data(), c.phist.data(), c.comm, c.pm, nullptr};
+  c.pcg_args.resize(sizeof(PcgArgs));
+  const PcgArgs* dargs = reinterpret_cast<const PcgArgs*>(c.pcg_args.data());
+  WG_CUDA(cudaMemcpyAsync(c.pcg_args.data(), &args, sizeof(args), cudaMemcpyHostToDevice, s));
+  auto k = k_pcg_persistent_rows<false, float>;
+  int sms = 0, occ = 0;
+  WG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device));
+  WG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, threads, 0));
+  const int grid = std::max(1, std::min(std::max(1, occ) * sms, nblocks));
+  void* kargs[] = {(void*)&dargs, (void*)&c.pcg};
+  WG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k), dim3(grid), dim3(threads), kargs, 0, s));
+  ++c.launches;
+  auto* hs = static_cast<PcgState*>(c.pcg_host);
+  WG_CUDA(cudaMemcpyAsync(hs, c.pcg, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
+  WG_CUDA(cudaStreamSynchronize(s));
+  res.iterations = hs->iter;
+  res.converged = hs->converged;
+  res.rel_residual = hs->r_norm / b_norm;
+  if (hs->status == 1)
+    throw Error(WEFT_ERR_SOLVER, "pcg: non-finite curvature at iteration " + std::to_string(hs->iter));
+  if (hs->status == 2)
+    throw Error(WEFT_ERR_SOLVER,
+                "pcg: non-positive curvature at iteration " + std::to_string(hs->iter) + " (matrix not SPD)");
+  if (hs->status == 3)
+    throw Error(WEFT_ERR_SOLVER,
+                "pcg: divergence (non-finite residual) at iteration " + std::to_string(hs->iter));
+  log_line(c, "event=pcg iterations=" + std::to_string(res.iterations) + " rel_residual=" + fmt_g(res.rel_residual) +
+                  " converged=" + std::to_string(res.converged ? 1 : 0));
+  if (hist_host && res.iterations)
+    WG_CUDA(cudaMemcpyAsync(hist_host, c.hist.data(), sizeof(double) * res.iterations, cudaMemcpyDeviceToHost, s));
+  if (phist_host && res.iterations)
+    WG_CUDA(cudaMemcpyAsync(phist_host, c.phist.data(), sizeof(double) * res.iterations, cudaMemcpyDeviceToHost, s));
+  WG_CUDA(cudaStreamSynchronize(s));
+  return res;
+}
+
+// Single-precision systems from a block CSR (values exact in float): the
+// double layout is built, then its values are narrowed once on the device.
+__global__ void k_narrow_vals(int64_t n, const double* __restrict__ in, float* __restrict__ out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) out[i] = static_cast<float>(in[i]);
+}
+
+void set_matrix_csr_f32(Ctx& c, int rows, const int64_t* row_ptr, const int32_t* cols, const float* vals) {
+  const int64_t nnz = rows > 0 ? row_ptr[rows] : 0;
+  std::vector<double> vd(9 * static_cast<size_t>(nnz));
+  for (size_t i = 0; i < vd.size(); ++i) vd[i] = vals[i];
+  set_matrix_csr(c, rows, row_ptr, cols, vd.data());
+  narrow_to_f32(c);
+}
+
+void narrow_to_f32(Ctx& c) {
+  SellMatrix& A = c.A;
+  const int64_t n = 9 * A.total;
+  A.vals32.resize(static_cast<size_t>(n) + 9);
+  if (n) k_narrow_vals<<<div_up(n, 256), 256, 0, ls(c)>>>(n, A.vals.data(), A.vals32.data());
+  WG_CUDA(cudaGetLastError());
+  A.f32 = true;
 }
 
 }  // namespace weft_gpu

@@ -383,13 +383,29 @@ class Engine:
 
     # -- sparse -------------------------------------------------------------
     def set_matrix(self, m: BlockCsr):
-        _check(LIB.weft_gpu_set_matrix(self._ctx, C.c_int32(m.rows), _ptr(np.ascontiguousarray(m.row_ptr, np.int64)),
-                                       _ptr(np.ascontiguousarray(m.cols, np.int32)), _ptr(_f64(m.vals))))
+        """float32 values: a Precision::Single system (BellMatrix<float>);
+        spmv_pipelined / pcg_solve then take and return float32 vectors."""
+        rp = _ptr(np.ascontiguousarray(m.row_ptr, np.int64))
+        cl = _ptr(np.ascontiguousarray(m.cols, np.int32))
+        if np.asarray(m.vals).dtype == np.float32:
+            v32 = np.ascontiguousarray(m.vals, np.float32)
+            _check(LIB.weft_gpu_set_matrix_f32(self._ctx, C.c_int32(m.rows), rp, cl, _ptr(v32)))
+            self._f32 = True
+        else:
+            _check(LIB.weft_gpu_set_matrix(self._ctx, C.c_int32(m.rows), rp, cl, _ptr(_f64(m.vals))))
+            self._f32 = False
 
     def spmv_pipelined(self, m: BlockCsr | None, x) -> np.ndarray:
         if m is not None:
             self.set_matrix(m)
         rows = self.rank_info().global_rows
+        if getattr(self, "_f32", False):
+            x = np.ascontiguousarray(x, np.float32)
+            if len(x) != 3 * rows:
+                raise DimensionError("spmv_pipelined: dim(x) != rows")
+            y = np.zeros(3 * rows, np.float32)
+            _check(LIB.weft_gpu_spmv_f32(self._ctx, _ptr(x), _ptr(y)))
+            return y
         x = _f64(x)
         if len(x) != 3 * rows:
             raise DimensionError("spmv_pipelined: dim(x) != rows")
@@ -406,8 +422,12 @@ class Engine:
         info = self.matrix_info()
         rp = np.zeros(info.block_rows + 1, np.int64)
         cols = np.zeros(max(info.nnzb, 1), np.int32)
-        vals = np.zeros(max(info.nnzb, 1) * 9)
-        _check(LIB.weft_gpu_download_matrix(self._ctx, _ptr(rp), _ptr(cols), _ptr(vals)))
+        if getattr(self, "_f32", False):
+            vals = np.zeros(max(info.nnzb, 1) * 9, np.float32)
+            _check(LIB.weft_gpu_download_matrix_f32(self._ctx, _ptr(rp), _ptr(cols), _ptr(vals)))
+        else:
+            vals = np.zeros(max(info.nnzb, 1) * 9)
+            _check(LIB.weft_gpu_download_matrix(self._ctx, _ptr(rp), _ptr(cols), _ptr(vals)))
         return BlockCsr(info.block_rows, rp, cols[: info.nnzb], vals[: 9 * info.nnzb].reshape(-1, 9))
 
     def download_rhs(self) -> np.ndarray:
@@ -423,13 +443,18 @@ class Engine:
             self.set_matrix(m)
         config = config or PcgConfig()
         n = 3 * self.rank_info().global_rows
-        x = np.zeros(n)
+        f32 = getattr(self, "_f32", False)
+        x = np.zeros(n, np.float32 if f32 else np.float64)
         hist = np.zeros(max(config.max_iterations, 1))
         phist = np.zeros(max(config.max_iterations, 1))
         rep = _PcgReport(0, 0, 0.0, hist.ctypes.data_as(C.POINTER(C.c_double)),
                          phist.ctypes.data_as(C.POINTER(C.c_double)))
-        bb = None if b is None else _f64(b)
-        _check(LIB.weft_gpu_pcg(self._ctx, _ptr(bb), _ptr(x), C.byref(config), C.byref(rep)))
+        if f32:
+            bb = None if b is None else np.ascontiguousarray(b, np.float32)
+            _check(LIB.weft_gpu_pcg_f32(self._ctx, _ptr(bb), _ptr(x), C.byref(config), C.byref(rep)))
+        else:
+            bb = None if b is None else _f64(b)
+            _check(LIB.weft_gpu_pcg(self._ctx, _ptr(bb), _ptr(x), C.byref(config), C.byref(rep)))
         return x, PcgReport(rep.iterations, rep.rel_residual, bool(rep.converged), hist[: rep.iterations].copy(),
                             phist[: rep.iterations].copy())
 

@@ -283,6 +283,31 @@ class Ref:
             raise RuntimeError(self.lib.ref_last_error().decode())
         return y
 
+    def spmv_f32(self, s: System, x, n=1):
+        """spmv_pipelined<float> (Precision::Single); s.vals as float32."""
+        y = np.zeros(3 * s.rows, np.float32)
+        st = self.lib.ref_spmv_f32(C.c_int32(s.rows), ptr(s.row_ptr), ptr(s.cols),
+                                   ptr(np.ascontiguousarray(s.vals, np.float32)), C.c_int32(n),
+                                   ptr(np.ascontiguousarray(x, np.float32)), ptr(y))
+        if st:
+            raise RuntimeError(self.lib.ref_last_error().decode())
+        return y
+
+    def pcg_f32(self, s: System, b, n=1, tol=1e-4, max_it=400, precond=PRECOND_BJ):
+        """pcg_solve<float> (Precision::Single)."""
+        x = np.zeros(3 * s.rows, np.float32)
+        hist = np.zeros(max(max_it, 1))
+        phist = np.zeros(max(max_it, 1))
+        cfg = PcgConfig(tol, max_it, precond)
+        rep = PcgReport(0, 0, 0.0, hist.ctypes.data_as(C.POINTER(C.c_double)), phist.ctypes.data_as(C.POINTER(C.c_double)))
+        st = self.lib.ref_pcg_f32(C.c_int32(s.rows), ptr(s.row_ptr), ptr(s.cols),
+                                  ptr(np.ascontiguousarray(s.vals, np.float32)), C.c_int32(n),
+                                  ptr(np.ascontiguousarray(b, np.float32)), ptr(x), C.byref(cfg), C.byref(rep))
+        if st:
+            raise RuntimeError(self.lib.ref_last_error().decode())
+        return x, dict(iterations=rep.iterations, converged=bool(rep.converged), rel_residual=rep.rel_residual,
+                       residual_history=hist[: rep.iterations].copy())
+
     def pcg(self, s: System, b, n=1, tol=1e-4, max_it=400, precond=PRECOND_BJ):
         x = np.zeros(3 * s.rows)
         hist = np.zeros(max(max_it, 1))
