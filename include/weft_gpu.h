@@ -214,6 +214,14 @@ weft_status weft_gpu_spmv_f32(weft_gpu_ctx* ctx, const float* x, float* y);
 weft_status weft_gpu_pcg_f32(weft_gpu_ctx* ctx, const float* b, float* x, const weft_pcg_config* config,
                              weft_pcg_report* report);
 weft_status weft_gpu_download_matrix_f32(weft_gpu_ctx* ctx, int64_t* row_ptr, int32_t* cols, float* vals);
+/* fill_matrix<float> / step_system<float> (assembly.hpp:74-220 and
+ * physics.hpp:44-69 with Real = float: each contribution computed in double,
+ * cast to float, added in float) and the float rhs. */
+weft_status weft_gpu_fill_matrix_f32(weft_gpu_ctx* ctx, const double* x_cur, const double* x_adv,
+                                     const double* velocity, double dt, int32_t jac_mode);
+weft_status weft_gpu_step_system_f32(weft_gpu_ctx* ctx, const double* x, const double* v, double dt,
+                                     int32_t jac_mode);
+weft_status weft_gpu_download_rhs_f32(weft_gpu_ctx* ctx, float* rhs);
 
 /* ---------------------------------------------------------------------- */
 /* Assembly (proj/include/weft/assembly.hpp:48-220, physics.hpp:44-69)    */
@@ -377,6 +385,11 @@ typedef struct weft_sim_params {
    * and the commit's velocity correction (:195-204): the full step_impl. */
   int32_t zones;
   weft_zone_params zone;
+  /* SimConfig::precision (driver.hpp:13,35): 0 = Precision::Double, 1 =
+   * Precision::Single — step_impl<float> (driver.cpp:92-94): the system
+   * assembled as AssembledSystem<float>, pcg_solve<float>, v += double(dv).
+   * One rank. */
+  int32_t precision;
 } weft_sim_params;
 
 typedef struct weft_step_report {

@@ -151,14 +151,15 @@ struct Csr {
   std::vector<double> rhs;
 };
 
-Csr from_bell(const BellMatrix<double>& a) {
+template <class Real = double>
+Csr from_bell(const BellMatrix<Real>& a) {
   Csr c;
   c.rows = a.block_rows();
   c.row_ptr.assign(static_cast<std::size_t>(c.rows) + 1, 0);
   for (int r = 0; r < c.rows; ++r) {
     for (int s = 0; s < a.ell_width(); ++s) {
       const int32_t col = a.col_at(r, s);
-      if (col == BellMatrix<double>::kNoBlock) break;
+      if (col == BellMatrix<Real>::kNoBlock) break;
       c.cols.push_back(col);
       for (int i = 0; i < 3; ++i)
         for (int j = 0; j < 3; ++j) c.vals.push_back(a.value_at(r, s, i, j));
@@ -268,9 +269,11 @@ extern "C" {
 const char* ref_last_error() { return g_err.c_str(); }
 
 // ---------------------------------------------------------------- systems
-void* ref_fill_matrix(int32_t p, int32_t n, int64_t n_elem, const weft_element* elems, const double* x_cur,
-                      const double* x_adv, const double* vel, const double* mass, const uint8_t* pinned,
-                      double dt, int32_t mode, int32_t* status) {
+}  // extern "C"
+template <class Real>
+void* ref_fill_matrix_t(int32_t p, int32_t n, int64_t n_elem, const weft_element* elems, const double* x_cur,
+                        const double* x_adv, const double* vel, const double* mass, const uint8_t* pinned,
+                        double dt, int32_t mode, int32_t* status) {
   try {
     std::vector<AssemblyElement> elements;
     elements.reserve(static_cast<std::size_t>(n_elem));
@@ -290,15 +293,28 @@ void* ref_fill_matrix(int32_t p, int32_t n, int64_t n_elem, const weft_element* 
     Engine engine(n);
     const auto parts = make_partitions(p, n);
     const auto dist = distribute_elements(elements, parts);
-    const auto sys = fill_matrix<double>(engine, dist, in, parts);
-    auto* out = new Csr(from_bell(gather_matrix(sys.matrix)));
-    out->rhs = sys.rhs.gather();
+    const auto sys = fill_matrix<Real>(engine, dist, in, parts);
+    auto* out = new Csr(from_bell<Real>(gather_matrix(sys.matrix)));  // float values exact in double
+    const auto rg = sys.rhs.gather();
+    out->rhs.assign(rg.begin(), rg.end());
     *status = 0;
     return out;
   } catch (const std::exception& e) {
     *status = set_error(e);
     return nullptr;
   }
+}
+extern "C" {
+void* ref_fill_matrix(int32_t p, int32_t n, int64_t n_elem, const weft_element* elems, const double* x_cur,
+                      const double* x_adv, const double* vel, const double* mass, const uint8_t* pinned,
+                      double dt, int32_t mode, int32_t* status) {
+  return ref_fill_matrix_t<double>(p, n, n_elem, elems, x_cur, x_adv, vel, mass, pinned, dt, mode, status);
+}
+// fill_matrix<float> (Precision::Single)
+void* ref_fill_matrix_f32(int32_t p, int32_t n, int64_t n_elem, const weft_element* elems, const double* x_cur,
+                          const double* x_adv, const double* vel, const double* mass, const uint8_t* pinned,
+                          double dt, int32_t mode, int32_t* status) {
+  return ref_fill_matrix_t<float>(p, n, n_elem, elems, x_cur, x_adv, vel, mass, pinned, dt, mode, status);
 }
 
 void ref_system_info(void* h, int32_t* rows, int64_t* nnzb) {

@@ -22,6 +22,8 @@
 //    partition count (test_assembly.cpp:263-280).
 #include <cub/cub.cuh>
 
+#include <type_traits>
+
 #include <algorithm>
 #include <cstring>
 #include <vector>
@@ -584,6 +586,8 @@ struct FillArgs {
   double* __restrict__ vals;
   int64_t total;
   double* __restrict__ rhs;
+  float* __restrict__ vals32;  // Precision::Single outputs (T = float)
+  float* __restrict__ rhs32;
   const double* __restrict__ mass;
   const uint8_t* __restrict__ pinned;
   const int64_t* __restrict__ inc_ptr;
@@ -601,21 +605,26 @@ struct FillArgs {
 };
 
 // Accumulator access: shared (Wide = false) or the output planes directly.
-template <bool Wide>
+// T = float: Precision::Single — each contribution cast to float and added
+// in float (BellMatrix<float>::add_value, assembly.hpp:212).
+template <bool Wide, class T = double>
 struct Acc {
-  double* sm;   // [wcap][9][blockDim] for this block
+  T* sm;   // [wcap][9][blockDim] for this block
   int tid, bs;
-  double* gv;   // output planes (Wide)
+  T* gv;   // output planes (Wide)
   int64_t total, base;
-  __device__ __forceinline__ double& at(int slot, int q) {
+  __device__ __forceinline__ T& at(int slot, int q) {
     if (Wide) return gv[vidx(base + (int64_t)slot * kSlice, tid & 31, q)];
     return sm[(slot * 9 + q) * bs + tid];
   }
 };
 
-template <bool Wide, bool Exact>
+template <bool Wide, bool Exact, class T = double>
 __global__ void __launch_bounds__(64) k_fill(FillArgs f) {
-  extern __shared__ double smem[];
+  extern __shared__ double smem_d[];
+  T* smem = reinterpret_cast<T*>(smem_d);
+  T* const vals = std::is_same_v<T, float> ? reinterpret_cast<T*>(f.vals32) : reinterpret_cast<T*>(f.vals);
+  T* const rhs = std::is_same_v<T, float> ? reinterpret_cast<T*>(f.rhs32) : reinterpret_cast<T*>(f.rhs);
   const int lr = blockIdx.x * blockDim.x + threadIdx.x;  // matrix position
   const int len = lr < f.p ? f.rowlen[lr] : 0;
   const bool mine = lr < f.p && (Wide ? len > f.wcap : len <= f.wcap);
@@ -623,7 +632,7 @@ __global__ void __launch_bounds__(64) k_fill(FillArgs f) {
   const int r = f.row0 + f.perm[lr];
   const int64_t base = f.slice_off[lr >> 5] + (lr & 31);
   int32_t* colbuf = reinterpret_cast<int32_t*>(smem + (size_t)f.wcap * 9 * blockDim.x);
-  Acc<Wide> acc{smem, (int)threadIdx.x, (int)blockDim.x, f.vals, f.total, base};
+  Acc<Wide, T> acc{smem, (int)threadIdx.x, (int)blockDim.x, vals, f.total, base};
   static_assert(kFillThreadsConst % 32 == 0, "row lanes must match threadIdx.x % 32");
   auto col_of = [&](int k) -> int {
     if (!Wide) return colbuf[k * blockDim.x + threadIdx.x];
@@ -632,7 +641,7 @@ __global__ void __launch_bounds__(64) k_fill(FillArgs f) {
   for (int k = 0; k < len; ++k) {
     if (!Wide) colbuf[k * blockDim.x + threadIdx.x] = f.cols[base + (int64_t)k * kSlice] & kColMask;
 #pragma unroll
-    for (int q = 0; q < 9; ++q) acc.at(k, q) = 0.0;
+    for (int q = 0; q < 9; ++q) acc.at(k, q) = 0;
   }
   auto find = [&](int col) -> int {
     for (int k = 0; k < len; ++k)
@@ -645,12 +654,12 @@ __global__ void __launch_bounds__(64) k_fill(FillArgs f) {
   if (!pin && m <= 0.0) atomicMin(f.bad_mass, r);
   {
     const int ds = find(r);
-    const double mv = pin ? 1.0 : m;
+    const T mv = pin ? T(1) : static_cast<T>(m);
     acc.at(ds, 0) = acc.at(ds, 0) + mv;
     acc.at(ds, 4) = acc.at(ds, 4) + mv;
     acc.at(ds, 8) = acc.at(ds, 8) + mv;
   }
-  double r0 = 0.0, r1 = 0.0, r2 = 0.0;
+  T r0 = 0, r1 = 0, r2 = 0;
   const double dt = f.dt;
   // then every element instance of this row in ascending element order
   for (int pass = 0; pass < 2; ++pass) {
@@ -685,7 +694,7 @@ __global__ void __launch_bounds__(64) k_fill(FillArgs f) {
                  for (int q = 0; q < 9; ++q) {
                    double cv = nscale * J[q];
                    if (D) cv = cv + dt * D[q];
-                   acc.at(slot, q) = acc.at(slot, q) + cv;
+                   acc.at(slot, q) = acc.at(slot, q) + static_cast<T>(cv);
                  }
                });
       // rhs (assembly.hpp:185-197): f = force + friction, then the damping
@@ -698,25 +707,26 @@ __global__ void __launch_bounds__(64) k_fill(FillArgs f) {
           fz = fz + damping * mv[b][2];
         }
       }
-      r0 = r0 + dt * fx;
-      r1 = r1 + dt * fy;
-      r2 = r2 + dt * fz;
+      r0 = r0 + static_cast<T>(dt * fx);
+      r1 = r1 + static_cast<T>(dt * fy);
+      r2 = r2 + static_cast<T>(dt * fz);
     }
   }
-  f.rhs[3 * r] = r0;
-  f.rhs[3 * r + 1] = r1;
-  f.rhs[3 * r + 2] = r2;
+  rhs[3 * r] = r0;
+  rhs[3 * r + 1] = r1;
+  rhs[3 * r + 2] = r2;
   if (!Wide) {
     for (int k = 0; k < len; ++k)
 #pragma unroll
-      for (int q = 0; q < 9; ++q) f.vals[vidx(base + (int64_t)k * kSlice, lr & 31, q)] = acc.at(k, q);
+      for (int q = 0; q < 9; ++q) vals[vidx(base + (int64_t)k * kSlice, lr & 31, q)] = acc.at(k, q);
   }
 }
 
 // Padding slots must hold zeros (they are never read by the SpMV, which
 // stops at rowlen, but downloads and ncu byte counts stay honest).
+template <class T>
 __global__ void k_zero_padding(int p, const int64_t* __restrict__ soff, const int32_t* __restrict__ rowlen,
-                               double* __restrict__ vals, int64_t total) {
+                               T* __restrict__ vals, int64_t total) {
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= p) return;
   const int s = r >> 5;
@@ -724,7 +734,7 @@ __global__ void k_zero_padding(int p, const int64_t* __restrict__ soff, const in
   const int64_t base = soff[s] + (r & 31);
   for (int k = rowlen[r]; k < width; ++k)
 #pragma unroll
-    for (int q = 0; q < 9; ++q) vals[vidx(base + (int64_t)k * kSlice, r & 31, q)] = 0.0;
+    for (int q = 0; q < 9; ++q) vals[vidx(base + (int64_t)k * kSlice, r & 31, q)] = 0;
 }
 
 // ---------------------------------------------------------------------------
@@ -1080,6 +1090,8 @@ struct SlotArgs {
   const double* __restrict__ eres;
   double* __restrict__ rhs;
   int* __restrict__ bad_mass;
+  float* __restrict__ vals32;  // Precision::Single outputs (T = float)
+  float* __restrict__ rhs32;
 };
 
 #ifndef WEFT_SLOT_WARPS
@@ -1103,9 +1115,11 @@ struct StagedInc {
 };
 
 // acc += (-scale) J_ab (+ dt D_ab) for one coupling, block regenerated from
-// the element's phase-1 state (bitwise the blocks fill_matrix adds).
+// the element's phase-1 state (bitwise the blocks fill_matrix adds); each
+// contribution computed in double and cast to Real before the add.
+template <class T = double>
 __device__ __forceinline__ void add_block(const StagedInc& si, int b, const double* __restrict__ epay,
-                                          const double* __restrict__ eres, double dt, double acc[9]) {
+                                          const double* __restrict__ eres, double dt, T acc[9]) {
   // acc += (-scale) J_ab (+ dt D_ab), entry by entry with elem_block's exact
   // expressions but no 3x3 temporaries (register pressure of k_fill_slots)
   const int kind = si.kind_ss_a & 0xff, a = (si.kind_ss_a >> 16) & 0xff;
@@ -1116,7 +1130,7 @@ __device__ __forceinline__ void add_block(const StagedInc& si, int b, const doub
     case WEFT_STRETCH: {
       if (S[15] == 0.0) {
 #pragma unroll
-        for (int q = 0; q < 9; ++q) acc[q] = acc[q] + nscale * 0.0;
+        for (int q = 0; q < 9; ++q) acc[q] = acc[q] + static_cast<T>(nscale * 0.0);
         return;
       }
       const V3 wu_hat = v3(S[0], S[1], S[2]), wv_hat = v3(S[3], S[4], S[5]);
@@ -1142,7 +1156,7 @@ __device__ __forceinline__ void add_block(const StagedInc& si, int b, const doub
           m = m - d[9] * (comp(gsi, r) * comp(gsj, c));
           if (keep_u2) m = m - su2 * (id - comp(wu_hat, r) * comp(wu_hat, c));
           if (keep_v2) m = m - sv2 * (id - comp(wv_hat, r) * comp(wv_hat, c));
-          acc[r * 3 + c] = acc[r * 3 + c] + nscale * (0.0 + m);
+          acc[r * 3 + c] = acc[r * 3 + c] + static_cast<T>(nscale * (0.0 + m));
         }
       return;
     }
@@ -1153,7 +1167,8 @@ __device__ __forceinline__ void add_block(const StagedInc& si, int b, const doub
 #pragma unroll
       for (int r = 0; r < 3; ++r)
 #pragma unroll
-        for (int c = 0; c < 3; ++c) acc[r * 3 + c] = acc[r * 3 + c] + nscale * (0.0 + nk * (comp(ga, r) * comp(gb, c)));
+        for (int c = 0; c < 3; ++c)
+          acc[r * 3 + c] = acc[r * 3 + c] + static_cast<T>(nscale * (0.0 + nk * (comp(ga, r) * comp(gb, c))));
       return;
     }
     default: {
@@ -1163,7 +1178,7 @@ __device__ __forceinline__ void add_block(const StagedInc& si, int b, const doub
       for (int q = 0; q < 9; ++q) {
         double cv = nscale * J[q];
         if (damped) cv = cv + dt * D[q];
-        acc[q] = acc[q] + cv;
+        acc[q] = acc[q] + static_cast<T>(cv);
       }
     }
   }
@@ -1172,8 +1187,10 @@ __device__ __forceinline__ void add_block(const StagedInc& si, int b, const doub
 // Phase 2: one CTA per slice of 32 rows. The slice's incidences (static then
 // contact, each ascending element per row) are staged in shared memory;
 // warp w computes slots w, w+8, ... of its lane's row.
-template <int kCap>
+template <int kCap, class T = double>
 __global__ void __launch_bounds__(kSlotWarps * 32, WEFT_SLOT_MINB) k_fill_slots(SlotArgs g) {
+  T* const out_vals = std::is_same_v<T, float> ? reinterpret_cast<T*>(g.vals32) : reinterpret_cast<T*>(g.vals);
+  T* const out_rhs = std::is_same_v<T, float> ? reinterpret_cast<T*>(g.rhs32) : reinterpret_cast<T*>(g.rhs);
   __shared__ int4 sm_st[kCap];
   __shared__ int sm_ksa[kCap], sm_pay[kCap], sm_res[kCap];
   __shared__ double sm_damp[kCap];
@@ -1246,11 +1263,11 @@ __global__ void __launch_bounds__(kSlotWarps * 32, WEFT_SLOT_MINB) k_fill_slots(
   for (int k = warp; k < len; k += kSlotWarps) {
     const int64_t at = base + (int64_t)k * kSlice;
     const int col = g.cols[at] & kColMask;
-    double acc[9];
+    T acc[9];
 #pragma unroll
-    for (int q = 0; q < 9; ++q) acc[q] = 0.0;
+    for (int q = 0; q < 9; ++q) acc[q] = 0;
     if (col == r) {  // mass diagonal first (assembly.hpp:155-166)
-      const double m = g.pinned[r] ? 1.0 : g.mass[r];
+      const T m = g.pinned[r] ? T(1) : static_cast<T>(g.mass[r]);
       acc[0] = acc[0] + m;
       acc[4] = acc[4] + m;
       acc[8] = acc[8] + m;
@@ -1266,7 +1283,7 @@ __global__ void __launch_bounds__(kSlotWarps * 32, WEFT_SLOT_MINB) k_fill_slots(
           for (int b = 0; b < 4; ++b) {
             if (b < ss && stv[b] == col) {
               StagedInc si{st4, sm_ksa[i], sm_pay[i], sm_res[i], sm_damp[i]};
-              add_block(si, b, g.epay, g.eres, dt, acc);
+              add_block<T>(si, b, g.epay, g.eres, dt, acc);
             }
           }
         }
@@ -1290,12 +1307,12 @@ __global__ void __launch_bounds__(kSlotWarps * 32, WEFT_SLOT_MINB) k_fill_slots(
           const int stv[4] = {si.st.x, si.st.y, si.st.z, si.st.w};
 #pragma unroll
           for (int b = 0; b < 4; ++b)
-            if (b < ss && stv[b] == col) add_block(si, b, g.epay, g.eres, dt, acc);
+            if (b < ss && stv[b] == col) add_block<T>(si, b, g.epay, g.eres, dt, acc);
         }
       }
     }
 #pragma unroll
-    for (int q = 0; q < 9; ++q) g.vals[vidx(at, lane, q)] = acc[q];
+    for (int q = 0; q < 9; ++q) out_vals[vidx(at, lane, q)] = acc[q];
   }
   // rhs of the lane's row (assembly.hpp:182-197): the phase-1 contributions
   // dt f_a of its incidences in ascending element order. Each sits right
@@ -1304,16 +1321,16 @@ __global__ void __launch_bounds__(kSlotWarps * 32, WEFT_SLOT_MINB) k_fill_slots(
   // Done by the last warp, which has the fewest slots.
   if (warp == kSlotWarps - 1) {
     if (!g.pinned[r] && g.mass[r] <= 0.0) atomicMin(g.bad_mass, r);
-    double r0 = 0.0, r1 = 0.0, r2 = 0.0;
+    T r0 = 0, r1 = 0, r2 = 0;
     for (int pass = 0; pass < 2; ++pass) {
       if (staged) {
         const int i1 = sm_row[pass][lane + 1];
         for (int i = sm_row[pass][lane]; i < i1; ++i) {
           const int ksa = sm_ksa[i];
           const double* R = g.eres + sm_res[i] - 3 * ((ksa >> 8) & 0xff) + 3 * ((ksa >> 16) & 0xff);
-          r0 = r0 + R[0];
-          r1 = r1 + R[1];
-          r2 = r2 + R[2];
+          r0 = r0 + static_cast<T>(R[0]);
+          r1 = r1 + static_cast<T>(R[1]);
+          r2 = r2 + static_cast<T>(R[2]);
         }
       } else {
         const int64_t* ip = pass == 0 ? g.inc_ptr : g.cinc_ptr;
@@ -1323,15 +1340,15 @@ __global__ void __launch_bounds__(kSlotWarps * 32, WEFT_SLOT_MINB) k_fill_slots(
           const int code = il[ii];
           const int64_t e = (pass == 0 ? 0 : g.n_static) + (code >> 2);
           const double* R = g.eres + g.eres_off[e] + 3 * (code & 3);
-          r0 = r0 + R[0];
-          r1 = r1 + R[1];
-          r2 = r2 + R[2];
+          r0 = r0 + static_cast<T>(R[0]);
+          r1 = r1 + static_cast<T>(R[1]);
+          r2 = r2 + static_cast<T>(R[2]);
         }
       }
     }
-    g.rhs[3 * r] = r0;
-    g.rhs[3 * r + 1] = r1;
-    g.rhs[3 * r + 2] = r2;
+    out_rhs[3 * r] = r0;
+    out_rhs[3 * r + 1] = r1;
+    out_rhs[3 * r + 2] = r2;
   }
 }
 
@@ -1377,8 +1394,10 @@ static int64_t select_rank_elements(Ctx& c) {
   return h;
 }
 
-void fill_matrix(Ctx& c, const double* xc, const double* xa, const double* vel, double dt, int mode, bool finish) {
+void fill_matrix(Ctx& c, const double* xc, const double* xa, const double* vel, double dt, int mode, bool finish,
+                 bool f32) {
   if (!(dt > 0.0)) throw Error(WEFT_ERR_DIMENSION, "fill_matrix: dt must be positive");
+  if (f32 && c.world > 1) throw Error(WEFT_ERR_INVALID, "fill_matrix: Precision::Single runs on one rank");
   if (c.p == 0 && c.n_static == 0) throw Error(WEFT_ERR_INVALID, "fill_matrix: set_vertices/set_elements first");
   if (c.spat_ptr.size() != static_cast<size_t>(c.p) + 1) throw Error(WEFT_ERR_INVALID, "fill_matrix: set_elements first");
   cudaStream_t s = c.stream;
@@ -1388,7 +1407,8 @@ void fill_matrix(Ctx& c, const double* xc, const double* xa, const double* vel, 
     c.have_pattern_for_contacts = c.n_contacts == 0;
   }
   SellMatrix& A = c.A;
-  c.rhs.resize(3 * static_cast<size_t>(c.p) + 3);
+  c.rhs.resize(3 * static_cast<size_t>(c.p) + 3);  // holds 3p floats for Precision::Single
+  if (f32) A.vals32.resize(9 * static_cast<size_t>(A.total) + 9);
   c.scalars.resize(64);
   int* bad = reinterpret_cast<int*>(c.scalars.data() + 8);
   const int big = INT32_MAX;
@@ -1408,6 +1428,8 @@ void fill_matrix(Ctx& c, const double* xc, const double* xa, const double* vel, 
   f.vals = A.vals.data();
   f.total = A.total;
   f.rhs = c.rhs.data();
+  f.vals32 = A.vals32.data();
+  f.rhs32 = reinterpret_cast<float*>(c.rhs.data());
   f.mass = c.mass.data();
   f.pinned = c.pinned.data();
   f.inc_ptr = c.inc_ptr.data();
@@ -1422,10 +1444,16 @@ void fill_matrix(Ctx& c, const double* xc, const double* xa, const double* vel, 
   f.xa = xa;
   f.vel = vel;
   f.bad_mass = bad;
+  auto zero_padding = [&]() {  // the precision's value planes
+    if (f32)
+      k_zero_padding<float><<<div_up(nloc, 256), 256, 0, ls(c)>>>(nloc, A.slice_off.data(), A.rowlen.data(),
+                                                                  A.vals32.data(), A.total);
+    else if (!layout_cached)
+      k_zero_padding<double><<<div_up(nloc, 256), 256, 0, ls(c)>>>(nloc, A.slice_off.data(), A.rowlen.data(),
+                                                                   A.vals.data(), A.total);
+  };
   if (nloc && !f.exact) {
-    if (!layout_cached)
-      k_zero_padding<<<div_up(nloc, 256), 256, 0, ls(c)>>>(nloc, A.slice_off.data(), A.rowlen.data(), A.vals.data(),
-                                                         A.total);
+    zero_padding();
     // phase 1 over every element (one rank) or over the elements coupled to
     // this rank's rows (distribute_elements, assembly.cpp:28-51)
     int64_t ne = c.n_static + c.n_contacts;
@@ -1463,17 +1491,22 @@ void fill_matrix(Ctx& c, const double* xc, const double* xa, const double* vel, 
     SlotArgs sa{nloc, c.row0, A.perm.data(), c.n_static, dt, A.slice_off.data(), A.rowlen.data(), A.cols.data(), A.vals.data(),
                 A.total, c.mass.data(), c.pinned.data(), c.inc_ptr.data(), c.inc.data(), c.cinc_ptr.data(),
                 c.cinc.data(), c.est.data(), c.einfo.data(), c.edamp.data(), c.epay.data(), c.eres_off.data(),
-                c.eres.data(), c.rhs.data(), bad};
-    if (c.n_contacts > 0) k_fill_slots<kStageCapContacts><<<A.nslices, kSlotWarps * 32, 0, ls(c)>>>(sa);
-    else k_fill_slots<kStageCap><<<A.nslices, kSlotWarps * 32, 0, ls(c)>>>(sa);
+                c.eres.data(), c.rhs.data(), bad, A.vals32.data(), reinterpret_cast<float*>(c.rhs.data())};
+    if (f32) {
+      if (c.n_contacts > 0) k_fill_slots<kStageCapContacts, float><<<A.nslices, kSlotWarps * 32, 0, ls(c)>>>(sa);
+      else k_fill_slots<kStageCap, float><<<A.nslices, kSlotWarps * 32, 0, ls(c)>>>(sa);
+    } else {
+      if (c.n_contacts > 0) k_fill_slots<kStageCapContacts><<<A.nslices, kSlotWarps * 32, 0, ls(c)>>>(sa);
+      else k_fill_slots<kStageCap><<<A.nslices, kSlotWarps * 32, 0, ls(c)>>>(sa);
+    }
     WG_CUDA(cudaGetLastError());
   } else if (nloc) {
-    if (!layout_cached)
-      k_zero_padding<<<div_up(nloc, 256), 256, 0, ls(c)>>>(nloc, A.slice_off.data(), A.rowlen.data(), A.vals.data(),
-                                                         A.total);
+    zero_padding();
     const size_t smem = static_cast<size_t>(f.wcap) * (9 * sizeof(double) + sizeof(int32_t)) * kFillThreads;
-    auto narrow = f.exact ? k_fill<false, true> : k_fill<false, false>;
-    auto wide = f.exact ? k_fill<true, true> : k_fill<true, false>;
+    auto narrow = f32 ? (f.exact ? k_fill<false, true, float> : k_fill<false, false, float>)
+                      : (f.exact ? k_fill<false, true> : k_fill<false, false>);
+    auto wide = f32 ? (f.exact ? k_fill<true, true, float> : k_fill<true, false, float>)
+                    : (f.exact ? k_fill<true, true> : k_fill<true, false>);
     WG_CUDA(cudaFuncSetAttribute(narrow, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     narrow<<<div_up(nloc, kFillThreads), kFillThreads, smem, ls(c)>>>(f);
     if (A.max_len > kWideCap) {
@@ -1482,6 +1515,7 @@ void fill_matrix(Ctx& c, const double* xc, const double* xa, const double* vel, 
     }
     WG_CUDA(cudaGetLastError());
   }
+  A.f32 = f32;
   c.has_matrix = true;
   c.has_rhs = true;
   if (finish) fill_matrix_finish(c);

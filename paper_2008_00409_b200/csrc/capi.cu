@@ -331,6 +331,7 @@ weft_status weft_gpu_download_rhs(weft_gpu_ctx* ctx, double* rhs) {
   return guard(ctx, [&] {
     auto& c = ctx->c;
     need(c.has_rhs, WEFT_ERR_INVALID, "download_rhs: no assembled system");
+    need(!c.A.f32, WEFT_ERR_INVALID, "download_rhs: single-precision system (use the f32 entry)");
     WG_CUDA(cudaMemcpyAsync(rhs, c.rhs.data() + 3 * static_cast<size_t>(c.row0), 3 * sizeof(double) * c.A.rows,
                             cudaMemcpyDefault, c.stream));
     WG_CUDA(cudaStreamSynchronize(c.stream));

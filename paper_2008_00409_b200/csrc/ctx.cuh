@@ -281,8 +281,10 @@ void set_elements(Ctx& c, int64_t count, const weft_element* elems);
 void set_contacts(Ctx& c, int64_t count, const weft_element* elems);
 // finish = false leaves the final host check (non-positive mass) to
 // fill_matrix_finish, so other streams can be fed while the kernels run.
+// f32: Precision::Single — AssembledSystem<float> (each contribution cast to
+// float and added in float, assembly.hpp:163,196,212), one rank.
 void fill_matrix(Ctx& c, const double* xc, const double* xa, const double* vel, double dt, int mode,
-                 bool finish = true);
+                 bool finish = true, bool f32 = false);
 void fill_matrix_finish(Ctx& c);
 
 void set_soup(Ctx& c, int verts, int ntris, const int32_t* tris);

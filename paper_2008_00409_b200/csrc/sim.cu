@@ -20,11 +20,13 @@ __global__ void k_advance(int64_t n, const double* __restrict__ x, const double*
 
 // v += dv; x_cand = x + dt v (driver.cpp:165-176) over entries [i0, i1)
 // (this rank's rows)
+// dv: Real (float under Precision::Single; v_cand += double(dv), driver.cpp:166-170)
+template <class T>
 __global__ void k_candidate(int64_t i0, int64_t i1, const double* __restrict__ x, double* __restrict__ v,
-                            const double* __restrict__ dv, double dt, double* __restrict__ xc) {
+                            const T* __restrict__ dv, double dt, double* __restrict__ xc) {
   const int64_t i = i0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= i1) return;
-  const double vi = v[i] + dv[i];
+  const double vi = v[i] + static_cast<double>(dv[i]);
   v[i] = vi;
   xc[i] = x[i] + dt * vi;
 }
@@ -86,6 +88,42 @@ weft_status weft_gpu_fill_matrix(weft_gpu_ctx* ctx, const double* x_cur, const d
     weft_gpu::upload_vec(c, c.x_adv, x_adv, n);
     weft_gpu::upload_vec(c, c.vel, velocity, n);
     weft_gpu::fill_matrix(c, c.x_cur.data(), c.x_adv.data(), c.vel.data(), dt, jac_mode);
+  });
+}
+
+weft_status weft_gpu_fill_matrix_f32(weft_gpu_ctx* ctx, const double* x_cur, const double* x_adv,
+                                     const double* velocity, double dt, int32_t jac_mode) {
+  return guard2(ctx, [&](Ctx& c) {
+    const size_t n = 3 * static_cast<size_t>(c.p);
+    weft_gpu::upload_vec(c, c.x_cur, x_cur, n);
+    weft_gpu::upload_vec(c, c.x_adv, x_adv, n);
+    weft_gpu::upload_vec(c, c.vel, velocity, n);
+    weft_gpu::fill_matrix(c, c.x_cur.data(), c.x_adv.data(), c.vel.data(), dt, jac_mode, true, true);
+  });
+}
+
+weft_status weft_gpu_step_system_f32(weft_gpu_ctx* ctx, const double* x, const double* v, double dt,
+                                     int32_t jac_mode) {
+  return guard2(ctx, [&](Ctx& c) {
+    const size_t n = 3 * static_cast<size_t>(c.p);
+    weft_gpu::upload_vec(c, c.x_cur, x, n);
+    weft_gpu::upload_vec(c, c.vel, v, n);
+    c.x_adv.resize(n);
+    if (n)
+      weft_gpu::k_advance<<<weft_gpu::div_up(n, 256), 256, 0, ls(c)>>>(n, c.x_cur.data(), c.vel.data(), dt,
+                                                                          c.x_adv.data());
+    WG_CUDA(cudaGetLastError());
+    weft_gpu::fill_matrix(c, c.x_cur.data(), c.x_adv.data(), c.vel.data(), dt, jac_mode, true, true);
+  });
+}
+
+weft_status weft_gpu_download_rhs_f32(weft_gpu_ctx* ctx, float* rhs) {
+  return guard2(ctx, [&](Ctx& c) {
+    if (!c.has_rhs || !c.A.f32) throw Error(WEFT_ERR_INVALID, "download_rhs: no single-precision rhs");
+    const size_t o = 3 * static_cast<size_t>(c.row0), m = 3 * static_cast<size_t>(c.row1 - c.row0);
+    WG_CUDA(cudaMemcpyAsync(rhs, reinterpret_cast<const float*>(c.rhs.data()) + o, m * sizeof(float),
+                            cudaMemcpyDefault, c.stream));
+    WG_CUDA(cudaStreamSynchronize(c.stream));
   });
 }
 
@@ -318,6 +356,8 @@ weft_status weft_gpu_sim_step(weft_gpu_ctx* ctx, const weft_sim_params* prm, wef
     cudaStream_t s = c.stream;
     const int64_t n = 3 * static_cast<int64_t>(c.p);
     const double dt = prm->dt;
+    const bool f32 = prm->precision == 1;
+    if (f32 && c.world > 1) throw Error(WEFT_ERR_INVALID, "sim_step: Precision::Single runs on one rank");
     cudaEvent_t* ev = c.ev;
     // the grid is replicated on every rank (collision.cpp:397-399); each
     // rank walks its split_workload share of the pair space (:181-192)
@@ -346,7 +386,7 @@ weft_status weft_gpu_sim_step(weft_gpu_ctx* ctx, const weft_sim_params* prm, wef
       c.x_adv.resize(static_cast<size_t>(n));
       weft_gpu::k_advance<<<weft_gpu::div_up(n, 256), 256, 0, ls(c)>>>(n, c.sim_x.data(), c.sim_v.data(), dt,
                                                                     c.x_adv.data());
-      weft_gpu::fill_matrix(c, c.sim_x.data(), c.x_adv.data(), c.sim_v.data(), dt, prm->jac_mode);
+      weft_gpu::fill_matrix(c, c.sim_x.data(), c.x_adv.data(), c.sim_v.data(), dt, prm->jac_mode, true, f32);
       WG_CUDA(cudaEventRecord(ev[2], s));
       WG_CUDA(cudaEventRecord(ev[1], s));
     } else if (c.io_vin) {
@@ -364,7 +404,7 @@ weft_status weft_gpu_sim_step(weft_gpu_ctx* ctx, const weft_sim_params* prm, wef
     c.x_adv.resize(static_cast<size_t>(n));
     weft_gpu::k_advance<<<weft_gpu::div_up(n, 256), 256, 0, ls(c)>>>(n, c.sim_x.data(), c.sim_v.data(), dt,
                                                                   c.x_adv.data());
-    weft_gpu::fill_matrix(c, c.sim_x.data(), c.x_adv.data(), c.sim_v.data(), dt, prm->jac_mode);
+    weft_gpu::fill_matrix(c, c.sim_x.data(), c.x_adv.data(), c.sim_v.data(), dt, prm->jac_mode, true, f32);
     WG_CUDA(cudaEventRecord(ev[2], s));
     WG_CUDA(cudaEventRecord(ev[1], s));
     } else {
@@ -378,7 +418,8 @@ weft_status weft_gpu_sim_step(weft_gpu_ctx* ctx, const weft_sim_params* prm, wef
     c.x_adv.resize(static_cast<size_t>(n));
     weft_gpu::k_advance<<<weft_gpu::div_up(n, 256), 256, 0, ls(c)>>>(n, c.sim_x.data(), c.sim_v.data(), dt,
                                                                   c.x_adv.data());
-    weft_gpu::fill_matrix(c, c.sim_x.data(), c.x_adv.data(), c.sim_v.data(), dt, prm->jac_mode, /*finish=*/false);
+    weft_gpu::fill_matrix(c, c.sim_x.data(), c.x_adv.data(), c.sim_v.data(), dt, prm->jac_mode, /*finish=*/false,
+                          f32);
     WG_CUDA(cudaEventRecord(ev[2], s));
     // A/B knob (WEFT_SIM_OVERLAP=1): measured no gain on B200 — the
     // assembly's grids fill every SM, so the side-stream broad phase only
@@ -403,7 +444,9 @@ weft_status weft_gpu_sim_step(weft_gpu_ctx* ctx, const weft_sim_params* prm, wef
     WG_CUDA(cudaEventRecord(ev[1], s));
     }
     // 3. PCG for dv
-    const weft_gpu::PcgResult pr = weft_gpu::pcg_solve(c, c.rhs.data(), prm->pcg, nullptr, nullptr);
+    const weft_gpu::PcgResult pr =
+        f32 ? weft_gpu::pcg_solve_f32(c, reinterpret_cast<const float*>(c.rhs.data()), prm->pcg, nullptr, nullptr)
+            : weft_gpu::pcg_solve(c, c.rhs.data(), prm->pcg, nullptr, nullptr);
     WG_CUDA(cudaEventRecord(ev[3], s));
     if (!pr.converged)  // driver.cpp:158-161
       throw Error(WEFT_ERR_SOLVER, "PCG did not converge (residual " + std::to_string(pr.rel_residual) + ")");
@@ -425,9 +468,16 @@ weft_status weft_gpu_sim_step(weft_gpu_ctx* ctx, const weft_sim_params* prm, wef
       }
     } v_restore{c, n};
     const int64_t i0 = 3 * static_cast<int64_t>(c.row0), i1 = 3 * static_cast<int64_t>(c.row1);
-    if (pr.iterations == 0) WG_CUDA(cudaMemsetAsync(c.xs.data() + i0, 0, (i1 - i0) * sizeof(double), s));
-    weft_gpu::k_candidate<<<weft_gpu::div_up(i1 - i0, 256), 256, 0, ls(c)>>>(i0, i1, c.sim_x.data(), c.sim_v.data(),
-                                                                          c.xs.data(), dt, c.sim_xc.data());
+    if (f32) {
+      float* dv = reinterpret_cast<float*>(c.xs.data());
+      if (pr.iterations == 0) WG_CUDA(cudaMemsetAsync(dv + i0, 0, (i1 - i0) * sizeof(float), s));
+      weft_gpu::k_candidate<float><<<weft_gpu::div_up(i1 - i0, 256), 256, 0, ls(c)>>>(
+          i0, i1, c.sim_x.data(), c.sim_v.data(), dv, dt, c.sim_xc.data());
+    } else {
+      if (pr.iterations == 0) WG_CUDA(cudaMemsetAsync(c.xs.data() + i0, 0, (i1 - i0) * sizeof(double), s));
+      weft_gpu::k_candidate<double><<<weft_gpu::div_up(i1 - i0, 256), 256, 0, ls(c)>>>(
+          i0, i1, c.sim_x.data(), c.sim_v.data(), c.xs.data(), dt, c.sim_xc.data());
+    }
     if (c.world > 1) weft_gpu::exchange_state(c);  // all rows of v and x_cand on every rank
     WG_CUDA(cudaEventRecord(ev[4], s));
     const bool io_out_early = c.io_xout && !contacts;  // v and x_cand are final here

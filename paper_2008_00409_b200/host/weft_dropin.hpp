@@ -19,6 +19,7 @@
 #include <span>
 #include <stdexcept>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "weft/assembly.hpp"
@@ -158,40 +159,53 @@ inline std::vector<double> flat3(std::span<const Vec3> v) {
 
 // Global block CSR -> the reference's partitioned BELL type
 // (partition_matrix(from_entries(...)), sparse.hpp:103-147).
-inline PartitionedMatrix<double> to_partitioned(int rows, const std::vector<int64_t>& rp, const std::vector<int32_t>& cols,
-                                                const std::vector<double>& vals,
-                                                const std::vector<DevicePartition>& parts) {
-  std::vector<BlockEntry<double>> entries;
+template <class Real>
+PartitionedMatrix<Real> to_partitioned(int rows, const std::vector<int64_t>& rp, const std::vector<int32_t>& cols,
+                                       const std::vector<Real>& vals, const std::vector<DevicePartition>& parts) {
+  std::vector<BlockEntry<Real>> entries;
   entries.reserve(cols.size());
   for (int r = 0; r < rows; ++r)
     for (int64_t k = rp[static_cast<std::size_t>(r)]; k < rp[static_cast<std::size_t>(r) + 1]; ++k) {
-      BlockEntry<double> e;
+      BlockEntry<Real> e;
       e.row = r;
       e.col = cols[static_cast<std::size_t>(k)];
-      std::memcpy(e.m.data(), &vals[static_cast<std::size_t>(9 * k)], sizeof(double) * 9);
+      std::memcpy(e.m.data(), &vals[static_cast<std::size_t>(9 * k)], sizeof(Real) * 9);
       entries.push_back(e);
     }
-  return partition_matrix(BellMatrix<double>::from_entries(rows, entries), parts);
+  return partition_matrix(BellMatrix<Real>::from_entries(rows, entries), parts);
 }
 
-inline void upload_partitioned(Context& cx, const PartitionedMatrix<double>& a) {
+// Real-dispatched C-ABI calls (Precision::Single: the _f32 entry points).
+inline weft_status set_matrix_r(weft_gpu_ctx* c, int32_t rows, const int64_t* rp, const int32_t* cols,
+                                const double* vals) {
+  return weft_gpu_set_matrix(c, rows, rp, cols, vals);
+}
+inline weft_status set_matrix_r(weft_gpu_ctx* c, int32_t rows, const int64_t* rp, const int32_t* cols,
+                                const float* vals) {
+  return weft_gpu_set_matrix_f32(c, rows, rp, cols, vals);
+}
+inline weft_status spmv_r(weft_gpu_ctx* c, const double* x, double* y) { return weft_gpu_spmv(c, x, y); }
+inline weft_status spmv_r(weft_gpu_ctx* c, const float* x, float* y) { return weft_gpu_spmv_f32(c, x, y); }
+
+template <class Real>
+void upload_partitioned(Context& cx, const PartitionedMatrix<Real>& a) {
   weft_gpu_ctx* ctx = cx.get();
   cx.vertices_set = cx.elements_set = false;  // set_matrix replaces the assembled system
   const auto g = gather_matrix(a);
   std::vector<int64_t> rp(static_cast<std::size_t>(g.block_rows()) + 1, 0);
   std::vector<int32_t> cols;
-  std::vector<double> vals;
+  std::vector<Real> vals;
   for (int r = 0; r < g.block_rows(); ++r) {
     for (int s = 0; s < g.ell_width(); ++s) {
       const int32_t c = g.col_at(r, s);
-      if (c == BellMatrix<double>::kNoBlock) break;
+      if (c == BellMatrix<Real>::kNoBlock) break;
       cols.push_back(c);
       for (int i = 0; i < 3; ++i)
         for (int j = 0; j < 3; ++j) vals.push_back(g.value_at(r, s, i, j));
     }
     rp[static_cast<std::size_t>(r) + 1] = static_cast<int64_t>(cols.size());
   }
-  check(weft_gpu_set_matrix(ctx, g.block_rows(), rp.data(), cols.data(), vals.data()));
+  check(set_matrix_r(ctx, g.block_rows(), rp.data(), cols.data(), vals.data()));
 }
 
 // Uploads the vertex data and the static element list only when they differ
@@ -228,17 +242,23 @@ inline void sync_inputs(Context& cx, int p, std::span<const double> mass, std::s
 }
 
 // The context's assembled system downloaded into the reference's types.
-inline AssembledSystem<double> download_system(Engine& engine, weft_gpu_ctx* ctx, int p,
-                                               const std::vector<DevicePartition>& partitions) {
+template <class Real>
+AssembledSystem<Real> download_system(Engine& engine, weft_gpu_ctx* ctx, int p,
+                                      const std::vector<DevicePartition>& partitions) {
   weft_matrix_info info{};
   check(weft_gpu_matrix_info(ctx, &info));
   std::vector<int64_t> rp(static_cast<std::size_t>(info.block_rows) + 1);
   std::vector<int32_t> cols(static_cast<std::size_t>(info.nnzb));
-  std::vector<double> vals(9 * static_cast<std::size_t>(info.nnzb)), rhs(3 * static_cast<std::size_t>(p));
-  check(weft_gpu_download_matrix(ctx, rp.data(), cols.data(), vals.data()));
-  check(weft_gpu_download_rhs(ctx, rhs.data()));
-  AssembledSystem<double> out{to_partitioned(info.block_rows, rp, cols, vals, partitions),
-                              DistVector<double>(&engine, partitions)};
+  std::vector<Real> vals(9 * static_cast<std::size_t>(info.nnzb)), rhs(3 * static_cast<std::size_t>(p));
+  if constexpr (std::is_same_v<Real, float>) {
+    check(weft_gpu_download_matrix_f32(ctx, rp.data(), cols.data(), vals.data()));
+    check(weft_gpu_download_rhs_f32(ctx, rhs.data()));
+  } else {
+    check(weft_gpu_download_matrix(ctx, rp.data(), cols.data(), vals.data()));
+    check(weft_gpu_download_rhs(ctx, rhs.data()));
+  }
+  AssembledSystem<Real> out{to_partitioned<Real>(info.block_rows, rp, cols, vals, partitions),
+                            DistVector<Real>(&engine, partitions)};
   for (const auto& part : partitions) {
     auto local = out.rhs.local(part.device_id);
     std::copy(rhs.begin() + 3 * part.begin, rhs.begin() + 3 * part.end, local.begin());
@@ -253,9 +273,7 @@ inline AssembledSystem<double> download_system(Engine& engine, weft_gpu_ctx* ctx
 template <class Real>
 AssembledSystem<Real> fill_matrix(Engine& engine, const DistributedElements& /*dist*/, const SystemInputs& in,
                                   const std::vector<DevicePartition>& partitions) {
-  if constexpr (!std::is_same_v<Real, double>) {
-    throw Error("weft::gpu::fill_matrix: only double precision runs on the GPU path");
-  } else {
+  {
     if (in.dt <= 0.0) throw DimensionError("fill_matrix: dt must be positive");
     Lease lease = acquire(engine);
     weft_gpu_ctx* ctx = lease.get();
@@ -269,9 +287,12 @@ AssembledSystem<Real> fill_matrix(Engine& engine, const DistributedElements& /*d
     }
     sync_inputs(lease.c, p, in.mass, in.pinned, stat, cont);
     const auto xc = flat3(in.x_current), xa = flat3(in.x_advanced), v = flat3(in.velocity);
-    check(weft_gpu_fill_matrix(ctx, xc.data(), xa.data(), v.data(), in.dt,
-                               in.mode == JacobianMode::Exact ? WEFT_JAC_EXACT : WEFT_JAC_SPD_PROJECTED));
-    return download_system(engine, ctx, p, partitions);
+    const int jm = in.mode == JacobianMode::Exact ? WEFT_JAC_EXACT : WEFT_JAC_SPD_PROJECTED;
+    if constexpr (std::is_same_v<Real, float>)  // fill_matrix<float>: one rank
+      check(weft_gpu_fill_matrix_f32(ctx, xc.data(), xa.data(), v.data(), in.dt, jm));
+    else
+      check(weft_gpu_fill_matrix(ctx, xc.data(), xa.data(), v.data(), in.dt, jm));
+    return download_system<Real>(engine, ctx, p, partitions);
   }
 }
 
@@ -288,9 +309,7 @@ AssembledSystem<Real> step_system(Engine& engine, const ClothMesh& mesh, const S
                                   const MaterialParams& params, std::span<const std::uint8_t> pinned,
                                   std::vector<AssemblyElement> contact_elements, double dt, const Vec3& gravity,
                                   const Vec3& wind, JacobianMode mode = JacobianMode::SpdProjected) {
-  if constexpr (!std::is_same_v<Real, double>) {
-    throw Error("weft::gpu::step_system: only double precision runs on the GPU path");
-  } else {
+  {
     if (dt <= 0.0) throw DimensionError("fill_matrix: dt must be positive");
     const int p = mesh.vertex_count();
     if (state.x.size() != static_cast<std::size_t>(p) || state.v.size() != static_cast<std::size_t>(p))
@@ -320,9 +339,12 @@ AssembledSystem<Real> step_system(Engine& engine, const ClothMesh& mesh, const S
     cx.mesh_key = &mesh;
     cx.elem_params = key;
     const auto x = flat3(state.x), v = flat3(state.v);
-    check(weft_gpu_step_system(ctx, x.data(), v.data(), dt,
-                               mode == JacobianMode::Exact ? WEFT_JAC_EXACT : WEFT_JAC_SPD_PROJECTED));
-    return download_system(engine, ctx, p, make_partitions(p, engine.devices()));
+    const int jm = mode == JacobianMode::Exact ? WEFT_JAC_EXACT : WEFT_JAC_SPD_PROJECTED;
+    if constexpr (std::is_same_v<Real, float>)
+      check(weft_gpu_step_system_f32(ctx, x.data(), v.data(), dt, jm));
+    else
+      check(weft_gpu_step_system(ctx, x.data(), v.data(), dt, jm));
+    return download_system<Real>(engine, ctx, p, make_partitions(p, engine.devices()));
   }
 }
 
@@ -331,30 +353,28 @@ AssembledSystem<Real> step_system(Engine& engine, const ClothMesh& mesh, const S
 // bell.cpp:87-129) — the one-partition GPU SpMV, bitwise.
 template <class Real>
 std::vector<Real> spmv_serial(const BellMatrix<Real>& a, std::span<const Real> x) {
-  if constexpr (!std::is_same_v<Real, double>) {
-    throw Error("weft::gpu::spmv_serial: only double precision runs on the GPU path");
-  } else {
+  {
     if (static_cast<int>(x.size()) != a.rows()) throw DimensionError("spmv_serial: dim(x) != rows");
     Lease lease = acquire(1);
     weft_gpu_ctx* ctx = lease.get();
     std::vector<int64_t> rp(static_cast<std::size_t>(a.block_rows()) + 1, 0);
     std::vector<int32_t> cols;
-    std::vector<double> vals;
+    std::vector<Real> vals;
     for (int r = 0; r < a.block_rows(); ++r) {
       for (int s = 0; s < a.ell_width(); ++s) {
         const int32_t c = a.col_at(r, s);
-        if (c == BellMatrix<double>::kNoBlock) break;
+        if (c == BellMatrix<Real>::kNoBlock) break;
         cols.push_back(c);
         for (int i = 0; i < 3; ++i)
           for (int j = 0; j < 3; ++j) vals.push_back(a.value_at(r, s, i, j));
       }
       rp[static_cast<std::size_t>(r) + 1] = static_cast<int64_t>(cols.size());
     }
-    std::vector<double> y(x.size(), 0.0);
+    std::vector<Real> y(x.size(), Real(0));
     if (a.block_rows() == 0) return y;
     lease.c.vertices_set = lease.c.elements_set = false;  // set_matrix replaces the assembled system
-    check(weft_gpu_set_matrix(ctx, a.block_rows(), rp.data(), cols.data(), vals.data()));
-    check(weft_gpu_spmv(ctx, x.data(), y.data()));
+    check(set_matrix_r(ctx, a.block_rows(), rp.data(), cols.data(), vals.data()));
+    check(spmv_r(ctx, x.data(), y.data()));
     return y;
   }
 }
@@ -363,17 +383,15 @@ std::vector<Real> spmv_serial(const BellMatrix<Real>& a, std::span<const Real> x
 template <class Real>
 void spmv_pipelined(Engine& engine, const PartitionedMatrix<Real>& a, const ValidatedSchedule& sched,
                     const DistVector<Real>& x, DistVector<Real>& y, SpmvWorkspace<Real>& /*ws*/) {
-  if constexpr (!std::is_same_v<Real, double>) {
-    throw Error("weft::gpu::spmv_pipelined: only double precision runs on the GPU path");
-  } else {
+  {
     if (engine.devices() != a.devices || sched.devices() != a.devices)
       throw DimensionError("spmv_pipelined: engine/schedule/matrix device counts differ");
     Lease lease = acquire(engine);
     weft_gpu_ctx* ctx = lease.get();
     upload_partitioned(lease.c, a);
     const auto xg = x.gather();
-    std::vector<double> yg(xg.size());
-    check(weft_gpu_spmv(ctx, xg.data(), yg.data()));
+    std::vector<Real> yg(xg.size());
+    check(spmv_r(ctx, xg.data(), yg.data()));
     for (const auto& part : a.partitions) {
       auto local = y.local(part.device_id);
       std::copy(yg.begin() + 3 * part.begin, yg.begin() + 3 * part.end, local.begin());
@@ -385,21 +403,22 @@ void spmv_pipelined(Engine& engine, const PartitionedMatrix<Real>& a, const Vali
 template <class Real>
 PcgReport pcg_solve(Engine& engine, const PartitionedMatrix<Real>& a, const ValidatedSchedule& /*sched*/,
                     const DistVector<Real>& b, DistVector<Real>& x, const PcgConfig& config) {
-  if constexpr (!std::is_same_v<Real, double>) {
-    throw Error("weft::gpu::pcg_solve: only double precision runs on the GPU path");
-  } else {
+  {
     if (engine.devices() != a.devices) throw DimensionError("pcg_solve: engine/matrix device count mismatch");
     Lease lease = acquire(engine);
     weft_gpu_ctx* ctx = lease.get();
     upload_partitioned(lease.c, a);
     const auto bg = b.gather();
-    std::vector<double> xg(bg.size());
+    std::vector<Real> xg(bg.size());
     weft_pcg_config cfg{config.rel_tolerance, config.max_iterations,
                         config.preconditioner == Preconditioner::None ? WEFT_PRECOND_NONE : WEFT_PRECOND_BLOCK_JACOBI};
     std::vector<double> hist(static_cast<std::size_t>(std::max(config.max_iterations, 1)));
     std::vector<double> phist(hist.size());
     weft_pcg_report rep{0, 0, 0.0, hist.data(), phist.data()};
-    check(weft_gpu_pcg(ctx, bg.data(), xg.data(), &cfg, &rep));
+    if constexpr (std::is_same_v<Real, float>)  // pcg_solve<float>
+      check(weft_gpu_pcg_f32(ctx, bg.data(), xg.data(), &cfg, &rep));
+    else
+      check(weft_gpu_pcg(ctx, bg.data(), xg.data(), &cfg, &rep));
     for (const auto& part : a.partitions) {
       auto local = x.local(part.device_id);
       std::copy(xg.begin() + 3 * part.begin, xg.begin() + 3 * part.end, local.begin());
@@ -412,7 +431,7 @@ PcgReport pcg_solve(Engine& engine, const PartitionedMatrix<Real>& a, const Vali
     out.precond_norm_history.assign(phist.begin(), phist.begin() + rep.iterations);
     if (engine.options().instrument != nullptr && bg.size()) {  // solver.hpp:171-175 (not for b = 0)
       bool zero = true;
-      for (double v : bg) zero = zero && v == 0.0;
+      for (Real v : bg) zero = zero && v == Real(0);
       if (!zero) {
         std::ostringstream os;
         os << "event=pcg iterations=" << out.iterations << " rel_residual=" << out.rel_residual

@@ -469,8 +469,6 @@ class Simulator:
         reference's event lines — stage (driver.cpp:104-111), pcg
         (solver.hpp:171-175) and zones (response.cpp:383-388) — in its
         order and format."""
-        if scene.config.precision != "double":
-            raise SceneError("the GPU path computes in double precision (Precision::Double)")
         self.scene = scene
         cfg = scene.config
         self.mesh = scene.cloth
@@ -499,7 +497,8 @@ class Simulator:
                             weft.PRECOND_BLOCK_JACOBI if cfg.preconditioner == "block-jacobi" else weft.PRECOND_NONE)
         self.params = weft.SimParams(cfg.dt, cfg.thickness, cfg.cell_scale, pc, weft.JAC_SPD, contacts=1,
                                      stiffness_scale=cfg.stiffness_scale, friction=cfg.friction,
-                                     contact_damping=cfg.contact_damping, zones=1, zone=zp)
+                                     contact_damping=cfg.contact_damping, zones=1, zone=zp,
+                                     precision=1 if cfg.precision == "single" else 0)  # step_impl<Real>
 
     def _obstacles_at(self, t: float) -> np.ndarray:
         if not self.scene.obstacles:

@@ -163,10 +163,10 @@ class SimParams(C.Structure):
     _fields_ = [("dt", C.c_double), ("thickness", C.c_double), ("cell_scale", C.c_double), ("pcg", PcgConfig),
                 ("jac_mode", C.c_int32), ("contacts", C.c_int32), ("stiffness_scale", C.c_double),
                 ("friction", C.c_double), ("contact_damping", C.c_double), ("zones", C.c_int32),
-                ("zone", ZoneParams)]
+                ("zone", ZoneParams), ("precision", C.c_int32)]
 
     def __init__(self, dt=1.0 / 240.0, thickness=0.005, cell_scale=1.5, pcg=None, jac_mode=1, contacts=0,
-                 stiffness_scale=4.0, friction=0.2, contact_damping=0.0, zones=0, zone=None):
+                 stiffness_scale=4.0, friction=0.2, contact_damping=0.0, zones=0, zone=None, precision=0):
         """SimConfig subset (driver.hpp:30-45): collision, ContactParams
         (response.hpp:13-21) and ZoneSolveParams defaults of the reference;
         the zone clearance follows Simulator's rule clearance_fraction (0.5) *
@@ -174,7 +174,7 @@ class SimParams(C.Structure):
         if zone is None:
             zone = ZoneParams(clearance=0.5 * thickness)
         super().__init__(dt, thickness, cell_scale, pcg if pcg is not None else PcgConfig(), jac_mode, contacts,
-                         stiffness_scale, friction, contact_damping, zones, zone)
+                         stiffness_scale, friction, contact_damping, zones, zone, precision)
 
 
 class StepReport(C.Structure):
@@ -432,6 +432,10 @@ class Engine:
 
     def download_rhs(self) -> np.ndarray:
         info = self.matrix_info()
+        if getattr(self, "_f32", False):
+            rhs = np.zeros(3 * info.block_rows, np.float32)
+            _check(LIB.weft_gpu_download_rhs_f32(self._ctx, _ptr(rhs)))
+            return rhs
         rhs = np.zeros(3 * info.block_rows)
         _check(LIB.weft_gpu_download_rhs(self._ctx, _ptr(rhs)))
         return rhs
@@ -472,14 +476,19 @@ class Engine:
         e = np.ascontiguousarray(contacts if contacts is not None else np.zeros(0, ELEMENT_DTYPE), ELEMENT_DTYPE)
         _check(LIB.weft_gpu_set_contacts(self._ctx, C.c_int64(len(e)), _ptr(e)))
 
-    def fill_matrix(self, x_current, x_advanced, velocity, dt: float, mode: int = JAC_SPD):
+    def fill_matrix(self, x_current, x_advanced, velocity, dt: float, mode: int = JAC_SPD, single: bool = False):
         """fill_matrix over the context's static + contact elements; the
-        system stays resident (download_matrix / download_rhs to read)."""
-        _check(LIB.weft_gpu_fill_matrix(self._ctx, _ptr(_f64(x_current)), _ptr(_f64(x_advanced)),
-                                        _ptr(_f64(velocity)), C.c_double(dt), C.c_int32(mode)))
+        system stays resident (download_matrix / download_rhs to read).
+        single: fill_matrix<float> (Precision::Single)."""
+        fn = LIB.weft_gpu_fill_matrix_f32 if single else LIB.weft_gpu_fill_matrix
+        _check(fn(self._ctx, _ptr(_f64(x_current)), _ptr(_f64(x_advanced)), _ptr(_f64(velocity)), C.c_double(dt),
+                  C.c_int32(mode)))
+        self._f32 = bool(single)
 
-    def step_system(self, x, v, dt: float, mode: int = JAC_SPD):
-        _check(LIB.weft_gpu_step_system(self._ctx, _ptr(_f64(x)), _ptr(_f64(v)), C.c_double(dt), C.c_int32(mode)))
+    def step_system(self, x, v, dt: float, mode: int = JAC_SPD, single: bool = False):
+        fn = LIB.weft_gpu_step_system_f32 if single else LIB.weft_gpu_step_system
+        _check(fn(self._ctx, _ptr(_f64(x)), _ptr(_f64(v)), C.c_double(dt), C.c_int32(mode)))
+        self._f32 = bool(single)
 
     # -- broad phase --------------------------------------------------------
     def set_soup(self, vertex_count: int, tris):

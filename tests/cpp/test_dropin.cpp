@@ -381,3 +381,75 @@ TEST_CASE("a Simulator-style loop on the drop-ins tracks the reference loop") {
     CHECK(err <= 1e-6);
   }
 }
+
+TEST_CASE("Precision::Single drop-ins: spmv_pipelined<float> bitwise, pcg_solve<float> and step_system<float> track the reference") {
+  oracle::Rng rng(31);
+  for (int n : {1, 2}) {
+    Engine engine(n);
+    ValidatedSchedule sched = n == 1 ? ValidatedSchedule() : ValidatedSchedule(generate_work_queues(FatTree::make(n)), n);
+    const int rows = 30;
+    const auto g64 = oracle::random_bell(rng, rows, 3);
+    std::vector<BlockEntry<float>> entries;
+    for (int r = 0; r < rows; ++r)
+      for (int s = 0; s < g64.ell_width(); ++s) {
+        const auto c = g64.col_at(r, s);
+        if (c == BellMatrix<double>::kNoBlock) break;
+        BlockEntry<float> e;
+        e.row = r;
+        e.col = c;
+        for (int i = 0; i < 3; ++i)
+          for (int j = 0; j < 3; ++j) e.m[static_cast<std::size_t>(3 * i + j)] = static_cast<float>(g64.value_at(r, s, i, j));
+        entries.push_back(e);
+      }
+    const auto parts = make_partitions(rows, n);
+    const auto split = partition_matrix(BellMatrix<float>::from_entries(rows, entries), parts);
+    std::vector<float> xg(static_cast<std::size_t>(3 * rows));
+    for (auto& v : xg) v = static_cast<float>(rng.uniform(-1.0, 1.0));
+    DistVector<float> x(&engine, parts), y(&engine, parts), yr(&engine, parts);
+    for (const auto& part : parts)
+      std::copy(xg.begin() + 3 * part.begin, xg.begin() + 3 * part.end, x.local(part.device_id).begin());
+    SpmvWorkspace<float> ws(n, split.padded_len);
+    gpu::spmv_pipelined(engine, split, sched, x, y, ws);
+    spmv_pipelined(engine, split, sched, x, yr, ws);
+    CHECK(y.gather() == yr.gather());
+  }
+  // step_system<float> + pcg_solve<float> on a small cloth vs the reference's
+  const auto mesh = make_grid_mesh(12, 12, 0.2, 0.2, Vec3(0, 0, 0), 0.15);
+  MaterialParams mat;
+  std::vector<std::uint8_t> pinned(static_cast<std::size_t>(mesh.vertex_count()), 0);
+  for (int i = 0; i < 12; ++i) pinned[static_cast<std::size_t>(i)] = 1;
+  SimState st = SimState::rest(mesh);
+  for (auto& v : st.v) v = Vec3(rng.uniform(-0.1, 0.1), rng.uniform(-0.1, 0.1), rng.uniform(-0.1, 0.1));
+  for (int n : {1, 2}) {
+    Engine engine(n);
+    ValidatedSchedule sched = n == 1 ? ValidatedSchedule() : ValidatedSchedule(generate_work_queues(FatTree::make(n)), n);
+    const Vec3 g(0, 0, -9.81), w(0, 0, 0);
+    auto sg = gpu::step_system<float>(engine, mesh, st, mat, pinned, {}, 1.0 / 240, g, w);
+    auto sr = step_system<float>(engine, mesh, st, mat, pinned, {}, 1.0 / 240, g, w);
+    const auto mg = gather_matrix(sg.matrix), mr = gather_matrix(sr.matrix);
+    CHECK(mg.block_rows() == mr.block_rows());
+    bool same = true;
+    for (int r = 0; r < mr.block_rows(); ++r)
+      for (int s = 0; s < mr.ell_width(); ++s) {
+        if (mr.col_at(r, s) != mg.col_at(r, s)) same = false;
+        if (mr.col_at(r, s) == BellMatrix<float>::kNoBlock) break;
+        for (int i = 0; i < 3; ++i)
+          for (int j = 0; j < 3; ++j) same = same && mr.value_at(r, s, i, j) == mg.value_at(r, s, i, j);
+      }
+    CHECK(same);  // SpdProjected: bitwise
+    PcgConfig cfg;
+    cfg.rel_tolerance = 1e-5;
+    DistVector<float> dg(&engine, sg.matrix.partitions), dr(&engine, sr.matrix.partitions);
+    const auto rg = gpu::pcg_solve(engine, sg.matrix, sched, sg.rhs, dg, cfg);
+    const auto rr = pcg_solve(engine, sr.matrix, sched, sr.rhs, dr, cfg);
+    CHECK(rg.converged);
+    CHECK(std::abs(rg.iterations - rr.iterations) <= 2);
+    const auto a = dg.gather(), b = dr.gather();
+    double diff = 0.0, mag = 0.0;
+    for (std::size_t i = 0; i < a.size(); ++i) {
+      diff = std::max(diff, std::abs(static_cast<double>(a[i]) - static_cast<double>(b[i])));
+      mag = std::max(mag, std::abs(static_cast<double>(b[i])));
+    }
+    CHECK(diff <= 1e-3 * mag);
+  }
+}

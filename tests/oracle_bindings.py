@@ -262,9 +262,13 @@ class Ref:
         self.lib.ref_system_free(C.c_void_p(h))
         return s
 
-    def fill_matrix(self, elems, x_cur, x_adv, vel, mass, pinned, dt, mode=JAC_SPD, n=1) -> System:
+    def fill_matrix(self, elems, x_cur, x_adv, vel, mass, pinned, dt, mode=JAC_SPD, n=1, single=False) -> System:
+        """fill_matrix<double>, or fill_matrix<float> with single=True (values
+        and rhs returned as the float values, exact in float64)."""
         st = C.c_int32()
-        h = self.lib.ref_fill_matrix(
+        fn = self.lib.ref_fill_matrix_f32 if single else self.lib.ref_fill_matrix
+        fn.restype = C.c_void_p
+        h = fn(
             C.c_int32(len(mass)), C.c_int32(n), C.c_int64(len(elems)), ptr(elems), ptr(x_cur), ptr(x_adv), ptr(vel),
             ptr(mass), ptr(pinned), C.c_double(dt), C.c_int32(mode), C.byref(st),
         )
