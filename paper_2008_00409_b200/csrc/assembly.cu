@@ -1525,8 +1525,7 @@ void fill_matrix_finish(Ctx& c) {
   const int big = INT32_MAX;
   int hbad = big;
   const int* bad = reinterpret_cast<const int*>(c.scalars.data() + 8);
-  WG_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
-  WG_CUDA(cudaStreamSynchronize(c.stream));
+  read_small(c, c.stream, {bad, &hbad, sizeof(int)});
   if (hbad != big) {
     c.has_matrix = false;
     c.has_rhs = false;

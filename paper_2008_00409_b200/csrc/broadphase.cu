@@ -45,6 +45,37 @@ __device__ __forceinline__ uint64_t pack_cell(int ix, int iy, int iz) {
          static_cast<uint64_t>(iz + kLatBias);
 }
 
+__global__ void k_read_small(const unsigned char* a, int na, const unsigned char* b, int nb, const unsigned char* d,
+                             int nd, unsigned char* out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  for (int i = 0; i < na; ++i) out[i] = a[i];
+  for (int i = 0; i < nb; ++i) out[128 + i] = b[i];
+  for (int i = 0; i < nd; ++i) out[256 + i] = d[i];
+}
+
+void read_small(Ctx& c, cudaStream_t s, SmallRead a, SmallRead b, SmallRead d) {
+  if (!c.map_host) {
+    WG_CUDA(cudaHostAlloc(&c.map_host, 384, cudaHostAllocMapped));
+    WG_CUDA(cudaHostGetDevicePointer(&c.map_dev, c.map_host, 0));
+  }
+  k_read_small<<<1, 32, 0, s>>>(static_cast<const unsigned char*>(a.src), a.bytes,
+                                static_cast<const unsigned char*>(b.src), b.bytes,
+                                static_cast<const unsigned char*>(d.src), d.bytes,
+                                static_cast<unsigned char*>(c.map_dev));
+  ++c.launches;
+  WG_CUDA(cudaGetLastError());
+  WG_CUDA(cudaStreamSynchronize(s));
+  const auto* h = static_cast<const volatile unsigned char*>(c.map_host);
+  auto take = [&](const SmallRead& r, int off) {
+    auto* o = static_cast<unsigned char*>(r.dst);
+    for (int i = 0; i < r.bytes; ++i) o[i] = h[off + i];
+  };
+  if (a.bytes > 128 || b.bytes > 128 || d.bytes > 128) throw Error(WEFT_ERR_INVALID, "read_small: > 128 bytes");
+  take(a, 0);
+  take(b, 128);
+  take(d, 256);
+}
+
 void set_soup(Ctx& c, int verts, int ntris, const int32_t* tris) {
   if (verts < 0 || ntris < 0) throw Error(WEFT_ERR_DIMENSION, "set_soup: negative size");
   std::vector<int32_t> h(3 * static_cast<size_t>(ntris));
@@ -623,10 +654,8 @@ void build_grid(Ctx& c, const double* x0, const double* x1, int mode, double thi
   if (T) k_lat_bounds<<<div_up(T, 256), 256, 0, ls(c)>>>(T, c.lat.data(), bounds);
   int64_t K = 0;
   int hb[6];
-  WG_CUDA(cudaMemcpyAsync(&K, c.ecount.data() + T, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-  WG_CUDA(cudaMemcpyAsync(hb, bounds, sizeof(hb), cudaMemcpyDeviceToHost, s));
-  WG_CUDA(cudaMemcpyAsync(&c.grid_cell_size, c.cell_size.data(), sizeof(double), cudaMemcpyDeviceToHost, s));
-  WG_CUDA(cudaStreamSynchronize(s));
+  read_small(c, s, {c.ecount.data() + T, &K, sizeof(int64_t)}, {bounds, hb, sizeof(hb)},
+             {c.cell_size.data(), &c.grid_cell_size, sizeof(double)});
   if (K > (int64_t(1) << 31) - 1) throw Error(WEFT_ERR_DIMENSION, "build_grid: more than 2^31 cell entries");
   KeyFrame f{0, 0, 0, 1, 1};
   int bits = 1;
@@ -673,8 +702,7 @@ void build_grid(Ctx& c, const double* x0, const double* x1, int mode, double thi
   t = scratch(c, tmp);
   WG_CUDA(cub::DeviceScan::ExclusiveSum(t, tmp, c.cell_flag.data(), c.cell_flag.data(), K + 1, s));
   int32_t cells32 = 0;
-  WG_CUDA(cudaMemcpyAsync(&cells32, c.cell_flag.data() + K, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-  WG_CUDA(cudaStreamSynchronize(s));
+  read_small(c, s, {c.cell_flag.data() + K, &cells32, sizeof(int32_t)});
   const int64_t cells = cells32;
   c.cell_keys.resize(static_cast<size_t>(cells) + 1);
   c.cell_off.resize(static_cast<size_t>(cells) + 1);
@@ -690,9 +718,8 @@ void build_grid(Ctx& c, const double* x0, const double* x1, int mode, double thi
   cub::DeviceScan::ExclusiveSum(nullptr, tmp, c.wprefix.data(), c.wprefix.data(), cells + 1, s);
   t = scratch(c, tmp);
   WG_CUDA(cub::DeviceScan::ExclusiveSum(t, tmp, c.wprefix.data(), c.wprefix.data(), cells + 1, s));
-  WG_CUDA(cudaMemcpyAsync(&c.grid_total, c.wprefix.data() + cells, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
   WG_CUDA(cudaGetLastError());
-  WG_CUDA(cudaStreamSynchronize(s));
+  read_small(c, s, {c.wprefix.data() + cells, &c.grid_total, sizeof(int64_t)});
   c.grid_entries = K;
   c.grid_cells = cells;
   c.has_grid = true;
@@ -927,8 +954,7 @@ int64_t candidates(Ctx& c, int64_t begin, int64_t end, int32_t* pairs_out, bool 
   void* t = scratch(c, tmp);
   WG_CUDA(cub::DeviceScan::ExclusiveSum(t, tmp, c.cand_count.data(), c.cand_count.data(), cells + 1, s));
   int64_t n = 0;
-  WG_CUDA(cudaMemcpyAsync(&n, c.cand_count.data() + cells, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-  WG_CUDA(cudaStreamSynchronize(s));
+  read_small(c, s, {c.cand_count.data() + cells, &n, sizeof(int64_t)});
   if (count_only) return n;  // the walk's count pass is the whole result
   c.cand_pairs.resize(2 * static_cast<size_t>(n) + 2);
   k_cell_walk<true><<<blocks, kWalkWarps * 32, 0, ls(c)>>>(w, nullptr, c.cand_count.data(),

@@ -178,6 +178,7 @@ weft_status weft_gpu_destroy(weft_gpu_ctx* ctx) {
     WG_CUDA(cudaStreamSynchronize(c.side));
     for (auto& e : c.ev) cudaEventDestroy(e);
     for (auto& e : c.ev_side) cudaEventDestroy(e);
+    if (c.map_host) cudaFreeHost(c.map_host);
     cudaStreamDestroy(c.side);
     cudaStreamDestroy(c.stream);
   });

@@ -189,6 +189,10 @@ struct Ctx {
   DBuf<uint64_t> sc_pat_k1, sc_pat_k2;
   DBuf<uint8_t> sc_sel_flag;
 
+  // ---- small device->host reads through mapped pinned memory (read_small)
+  void* map_host = nullptr;
+  void* map_dev = nullptr;
+
   // ---- CUB scratch (one per stream)
   DBuf<unsigned char> scratch;
   DBuf<unsigned char> scratch_side;
@@ -336,6 +340,16 @@ int64_t collide(Ctx& c, const double* x0, const double* x1, int mode, double thi
 
 // CUB scratch helper
 void* scratch(Ctx& c, size_t bytes);
+// Reads up to three small device values (bytes each <= 128) on stream s and
+// waits: a one-thread kernel stores them into mapped pinned host memory, so
+// the read never queues on a copy engine behind a large transfer (the e2e
+// step's 40 MB read-back runs concurrently with the CCD broad phase).
+struct SmallRead {
+  const void* src;
+  void* dst;
+  int bytes;
+};
+void read_small(Ctx& c, cudaStream_t s, SmallRead a, SmallRead b = {}, SmallRead d = {});
 
 }  // namespace weft_gpu
 

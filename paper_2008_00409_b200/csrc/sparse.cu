@@ -761,7 +761,7 @@ __device__ void finalize_sums(const PartBlocks& pb, const double* partials, doub
 // ---------------------------------------------------------------------------
 // PCG
 // ---------------------------------------------------------------------------
-struct PcgState {
+struct PcgState {  // read back with read_small (<= 128 bytes)
   double rho, alpha, beta, b_norm, tol, r_norm;
   int iter;       // completed iterations
   int done;       // 1 = stop (converged, error, or max iterations)
@@ -2007,9 +2007,12 @@ PcgResult pcg_solve(Ctx& c, const double* b_dev, const weft_pcg_config& cfg, dou
   }
   double hd[2] = {0.0, 0.0};
   int asym = 1;
-  if (rows > 0) WG_CUDA(cudaMemcpyAsync(hd, dots, sizeof(hd), cudaMemcpyDeviceToHost, s));
-  if (rows > 0 && persistent && bj) WG_CUDA(cudaMemcpyAsync(&asym, dinv_asym, sizeof(int), cudaMemcpyDeviceToHost, s));
-  WG_CUDA(cudaStreamSynchronize(s));
+  if (rows > 0 && persistent && bj)
+    read_small(c, s, {dots, hd, sizeof(hd)}, {dinv_asym, &asym, sizeof(int)});
+  else if (rows > 0)
+    read_small(c, s, {dots, hd, sizeof(hd)});
+  else
+    WG_CUDA(cudaStreamSynchronize(s));
   comm_check(c);
   PcgResult res;
   const double b_norm = std::sqrt(hd[0]);
@@ -2120,8 +2123,7 @@ PcgResult pcg_solve(Ctx& c, const double* b_dev, const weft_pcg_config& cfg, dou
     ++c.launches;
     if (c.profile) WG_CUDA(cudaEventRecord(c.ev[7], s));
     k_scatter_rows<<<div_up(rows, threads), threads, 0, ls(c)>>>(rows, c.A.perm.data(), c.xp.data(), c.xs.data());
-    WG_CUDA(cudaMemcpyAsync(hs, c.pcg, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
-    WG_CUDA(cudaStreamSynchronize(s));
+    read_small(c, s, {c.pcg, hs, sizeof(PcgState)});
     if (args.timing && hs->iter) {
       unsigned long long t[4];
       WG_CUDA(cudaMemcpy(t, args.timing, sizeof(t), cudaMemcpyDeviceToHost));
