@@ -745,7 +745,22 @@ struct WalkArgs {
   const int32_t* __restrict__ cell_tris;
   const uint64_t* __restrict__ cell_keys;
   const int* __restrict__ lat;
+  // narrow-phase feed (null: every candidate): only pairs whose conservative
+  // float boxes are within `margin` are emitted — the whole-pair rejection
+  // k_narrow applies first (narrow.cu), so the same hits; the unfiltered
+  // candidate count still goes to *all_count
+  const float4* __restrict__ tbox;
+  double margin;
+  unsigned long long* __restrict__ all_count;
 };
+
+__device__ __forceinline__ bool boxes_apart(const float4* __restrict__ tbox, int t1, int t2, double margin) {
+  const float4 la = __ldg(tbox + 2 * t1), ha = __ldg(tbox + 2 * t1 + 1);
+  const float4 lb = __ldg(tbox + 2 * t2), hb = __ldg(tbox + 2 * t2 + 1);
+  return (double)la.x > (double)hb.x + margin || (double)lb.x > (double)ha.x + margin ||
+         (double)la.y > (double)hb.y + margin || (double)lb.y > (double)ha.y + margin ||
+         (double)la.z > (double)hb.z + margin || (double)lb.z > (double)ha.z + margin;
+}
 
 // row i of the upper triangle starts at local index i*s - i(i+1)/2
 __device__ __forceinline__ int64_t tri_start(int64_t i, int64_t s) { return i * s - i * (i + 1) / 2; }
@@ -766,7 +781,8 @@ constexpr int kBitsetMax = 256;
 template <bool kWrite>
 __device__ __forceinline__ int64_t walk_bitset(int s, int lane, int64_t l0, int64_t l1, const int32_t* __restrict__ tl,
                                                const int* __restrict__ lat, int cx, int cy, int cz, int* sm_id,
-                                               unsigned* sm_set, int64_t o, int2* __restrict__ out) {
+                                               unsigned* sm_set, int64_t o, int2* __restrict__ out,
+                                               const float4* __restrict__ tbox, double margin, int64_t& nall) {
   constexpr int G = kBitsetMax / 32;
   const int ng = (s + 31) >> 5;
   int m[G];
@@ -797,19 +813,31 @@ __device__ __forceinline__ int64_t walk_bitset(int s, int lane, int64_t l0, int6
     int c = 0;
     int64_t jlo = 0, jhi = 0;
     const unsigned* Sr = sm_set + (7 & ~m[h]) * G;
+    int call = 0;
     if (i < s) {
       // the split range: the local index of (i, j) is tri_start(i, s) + j - i - 1
       const int64_t rs = tri_start(i, s);
       jlo = max(l0 - rs + i + 1, static_cast<int64_t>(i + 1));
       jhi = min(l1 - rs + i + 1, static_cast<int64_t>(s));
+      const int ti = tbox ? sm_id[i] : 0;
       for (int g = static_cast<int>(jlo >> 5); g < ng && 32 * g < jhi; ++g) {
         unsigned bits = Sr[g];
         const int64_t b0 = jlo - 32 * g, b1 = jhi - 32 * g;  // keep bits in [b0, b1)
         if (b0 > 0) bits &= ~0u << b0;
         if (b1 < 32) bits &= (1u << b1) - 1u;
-        c += __popc(bits);
+        call += __popc(bits);
+        if (tbox) {
+          while (bits) {
+            const int j = 32 * g + __ffs(bits) - 1;
+            bits &= bits - 1;
+            c += boxes_apart(tbox, ti, sm_id[j], margin) ? 0 : 1;
+          }
+        } else {
+          c += __popc(bits);
+        }
       }
     }
+    nall += __reduce_add_sync(0xffffffffu, call);
     if (kWrite) {
       int x = c;  // inclusive scan of the rows' counts (row order = lane order)
 #pragma unroll
@@ -828,7 +856,8 @@ __device__ __forceinline__ int64_t walk_bitset(int s, int lane, int64_t l0, int6
           while (bits) {
             const int j = 32 * g + __ffs(bits) - 1;
             bits &= bits - 1;
-            out[w++] = make_int2(ti, sm_id[j]);
+            const int tj = sm_id[j];
+            if (!tbox || !boxes_apart(tbox, ti, tj, margin)) out[w++] = make_int2(ti, tj);
           }
         }
       }
@@ -863,9 +892,13 @@ __global__ void __launch_bounds__(kWalkWarps * 32) k_cell_walk(WalkArgs w, int64
     const int cz = static_cast<int>(key & 0x1FFFFF) - static_cast<int>(kLatBias);
     if (s <= kBitsetMax) {  // bitset walk (above)
       const int64_t l0 = lo - p0, l1 = hi - p0;
+      int64_t nall = 0;
       n = walk_bitset<kWrite>(static_cast<int>(s), lane, l0, l1, tl, w.lat, cx, cy, cz, sm_id[warp], sm_set[warp], o,
-                              out);
-      if (!kWrite && lane == 0) counts[cell] = n;
+                              out, w.tbox, w.margin, nall);
+      if (!kWrite && lane == 0) {
+        counts[cell] = n;
+        if (w.all_count) atomicAdd(w.all_count, static_cast<unsigned long long>(nall));
+      }
       return;
     }
     const bool staged = s <= kWalkStage;
@@ -908,6 +941,11 @@ __global__ void __launch_bounds__(kWalkWarps * 32) k_cell_walk(WalkArgs w, int64
         load(j, t2, c);
         hit = max(a.x, c.x) == cx && max(a.y, c.y) == cy && max(a.z, c.z) == cz;
       }
+      if (w.tbox) {
+        const unsigned ma = __ballot_sync(0xffffffffu, hit);
+        if (!kWrite && lane == 0 && w.all_count) atomicAdd(w.all_count, static_cast<unsigned long long>(__popc(ma)));
+        if (hit && boxes_apart(w.tbox, t1, t2, w.margin)) hit = false;
+      }
       const unsigned m = __ballot_sync(0xffffffffu, hit);
       if (kWrite && hit) out[o + __popc(m & ((1u << lane) - 1u))] = make_int2(t1, t2);
       o += __popc(m);
@@ -936,15 +974,18 @@ __global__ void __launch_bounds__(kWalkWarps * 32) k_cell_walk(WalkArgs w, int64
 // Returns the candidate count of [begin, end); when pairs_out is non-null
 // the pairs are written there (device or host pointer). Device-resident
 // pairs stay in c.cand_pairs.
-int64_t candidates(Ctx& c, int64_t begin, int64_t end, int32_t* pairs_out, bool count_only) {
+int64_t candidates(Ctx& c, int64_t begin, int64_t end, int32_t* pairs_out, bool count_only, const float4* tbox,
+                   double margin, int64_t* all) {
   if (!c.has_grid) throw Error(WEFT_ERR_INVALID, "candidates: build_grid first");
   begin = std::max<int64_t>(begin, 0);
   end = std::min<int64_t>(end, c.grid_total);
   if (begin >= end) return 0;
   cudaStream_t s = c.cur;
   const int64_t cells = c.grid_cells;
+  c.cand_all.resize(1);
+  if (tbox) WG_CUDA(cudaMemsetAsync(c.cand_all.data(), 0, sizeof(unsigned long long), s));
   WalkArgs w{begin, end, cells, c.wprefix.data(), c.cell_off.data(), c.vals_b.data(), c.cell_keys.data(),
-             c.lat.data()};
+             c.lat.data(), tbox, margin, tbox ? c.cand_all.data() : nullptr};
   c.cand_count.resize(static_cast<size_t>(cells) + 1);
   WG_CUDA(cudaMemsetAsync(c.cand_count.data() + cells, 0, sizeof(int64_t), s));
   const int blocks = div_up(cells, kWalkWarps);
@@ -954,7 +995,14 @@ int64_t candidates(Ctx& c, int64_t begin, int64_t end, int32_t* pairs_out, bool 
   void* t = scratch(c, tmp);
   WG_CUDA(cub::DeviceScan::ExclusiveSum(t, tmp, c.cand_count.data(), c.cand_count.data(), cells + 1, s));
   int64_t n = 0;
-  read_small(c, s, {c.cand_count.data() + cells, &n, sizeof(int64_t)});
+  if (tbox && all) {
+    unsigned long long na = 0;
+    read_small(c, s, {c.cand_count.data() + cells, &n, sizeof(int64_t)}, {c.cand_all.data(), &na, sizeof(na)});
+    *all = static_cast<int64_t>(na);
+  } else {
+    read_small(c, s, {c.cand_count.data() + cells, &n, sizeof(int64_t)});
+    if (all) *all = n;
+  }
   if (count_only) return n;  // the walk's count pass is the whole result
   c.cand_pairs.resize(2 * static_cast<size_t>(n) + 2);
   k_cell_walk<true><<<blocks, kWalkWarps * 32, 0, ls(c)>>>(w, nullptr, c.cand_count.data(),

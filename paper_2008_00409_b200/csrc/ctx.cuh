@@ -165,6 +165,7 @@ struct Ctx {
   int64_t grid_entries = 0, grid_cells = 0, grid_total = 0;
   double grid_cell_size = 0.0;
   DBuf<int64_t> cand_count;
+  DBuf<unsigned long long> cand_all;  // unfiltered candidates of a filtered walk
   DBuf<int32_t> cand_pairs;
   bool has_grid = false;
 
@@ -293,7 +294,11 @@ void fill_matrix_finish(Ctx& c);
 
 void set_soup(Ctx& c, int verts, int ntris, const int32_t* tris);
 void build_grid(Ctx& c, const double* x0_dev, const double* x1_dev, int mode, double thickness, double cell_scale);
-int64_t candidates(Ctx& c, int64_t begin, int64_t end, int32_t* pairs_dev_or_null, bool count_only = false);
+// tbox (narrow phase): emit only the candidates whose conservative float
+// boxes are within margin (k_narrow's whole-pair rejection); *all gets the
+// unfiltered candidate count.
+int64_t candidates(Ctx& c, int64_t begin, int64_t end, int32_t* pairs_dev_or_null, bool count_only = false,
+                   const float4* tbox = nullptr, double margin = 0.0, int64_t* all = nullptr);
 
 void serial_sum(Ctx& c, int n, const double* d_host, double* exact, double* naive, int fast);
 
