@@ -232,10 +232,14 @@ __device__ __forceinline__ void row_product(const SellView& A, int lr, int ngrou
   int cg = 0;
   unsigned seen = 0;
   y0 = y1 = y2 = 0.0;
+  // the column word of slot k+1 is fetched while slot k is processed, so a
+  // slot's gathers only wait on their own round trip (as row_product_1)
+  int pn = len > 0 ? __ldg(A.cols + base) : 0;
 #pragma unroll kMgUnroll
   for (int k = 0; k < len; ++k) {
     const int64_t at = base + (int64_t)k * kSlice;
-    const int packed = __ldg(A.cols + at);
+    const int packed = pn;
+    if (k + 1 < len) pn = __ldg(A.cols + at + kSlice);
     const int c = packed & kColMask;
     const int g = (int)((unsigned)packed >> kGroupShift);
     while (cg < g) {
