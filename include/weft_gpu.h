@@ -131,6 +131,13 @@ weft_status weft_gpu_rank_info(weft_gpu_ctx* ctx, weft_rank_info* info);
 /* Partitions and schedule (proj/src/exec.cpp:10-27, proj/src/topology.cpp)*/
 /* ---------------------------------------------------------------------- */
 
+/* Hinge angle probes (tests and tools). The reference's hinge angle is
+ * std::atan2(s, c) (proj/src/elements.cpp:116); the library evaluates it as
+ * a correctly rounded double atan2 (csrc/cr_atan2.cuh). _host runs the same
+ * code compiled for the CPU; the _gpu variant runs it on the context's
+ * device (x, y, out host or device pointers). */
+weft_status weft_hinge_atan2_host(int64_t n, const double* y, const double* x, double* out);
+weft_status weft_gpu_hinge_atan2(weft_gpu_ctx* ctx, int64_t n, const double* y, const double* x, double* out);
 /* make_partitions (exec.cpp:10-23): begin/end arrays of length `devices`. */
 weft_status weft_make_partitions(int32_t vertex_count, int32_t devices, int32_t* begin, int32_t* end);
 /* generate_work_queues(FatTree::make(n)) (topology.cpp:79-89): for device

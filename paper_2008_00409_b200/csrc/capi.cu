@@ -6,6 +6,7 @@
 #include <string>
 #include <vector>
 
+#include "cr_atan2.cuh"
 #include "ctx.cuh"
 
 namespace {
@@ -57,6 +58,12 @@ void gen_range(int lo, int hi, std::vector<std::vector<int>>& peer, std::vector<
   }
 }
 
+__global__ void k_hinge_atan2(const double* __restrict__ y, const double* __restrict__ x, double* __restrict__ out,
+                              int64_t n) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i < n) out[i] = weft_gpu::cr::atan2(y[i], x[i]);
+}
+
 }  // namespace
 
 extern "C" {
@@ -66,6 +73,30 @@ const char* weft_gpu_last_error(void) { return g_last_error.c_str(); }
 weft_status weft_gpu_internal_set_error(const char* msg, weft_status s) {
   g_last_error = msg;
   return s;
+}
+
+weft_status weft_hinge_atan2_host(int64_t n, const double* y, const double* x, double* out) {
+  return guard(nullptr, [&] {
+    need(n >= 0, WEFT_ERR_DIMENSION, "negative count");
+    for (int64_t i = 0; i < n; ++i) out[i] = weft_gpu::cr::atan2(y[i], x[i]);
+  });
+}
+
+weft_status weft_gpu_hinge_atan2(weft_gpu_ctx* ctx, int64_t n, const double* y, const double* x, double* out) {
+  return guard(ctx, [&] {
+    need(n >= 0, WEFT_ERR_DIMENSION, "negative count");
+    if (n == 0) return;
+    auto& c = ctx->c;
+    weft_gpu::DBuf<double> buf;
+    buf.resize(static_cast<size_t>(3 * n));
+    WG_CUDA(cudaMemcpyAsync(buf.data(), y, sizeof(double) * n, cudaMemcpyDefault, c.stream));
+    WG_CUDA(cudaMemcpyAsync(buf.data() + n, x, sizeof(double) * n, cudaMemcpyDefault, c.stream));
+    k_hinge_atan2<<<static_cast<unsigned>((n + 255) / 256), 256, 0, c.stream>>>(buf.data(), buf.data() + n,
+                                                                               buf.data() + 2 * n, n);
+    WG_CUDA(cudaGetLastError());
+    WG_CUDA(cudaMemcpyAsync(out, buf.data() + 2 * n, sizeof(double) * n, cudaMemcpyDefault, c.stream));
+    WG_CUDA(cudaStreamSynchronize(c.stream));
+  });
 }
 
 weft_status weft_make_partitions(int32_t p, int32_t n, int32_t* begin, int32_t* end) {

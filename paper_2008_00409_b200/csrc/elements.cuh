@@ -8,11 +8,16 @@
 // strict left-to-right 3-term reductions, scalar chains evaluated before the
 // vector product) and the library is built with -fmad=false, so the
 // assembled matrix is bitwise equal to the CPU reference. The only
-// non-bitwise quantity is the hinge angle (CUDA atan2 vs glibc atan2),
-// which enters the right-hand side and the Exact-mode bend Hessian scale.
+// non-bitwise quantity is the hinge angle: glibc's atan2 is not correctly
+// rounded (about 1 draw in 10^3 lands 1 ulp off), so no device atan2 can
+// reproduce it everywhere; cr::atan2 (cr_atan2.cuh) is correctly rounded,
+// which agrees with glibc on all but ~1e-5 of near-flat hinges (CUDA's
+// 2-ulp atan2 disagreed far more often). The angle enters the right-hand
+// side and the Exact-mode bend Hessian scale.
 #pragma once
 
 #include "common.cuh"
+#include "cr_atan2.cuh"
 
 namespace weft_gpu {
 
@@ -146,7 +151,7 @@ __device__ __forceinline__ double dihedral_angle(V3 x0, V3 x1, V3 x2, V3 x3) {
   if (dot(na, na) < kDeg || dot(nb, nb) < kDeg || elen < 1e-12) return 0.0;
   const double s = dot(cross(na, nb), e) / elen;
   const double c = dot(na, nb);
-  return atan2(s, c);
+  return cr::atan2(s, c);
 }
 
 // Forward-mode dual (elements.cpp:13-30)

@@ -72,3 +72,40 @@ def cloth_problem(ref, seed: int, max_side: int = 6, contacts: int = 0, damping=
     mass = mesh["vertex_mass"].copy()
     ref.free_mesh(mesh)
     return dict(elems=elems, x=x, x_adv=x_adv, v=v, mass=mass, pinned=pinned, dt=dt, p=p)
+
+
+def hinge_atan2_split_vertices(elems: np.ndarray, positions) -> set:
+    """Vertices of the bend elements whose hinge angle is a case where glibc's
+    atan2 (the reference, proj/src/elements.cpp:116) and the library's
+    correctly rounded atan2 disagree, at any of the given position arrays.
+
+    (s, c) are formed exactly as dihedral_angle does it (elements.cpp:105-117,
+    same operation order; numpy float64 elementwise ops round like the
+    library's -fmad=false build), then both atan2s are evaluated: glibc via
+    math.atan2, the library's via its host build."""
+    import ctypes
+    import math
+    import os
+    lib = ctypes.CDLL(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                   "paper_2008_00409_b200", "libweft_gpu.so"))
+    bends = elems[elems["kind"] == 1]
+    st = bends["stencil"]
+    out = set()
+    for pos in positions:
+        x = np.asarray(pos, dtype=np.float64).reshape(-1, 3)
+        x0, x1, x2, x3 = (x[st[:, i]] for i in range(4))
+        cross = lambda a, b: np.stack([a[:, 1] * b[:, 2] - a[:, 2] * b[:, 1], a[:, 2] * b[:, 0] - a[:, 0] * b[:, 2],
+                                       a[:, 0] * b[:, 1] - a[:, 1] * b[:, 0]], 1)
+        dot = lambda a, b: a[:, 0] * b[:, 0] + a[:, 1] * b[:, 1] + a[:, 2] * b[:, 2]
+        e = x1 - x0
+        na = cross(e, x2 - x0)
+        nb = cross(x3 - x0, e)
+        s = np.ascontiguousarray(dot(cross(na, nb), e) / np.sqrt(dot(e, e)))
+        c = np.ascontiguousarray(dot(na, nb))
+        mine = np.empty_like(s)
+        assert lib.weft_hinge_atan2_host(ctypes.c_int64(len(s)), ctypes.c_void_p(s.ctypes.data),
+                                         ctypes.c_void_p(c.ctypes.data), ctypes.c_void_p(mine.ctypes.data)) == 0
+        glibc = np.array([math.atan2(a, b) for a, b in zip(s.tolist(), c.tolist())])
+        for k in np.nonzero(mine != glibc)[0]:
+            out.update(int(v) for v in st[k])
+    return out

@@ -1,6 +1,9 @@
-"""GPU assembly parity: pattern + matrix bitwise vs the reference (golden
-fixtures) and the C oracle; rhs within 1e-12 relative (hinge angles use CUDA
-atan2, the reference glibc atan2)."""
+"""GPU assembly parity: pattern, matrix and rhs bitwise vs the reference
+(golden fixtures) and the C oracle, in SpdProjected and Exact modes. The
+hinge angle uses a correctly rounded atan2 and the reference glibc's, which
+is not (tests/test_hinge_atan2.py): they agree on these inputs; at config D
+a handful of near-midpoint hinges differ by one ulp (test_gpu_configD.py
+counts them)."""
 import glob
 import os
 
@@ -8,7 +11,7 @@ import numpy as np
 import pytest
 
 from oracle_bindings import ELEMENT_DTYPE, JAC_EXACT, JAC_SPD, ORACLE
-from problems import contact_elements, with_drag
+from problems import contact_elements, hinge_atan2_split_vertices, with_drag
 
 pytestmark = pytest.mark.gpu
 GOLD = os.path.join(os.path.dirname(__file__), "golden")
@@ -32,11 +35,6 @@ def gpu_fill(weft, n, elems, x, xa, v, mass, pinned, dt, mode, contacts=None):
     return eng, m
 
 
-def rhs_close(a, b):
-    scale = max(np.abs(b).max(), 1e-12)
-    return np.abs(a - b).max() <= 1e-12 * scale
-
-
 @pytest.mark.parametrize("path", sorted(glob.glob(os.path.join(GOLD, "assembly_*.npz"))))
 @pytest.mark.parametrize("mode,tag", [(JAC_SPD, "spd"), (JAC_EXACT, "exact")])
 @pytest.mark.parametrize("n", [1, 2, 4])
@@ -48,12 +46,31 @@ def test_assembly_vs_reference_golden(weft, path, mode, tag, n):
     eng, m = gpu_fill(weft, n, elems[:k], g["x"], g["x_adv"], g["v"], g["mass"], g["pinned"], float(g["dt"]), mode,
                       elems[k:] if k < len(elems) else None)
     assert np.array_equal(m.row_ptr, g[f"{tag}_row_ptr"]) and np.array_equal(m.cols, g[f"{tag}_cols"])
-    if mode == JAC_SPD:
-        assert np.array_equal(m.vals, g[f"{tag}_vals"])
-    else:  # the Exact bend Hessian is scaled by (theta - theta0): atan2
-        assert np.abs(m.vals - g[f"{tag}_vals"]).max() <= 1e-12 * np.abs(g[f"{tag}_vals"]).max()
-    assert rhs_close(m.rhs, g[f"{tag}_rhs"])
+    # Exact mode scales the bend Hessian by (theta - theta0) and the rhs
+    # carries the bend force: both go through the hinge atan2 and are
+    # bitwise on these fixtures.
+    assert np.array_equal(m.vals.view(np.int64), g[f"{tag}_vals"].view(np.int64))
+    assert np.array_equal(m.rhs.view(np.int64), g[f"{tag}_rhs"].view(np.int64)), \
+        f"{int((m.rhs != g[f'{tag}_rhs']).sum())} rhs entries differ (hinge atan2 1-ulp case?)"
     eng.close()
+
+
+def test_hinge_atan2_device_equals_host(weft):
+    """The device build of cr::atan2 is bitwise the host build (no
+    contraction or fast-math difference between them)."""
+    import ctypes
+    lib = weft.LIB
+    rng = np.random.default_rng(4)
+    n = 1 << 20
+    y = np.concatenate([rng.uniform(-1, 1, n), rng.uniform(-1e-6, 1e-6, n), rng.uniform(-1, 1, n) * 1e-200])
+    x = np.concatenate([rng.uniform(-1, 1, n), rng.uniform(1e-5, 1e-4, n), rng.uniform(-1, 1, n) * 1e200])
+    host, dev = np.empty_like(y), np.empty_like(y)
+    p = lambda a: ctypes.c_void_p(a.ctypes.data)
+    assert lib.weft_hinge_atan2_host(ctypes.c_int64(len(y)), p(y), p(x), p(host)) == 0
+    eng = weft.Engine(1)
+    assert lib.weft_gpu_hinge_atan2(eng._ctx, ctypes.c_int64(len(y)), p(y), p(x), p(dev)) == 0
+    eng.close()
+    assert np.array_equal(host.view(np.int64), dev.view(np.int64))
 
 
 def layered_problem(weft, layers=3, nx=24, contacts=40, seed=5, drag=True, damping=0.002):
@@ -75,6 +92,24 @@ def layered_problem(weft, layers=3, nx=24, contacts=40, seed=5, drag=True, dampi
     return dict(elems=elems, contacts=cts, x=x, xa=xa, v=v, mass=mesh.vertex_mass, pinned=sc.pinned, dt=dt)
 
 
+def assert_bitwise_but_split_hinges(m, o, pr):
+    """Bitwise, except rows/blocks touching a hinge whose angle glibc rounds
+    differently from the correctly rounded atan2 (one ulp of the angle)."""
+    dv = np.nonzero((m.vals.view(np.int64) != o.vals.view(np.int64)).reshape(len(m.cols), -1).any(axis=1))[0]
+    dr = np.nonzero(m.rhs.view(np.int64) != o.rhs.view(np.int64))[0]
+    if len(dv) == 0 and len(dr) == 0:
+        return
+    split = hinge_atan2_split_vertices(pr["elems"], [pr["x"], pr["xa"]])
+    rows_r = set((dr // 3).tolist())
+    assert rows_r <= split, sorted(rows_r - split)[:10]
+    blk = dv
+    brow = np.searchsorted(m.row_ptr, blk, side="right") - 1
+    bad = [(int(r), int(c)) for r, c in zip(brow, m.cols[blk]) if int(r) not in split or int(c) not in split]
+    assert not bad, bad[:10]
+    rel = np.abs(m.rhs - o.rhs).max() / np.abs(o.rhs).max()
+    assert rel <= 1e-12
+
+
 @pytest.mark.parametrize("contacts", [0, 50])
 @pytest.mark.parametrize("mode", [JAC_SPD, JAC_EXACT])
 def test_assembly_vs_oracle_layered(weft, contacts, mode):
@@ -86,11 +121,7 @@ def test_assembly_vs_oracle_layered(weft, contacts, mode):
         eng, m = gpu_fill(weft, n, pr["elems"], pr["x"], pr["xa"], pr["v"], pr["mass"], pr["pinned"], pr["dt"], mode,
                           pr["contacts"])
         assert np.array_equal(m.row_ptr, o.row_ptr) and np.array_equal(m.cols, o.cols)
-        if mode == JAC_SPD:
-            assert np.array_equal(m.vals, o.vals)
-        else:
-            assert np.abs(m.vals - o.vals).max() <= 1e-12 * np.abs(o.vals).max()
-        assert rhs_close(m.rhs, o.rhs)
+        assert_bitwise_but_split_hinges(m, o, pr)
         mats.append(m)
         eng.close()
     # partition independence of the gathered matrix (test_assembly.cpp:263-280)
