@@ -35,6 +35,9 @@ struct SellMatrix {
   int64_t colp_id = -1;     // layout colp was built for
   DBuf<int16_t> colp16;     // total: colp as offsets from the row position (when all fit 16 bits)
   bool colp16_ok = false;   // ... for the layout colp_id
+  DBuf<int32_t> pair_at;    // total: slot of each lower block's transposed twin, -1 none (layout pair_id)
+  int64_t pair_id = -1;
+  DBuf<uint32_t> mwords;    // total: column offset | twin slot delta of blocks bitwise equal to it (per solve)
   DBuf<int32_t> cols;       // total (packed col | group << 28; -1 padding)
   DBuf<double> vals;        // 9 * total
   DBuf<float> vals32;       // 9 * total: the values of a Precision::Single system
@@ -210,6 +213,7 @@ struct Ctx {
   int64_t pcg_iterations = 0;     // their iterations
   double pcg_ms = 0.0;            // their summed device time
   double pcg_bytes = 0.0;         // their summed algorithmic bytes
+  int64_t pcg_mirrored = 0;       // blocks the last mirrored persistent solve read from their twins
   std::vector<cudaEvent_t> prof_ev;
 
   // ---- resident simulation state

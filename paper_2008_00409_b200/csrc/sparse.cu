@@ -116,6 +116,11 @@ __device__ __forceinline__ int ld_nc_hint(const int* p, uint64_t pol) {
   asm volatile("ld.global.nc.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
   return v;
 }
+__device__ __forceinline__ uint32_t ld_nc_hint(const uint32_t* p, uint64_t pol) {
+  uint32_t v;
+  asm volatile("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+  return v;
+}
 __device__ __forceinline__ int ld_nc_hint(const int16_t* p, uint64_t pol) {
   short v;
   asm volatile("ld.global.nc.L2::cache_hint.s16 %0, [%1], %2;" : "=h"(v) : "l"(p), "l"(pol));
@@ -946,6 +951,7 @@ struct PcgArgs {
   const double* dinv6;  // persistent solve: packed symmetric D^-1 (null: 9-double form)
   float vec_el_frac;    // persistent solve: fraction of the gathered z / p lines kept evict_last
   const int16_t* colp16;  // persistent solve: 16-bit column offsets (null: A.cols)
+  const uint32_t* mwords;  // persistent solve, kMir: column offset (low 16) | mirror slot delta (high 16)
   unsigned long long* timing;  // dev instrumentation (WEFT_PCG_TIMING=1): ns per phase, summed
 };
 
@@ -1501,10 +1507,19 @@ __device__ __forceinline__ void vstore3(double* v, int i, double a, double b, do
 // kC16: the column words as 16-bit offsets from the row's own position
 // (c16, built per layout when every column of the system is within +-32767
 // positions: 2 instead of 4 streamed bytes per block).
-template <int PMode, int kUnroll, int Vs, bool kC16>
+//
+// kMir: the column word is 32 bits, the 16-bit column offset in the low half
+// and in the high half the slot distance to the block's transposed twin
+// (0: read the own block). A lower-triangle block that is bitwise the
+// transpose of its upper twin is read from the twin, which the wavefront
+// order streamed from HBM moments earlier: the second read is an L2 hit, so
+// the symmetric part of the matrix crosses HBM once per iteration. Same
+// values, same products, same order: bitwise the plain product.
+template <int PMode, int kUnroll, int Vs, bool kC16, bool kMir = false>
 __device__ __forceinline__ void row_product_cg(const SellView& A, int r, const double* __restrict__ z,
                                                const double* __restrict__ pold, double beta, double& y0, double& y1,
-                                               double& y2, float vec_frac, const int16_t* __restrict__ c16) {
+                                               double& y2, float vec_frac, const int16_t* __restrict__ c16,
+                                               const uint32_t* __restrict__ cm = nullptr) {
 #if WEFT_MAT_EF
   const uint64_t mpol = l2_policy_evict_first();
 #endif
@@ -1518,16 +1533,41 @@ __device__ __forceinline__ void row_product_cg(const SellView& A, int r, const d
     if constexpr (kC16) return r + WEFT_MAT_LD(c16 + at);
     else return WEFT_MAT_LD(A.cols + at) & kColMask;
   };
-  int cn = len > 0 ? col(base) : 0;
+  uint32_t wn = 0;
+  int cn = 0;
+  if constexpr (kMir) wn = len > 0 ? __ldg(cm + base) : 0u;
+  else cn = len > 0 ? col(base) : 0;
 #pragma unroll kUnroll
   for (int k = 0; k < len; ++k) {
     const int64_t at = base + (int64_t)k * kSlice;
-    const int c = cn;
-    if (k + 1 < len) cn = col(at + kSlice);
-    const double* v = A.vals + vidx(at, r & 31, 0);
-    const double v0 = WEFT_MAT_LD(v), v1 = WEFT_MAT_LD(v + 32), v2 = WEFT_MAT_LD(v + 64);
-    const double v3 = WEFT_MAT_LD(v + 96), v4 = WEFT_MAT_LD(v + 128), v5 = WEFT_MAT_LD(v + 160);
-    const double v6 = WEFT_MAT_LD(v + 192), v7 = WEFT_MAT_LD(v + 224), v8 = WEFT_MAT_LD(v + 256);
+    int c;
+    const double* v;
+    int sa = 96, sb = 32;  // element (i, j) of the block at v + sa * i + sb * j
+    if constexpr (kMir) {
+      const uint32_t w = wn;
+      if (k + 1 < len) wn = __ldg(cm + at + kSlice);
+      c = r + static_cast<int>(static_cast<int16_t>(w & 0xffffu));
+      const int d = static_cast<int>(static_cast<int16_t>(w >> 16));
+      v = A.vals + (d ? vidx(at + d, c & 31, 0) : vidx(at, r & 31, 0));
+      if (d) {
+        sa = 32;
+        sb = 96;
+      }
+
+    } else {
+      c = cn;
+      if (k + 1 < len) cn = col(at + kSlice);
+      v = A.vals + vidx(at, r & 31, 0);
+    }
+    // kMir: default L2 policy (an evict_first stream drops the twins before
+    // their second read; measured: HBM reads 89.6 vs 141 GB per solve)
+    auto mld = [&](const double* q) -> double {
+      if constexpr (kMir) return __ldg(q);
+      else return WEFT_MAT_LD(q);
+    };
+    const double v0 = mld(v), v1 = mld(v + sb), v2 = mld(v + 2 * sb);
+    const double v3 = mld(v + sa), v4 = mld(v + sa + sb), v5 = mld(v + sa + 2 * sb);
+    const double v6 = mld(v + 2 * sa), v7 = mld(v + 2 * sa + sb), v8 = mld(v + 2 * sa + 2 * sb);
 #if WEFT_VEC_EL
     double x0, x1, x2;
     if constexpr (Vs == 4) {
@@ -1592,7 +1632,8 @@ __device__ __forceinline__ void all_blocks_sum(const double* partials, int n, do
 // kUnroll: slots per row-loop trip. Grid rows (<= 13 slots) run best at 1;
 // the long contact rows (up to ~40 slots) need the deeper unroll to keep
 // enough gathers in flight (config D contacts mode: 44.1 -> 36.9 ms at 4).
-template <bool kQs, int kUnroll, int Vs, bool kC16>
+// kMir: column words with mirror deltas (row_product_cg).
+template <bool kQs, int kUnroll, int Vs, bool kC16, bool kMir = false>
 __global__ void __launch_bounds__(kPersistThreads, WEFT_PERSIST_MINB) k_pcg_persistent(const PcgArgs* __restrict__ args, PcgState* st) {
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
@@ -1630,8 +1671,18 @@ __global__ void __launch_bounds__(kPersistThreads, WEFT_PERSIST_MINB) k_pcg_pers
   // short rows (a strided assignment, with tw a multiple of the 8 slices
   // per window, gave some warps only the long window heads). Splitting by
   // equal slot counts instead measured slower on the hot path.
-  const int sl_begin = static_cast<int>((static_cast<int64_t>(gw) * nslices) / tw);
-  const int sl_end = static_cast<int>((static_cast<int64_t>(gw + 1) * nslices) / tw);
+  //
+  // kMir: instead, step j deals slices [j tw, (j+1) tw) to the warps,
+  // rotated by j (warp gw takes slice j tw + (gw + j) mod tw), so the window
+  // position a warp sees changes every step. The whole grid then sweeps the
+  // matrix as one front a few tens of MB wide: a block's transposed twin in
+  // a row ~nx positions back was streamed moments before (kMir reads it
+  // from L2), and the front stays a contiguous HBM stream.
+  constexpr bool wave = kMir;  // a runtime switch here costs the default order 11% (measured)
+  const int sl_begin = wave ? 0 : static_cast<int>((static_cast<int64_t>(gw) * nslices) / tw);
+  const int sl_end = wave ? (nslices + tw - 1) / tw
+                          : static_cast<int>((static_cast<int64_t>(gw + 1) * nslices) / tw);
+  auto slice_of = [&](int j) -> int { return wave ? j * tw + (gw + j) % tw : j; };
   double* const qw = q_s + static_cast<size_t>(threadIdx.x >> 5) * g.q_msw * 96 + lane;  // kQs: this warp's rows
 #if WEFT_ZP_ST_EL
   const uint64_t elpol = l2_policy_evict_last();
@@ -1647,19 +1698,24 @@ __global__ void __launch_bounds__(kPersistThreads, WEFT_PERSIST_MINB) k_pcg_pers
     unsigned long long tm0 = 0;
     if (g.timing && lead) tm0 = global_ns();
     double s1[1] = {0.0};
-    for (int sl = sl_begin; sl < sl_end; ++sl) {
+    for (int j = sl_begin; j < sl_end; ++j) {
+      const int sl = slice_of(j);
 #if WEFT_PK_PREFETCH == 1
       // stream this warp's next slice into L2 while this one computes
-      if (lane == 0 && sl + 1 < sl_end) prefetch_slice_l2(A, sl + 1);
+      if (lane == 0 && j + 1 < sl_end && slice_of(j + 1) < nslices) prefetch_slice_l2(A, slice_of(j + 1));
 #elif WEFT_PK_PREFETCH == 2
       // request this slice's whole record stream at once (one bulk L2 prefetch)
-      if (lane == 0) prefetch_slice_l2(A, sl);
+      if (lane == 0 && sl < nslices) prefetch_slice_l2(A, sl);
 #endif
       const int i = sl * kSlice + lane;  // matrix position == vector index (position space)
-      if (i < rows) {
+      if (sl < nslices && i < rows) {
         double y0, y1, y2;
-        if (first) row_product_cg<1, kUnroll, Vs, kC16>(A, i, z, pcur, beta, y0, y1, y2, g.vec_el_frac, g.colp16);
-        else row_product_cg<2, kUnroll, Vs, kC16>(A, i, z, pcur, beta, y0, y1, y2, g.vec_el_frac, g.colp16);
+        if (first)
+          row_product_cg<1, kUnroll, Vs, kC16, kMir>(A, i, z, pcur, beta, y0, y1, y2, g.vec_el_frac, g.colp16,
+                                                     g.mwords);
+        else
+          row_product_cg<2, kUnroll, Vs, kC16, kMir>(A, i, z, pcur, beta, y0, y1, y2, g.vec_el_frac, g.colp16,
+                                                     g.mwords);
         double p0, p1, p2;
         vload3<Vs>(z, i, p0, p1, p2);
         if (!first) {
@@ -1670,7 +1726,7 @@ __global__ void __launch_bounds__(kPersistThreads, WEFT_PERSIST_MINB) k_pcg_pers
           p2 = p2 + beta * o2;
         }
         if constexpr (kQs) {
-          double* qq = qw + (sl - sl_begin) * 96;
+          double* qq = qw + (j - sl_begin) * 96;
           qq[0] = y0;
           qq[32] = y1;
           qq[64] = y2;
@@ -1714,14 +1770,16 @@ __global__ void __launch_bounds__(kPersistThreads, WEFT_PERSIST_MINB) k_pcg_pers
     double s2[2] = {0.0, 0.0};
     // kQs: the rows of this warp's slice run (q from shared memory);
     // otherwise row-linear over the grid
-    const int pb_begin = kQs ? sl_begin * kSlice + lane : blockIdx.x * blockDim.x + threadIdx.x;
-    const int pb_end = kQs ? min(rows, sl_end * kSlice) : rows;
-    const int pb_step = kQs ? kSlice : gridDim.x * blockDim.x;
-    for (int i = pb_begin; i < pb_end; i += pb_step) {
+    const int pb_begin = kQs ? sl_begin : blockIdx.x * blockDim.x + threadIdx.x;
+    const int pb_end = kQs ? sl_end : rows;
+    const int pb_step = kQs ? 1 : gridDim.x * blockDim.x;
+    for (int t = pb_begin; t < pb_end; t += pb_step) {
+      const int i = kQs ? slice_of(t) * kSlice + lane : t;
+      if (kQs && i >= rows) continue;
       double qv[3], rv[3], m[9];
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
-        if constexpr (kQs) qv[c] = qw[((i - lane) / kSlice - sl_begin) * 96 + 32 * c];
+        if constexpr (kQs) qv[c] = qw[(t - sl_begin) * 96 + 32 * c];
         else qv[c] = __ldcg(q + 3 * i + c);
         rv[c] = PB_LD(r + 3 * i + c);
       }
@@ -1822,10 +1880,12 @@ __global__ void __launch_bounds__(kPersistThreads, WEFT_PERSIST_MINB) k_pcg_pers
   if (x_pending && status == 0) {
     // the last iteration's deferred x update (its p is in pnew: the swap
     // below the residual test is skipped on exit), over phase B's rows
-    const int pb_begin = kQs ? sl_begin * kSlice + lane : blockIdx.x * blockDim.x + threadIdx.x;
-    const int pb_end = kQs ? min(rows, sl_end * kSlice) : rows;
-    const int pb_step = kQs ? kSlice : gridDim.x * blockDim.x;
-    for (int i = pb_begin; i < pb_end; i += pb_step) {
+    const int pb_begin = kQs ? sl_begin : blockIdx.x * blockDim.x + threadIdx.x;
+    const int pb_end = kQs ? sl_end : rows;
+    const int pb_step = kQs ? 1 : gridDim.x * blockDim.x;
+    for (int t = pb_begin; t < pb_end; t += pb_step) {
+      const int i = kQs ? slice_of(t) * kSlice + lane : t;
+      if (kQs && i >= rows) continue;
       double pv[3];
       vload3<Vs>(pnew, i, pv[0], pv[1], pv[2]);
 #pragma unroll
@@ -1865,6 +1925,73 @@ __global__ void k_colpos16(int nslices, const int64_t* __restrict__ soff, const 
     if (d < -32768 || d > 32767) atomicOr(bad, 1);
     c16[base + (int64_t)k * kSlice] = static_cast<int16_t>(d);
   }
+}
+
+// Twins of the lower-triangle blocks, once per layout (position space, one
+// partition): pair_at[slot of (m, c)] = slot of (c, m) for c < m, else -1.
+__global__ void k_pair_at(int nslices, const int64_t* __restrict__ soff, const int32_t* __restrict__ rowlen,
+                          const int32_t* __restrict__ colp, int32_t* __restrict__ pair_at) {
+  const int m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= nslices * kSlice) return;
+  const int len = rowlen[m];
+  const int64_t base = soff[m >> 5] + (m & 31);
+  for (int k = 0; k < len; ++k) {
+    const int64_t at = base + (int64_t)k * kSlice;
+    const int c = colp[at];
+    int64_t pa = -1;
+    if (c >= 0 && c < m) {
+      const int lc = rowlen[c];
+      const int64_t bc = soff[c >> 5] + (c & 31);
+      for (int k2 = 0; k2 < lc; ++k2)
+        if (colp[bc + (int64_t)k2 * kSlice] == m) {
+          pa = bc + (int64_t)k2 * kSlice;
+          break;
+        }
+    }
+    pair_at[at] = static_cast<int32_t>(pa);
+  }
+}
+
+// Column words of the mirrored persistent solve, per solve (the values
+// change every step): low 16 bits the column offset; high 16 bits, for a
+// lower block that is BITWISE the transpose of its twin (slot distance
+// within +-32767), that distance, else 0. *nmir counts mirrored blocks.
+__global__ void k_mirror_words(int nslices, const int64_t* __restrict__ soff, const int32_t* __restrict__ rowlen,
+                               const int16_t* __restrict__ c16, const int32_t* __restrict__ pair_at,
+                               const double* __restrict__ vals, uint32_t* __restrict__ words,
+                               unsigned long long* __restrict__ nmir) {
+  const int m = blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned n = 0;
+  if (m < nslices * kSlice) {
+    const int len = rowlen[m];
+    const int64_t base = soff[m >> 5] + (m & 31);
+    for (int k = 0; k < len; ++k) {
+      const int64_t at = base + (int64_t)k * kSlice;
+      const int off = c16[at];
+      uint32_t w = static_cast<uint16_t>(off);
+      const int64_t pa = pair_at[at];
+      const int64_t d = pa - at;
+      if (pa >= 0 && d >= -32767 && d <= 32767) {
+        const int c = m + off;
+        const double* own = vals + vidx(at, m & 31, 0);
+        const double* tw = vals + vidx(pa, c & 31, 0);
+        bool eq = true;
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+          for (int j = 0; j < 3; ++j)
+            eq = eq && __double_as_longlong(__ldg(own + 96 * i + 32 * j)) ==
+                           __double_as_longlong(__ldg(tw + 32 * i + 96 * j));
+        if (eq) {
+          w |= static_cast<uint32_t>(static_cast<uint16_t>(static_cast<int16_t>(d))) << 16;
+          ++n;
+        }
+      }
+      words[at] = w;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) n += __shfl_xor_sync(0xffffffffu, n, o);
+  if ((threadIdx.x & 31) == 0 && n) atomicAdd(nmir, static_cast<unsigned long long>(n));
 }
 
 // PCG init in position space: r = b[perm], z = M^-1 r, x = 0, p = 0.
@@ -1959,6 +2086,8 @@ PcgResult pcg_solve(Ctx& c, const double* b_dev, const weft_pcg_config& cfg, dou
   WG_CUDA(cudaMemcpyAsync(c.pcg, &init, sizeof(init), cudaMemcpyHostToDevice, s));
   double* dots = reinterpret_cast<double*>(c.scalars.data());
   int* dinv_asym = reinterpret_cast<int*>(c.scalars.data() + 12);
+  auto* nmir = reinterpret_cast<unsigned long long*>(c.scalars.data() + 14);
+  bool mir = false;
   if (rows > 0) {
     if (persistent) {
       if (c.A.colp_id != c.A.layout_id) {  // position-space column words, once per layout
@@ -1982,6 +2111,25 @@ PcgResult pcg_solve(Ctx& c, const double* b_dev, const weft_pcg_config& cfg, dou
           c.A.colp16_ok = hbad == 0;
         }
         c.A.colp_id = c.A.layout_id;
+      }
+      // kMir: lower-triangle blocks read from their bitwise-transposed twins
+      // (opt-in, WEFT_PCG_MIRROR=1: HBM reads drop 126 -> 90 GB per config-D
+      // solve but the solve time does not move, ~27 ms either way — the
+      // kernel is latency-bound, not HBM-bound)
+      static const bool mir_on = std::getenv("WEFT_PCG_MIRROR") && std::atoi(std::getenv("WEFT_PCG_MIRROR")) == 1;
+      mir = mir_on && c.A.colp16_ok && v4 && c.A.total > 0 && c.A.total < (int64_t{1} << 31);
+      if (mir) {
+        if (c.A.pair_id != c.A.layout_id) {
+          c.A.pair_at.resize(static_cast<size_t>(c.A.total) + 1);
+          k_pair_at<<<div_up(c.A.nslices * kSlice, 256), 256, 0, ls(c)>>>(
+              c.A.nslices, c.A.slice_off.data(), c.A.rowlen.data(), c.A.colp.data(), c.A.pair_at.data());
+          c.A.pair_id = c.A.layout_id;
+        }
+        c.A.mwords.resize(static_cast<size_t>(c.A.total) + 1);
+        WG_CUDA(cudaMemsetAsync(nmir, 0, sizeof(unsigned long long), s));
+        k_mirror_words<<<div_up(c.A.nslices * kSlice, 256), 256, 0, ls(c)>>>(
+            c.A.nslices, c.A.slice_off.data(), c.A.rowlen.data(), c.A.colp16.data(), c.A.pair_at.data(),
+            c.A.vals.data(), c.A.mwords.data(), nmir);
       }
       c.xp.resize(len);
       c.dinv6.resize(6 * static_cast<size_t>(rows) + 6);
@@ -2040,6 +2188,10 @@ PcgResult pcg_solve(Ctx& c, const double* b_dev, const weft_pcg_config& cfg, dou
   const int unroll = (unroll_env ? unroll_env : (c.n_contacts > 0 ? 4 : kPkUnroll)) >= 4 ? 4 : 1;
   const bool c16 = persistent && c.A.colp16_ok;
   auto pick = [&](bool q) -> decltype(&k_pcg_persistent<false, 1, 3, false>) {
+    if (mir) {
+      if (unroll == 4) return q ? k_pcg_persistent<true, 4, 4, true, true> : k_pcg_persistent<false, 4, 4, true, true>;
+      return q ? k_pcg_persistent<true, 1, 4, true, true> : k_pcg_persistent<false, 1, 4, true, true>;
+    }
     if (c16) {
       if (v4) {
         if (unroll == 4) return q ? k_pcg_persistent<true, 4, 4, true> : k_pcg_persistent<false, 4, 4, true>;
@@ -2090,6 +2242,7 @@ PcgResult pcg_solve(Ctx& c, const double* b_dev, const weft_pcg_config& cfg, dou
   if (persistent) {
     args.A.cols = c.A.colp.data();  // columns as positions
     args.colp16 = c16 ? c.A.colp16.data() : nullptr;
+    args.mwords = mir ? c.A.mwords.data() : nullptr;
     args.x = c.xp.data();
     if (v4) {  // gathered vectors 32 bytes per row
       args.z = c.z4.data();
@@ -2148,6 +2301,13 @@ PcgResult pcg_solve(Ctx& c, const double* b_dev, const weft_pcg_config& cfg, dou
       // read unless shared)
       const double per_row =
           4.0 + 48.0 + 24.0 + 24.0 + (args.dinv6 ? 48.0 : 72.0) + 48.0 + 48.0 + (qs_bytes ? 0.0 : 48.0);
+      // kMir: mirrored blocks come from L2, not HBM (their 72 bytes are not
+      // counted); the column word is 4 bytes
+      // (kMir reads its mirrored blocks from L2: fewer HBM bytes than this
+      // algorithmic count, which stays the SURVEY 8(d) figure)
+      unsigned long long nm = 0;
+      if (mir) WG_CUDA(cudaMemcpy(&nm, nmir, sizeof(nm), cudaMemcpyDeviceToHost));
+      c.pcg_mirrored = static_cast<int64_t>(nm);
       c.pcg_bytes += hs->iter * (76.0 * static_cast<double>(c.A.nnzb) + per_row * rows);
     }
   } else if (prows) {
