@@ -503,6 +503,27 @@ def gpu_arm(args, rank, world, local):
                "d2h_bytes_per_step": world * 2 * 8 * 3 * p,
                "same_trajectory_as_value": bool(torch.equal(xa.to(xk.device), xk))}
 
+    # SpMV alone (SURVEY §8(d)'s SpMV microbench): y = A x through
+    # weft_gpu_spmv on the assembled system of the last step, x ~ U(-1, 1);
+    # the kernel timed by the library's CUDA events (the host copies of x and
+    # y are outside them); the 0.69 GB matrix is larger than L2
+    spmv = None
+    if world == 1:
+        xr = np.random.default_rng(args.seed).uniform(-1.0, 1.0, 3 * p)
+        for _ in range(3):
+            eng.spmv_pipelined(None, xr)
+        eng.profile(True)
+        for _ in range(20):
+            eng.spmv_pipelined(None, xr)
+        sst = eng.stats()
+        eng.profile(False)
+        info_now = eng.matrix_info()
+        sp_ms = sst.spmv_ms / max(sst.spmv_launches, 1)
+        sp_bytes = 76.0 * info_now.nnzb + 52.0 * info_now.block_rows
+        spmv = {"kernel": "k_spmv (weft_gpu_spmv, y = A x in the reference's order)", "launches": int(sst.spmv_launches),
+                "ms": sp_ms, "alg_bytes": sp_bytes, "achieved": sp_bytes / sp_ms / 1e6, "unit": "GB/s",
+                "bytes_note": "SURVEY 8(d): nnzb (72 values + 4 column) + rows (4 length + 24 x + 24 y)"}
+
     # narrow phase (not part of the hot-path step): collide()
     # = broad phase + elementary DCD / CCD tests + dedup at the timed region's start state
     narrow = None
@@ -575,6 +596,8 @@ def gpu_arm(args, rank, world, local):
         return
     value = args.steps / (ms_total / 1e3)  # whole-job steps/s (one step = the whole cloth on all ranks)
     peak, peak_src = peaks()
+    if spmv is not None:
+        spmv.update({"peak": peak, "frac": spmv["achieved"] / peak, "peak_source": peak_src})
     if st.pcg_solves:
         # k_pcg_persistent: per iteration 76 B per streamed
         # live block (9 FP64 values + int32 column) and per row 268 B (q kept
@@ -644,6 +667,7 @@ def gpu_arm(args, rank, world, local):
             "impact_zones": zones,
             "body_proxy": proxy,
             "assembly_roofline": assembly_roofline,
+            "spmv": spmv,
         },
         "roofline": {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "alg_bytes_per_launch": alg_bytes,

@@ -452,7 +452,7 @@ weft_status weft_gpu_sim_get_state(weft_gpu_ctx* ctx, double* x, double* v);
 
 typedef struct weft_gpu_stats_t {
   int64_t launches;       /* kernels of this library launched by the context */
-  int64_t spmv_launches;  /* PCG SpMV launches timed while profiling (graph/launch path) */
+  int64_t spmv_launches;  /* SpMV launches timed while profiling (PCG graph/launch path, weft_gpu_spmv) */
   double spmv_ms;         /* their summed device time (CUDA events) */
   int64_t pcg_solves;     /* persistent PCG kernels timed while profiling */
   int64_t pcg_iterations; /* their iterations */

@@ -1325,6 +1325,7 @@ __global__ void __launch_bounds__(kSlotWarps * 32, WEFT_SLOT_MINB) k_fill_slots(
     for (int pass = 0; pass < 2; ++pass) {
       if (staged) {
         const int i1 = sm_row[pass][lane + 1];
+#pragma unroll 4  // the loads of four incidences in flight at once (same summation order)
         for (int i = sm_row[pass][lane]; i < i1; ++i) {
           const int ksa = sm_ksa[i];
           const double* R = g.eres + sm_res[i] - 3 * ((ksa >> 8) & 0xff) + 3 * ((ksa >> 16) & 0xff);

@@ -324,7 +324,16 @@ weft_status weft_gpu_spmv(weft_gpu_ctx* ctx, const double* x, double* y) {
     if (c.world == 1) {
       c.r.resize(len);
       WG_CUDA(cudaMemcpyAsync(c.r.data(), x, len * sizeof(double), cudaMemcpyDefault, c.stream));
+      if (c.profile) WG_CUDA(cudaEventRecord(c.ev[6], c.stream));
       weft_gpu::spmv(c, c.r.data(), c.q.data());
+      if (c.profile) {  // the kernel alone (the copies of x and y are outside the events)
+        WG_CUDA(cudaEventRecord(c.ev[7], c.stream));
+        WG_CUDA(cudaEventSynchronize(c.ev[7]));
+        float ms = 0.f;
+        WG_CUDA(cudaEventElapsedTime(&ms, c.ev[6], c.ev[7]));
+        c.spmv_ms += ms;
+        ++c.spmv_launches;
+      }
       WG_CUDA(cudaMemcpyAsync(y, c.q.data(), len * sizeof(double), cudaMemcpyDefault, c.stream));
     } else {
       // own rows of x into the window; peers gather the rest from their owners
