@@ -1454,6 +1454,10 @@ constexpr int kPersistThreads = 256;
 #define WEFT_PK_UNROLL 1
 #endif
 constexpr int kPkUnroll = WEFT_PK_UNROLL;
+#ifndef WEFT_DEEP_WIDTH
+#define WEFT_DEEP_WIDTH 16
+#endif
+constexpr int kDeepWidth = WEFT_DEEP_WIDTH;  // slice width (slots) from which the unrolled row loop runs
 #ifndef WEFT_PK_PREFETCH
 #define WEFT_PK_PREFETCH 0
 #endif
@@ -1710,12 +1714,25 @@ __global__ void __launch_bounds__(kPersistThreads, WEFT_PERSIST_MINB) k_pcg_pers
       const int i = sl * kSlice + lane;  // matrix position == vector index (position space)
       if (sl < nslices && i < rows) {
         double y0, y1, y2;
-        if (first)
-          row_product_cg<1, kUnroll, Vs, kC16, kMir>(A, i, z, pcur, beta, y0, y1, y2, g.vec_el_frac, g.colp16,
-                                                     g.mwords);
-        else
-          row_product_cg<2, kUnroll, Vs, kC16, kMir>(A, i, z, pcur, beta, y0, y1, y2, g.vec_el_frac, g.colp16,
-                                                     g.mwords);
+        // kUnroll > 1 (systems with contacts): only the slices of long
+        // (contact) rows take the unrolled loop; grid-row slices keep the
+        // tighter single-slot loop (the slice width is warp-uniform)
+        const bool deep = kUnroll > 1 && (A.slice_off[sl + 1] - A.slice_off[sl]) > kDeepWidth * kSlice;
+        if (deep) {
+          if (first)
+            row_product_cg<1, kUnroll, Vs, kC16, kMir>(A, i, z, pcur, beta, y0, y1, y2, g.vec_el_frac, g.colp16,
+                                                       g.mwords);
+          else
+            row_product_cg<2, kUnroll, Vs, kC16, kMir>(A, i, z, pcur, beta, y0, y1, y2, g.vec_el_frac, g.colp16,
+                                                       g.mwords);
+        } else {
+          if (first)
+            row_product_cg<1, 1, Vs, kC16, kMir>(A, i, z, pcur, beta, y0, y1, y2, g.vec_el_frac, g.colp16,
+                                                 g.mwords);
+          else
+            row_product_cg<2, 1, Vs, kC16, kMir>(A, i, z, pcur, beta, y0, y1, y2, g.vec_el_frac, g.colp16,
+                                                 g.mwords);
+        }
         double p0, p1, p2;
         vload3<Vs>(z, i, p0, p1, p2);
         if (!first) {
