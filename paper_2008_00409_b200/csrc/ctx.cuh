@@ -238,6 +238,8 @@ struct Ctx {
   DBuf<double> zn_cn, zn_lam, zn_force, zn_tc, zn_tv, zn_grad, zn_saved, zn_prop, zn_pre;
   DBuf<int32_t> zn_fail;
   DBuf<float4> zn_tbox;  // narrow phase: conservative float triangle boxes
+  DBuf<double> zn_dbox;  // narrow phase: exact triangle boxes (6 per triangle)
+  DBuf<double> zn_vbox;  // narrow phase: exact vertex boxes (6 per vertex)
   int64_t zn_m = 0;      // accumulated impacts
   int32_t zn_nz = 0;     // zones of the last build
   int64_t zn_nzv = 0;    // zone vertices of the last build

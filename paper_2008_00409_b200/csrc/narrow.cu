@@ -371,6 +371,8 @@ struct NarrowArgs {
   unsigned long long* __restrict__ count;
   unsigned long long cap;
   const float4* __restrict__ tbox;  // per triangle: (lo xyz, -) (hi xyz, -), rounded outward
+  const double* __restrict__ vbox;  // per vertex: lo xyz, hi xyz over begin (and end) positions (exact)
+  const double* __restrict__ dbox;  // per triangle: the same over its 3 vertices (exact)
 };
 
 // Per-triangle box over the 3 vertices (begin and, for CCD, end positions),
@@ -379,7 +381,8 @@ struct NarrowArgs {
 // hi + margin rounds monotonically, so "apart" on the float boxes implies
 // apart on the exact ones).
 __global__ void k_tri_fbox(int ntris, const int32_t* __restrict__ tris, const double* __restrict__ x0,
-                           const double* __restrict__ x1, bool ccd, float4* __restrict__ out) {
+                           const double* __restrict__ x1, bool ccd, float4* __restrict__ out,
+                           double* __restrict__ dbox) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= ntris) return;
   double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
@@ -399,6 +402,56 @@ __global__ void k_tri_fbox(int ntris, const int32_t* __restrict__ tris, const do
   }
   out[2 * t] = make_float4(__double2float_rd(lo[0]), __double2float_rd(lo[1]), __double2float_rd(lo[2]), 0.f);
   out[2 * t + 1] = make_float4(__double2float_ru(hi[0]), __double2float_ru(hi[1]), __double2float_ru(hi[2]), 0.f);
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    dbox[6 * t + a] = lo[a];
+    dbox[6 * t + 3 + a] = hi[a];
+  }
+}
+
+// Per-vertex box over its begin (and, for CCD, end) position, with
+// feature_apart's sentinels: dmin / dmax ignore a NaN second operand and
+// never return one here, so combining these boxes (and the triangle boxes
+// of k_tri_fbox) gives exactly the lo / hi feature_apart's running min / max
+// over the feature's positions gives, for any input.
+__global__ void k_vert_box(int nverts, const double* __restrict__ x0, const double* __restrict__ x1, bool ccd,
+                           double* __restrict__ vbox) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= nverts) return;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    double lo = dmin(1e300, x0[3 * v + a]), hi = dmax(-1e300, x0[3 * v + a]);
+    if (ccd) {
+      lo = dmin(lo, x1[3 * v + a]);
+      hi = dmax(hi, x1[3 * v + a]);
+    }
+    vbox[6 * v + a] = lo;
+    vbox[6 * v + 3 + a] = hi;
+  }
+}
+
+// feature_apart on precomputed exact boxes (box a = the min / max of the
+// boxes at pa[0..NA), box b likewise): same decision as feature_apart below.
+template <int NA, int NB>
+__device__ __forceinline__ bool boxes_apart_d(const double* const (&pa)[NA], const double* const (&pb)[NB],
+                                              double margin) {
+#pragma unroll
+  for (int axis = 0; axis < 3; ++axis) {
+    double lo_a = __ldg(pa[0] + axis), hi_a = __ldg(pa[0] + 3 + axis);
+#pragma unroll
+    for (int k = 1; k < NA; ++k) {
+      lo_a = dmin(lo_a, __ldg(pa[k] + axis));
+      hi_a = dmax(hi_a, __ldg(pa[k] + 3 + axis));
+    }
+    double lo_b = __ldg(pb[0] + axis), hi_b = __ldg(pb[0] + 3 + axis);
+#pragma unroll
+    for (int k = 1; k < NB; ++k) {
+      lo_b = dmin(lo_b, __ldg(pb[k] + axis));
+      hi_b = dmax(hi_b, __ldg(pb[k] + 3 + axis));
+    }
+    if (lo_a > hi_b + margin || lo_b > hi_a + margin) return true;
+  }
+  return false;
 }
 
 __device__ __forceinline__ void emit(const NarrowArgs& g, int kind, int a, int b, const Hit& h) {
@@ -476,7 +529,11 @@ __global__ void __launch_bounds__(128) k_narrow(NarrowArgs g) {
   // triangle's box (min / max are exact and x + margin rounds monotonically),
   // so triangle boxes apart by more than the margin imply that all 15
   // feature_apart tests below reject — same hits, far less work.
-  if (feature_apart<kCcd>(g, tri1, tri2, margin)) return;
+  {
+    const double* const ta[1] = {g.dbox + 6 * (size_t)t1};
+    const double* const tb[1] = {g.dbox + 6 * (size_t)t2};
+    if (boxes_apart_d(ta, tb, margin)) return;
+  }
   // vertex-face, both directions; shared vertices are exempt
   for (int dir = 0; dir < 2; ++dir) {
     const int* vt = dir == 0 ? tri1 : tri2;
@@ -486,9 +543,9 @@ __global__ void __launch_bounds__(128) k_narrow(NarrowArgs g) {
       const int v = vt[k];
       if (ft[0] == v || ft[1] == v || ft[2] == v) continue;
       if (!g.movable[v] && !g.movable[ft[0]] && !g.movable[ft[1]] && !g.movable[ft[2]]) continue;
-      const int fa[1] = {v};
-      const int fb[3] = {ft[0], ft[1], ft[2]};
-      if (feature_apart<kCcd>(g, fa, fb, margin)) continue;
+      const double* const fa[1] = {g.vbox + 6 * (size_t)v};
+      const double* const fb[1] = {g.dbox + 6 * (size_t)face_id};
+      if (boxes_apart_d(fa, fb, margin)) continue;
       Hit h;
       bool hit;
       if (!kCcd) {
@@ -510,9 +567,9 @@ __global__ void __launch_bounds__(128) k_narrow(NarrowArgs g) {
       const int2 e1 = g.edges[lo], e2 = g.edges[hi];
       if (e1.x == e2.x || e1.x == e2.y || e1.y == e2.x || e1.y == e2.y) continue;
       if (!g.movable[e1.x] && !g.movable[e1.y] && !g.movable[e2.x] && !g.movable[e2.y]) continue;
-      const int fa[2] = {e1.x, e1.y};
-      const int fb[2] = {e2.x, e2.y};
-      if (feature_apart<kCcd>(g, fa, fb, margin)) continue;
+      const double* const fa[2] = {g.vbox + 6 * (size_t)e1.x, g.vbox + 6 * (size_t)e1.y};
+      const double* const fb[2] = {g.vbox + 6 * (size_t)e2.x, g.vbox + 6 * (size_t)e2.y};
+      if (boxes_apart_d(fa, fb, margin)) continue;
       Hit h;
       bool hit;
       if (!kCcd) {
@@ -770,9 +827,14 @@ int64_t narrow_phase(Ctx& c, const double* x0, const double* x1, int mode, doubl
   // pairs they do not separate by the margin (most do not reach a feature
   // test: ~92 % of config-D DCD candidates), k_narrow tests the rest
   c.zn_tbox.resize(2 * static_cast<size_t>(c.soup_tris) + 2);
+  c.zn_dbox.resize(6 * static_cast<size_t>(c.soup_tris) + 6);
+  c.zn_vbox.resize(6 * static_cast<size_t>(c.soup_verts) + 6);
   if (c.soup_tris)
     k_tri_fbox<<<div_up(c.soup_tris, 256), 256, 0, ls(c)>>>(c.soup_tris, c.tris.data(), x0, ccd ? x1 : x0, ccd,
-                                                            c.zn_tbox.data());
+                                                            c.zn_tbox.data(), c.zn_dbox.data());
+  if (c.soup_verts)
+    k_vert_box<<<div_up(c.soup_verts, 256), 256, 0, ls(c)>>>(c.soup_verts, x0, ccd ? x1 : x0, ccd,
+                                                             c.zn_vbox.data());
   int64_t all = 0;
   const int64_t npairs = candidates(c, begin, end, nullptr, /*count_only=*/false, c.zn_tbox.data(),
                                     ccd ? 1e-9 : thickness, &all);
@@ -792,6 +854,8 @@ int64_t narrow_phase(Ctx& c, const double* x0, const double* x1, int mode, doubl
                0,
                nullptr};
   g.tbox = c.zn_tbox.data();
+  g.vbox = c.zn_vbox.data();
+  g.dbox = c.zn_dbox.data();
   c.hit_count.resize(1);
   unsigned long long nh = 0;
   if (npairs) {
