@@ -430,8 +430,9 @@ __global__ void k_vert_box(int nverts, const double* __restrict__ x0, const doub
   }
 }
 
-// feature_apart on precomputed exact boxes (box a = the min / max of the
-// boxes at pa[0..NA), box b likewise): same decision as feature_apart below.
+// feature_apart (collision.cpp:226-254) on precomputed exact boxes: box a =
+// the min / max of the boxes at pa[0..NA), box b likewise; apart when some
+// axis separates them by more than the margin.
 template <int NA, int NB>
 __device__ __forceinline__ bool boxes_apart_d(const double* const (&pa)[NA], const double* const (&pb)[NB],
                                               double margin) {
@@ -468,40 +469,6 @@ __device__ __forceinline__ void emit(const NarrowArgs& g, int kind, int a, int b
   o[5] = h.w[1];
   o[6] = h.w[2];
   o[7] = h.w[3];
-}
-
-// feature_apart (collision.cpp:226-254): box separation beyond the margin on
-// some axis, over begin (and, for CCD, end) positions.
-template <bool kCcd, int NA, int NB>
-__device__ __forceinline__ bool feature_apart(const NarrowArgs& g, const int (&fa)[NA], const int (&fb)[NB],
-                                              double margin) {
-  for (int axis = 0; axis < 3; ++axis) {
-    double lo_a = 1e300, hi_a = -1e300, lo_b = 1e300, hi_b = -1e300;
-#pragma unroll
-    for (int k = 0; k < NA; ++k) {
-      const double p0 = g.x0[3 * fa[k] + axis];
-      lo_a = dmin(lo_a, p0);
-      hi_a = dmax(hi_a, p0);
-      if (kCcd) {
-        const double p1 = g.x1[3 * fa[k] + axis];
-        lo_a = dmin(lo_a, p1);
-        hi_a = dmax(hi_a, p1);
-      }
-    }
-#pragma unroll
-    for (int k = 0; k < NB; ++k) {
-      const double p0 = g.x0[3 * fb[k] + axis];
-      lo_b = dmin(lo_b, p0);
-      hi_b = dmax(hi_b, p0);
-      if (kCcd) {
-        const double p1 = g.x1[3 * fb[k] + axis];
-        lo_b = dmin(lo_b, p1);
-        hi_b = dmax(hi_b, p1);
-      }
-    }
-    if (lo_a > hi_b + margin || lo_b > hi_a + margin) return true;
-  }
-  return false;
 }
 
 // narrow_phase_pair (collision.cpp:214-309), one thread per candidate pair.
