@@ -409,11 +409,12 @@ __global__ void k_tri_fbox(int ntris, const int32_t* __restrict__ tris, const do
   }
 }
 
-// Per-vertex box over its begin (and, for CCD, end) position, with
-// feature_apart's sentinels: dmin / dmax ignore a NaN second operand and
-// never return one here, so combining these boxes (and the triangle boxes
-// of k_tri_fbox) gives exactly the lo / hi feature_apart's running min / max
-// over the feature's positions gives, for any input.
+// Per-vertex box over its begin (and, for CCD, end) position, with the
+// sentinels of the reference's feature_apart (collision.cpp:226-254, running
+// std::min / std::max from +-1e300): dmin / dmax ignore a NaN second operand
+// and never return one here, so combining these boxes (and the triangle
+// boxes of k_tri_fbox) gives exactly the lo / hi that running min / max over
+// the feature's positions gives, for any input.
 __global__ void k_vert_box(int nverts, const double* __restrict__ x0, const double* __restrict__ x1, bool ccd,
                            double* __restrict__ vbox) {
   const int v = blockIdx.x * blockDim.x + threadIdx.x;
