@@ -752,7 +752,26 @@ struct WalkArgs {
   const float4* __restrict__ tbox;
   double margin;
   unsigned long long* __restrict__ all_count;
+  // append mode (kMode 2, the narrow-phase feed): pairs in no particular
+  // order, claimed from *cursor; entries at or beyond cap are dropped and the
+  // caller re-runs with the exact count
+  unsigned long long* __restrict__ cursor;
+  int64_t cap;
 };
+
+// Append mode: a warp's passing pairs gather in a shared-memory buffer and
+// go out with one atomic claim per flush (coalesced copies).
+constexpr int kAppendBuf = 480;  // int2 entries: the bitset path's unused sm_lo stage of the warp
+__device__ __forceinline__ void append_flush(const WalkArgs& w, int2* buf, int& bn, int lane, int2* __restrict__ out) {
+  __syncwarp();
+  unsigned long long base = 0;
+  if (lane == 0) base = atomicAdd(w.cursor, static_cast<unsigned long long>(bn));
+  base = __shfl_sync(0xffffffffu, base, 0);
+  for (int k = lane; k < bn; k += 32)
+    if (base + k < static_cast<unsigned long long>(w.cap)) out[base + k] = buf[k];
+  __syncwarp();
+  bn = 0;
+}
 
 __device__ __forceinline__ bool boxes_apart(const float4* __restrict__ tbox, int t1, int t2, double margin) {
   const float4 la = __ldg(tbox + 2 * t1), ha = __ldg(tbox + 2 * t1 + 1);
@@ -778,11 +797,14 @@ __device__ __forceinline__ int64_t tri_start(int64_t i, int64_t s) { return i * 
 // pairs per build; 178 at most.)
 constexpr int kBitsetMax = 256;
 
-template <bool kWrite>
-__device__ __forceinline__ int64_t walk_bitset(int s, int lane, int64_t l0, int64_t l1, const int32_t* __restrict__ tl,
-                                               const int* __restrict__ lat, int cx, int cy, int cz, int* sm_id,
-                                               unsigned* sm_set, int64_t o, int2* __restrict__ out,
-                                               const float4* __restrict__ tbox, double margin, int64_t& nall) {
+// kMode: 0 count, 1 write in walk order at o, 2 append (w.cursor; needs tbox)
+template <int kMode>
+__device__ __forceinline__ int64_t walk_bitset(const WalkArgs& wa, int s, int lane, int64_t l0, int64_t l1,
+                                               const int32_t* __restrict__ tl, const int* __restrict__ lat, int cx,
+                                               int cy, int cz, int* sm_id, unsigned* sm_set, int2* sm_buf, int64_t o,
+                                               int2* __restrict__ out, const float4* __restrict__ tbox, double margin,
+                                               int64_t& nall) {
+  constexpr bool kWrite = kMode == 1;
   constexpr int G = kBitsetMax / 32;
   const int ng = (s + 31) >> 5;
   int m[G];
@@ -806,6 +828,61 @@ __device__ __forceinline__ int64_t walk_bitset(int s, int lane, int64_t l0, int6
   }
   __syncwarp();
   int64_t n = 0;
+  if constexpr (kMode == 2) {
+    // one pass: every lane steps through its candidates one per round
+    // (warp-synchronous), the survivors of the float-box test are compacted
+    // into the warp's buffer by ballot
+    int bn = 0;
+#pragma unroll
+    for (int h = 0; h < G; ++h) {
+      if (h >= ng) break;  // warp-uniform
+      const int i = lane + 32 * h;
+      const unsigned* Sr = sm_set + (7 & ~m[h]) * G;
+      int64_t jlo = 0, jhi = 0;
+      int call = 0, g = ng;
+      unsigned bits = 0;
+      auto group_bits = [&](int gg) -> unsigned {
+        unsigned b = Sr[gg];
+        const int64_t b0 = jlo - 32 * gg, b1 = jhi - 32 * gg;  // keep bits in [b0, b1)
+        if (b0 > 0) b &= ~0u << b0;
+        if (b1 < 32) b &= (1u << b1) - 1u;
+        return b;
+      };
+      if (i < s) {
+        const int64_t rs = tri_start(i, s);
+        jlo = max(l0 - rs + i + 1, static_cast<int64_t>(i + 1));
+        jhi = min(l1 - rs + i + 1, static_cast<int64_t>(s));
+        for (int gg = static_cast<int>(jlo >> 5); gg < ng && 32 * gg < jhi; ++gg) call += __popc(group_bits(gg));
+        g = static_cast<int>(jlo >> 5);
+        while (g < ng && 32 * g < jhi && !(bits = group_bits(g))) ++g;
+        if (!(g < ng && 32 * g < jhi)) bits = 0;
+      }
+      nall += __reduce_add_sync(0xffffffffu, call);
+      const int ti = i < s ? sm_id[i] : 0;
+      while (__any_sync(0xffffffffu, bits != 0)) {
+        bool pass = false;
+        int tj = 0;
+        if (bits) {
+          const int j = 32 * g + __ffs(bits) - 1;
+          bits &= bits - 1;
+          tj = sm_id[j];
+          pass = !boxes_apart(tbox, ti, tj, margin);
+          if (!bits) {
+            ++g;
+            while (g < ng && 32 * g < jhi && !(bits = group_bits(g))) ++g;
+          }
+        }
+        const unsigned pm = __ballot_sync(0xffffffffu, pass);
+        if (pass) sm_buf[bn + __popc(pm & ((1u << lane) - 1u))] = make_int2(ti, tj);
+        bn += __popc(pm);
+        n += __popc(pm);
+        if (bn > kAppendBuf - 32) append_flush(wa, sm_buf, bn, lane, out);
+      }
+    }
+    if (bn) append_flush(wa, sm_buf, bn, lane, out);
+    __syncwarp();
+    return n;
+  }
 #pragma unroll
   for (int h = 0; h < G; ++h) {
     if (h >= ng) break;  // warp-uniform
@@ -868,11 +945,13 @@ __device__ __forceinline__ int64_t walk_bitset(int s, int lane, int64_t l0, int6
   return n;
 }
 
-template <bool kWrite>
+template <int kMode>
 __global__ void __launch_bounds__(kWalkWarps * 32) k_cell_walk(WalkArgs w, int64_t* __restrict__ counts,
                                                                const int64_t* __restrict__ offs,
                                                                int2* __restrict__ out) {
-  __shared__ int3 sm_lo[kWalkWarps][kWalkStage];
+  constexpr bool kWrite = kMode == 1;
+  static_assert(kAppendBuf * sizeof(int2) <= kWalkStage * sizeof(int3), "append buffer aliases sm_lo");
+  __shared__ __align__(16) int3 sm_lo[kWalkWarps][kWalkStage];  // (also the append buffer: int2)
   __shared__ int sm_id[kWalkWarps][kWalkStage];
   __shared__ unsigned sm_set[kWalkWarps][8 * (kBitsetMax / 32)];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -893,10 +972,10 @@ __global__ void __launch_bounds__(kWalkWarps * 32) k_cell_walk(WalkArgs w, int64
     if (s <= kBitsetMax) {  // bitset walk (above)
       const int64_t l0 = lo - p0, l1 = hi - p0;
       int64_t nall = 0;
-      n = walk_bitset<kWrite>(static_cast<int>(s), lane, l0, l1, tl, w.lat, cx, cy, cz, sm_id[warp], sm_set[warp], o,
-                              out, w.tbox, w.margin, nall);
+      n = walk_bitset<kMode>(w, static_cast<int>(s), lane, l0, l1, tl, w.lat, cx, cy, cz, sm_id[warp], sm_set[warp],
+                             reinterpret_cast<int2*>(sm_lo[warp]), o, out, w.tbox, w.margin, nall);
       if (!kWrite && lane == 0) {
-        counts[cell] = n;
+        if (kMode == 0) counts[cell] = n;
         if (w.all_count) atomicAdd(w.all_count, static_cast<unsigned long long>(nall));
       }
       return;
@@ -948,6 +1027,12 @@ __global__ void __launch_bounds__(kWalkWarps * 32) k_cell_walk(WalkArgs w, int64
       }
       const unsigned m = __ballot_sync(0xffffffffu, hit);
       if (kWrite && hit) out[o + __popc(m & ((1u << lane) - 1u))] = make_int2(t1, t2);
+      if (kMode == 2 && m) {  // cells over kBitsetMax (rare): one claim per round
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(w.cursor, static_cast<unsigned long long>(__popc(m)));
+        base = __shfl_sync(0xffffffffu, base, 0) + __popc(m & ((1u << lane) - 1u));
+        if (hit && base < static_cast<unsigned long long>(w.cap)) out[base] = make_int2(t1, t2);
+      }
       o += __popc(m);
       n += __popc(m);
       // advance this lane by 32 local indices
@@ -968,7 +1053,7 @@ __global__ void __launch_bounds__(kWalkWarps * 32) k_cell_walk(WalkArgs w, int64
       }
     }
   }
-  if (!kWrite && lane == 0) counts[cell] = n;
+  if (kMode == 0 && lane == 0) counts[cell] = n;
 }
 
 // Returns the candidate count of [begin, end); when pairs_out is non-null
@@ -985,11 +1070,37 @@ int64_t candidates(Ctx& c, int64_t begin, int64_t end, int32_t* pairs_out, bool 
   c.cand_all.resize(1);
   if (tbox) WG_CUDA(cudaMemsetAsync(c.cand_all.data(), 0, sizeof(unsigned long long), s));
   WalkArgs w{begin, end, cells, c.wprefix.data(), c.cell_off.data(), c.vals_b.data(), c.cell_keys.data(),
-             c.lat.data(), tbox, margin, tbox ? c.cand_all.data() : nullptr};
+             c.lat.data(), tbox, margin, tbox ? c.cand_all.data() : nullptr, nullptr, 0};
+  const int blocks = div_up(cells, kWalkWarps);
+  static const bool append_off = std::getenv("WEFT_WALK_APPEND") && std::atoi(std::getenv("WEFT_WALK_APPEND")) == 0;
+  if (tbox && !count_only && !pairs_out && !append_off) {
+    // the narrow-phase feed: its consumer sorts the hits, so the pairs go
+    // out in one order-free pass (append mode) — no count pass, no scan
+    c.cand_cursor.resize(1);
+    w.cursor = c.cand_cursor.data();
+    // the pairs the buffer already holds (never grows it on its own), at least 4 M
+    int64_t cap = std::max<int64_t>((static_cast<int64_t>(c.cand_pairs.cap) - 2) / 2, int64_t{1} << 22);
+    int64_t n = 0;
+    for (int attempt = 0; attempt < 2; ++attempt) {
+      c.cand_pairs.resize(2 * static_cast<size_t>(cap) + 2);
+      w.cap = cap;
+      WG_CUDA(cudaMemsetAsync(c.cand_cursor.data(), 0, sizeof(unsigned long long), s));
+      WG_CUDA(cudaMemsetAsync(c.cand_all.data(), 0, sizeof(unsigned long long), s));
+      k_cell_walk<2><<<blocks, kWalkWarps * 32, 0, ls(c)>>>(w, nullptr, nullptr,
+                                                            reinterpret_cast<int2*>(c.cand_pairs.data()));
+      WG_CUDA(cudaGetLastError());
+      unsigned long long nc = 0, na = 0;
+      read_small(c, s, {c.cand_cursor.data(), &nc, sizeof(nc)}, {c.cand_all.data(), &na, sizeof(na)});
+      n = static_cast<int64_t>(nc);
+      if (all) *all = static_cast<int64_t>(na);
+      if (n <= cap) break;
+      cap = n;  // exact capacity, run once more
+    }
+    return n;
+  }
   c.cand_count.resize(static_cast<size_t>(cells) + 1);
   WG_CUDA(cudaMemsetAsync(c.cand_count.data() + cells, 0, sizeof(int64_t), s));
-  const int blocks = div_up(cells, kWalkWarps);
-  k_cell_walk<false><<<blocks, kWalkWarps * 32, 0, ls(c)>>>(w, c.cand_count.data(), nullptr, nullptr);
+  k_cell_walk<0><<<blocks, kWalkWarps * 32, 0, ls(c)>>>(w, c.cand_count.data(), nullptr, nullptr);
   size_t tmp = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, tmp, c.cand_count.data(), c.cand_count.data(), cells + 1, s);
   void* t = scratch(c, tmp);
@@ -1005,8 +1116,8 @@ int64_t candidates(Ctx& c, int64_t begin, int64_t end, int32_t* pairs_out, bool 
   }
   if (count_only) return n;  // the walk's count pass is the whole result
   c.cand_pairs.resize(2 * static_cast<size_t>(n) + 2);
-  k_cell_walk<true><<<blocks, kWalkWarps * 32, 0, ls(c)>>>(w, nullptr, c.cand_count.data(),
-                                                           reinterpret_cast<int2*>(c.cand_pairs.data()));
+  k_cell_walk<1><<<blocks, kWalkWarps * 32, 0, ls(c)>>>(w, nullptr, c.cand_count.data(),
+                                                        reinterpret_cast<int2*>(c.cand_pairs.data()));
   WG_CUDA(cudaGetLastError());
   if (pairs_out && n)
     WG_CUDA(cudaMemcpyAsync(pairs_out, c.cand_pairs.data(), 2 * sizeof(int32_t) * n, cudaMemcpyDefault, s));

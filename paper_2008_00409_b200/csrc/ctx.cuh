@@ -240,6 +240,7 @@ struct Ctx {
   DBuf<float4> zn_tbox;  // narrow phase: conservative float triangle boxes
   DBuf<double> zn_dbox;  // narrow phase: exact triangle boxes (6 per triangle)
   DBuf<double> zn_vbox;  // narrow phase: exact vertex boxes (6 per vertex)
+  DBuf<unsigned long long> cand_cursor;  // append-mode candidate walk: pairs claimed
   int64_t zn_m = 0;      // accumulated impacts
   int32_t zn_nz = 0;     // zones of the last build
   int64_t zn_nzv = 0;    // zone vertices of the last build
