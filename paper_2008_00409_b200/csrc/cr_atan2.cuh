@@ -47,7 +47,7 @@ struct DD {
 #endif
 
 #ifdef __CUDACC__
-__device__ __constant__ double kAtanTabDev[130] = {
+static __device__ __constant__ double kAtanTabDev[130] = {  // internal linkage: one copy per TU, also under -rdc
     0x0.0p+0, 0x0.0p+0,
     0x1.fff555bbb729bp-7, -0x1.220c39d4dff50p-61,
     0x1.ffd55bba97625p-6, -0x1.5ec431444912cp-60,
