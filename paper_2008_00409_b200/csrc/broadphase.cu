@@ -1078,8 +1078,11 @@ int64_t candidates(Ctx& c, int64_t begin, int64_t end, int32_t* pairs_out, bool 
     // out in one order-free pass (append mode) — no count pass, no scan
     c.cand_cursor.resize(1);
     w.cursor = c.cand_cursor.data();
-    // the pairs the buffer already holds (never grows it on its own), at least 4 M
-    int64_t cap = std::max<int64_t>((static_cast<int64_t>(c.cand_pairs.cap) - 2) / 2, int64_t{1} << 22);
+    // the pairs the buffer already holds (never grows it on its own), at least
+    // 4 M (WEFT_WALK_CAP: an exact first capacity, tests of the re-run path)
+    static const int64_t cap_env = std::getenv("WEFT_WALK_CAP") ? std::atoll(std::getenv("WEFT_WALK_CAP")) : 0;
+    int64_t cap = cap_env > 0 ? cap_env
+                              : std::max<int64_t>((static_cast<int64_t>(c.cand_pairs.cap) - 2) / 2, int64_t{1} << 22);
     int64_t n = 0;
     for (int attempt = 0; attempt < 2; ++attempt) {
       c.cand_pairs.resize(2 * static_cast<size_t>(cap) + 2);

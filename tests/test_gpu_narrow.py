@@ -88,3 +88,41 @@ def test_known_answers(weft):
     assert len(kab) == 0
     kab, _ = gpu_collide(weft, 6, tris, x.reshape(-1), None, DISCRETE, 0.005)
     assert len(kab) > 0
+
+
+APPEND_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1]); sys.path.insert(0, sys.argv[1] + "/tests")
+from paper_2008_00409_b200 import scenes, weft
+sc = scenes.layered_cloth(3, 30, seed=8)
+rng = np.random.default_rng(4)
+x0 = sc.verts.reshape(-1)
+x1 = x0 + rng.uniform(-0.6, 0.6, x0.shape) * sc.spacing
+out = []
+with weft.Engine(1) as eng:
+    eng.set_soup(len(sc.verts), sc.tris)
+    for mode, th in ((weft.DISCRETE, 2 * sc.thickness), (weft.CONTINUOUS, 1e-9)):
+        kab, vals = eng.collide(x0, x1, mode, th)
+        out += [kab.astype(np.float64).ravel(), vals.ravel()]
+np.save(sys.argv[2], np.concatenate(out))
+"""
+
+
+@pytest.mark.parametrize("env", [{"WEFT_WALK_CAP": "64"}, {"WEFT_WALK_APPEND": "0"}])
+def test_append_feed_overflow_and_ordered_feed(tmp_path, env):
+    """The order-free narrow-phase feed (append mode of the candidate walk)
+    re-run after overflowing a tiny first capacity, and the two-pass ordered
+    feed, give the default run's hits bit for bit (each in its own process:
+    the switches are read once)."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for tag, e in (("default", {}), ("variant", env)):
+        out = str(tmp_path / f"{tag}.npy")
+        r = subprocess.run([sys.executable, "-c", APPEND_SCRIPT, root, out], env={**os.environ, **e},
+                           capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        res[tag] = np.load(out)
+    assert len(res["default"]) > 1000
+    assert np.array_equal(res["default"].view(np.int64), res["variant"].view(np.int64))
