@@ -1092,6 +1092,7 @@ struct SlotArgs {
   int* __restrict__ bad_mass;
   float* __restrict__ vals32;  // Precision::Single outputs (T = float)
   float* __restrict__ rhs32;
+  int stage_cap;  // k_fill_slots<0>: staged incidences per slice (dynamic shared memory)
 };
 
 #ifndef WEFT_SLOT_WARPS
@@ -1191,9 +1192,20 @@ template <int kCap, class T = double>
 __global__ void __launch_bounds__(kSlotWarps * 32, WEFT_SLOT_MINB) k_fill_slots(SlotArgs g) {
   T* const out_vals = std::is_same_v<T, float> ? reinterpret_cast<T*>(g.vals32) : reinterpret_cast<T*>(g.vals);
   T* const out_rhs = std::is_same_v<T, float> ? reinterpret_cast<T*>(g.rhs32) : reinterpret_cast<T*>(g.rhs);
-  __shared__ int4 sm_st[kCap];
-  __shared__ int sm_ksa[kCap], sm_pay[kCap], sm_res[kCap];
-  __shared__ double sm_damp[kCap];
+  // kCap == 0: the staging arrays live in dynamic shared memory sized
+  // g.stage_cap (systems with contacts: room for the heaviest slices)
+  constexpr bool kDyn = kCap == 0;
+  constexpr int kS = kDyn ? 1 : kCap;
+  __shared__ int4 sm_st_s[kS];
+  __shared__ int sm_ksa_s[kS], sm_pay_s[kS], sm_res_s[kS];
+  __shared__ double sm_damp_s[kS];
+  extern __shared__ __align__(16) unsigned char fs_dyn[];
+  const int cap = kDyn ? g.stage_cap : kCap;
+  int4* const sm_st = kDyn ? reinterpret_cast<int4*>(fs_dyn) : sm_st_s;
+  double* const sm_damp = kDyn ? reinterpret_cast<double*>(fs_dyn + 16 * (size_t)cap) : sm_damp_s;
+  int* const sm_ksa = kDyn ? reinterpret_cast<int*>(fs_dyn + 24 * (size_t)cap) : sm_ksa_s;
+  int* const sm_pay = kDyn ? reinterpret_cast<int*>(fs_dyn + 28 * (size_t)cap) : sm_pay_s;
+  int* const sm_res = kDyn ? reinterpret_cast<int*>(fs_dyn + 32 * (size_t)cap) : sm_res_s;
   __shared__ int sm_row[2][kSlice + 1];  // per pass: lane -> first staged entry
   __shared__ int64_t sm_beg[2][kSlice];   // per pass: lane -> first incidence
   __shared__ int sm_rid[kSlice];          // lane -> global row
@@ -1232,7 +1244,7 @@ __global__ void __launch_bounds__(kSlotWarps * 32, WEFT_SLOT_MINB) k_fill_slots(
   }
   __syncthreads();
   const int nstat = sm_row[0][32], ncont = sm_row[1][32] - nstat;
-  const bool staged = nstat + ncont <= kCap;
+  const bool staged = nstat + ncont <= cap;
   if (staged) {
     for (int i = threadIdx.x; i < nstat + ncont; i += blockDim.x) {
       const bool cpass = i >= nstat;
@@ -1497,7 +1509,18 @@ void fill_matrix(Ctx& c, const double* xc, const double* xa, const double* vel, 
       if (c.n_contacts > 0) k_fill_slots<kStageCapContacts, float><<<A.nslices, kSlotWarps * 32, 0, ls(c)>>>(sa);
       else k_fill_slots<kStageCap, float><<<A.nslices, kSlotWarps * 32, 0, ls(c)>>>(sa);
     } else {
-      if (c.n_contacts > 0) k_fill_slots<kStageCapContacts><<<A.nslices, kSlotWarps * 32, 0, ls(c)>>>(sa);
+      if (c.n_contacts > 0) {
+        // 36 bytes per staged incidence; 1536 keeps 4 CTAs per SM (221 KB)
+        static const int cap_env = std::getenv("WEFT_FS_CAP") ? std::atoi(std::getenv("WEFT_FS_CAP")) : 1536;
+        sa.stage_cap = cap_env;
+        const int bytes = 36 * cap_env;
+        static int set_bytes = 0;
+        if (bytes > set_bytes) {
+          WG_CUDA(cudaFuncSetAttribute(k_fill_slots<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+          set_bytes = bytes;
+        }
+        k_fill_slots<0><<<A.nslices, kSlotWarps * 32, bytes, ls(c)>>>(sa);
+      }
       else k_fill_slots<kStageCap><<<A.nslices, kSlotWarps * 32, 0, ls(c)>>>(sa);
     }
     WG_CUDA(cudaGetLastError());
