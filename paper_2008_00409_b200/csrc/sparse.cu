@@ -2235,11 +2235,12 @@ PcgResult pcg_solve(Ctx& c, const double* b_dev, const weft_pcg_config& cfg, dou
     msw = div_up(nsl, static_cast<int64_t>(sms) * WEFT_PERSIST_MINB * warps_per_cta);
     qs_bytes = static_cast<size_t>(warps_per_cta) * msw * 96 * sizeof(double);
     static const bool qs_off = std::getenv("WEFT_PCG_QSMEM") && std::atoi(std::getenv("WEFT_PCG_QSMEM")) == 0;
-    // With contact elements in the system, q through HBM measured faster
-    // (52.5 -> 50.3 ms at config D: the 67 KB of q per CTA come out of L1,
-    // which the contact columns' far gathers need); without, q in shared
-    // memory (29.2 -> 28.0 ms).
-    const bool qs = !qs_off && c.n_contacts == 0 && qs_bytes <= 100 * 1024;
+    // q in shared memory: 29.2 -> 28.0 ms at config D without contacts. With
+    // contact elements it first measured slower (52.5 vs 50.3 ms: the 67 KB
+    // of q per CTA come out of L1, which the far contact gathers used); since
+    // the unrolled row loop runs only in the wide contact slices it is faster
+    // there too (34.5 -> 33.3 ms).
+    const bool qs = !qs_off && qs_bytes <= 100 * 1024;
     if (qs) {
       pkern = pick(true);
       WG_CUDA(cudaFuncSetAttribute(pkern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(qs_bytes)));
