@@ -1514,11 +1514,8 @@ void fill_matrix(Ctx& c, const double* xc, const double* xa, const double* vel, 
         static const int cap_env = std::getenv("WEFT_FS_CAP") ? std::atoi(std::getenv("WEFT_FS_CAP")) : 1536;
         sa.stage_cap = cap_env;
         const int bytes = 36 * cap_env;
-        static int set_bytes = 0;
-        if (bytes > set_bytes) {
-          WG_CUDA(cudaFuncSetAttribute(k_fill_slots<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-          set_bytes = bytes;
-        }
+        // per call: the attribute belongs to the current device's module
+        WG_CUDA(cudaFuncSetAttribute(k_fill_slots<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
         k_fill_slots<0><<<A.nslices, kSlotWarps * 32, bytes, ls(c)>>>(sa);
       }
       else k_fill_slots<kStageCap><<<A.nslices, kSlotWarps * 32, 0, ls(c)>>>(sa);
