@@ -241,6 +241,8 @@ struct Ctx {
   DBuf<double> zn_dbox;  // narrow phase: exact triangle boxes (6 per triangle)
   DBuf<double> zn_vbox;  // narrow phase: exact vertex boxes (6 per vertex)
   DBuf<unsigned long long> cand_cursor;  // append-mode candidate walk: pairs claimed
+  DBuf<int4> zn_feats;                  // two-pass narrow phase: surviving features (2 int4 each)
+  DBuf<unsigned long long> zn_feat_count;
   int64_t zn_m = 0;      // accumulated impacts
   int32_t zn_nz = 0;     // zones of the last build
   int64_t zn_nzv = 0;    // zone vertices of the last build

@@ -373,6 +373,13 @@ struct NarrowArgs {
   const float4* __restrict__ tbox;  // per triangle: (lo xyz, -) (hi xyz, -), rounded outward
   const double* __restrict__ vbox;  // per vertex: lo xyz, hi xyz over begin (and end) positions (exact)
   const double* __restrict__ dbox;  // per triangle: the same over its 3 vertices (exact)
+  // two-pass narrow phase: features that survive their box test, as
+  // {kind, a, b, v0} {v1, v2, v3, 0} (a, b = the hit key's ids; v = the
+  // feature's vertices), claimed from *feat_count; entries at or beyond
+  // feat_cap are dropped and the host re-runs with the exact count
+  int4* __restrict__ feats;
+  unsigned long long* __restrict__ feat_count;
+  unsigned long long feat_cap;
 };
 
 // Per-triangle box over the 3 vertices (begin and, for CCD, end positions),
@@ -549,6 +556,150 @@ __global__ void __launch_bounds__(128) k_narrow(NarrowArgs g) {
       if (hit) emit(g, 1, lo, hi, h);
     }
   }
+}
+
+// Two-pass narrow phase, pass 1: the box tests of k_narrow, one thread per
+// candidate pair, every survivor compacted by ballot into the warp's
+// shared-memory buffer (flushed with one atomic claim). The elementary tests
+// then run densely in pass 2 (k_narrow_solve): in the CCD only ~0.5 features
+// per pair reach the cubic solve, which left most lanes of a fused warp idle.
+constexpr int kFeatBuf = 256;  // records per warp
+constexpr int kFeatWarps = 4;
+__device__ __forceinline__ void feat_flush(const NarrowArgs& g, int4* buf, int& bn, int lane) {
+  __syncwarp();
+  unsigned long long base = 0;
+  if (lane == 0) base = atomicAdd(g.feat_count, static_cast<unsigned long long>(bn));
+  base = __shfl_sync(0xffffffffu, base, 0);
+  for (int k = lane; k < 2 * bn; k += 32)
+    if (base + (k >> 1) < g.feat_cap) g.feats[2 * base + k] = buf[k];
+  __syncwarp();
+  bn = 0;
+}
+
+template <bool kCcd>
+__global__ void __launch_bounds__(kFeatWarps * 32) k_narrow_feats(NarrowArgs g) {
+  __shared__ int4 sm_buf[kFeatWarps][2 * kFeatBuf];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int4* buf = sm_buf[warp];
+  int bn = 0;
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  bool alive = i < g.npairs;
+  int t1 = 0, t2 = 0;
+  if (alive) {
+    const int2 pr = g.pairs[i];
+    t1 = pr.x;
+    t2 = pr.y;
+  }
+  const double margin = kCcd ? 1e-9 : g.thickness;
+  if (alive) {  // the whole-pair rejections of k_narrow (float, then exact boxes)
+    const float4 la = __ldg(g.tbox + 2 * t1), ha = __ldg(g.tbox + 2 * t1 + 1);
+    const float4 lb = __ldg(g.tbox + 2 * t2), hb = __ldg(g.tbox + 2 * t2 + 1);
+    if ((double)la.x > (double)hb.x + margin || (double)lb.x > (double)ha.x + margin ||
+        (double)la.y > (double)hb.y + margin || (double)lb.y > (double)ha.y + margin ||
+        (double)la.z > (double)hb.z + margin || (double)lb.z > (double)ha.z + margin)
+      alive = false;
+  }
+  if (alive) {
+    const double* const ta[1] = {g.dbox + 6 * (size_t)t1};
+    const double* const tb[1] = {g.dbox + 6 * (size_t)t2};
+    if (boxes_apart_d(ta, tb, margin)) alive = false;
+  }
+  int tri1[3] = {0, 0, 0}, tri2[3] = {0, 0, 0};
+  if (alive) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      tri1[k] = g.tris[3 * t1 + k];
+      tri2[k] = g.tris[3 * t2 + k];
+    }
+  }
+  auto push = [&](bool keep, int4 r0, int4 r1) {
+    const unsigned m = __ballot_sync(0xffffffffu, keep);
+    if (keep) {
+      const int at = bn + __popc(m & ((1u << lane) - 1u));
+      buf[2 * at] = r0;
+      buf[2 * at + 1] = r1;
+    }
+    bn += __popc(m);
+    if (bn > kFeatBuf - 32) feat_flush(g, buf, bn, lane);
+  };
+  // vertex-face, both directions (k_narrow's order and skips)
+  for (int dir = 0; dir < 2; ++dir) {
+    for (int k = 0; k < 3; ++k) {
+      bool keep = false;
+      int v = 0, f0 = 0, f1 = 0, f2 = 0, face_id = 0;
+      if (alive) {
+        const int* vt = dir == 0 ? tri1 : tri2;
+        const int* ft = dir == 0 ? tri2 : tri1;
+        face_id = dir == 0 ? t2 : t1;
+        v = vt[k];
+        f0 = ft[0];
+        f1 = ft[1];
+        f2 = ft[2];
+        keep = !(f0 == v || f1 == v || f2 == v) && (g.movable[v] || g.movable[f0] || g.movable[f1] || g.movable[f2]);
+        if (keep) {
+          const double* const fa[1] = {g.vbox + 6 * (size_t)v};
+          const double* const fb[1] = {g.dbox + 6 * (size_t)face_id};
+          keep = !boxes_apart_d(fa, fb, margin);
+        }
+      }
+      push(keep, make_int4(0, v, face_id, v), make_int4(f0, f1, f2, 0));
+    }
+  }
+  // edge-edge in canonical (min id, max id) orientation
+  for (int ka = 0; ka < 3; ++ka) {
+    for (int kb = 0; kb < 3; ++kb) {
+      bool keep = false;
+      int lo = 0, hi = 0;
+      int2 e1 = make_int2(0, 0), e2 = make_int2(0, 0);
+      if (alive) {
+        const int ea = g.tri_edges[3 * t1 + ka], eb = g.tri_edges[3 * t2 + kb];
+        if (ea != eb) {
+          lo = ea < eb ? ea : eb;
+          hi = ea < eb ? eb : ea;
+          e1 = g.edges[lo];
+          e2 = g.edges[hi];
+          keep = !(e1.x == e2.x || e1.x == e2.y || e1.y == e2.x || e1.y == e2.y) &&
+                 (g.movable[e1.x] || g.movable[e1.y] || g.movable[e2.x] || g.movable[e2.y]);
+          if (keep) {
+            const double* const fa[2] = {g.vbox + 6 * (size_t)e1.x, g.vbox + 6 * (size_t)e1.y};
+            const double* const fb[2] = {g.vbox + 6 * (size_t)e2.x, g.vbox + 6 * (size_t)e2.y};
+            keep = !boxes_apart_d(fa, fb, margin);
+          }
+        }
+      }
+      push(keep, make_int4(1, lo, hi, e1.x), make_int4(e1.y, e2.x, e2.y, 0));
+    }
+  }
+  if (bn) feat_flush(g, buf, bn, lane);
+}
+
+// Pass 2: one thread per surviving feature, the elementary test of k_narrow.
+template <bool kCcd>
+__global__ void __launch_bounds__(128) k_narrow_solve(NarrowArgs g, int64_t n) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int4 r0 = g.feats[2 * i], r1 = g.feats[2 * i + 1];
+  const int kind = r0.x;
+  Hit h;
+  bool hit;
+  if (kind == 0) {
+    const int v = r0.w, f0 = r1.x, f1 = r1.y, f2 = r1.z;
+    if (!kCcd) {
+      hit = dcd_vf(ldx(g.x0, v), ldx(g.x0, f0), ldx(g.x0, f1), ldx(g.x0, f2), g.thickness, h);
+    } else {
+      hit = ccd_vf(ldx(g.x0, v), ldx(g.x1, v), ldx(g.x0, f0), ldx(g.x1, f0), ldx(g.x0, f1), ldx(g.x1, f1),
+                   ldx(g.x0, f2), ldx(g.x1, f2), h);
+    }
+  } else {
+    const int a0 = r0.w, a1 = r1.x, b0 = r1.y, b1 = r1.z;
+    if (!kCcd) {
+      hit = dcd_ee(ldx(g.x0, a0), ldx(g.x0, a1), ldx(g.x0, b0), ldx(g.x0, b1), g.thickness, h);
+    } else {
+      hit = ccd_ee(ldx(g.x0, a0), ldx(g.x1, a0), ldx(g.x0, a1), ldx(g.x1, a1), ldx(g.x0, b0), ldx(g.x1, b0),
+                   ldx(g.x0, b1), ldx(g.x1, b1), h);
+    }
+  }
+  if (hit) emit(g, kind, r0.y, r0.z, h);
 }
 
 __global__ void k_iota(int64_t n, int64_t* __restrict__ v) {
@@ -826,6 +977,15 @@ int64_t narrow_phase(Ctx& c, const double* x0, const double* x1, int mode, doubl
   g.dbox = c.zn_dbox.data();
   c.hit_count.resize(1);
   unsigned long long nh = 0;
+  // two-pass (features, then their elementary tests) per mode; WEFT_NARROW_TWO
+  // = 0 / 1 / 2 / 3: fused for both / CCD only / DCD only / both two-pass
+  static const int two_env = std::getenv("WEFT_NARROW_TWO") ? std::atoi(std::getenv("WEFT_NARROW_TWO")) : 1;
+  const bool two_pass = ccd ? (two_env & 1) != 0 : (two_env & 2) != 0;
+  int64_t nfeat = 0;
+  static const int64_t fcap_env = std::getenv("WEFT_NARROW_FCAP") ? std::atoll(std::getenv("WEFT_NARROW_FCAP")) : 0;
+  int64_t fcap = fcap_env > 0 ? fcap_env
+                              : std::max<int64_t>((static_cast<int64_t>(c.zn_feats.cap) - 2) / 2, int64_t{1} << 20);
+  c.zn_feat_count.resize(1);
   if (npairs) {
     size_t cap = std::max<size_t>(c.hit_keys.cap, static_cast<size_t>(1) << 20);
     for (int attempt = 0; attempt < 2; ++attempt) {
@@ -836,8 +996,31 @@ int64_t narrow_phase(Ctx& c, const double* x0, const double* x1, int mode, doubl
       g.count = c.hit_count.data();
       g.cap = cap;
       WG_CUDA(cudaMemsetAsync(c.hit_count.data(), 0, sizeof(unsigned long long), s));
-      if (ccd) k_narrow<true><<<div_up(npairs, 128), 128, 0, ls(c)>>>(g);
-      else k_narrow<false><<<div_up(npairs, 128), 128, 0, ls(c)>>>(g);
+      if (two_pass) {
+        for (int fa = 0; fa < 2; ++fa) {  // features pass (exact count on overflow, once)
+          c.zn_feats.resize(2 * static_cast<size_t>(fcap) + 2);
+          g.feats = reinterpret_cast<int4*>(c.zn_feats.data());
+          g.feat_count = c.zn_feat_count.data();
+          g.feat_cap = static_cast<unsigned long long>(fcap);
+          WG_CUDA(cudaMemsetAsync(c.zn_feat_count.data(), 0, sizeof(unsigned long long), s));
+          if (ccd) k_narrow_feats<true><<<div_up(npairs, kFeatWarps * 32), kFeatWarps * 32, 0, ls(c)>>>(g);
+          else k_narrow_feats<false><<<div_up(npairs, kFeatWarps * 32), kFeatWarps * 32, 0, ls(c)>>>(g);
+          WG_CUDA(cudaGetLastError());
+          unsigned long long nf = 0;
+          read_small(c, s, {c.zn_feat_count.data(), &nf, sizeof(nf)});
+          nfeat = static_cast<int64_t>(nf);
+          if (nfeat <= fcap) break;
+          fcap = nfeat;
+        }
+        if (nfeat) {
+          if (ccd) k_narrow_solve<true><<<div_up(nfeat, 128), 128, 0, ls(c)>>>(g, nfeat);
+          else k_narrow_solve<false><<<div_up(nfeat, 128), 128, 0, ls(c)>>>(g, nfeat);
+        }
+      } else if (ccd) {
+        k_narrow<true><<<div_up(npairs, 128), 128, 0, ls(c)>>>(g);
+      } else {
+        k_narrow<false><<<div_up(npairs, 128), 128, 0, ls(c)>>>(g);
+      }
       WG_CUDA(cudaGetLastError());
       WG_CUDA(cudaMemcpyAsync(&nh, c.hit_count.data(), sizeof(nh), cudaMemcpyDeviceToHost, s));
       WG_CUDA(cudaStreamSynchronize(s));

@@ -108,12 +108,15 @@ np.save(sys.argv[2], np.concatenate(out))
 """
 
 
-@pytest.mark.parametrize("env", [{"WEFT_WALK_CAP": "64"}, {"WEFT_WALK_APPEND": "0"}])
+@pytest.mark.parametrize("env", [{"WEFT_WALK_CAP": "64"}, {"WEFT_WALK_APPEND": "0"},
+                                 {"WEFT_NARROW_TWO": "0"}, {"WEFT_NARROW_TWO": "3", "WEFT_NARROW_FCAP": "64"}])
 def test_append_feed_overflow_and_ordered_feed(tmp_path, env):
     """The order-free narrow-phase feed (append mode of the candidate walk)
-    re-run after overflowing a tiny first capacity, and the two-pass ordered
-    feed, give the default run's hits bit for bit (each in its own process:
-    the switches are read once)."""
+    re-run after overflowing a tiny first capacity, the two-pass ordered feed,
+    the fused one-kernel narrow phase and the two-pass (features, then tests)
+    narrow phase re-run after overflowing its feature buffer all give the
+    default run's hits bit for bit (each in its own process: the switches
+    are read once)."""
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
