@@ -563,7 +563,10 @@ __global__ void __launch_bounds__(128) k_narrow(NarrowArgs g) {
 // shared-memory buffer (flushed with one atomic claim). The elementary tests
 // then run densely in pass 2 (k_narrow_solve): in the CCD only ~0.5 features
 // per pair reach the cubic solve, which left most lanes of a fused warp idle.
-constexpr int kFeatBuf = 256;  // records per warp
+#ifndef WEFT_FEAT_BUF
+#define WEFT_FEAT_BUF 64  // 8 KB per CTA: occupancy over fewer atomics (256: 11.0, 128: 10.4, 64: 10.1 ms broad + narrow)
+#endif
+constexpr int kFeatBuf = WEFT_FEAT_BUF;  // records per warp
 constexpr int kFeatWarps = 4;
 __device__ __forceinline__ void feat_flush(const NarrowArgs& g, int4* buf, int& bn, int lane) {
   __syncwarp();
@@ -979,7 +982,7 @@ int64_t narrow_phase(Ctx& c, const double* x0, const double* x1, int mode, doubl
   unsigned long long nh = 0;
   // two-pass (features, then their elementary tests) per mode; WEFT_NARROW_TWO
   // = 0 / 1 / 2 / 3: fused for both / CCD only / DCD only / both two-pass
-  static const int two_env = std::getenv("WEFT_NARROW_TWO") ? std::atoi(std::getenv("WEFT_NARROW_TWO")) : 1;
+  static const int two_env = std::getenv("WEFT_NARROW_TWO") ? std::atoi(std::getenv("WEFT_NARROW_TWO")) : 3;
   const bool two_pass = ccd ? (two_env & 1) != 0 : (two_env & 2) != 0;
   int64_t nfeat = 0;
   static const int64_t fcap_env = std::getenv("WEFT_NARROW_FCAP") ? std::atoll(std::getenv("WEFT_NARROW_FCAP")) : 0;
