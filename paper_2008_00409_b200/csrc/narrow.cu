@@ -561,8 +561,9 @@ __global__ void __launch_bounds__(128) k_narrow(NarrowArgs g) {
 // Two-pass narrow phase, pass 1: the box tests of k_narrow, one thread per
 // candidate pair, every survivor compacted by ballot into the warp's
 // shared-memory buffer (flushed with one atomic claim). The elementary tests
-// then run densely in pass 2 (k_narrow_solve): in the CCD only ~0.5 features
-// per pair reach the cubic solve, which left most lanes of a fused warp idle.
+// then run densely in pass 2 (k_narrow_solve): at config D ~0.5 features
+// per pair reach the CCD cubic solve and ~1.9 the DCD distance tests, which
+// left most lanes of a fused warp (k_narrow, WEFT_NARROW_TWO=0) idle.
 #ifndef WEFT_FEAT_BUF
 #define WEFT_FEAT_BUF 64  // 8 KB per CTA: occupancy over fewer atomics (256: 11.0, 128: 10.4, 64: 10.1 ms broad + narrow)
 #endif
